@@ -1,0 +1,104 @@
+/* oracle.h -- plain, slow, obviously-correct CPU oracle for the ForestClaw hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg may load liboracle.so.  The product path (paper_1308_1472_b200/) never
+ * includes, links or calls anything here, and this oracle shares no source with it.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, SURVEY.md §8(c) readings):
+ *   - forest decode: leaves in Morton order -> (tree, level, x, y)        PAPER.md:240-245 [§4]
+ *   - ghost-source classification by brute-force geometry (point location of every ghost-cell
+ *     centre, crossing tree faces through the connectivity)               PAPER.md:137-146 [§2], 258-260 [§4]
+ *   - ghost fill: copy / average / limited interpolation / physical BC / CORNER3
+ *                                                                          PAPER.md:187-201 [§3]
+ *   - Clawpack wave-propagation patch update (normal + transverse Riemann solves, wave limiter,
+ *     second-order corrections) and the CFL number                       PAPER.md:168-182 [§3]
+ * All floating point is IEEE fp64, compiled with -ffp-contract=off.
+ *
+ * Parity pins: see DESIGN.md "Oracle pins".  Functions without a pin say so in DESIGN.md.
+ */
+#ifndef FC_ORACLE_H
+#define FC_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORC_OK = 0, ORC_EINVAL = -1, ORC_ETILING = -2, ORC_ECONN = -3, ORC_EBALANCE = -4,
+       ORC_ENOMEM = -5, ORC_EUNSUP = -6, ORC_EPHYS = -7 };
+
+/* ghost-table record ops (canonical EXPANDED table) */
+enum { ORC_OP_NONE = 0, ORC_OP_COPY = 1, ORC_OP_AVG4 = 2, ORC_OP_INTERP = 3, ORC_OP_BCX = 4,
+       ORC_OP_BCY = 5, ORC_OP_CORNER3 = 6 };
+
+enum { ORC_ADV_CONST = 0, ORC_ADV_EDGEVEL_CAPA = 1, ORC_SWE_ROE = 2, ORC_EULER_ROE = 3 };
+enum { ORC_LIM_NONE = 0, ORC_LIM_MINMOD = 1, ORC_LIM_MC = 2 };
+enum { ORC_BC_OUTFLOW = 0, ORC_BC_WALL = 1 };
+
+typedef struct orc_forest orc_forest;
+
+typedef struct {
+  int kind;        /* ORC_ADV_CONST ... */
+  double p0, p1;   /* (u, v) | unused | (g, -) | (gamma, efix) */
+  int limiter;     /* ORC_LIM_* */
+  int method2;     /* 1: first order, 2: + limited second-order corrections */
+  int method3;     /* 0: none, 1: transverse of A+-dq, 2: transverse of A+-dq -+ F~ */
+} orc_problem;
+
+int orc_forest_create(int64_t num_patches, const int8_t* levels, const int32_t* tree_ids,
+                      int32_t num_trees, const int32_t* tree_to_tree, const int8_t* tree_to_face,
+                      const int8_t* face_bc, int m, orc_forest** out);
+void orc_forest_destroy(orc_forest* f);
+/* decoded leaf coordinates in units of level-Lmax leaves */
+int orc_forest_coords(const orc_forest* f, int64_t* x, int64_t* y, int* lmax);
+
+/* ring cells per patch and the record width */
+int orc_ring_count(int m);
+#define ORC_REC 8
+/* canonical ghost records of patch p: ring cells in storage order (j = -1..m+2 outer,
+ * i = -1..m+2 inner, interior skipped); each record {op, src_patch, src_i, src_j, a, b, c, d} */
+int orc_ghost_records(const orc_forest* f, int64_t p, int32_t* rec);
+int orc_ghost_table(const orc_forest* f, int32_t* rec /* [P][G][8] */);
+
+/* Fill the ghost rings of all patches of qpad[P][meqn][n][n] (n = m+4) in the phase order
+ * A (copy, average) -> C (BC x then y) -> for each level ascending: B (interpolate) -> C -> CORNER3 */
+int orc_ghost_fill(const orc_forest* f, double* qpad, int meqn);
+
+/* One step on every patch: ghost fill of qpad (rings overwritten), then the wave-propagation
+ * update written into the interiors of qout (same layout).  aux: [P][maux][n][n] or NULL.
+ * *cfl = max over patches.  nthreads <= 1 runs single-threaded (bitwise identical). */
+int orc_step(const orc_forest* f, const orc_problem* pr, double* qpad, const double* aux,
+             double dt, double dx0, double* qout, double* cfl, int nthreads);
+/* dx0 = cell width of a level-0 patch (tree edge / m); a level-l patch has dx = dx0 2^-l */
+
+/* One step from interior-only data q[P][meqn][m][m] for the listed patches only (sampled
+ * parity at full size): rings are built from the neighbours' interiors.  out[ns][meqn][m][m]. */
+int orc_step_sample(const orc_forest* f, const orc_problem* pr, const double* q,
+                    const double* aux, double dt, double dx0,
+                    const int64_t* ids, int64_t ns, double* out, double* cfl_out);
+/* padded array [meqn][n][n] of patch p with its ring filled from interior-only data q */
+int orc_build_padded_sample(const orc_forest* f, const double* q, int meqn, int64_t p, double* out);
+
+/* single-patch update on a padded patch (ring already filled) -> patch CFL */
+double orc_step_patch(const orc_problem* pr, int m, int meqn, const double* qp, const double* auxp,
+                      double dt, double dx, double dy, double* qnew);
+
+/* pieces exposed for the pin tests */
+double orc_limiter(int limiter, double theta);
+int orc_meqn(int kind);
+int orc_mwaves(int kind);
+/* normal Riemann solve at one edge: waves[mwaves][meqn], s[mwaves], amdq[meqn], apdq[meqn] */
+int orc_rpn2(const orc_problem* pr, int ixy, const double* ql, const double* qr,
+             const double* auxl, const double* auxr, double* waves, double* s, double* amdq,
+             double* apdq);
+/* transverse split of asdq at the edge between ql and qr (ixy = direction of the edge normal);
+ * aux_recv = aux of the receiving cell (3 values) and aux_recv_next = aux of the cell above
+ * (ixy = 1) / to the right (ixy = 2) of it, for ADV_EDGEVEL_CAPA */
+int orc_rpt2(const orc_problem* pr, int ixy, const double* ql, const double* qr,
+             const double* aux_recv, const double* aux_recv_next, const double* asdq,
+             double* bmasdq, double* bpasdq);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,354 @@
+"""Pins for the oracle's wave-propagation update (oracle/claw.c) and forest stepping.
+
+Independent references used here: exact integer shifts at Courant number 1, exact translation of
+affine (and, for Lax-Wendroff, quadratic) data, constant states, discrete conservation, mirror /
+transpose symmetries of symmetric problems, a monolithic single-patch grid, the exact solutions of
+the Sod shock tube and the Stoker dam break (written out here), and the convergence rate against
+the exact periodic translate.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import forests as F
+from workloads.configs import (ADV_CONST, EULER_ROE, SWE_ROE, Workload, c1, c3, c5,
+                               euler_shock_bubble_state)
+
+GAM = 1.4
+
+
+def workload(forest, m, meqn, kind, params, q0, steps, dt0, policy="fixed", **kw):
+    return Workload("test", forest, m, meqn, 0, kind, params, q0, None, steps, dt0, policy, **kw)
+
+
+def assemble(w, q):
+    m = w.m
+    lvl = int(w.forest.levels[0])
+    nt = w.forest.conn.num_trees
+    N = 2 ** lvl * m
+    G = np.zeros((q.shape[1], N, nt * N))
+    for p in range(w.num_patches):
+        t = int(w.forest.tree_ids[p])
+        x0 = t * N + int(w.forest.ix[p]) * m
+        y0 = int(w.forest.iy[p]) * m
+        G[:, y0:y0 + m, x0:x0 + m] = q[p]
+    return G
+
+
+def scatter(w, G):
+    m = w.m
+    lvl = int(w.forest.levels[0])
+    N = 2 ** lvl * m
+    q = np.zeros((w.num_patches, G.shape[0], m, m))
+    for p in range(w.num_patches):
+        t = int(w.forest.tree_ids[p])
+        x0 = t * N + int(w.forest.ix[p]) * m
+        y0 = int(w.forest.iy[p]) * m
+        q[p] = G[:, y0:y0 + m, x0:x0 + m]
+    return q
+
+
+# ---- exact special cases ---------------------------------------------------------------------------
+def test_constant_state_preserved_bitwise():
+    cases = []
+    f1 = F.forest_uniform(F.periodic_unit_square(), 2)
+    cases.append(workload(f1, 8, 1, ADV_CONST, (1.0, 0.5), np.full((16, 1, 8, 8), 0.37), 3, 0.028125))
+    f3 = F.forest_uniform(F.walled_unit_square(F.WALL), 2)
+    q3 = np.zeros((16, 3, 8, 8)); q3[:, 0] = 1.3
+    cases.append(workload(f3, 8, 3, SWE_ROE, (1.0, 0.0), q3, 3, 0.01))
+    f5 = F.forest_uniform(F.brick(4, 1, bc=F.OUTFLOW), 1)
+    rho, u, v, p = 1.2, 0.7, -0.3, 2.0
+    q5 = np.empty((16, 4, 8, 8))
+    q5[:, 0], q5[:, 1], q5[:, 2] = rho, rho * u, rho * v
+    q5[:, 3] = p / (GAM - 1) + 0.5 * rho * (u * u + v * v)
+    cases.append(workload(f5, 8, 4, EULER_ROE, (GAM, 1.0), q5, 3, 0.01))
+    for w in cases:
+        q, cfl, _ = oracle.run(w)
+        np.testing.assert_array_equal(q, w.q0)
+
+
+@pytest.mark.parametrize("method2", [1, 2])
+@pytest.mark.parametrize("uv", [(1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (-1, -1), (1, -1), (-1, 1)])
+def test_cfl1_exact_integer_shift(rng, method2, uv):
+    """north_star: first-order upwind at Courant number exactly 1 reproduces an exact integer cell
+    shift; with |s| dt/dx = 1 the corrections F~ vanish, so method2 = 2 shifts exactly too, and the
+    corner-transport (transverse) terms make the diagonal shift exact."""
+    for conn, ntrees in ((F.periodic_unit_square(), 1), (F.brick(2, 1, periodic_x=True, periodic_y=True), 2)):
+        fr = F.forest_uniform(conn, 2)
+        m = 8
+        w = workload(fr, m, 1, ADV_CONST, (float(uv[0]), float(uv[1])), None, 3, 1.0 / 32,
+                     method2=method2, method3=2)
+        G = rng.integers(0, 256, size=(1, 32, 32 * ntrees)).astype(np.float64)
+        w.q0 = scatter(w, G)
+        q, cfl, _ = oracle.run(w)
+        expect = np.roll(G, shift=(3 * uv[1], 3 * uv[0]), axis=(1, 2))
+        np.testing.assert_array_equal(assemble(w, q), expect)
+        assert (cfl == 1.0).all()
+
+
+def _padded_centres(m, x0=0.3, y0=0.1, h=1.0 / 16):
+    k = np.arange(-2, m + 2) + 0.5
+    X = x0 + h * k[None, :]
+    Y = y0 + h * k[:, None]
+    return np.broadcast_to(X, (m + 4, m + 4)), np.broadcast_to(Y, (m + 4, m + 4)), h
+
+
+def test_affine_data_translated_exactly(rng):
+    """Constant velocity, affine data (theta = 1, phi = 1): one step translates it exactly."""
+    m = 8
+    X, Y, h = _padded_centres(m)
+    for _ in range(10):
+        u, v = rng.uniform(-1, 1, 2)
+        a, b, c = rng.normal(size=3)
+        dt = 0.8 * h / max(abs(u), abs(v))
+        qp = (a + b * X + c * Y)[None].copy()
+        pr = oracle.problem(oracle.ADV_CONST, (u, v), oracle.LIM_MC)
+        out, cfl = oracle.step_patch(pr, qp, dt, h, h)
+        exact = a + b * (X - u * dt) + c * (Y - v * dt)
+        np.testing.assert_allclose(out[0, 2:m + 2, 2:m + 2], exact[2:m + 2, 2:m + 2], rtol=0, atol=1e-13)
+
+
+def test_lax_wendroff_exact_for_quadratics(rng):
+    """Unlimited second-order correction in 1D is Lax-Wendroff, exact for quadratic data."""
+    m = 8
+    X, Y, h = _padded_centres(m)
+    for axis in (0, 1):
+        for _ in range(5):
+            s = rng.uniform(-1, 1)
+            uv = (s, 0.0) if axis == 0 else (0.0, s)
+            Z = X if axis == 0 else Y
+            a, b, c = rng.normal(size=3)
+            dt = 0.7 * h / abs(s)
+            qp = (a + b * Z + c * Z * Z)[None].copy()
+            pr = oracle.problem(oracle.ADV_CONST, uv, oracle.LIM_NONE)
+            out, _ = oracle.step_patch(pr, qp, dt, h, h)
+            Zs = Z - s * dt
+            exact = a + b * Zs + c * Zs * Zs
+            np.testing.assert_allclose(out[0, 2:m + 2, 2:m + 2], exact[2:m + 2, 2:m + 2], rtol=0, atol=1e-13)
+
+
+# ---- conservation and symmetry -------------------------------------------------------------------------
+def test_conservation_periodic_advection():
+    """SPEC.md:288 / north_star: sum q area invariant on a periodic domain (C1, 100 steps)."""
+    w = c1()
+    q, _, _ = oracle.run(w, steps=100)
+    m0 = w.q0.sum()
+    assert abs(q.sum() - m0) <= 1e-14 * 100 * abs(m0)
+
+
+def test_conservation_periodic_euler(rng):
+    fr = F.forest_uniform(F.brick(2, 1, periodic_x=True, periodic_y=True), 2)
+    m = 8
+    w = workload(fr, m, 4, EULER_ROE, (GAM, 1.0), None, 20, 1e-3, policy="cfl")
+    X, Y = F.cell_centres(fr, m)
+    X = X + fr.tree_ids[:, None, None]
+    rho = 1.0 + 0.5 * np.exp(-20 * ((X - 1.0) ** 2 + (Y - 0.5) ** 2))
+    u, v, p = 0.3 * np.ones_like(X), -0.2 * np.ones_like(X), 1.0 + 0.3 * np.sin(2 * np.pi * X)
+    q0 = np.stack([rho, rho * u, rho * v, p / (GAM - 1) + 0.5 * rho * (u * u + v * v)], 1)
+    w.q0 = q0
+    q, cfls, _ = oracle.run(w)
+    for k in range(4):
+        assert abs(q[:, k].sum() - q0[:, k].sum()) <= 1e-14 * 20 * np.abs(q0[:, k]).sum()
+
+
+def test_swe_dam_break_walls_mass_and_symmetry():
+    """C3 physics at level 2: depth conserved with reflecting walls; the radially symmetric data
+    stays symmetric under transposition and mirrors (hu <-> hv under transposition)."""
+    w = c3(level=2, m=8)
+    q, cfl, _ = oracle.run(w, steps=30)
+    assert abs(q[:, 0].sum() - w.q0[:, 0].sum()) <= 1e-14 * 30 * w.q0[:, 0].sum()
+    G = assemble(w, q)
+    h, hu, hv = G
+    tol = 1e-13 * np.abs(G).max()
+    np.testing.assert_allclose(h, h.T, rtol=0, atol=tol)
+    np.testing.assert_allclose(hu, hv.T, rtol=0, atol=tol)
+    np.testing.assert_allclose(h, h[:, ::-1], rtol=0, atol=tol)
+    np.testing.assert_allclose(h, h[::-1, :], rtol=0, atol=tol)
+    np.testing.assert_allclose(hu, -hu[:, ::-1], rtol=0, atol=tol)
+
+
+def test_euler_shock_bubble_mirror_symmetry():
+    """C5 physics (level 2): the data are symmetric about y = 1/2, so rho(x, y) = rho(x, 1-y)
+    and rho v is odd."""
+    w = c5(level=2, m=8)
+    q, cfl, _ = oracle.run(w, steps=25)
+    G = assemble(w, q)
+    tol = 1e-13 * np.abs(G).max()
+    for k in (0, 1, 3):
+        np.testing.assert_allclose(G[k], G[k][::-1, :], rtol=0, atol=tol)
+    np.testing.assert_allclose(G[2], -G[2][::-1, :], rtol=0, atol=tol)
+
+
+def test_monolithic_single_patch_equivalence():
+    """A uniform forest of small patches equals one big patch covering the same cells (copy,
+    corner and BC ghosts are exactly the big grid's neighbours), bitwise, over several steps."""
+    # periodic advection: 16 patches of 8 vs 1 patch of 32
+    a, b = c1(), c1(level=0, m=32)
+    qa, ca, _ = oracle.run(a)
+    qb, cb, _ = oracle.run(b)
+    np.testing.assert_array_equal(assemble(a, qa), assemble(b, qb))
+    np.testing.assert_array_equal(ca, cb)
+    # SWE with walls: 16 patches of 8 vs 1 of 32 (replay the same dt sequence)
+    a, b = c3(level=2, m=8), c3(level=0, m=32)
+    qa, ca, da = oracle.run(a, steps=15)
+    qb, cb, _ = oracle.run(b, steps=15, dt_list=da)
+    np.testing.assert_array_equal(assemble(a, qa), assemble(b, qb))
+    np.testing.assert_array_equal(ca, cb)
+    # Euler on the 4-tree brick: 4x(4 patches of 8) vs 4x(1 patch of 16)
+    a, b = c5(level=1, m=8), c5(level=0, m=16)
+    qa, ca, da = oracle.run(a, steps=15)
+    qb, cb, _ = oracle.run(b, steps=15, dt_list=da)
+    np.testing.assert_array_equal(assemble(a, qa), assemble(b, qb))
+
+
+def test_openmp_bitwise_equal_to_one_thread():
+    w = c5(level=2, m=8)
+    q1, c1_, d1 = oracle.run(w, steps=5, nthreads=1)
+    q4, c4_, d4 = oracle.run(w, steps=5, nthreads=4)
+    np.testing.assert_array_equal(q1, q4)
+    np.testing.assert_array_equal(c1_, c4_)
+
+
+# ---- accuracy against exact solutions ----------------------------------------------------------------
+def test_convergence_against_exact_translate():
+    """C1's IC under (u, v) = (1, 0.5) on the periodic square is an exact translate; the error
+    falls at a rate between first and second order (MC clips the peak) under refinement."""
+    errs = []
+    T = 0.25
+    for lvl in (2, 3, 4):
+        w = c1(level=lvl, m=8)
+        dx = 0.5 ** lvl / 8
+        nsteps = int(round(T / (0.5 * dx)))
+        w.dt0 = T / nsteps
+        q, _, _ = oracle.run(w, steps=nsteps)
+        X, Y = F.cell_centres(w.forest, 8)
+        # exact: periodic translate of the Gaussian, summed over images
+        ex = np.zeros_like(X)
+        for sx in (-1, 0, 1):
+            for sy in (-1, 0, 1):
+                ex += np.exp(-100.0 * ((X - T - 0.5 + sx) ** 2 + (Y - 0.5 * T - 0.5 + sy) ** 2))
+        errs.append(np.abs(q[:, 0] - ex).sum() * dx * dx)
+    r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
+    assert 2.5 < r2 < 4.5 and r1 > 2.0, errs
+
+
+def _sod_exact(xi, L, R, gam=GAM):
+    rl, ul, pl = L
+    rr, ur, pr = R
+    cl, cr = math.sqrt(gam * pl / rl), math.sqrt(gam * pr / rr)
+
+    def fk(p, r, pk, ck):
+        if p > pk:
+            A, B = 2.0 / ((gam + 1) * r), (gam - 1) / (gam + 1) * pk
+            return (p - pk) * math.sqrt(A / (p + B))
+        return 2 * ck / (gam - 1) * ((p / pk) ** ((gam - 1) / (2 * gam)) - 1)
+
+    lo, hi = 1e-8, 100.0
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if fk(mid, rl, pl, cl) + fk(mid, rr, pr, cr) + ur - ul > 0:
+            hi = mid
+        else:
+            lo = mid
+    ps = 0.5 * (lo + hi)
+    us = 0.5 * (ul + ur) + 0.5 * (fk(ps, rr, pr, cr) - fk(ps, rl, pl, cl))
+    g1 = (gam - 1) / (gam + 1)
+    out = np.zeros_like(xi)
+    for n, s in enumerate(xi):
+        if s <= us:
+            if ps > pl:
+                SL = ul - cl * math.sqrt((gam + 1) / (2 * gam) * ps / pl + (gam - 1) / (2 * gam))
+                out[n] = rl if s <= SL else rl * (ps / pl + g1) / (g1 * ps / pl + 1)
+            else:
+                csl = cl * (ps / pl) ** ((gam - 1) / (2 * gam))
+                if s <= ul - cl:
+                    out[n] = rl
+                elif s > us - csl:
+                    out[n] = rl * (ps / pl) ** (1 / gam)
+                else:
+                    c = 2 / (gam + 1) * (cl + (gam - 1) / 2 * (ul - s))
+                    out[n] = rl * (c / cl) ** (2 / (gam - 1))
+        else:
+            if ps > pr:
+                SR = ur + cr * math.sqrt((gam + 1) / (2 * gam) * ps / pr + (gam - 1) / (2 * gam))
+                out[n] = rr if s >= SR else rr * (ps / pr + g1) / (g1 * ps / pr + 1)
+            else:
+                csr = cr * (ps / pr) ** ((gam - 1) / (2 * gam))
+                if s >= ur + cr:
+                    out[n] = rr
+                elif s < us + csr:
+                    out[n] = rr * (ps / pr) ** (1 / gam)
+                else:
+                    c = 2 / (gam + 1) * (cr - (gam - 1) / 2 * (ur - s))
+                    out[n] = rr * (c / cr) ** (2 / (gam - 1))
+    return out
+
+
+def _stoker_exact(xi, hl, hr, g=1.0):
+    f = lambda h: 2 * (math.sqrt(g * hl) - math.sqrt(g * h)) - (h - hr) * math.sqrt(0.5 * g * (1 / h + 1 / hr))
+    lo, hi = hr, hl
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if f(mid) > 0:
+            lo = mid
+        else:
+            hi = mid
+    hm = 0.5 * (lo + hi)
+    um = 2 * (math.sqrt(g * hl) - math.sqrt(g * hm))
+    s = hm * um / (hm - hr)
+    out = np.where(xi <= -math.sqrt(g * hl), hl,
+                   np.where(xi <= um - math.sqrt(g * hm), (2 * math.sqrt(g * hl) - xi) ** 2 / (9 * g),
+                            np.where(xi <= s, hm, hr)))
+    return out
+
+
+def _shock_tube(kind, level, t_end):
+    conn = F.brick(1, 1, periodic_y=True, bc=F.OUTFLOW)
+    fr = F.forest_uniform(conn, level)
+    m = 8
+    X, Y = F.cell_centres(fr, m)
+    left = X < 0.5
+    if kind == EULER_ROE:
+        rho = np.where(left, 1.0, 0.125)
+        p = np.where(left, 1.0, 0.1)
+        q0 = np.stack([rho, 0 * rho, 0 * rho, p / (GAM - 1)], 1)
+        w = workload(fr, m, 4, EULER_ROE, (GAM, 1.0), q0, 0, 0.0, policy="cfl")
+        smax = math.sqrt(GAM)
+    else:
+        h = np.where(left, 2.0, 1.0)
+        q0 = np.stack([h, 0 * h, 0 * h], 1)
+        w = workload(fr, m, 3, SWE_ROE, (1.0, 0.0), q0, 0, 0.0, policy="cfl")
+        smax = math.sqrt(2.0)
+    dx = 0.5 ** level / m
+    dt = 0.9 * dx / smax
+    f = oracle.forest_for(w)
+    pr = oracle.problem_for(w)
+    qp = f.pad(q0)
+    t = 0.0
+    while t < t_end - 1e-15:
+        dt = min(dt, t_end - t)
+        out, cfl = f.step(pr, qp, dt, 1.0 / m)
+        if cfl > 1.0:                        # Clawpack retake with the reduced dt
+            dt = dt * 0.9 / cfl
+            continue
+        qp, t = out, t + dt
+        dt = dt * 0.9 / cfl
+    q = qp[:, :, 2:m + 2, 2:m + 2]
+    return X[:, :, :], q[:, 0], dx
+
+
+@pytest.mark.parametrize("kind", [EULER_ROE, SWE_ROE])
+def test_shock_tube_converges_to_exact(kind):
+    """Sod (Euler) and Stoker's dam break (SWE) as y-independent 2D runs: the L1 error of the
+    density/depth against the exact Riemann solution falls under refinement and is small."""
+    t_end = 0.15
+    errs = []
+    for lvl in (3, 4):
+        X, r, dx = _shock_tube(kind, lvl, t_end)
+        xi = (X.ravel() - 0.5) / t_end
+        ex = _sod_exact(xi, (1.0, 0.0, 1.0), (0.125, 0.0, 0.1)) if kind == EULER_ROE \
+            else _stoker_exact(xi, 2.0, 1.0)
+        errs.append(np.abs(r.ravel() - ex).mean())
+    assert errs[1] < 0.75 * errs[0] and errs[1] < 0.02, errs
