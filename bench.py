@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""bench.py -- fp64 cell-updates/s of the ForestClaw hot path (ghost fill + wave-propagation
+update + CFL reduction) on 1..8 B200s, plus roofline, end-to-end and oracle baselines.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5] [--impl fc|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N --steps K --warmup W
+
+One "step" = one fc_step: ghost fill (incl. the NCCL halo exchange for N > 1), the update of every
+local patch, the global CFL max-allreduce and the CFL read-back that drives the next dt (the
+Clawpack variable-dt rule of the workload).  The workload is BASELINE.json configs[4] (C5: Euler
+shock-bubble on a 4-tree brick, level 8, m = 16, 262,144 patches, 67.1M cells) -- the config
+BASELINE's metric is quoted on at 1/2/4/8 GPUs -- Morton-sharded across ranks (strong scaling).
+Its state (2 x 3.36 GB) is far larger than L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 cell-updates/sec per step (ghost fill + update) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "cell-updates/s"
+WORKLOADS = {
+    "C5": ("C5: 2D Euler shock-bubble, Roe + Harten-Hyman, MC limiter, 4-tree brick [0,4]x[0,1] "
+           "outflow, uniform level 8, m=16, mbc=2 (BASELINE.json configs[4])"),
+    "C3": ("C3: shallow-water radial dam break, Roe, MC limiter, walls, uniform level 6, m=32 "
+           "(BASELINE.json configs[2])"),
+}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def make_workload(name: str):
+    from workloads.configs import c3, c5
+    if name == "C5":
+        return c5(lazy=True)
+    if name == "C3":
+        return c3(lazy=True)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def bytes_per_cell_update(w) -> int:
+    """Compulsory (algorithmic) HBM bytes per cell-update: q read + q written + aux read."""
+    return 16 * w.meqn + 8 * w.maux
+
+
+# ---------------------------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                idx = int(parts[0])
+            except ValueError:
+                continue
+            if idx not in self.gpus:
+                continue
+            rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, nm in enumerate(names):
+                if r[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())
+                if any(r[3].replace(".", "").isdigit() for r in rows) else None}
+
+
+# ---------------------------------------------------------------------------------------------
+def oracle_rate(w, seconds: float, sample_patches: int = 256, seed: int = 1308147):
+    """The CPU oracle as it stands (oracle/*.c, gcc -O2, single thread) on a bounded sample of
+    the same workload: repeated one-step updates of `sample_patches` patches from the IC (each
+    patch's ghost ring built from its neighbours, then the update) until `seconds` elapsed."""
+    import numpy as np
+    import oracle
+    f = oracle.forest_for(w)
+    rng = np.random.default_rng(seed)
+    ids = np.sort(rng.choice(w.num_patches, size=sample_patches, replace=False)).astype(np.int64)
+    q = w.q0 if w.q0 is not None else None
+    if q is None:   # the sampled patches' rings need their neighbours: materialise the IC once
+        w.materialise()
+        q = w.q0
+    pr = oracle.problem_for(w)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        f.step_sample(pr, q, w.dt0, 1.0 / w.m, ids)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    cells = reps * len(ids) * w.m * w.m
+    return cells / el, el, reps, len(ids)
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed on the host (rank 0 only under torchrun)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = make_workload(args.workload)
+    import numpy as np
+    import oracle
+    w.materialise()
+    f = oracle.forest_for(w)
+    pr = oracle.problem_for(w)
+    rng = np.random.default_rng(1308147)
+    ids = np.sort(rng.choice(w.num_patches, size=args.ref_patches, replace=False)).astype(np.int64)
+    for _ in range(args.warmup):
+        f.step_sample(pr, w.q0, w.dt0, 1.0 / w.m, ids)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        f.step_sample(pr, w.q0, w.dt0, 1.0 / w.m, ids)
+    el = time.perf_counter() - t0
+    cells = len(ids) * w.m * w.m
+    value = cells * args.steps / el
+    sample = (f"{len(ids)} random patches of {w.name} ({cells} cells) per step: ghost ring from "
+              f"neighbour interiors + one wave-propagation update, single thread, from the IC")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * el / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOADS[args.workload], "cells_per_step": cells},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="C5", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="fc", choices=["fc", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-patches", type=int, default=256)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1308_1472_b200 import build as libbuild
+    libbuild.build()
+    from paper_1308_1472_b200 import fc
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    w = make_workload(args.workload)
+    P = w.num_patches
+    p0, p1 = (rank * P) // world, ((rank + 1) * P) // world
+    nccl_id = None
+    if world > 1:
+        obj = [fc.fc_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0,
+                  local, rank, world, nccl_id)
+    assert (f.first, f.count) == (p0, p1 - p0)
+    f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject)
+    q0 = torch.from_numpy(w.q0_range(p0, p1)).pin_memory()
+    qdev = q0.cuda()
+    stream = torch.cuda.current_stream()
+    f.set_stream(stream.cuda_stream)
+    cells_total = w.cells
+    local_cells = (p1 - p0) * w.m * w.m
+
+    def steps(n, dt):
+        cfls = []
+        for _ in range(n):
+            rc, cfl = f.step(dt, raise_on_reject=False)
+            if rc == fc.FC_ECFL:             # Clawpack retake with the reduced dt
+                dt = dt * w.cfl_target / cfl
+                rc, cfl = f.step(dt)
+            cfls.append(cfl)
+            dt = w.next_dt(dt, cfl)
+        return dt, cfls
+
+    # ---- device-resident timed run ----
+    f.set_q(qdev)
+    dt, _ = steps(args.warmup, w.dt0)
+    f.reset_stats()
+    f.set_timing(True)
+    clocks = Clocks(list(range(max(1, world)))) if rank == 0 else None
+    barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    dt, cfls = steps(args.steps, dt)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop() if clocks else None
+    ms = allmax(ev0.elapsed_time(ev1))
+    st = f.stats()
+    f.set_timing(False)
+    value = cells_total * args.steps / (ms / 1000.0)
+
+    # dominant kernel: the fused update (avg launch time from CUDA events on the lib's stream)
+    pk, pk_src = peaks()
+    step_ms = st["ms_step"] / max(1, st["step_kernel_launches"])
+    ghost_ms = st["ms_ghost"] / max(1, st["steps"])
+    bpc = bytes_per_cell_update(w)
+    ach_gbs = local_cells * bpc / (step_ms / 1000.0) / 1e9
+    hbm_peak = float(pk["hbm_gbs"])
+    roofline = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach_gbs / hbm_peak, "traffic": None,
+                "kernel": "k_step<EulerRoe,16,320>" if args.workload == "C5" else "k_step",
+                "algorithmic_bytes_per_cell_update": bpc, "launch_ms": step_ms,
+                "peak_source": f"{pk_src} MEASURED_PEAKS.json hbm_gbs",
+                "note": "fp64-ALU-bound kernel: see roofline_alu in DESIGN.md; HBM fraction is the metric's own figure"}
+
+    # ---- end-to-end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        qh = torch.empty_like(q0).pin_memory()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        f.set_q(q0)                       # H2D from pinned host memory + scatter into q_old
+        _, _ = steps(args.steps, w.dt0)
+        f.get_q(qh)                       # gather + D2H into pinned host memory
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = allmax(e0.elapsed_time(e1))
+        qbytes = q0.numel() * 8
+        e2e = {"value": cells_total * args.steps / (ems / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": qbytes / args.steps, "d2h_bytes_per_step": (qbytes + 8 * args.steps) / args.steps,
+               "ms_total": ems,
+               "definition": "fc_set_q(pinned host) + K x fc_step (CFL to host each step) + fc_get_q(pinned host), per-rank bytes"}
+
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_seconds > 0:
+        w.q0 = q0.numpy()                 # the full IC is already on the host at N = 1
+        rate, el, reps, ns = oracle_rate(w, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{reps} x one-step updates of {ns} random {w.name} patches ({ns * w.m * w.m} cells) "
+                         f"from the IC, ring built from neighbours, {el:.1f} s single-threaded"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": WORKLOADS[args.workload], "patches": P, "cells": cells_total,
+                           "parallelism": f"morton-shard x{world}" + (" (NCCL halo)" if world > 1 else ""),
+                           "l2": "state 2 x %.2f GB >> 126 MB L2 (no flush needed)" % (P * w.meqn * (w.m + 4) ** 2 * 8 / 1e9),
+                           "dt_policy": "Clawpack variable dt (0.9 / CFL)", "final_cfl": cfls[-1]},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": st["kernel_launches"],
+                "phase_ms_per_step": {"ghost": ghost_ms, "update": step_ms, "cfl_allreduce": st["ms_comm"] / max(1, st["steps"])},
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    f.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,185 @@
+/* fc.h -- C ABI of libfc: the B200-native ForestClaw hot path (arXiv 1308.1472).
+ *
+ * One global-dt time step on every leaf patch of a static forest of quadtrees
+ * (PAPER.md:275-277 [§4] "one such parallel data exchange per time step for a global value of
+ * the time step length dt"): ghost-cell fill (PAPER.md:187-201 [§3]: same-level copy, fine->coarse
+ * averaging, coarse->fine limited interpolation, tree-boundary index remap PAPER.md:258-260 [§4],
+ * physical boundaries), then the Clawpack wave-propagation update (PAPER.md:168-182 [§3]) and the
+ * CFL max-reduction.  Hand-written CUDA for sm_100a, fp64 throughout, NCCL between GPUs.
+ *
+ * Conventions shared by every call:
+ *   - All functions return FC_OK (0) or a negative FC_E* code; nothing throws across the ABI.
+ *     fc_last_error() returns a thread-local message for the last failure.
+ *   - Handles are opaque, owned by the library, not thread-safe: one handle per process/GPU.
+ *   - Patches are in global Morton order (trees ascending, z-order inside a tree, x on the even
+ *     bits).  Rank r of R owns patches [floor(r P / R), floor((r+1) P / R)) ("local" patches).
+ *   - Cell arrays are fp64, structure of arrays per patch, x fastest:
+ *       interior  q[P_local][meqn][m][m]
+ *       padded    q[P_local][meqn][n][n], n = m + 2 mbc, cell (i, j) (1-based, i, j in
+ *                 [-1, m+2]) at [(j+1) n + (i+1)]
+ *   - `where` selects the memory space of a user pointer: FC_HOST (pageable or pinned host
+ *     memory) or FC_DEVICE (a device pointer on the handle's GPU, e.g. torch data_ptr()).
+ *     User buffers are copied; the caller keeps ownership.
+ *   - All device work is issued on the handle's stream (fc_set_stream, default: a private
+ *     non-blocking stream).  Calls that return data to the host synchronise that stream.
+ */
+#ifndef FC_H
+#define FC_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes ---------------------------------------------------------------------------- */
+#define FC_OK 0
+#define FC_EINVAL -1      /* bad argument / descriptor field */
+#define FC_ETILING -2     /* leaves do not tile every tree in z-order (Morton decode failed) */
+#define FC_ECONN -3       /* connectivity not symmetric or out of range */
+#define FC_EBALANCE -4    /* face or corner level jump > 1 (2:1 balance) */
+#define FC_ECUDA -5       /* CUDA runtime error */
+#define FC_ENCCL -6       /* NCCL error */
+#define FC_ENOMEM -7      /* host or device allocation failed */
+#define FC_ESTATE -8      /* call out of order (e.g. fc_step before fc_set_problem / fc_set_q) */
+#define FC_ECFL -9        /* step rejected: max CFL > cfl_reject; state unchanged */
+#define FC_ENONFINITE -10 /* CFL is NaN/Inf; state unchanged */
+#define FC_EUNSUP -11     /* configuration outside what this build supports */
+
+/* ---- enums --------------------------------------------------------------------------------- */
+#define FC_HOST 0
+#define FC_DEVICE 1
+
+#define FC_ADV_CONST 0        /* q_t + u q_x + v q_y = 0, (p0, p1) = (u, v); meqn 1, maux 0 */
+#define FC_ADV_EDGEVEL_CAPA 1 /* kappa q_t + (u~ q)_xi + (v~ q)_eta advective form; aux = {kappa, u~ (left edge), v~ (bottom edge)}; meqn 1, maux 3 */
+#define FC_SWE_ROE 2          /* shallow water (h, hu, hv), p0 = g; meqn 3 */
+#define FC_EULER_ROE 3        /* Euler (rho, rho u, rho v, E), p0 = gamma, p1 != 0: Harten-Hyman entropy fix; meqn 4 */
+
+#define FC_LIM_NONE 0
+#define FC_LIM_MINMOD 1
+#define FC_LIM_MC 2
+
+#define FC_BC_OUTFLOW 0
+#define FC_BC_WALL 1
+
+#define FC_TABLE_EXPANDED 1   /* per ghost cell records, see fc_get_ghost_table */
+
+/* ---- descriptors --------------------------------------------------------------------------- */
+typedef struct fc_forest fc_forest;
+
+typedef struct {
+  int64_t num_patches;          /* P, global */
+  const int8_t* levels;         /* [P] leaf levels, global Morton order */
+  const int32_t* tree_ids;      /* [P] non-decreasing tree ids */
+  int32_t num_trees;            /* T */
+  const int32_t* tree_to_tree;  /* [4T] neighbour tree across face f = 0 (-x), 1 (+x), 2 (-y), 3 (+y) */
+  const int8_t* tree_to_face;   /* [4T] neighbour face + 4 * reversed; (t, f) -> (t, f) = physical */
+  const int8_t* face_bc;        /* [4T] FC_BC_OUTFLOW | FC_BC_WALL on physical faces */
+  int32_t m;                    /* cells per patch side, even, >= 4 */
+  int32_t mbc;                  /* ghost layers, must be 2 */
+  int32_t meqn;                 /* equations (must match the problem kind) */
+  int32_t maux;                 /* aux fields (3 for FC_ADV_EDGEVEL_CAPA, else 0) */
+  double tree_dx0;              /* tree edge length (a level-l cell is tree_dx0 2^-l / m wide) */
+  int32_t device;               /* CUDA device ordinal; -1 = host-only planning handle (tables only) */
+  int32_t rank, nranks;         /* this process among nranks (1 = single GPU) */
+  const void* nccl_id;          /* 128-byte ncclUniqueId when nranks > 1 (fc_nccl_unique_id on rank 0) */
+} fc_forest_desc;
+
+typedef struct {
+  int32_t kind;                 /* FC_ADV_CONST ... */
+  double p0, p1;                /* physical parameters, see the kind */
+  int32_t limiter;              /* FC_LIM_* (wave limiter) */
+  int32_t method2;              /* 1: first order; 2: + limited second-order corrections */
+  int32_t method3;              /* 0: no transverse; 1: transverse of A+-dq; 2: also of the corrections */
+  double cfl_reject;            /* fc_step rejects (FC_ECFL) when max CFL exceeds this (e.g. 1.0) */
+} fc_problem;
+
+typedef struct {
+  int64_t kernel_launches;      /* kernels this handle launched since creation / last reset */
+  int64_t steps;                /* committed steps */
+  double ms_ghost;              /* accumulated device time in ghost-fill kernels (timing on) */
+  double ms_step;               /* accumulated device time in the update kernel (timing on) */
+  double ms_comm;               /* accumulated device time in halo pack/NCCL/unpack + allreduce */
+  int64_t step_kernel_launches; /* launches of the update kernel counted in ms_step */
+  int64_t local_patches;        /* patches owned by this rank */
+  int64_t halo_cells;           /* remote cells received per step (all rounds) */
+  int32_t uniform_fast_path;    /* 1 if the fused gather path (no ring writes) is used */
+  int32_t pad_;
+} fc_stats;
+
+/* ---- calls --------------------------------------------------------------------------------- */
+
+/* Copy and validate the forest, decode Morton order, build the neighbour / ghost tables and the
+ * shard + halo plan, allocate device state (q_old, q_new double buffer, aux) and, when
+ * nranks > 1, create the NCCL communicator.  Validation: tree ids non-decreasing and every tree
+ * tiled exactly (FC_ETILING); connectivity symmetric (FC_ECONN); m even >= 4, mbc == 2
+ * (FC_EINVAL); face and corner level jumps <= 1 (FC_EBALANCE).  *out is NULL on failure. */
+int fc_forest_create(const fc_forest_desc* desc, fc_forest** out);
+
+/* Free everything the handle owns (device memory, streams, events, communicator). */
+int fc_forest_destroy(fc_forest* f);
+
+/* Select the solver.  FC_EINVAL if kind/meqn/maux disagree or parameters are out of range. */
+int fc_set_problem(fc_forest* f, const fc_problem* pr);
+
+/* aux[P_local][maux][n][n] including the ghost ring (FC_ADV_EDGEVEL_CAPA only): kappa, u~ at
+ * each cell's left edge, v~ at its bottom edge.  Copied into device memory. */
+int fc_set_aux(fc_forest* f, const double* aux, int where);
+
+/* q[P_local][meqn][m][m] -> interior of q_old.  The ghost ring becomes stale until the next
+ * fill.  FC_ESTATE before fc_set_problem. */
+int fc_set_q(fc_forest* f, const double* q, int where);
+
+/* Fill the ghost rings of q_old (halo exchange included) -- inspection / tests; fc_step does its
+ * own fill.  Ring contents are then readable with fc_get_q_padded. */
+int fc_ghost_fill(fc_forest* f);
+
+/* One step: ghost fill + wave-propagation update of every local patch + global max CFL
+ * (*max_cfl, max over edges and waves of dt |s| / (kappa dx) taken on the upwind side,
+ * PAPER.md:276-277).  Commits (swaps q_old / q_new) iff max_cfl <= cfl_reject; otherwise returns
+ * FC_ECFL with q unchanged.  FC_EINVAL if dt <= 0 or not finite; FC_ENONFINITE if the CFL is
+ * NaN/Inf (state unchanged).  Synchronises the handle's stream (the CFL is returned to the host). */
+int fc_step(fc_forest* f, double dt, double* max_cfl);
+
+/* Interior q_old -> q[P_local][meqn][m][m].  Synchronous. */
+int fc_get_q(fc_forest* f, double* q, int where);
+
+/* Padded q_old (ring as left by the last fill) -> q[P_local][meqn][n][n].  Synchronous. */
+int fc_get_q_padded(fc_forest* f, double* q, int where);
+
+/* Canonical ghost table of the LOCAL patches (global patch ids, independent of sharding):
+ * which = FC_TABLE_EXPANDED: for each local patch, for each ring cell in storage order
+ * (j = -1..m+2 outer, i = -1..m+2 inner, interior skipped; G = n^2 - m^2 cells), 8 int32
+ * {op, src_patch, src_i, src_j, a, b, c, d} with op 1 COPY (src cell), 2 AVG4 (lower-left cell of
+ * the 2x2 fine block, source frame), 3 INTERP (coarse cell; a, b = +-1 offset signs in the coarse
+ * frame), 4 BCX / 5 BCY (own cell mirrored or extrapolated; a = bc kind), 6 CORNER3 (average of
+ * own cells (src_i, src_j) and (c, d)).  *len = P_local * G * 8; FC_EINVAL if cap < *len
+ * (len is still set).  Works on host-only handles (device = -1). */
+int fc_get_ghost_table(fc_forest* f, int which, int32_t* buf, int64_t cap, int64_t* len);
+
+/* Use the caller's cudaStream_t for all subsequent work (NULL = the handle's own stream). */
+int fc_set_stream(fc_forest* f, void* stream);
+
+/* Enable (1) / disable (0) per-phase CUDA-event timing accumulated into fc_stats. */
+int fc_set_timing(fc_forest* f, int on);
+
+/* Counters and timings; fc_reset_stats zeroes the accumulating fields. */
+int fc_get_stats(fc_forest* f, fc_stats* out);
+int fc_reset_stats(fc_forest* f);
+
+/* First local patch (global id) and count of local patches. */
+int fc_local_range(fc_forest* f, int64_t* first, int64_t* count);
+
+/* Halo plan of this rank for tests of the sharded path: per peer the number of remote cells this
+ * rank receives per step (counts[nranks]).  Works on host-only handles. */
+int fc_halo_counts(fc_forest* f, int64_t* counts);
+
+/* Write a fresh 128-byte ncclUniqueId into out (call on rank 0, broadcast to the others). */
+int fc_nccl_unique_id(void* out);
+
+/* Thread-local message describing the last error (never NULL). */
+const char* fc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

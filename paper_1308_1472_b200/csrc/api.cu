@@ -1,0 +1,527 @@
+// api.cu -- the libfc C ABI (include/fc.h): handle lifetime, device state, ghost-fill schedule,
+// halo exchange over NCCL, the step with its CFL reduction, and instrumentation.
+//
+// Schedule of one step (PAPER.md:264-277 [§4]: one ghost exchange per global-dt step, before the
+// local neighbour work):
+//   [halo round 1: pack -> ncclSend/Recv -> unpack]  A: copy, average  ->  C: BC x, BC y
+//   [halo round 2]  for each level ascending: B: interpolate -> C of that level  ->  CORNER3
+//   step kernel (q_old -> q_new, per-CTA CFL max -> atomicMax)  [ncclAllReduce(max)]
+//   CFL -> host; commit (swap) iff CFL <= cfl_reject.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fc_internal.h"
+
+namespace fc {
+int launch_ghost(int op, double* q, const int32_t* list, int64_t nrec, int meqn, int n2, cudaStream_t st);
+int launch_pack(const double* q, const int32_t* idx, int64_t cnt, int meqn, int n2, double* buf, cudaStream_t st);
+int launch_unpack(double* q, const int32_t* idx, int64_t cnt, int meqn, int n2, const double* buf, cudaStream_t st);
+int launch_scatter(const double* src, double* q, int64_t P, int meqn, int m, cudaStream_t st);
+int launch_gather(const double* q, double* dst, int64_t P, int meqn, int m, cudaStream_t st);
+int launch_step(int kind, const double* qold, double* qnew, const double* aux, const int8_t* level,
+                int64_t npatch, int m, double dt, double dx0, double p0, double p1, int limiter,
+                int method2, int method3, unsigned long long* cfl_bits, cudaStream_t st);
+}  // namespace fc
+
+using namespace fc;
+
+static thread_local std::string g_err = "no error";
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(FC_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+#define NK(call)                                                                       \
+  do {                                                                                 \
+    ncclResult_t r_ = (call);                                                          \
+    if (r_ != ncclSuccess)                                                             \
+      return fail(FC_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));       \
+  } while (0)
+
+struct DevList {
+  int32_t* d = nullptr;
+  int64_t nrec = 0;
+};
+
+struct fc_forest {
+  Plan pl;
+  GhostLists gl;
+  bool host_only = true;
+  int device = -1;
+  int64_t Pl = 0, Pv = 0;        // local patches, + virtual halo patches
+  size_t state_doubles = 0;
+  cudaStream_t stream = nullptr, own_stream = nullptr;
+  double *qold = nullptr, *qnew = nullptr, *aux = nullptr;
+  int8_t* d_level = nullptr;
+  unsigned long long* d_cfl = nullptr;
+  double* h_cfl = nullptr;
+  DevList copy, avg, bcx, bcy, corner3;
+  std::vector<DevList> interp, bcx_l, bcy_l;
+  fc_problem prob{};
+  bool has_problem = false, has_q = false, has_aux = false;
+  // halo
+  ncclComm_t comm = nullptr;
+  // per round: concatenated pack / unpack index lists and per-peer counts
+  int32_t *d_pack[2] = {nullptr, nullptr}, *d_unpack[2] = {nullptr, nullptr};
+  int64_t npack[2] = {0, 0}, nunpack[2] = {0, 0};
+  std::vector<int64_t> send_cnt[2], recv_cnt[2];
+  double *d_sendbuf = nullptr, *d_recvbuf = nullptr;
+  // instrumentation
+  fc_stats st{};
+  bool timing = false;
+  cudaEvent_t ev[6] = {};
+};
+
+static int to_dev(fc_forest* f, const std::vector<int32_t>& v, int rec, DevList& out) {
+  out.nrec = (int64_t)v.size() / rec;
+  if (v.empty()) return FC_OK;
+  CK(cudaMalloc(&out.d, v.size() * sizeof(int32_t)));
+  CK(cudaMemcpy(out.d, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  (void)f;
+  return FC_OK;
+}
+
+static void free_list(DevList& l) {
+  if (l.d) cudaFree(l.d);
+  l.d = nullptr;
+}
+
+// one-time NCCL exchange of halo requests -> pack / unpack lists
+static int setup_halo(fc_forest* f, const void* nccl_id) {
+  Plan& pl = f->pl;
+  const int R = pl.nranks, me = pl.rank;
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id, sizeof(id));
+  NK(ncclCommInitRank(&f->comm, R, id, me));
+  const int64_t n2 = (int64_t)pl.n * pl.n;
+  const int64_t S = (int64_t)pl.meqn * n2;
+  // counts matrix: row r = what rank r needs from each peer, rounds 1 and 2
+  std::vector<int64_t> mine(2 * R), all((size_t)2 * R * R);
+  for (int s = 0; s < R; ++s) {
+    mine[s] = (int64_t)pl.halo.need1[s].size();
+    mine[R + s] = (int64_t)pl.halo.need2[s].size();
+  }
+  int64_t *d_mine = nullptr, *d_all = nullptr;
+  CK(cudaMalloc(&d_mine, mine.size() * sizeof(int64_t)));
+  CK(cudaMalloc(&d_all, all.size() * sizeof(int64_t)));
+  CK(cudaMemcpy(d_mine, mine.data(), mine.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  NK(ncclAllGather(d_mine, d_all, 2 * R, ncclInt64, f->comm, f->stream));
+  CK(cudaMemcpyAsync(all.data(), d_all, all.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  cudaFree(d_mine);
+  cudaFree(d_all);
+  for (int round = 0; round < 2; ++round) {
+    f->send_cnt[round].assign(R, 0);
+    f->recv_cnt[round].assign(R, 0);
+    for (int s = 0; s < R; ++s) {
+      f->recv_cnt[round][s] = mine[round * R + s];          // I need from s
+      f->send_cnt[round][s] = all[(size_t)s * 2 * R + round * R + me];  // s needs from me
+    }
+    // send my requests to the owners, receive the peers' requests
+    const auto& need = round == 0 ? pl.halo.need1 : pl.halo.need2;
+    std::vector<int64_t> req_out, req_in;
+    std::vector<int64_t> off_out(R + 1, 0), off_in(R + 1, 0);
+    for (int s = 0; s < R; ++s) {
+      off_out[s + 1] = off_out[s] + (int64_t)need[s].size();
+      off_in[s + 1] = off_in[s] + f->send_cnt[round][s];
+      req_out.insert(req_out.end(), need[s].begin(), need[s].end());
+    }
+    req_in.resize(off_in[R]);
+    int64_t *d_out = nullptr, *d_in = nullptr;
+    CK(cudaMalloc(&d_out, std::max<int64_t>(1, off_out[R]) * sizeof(int64_t)));
+    CK(cudaMalloc(&d_in, std::max<int64_t>(1, off_in[R]) * sizeof(int64_t)));
+    if (off_out[R])
+      CK(cudaMemcpy(d_out, req_out.data(), off_out[R] * sizeof(int64_t), cudaMemcpyHostToDevice));
+    NK(ncclGroupStart());
+    for (int s = 0; s < R; ++s) {
+      if (s == me) continue;
+      if (need[s].size()) NK(ncclSend(d_out + off_out[s], need[s].size(), ncclInt64, s, f->comm, f->stream));
+      if (f->send_cnt[round][s]) NK(ncclRecv(d_in + off_in[s], f->send_cnt[round][s], ncclInt64, s, f->comm, f->stream));
+    }
+    NK(ncclGroupEnd());
+    CK(cudaStreamSynchronize(f->stream));
+    if (off_in[R])
+      CK(cudaMemcpy(req_in.data(), d_in, off_in[R] * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    cudaFree(d_out);
+    cudaFree(d_in);
+    // pack list: requested (global patch, cell) -> local offset of component 0
+    std::vector<int32_t> pack(off_in[R]), unpack;
+    for (int64_t k = 0; k < off_in[R]; ++k) {
+      const int64_t q = req_in[k] / n2, cell = req_in[k] % n2;
+      if (q < pl.p0 || q >= pl.p1) return fail(FC_EINVAL, "halo request for a patch this rank does not own");
+      pack[k] = (int32_t)((q - pl.p0) * S + cell);
+    }
+    // unpack list: my requests in slot order
+    for (int s = 0; s < R; ++s)
+      for (int64_t key : need[s]) {
+        const int64_t h = pl.halo.slot.at(key * 2 + round);
+        unpack.push_back((int32_t)((f->Pl + h / n2) * S + h % n2));
+      }
+    f->npack[round] = (int64_t)pack.size();
+    f->nunpack[round] = (int64_t)unpack.size();
+    if (!pack.empty()) {
+      CK(cudaMalloc(&f->d_pack[round], pack.size() * sizeof(int32_t)));
+      CK(cudaMemcpy(f->d_pack[round], pack.data(), pack.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    if (!unpack.empty()) {
+      CK(cudaMalloc(&f->d_unpack[round], unpack.size() * sizeof(int32_t)));
+      CK(cudaMemcpy(f->d_unpack[round], unpack.data(), unpack.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+  }
+  const int64_t maxs = std::max(f->npack[0], f->npack[1]), maxr = std::max(f->nunpack[0], f->nunpack[1]);
+  CK(cudaMalloc(&f->d_sendbuf, std::max<int64_t>(1, maxs) * pl.meqn * sizeof(double)));
+  CK(cudaMalloc(&f->d_recvbuf, std::max<int64_t>(1, maxr) * pl.meqn * sizeof(double)));
+  f->st.halo_cells = f->nunpack[0] + f->nunpack[1];
+  return FC_OK;
+}
+
+static int halo_round(fc_forest* f, int round) {
+  if (f->pl.nranks <= 1) return FC_OK;
+  const int R = f->pl.nranks, me = f->pl.rank, meqn = f->pl.meqn;
+  const int n2 = f->pl.n * f->pl.n;
+  f->st.kernel_launches += launch_pack(f->qold, f->d_pack[round], f->npack[round], meqn, n2, f->d_sendbuf, f->stream);
+  CK(cudaGetLastError());
+  NK(ncclGroupStart());
+  int64_t so = 0, ro = 0;
+  for (int s = 0; s < R; ++s) {
+    const int64_t sc = f->send_cnt[round][s], rc = f->recv_cnt[round][s];
+    if (s != me && sc) NK(ncclSend(f->d_sendbuf + so * meqn, sc * meqn, ncclDouble, s, f->comm, f->stream));
+    if (s != me && rc) NK(ncclRecv(f->d_recvbuf + ro * meqn, rc * meqn, ncclDouble, s, f->comm, f->stream));
+    so += sc;
+    ro += rc;
+  }
+  NK(ncclGroupEnd());
+  f->st.kernel_launches += launch_unpack(f->qold, f->d_unpack[round], f->nunpack[round], meqn, n2, f->d_recvbuf, f->stream);
+  CK(cudaGetLastError());
+  return FC_OK;
+}
+
+static int ghost_fill_internal(fc_forest* f) {
+  const int meqn = f->pl.meqn, n2 = f->pl.n * f->pl.n;
+  int rc;
+  if ((rc = halo_round(f, 0))) return rc;
+  auto run = [&](int op, const DevList& l) {
+    f->st.kernel_launches += launch_ghost(op, f->qold, l.d, l.nrec, meqn, n2, f->stream);
+  };
+  run(OP_COPY, f->copy);
+  run(OP_AVG4, f->avg);
+  run(4, f->bcx);
+  run(4, f->bcy);
+  CK(cudaGetLastError());
+  if (f->npack[1] || f->nunpack[1])
+    if ((rc = halo_round(f, 1))) return rc;
+  for (size_t l = 0; l < f->interp.size(); ++l) {
+    if (!f->interp[l].nrec) continue;
+    run(OP_INTERP, f->interp[l]);
+    run(4, f->bcx_l[l]);
+    run(4, f->bcy_l[l]);
+  }
+  run(6, f->corner3);
+  CK(cudaGetLastError());
+  return FC_OK;
+}
+
+static void destroy(fc_forest* f) {
+  if (!f) return;
+  if (!f->host_only) {
+    cudaSetDevice(f->device);
+    if (f->stream) cudaStreamSynchronize(f->stream);
+    cudaFree(f->qold); cudaFree(f->qnew); cudaFree(f->aux); cudaFree(f->d_level); cudaFree(f->d_cfl);
+    if (f->h_cfl) cudaFreeHost(f->h_cfl);
+    free_list(f->copy); free_list(f->avg); free_list(f->bcx); free_list(f->bcy); free_list(f->corner3);
+    for (auto& l : f->interp) free_list(l);
+    for (auto& l : f->bcx_l) free_list(l);
+    for (auto& l : f->bcy_l) free_list(l);
+    for (int r = 0; r < 2; ++r) { cudaFree(f->d_pack[r]); cudaFree(f->d_unpack[r]); }
+    cudaFree(f->d_sendbuf); cudaFree(f->d_recvbuf);
+    for (auto& e : f->ev) if (e) cudaEventDestroy(e);
+    if (f->comm) ncclCommDestroy(f->comm);
+    if (f->own_stream) cudaStreamDestroy(f->own_stream);
+  }
+  delete f;
+}
+
+extern "C" {
+
+const char* fc_last_error(void) { return g_err.c_str(); }
+
+int fc_nccl_unique_id(void* out) {
+  if (!out) return fail(FC_EINVAL, "null output");
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return FC_OK;
+}
+
+int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
+  if (!out) return fail(FC_EINVAL, "null output handle");
+  *out = nullptr;
+  fc_forest* f = new (std::nothrow) fc_forest();
+  if (!f) return fail(FC_ENOMEM, "host allocation failed");
+  std::string err;
+  int rc = plan_build(d, f->pl, err);
+  if (rc) { delete f; return fail(rc, err); }
+  f->Pl = f->pl.p1 - f->pl.p0;
+  f->st.local_patches = f->Pl;
+  f->st.uniform_fast_path = 0;
+  if (d->device < 0) {           // host-only planning handle: tables and plans, no device work
+    f->host_only = true;
+    *out = f;
+    return FC_OK;
+  }
+  if (d->nranks > 1 && !d->nccl_id) { delete f; return fail(FC_EINVAL, "nranks > 1 needs nccl_id"); }
+  f->host_only = false;
+  f->device = d->device;
+  const Plan& pl = f->pl;
+  const int64_t n2 = (int64_t)pl.n * pl.n;
+  auto cuda_fail = [&](cudaError_t e, const char* what) {
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    destroy(f);
+    return fail(e == cudaErrorMemoryAllocation ? FC_ENOMEM : FC_ECUDA, m);
+  };
+  cudaError_t e;
+  if ((e = cudaSetDevice(f->device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  if ((e = cudaStreamCreateWithFlags(&f->own_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return cuda_fail(e, "cudaStreamCreate");
+  f->stream = f->own_stream;
+  const int64_t nhalo = pl.halo.n1 + pl.halo.n2;
+  f->Pv = (nhalo + n2 - 1) / n2;
+  f->state_doubles = (size_t)(f->Pl + f->Pv) * pl.meqn * n2;
+  if ((e = cudaMalloc(&f->qold, f->state_doubles * sizeof(double))) != cudaSuccess) return cuda_fail(e, "cudaMalloc q_old");
+  if ((e = cudaMalloc(&f->qnew, f->state_doubles * sizeof(double))) != cudaSuccess) return cuda_fail(e, "cudaMalloc q_new");
+  cudaMemset(f->qold, 0, f->state_doubles * sizeof(double));
+  cudaMemset(f->qnew, 0, f->state_doubles * sizeof(double));
+  if (pl.maux > 0) {
+    if ((e = cudaMalloc(&f->aux, (size_t)f->Pl * pl.maux * n2 * sizeof(double))) != cudaSuccess)
+      return cuda_fail(e, "cudaMalloc aux");
+  }
+  std::vector<int8_t> lv(f->Pl);
+  for (int64_t p = 0; p < f->Pl; ++p) lv[p] = (int8_t)pl.leaves[pl.p0 + p].level;
+  if ((e = cudaMalloc(&f->d_level, std::max<int64_t>(1, f->Pl))) != cudaSuccess) return cuda_fail(e, "cudaMalloc level");
+  cudaMemcpy(f->d_level, lv.data(), f->Pl, cudaMemcpyHostToDevice);
+  if ((e = cudaMalloc(&f->d_cfl, sizeof(unsigned long long))) != cudaSuccess) return cuda_fail(e, "cudaMalloc cfl");
+  if ((e = cudaMallocHost(&f->h_cfl, sizeof(double))) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+  for (auto& ev : f->ev)
+    if ((e = cudaEventCreate(&ev)) != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+  rc = plan_lists(f->pl, pl.meqn, f->gl, err);
+  if (rc) { destroy(f); return fail(rc, err); }
+  if ((rc = to_dev(f, f->gl.copy, 2, f->copy)) || (rc = to_dev(f, f->gl.avg, 5, f->avg)) ||
+      (rc = to_dev(f, f->gl.bcx, 3, f->bcx)) || (rc = to_dev(f, f->gl.bcy, 3, f->bcy)) ||
+      (rc = to_dev(f, f->gl.corner3, 3, f->corner3))) {
+    std::string m = g_err;
+    destroy(f);
+    return fail(rc, m);
+  }
+  f->interp.resize(f->gl.interp.size());
+  f->bcx_l.resize(f->gl.interp.size());
+  f->bcy_l.resize(f->gl.interp.size());
+  for (size_t l = 0; l < f->gl.interp.size(); ++l) {
+    if ((rc = to_dev(f, f->gl.interp[l], 8, f->interp[l])) || (rc = to_dev(f, f->gl.bcx_l[l], 3, f->bcx_l[l])) ||
+        (rc = to_dev(f, f->gl.bcy_l[l], 3, f->bcy_l[l]))) {
+      std::string m = g_err;
+      destroy(f);
+      return fail(rc, m);
+    }
+  }
+  if (pl.nranks > 1) {
+    rc = setup_halo(f, d->nccl_id);
+    if (rc) { std::string m = g_err; destroy(f); return fail(rc, m); }
+  }
+  *out = f;
+  return FC_OK;
+}
+
+int fc_forest_destroy(fc_forest* f) {
+  destroy(f);
+  return FC_OK;
+}
+
+int fc_set_problem(fc_forest* f, const fc_problem* pr) {
+  if (!f || !pr) return fail(FC_EINVAL, "null argument");
+  static const int meqn_of[4] = {1, 1, 3, 4}, maux_of[4] = {0, 3, 0, 0};
+  if (pr->kind < 0 || pr->kind > 3) return fail(FC_EINVAL, "unknown problem kind");
+  if (meqn_of[pr->kind] != f->pl.meqn || maux_of[pr->kind] != f->pl.maux)
+    return fail(FC_EINVAL, "meqn/maux of the forest do not match the problem kind");
+  if (pr->limiter < 0 || pr->limiter > 2 || pr->method2 < 1 || pr->method2 > 2 || pr->method3 < 0 ||
+      pr->method3 > 2)
+    return fail(FC_EINVAL, "limiter/method out of range");
+  if ((pr->kind == FC_SWE_ROE || pr->kind == FC_EULER_ROE) && !(pr->p0 > 0.0))
+    return fail(FC_EINVAL, "g / gamma must be positive");
+  if (pr->kind == FC_EULER_ROE && !(pr->p0 > 1.0)) return fail(FC_EINVAL, "gamma must exceed 1");
+  f->prob = *pr;
+  f->has_problem = true;
+  return FC_OK;
+}
+
+int fc_set_stream(fc_forest* f, void* stream) {
+  if (!f) return fail(FC_EINVAL, "null handle");
+  if (f->host_only) return fail(FC_ESTATE, "host-only handle");
+  f->stream = stream ? (cudaStream_t)stream : f->own_stream;
+  return FC_OK;
+}
+
+int fc_set_timing(fc_forest* f, int on) {
+  if (!f) return fail(FC_EINVAL, "null handle");
+  f->timing = on != 0;
+  return FC_OK;
+}
+
+int fc_get_stats(fc_forest* f, fc_stats* out) {
+  if (!f || !out) return fail(FC_EINVAL, "null argument");
+  *out = f->st;
+  return FC_OK;
+}
+
+int fc_reset_stats(fc_forest* f) {
+  if (!f) return fail(FC_EINVAL, "null handle");
+  f->st.kernel_launches = 0;
+  f->st.steps = 0;
+  f->st.ms_ghost = f->st.ms_step = f->st.ms_comm = 0.0;
+  f->st.step_kernel_launches = 0;
+  return FC_OK;
+}
+
+int fc_local_range(fc_forest* f, int64_t* first, int64_t* count) {
+  if (!f || !first || !count) return fail(FC_EINVAL, "null argument");
+  *first = f->pl.p0;
+  *count = f->Pl;
+  return FC_OK;
+}
+
+int fc_halo_counts(fc_forest* f, int64_t* counts) {
+  if (!f || !counts) return fail(FC_EINVAL, "null argument");
+  for (int s = 0; s < f->pl.nranks; ++s)
+    counts[s] = (int64_t)(f->pl.halo.need1[s].size() + f->pl.halo.need2[s].size());
+  return FC_OK;
+}
+
+int fc_get_ghost_table(fc_forest* f, int which, int32_t* buf, int64_t cap, int64_t* len) {
+  if (!f || !len) return fail(FC_EINVAL, "null argument");
+  if (which != FC_TABLE_EXPANDED) return fail(FC_EINVAL, "unknown table kind");
+  *len = (int64_t)f->pl.table.size();
+  if (!buf || cap < *len) return fail(FC_EINVAL, "buffer too small");
+  std::memcpy(buf, f->pl.table.data(), f->pl.table.size() * sizeof(int32_t));
+  return FC_OK;
+}
+
+int fc_set_aux(fc_forest* f, const double* aux, int where) {
+  if (!f || !aux) return fail(FC_EINVAL, "null argument");
+  if (f->host_only) return fail(FC_ESTATE, "host-only handle");
+  if (f->pl.maux == 0) return fail(FC_EINVAL, "forest has maux = 0");
+  CK(cudaSetDevice(f->device));
+  const size_t bytes = (size_t)f->Pl * f->pl.maux * f->pl.n * f->pl.n * sizeof(double);
+  CK(cudaMemcpyAsync(f->aux, aux, bytes, where == FC_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  f->has_aux = true;
+  return FC_OK;
+}
+
+int fc_set_q(fc_forest* f, const double* q, int where) {
+  if (!f || !q) return fail(FC_EINVAL, "null argument");
+  if (f->host_only) return fail(FC_ESTATE, "host-only handle");
+  if (!f->has_problem) return fail(FC_ESTATE, "fc_set_problem first");
+  CK(cudaSetDevice(f->device));
+  const int m = f->pl.m, meqn = f->pl.meqn;
+  const size_t bytes = (size_t)f->Pl * meqn * m * m * sizeof(double);
+  const double* src = q;
+  if (where != FC_DEVICE) {   // stage through q_new (free between steps)
+    CK(cudaMemcpyAsync(f->qnew, q, bytes, cudaMemcpyHostToDevice, f->stream));
+    src = f->qnew;
+  }
+  f->st.kernel_launches += launch_scatter(src, f->qold, f->Pl, meqn, m, f->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(f->stream));
+  f->has_q = true;
+  return FC_OK;
+}
+
+int fc_get_q(fc_forest* f, double* q, int where) {
+  if (!f || !q) return fail(FC_EINVAL, "null argument");
+  if (f->host_only || !f->has_q) return fail(FC_ESTATE, "no state");
+  CK(cudaSetDevice(f->device));
+  const int m = f->pl.m, meqn = f->pl.meqn;
+  const size_t bytes = (size_t)f->Pl * meqn * m * m * sizeof(double);
+  double* dst = where == FC_DEVICE ? q : f->qnew;
+  f->st.kernel_launches += launch_gather(f->qold, dst, f->Pl, meqn, m, f->stream);
+  CK(cudaGetLastError());
+  if (where != FC_DEVICE) CK(cudaMemcpyAsync(q, f->qnew, bytes, cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  return FC_OK;
+}
+
+int fc_get_q_padded(fc_forest* f, double* q, int where) {
+  if (!f || !q) return fail(FC_EINVAL, "null argument");
+  if (f->host_only || !f->has_q) return fail(FC_ESTATE, "no state");
+  CK(cudaSetDevice(f->device));
+  const size_t bytes = (size_t)f->Pl * f->pl.meqn * f->pl.n * f->pl.n * sizeof(double);
+  CK(cudaMemcpyAsync(q, f->qold, bytes, where == FC_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  return FC_OK;
+}
+
+int fc_ghost_fill(fc_forest* f) {
+  if (!f) return fail(FC_EINVAL, "null handle");
+  if (f->host_only || !f->has_q) return fail(FC_ESTATE, "no state");
+  CK(cudaSetDevice(f->device));
+  int rc = ghost_fill_internal(f);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(f->stream));
+  return FC_OK;
+}
+
+int fc_step(fc_forest* f, double dt, double* max_cfl) {
+  if (!f) return fail(FC_EINVAL, "null handle");
+  if (f->host_only || !f->has_q || !f->has_problem) return fail(FC_ESTATE, "set problem and q first");
+  if (f->pl.maux > 0 && !f->has_aux) return fail(FC_ESTATE, "set aux first");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(FC_EINVAL, "dt must be positive and finite");
+  CK(cudaSetDevice(f->device));
+  if (f->timing) CK(cudaEventRecord(f->ev[0], f->stream));
+  int rc = ghost_fill_internal(f);
+  if (rc) return rc;
+  if (f->timing) CK(cudaEventRecord(f->ev[1], f->stream));
+  CK(cudaMemsetAsync(f->d_cfl, 0, sizeof(unsigned long long), f->stream));
+  const fc_problem& p = f->prob;
+  int lr = launch_step(p.kind, f->qold, f->qnew, f->aux, f->d_level, f->Pl, f->pl.m, dt, f->pl.dx0,
+                       p.p0, p.p1, p.limiter, p.method2, p.method3, f->d_cfl, f->stream);
+  if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
+  f->st.kernel_launches += lr;
+  f->st.step_kernel_launches += lr;
+  CK(cudaGetLastError());
+  if (f->timing) CK(cudaEventRecord(f->ev[2], f->stream));
+  if (f->pl.nranks > 1)
+    NK(ncclAllReduce(f->d_cfl, f->d_cfl, 1, ncclDouble, ncclMax, f->comm, f->stream));
+  if (f->timing) CK(cudaEventRecord(f->ev[3], f->stream));
+  CK(cudaMemcpyAsync(f->h_cfl, f->d_cfl, sizeof(double), cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  if (f->timing) {
+    float a = 0.f, b = 0.f, c = 0.f;
+    cudaEventElapsedTime(&a, f->ev[0], f->ev[1]);
+    cudaEventElapsedTime(&b, f->ev[1], f->ev[2]);
+    cudaEventElapsedTime(&c, f->ev[2], f->ev[3]);
+    f->st.ms_ghost += a;
+    f->st.ms_step += b;
+    f->st.ms_comm += c;
+  }
+  const double cfl = *f->h_cfl;
+  if (max_cfl) *max_cfl = cfl;
+  if (!std::isfinite(cfl)) return fail(FC_ENONFINITE, "CFL is not finite");
+  if (cfl > p.cfl_reject) return fail(FC_ECFL, "CFL above cfl_reject; step not committed");
+  std::swap(f->qold, f->qnew);
+  f->st.steps += 1;
+  return FC_OK;
+}
+
+}  // extern "C"

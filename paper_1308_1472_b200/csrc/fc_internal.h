@@ -1,0 +1,92 @@
+// fc_internal.h -- libfc private structures (host planner <-> device runtime).
+// Nothing here is shared with oracle/ (the oracle has its own sources and header).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/fc.h"
+
+namespace fc {
+
+// ghost-record ops (canonical EXPANDED table, include/fc.h)
+enum Op : int32_t { OP_NONE = 0, OP_COPY = 1, OP_AVG4 = 2, OP_INTERP = 3, OP_BCX = 4, OP_BCY = 5, OP_CORNER3 = 6 };
+constexpr int REC = 8;
+
+struct Leaf {
+  int32_t tree;
+  int32_t level;
+  int64_t x, y;  // origin in units of level-Lmax leaves
+};
+
+// Isometry of the plane on "fine units" (1 unit = half a level-Lmax cell; tree edge E = 2 m 2^Lmax):
+// P' = R P + b, landing in tree `tree`.
+struct Affine {
+  int r00 = 1, r01 = 0, r10 = 0, r11 = 1;
+  int64_t b0 = 0, b1 = 0;
+  int32_t tree = 0;
+  bool operator==(const Affine& o) const {
+    return r00 == o.r00 && r01 == o.r01 && r10 == o.r10 && r11 == o.r11 && b0 == o.b0 &&
+           b1 == o.b1 && tree == o.tree;
+  }
+};
+
+enum DirKind : int { D_SAME = 0, D_COARSER = 1, D_FINER = 2, D_PHYS = 3, D_CORNER3 = 4 };
+
+struct DirInfo {
+  DirKind kind;
+  Affine T;        // p's tree coordinates -> neighbour tree coordinates
+  int64_t leaf;    // SAME / COARSER: the neighbour leaf; FINER: resolved per cell
+};
+
+struct LeafKeyHash {
+  size_t operator()(const std::tuple<int32_t, int32_t, int64_t, int64_t>& k) const {
+    uint64_t h = (uint64_t)std::get<0>(k) * 0x9E3779B97F4A7C15ull;
+    h ^= (uint64_t)std::get<1>(k) + 0x7F4A7C159E3779B9ull + (h << 6) + (h >> 2);
+    h ^= (uint64_t)std::get<2>(k) * 0xC2B2AE3D27D4EB4Full + (h << 6) + (h >> 2);
+    h ^= (uint64_t)std::get<3>(k) * 0x165667B19E3779F9ull + (h << 6) + (h >> 2);
+    return (size_t)h;
+  }
+};
+
+// Typed ghost work lists, offsets in doubles relative to the state base:
+// local patch slot s, cell c -> s * S + c (S = meqn n^2); halo cell h -> (Pl + h / n2) * S + h % n2.
+struct GhostLists {
+  std::vector<int32_t> copy;      // {dst, src}
+  std::vector<int32_t> avg;       // {dst, s00, s10, s01, s11}
+  std::vector<int32_t> bcx, bcy;  // {dst, src, negated component or -1}  (all patches)
+  std::vector<int32_t> corner3;   // {dst, a, b}
+  // per level l: INTERP records {dst, c, xm, xp, ym, yp, sigx, sigy} and that level's BC records
+  std::vector<std::vector<int32_t>> interp, bcx_l, bcy_l;
+};
+
+struct HaloPlan {
+  // per peer: requested remote cells (global patch id * n2 + cell), rounds 1 and 2
+  std::vector<std::vector<int64_t>> need1, need2;
+  int64_t n1 = 0, n2 = 0;   // total halo cells per round
+  std::unordered_map<int64_t, int64_t> slot;   // key (gpatch * n2 + cell) * 2 + (round - 1) -> slot
+};
+
+struct Plan {
+  int64_t P = 0;
+  int32_t T = 0, m = 0, n = 0, meqn = 0, maux = 0, lmax = 0;
+  double dx0 = 0.0;
+  std::vector<Leaf> leaves;
+  std::unordered_map<std::tuple<int32_t, int32_t, int64_t, int64_t>, int64_t, LeafKeyHash> index;
+  std::vector<int32_t> t2t;
+  std::vector<int8_t> t2f, fbc;
+  int rank = 0, nranks = 1;
+  int64_t p0 = 0, p1 = 0;           // local range [p0, p1)
+  std::vector<int32_t> table;       // expanded records of local patches [Pl][G][8]
+  HaloPlan halo;
+  bool uniform_same = false;        // every ring cell is COPY/BC (no AVG/INTERP/CORNER3)
+  int lmin_local = 0, lmax_local = 0;
+};
+
+// planner entry points (plan.cpp); return FC_OK or an FC_E* code with err set
+int plan_build(const fc_forest_desc* d, Plan& pl, std::string& err);
+// build typed lists for `meqn` (component stride n^2); halo slots from pl.halo
+int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err);
+
+}  // namespace fc

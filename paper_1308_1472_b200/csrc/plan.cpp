@@ -1,0 +1,463 @@
+// plan.cpp -- libfc host planner: forest decode, per-direction neighbour lookup with inter-tree
+// transforms, canonical ghost records, typed GPU work lists and the multi-GPU halo plan.
+//
+// PAPER.md:137-146 [§2]: "an interface that provides ... the sequence of blocks, the list of
+// patches per-block, and a constant-time lookup of neighbor patches (and their relative and, in
+// general, nontrivial orientation between blocks)".  PAPER.md:258-260 [§4]: "When ForestClaw
+// accesses neighbor patches, they can be on the same or a different block.  In the latter case,
+// coordinate transformations are carried out."  PAPER.md:264-272 [§4]: ghost patches of remote
+// ranks are exchanged before the local neighbour work.
+//
+// Unlike the oracle (which locates every ghost-cell centre by a Morton-range search), this planner
+// looks up the neighbour region of each of the 8 directions of a patch once, in a hash of
+// (tree, level, x, y), after composing face-crossing isometries; cells are then expanded through
+// that direction's affine map.  The two must produce bit-identical tables (tests/).
+#include <algorithm>
+#include <cstring>
+#include <tuple>
+
+#include "fc_internal.h"
+
+namespace fc {
+
+static const int NX[4] = {-1, 1, 0, 0}, NY[4] = {0, 0, -1, 1};  // outward normals
+static const int TX[4] = {0, 0, 1, 1}, TY[4] = {1, 1, 0, 0};    // tangents
+
+static uint64_t compact_even_bits(uint64_t v) {
+  v &= 0x5555555555555555ull;
+  v = (v | (v >> 1)) & 0x3333333333333333ull;
+  v = (v | (v >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v >> 4)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v >> 8)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v >> 16)) & 0x00000000FFFFFFFFull;
+  return v;
+}
+
+static int face_of_normal(int nx, int ny) {
+  if (nx < 0) return 0;
+  if (nx > 0) return 1;
+  if (ny < 0) return 2;
+  return 3;
+}
+
+static bool is_phys(const Plan& pl, int t, int f) {
+  return pl.t2t[4 * t + f] == t && (pl.t2f[4 * t + f] & 3) == f;
+}
+
+// isometry carrying points just outside face f of tree t to the neighbour tree's coordinates:
+// P' = o_nf + tau'(P) tau_nf - d(P) n_nf with tau = tau_f.(P - o_f), d = n_f.(P - o_f) and
+// tau' = tau (aligned) or E - tau (reversed).  Returns false on a physical face.
+static bool cross_map(const Plan& pl, int t, int f, int64_t E, Affine& A) {
+  const int nt = pl.t2t[4 * t + f], code = pl.t2f[4 * t + f];
+  const int nf = code & 3, rev = code >> 2;
+  if (nt == t && nf == f) return false;
+  const int s = rev ? -1 : 1;
+  A.r00 = s * TX[nf] * TX[f] - NX[nf] * NX[f];
+  A.r01 = s * TX[nf] * TY[f] - NX[nf] * NY[f];
+  A.r10 = s * TY[nf] * TX[f] - NY[nf] * NX[f];
+  A.r11 = s * TY[nf] * TY[f] - NY[nf] * NY[f];
+  const int64_t ofx = (f == 1) ? E : 0, ofy = (f == 3) ? E : 0;
+  const int64_t onx = (nf == 1) ? E : 0, ony = (nf == 3) ? E : 0;
+  A.b0 = onx + (rev ? E * TX[nf] : 0) - (A.r00 * ofx + A.r01 * ofy);
+  A.b1 = ony + (rev ? E * TY[nf] : 0) - (A.r10 * ofx + A.r11 * ofy);
+  A.tree = nt;
+  return true;
+}
+
+static Affine compose(const Affine& A2, const Affine& A1) {  // A2 o A1
+  Affine C;
+  C.r00 = A2.r00 * A1.r00 + A2.r01 * A1.r10;
+  C.r01 = A2.r00 * A1.r01 + A2.r01 * A1.r11;
+  C.r10 = A2.r10 * A1.r00 + A2.r11 * A1.r10;
+  C.r11 = A2.r10 * A1.r01 + A2.r11 * A1.r11;
+  C.b0 = A2.r00 * A1.b0 + A2.r01 * A1.b1 + A2.b0;
+  C.b1 = A2.r10 * A1.b0 + A2.r11 * A1.b1 + A2.b1;
+  C.tree = A2.tree;
+  return C;
+}
+
+static inline void apply(const Affine& A, int64_t X, int64_t Y, int64_t& Xo, int64_t& Yo) {
+  Xo = A.r00 * X + A.r01 * Y + A.b0;
+  Yo = A.r10 * X + A.r11 * Y + A.b1;
+}
+
+static int64_t find_leaf(const Plan& pl, int t, int l, int64_t x, int64_t y) {
+  auto it = pl.index.find(std::make_tuple((int32_t)t, (int32_t)l, x, y));
+  return it == pl.index.end() ? -1 : it->second;
+}
+
+// neighbour region of patch p in direction (di, dj)
+static int dir_info(const Plan& pl, int64_t p, int di, int dj, DirInfo& D, std::string& err) {
+  const Leaf& L = pl.leaves[p];
+  const int64_t m2 = 2 * (int64_t)pl.m;
+  const int64_t E = m2 << pl.lmax;
+  const int64_t sz = 1ll << (pl.lmax - L.level);  // leaf size in level-Lmax leaves
+  const int64_t S = m2 * sz;                      // in fine units
+  const int64_t X0 = L.x * m2, Y0 = L.y * m2;
+  const bool outx = (di < 0 && X0 == 0) || (di > 0 && X0 + S == E);
+  const bool outy = (dj < 0 && Y0 == 0) || (dj > 0 && Y0 + S == E);
+  const int fx = di < 0 ? 0 : 1, fy = dj < 0 ? 2 : 3;
+  Affine T;
+  T.tree = L.tree;
+  D.leaf = -1;
+  if (outx && outy) {
+    Affine a1, a2, b1, b2;
+    bool ok = cross_map(pl, L.tree, fx, E, a1);
+    if (ok) ok = cross_map(pl, a1.tree, face_of_normal(a1.r01 * dj, a1.r11 * dj), E, a2);
+    bool okb = cross_map(pl, L.tree, fy, E, b1);
+    if (okb) okb = cross_map(pl, b1.tree, face_of_normal(b1.r00 * di, b1.r10 * di), E, b2);
+    if (!ok || !okb) { D.kind = D_PHYS; return FC_OK; }
+    Affine ta = compose(a2, a1), tb = compose(b2, b1);
+    if (!(ta == tb)) { D.kind = D_CORNER3; return FC_OK; }
+    T = ta;
+  } else if (outx) {
+    if (!cross_map(pl, L.tree, fx, E, T)) { D.kind = D_PHYS; return FC_OK; }
+  } else if (outy) {
+    if (!cross_map(pl, L.tree, fy, E, T)) { D.kind = D_PHYS; return FC_OK; }
+  }
+  D.T = T;
+  // image of the same-size neighbour region
+  int64_t ax, ay, bx, by;
+  apply(T, X0 + di * S, Y0 + dj * S, ax, ay);
+  apply(T, X0 + di * S + S, Y0 + dj * S + S, bx, by);
+  const int64_t ox = std::min(ax, bx), oy = std::min(ay, by);
+  if (ox % m2 || oy % m2 || ox < 0 || oy < 0 || ox + S > E || oy + S > E) {
+    err = "neighbour region not aligned (connectivity inconsistent)";
+    return FC_ECONN;
+  }
+  const int64_t qx = ox / m2, qy = oy / m2;
+  int64_t id = find_leaf(pl, T.tree, L.level, qx, qy);
+  if (id >= 0) { D.kind = D_SAME; D.leaf = id; return FC_OK; }
+  if (L.level >= 1) {
+    const int64_t ps = 2 * sz;
+    id = find_leaf(pl, T.tree, L.level - 1, (qx / ps) * ps, (qy / ps) * ps);
+    if (id >= 0) { D.kind = D_COARSER; D.leaf = id; return FC_OK; }
+  }
+  if (L.level < pl.lmax) { D.kind = D_FINER; return FC_OK; }
+  err = "2:1 balance violated (coarser-by-two neighbour)";
+  return FC_EBALANCE;
+}
+
+// canonical expanded records of any patch p (global id); rec[G][8]
+static int patch_records(const Plan& pl, int64_t p, int32_t* rec, std::string& err) {
+  const Leaf& L = pl.leaves[p];
+  const int m = pl.m;
+  const int64_t m2 = 2 * (int64_t)m;
+  const int64_t E = m2 << pl.lmax;
+  const int64_t sz = 1ll << (pl.lmax - L.level);
+  const int64_t S = m2 * sz, h = sz;  // h = half a cell of p in fine units
+  const int64_t X0 = L.x * m2, Y0 = L.y * m2;
+  DirInfo dirs[9];
+  for (int dj = -1; dj <= 1; ++dj)
+    for (int di = -1; di <= 1; ++di) {
+      if (!di && !dj) continue;
+      int rc = dir_info(pl, p, di, dj, dirs[(dj + 1) * 3 + (di + 1)], err);
+      if (rc) return rc;
+    }
+  int r = 0;
+  for (int j = -1; j <= m + 2; ++j)
+    for (int i = -1; i <= m + 2; ++i) {
+      if (i >= 1 && i <= m && j >= 1 && j <= m) continue;
+      int32_t* o = rec + REC * (r++);
+      std::memset(o, 0, REC * sizeof(int32_t));
+      const int di = i < 1 ? -1 : (i > m ? 1 : 0), dj = j < 1 ? -1 : (j > m ? 1 : 0);
+      const DirInfo& D = dirs[(dj + 1) * 3 + (di + 1)];
+      if (D.kind == D_PHYS) {
+        const bool yphys = dj != 0 && ((dj < 0 && Y0 == 0) || (dj > 0 && Y0 + S == E)) &&
+                           is_phys(pl, L.tree, dj < 0 ? 2 : 3);
+        const bool xphys = di != 0 && ((di < 0 && X0 == 0) || (di > 0 && X0 + S == E)) &&
+                           is_phys(pl, L.tree, di < 0 ? 0 : 1);
+        if (yphys) {
+          const int f = dj < 0 ? 2 : 3;
+          const bool wall = pl.fbc[4 * L.tree + f] == FC_BC_WALL;
+          o[0] = OP_BCY; o[1] = (int32_t)p; o[2] = i;
+          o[3] = dj < 0 ? (wall ? 1 - j : 1) : (wall ? 2 * m + 1 - j : m);
+          o[4] = pl.fbc[4 * L.tree + f];
+        } else if (xphys) {
+          const int f = di < 0 ? 0 : 1;
+          const bool wall = pl.fbc[4 * L.tree + f] == FC_BC_WALL;
+          o[0] = OP_BCX; o[1] = (int32_t)p; o[3] = j;
+          o[2] = di < 0 ? (wall ? 1 - i : 1) : (wall ? 2 * m + 1 - i : m);
+          o[4] = pl.fbc[4 * L.tree + f];
+        } else {
+          err = "physical corner outside a non-convex domain is not supported";
+          return FC_EUNSUP;
+        }
+        continue;
+      }
+      if (D.kind == D_CORNER3) {
+        o[0] = OP_CORNER3; o[1] = (int32_t)p;
+        o[2] = i; o[3] = (j < 1) ? 1 - j : 2 * m + 1 - j;
+        o[6] = (i < 1) ? 1 - i : 2 * m + 1 - i; o[7] = j;
+        continue;
+      }
+      int64_t cx, cy;
+      apply(D.T, X0 + (2 * i - 1) * h, Y0 + (2 * j - 1) * h, cx, cy);
+      if (D.kind == D_SAME || D.kind == D_COARSER) {
+        const Leaf& N = pl.leaves[D.leaf];
+        const int64_t xl = cx - N.x * m2, yl = cy - N.y * m2;
+        o[1] = (int32_t)D.leaf;
+        if (D.kind == D_SAME) {
+          o[0] = OP_COPY;
+          o[2] = (int32_t)((xl / h + 1) / 2);
+          o[3] = (int32_t)((yl / h + 1) / 2);
+        } else {
+          o[0] = OP_INTERP;
+          const int64_t I = xl / (4 * h), J = yl / (4 * h);
+          o[2] = (int32_t)(I + 1);
+          o[3] = (int32_t)(J + 1);
+          o[4] = (xl - I * 4 * h > 2 * h) ? 1 : -1;
+          o[5] = (yl - J * 4 * h > 2 * h) ? 1 : -1;
+        }
+        if (o[2] < 1 || o[2] > m || o[3] < 1 || o[3] > m) { err = "ghost source outside leaf"; return FC_EBALANCE; }
+      } else {  // FINER: the child leaf holding the 2x2 block centred on the ghost centre
+        const int64_t csz = sz / 2, cw = m2 * csz;
+        const int64_t kx = ((cx - 1) / cw) * csz, ky = ((cy - 1) / cw) * csz;
+        const int64_t id = find_leaf(pl, D.T.tree, L.level + 1, kx, ky);
+        if (id < 0) { err = "2:1 balance violated (finer-by-two neighbour)"; return FC_EBALANCE; }
+        const Leaf& N = pl.leaves[id];
+        o[0] = OP_AVG4; o[1] = (int32_t)id;
+        o[2] = (int32_t)((cx - N.x * m2) / h);
+        o[3] = (int32_t)((cy - N.y * m2) / h);
+        if (o[2] < 1 || o[2] > m - 1 || o[3] < 1 || o[3] > m - 1) { err = "fine block outside leaf"; return FC_EBALANCE; }
+      }
+    }
+  return FC_OK;
+}
+
+static int64_t owner_of(const Plan& pl, int64_t q) {
+  int64_t r = (q * pl.nranks) / pl.P;  // first guess, then fix up against the floor() ranges
+  while (r > 0 && (r * pl.P) / pl.nranks > q) --r;
+  while (r + 1 < pl.nranks && ((r + 1) * pl.P) / pl.nranks <= q) ++r;
+  return r;
+}
+
+static inline bool is_ring(int m, int i, int j) { return !(i >= 1 && i <= m && j >= 1 && j <= m); }
+
+int plan_build(const fc_forest_desc* d, Plan& pl, std::string& err) {
+  if (!d || !d->levels || !d->tree_ids || !d->tree_to_tree || !d->tree_to_face || !d->face_bc) {
+    err = "null descriptor field"; return FC_EINVAL;
+  }
+  if (d->num_patches <= 0 || d->num_trees <= 0) { err = "empty forest"; return FC_EINVAL; }
+  if (d->m < 4 || (d->m & 1)) { err = "m must be even and >= 4"; return FC_EINVAL; }
+  if (d->mbc != 2) { err = "mbc must be 2"; return FC_EINVAL; }
+  if (d->meqn < 1 || d->meqn > 4 || d->maux < 0 || d->maux > 3) { err = "meqn/maux out of range"; return FC_EINVAL; }
+  if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks) { err = "bad rank/nranks"; return FC_EINVAL; }
+  if (!(d->tree_dx0 > 0.0)) { err = "tree_dx0 must be positive"; return FC_EINVAL; }
+  pl.P = d->num_patches; pl.T = d->num_trees; pl.m = d->m; pl.n = d->m + 4;
+  pl.meqn = d->meqn; pl.maux = d->maux; pl.dx0 = d->tree_dx0 / d->m;
+  pl.rank = d->rank; pl.nranks = d->nranks;
+  pl.t2t.assign(d->tree_to_tree, d->tree_to_tree + 4 * pl.T);
+  pl.t2f.assign(d->tree_to_face, d->tree_to_face + 4 * pl.T);
+  pl.fbc.assign(d->face_bc, d->face_bc + 4 * pl.T);
+  for (int t = 0; t < pl.T; ++t)
+    for (int f = 0; f < 4; ++f) {
+      const int nt = pl.t2t[4 * t + f], code = pl.t2f[4 * t + f];
+      if (nt < 0 || nt >= pl.T || code < 0 || code > 7) { err = "connectivity out of range"; return FC_ECONN; }
+      const int nf = code & 3, rev = code >> 2;
+      if (pl.t2t[4 * nt + nf] != t || pl.t2f[4 * nt + nf] != f + 4 * rev || (nt == t && nf == f && rev)) {
+        err = "connectivity not symmetric"; return FC_ECONN;
+      }
+    }
+  // decode: a Morton cursor per tree, leaves aligned to their size
+  int lmax = 0;
+  for (int64_t p = 0; p < pl.P; ++p) {
+    if (d->levels[p] < 0 || d->levels[p] > 28) { err = "level out of range"; return FC_EINVAL; }
+    lmax = std::max(lmax, (int)d->levels[p]);
+    if (d->tree_ids[p] < 0 || d->tree_ids[p] >= pl.T || (p && d->tree_ids[p] < d->tree_ids[p - 1])) {
+      err = "tree ids must be non-decreasing and in range"; return FC_ETILING;
+    }
+  }
+  pl.lmax = lmax;
+  pl.leaves.resize(pl.P);
+  pl.index.reserve((size_t)pl.P * 2);
+  const uint64_t full = 1ull << (2 * lmax);
+  int64_t p = 0;
+  for (int t = 0; t < pl.T; ++t) {
+    uint64_t c = 0;
+    int64_t first = p;
+    while (p < pl.P && d->tree_ids[p] == t) {
+      const int l = d->levels[p];
+      const uint64_t span = 1ull << (2 * (lmax - l));
+      if ((c & (span - 1)) != 0 || c + span > full) { err = "leaves do not tile tree in z-order"; return FC_ETILING; }
+      Leaf& L = pl.leaves[p];
+      L.tree = t; L.level = l;
+      L.x = (int64_t)compact_even_bits(c);
+      L.y = (int64_t)compact_even_bits(c >> 1);
+      pl.index.emplace(std::make_tuple((int32_t)t, (int32_t)l, L.x, L.y), p);
+      c += span;
+      ++p;
+    }
+    if (c != full || p == first) { err = "tree not covered exactly"; return FC_ETILING; }
+  }
+  // local range and expanded table of local patches
+  pl.p0 = (pl.rank * pl.P) / pl.nranks;
+  pl.p1 = ((pl.rank + 1) * pl.P) / pl.nranks;
+  const int64_t Pl = pl.p1 - pl.p0, G = (int64_t)pl.n * pl.n - (int64_t)pl.m * pl.m;
+  pl.table.assign((size_t)Pl * G * REC, 0);
+  pl.uniform_same = true;
+  pl.lmin_local = 99; pl.lmax_local = 0;
+  for (int64_t q = pl.p0; q < pl.p1; ++q) {
+    int rc = patch_records(pl, q, pl.table.data() + (q - pl.p0) * G * REC, err);
+    if (rc) return rc;
+    pl.lmin_local = std::min(pl.lmin_local, pl.leaves[q].level);
+    pl.lmax_local = std::max(pl.lmax_local, pl.leaves[q].level);
+  }
+  for (int64_t k = 0; k < Pl * G; ++k) {
+    const int op = pl.table[k * REC];
+    if (op != OP_COPY && op != OP_BCX && op != OP_BCY) { pl.uniform_same = false; break; }
+  }
+  // halo plan: remote sources grouped by owner, round 1 (interior cells) / round 2 (ring cells)
+  pl.halo = HaloPlan();
+  pl.halo.need1.assign(pl.nranks, {});
+  pl.halo.need2.assign(pl.nranks, {});
+  if (pl.nranks > 1) {
+    const int m = pl.m, n = pl.n;
+    const int64_t n2 = (int64_t)n * n;
+    std::unordered_map<int64_t, std::vector<int32_t>> remote_cache;
+    auto need = [&](int64_t q, int i, int j) -> int {
+      if (q >= pl.p0 && q < pl.p1) return FC_OK;
+      const int64_t key = q * n2 + (int64_t)(j + 1) * n + (i + 1);
+      const int64_t own = owner_of(pl, q);
+      if (!is_ring(m, i, j)) { pl.halo.need1[own].push_back(key); return FC_OK; }
+      // a remote ring cell read by interpolation: must be final after the owner's phases A + C
+      auto it = remote_cache.find(q);
+      if (it == remote_cache.end()) {
+        std::vector<int32_t> rr((size_t)G * REC);
+        int rc = patch_records(pl, q, rr.data(), err);
+        if (rc) return rc;
+        it = remote_cache.emplace(q, std::move(rr)).first;
+      }
+      int r = 0;
+      for (int jj = -1; jj <= m + 2; ++jj)
+        for (int ii = -1; ii <= m + 2; ++ii) {
+          if (!is_ring(m, ii, jj)) continue;
+          if (ii == i && jj == j) {
+            const int32_t* o = it->second.data() + (size_t)r * REC;
+            bool ok = o[0] == OP_COPY || o[0] == OP_AVG4;
+            if (o[0] == OP_BCX || o[0] == OP_BCY) ok = !is_ring(m, o[2], o[3]);
+            if (!ok) { err = "multi-level interpolation chain across a shard cut"; return FC_EUNSUP; }
+          }
+          ++r;
+        }
+      pl.halo.need2[own].push_back(key);
+      return FC_OK;
+    };
+    for (int64_t k = 0; k < Pl * G; ++k) {
+      const int32_t* o = pl.table.data() + k * REC;
+      int rc = FC_OK;
+      switch (o[0]) {
+        case OP_COPY: rc = need(o[1], o[2], o[3]); break;
+        case OP_AVG4:
+          for (int b = 0; b < 2 && !rc; ++b)
+            for (int a = 0; a < 2 && !rc; ++a) rc = need(o[1], o[2] + a, o[3] + b);
+          break;
+        case OP_INTERP:
+          rc = need(o[1], o[2], o[3]);
+          if (!rc) rc = need(o[1], o[2] - 1, o[3]);
+          if (!rc) rc = need(o[1], o[2] + 1, o[3]);
+          if (!rc) rc = need(o[1], o[2], o[3] - 1);
+          if (!rc) rc = need(o[1], o[2], o[3] + 1);
+          break;
+        default: break;
+      }
+      if (rc) return rc;
+    }
+    int64_t slot = 0;
+    for (int round = 1; round <= 2; ++round)
+      for (int r = 0; r < pl.nranks; ++r) {
+        auto& v = round == 1 ? pl.halo.need1[r] : pl.halo.need2[r];
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        for (int64_t key : v) pl.halo.slot.emplace(key * 2 + (round - 1), slot++);
+        (round == 1 ? pl.halo.n1 : pl.halo.n2) += (int64_t)v.size();
+      }
+  }
+  return FC_OK;
+}
+
+int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err) {
+  const int m = pl.m, n = pl.n;
+  const int64_t n2 = (int64_t)n * n, S = (int64_t)meqn * n2;
+  const int64_t Pl = pl.p1 - pl.p0, G = n2 - (int64_t)m * m;
+  const int64_t nhalo = pl.halo.n1 + pl.halo.n2;
+  const int64_t total = (Pl + (nhalo + n2 - 1) / n2) * S;
+  if (total >= (1ll << 31)) { err = "state too large for 32-bit offsets"; return FC_EUNSUP; }
+  gl = GhostLists();
+  gl.interp.assign(pl.lmax + 1, {});
+  gl.bcx_l.assign(pl.lmax + 1, {});
+  gl.bcy_l.assign(pl.lmax + 1, {});
+  bool any_interp = false;
+  auto off = [&](int64_t q, int i, int j, int round) -> int32_t {
+    const int64_t cell = (int64_t)(j + 1) * n + (i + 1);
+    if (q >= pl.p0 && q < pl.p1) return (int32_t)((q - pl.p0) * S + cell);
+    const int64_t key = (q * n2 + cell) * 2 + (round - 1);
+    auto it = pl.halo.slot.find(key);
+    if (it == pl.halo.slot.end()) return -1;
+    const int64_t h = it->second;
+    return (int32_t)((Pl + h / n2) * S + h % n2);
+  };
+  for (int64_t lp = 0; lp < Pl; ++lp) {
+    const int lvl = pl.leaves[pl.p0 + lp].level;
+    int r = 0;
+    for (int j = -1; j <= m + 2; ++j)
+      for (int i = -1; i <= m + 2; ++i) {
+        if (!is_ring(m, i, j)) continue;
+        const int32_t* o = pl.table.data() + (lp * G + r++) * REC;
+        const int32_t dst = (int32_t)(lp * S + (int64_t)(j + 1) * n + (i + 1));
+        switch (o[0]) {
+          case OP_COPY: {
+            int32_t s = off(o[1], o[2], o[3], 1);
+            if (s < 0) { err = "missing halo slot"; return FC_EINVAL; }
+            gl.copy.insert(gl.copy.end(), {dst, s});
+            break;
+          }
+          case OP_AVG4: {
+            int32_t s[4] = {off(o[1], o[2], o[3], 1), off(o[1], o[2] + 1, o[3], 1),
+                            off(o[1], o[2], o[3] + 1, 1), off(o[1], o[2] + 1, o[3] + 1, 1)};
+            if (s[0] < 0 || s[1] < 0 || s[2] < 0 || s[3] < 0) { err = "missing halo slot"; return FC_EINVAL; }
+            gl.avg.insert(gl.avg.end(), {dst, s[0], s[1], s[2], s[3]});
+            break;
+          }
+          case OP_INTERP: {
+            auto rnd = [&](int ii, int jj) { return is_ring(m, ii, jj) ? 2 : 1; };
+            const int I = o[2], J = o[3];
+            int32_t s[5] = {off(o[1], I, J, rnd(I, J)), off(o[1], I - 1, J, rnd(I - 1, J)),
+                            off(o[1], I + 1, J, rnd(I + 1, J)), off(o[1], I, J - 1, rnd(I, J - 1)),
+                            off(o[1], I, J + 1, rnd(I, J + 1))};
+            for (int k = 0; k < 5; ++k)
+              if (s[k] < 0) { err = "missing halo slot"; return FC_EINVAL; }
+            gl.interp[lvl].insert(gl.interp[lvl].end(), {dst, s[0], s[1], s[2], s[3], s[4], o[4], o[5]});
+            any_interp = true;
+            break;
+          }
+          case OP_BCX:
+          case OP_BCY: {
+            const int32_t s = (int32_t)(lp * S + (int64_t)(o[3] + 1) * n + (o[2] + 1));
+            const int32_t neg = (o[4] == FC_BC_WALL && meqn >= 3) ? (o[0] == OP_BCX ? 1 : 2) : -1;
+            auto& v = o[0] == OP_BCX ? gl.bcx : gl.bcy;
+            v.insert(v.end(), {dst, s, neg});
+            auto& vl = o[0] == OP_BCX ? gl.bcx_l[lvl] : gl.bcy_l[lvl];
+            vl.insert(vl.end(), {dst, s, neg});
+            break;
+          }
+          case OP_CORNER3: {
+            const int32_t a = (int32_t)(lp * S + (int64_t)(o[3] + 1) * n + (o[2] + 1));
+            const int32_t b = (int32_t)(lp * S + (int64_t)(o[7] + 1) * n + (o[6] + 1));
+            gl.corner3.insert(gl.corner3.end(), {dst, a, b});
+            break;
+          }
+          default:
+            err = "unexpected ghost op";
+            return FC_EINVAL;
+        }
+      }
+  }
+  if (!any_interp) {  // no per-level B/C passes needed
+    for (auto& v : gl.bcx_l) v.clear();
+    for (auto& v : gl.bcy_l) v.clear();
+  }
+  return FC_OK;
+}
+
+}  // namespace fc

@@ -1,0 +1,254 @@
+"""Thin ctypes binding of libfc.so (include/fc.h).  Argument marshalling only: every step of the
+hot path runs in the library's CUDA kernels.  There is no fallback: if libfc.so is missing or a
+call fails, an exception is raised.
+
+Names follow the C ABI: fc_forest_create, fc_set_problem, fc_set_aux, fc_set_q, fc_ghost_fill,
+fc_step, fc_get_q, fc_get_q_padded, fc_get_ghost_table, ... ; `Forest` bundles them per handle.
+Host buffers are numpy arrays; device buffers are torch CUDA tensors (passed by data_ptr()).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfc.so")
+
+FC_OK, FC_EINVAL, FC_ETILING, FC_ECONN, FC_EBALANCE, FC_ECUDA, FC_ENCCL, FC_ENOMEM, FC_ESTATE, \
+    FC_ECFL, FC_ENONFINITE, FC_EUNSUP = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9, -10, -11
+FC_HOST, FC_DEVICE = 0, 1
+FC_ADV_CONST, FC_ADV_EDGEVEL_CAPA, FC_SWE_ROE, FC_EULER_ROE = 0, 1, 2, 3
+FC_LIM_NONE, FC_LIM_MINMOD, FC_LIM_MC = 0, 1, 2
+FC_TABLE_EXPANDED = 1
+
+ERRNAMES = {0: "FC_OK", -1: "FC_EINVAL", -2: "FC_ETILING", -3: "FC_ECONN", -4: "FC_EBALANCE",
+            -5: "FC_ECUDA", -6: "FC_ENCCL", -7: "FC_ENOMEM", -8: "FC_ESTATE", -9: "FC_ECFL",
+            -10: "FC_ENONFINITE", -11: "FC_EUNSUP"}
+
+# every symbol include/fc.h declares (checked by the CPU test suite)
+EXPORTS = ["fc_forest_create", "fc_forest_destroy", "fc_set_problem", "fc_set_aux", "fc_set_q",
+           "fc_ghost_fill", "fc_step", "fc_get_q", "fc_get_q_padded", "fc_get_ghost_table",
+           "fc_set_stream", "fc_set_timing", "fc_get_stats", "fc_reset_stats", "fc_local_range",
+           "fc_halo_counts", "fc_nccl_unique_id", "fc_last_error"]
+
+
+class FcError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str):
+        super().__init__(f"{where} -> {ERRNAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class ForestDesc(C.Structure):
+    _fields_ = [("num_patches", C.c_int64), ("levels", C.c_void_p), ("tree_ids", C.c_void_p),
+                ("num_trees", C.c_int32), ("tree_to_tree", C.c_void_p), ("tree_to_face", C.c_void_p),
+                ("face_bc", C.c_void_p), ("m", C.c_int32), ("mbc", C.c_int32), ("meqn", C.c_int32),
+                ("maux", C.c_int32), ("tree_dx0", C.c_double), ("device", C.c_int32),
+                ("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_id", C.c_void_p)]
+
+
+class Problem(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("p0", C.c_double), ("p1", C.c_double), ("limiter", C.c_int32),
+                ("method2", C.c_int32), ("method3", C.c_int32), ("cfl_reject", C.c_double)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("kernel_launches", C.c_int64), ("steps", C.c_int64), ("ms_ghost", C.c_double),
+                ("ms_step", C.c_double), ("ms_comm", C.c_double), ("step_kernel_launches", C.c_int64),
+                ("local_patches", C.c_int64), ("halo_cells", C.c_int64),
+                ("uniform_fast_path", C.c_int32), ("pad_", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
+
+
+_lib = None
+
+
+def lib():
+    """Load libfc.so (raises if it has not been built -- there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_1308_1472_b200.build` "
+                              "(the product path has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.fc_forest_create.argtypes = [C.POINTER(ForestDesc), C.POINTER(P)]
+        L.fc_forest_destroy.argtypes = [P]
+        L.fc_set_problem.argtypes = [P, C.POINTER(Problem)]
+        L.fc_set_aux.argtypes = [P, P, C.c_int]
+        L.fc_set_q.argtypes = [P, P, C.c_int]
+        L.fc_ghost_fill.argtypes = [P]
+        L.fc_step.argtypes = [P, C.c_double, C.POINTER(C.c_double)]
+        L.fc_get_q.argtypes = [P, P, C.c_int]
+        L.fc_get_q_padded.argtypes = [P, P, C.c_int]
+        L.fc_get_ghost_table.argtypes = [P, C.c_int, P, C.c_int64, C.POINTER(C.c_int64)]
+        L.fc_set_stream.argtypes = [P, P]
+        L.fc_set_timing.argtypes = [P, C.c_int]
+        L.fc_get_stats.argtypes = [P, C.POINTER(Stats)]
+        L.fc_reset_stats.argtypes = [P]
+        L.fc_local_range.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.fc_halo_counts.argtypes = [P, P]
+        L.fc_nccl_unique_id.argtypes = [P]
+        L.fc_last_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, where: str):
+    if rc != FC_OK:
+        raise FcError(rc, where, lib().fc_last_error().decode())
+
+
+def _ptr(a):
+    """numpy array -> (ptr, FC_HOST); torch tensor -> (data_ptr, FC_HOST/FC_DEVICE)."""
+    if isinstance(a, np.ndarray):
+        assert a.flags.c_contiguous and a.dtype == np.float64
+        return a.ctypes.data_as(C.c_void_p), FC_HOST
+    import torch
+    assert a.is_contiguous() and a.dtype == torch.float64
+    return C.c_void_p(a.data_ptr()), (FC_DEVICE if a.is_cuda else FC_HOST)
+
+
+def fc_nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(lib().fc_nccl_unique_id(buf), "fc_nccl_unique_id")
+    return bytes(buf)
+
+
+class Forest:
+    """One libfc handle (one per process / GPU)."""
+
+    def __init__(self, levels, tree_ids, conn, m: int, meqn: int, maux: int = 0,
+                 tree_dx0: float = 1.0, device: int = 0, rank: int = 0, nranks: int = 1,
+                 nccl_id: bytes | None = None):
+        self._keep = [np.ascontiguousarray(levels, np.int8), np.ascontiguousarray(tree_ids, np.int32),
+                      np.ascontiguousarray(conn.tree_to_tree, np.int32),
+                      np.ascontiguousarray(conn.tree_to_face, np.int8),
+                      np.ascontiguousarray(conn.face_bc, np.int8)]
+        lv, tr, t2t, t2f, fbc = self._keep
+        self._nid = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        d = ForestDesc(len(lv), lv.ctypes.data, tr.ctypes.data, len(t2t) // 4, t2t.ctypes.data,
+                       t2f.ctypes.data, fbc.ctypes.data, m, 2, meqn, maux, tree_dx0, device, rank,
+                       nranks, C.cast(self._nid, C.c_void_p) if self._nid else None)
+        h = C.c_void_p()
+        _check(lib().fc_forest_create(C.byref(d), C.byref(h)), "fc_forest_create")
+        self.h = h
+        self.m, self.meqn, self.maux, self.n = m, meqn, maux, m + 4
+        first, count = C.c_int64(), C.c_int64()
+        _check(lib().fc_local_range(h, C.byref(first), C.byref(count)), "fc_local_range")
+        self.first, self.count = first.value, count.value
+        self.nranks = nranks
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fc_forest_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- calls -----------------------------------------------------------------------------------
+    def set_problem(self, kind, p0=0.0, p1=0.0, limiter=FC_LIM_MC, method2=2, method3=2,
+                    cfl_reject=1.0):
+        pr = Problem(kind, p0, p1, limiter, method2, method3, cfl_reject)
+        _check(lib().fc_set_problem(self.h, C.byref(pr)), "fc_set_problem")
+
+    def set_aux(self, aux):
+        p, where = _ptr(aux)
+        _check(lib().fc_set_aux(self.h, p, where), "fc_set_aux")
+
+    def set_q(self, q):
+        p, where = _ptr(q)
+        _check(lib().fc_set_q(self.h, p, where), "fc_set_q")
+
+    def ghost_fill(self):
+        _check(lib().fc_ghost_fill(self.h), "fc_ghost_fill")
+
+    def step(self, dt: float, raise_on_reject: bool = True):
+        """Returns (rc, cfl).  rc is FC_OK, or FC_ECFL / FC_ENONFINITE when not committed."""
+        cfl = C.c_double(0.0)
+        rc = lib().fc_step(self.h, dt, C.byref(cfl))
+        if rc not in (FC_OK, FC_ECFL) or (raise_on_reject and rc != FC_OK):
+            _check(rc, "fc_step")
+        return rc, cfl.value
+
+    def get_q(self, out=None):
+        if out is None:
+            out = np.empty((self.count, self.meqn, self.m, self.m))
+        p, where = _ptr(out)
+        _check(lib().fc_get_q(self.h, p, where), "fc_get_q")
+        return out
+
+    def get_q_padded(self, out=None):
+        if out is None:
+            out = np.empty((self.count, self.meqn, self.n, self.n))
+        p, where = _ptr(out)
+        _check(lib().fc_get_q_padded(self.h, p, where), "fc_get_q_padded")
+        return out
+
+    def ghost_table(self) -> np.ndarray:
+        n = C.c_int64()
+        lib().fc_get_ghost_table(self.h, FC_TABLE_EXPANDED, None, 0, C.byref(n))
+        buf = np.empty(n.value, np.int32)
+        _check(lib().fc_get_ghost_table(self.h, FC_TABLE_EXPANDED, buf.ctypes.data_as(C.c_void_p),
+                                        n.value, C.byref(n)), "fc_get_ghost_table")
+        G = self.n * self.n - self.m * self.m
+        return buf.reshape(self.count, G, 8)
+
+    def set_stream(self, stream_ptr: int | None):
+        _check(lib().fc_set_stream(self.h, C.c_void_p(stream_ptr) if stream_ptr else None), "fc_set_stream")
+
+    def set_timing(self, on: bool):
+        _check(lib().fc_set_timing(self.h, 1 if on else 0), "fc_set_timing")
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(lib().fc_get_stats(self.h, C.byref(s)), "fc_get_stats")
+        return s.as_dict()
+
+    def reset_stats(self):
+        _check(lib().fc_reset_stats(self.h), "fc_reset_stats")
+
+    def halo_counts(self) -> np.ndarray:
+        out = np.zeros(self.nranks, np.int64)
+        _check(lib().fc_halo_counts(self.h, out.ctypes.data_as(C.c_void_p)), "fc_halo_counts")
+        return out
+
+
+def forest_for(w, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id=None) -> Forest:
+    """Handle for a workloads.Workload, with its problem (and aux, for local patches) set."""
+    f = Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0,
+               device, rank, nranks, nccl_id)
+    if device >= 0:
+        f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject)
+        if w.aux is not None:
+            f.set_aux(np.ascontiguousarray(w.aux[f.first:f.first + f.count]))
+    return f
+
+
+def run(w, steps: int | None = None, dt_list=None, device: int = 0, f: Forest | None = None):
+    """Run the workload's dt policy on the GPU (same policy as the oracle's driver).
+    Returns (q [P][meqn][m][m], cfls, dts)."""
+    f = f or forest_for(w, device)
+    f.set_q(np.ascontiguousarray(w.q0[f.first:f.first + f.count]))
+    steps = w.steps if steps is None else steps
+    dt = w.dt0
+    cfls, dts = [], []
+    for n in range(steps):
+        if dt_list is not None:
+            dt = dt_list[n]
+        rc, cfl = f.step(dt, raise_on_reject=dt_list is not None)
+        if rc == FC_ECFL:
+            dt = dt * w.cfl_target / cfl
+            rc, cfl = f.step(dt)
+        cfls.append(cfl)
+        dts.append(dt)
+        if dt_list is None:
+            dt = w.next_dt(dt, cfl)
+    return f.get_q(), np.array(cfls), np.array(dts)

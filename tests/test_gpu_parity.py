@@ -1,0 +1,179 @@
+"""GPU parity: the CUDA path (libfc.so through its C ABI) against the oracle on the same seeded
+inputs.  Bars (BASELINE.json north_star):
+  * ghost rings and index tables: bit-exact;
+  * state after the configured number of steps: max|dq_k| <= 1e-12 max|q_k| per component;
+  * total mass: relative difference <= 1e-13; returned CFLs: relative <= 1e-12;
+  * special cases (constant state, exact CFL-1 shifts): bitwise.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1308_1472_b200 import fc
+from workloads import forests as F
+from workloads.configs import ADV_CONST, Workload, c1, c2, c3, c5
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_forest(w):
+    return fc.forest_for(w, device=0)
+
+
+def assert_parity(w, qg, qo, cg, co, mass_rtol=1e-13):
+    for k in range(w.meqn):
+        scale = np.abs(qo[:, k]).max()
+        if scale == 0.0:
+            scale = np.abs(qo).max()
+        err = np.abs(qg[:, k] - qo[:, k]).max()
+        assert err <= 1e-12 * scale, (w.name, k, err, scale)
+        area = np.ldexp(1.0, -2 * w.forest.levels.astype(np.int64))[:, None, None]
+        mg, mo = (qg[:, k] * area).sum(), (qo[:, k] * area).sum()
+        assert abs(mg - mo) <= mass_rtol * max(abs(mo), (np.abs(qo[:, k]) * area).sum()), (w.name, k)
+    np.testing.assert_allclose(cg, co, rtol=1e-12, atol=0)
+
+
+# ---- ghost fill ---------------------------------------------------------------------------------
+def _ring_cases():
+    rng = np.random.default_rng(1308147 + 11)
+    out = [c1(), c2(), c3(level=2, m=8), c3(level=1, m=32), c5(level=2, m=16)]
+    for name, conn in (("walls", F.walled_unit_square(F.WALL)), ("brick", F.brick(3, 2, bc=F.OUTFLOW)),
+                       ("reversed", F.brick(2, 1, bc=F.OUTFLOW, reversed_x_links=(0,))),
+                       ("periodic", F.periodic_unit_square())):
+        fr = F.forest_refined(conn, 2, lambda t, x, y, h: rng.random(len(x)) < 0.4)
+        meqn = 3 if name == "walls" else 1
+        kind = 2 if meqn == 3 else ADV_CONST
+        q0 = np.zeros((fr.num_patches, meqn, 8, 8))
+        out.append(Workload(f"rand_{name}", fr, 8, meqn, 0, kind, (1.0, 0.5), q0, None, 1, 1e-3, "fixed"))
+    return out
+
+
+@pytest.mark.parametrize("w", _ring_cases(), ids=lambda w: w.name)
+def test_ghost_rings_bitwise(w, rng):
+    q = rng.standard_normal(w.q0.shape)
+    if w.meqn >= 3:
+        q[:, 0] = np.abs(q[:, 0]) + 1.0
+    f = gpu_forest(w)
+    f.set_q(np.ascontiguousarray(q))
+    f.ghost_fill()
+    g = f.get_q_padded()
+    of = oracle.forest_for(w)
+    o = of.ghost_fill(of.pad(q))
+    np.testing.assert_array_equal(g, o)
+    np.testing.assert_array_equal(f.ghost_table(), of.ghost_table())
+
+
+# ---- full runs vs the oracle ----------------------------------------------------------------------
+RUNS = [c1(), c2(), c3(level=3, m=32), c5(level=3, m=16), c5(level=2, m=8),
+        c1(level=2, m=24, steps=30), c1(level=1, m=20, steps=30), c1(level=1, m=6, steps=30)]
+
+
+@pytest.mark.parametrize("w", RUNS, ids=lambda w: w.name)
+def test_parity_against_oracle(w):
+    qo, co, do = oracle.run(w)
+    qg, cg, dg = fc.run(w, dt_list=do)
+    assert_parity(w, qg, qo, cg, co)
+
+
+def test_parity_c2_levels_and_dt_policy_on_gpu():
+    """C2 with the GPU driving its own dt policy (fixed dt) equals the oracle's run."""
+    w = c2()
+    qo, co, do = oracle.run(w)
+    qg, cg, dg = fc.run(w)
+    np.testing.assert_array_equal(dg, do)
+    assert_parity(w, qg, qo, cg, co)
+
+
+# ---- exact cases -------------------------------------------------------------------------------
+@pytest.mark.parametrize("uv", [(1, 0), (0, -1), (1, 1), (-1, 1)])
+@pytest.mark.parametrize("method2", [1, 2])
+def test_exact_cfl1_shift_bitwise(rng, uv, method2):
+    fr = F.forest_uniform(F.brick(2, 1, periodic_x=True, periodic_y=True), 2)
+    m = 8
+    G = rng.integers(0, 256, size=(1, 32, 64)).astype(np.float64)
+    q0 = np.zeros((fr.num_patches, 1, m, m))
+    for p in range(fr.num_patches):
+        t, x0, y0 = int(fr.tree_ids[p]), int(fr.ix[p]) * m, int(fr.iy[p]) * m
+        q0[p, 0] = G[0, y0:y0 + m, t * 32 + x0:t * 32 + x0 + m]
+    w = Workload("shift", fr, m, 1, 0, ADV_CONST, (float(uv[0]), float(uv[1])), q0, None, 3,
+                 1.0 / 32, "fixed", method2=method2)
+    qg, cg, _ = fc.run(w)
+    expect = np.roll(G, shift=(3 * uv[1], 3 * uv[0]), axis=(1, 2))
+    for p in range(fr.num_patches):
+        t, x0, y0 = int(fr.tree_ids[p]), int(fr.ix[p]) * m, int(fr.iy[p]) * m
+        np.testing.assert_array_equal(qg[p, 0], expect[0, y0:y0 + m, t * 32 + x0:t * 32 + x0 + m])
+    assert (cg == 1.0).all()
+
+
+def test_constant_state_bitwise():
+    w = c5(level=2, m=16)
+    rho, u, v, p = 1.2, 0.7, -0.3, 2.0
+    w.q0[:, 0], w.q0[:, 1], w.q0[:, 2] = rho, rho * u, rho * v
+    w.q0[:, 3] = p / 0.4 + 0.5 * rho * (u * u + v * v)
+    qg, _, _ = fc.run(w, steps=3)
+    np.testing.assert_array_equal(qg, w.q0)
+
+
+# ---- step acceptance / errors ----------------------------------------------------------------------
+def test_cfl_reject_keeps_state_and_errors():
+    w = c1()
+    f = gpu_forest(w)
+    f.set_q(np.ascontiguousarray(w.q0))
+    rc, cfl = f.step(10 * w.dt0, raise_on_reject=False)
+    assert rc == fc.FC_ECFL and cfl == pytest.approx(9.0, rel=1e-12)
+    np.testing.assert_array_equal(f.get_q(), w.q0)
+    with pytest.raises(fc.FcError) as ei:
+        f.step(-1.0)
+    assert ei.value.code == fc.FC_EINVAL
+    bad = w.q0.copy()
+    bad[3, 0, 2, 2] = np.nan
+    f.set_q(np.ascontiguousarray(bad))
+    with pytest.raises(fc.FcError) as ei:
+        f.step(w.dt0)
+    assert ei.value.code == fc.FC_ENONFINITE
+
+
+def test_device_pointers_roundtrip():
+    import torch
+    w = c3(level=2, m=8)
+    f = gpu_forest(w)
+    qd = torch.from_numpy(np.ascontiguousarray(w.q0)).cuda()
+    f.set_q(qd)
+    out = torch.empty_like(qd)
+    f.get_q(out)
+    assert torch.equal(out.cpu(), torch.from_numpy(w.q0))
+
+
+# ---- full-size launch configuration, sampled -------------------------------------------------------
+def _sample_ids(w, rng, extra):
+    P = w.num_patches
+    ids = set(rng.choice(P, size=min(P, 96), replace=False).tolist())
+    ids.update(extra)
+    return np.array(sorted(i for i in ids if 0 <= i < P), np.int64)
+
+
+@pytest.mark.parametrize("name", ["C5", "C3"])
+def test_full_size_first_step_sampled(name, rng):
+    """BASELINE.json's full sizes in the launch configuration bench.py times: one step from the IC
+    on the GPU, checked on sampled patches (random + shock/bubble/wall-adjacent ones) against
+    the oracle's per-patch step built from the same IC."""
+    w = c5() if name == "C5" else c3()
+    f = gpu_forest(w)
+    f.set_q(np.ascontiguousarray(w.q0))
+    rc, cfl = f.step(w.dt0)
+    qg = f.get_q()
+    x0, y0, h = w.forest.origin()
+    X = x0 + w.forest.tree_ids
+    if name == "C5":
+        extra = np.nonzero((np.abs(X + h / 2 - 1.29) < 0.01) | (np.abs(X + h / 2 - 1.3) < 0.02) |
+                           (y0 == 0) | (x0 + h >= 1.0 - 1e-12))[0][:64]
+    else:
+        extra = np.nonzero((x0 == 0) | (y0 == 0) | (np.abs(np.hypot(x0 + h / 2 - 0.5, y0 + h / 2 - 0.5) - 0.2) < 0.03))[0][:64]
+    ids = _sample_ids(w, rng, extra.tolist())
+    of = oracle.forest_for(w)
+    qo, co = of.step_sample(oracle.problem_for(w), w.q0, w.dt0, 1.0 / w.m, ids)
+    for k in range(w.meqn):
+        scale = max(np.abs(qo[:, k]).max(), 1e-300)
+        err = np.abs(qg[ids, k] - qo[:, k]).max()
+        assert err <= 1e-12 * max(scale, np.abs(qo).max() if scale == 1e-300 else scale), (k, err)
+    assert cfl >= co.max() * (1 - 1e-12) and cfl <= 1.0

@@ -1,0 +1,127 @@
+"""CPU tests of libfc.so without a GPU: it loads, exports every symbol include/fc.h declares, and
+its host planner (per-direction neighbour lookup + composed tree transforms) produces ghost
+tables bit-identical to the oracle's brute-force point-location tables; invalid forests are
+rejected with the same error classes; the sharded halo plan is consistent across ranks."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1308_1472_b200 import fc
+from workloads import forests as F
+from workloads.configs import c1, c2, c3, c5
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "fc.h")).read()
+    declared = sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(fc_\w+)\s*\(", hdr, re.M)))
+    assert declared == sorted(fc.EXPORTS)
+    L = fc.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def host_table(levels, tree_ids, conn, m, meqn=1, rank=0, nranks=1):
+    f = fc.Forest(levels, tree_ids, conn, m, meqn, device=-1, rank=rank, nranks=nranks)
+    return f, f.ghost_table()
+
+
+def oracle_table(levels, tree_ids, conn, m):
+    return oracle.OracleForest(levels, tree_ids, conn, m).ghost_table()
+
+
+@pytest.mark.parametrize("w", [c1(), c1(level=3, m=4), c2(), c3(level=2, m=8), c3(level=1, m=32),
+                               c5(level=2, m=8), c5(level=1, m=16)], ids=lambda w: w.name)
+def test_table_bit_exact_configs(w):
+    _, t = host_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m)
+    o = oracle_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m)
+    np.testing.assert_array_equal(t, o)
+
+
+def _random_forest(rng, conn, base, m):
+    def refine(t, x, y, h):
+        return rng.random(len(x)) < 0.35
+    return F.forest_refined(conn, base, refine)
+
+
+CONNS = {
+    "periodic": F.periodic_unit_square(),
+    "walls": F.walled_unit_square(F.WALL),
+    "outflow": F.walled_unit_square(F.OUTFLOW),
+    "brick3x2": F.brick(3, 2, bc=F.WALL),
+    "brick2x2_periodic": F.brick(2, 2, periodic_x=True, periodic_y=True),
+    "reversed": F.brick(2, 1, bc=F.OUTFLOW, reversed_x_links=(0,)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CONNS))
+def test_table_bit_exact_random_two_level_forests(rng, name):
+    conn = CONNS[name]
+    for trial in range(4):
+        m = [4, 8, 6, 16][trial]
+        fr = _random_forest(rng, conn, 2, m)
+        _, t = host_table(fr.levels, fr.tree_ids, conn, m)
+        o = oracle_table(fr.levels, fr.tree_ids, conn, m)
+        np.testing.assert_array_equal(t, o)
+
+
+def test_rejects_invalid_forests_like_the_oracle():
+    conn = F.periodic_unit_square()
+    cases = [([2, 1, 1, 1, 2, 2, 2], [0] * 7, conn, fc.FC_ETILING),      # misaligned leaf
+             ([1] * 3, [0] * 3, conn, fc.FC_ETILING),                     # incomplete tree
+             ([0, 0], [1, 0], F.brick(2, 1), fc.FC_ETILING)]              # decreasing tree ids
+    bad = F.brick(2, 1)
+    bad.tree_to_face[1] = 3
+    cases.append(([0, 0], [0, 1], bad, fc.FC_ECONN))
+    # a level-0 neighbour of a level-2 leaf: one tree refined twice at a corner, the other not
+    fr = F.forest_refined(F.brick(2, 1), 0, lambda t, x, y, h: np.array([t == 0]))
+    lv = list(fr.levels)
+    tr = list(fr.tree_ids)
+    lv = [1, 2, 2, 2, 2] + lv[2:]      # tree 0's SE child (touching tree 1, level 0) at level 2
+    tr = [0, 0, 0, 0, 0] + tr[2:]
+    cases.append((lv, tr, F.brick(2, 1), fc.FC_EBALANCE))
+    for levels, trees, cn, code in cases:
+        with pytest.raises(fc.FcError) as ei:
+            fc.Forest(np.array(levels), np.array(trees), cn, 8, 1, device=-1)
+        assert ei.value.code == code, (levels, code, ei.value)
+        with pytest.raises(ValueError):
+            oracle.OracleForest(np.array(levels, np.int8), np.array(trees, np.int32), cn, 8).ghost_table()
+
+
+def test_bad_descriptor_fields():
+    w = c1()
+    for kw in ({"m": 7}, {"m": 2}):
+        with pytest.raises(fc.FcError) as ei:
+            fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, kw["m"], 1, device=-1)
+        assert ei.value.code == fc.FC_EINVAL
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4, 8])
+def test_sharded_tables_and_halo_plan(nranks):
+    """Every rank's table is the oracle's table restricted to its Morton range, and the remote
+    cells a rank needs are exactly the sources in its table owned by other ranks."""
+    for w in (c1(), c2(), c5(level=2, m=8)):
+        o = oracle_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m)
+        P = w.num_patches
+        for r in range(nranks):
+            f, t = host_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, rank=r, nranks=nranks)
+            p0, p1 = (r * P) // nranks, ((r + 1) * P) // nranks
+            assert (f.first, f.count) == (p0, p1 - p0)
+            np.testing.assert_array_equal(t, o[p0:p1])
+            srcs = set()
+            for rec in t.reshape(-1, 8):
+                op, q = rec[0], rec[1]
+                if op in (1, 2, 3) and not (p0 <= q < p1):
+                    srcs.add(q)
+            counts = f.halo_counts()
+            assert counts[r] == 0
+            owners = {s * nranks // P for s in srcs}
+            for s in range(nranks):
+                lo, hi = (s * P) // nranks, ((s + 1) * P) // nranks
+                has = any(lo <= q < hi for q in srcs)
+                assert (counts[s] > 0) == has, (w.name, r, s)
+            del owners

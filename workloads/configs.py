@@ -35,7 +35,7 @@ class Workload:
     maux: int
     kind: int
     params: tuple            # (p0, p1): (u, v) | (unused) | (g, 0) | (gamma, efix)
-    q0: np.ndarray           # [P, meqn, m, m]
+    q0: np.ndarray | None    # [P, meqn, m, m] (None until materialised for lazy workloads)
     aux: np.ndarray | None   # [P, maux, m+4, m+4] or None
     steps: int
     dt0: float
@@ -47,6 +47,18 @@ class Workload:
     cfl_reject: float = 1.0
     mbc: int = 2
     info: dict = field(default_factory=dict)
+    ic: object = None        # ic(forest, m, p0, p1) -> q0[p1-p0] (analytic, deterministic)
+
+    def q0_range(self, p0: int, p1: int) -> np.ndarray:
+        """Initial state of patches [p0, p1) only (multi-rank runs build just their shard)."""
+        if self.q0 is not None:
+            return np.ascontiguousarray(self.q0[p0:p1])
+        return self.ic(self.forest, self.m, p0, p1)
+
+    def materialise(self):
+        if self.q0 is None:
+            self.q0 = self.ic(self.forest, self.m, 0, self.num_patches)
+        return self
 
     @property
     def num_patches(self) -> int:
@@ -89,17 +101,21 @@ def c2(base_level: int = 3, m: int = 16, steps: int = 100, radius: float = 0.25)
                     ADV_CONST, (1.0, 0.5), _gaussian_ic(f, m), None, steps, dt, "fixed")
 
 
-def c3(level: int = 6, m: int = 32, steps: int = 200) -> Workload:
+def c3_ic(f: Forest, m: int, p0: int, p1: int) -> np.ndarray:
+    X, Y = cell_centres(_subforest(f, p0, p1), m)
+    q = np.zeros((p1 - p0, 3, m, m))
+    q[:, 0] = np.where((X - 0.5) ** 2 + (Y - 0.5) ** 2 < 0.2 ** 2, 2.0, 1.0)
+    return q
+
+
+def c3(level: int = 6, m: int = 32, steps: int = 200, lazy: bool = False) -> Workload:
     """C3: shallow water (g=1) radial dam break with reflecting walls, uniform level 6, m=32."""
     f = forest_uniform(walled_unit_square(WALL), level)
-    X, Y = cell_centres(f, m)
-    h = np.where((X - 0.5) ** 2 + (Y - 0.5) ** 2 < 0.2 ** 2, 2.0, 1.0)
-    q = np.zeros((f.num_patches, 3, m, m))
-    q[:, 0] = h
+    q = None if lazy else c3_ic(f, m, 0, f.num_patches)
     dx = 0.5 ** level / m
     dt0 = 0.9 * dx / math.sqrt(1.0 * 2.0)   # max(|u|+c) = sqrt(g*h) at h = 2
     return Workload("C3" if (level, m) == (6, 32) else f"C3_L{level}_m{m}", f, m, 3, 0, SWE_ROE,
-                    (1.0, 0.0), q, None, steps, dt0, "cfl")
+                    (1.0, 0.0), q, None, steps, dt0, "cfl", ic=c3_ic)
 
 
 GAMMA = 1.4
@@ -120,22 +136,37 @@ def euler_shock_bubble_state(X, Y, x_shock: float = 1.29):
     return rho, rho * u, np.zeros_like(rho), E
 
 
-def c5(level: int = 8, m: int = 16, steps: int = 100, x_shock: float = 1.29) -> Workload:
+def _subforest(f: Forest, p0: int, p1: int) -> Forest:
+    return Forest(f.levels[p0:p1], f.tree_ids[p0:p1], f.ix[p0:p1], f.iy[p0:p1], f.conn)
+
+
+def c5_ic(f: Forest, m: int, p0: int, p1: int, x_shock: float = 1.29) -> np.ndarray:
+    out = np.empty((p1 - p0, 4, m, m))
+    step = 16384
+    for a in range(p0, p1, step):            # chunked: the full C5 IC is 2.15 GB
+        b = min(p1, a + step)
+        sf = _subforest(f, a, b)
+        X, Y = cell_centres(sf, m)
+        X = X + sf.tree_ids[:, None, None].astype(np.float64)   # tree t covers [t, t+1] x [0, 1]
+        for k, v in enumerate(euler_shock_bubble_state(X, Y, x_shock)):
+            out[a - p0:b - p0, k] = v
+    return out
+
+
+def c5(level: int = 8, m: int = 16, steps: int = 100, x_shock: float = 1.29,
+       lazy: bool = False) -> Workload:
     """C5: 2D Euler (gamma=1.4, Roe + Harten-Hyman), 4-tree brick [0,4]x[0,1], outflow,
     uniform level 8 in each tree (262,144 patches of m=16, 67.1M cells)."""
     conn = brick(4, 1, bc=OUTFLOW)
     f = forest_uniform(conn, level)
-    X, Y = cell_centres(f, m)
-    X = X + f.tree_ids[:, None, None].astype(np.float64)   # tree t covers [t, t+1] x [0, 1]
-    q = np.empty((f.num_patches, 4, m, m))
-    for k, a in enumerate(euler_shock_bubble_state(X, Y, x_shock)):
-        q[:, k] = a
+    ic = lambda ff, mm, p0, p1: c5_ic(ff, mm, p0, p1, x_shock)
+    q = None if lazy else ic(f, m, 0, f.num_patches)
     dx = 0.5 ** level / m
     rho_post, p_post = 27.0 / 7.0, 31.0 / 3.0
     smax = 20.0 / 9.0 * math.sqrt(GAMMA) + math.sqrt(GAMMA * p_post / rho_post)
     dt0 = 0.9 * dx / smax
     return Workload("C5" if (level, m) == (8, 16) else f"C5_L{level}_m{m}", f, m, 4, 0, EULER_ROE,
-                    (GAMMA, 1.0), q, None, steps, dt0, "cfl")
+                    (GAMMA, 1.0), q, None, steps, dt0, "cfl", ic=ic)
 
 
 def c4(base_level: int = 4, m: int = 16, steps: int = 500, band: float = 0.6) -> Workload:
