@@ -137,7 +137,7 @@ int fc_ghost_fill(fc_forest* f);
  * (*max_cfl, max over edges and waves of dt |s| / (kappa dx) taken on the upwind side,
  * PAPER.md:276-277).  Commits (swaps q_old / q_new) iff max_cfl <= cfl_reject; otherwise returns
  * FC_ECFL with q unchanged.  FC_EINVAL if dt <= 0 or not finite; FC_ENONFINITE if the CFL is
- * NaN/Inf (state unchanged).  Synchronises the handle's stream (the CFL is returned to the host). */
+ * NaN/Inf or the updated state is not finite (state unchanged).  Synchronises the handle's stream (the CFL is returned to the host). */
 int fc_step(fc_forest* f, double dt, double* max_cfl);
 
 /* Interior q_old -> q[P_local][meqn][m][m].  Synchronous. */

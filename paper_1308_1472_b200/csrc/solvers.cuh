@@ -4,13 +4,18 @@
 // waves propagating at speeds determined from the solution to the Riemann problem.  For scalar
 // advection, the speed of each wave is simply the local advection speed at the cell interface.
 // For non-linear problems and systems, an approximate Riemann solver, such as a Roe solver ...".
-// Each solver stores a compact per-edge state in shared memory during the normal solve (phase 1)
-// and reconstructs waves / fluctuations / transverse splittings from it in phase 2:
-//   AdvConst      scratch {dq}                         speed from the problem (u or v)
-//   AdvEdgeCapa   scratch {dq}                         speed = edge velocity in aux (capacity form)
-//   SweRoe        scratch {a1..a3, u, v, c}            Roe state shared by normal + transverse solves
-//   EulerRoe      scratch {a1..a4, u, v, H, c, A-dq}   A-dq carries the Harten-Hyman entropy fix
-// Directions: D = 1 (x-sweep, normal momentum = component 1) or D = 2 (y-sweep, component 2).
+//
+// Interface used by k_step (step.cu):
+//   NC          per-cell derived fields precomputed once per staged cell (shared by the 4 edges
+//               of the cell in both sweeps): Euler {sqrt(rho), u, v, H, c}; SWE {sqrt(h), u, v}
+//   NS          per-edge scratch written by the normal solve (phase 1) and read in phase 2:
+//               AdvConst / AdvEdgeCapa {dq}; SweRoe {a1..a3, u, v, c, 1/c};
+//               EulerRoe {a1..a4, u, v, H, c, 1/c, A-dq (Harten-Hyman fixed)} (A+dq = sum s W - A-dq)
+//   riemann<D>  normal solve on one edge (D = 1: x, normal momentum = component 1; D = 2: y)
+//   wave<D>     wave p of an edge from its scratch;  speed<D>, fluct<D>, transverse<D>
+// Divisions and square roots use the SFU approximations refined by Newton steps to ~1 ulp
+// (fast_rcp / fast_rsqrt): results agree with the oracle's IEEE-rounded operations to rounding
+// level (tolerance 1e-12 max|q|), not bitwise.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -22,7 +27,7 @@ struct SolverParams {
 
 // cell aux view: kappa, u~ (left edge), v~ (bottom edge) of one cell (smem window, stride WW)
 struct AuxCell {
-  const double* a;  // pointer to kappa of the cell; u~ at a[WW], v~ at a[2 WW]
+  const double* a;
   int WW;
   __device__ double kappa() const { return a[0]; }
   __device__ double ut() const { return a[WW]; }
@@ -32,15 +37,36 @@ struct AuxCell {
 __device__ __forceinline__ double dmin0(double s) { return s < 0.0 ? s : 0.0; }
 __device__ __forceinline__ double dmax0(double s) { return s > 0.0 ? s : 0.0; }
 
+// 1/x: SFU seed (MUFU.RCP64H, ~2^-22) + two Newton steps -> ~1 ulp (x normal, nonzero)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// 1/sqrt(x): SFU seed + two Newton steps -> ~1 ulp (x > 0 normal)
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = 0.5 * x;
+  double r = fma(-h * y, y, 0.5);
+  y = fma(y, r, y);
+  r = fma(-h * y, y, 0.5);
+  return fma(y, r, y);
+}
+
 // ----------------------------------------------------------------------------------------------
 struct AdvConst {
-  static constexpr int MEQN = 1, MW = 1, NS = 1;
+  static constexpr int MEQN = 1, MW = 1, NS = 1, NC = 0;
   static constexpr bool CAPA = false;
+  __device__ static void precompute(const double*, int, const SolverParams&, double*, int) {}
   template <int D>
-  __device__ static void riemann(const double* ql, const double* qr, AuxCell, AuxCell,
-                                 const SolverParams&, double* sc, int st) {
+  __device__ static void riemann(const double* ql, const double* qr, const double*, const double*,
+                                 int, AuxCell, AuxCell, const SolverParams&, double* sc, int) {
     sc[0] = qr[0] - ql[0];
-    (void)st;
   }
   template <int D>
   __device__ static double speed(const double*, int, int, const SolverParams& P, AuxCell) {
@@ -57,7 +83,6 @@ struct AdvConst {
     am[0] = dmin0(s) * sc[0];
     ap[0] = dmax0(s) * sc[0];
   }
-  // transverse split of X for the part entering `recv` (next = the cell after it transversally)
   template <int D>
   __device__ static void transverse(const double*, int, const SolverParams& P, const double* X,
                                     AuxCell, AuxCell, double* bm, double* bp) {
@@ -69,11 +94,12 @@ struct AdvConst {
 
 // ----------------------------------------------------------------------------------------------
 struct AdvEdgeCapa {
-  static constexpr int MEQN = 1, MW = 1, NS = 1;
+  static constexpr int MEQN = 1, MW = 1, NS = 1, NC = 0;
   static constexpr bool CAPA = true;
+  __device__ static void precompute(const double*, int, const SolverParams&, double*, int) {}
   template <int D>
-  __device__ static void riemann(const double* ql, const double* qr, AuxCell, AuxCell,
-                                 const SolverParams&, double* sc, int) {
+  __device__ static void riemann(const double* ql, const double* qr, const double*, const double*,
+                                 int, AuxCell, AuxCell, const SolverParams&, double* sc, int) {
     sc[0] = qr[0] - ql[0];
   }
   // the edge velocity is stored with the cell to the right of / above the edge
@@ -108,27 +134,39 @@ struct AdvEdgeCapa {
 // a1 = ((u+c) dh - dn)/(2c), a2 = dt - vt dh, a3 = ((c-u) dh + dn)/(2c); r1 = (1, u-c, v),
 // r2 = (0, 0, 1)_t, r3 = (1, u+c, v); speeds u-c, u, u+c (normal/tangential per direction).
 struct SweRoe {
-  static constexpr int MEQN = 3, MW = 3, NS = 6;
+  static constexpr int MEQN = 3, MW = 3, NS = 7, NC = 3;
   static constexpr bool CAPA = false;
+  // cell fields: sqrt(h), u, v
+  __device__ static void precompute(const double* q, int qs, const SolverParams&, double* c, int cs) {
+    const double h = q[0];
+    const double rs = fast_rsqrt(h);
+    const double ih = rs * rs;
+    c[0] = h * rs;
+    c[cs] = q[qs] * ih;
+    c[2 * cs] = q[2 * qs] * ih;
+  }
   template <int D>
-  __device__ static void riemann(const double* ql, const double* qr, AuxCell, AuxCell,
-                                 const SolverParams& P, double* sc, int st) {
+  __device__ static void riemann(const double* ql, const double* qr, const double* cl, const double* cr,
+                                 int cs, AuxCell, AuxCell, const SolverParams& P, double* sc, int st) {
     constexpr int nd = D, td = 3 - D;
-    const double hl = ql[0], hr = qr[0];
-    const double sl = sqrt(hl), sr = sqrt(hr);
-    const double inv = 1.0 / (sl + sr);
-    const double u = (ql[1] / sl + qr[1] / sr) * inv;   // (sqrt(h) (hu/h)) summed
-    const double v = (ql[2] / sl + qr[2] / sr) * inv;
-    const double c = sqrt(0.5 * P.p0 * (hl + hr));
+    const double wl = cl[0], wr = cr[0];
+    const double inv = fast_rcp(wl + wr);
+    const double al = wl * inv, ar = wr * inv;
+    const double u = al * cl[cs] + ar * cr[cs];
+    const double v = al * cl[2 * cs] + ar * cr[2 * cs];
+    const double c2 = 0.5 * P.p0 * (ql[0] + qr[0]);
+    const double ic = fast_rsqrt(c2);
+    const double c = c2 * ic;
     const double un = nd == 1 ? u : v, ut = nd == 1 ? v : u;
-    const double dh = hr - hl, dn = qr[nd] - ql[nd], dtg = qr[td] - ql[td];
-    const double i2c = 0.5 / c;
+    const double dh = qr[0] - ql[0], dn = qr[nd] - ql[nd], dtg = qr[td] - ql[td];
+    const double i2c = 0.5 * ic;
     sc[0] = ((un + c) * dh - dn) * i2c;
     sc[st] = dtg - ut * dh;
     sc[2 * st] = ((c - un) * dh + dn) * i2c;
     sc[3 * st] = u;
     sc[4 * st] = v;
     sc[5 * st] = c;
+    sc[6 * st] = ic;
   }
   template <int D>
   __device__ static double speed(const double* sc, int st, int p, const SolverParams&, AuxCell) {
@@ -163,27 +201,25 @@ struct SweRoe {
       }
     }
   }
-  // transverse direction td of this sweep, same Roe state
   template <int D>
   __device__ static void transverse(const double* sc, int st, const SolverParams&, const double* X,
                                     AuxCell, AuxCell, double* bm, double* bp) {
     constexpr int nd = 3 - D, td = D;   // eigen-decomposition along the transverse direction
-    const double u = sc[3 * st], v = sc[4 * st], c = sc[5 * st];
+    const double u = sc[3 * st], v = sc[4 * st], c = sc[5 * st], ic = sc[6 * st];
     const double vn = nd == 1 ? u : v, vt = nd == 1 ? v : u;
-    const double i2c = 0.5 / c;
+    const double i2c = 0.5 * ic;
     const double b1 = ((vn + c) * X[0] - X[nd]) * i2c;
     const double b2 = X[td] - vt * X[0];
     const double b3 = ((c - vn) * X[0] + X[nd]) * i2c;
     const double l1 = vn - c, l2 = vn, l3 = vn + c;
-    double r1[3], r3[3];
-    r1[0] = 1.0; r1[nd] = vn - c; r1[td] = vt;
-    r3[0] = 1.0; r3[nd] = vn + c; r3[td] = vt;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const double w2 = (k == td) ? b2 : 0.0;
-      bm[k] = dmin0(l1) * b1 * r1[k] + dmin0(l2) * w2 + dmin0(l3) * b3 * r3[k];
-      bp[k] = dmax0(l1) * b1 * r1[k] + dmax0(l2) * w2 + dmax0(l3) * b3 * r3[k];
-    }
+    const double m1 = dmin0(l1) * b1, m2 = dmin0(l2) * b2, m3 = dmin0(l3) * b3;
+    const double p1 = dmax0(l1) * b1, p2 = dmax0(l2) * b2, p3 = dmax0(l3) * b3;
+    bm[0] = m1 + m3;
+    bm[nd] = m1 * (vn - c) + m3 * (vn + c);
+    bm[td] = (m1 + m3) * vt + m2;
+    bp[0] = p1 + p3;
+    bp[nd] = p1 * (vn - c) + p3 * (vn + c);
+    bp[td] = (p1 + p3) * vt + p2;
   }
 };
 
@@ -194,85 +230,113 @@ struct SweRoe {
 // r1 = (1, un-c, vt, H - un c), r2 = (1, un, vt, (un^2+vt^2)/2), r3 = (0, 0, 1, vt)_t,
 // r4 = (1, un+c, vt, H + un c); speeds un-c, un, un, un+c.
 struct EulerRoe {
-  static constexpr int MEQN = 4, MW = 4, NS = 12;
+  static constexpr int MEQN = 4, MW = 4, NS = 13, NC = 5;
   static constexpr bool CAPA = false;
-  __device__ static double pressure(const double* q, double gm1) {
-    const double ir = 1.0 / q[0];
-    return gm1 * (q[3] - 0.5 * (q[1] * q[1] + q[2] * q[2]) * ir);
+  // cell fields: sqrt(rho), u, v, H, c
+  __device__ static void precompute(const double* q, int qs, const SolverParams& P, double* c, int cs) {
+    const double gam = P.p0, gm1 = gam - 1.0;
+    const double rho = q[0];
+    const double rs = fast_rsqrt(rho);
+    const double ir = rs * rs;
+    const double u = q[qs] * ir, v = q[2 * qs] * ir;
+    const double p = gm1 * (q[3 * qs] - 0.5 * rho * (u * u + v * v));
+    c[0] = rho * rs;
+    c[cs] = u;
+    c[2 * cs] = v;
+    c[3 * cs] = (q[3 * qs] + p) * ir;
+    const double c2 = gam * p * ir;
+    c[4 * cs] = c2 * fast_rsqrt(c2);
+  }
+  // sign test of lambda = m/rho -+ c at a conserved state without divisions:
+  // (m/rho)^2 > c^2  <=>  m^2 > gam (gam-1) (E rho - (m^2 + t^2)/2)   (rho > 0)
+  __device__ static bool supersonic(double rho, double mn, double mt, double E, double gam) {
+    return mn * mn > gam * (gam - 1.0) * (E * rho - 0.5 * (mn * mn + mt * mt));
   }
   template <int D>
-  __device__ static void riemann(const double* ql, const double* qr, AuxCell, AuxCell,
-                                 const SolverParams& P, double* sc, int st) {
+  __device__ static void riemann(const double* ql, const double* qr, const double* cl, const double* cr,
+                                 int cs, AuxCell, AuxCell, const SolverParams& P, double* sc, int st) {
     constexpr int nd = D, td = 3 - D;
     const double gam = P.p0, gm1 = gam - 1.0;
-    const double pl = pressure(ql, gm1), pr = pressure(qr, gm1);
-    const double sl = sqrt(ql[0]), sr = sqrt(qr[0]);
-    const double inv = 1.0 / (sl + sr);
-    const double u = (ql[1] / sl + qr[1] / sr) * inv;
-    const double v = (ql[2] / sl + qr[2] / sr) * inv;
-    const double H = ((ql[3] + pl) / sl + (qr[3] + pr) / sr) * inv;
+    const double wl = cl[0], wr = cr[0];
+    const double inv = fast_rcp(wl + wr);
+    const double al = wl * inv, ar = wr * inv;
+    const double u = al * cl[cs] + ar * cr[cs];
+    const double v = al * cl[2 * cs] + ar * cr[2 * cs];
+    const double H = al * cl[3 * cs] + ar * cr[3 * cs];
     const double c2 = gm1 * (H - 0.5 * (u * u + v * v));
-    const double c = sqrt(c2);
+    const double ic = fast_rsqrt(c2);
+    const double c = c2 * ic;
     const double un = nd == 1 ? u : v, vt = nd == 1 ? v : u;
     double d[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) d[k] = qr[k] - ql[k];
     const double a3 = d[td] - vt * d[0];
-    const double a2 = gm1 / c2 * ((H - un * un - vt * vt) * d[0] + un * d[nd] + vt * d[td] - d[3]);
-    const double a4 = (d[nd] + (c - un) * d[0] - c * a2) * (0.5 / c);
+    const double a2 = gm1 * (ic * ic) * ((H - un * un - vt * vt) * d[0] + un * d[nd] + vt * d[td] - d[3]);
+    const double a4 = (d[nd] + (c - un) * d[0] - c * a2) * (0.5 * ic);
     const double a1 = d[0] - a2 - a4;
     sc[0] = a1; sc[st] = a2; sc[2 * st] = a3; sc[3 * st] = a4;
-    sc[4 * st] = u; sc[5 * st] = v; sc[6 * st] = H; sc[7 * st] = c;
-    // A-dq
-    double am[4];
-    const double s1 = un - c, s2 = un, s4 = un + c;
-    double W1[4], W2[4], W3[4], W4[4];
+    sc[4 * st] = u; sc[5 * st] = v; sc[6 * st] = H; sc[7 * st] = c; sc[8 * st] = ic;
+    // waves 1 and 4 (2 and 3 move with un)
+    double W1[4], W4[4], W23[4];
     W1[0] = a1; W1[nd] = a1 * (un - c); W1[td] = a1 * vt; W1[3] = a1 * (H - un * c);
-    W2[0] = a2; W2[nd] = a2 * un; W2[td] = a2 * vt; W2[3] = a2 * 0.5 * (un * un + vt * vt);
-    W3[0] = 0.0; W3[nd] = 0.0; W3[td] = a3; W3[3] = a3 * vt;
     W4[0] = a4; W4[nd] = a4 * (un + c); W4[td] = a4 * vt; W4[3] = a4 * (H + un * c);
+    W23[0] = a2; W23[nd] = a2 * un; W23[td] = a2 * vt + a3;
+    W23[3] = a2 * 0.5 * (un * un + vt * vt) + a3 * vt;
+    const double s1 = un - c, s2 = un, s4 = un + c;
+    double am[4];
     if (P.p1 == 0.0) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        am[k] = dmin0(s1) * W1[k] + dmin0(s2) * (W2[k] + W3[k]) + dmin0(s4) * W4[k];
+      for (int k = 0; k < 4; ++k) am[k] = dmin0(s1) * W1[k] + dmin0(s2) * W23[k] + dmin0(s4) * W4[k];
     } else {
+      // Harten-Hyman; transonic tests are division-free sign tests,
+      // the exact eigenvalues are only formed in the (rare) transonic case
+      const double s0 = (nd == 1 ? cl[cs] : cl[2 * cs]) - cl[4 * cs];      // lambda_1(Q_l)
 #pragma unroll
       for (int k = 0; k < 4; ++k) am[k] = 0.0;
-      const double s0 = ql[nd] / ql[0] - sqrt(gam * pl / ql[0]);      // lambda_1(Q_l)
       if (!(s0 >= 0.0 && s1 > 0.0)) {
-        double q1[4];
+        double beta = s1 < 0.0 ? s1 : 0.0;
+        if (s0 < 0.0) {
+          double q1[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) q1[k] = ql[k] + W1[k];
-        const double p1 = pressure(q1, gm1);
-        const double s1r = q1[nd] / q1[0] - sqrt(gam * p1 / q1[0]);    // lambda_1(Q_l + W1)
-        double beta;
-        if (s0 < 0.0 && s1r > 0.0) beta = s0 * (s1r - s1) / (s1r - s0);
-        else if (s1 < 0.0) beta = s1;
-        else beta = 0.0;
+          for (int k = 0; k < 4; ++k) q1[k] = ql[k] + W1[k];
+          // lambda_1(Q_l + W1) > 0  <=>  q1n > 0 and supersonic
+          if (q1[nd] > 0.0 && supersonic(q1[0], q1[nd], q1[td], q1[3], gam)) {
+            const double ir = fast_rcp(q1[0]);
+            const double un1 = q1[nd] * ir, ut1 = q1[td] * ir;
+            const double p1 = gm1 * (q1[3] - 0.5 * q1[0] * (un1 * un1 + ut1 * ut1));
+            const double cc = gam * p1 * ir;
+            const double lr = un1 - cc * fast_rsqrt(cc);
+            beta = s0 * (lr - s1) * fast_rcp(lr - s0);
+          }
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) am[k] = beta * W1[k];
         if (s2 < 0.0) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) am[k] += s2 * (W2[k] + W3[k]);
-          double q3[4];
+          for (int k = 0; k < 4; ++k) am[k] += s2 * W23[k];
+          const double s4r = (nd == 1 ? cr[cs] : cr[2 * cs]) + cr[4 * cs];  // lambda_4(Q_r)
+          double b4 = s4 < 0.0 ? s4 : 0.0;
+          if (s4r > 0.0) {
+            double q3[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) q3[k] = qr[k] - W4[k];
-          const double p3 = pressure(q3, gm1);
-          const double s4l = q3[nd] / q3[0] + sqrt(gam * p3 / q3[0]);  // lambda_4(Q_r - W4)
-          const double s4r = qr[nd] / qr[0] + sqrt(gam * pr / qr[0]);  // lambda_4(Q_r)
-          if (s4l < 0.0 && s4r > 0.0) {
-            const double b4 = s4l * (s4r - s4) / (s4r - s4l);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) am[k] += b4 * W4[k];
-          } else if (s4 < 0.0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) am[k] += s4 * W4[k];
+            for (int k = 0; k < 4; ++k) q3[k] = qr[k] - W4[k];
+            // lambda_4(Q_r - W4) < 0  <=>  q3n < 0 and supersonic
+            if (q3[nd] < 0.0 && supersonic(q3[0], q3[nd], q3[td], q3[3], gam)) {
+              const double ir = fast_rcp(q3[0]);
+              const double un3 = q3[nd] * ir, ut3 = q3[td] * ir;
+              const double p3 = gm1 * (q3[3] - 0.5 * q3[0] * (un3 * un3 + ut3 * ut3));
+              const double cc = gam * p3 * ir;
+              const double ll = un3 + cc * fast_rsqrt(cc);
+              b4 = ll * (s4r - s4) * fast_rcp(s4r - ll);
+            }
           }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) am[k] += b4 * W4[k];
         }
       }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) sc[(8 + k) * st] = am[k];
+    for (int k = 0; k < 4; ++k) sc[(9 + k) * st] = am[k];
   }
   template <int D>
   __device__ static double speed(const double* sc, int st, int p, const SolverParams&, AuxCell) {
@@ -304,7 +368,7 @@ struct EulerRoe {
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      am[k] = sc[(8 + k) * st];
+      am[k] = sc[(9 + k) * st];
       ap[k] = df[k] - am[k];
     }
   }
@@ -313,24 +377,25 @@ struct EulerRoe {
                                     AuxCell, AuxCell, double* bm, double* bp) {
     constexpr int nd = 3 - D, td = D;
     const double gm1 = P.p0 - 1.0;
-    const double u = sc[4 * st], v = sc[5 * st], H = sc[6 * st], c = sc[7 * st];
+    const double u = sc[4 * st], v = sc[5 * st], H = sc[6 * st], c = sc[7 * st], ic = sc[8 * st];
     const double vn = nd == 1 ? u : v, vt = nd == 1 ? v : u;
-    const double c2 = c * c;
     const double b3 = X[td] - vt * X[0];
-    const double b2 = gm1 / c2 * ((H - vn * vn - vt * vt) * X[0] + vn * X[nd] + vt * X[td] - X[3]);
-    const double b4 = (X[nd] + (c - vn) * X[0] - c * b2) * (0.5 / c);
+    const double b2 = gm1 * (ic * ic) * ((H - vn * vn - vt * vt) * X[0] + vn * X[nd] + vt * X[td] - X[3]);
+    const double b4 = (X[nd] + (c - vn) * X[0] - c * b2) * (0.5 * ic);
     const double b1 = X[0] - b2 - b4;
-    double r1[4], r2[4], r3[4], r4[4];
-    r1[0] = 1.0; r1[nd] = vn - c; r1[td] = vt; r1[3] = H - vn * c;
-    r2[0] = 1.0; r2[nd] = vn; r2[td] = vt; r2[3] = 0.5 * (vn * vn + vt * vt);
-    r3[0] = 0.0; r3[nd] = 0.0; r3[td] = 1.0; r3[3] = vt;
-    r4[0] = 1.0; r4[nd] = vn + c; r4[td] = vt; r4[3] = H + vn * c;
     const double l1 = vn - c, l2 = vn, l4 = vn + c;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      bm[k] = dmin0(l1) * b1 * r1[k] + dmin0(l2) * (b2 * r2[k] + b3 * r3[k]) + dmin0(l4) * b4 * r4[k];
-      bp[k] = dmax0(l1) * b1 * r1[k] + dmax0(l2) * (b2 * r2[k] + b3 * r3[k]) + dmax0(l4) * b4 * r4[k];
-    }
+    const double ek = 0.5 * (vn * vn + vt * vt);
+    // B-X and B+X: sum over waves of min/max(lambda, 0) b r
+    const double m1 = dmin0(l1) * b1, m2 = dmin0(l2) * b2, m3 = dmin0(l2) * b3, m4 = dmin0(l4) * b4;
+    const double p1 = dmax0(l1) * b1, p2 = dmax0(l2) * b2, p3 = dmax0(l2) * b3, p4 = dmax0(l4) * b4;
+    bm[0] = m1 + m2 + m4;
+    bm[nd] = m1 * (vn - c) + m2 * vn + m4 * (vn + c);
+    bm[td] = (m1 + m2 + m4) * vt + m3;
+    bm[3] = m1 * (H - vn * c) + m2 * ek + m3 * vt + m4 * (H + vn * c);
+    bp[0] = p1 + p2 + p4;
+    bp[nd] = p1 * (vn - c) + p2 * vn + p4 * (vn + c);
+    bp[td] = (p1 + p2 + p4) * vt + p3;
+    bp[3] = p1 * (H - vn * c) + p2 * ek + p3 * vt + p4 * (H + vn * c);
   }
 };
 

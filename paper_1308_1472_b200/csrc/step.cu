@@ -1,0 +1,323 @@
+// step.cu -- the fused wave-propagation step kernel (libfc, sm_100a, fp64).
+//
+// PAPER.md:168-182 [§3]: Clawpack's wave propagation on one uniform patch -- Riemann problems at
+// every edge, left/right-going waves, a wave limiter, second-order corrections; transverse
+// (rpt2) corrections of the unsplit 2D method (readings in DESIGN.md).
+//
+// Layout: one CTA per T x T tile of a patch (T = 16 for m = 16, 32, ...; 8 for m = 8, ...); the
+// update of a cell reads only its 2-cell neighbourhood, so tiles of a patch are independent and
+// exact.  The tile plus its 2-cell halo (W = T + 4) is staged in shared memory from the padded
+// patch (ring filled by the ghost kernels).  Phases (one barrier between each):
+//   P   per-cell derived fields (sqrt(rho), u, v, H, c ...) for all W^2 staged cells
+//   X1  normal Riemann solve on all (T+3)(T+2) x-edges -> compact per-edge scratch
+//   X2  for the (T+1)(T+2) x-edges with corrections: limiter (upwind neighbour's unlimited wave),
+//       F~, CFL, L = A-dq + F~ / R = A+dq - F~, transverse splits B-+(L), B-+(R).  Each cell
+//       receives exactly one L part (from its right edge) and one R part (its left edge): L parts
+//       are stored with '=', then after a barrier R parts with '+=' -- no atomics, no zero fill.
+//   X3  fold G~ (transverse of the x-sweep) into the cell increments
+//   Y1/Y2 the same along y (reading Q^n: unsplit), transverse into F~ at x-edges
+//   Y3  fold F~ transverse, q_new = q + dq, non-finite check, CFL block max -> one atomicMax.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fc.h"
+#include "solvers.cuh"
+
+namespace fc {
+
+struct StepArgs {
+  const double* __restrict__ qold;
+  double* __restrict__ qnew;
+  const double* __restrict__ aux;     // [Pl][3][n][n] or null
+  const int8_t* __restrict__ level;   // [Pl]
+  double dt, dx0;
+  SolverParams sp;
+  int limiter, method2, method3;
+  int m, tiles;                       // tiles per side
+  unsigned long long* cfl_bits;
+};
+
+__device__ __forceinline__ double limiter_phi(int lim, double th) {
+  if (lim == 2) return fmax(0.0, fmin(fmin(0.5 * (1.0 + th), 2.0), 2.0 * th));
+  if (lim == 1) return fmax(0.0, fmin(1.0, th));
+  return 1.0;
+}
+
+template <class S, int T>
+struct StepShape {
+  static constexpr int W = T + 4;
+  static constexpr int WW = W * W;
+  static constexpr int EX = (T + 3) * (T + 2);   // edges per sweep (incl. limiter neighbours)
+  static constexpr int E2 = (T + 1) * (T + 2);   // edges with corrections / transverse
+  static constexpr int NTR = S::MEQN * T * (T + 2);
+  static constexpr size_t smem_doubles = (size_t)(S::MEQN + S::NC + (S::CAPA ? 3 : 0)) * WW +
+                                         (size_t)S::NS * EX + S::MEQN * T * T + 2 * NTR;
+  static constexpr size_t smem_bytes = smem_doubles * sizeof(double);
+};
+
+// second-order correction, CFL and transverse splits of one edge (phase 2 of a sweep)
+template <class S, int D>
+__device__ __forceinline__ void edge_phase2(const double* sc, const double* scm, const double* scp,
+                                            int st, const StepArgs& A, AuxCell ar, double rl, double rr,
+                                            AuxCell recvL, AuxCell nextL, AuxCell recvR, AuxCell nextR,
+                                            double& cfl, double* Lv, double* Rv, double* bmL, double* bpL,
+                                            double* bmR, double* bpR) {
+  constexpr int MEQN = S::MEQN;
+  double am[MEQN], ap[MEQN], F[MEQN];
+  S::template fluct<D>(sc, st, A.sp, ar, am, ap);
+#pragma unroll
+  for (int k = 0; k < MEQN; ++k) F[k] = 0.0;
+  const double rav = 0.5 * (rl + rr);
+#pragma unroll
+  for (int p = 0; p < S::MW; ++p) {
+    const double s = S::template speed<D>(sc, st, p, A.sp, ar);
+    cfl = fmax(cfl, fmax(rr * s, -rl * s));
+    if (A.method2 == 2) {
+      double Wp[MEQN], WI[MEQN];
+      S::template wave<D>(sc, st, p, A.sp, Wp);
+      S::template wave<D>(s > 0.0 ? scm : scp, st, p, A.sp, WI);
+      double wn2 = 0.0, dot = 0.0;
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) { wn2 = fma(Wp[k], Wp[k], wn2); dot = fma(WI[k], Wp[k], dot); }
+      if (wn2 != 0.0) {
+        const double phi = limiter_phi(A.limiter, dot * fast_rcp(wn2));
+        const double as = fabs(s);
+        const double c = 0.5 * as * (1.0 - as * rav) * phi;
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) F[k] = fma(c, Wp[k], F[k]);
+      }
+    }
+  }
+  const double m3 = A.method3 == 2 ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < MEQN; ++k) { Lv[k] = am[k] + F[k]; Rv[k] = ap[k] - F[k]; }
+  if (A.method3 >= 1) {
+    double XL[MEQN], XR[MEQN];
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) { XL[k] = am[k] + m3 * F[k]; XR[k] = ap[k] - m3 * F[k]; }
+    S::template transverse<D>(sc, st, A.sp, XL, recvL, nextL, bmL, bpL);
+    S::template transverse<D>(sc, st, A.sp, XR, recvR, nextR, bmR, bpR);
+  } else {
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) bmL[k] = bpL[k] = bmR[k] = bpR[k] = 0.0;
+  }
+}
+
+template <class S, int T, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A) {
+  using Sh = StepShape<S, T>;
+  constexpr int MEQN = S::MEQN, W = Sh::W, WW = Sh::WW, EX = Sh::EX, E2 = Sh::E2;
+  static_assert(E2 <= NT, "one round of corrections per sweep (single-writer L/R phases)");
+  extern __shared__ double sm[];
+  double* sq = sm;                                   // [MEQN][W][W]
+  double* scl = sq + MEQN * WW;                      // [NC][W][W] per-cell derived fields
+  double* sa = scl + S::NC * WW;                     // [3][W][W] aux (capacity form)
+  double* scr = sa + (S::CAPA ? 3 * WW : 0);         // [NS][EX] per-edge scratch
+  double* dq = scr + S::NS * EX;                     // [MEQN][T][T]
+  double* ta = dq + MEQN * T * T;                    // x: up / y: right
+  double* tb = ta + Sh::NTR;                         // x: down / y: left
+
+  const int tid = threadIdx.x;
+  const int tiles2 = A.tiles * A.tiles;
+  const int64_t patch = blockIdx.x / tiles2;
+  const int tile = blockIdx.x - (int)(patch * tiles2);
+  const int tx = tile % A.tiles, ty = tile / A.tiles;
+  const int n = A.m + 4, n2 = n * n;
+  const double* qb = A.qold + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T) * n + tx * T;
+
+  for (int t = tid; t < MEQN * WW; t += NT) {
+    const int k = t / WW, r = t - k * WW, b = r / W, a = r - b * W;
+    sq[t] = qb[(int64_t)k * n2 + b * n + a];
+  }
+  if (S::CAPA) {
+    const double* ab = A.aux + patch * 3ll * n2 + (int64_t)(ty * T) * n + tx * T;
+    for (int t = tid; t < 3 * WW; t += NT) {
+      const int k = t / WW, r = t - k * WW, b = r / W, a = r - b * W;
+      sa[t] = ab[(int64_t)k * n2 + b * n + a];
+    }
+  }
+  if (S::NC > 0) {
+    __syncthreads();
+    for (int t = tid; t < WW; t += NT) S::precompute(sq + t, WW, A.sp, scl + t, WW);
+  }
+  __syncthreads();
+
+  const double dx = ldexp(A.dx0, -(int)A.level[patch]);
+  const double dtdx = A.dt / dx;   // square cells: dt/dy = dt/dx
+  auto widx = [](int i, int j) { return (j + 1) * W + (i + 1); };   // tile-local 1-based cell
+  auto auxc = [&](int i, int j) { return AuxCell{sa + widx(i, j), WW}; };
+  auto rcell = [&](int i, int j) { return S::CAPA ? dtdx / sa[widx(i, j)] : dtdx; };
+  double cfl = 0.0;
+
+  // =============================== x-sweep ===============================
+  for (int e = tid; e < EX; e += NT) {       // edge i (cells i-1 | i), row j
+    const int i = e % (T + 3), j = e / (T + 3);
+    double ql[MEQN], qr[MEQN];
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) { ql[k] = sq[k * WW + widx(i - 1, j)]; qr[k] = sq[k * WW + widx(i, j)]; }
+    S::template riemann<1>(ql, qr, scl + widx(i - 1, j), scl + widx(i, j), WW, auxc(i - 1, j), auxc(i, j),
+                           A.sp, scr + e, EX);
+  }
+  __syncthreads();
+  {
+    const int e2 = tid;
+    const bool v = e2 < E2;
+    const int i = v ? 1 + e2 % (T + 1) : 1, j = v ? e2 / (T + 1) : 0;
+    double Lv[MEQN], Rv[MEQN], bmL[MEQN], bpL[MEQN], bmR[MEQN], bpR[MEQN];
+    const double rl = rcell(i - 1, j), rr = rcell(i, j);
+    if (v) {
+      const int e = j * (T + 3) + i;
+      edge_phase2<S, 1>(scr + e, scr + e - 1, scr + e + 1, EX, A, auxc(i, j), rl, rr, auxc(i - 1, j),
+                        auxc(i - 1, j + 1), auxc(i, j), auxc(i, j + 1), cfl, Lv, Rv, bmL, bpL, bmR, bpR);
+      if (i - 1 >= 1) {   // L part -> left cell (i-1, j): first writer
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) {
+          if (j >= 1 && j <= T) dq[(k * T + (j - 1)) * T + (i - 2)] = -rl * Lv[k];
+          ta[(k * (T + 2) + j) * T + (i - 2)] = -0.5 * rl * bpL[k];
+          tb[(k * (T + 2) + j) * T + (i - 2)] = -0.5 * rl * bmL[k];
+        }
+      }
+    }
+    __syncthreads();
+    if (v && i <= T) {    // R part -> right cell (i, j)
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) {
+        if (j >= 1 && j <= T) dq[(k * T + (j - 1)) * T + (i - 1)] -= rr * Rv[k];
+        ta[(k * (T + 2) + j) * T + (i - 1)] -= 0.5 * rr * bpR[k];
+        tb[(k * (T + 2) + j) * T + (i - 1)] -= 0.5 * rr * bmR[k];
+      }
+    }
+  }
+  __syncthreads();
+  // X3: G~(i, j+1/2) = up(i, j) + dn(i, j+1)
+  for (int t = tid; t < T * T; t += NT) {
+    const int i = 1 + t % T, j = 1 + t / T;
+    const double s = rcell(i, j);
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) {
+      const double* up = ta + k * (T + 2) * T;
+      const double* dn = tb + k * (T + 2) * T;
+      const double gt = up[j * T + (i - 1)] + dn[(j + 1) * T + (i - 1)];
+      const double gb = up[(j - 1) * T + (i - 1)] + dn[j * T + (i - 1)];
+      dq[(k * T + (j - 1)) * T + (i - 1)] -= s * (gt - gb);
+    }
+  }
+  __syncthreads();
+
+  // =============================== y-sweep ===============================
+  for (int e = tid; e < EX; e += NT) {       // column i, edge j (cells j-1 | j)
+    const int i = e % (T + 2), j = e / (T + 2);
+    double ql[MEQN], qr[MEQN];
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) { ql[k] = sq[k * WW + widx(i, j - 1)]; qr[k] = sq[k * WW + widx(i, j)]; }
+    S::template riemann<2>(ql, qr, scl + widx(i, j - 1), scl + widx(i, j), WW, auxc(i, j - 1), auxc(i, j),
+                           A.sp, scr + e, EX);
+  }
+  __syncthreads();
+  {
+    const int e2 = tid;
+    const bool v = e2 < E2;
+    const int i = v ? e2 % (T + 2) : 0, j = v ? 1 + e2 / (T + 2) : 1;
+    double Lv[MEQN], Rv[MEQN], bmL[MEQN], bpL[MEQN], bmR[MEQN], bpR[MEQN];
+    const double sl = rcell(i, j - 1), sr = rcell(i, j);
+    if (v) {
+      const int e = j * (T + 2) + i;
+      edge_phase2<S, 2>(scr + e, scr + e - (T + 2), scr + e + (T + 2), EX, A, auxc(i, j), sl, sr,
+                        auxc(i, j - 1), auxc(i + 1, j - 1), auxc(i, j), auxc(i + 1, j), cfl, Lv, Rv, bmL,
+                        bpL, bmR, bpR);
+      if (j - 1 >= 1) {   // L part -> lower cell (i, j-1)
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) {
+          if (i >= 1 && i <= T) dq[(k * T + (j - 2)) * T + (i - 1)] -= sl * Lv[k];
+          ta[(k * T + (j - 2)) * (T + 2) + i] = -0.5 * sl * bpL[k];
+          tb[(k * T + (j - 2)) * (T + 2) + i] = -0.5 * sl * bmL[k];
+        }
+      }
+    }
+    __syncthreads();
+    if (v && j <= T) {    // R part -> upper cell (i, j)
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) {
+        if (i >= 1 && i <= T) dq[(k * T + (j - 1)) * T + (i - 1)] -= sr * Rv[k];
+        ta[(k * T + (j - 1)) * (T + 2) + i] -= 0.5 * sr * bpR[k];
+        tb[(k * T + (j - 1)) * (T + 2) + i] -= 0.5 * sr * bmR[k];
+      }
+    }
+  }
+  __syncthreads();
+  // Y3: F~(i+1/2, j) = right(i, j) + left(i+1, j); q_new = q + dq
+  double* ob = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + 2) * n + tx * T + 2;
+  bool bad = false;
+  for (int t = tid; t < MEQN * T * T; t += NT) {
+    const int k = t / (T * T), r = t - k * T * T;
+    const int i = 1 + r % T, j = 1 + r / T;
+    const double rc = rcell(i, j);
+    const double* rt = ta + k * T * (T + 2);
+    const double* lf = tb + k * T * (T + 2);
+    const double fr = rt[(j - 1) * (T + 2) + i] + lf[(j - 1) * (T + 2) + i + 1];
+    const double fl = rt[(j - 1) * (T + 2) + i - 1] + lf[(j - 1) * (T + 2) + i];
+    const double val = sq[k * WW + widx(i, j)] + (dq[t] - rc * (fr - fl));
+    bad |= !isfinite(val);
+    ob[(int64_t)k * n2 + (int64_t)(j - 1) * n + (i - 1)] = val;
+  }
+  // a non-finite updated state makes the step's CFL +inf (fc_step -> FC_ENONFINITE)
+  if (__syncthreads_or(bad)) cfl = __longlong_as_double(0x7ff0000000000000ll);
+  if (cfl != cfl) cfl = __longlong_as_double(0x7ff0000000000000ll);
+  for (int o = 16; o > 0; o >>= 1) cfl = fmax(cfl, __shfl_xor_sync(0xffffffffu, cfl, o));
+  __shared__ double wmax[(NT + 31) / 32];
+  if ((tid & 31) == 0) wmax[tid >> 5] = cfl;
+  __syncthreads();
+  if (tid == 0) {
+    double c = wmax[0];
+    for (int w = 1; w < (NT + 31) / 32; ++w) c = fmax(c, wmax[w]);
+    atomicMax(A.cfl_bits, (unsigned long long)__double_as_longlong(c));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+template <class S, int T, int NT, int MINB>
+static int launch_step_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  const size_t smem = StepShape<S, T>::smem_bytes;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_step<S, T, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_step<S, T, NT, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    configured = true;
+  }
+  const int64_t grid = npatch * a.tiles * a.tiles;
+  k_step<S, T, NT, MINB><<<(unsigned)grid, NT, smem, st>>>(a);
+  return 1;
+}
+
+template <class S>
+static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  constexpr int MB16 = (S::MEQN >= 3) ? 2 : 4;
+  if (a.m % 16 == 0) return launch_step_t<S, 16, 320 + 32, MB16>(a, npatch, st);
+  if (a.m % 8 == 0) return launch_step_t<S, 8, 128, 4>(a, npatch, st);
+  if (a.m % 4 == 0) return launch_step_t<S, 4, 64, 8>(a, npatch, st);
+  if (a.m % 2 == 0) return launch_step_t<S, 2, 32, 8>(a, npatch, st);
+  return -1;
+}
+
+int launch_step(int kind, const double* qold, double* qnew, const double* aux, const int8_t* level,
+                int64_t npatch, int m, double dt, double dx0, double p0, double p1, int limiter,
+                int method2, int method3, unsigned long long* cfl_bits, cudaStream_t st) {
+  if (npatch <= 0) return 0;
+  StepArgs a;
+  a.qold = qold; a.qnew = qnew; a.aux = aux; a.level = level;
+  a.dt = dt; a.dx0 = dx0; a.sp.p0 = p0; a.sp.p1 = p1;
+  a.limiter = limiter; a.method2 = method2; a.method3 = method3;
+  a.m = m;
+  const int T = (m % 16 == 0) ? 16 : ((m % 8 == 0) ? 8 : ((m % 4 == 0) ? 4 : 2));
+  a.tiles = m / T;
+  a.cfl_bits = cfl_bits;
+  switch (kind) {
+    case FC_ADV_CONST: return launch_step_s<AdvConst>(a, npatch, st);
+    case FC_ADV_EDGEVEL_CAPA: return launch_step_s<AdvEdgeCapa>(a, npatch, st);
+    case FC_SWE_ROE: return launch_step_s<SweRoe>(a, npatch, st);
+    case FC_EULER_ROE: return launch_step_s<EulerRoe>(a, npatch, st);
+  }
+  return -1;
+}
+
+}  // namespace fc
