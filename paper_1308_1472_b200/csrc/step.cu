@@ -19,6 +19,7 @@
 //   Y3  fold F~ transverse, q_new = q + dq, non-finite check, CFL block max -> one atomicMax.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/fc.h"
 #include "solvers.cuh"
@@ -43,6 +44,39 @@ __device__ __forceinline__ double limiter_phi(int lim, double th) {
   return 1.0;
 }
 
+// ---- TMA bulk copies + mbarrier (sm_90+ / sm_100a) -------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy (UBLKCP); bytes and both addresses multiples of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// an opaque copy: keeps per-thread index arithmetic inside the tile loop instead of letting the
+// compiler hoist (and keep live in registers) every phase's thread->edge mapping
+__device__ __forceinline__ int opaque(int x) {
+  int y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 template <class S, int T>
 struct StepShape {
   static constexpr int W = T + 4;
@@ -50,20 +84,19 @@ struct StepShape {
   static constexpr int EX = (T + 3) * (T + 2);   // edges per sweep (incl. limiter neighbours)
   static constexpr int E2 = (T + 1) * (T + 2);   // edges with corrections / transverse
   static constexpr int NTR = S::MEQN * T * (T + 2);
-  static constexpr size_t smem_doubles = (size_t)(S::MEQN + S::NC + (S::CAPA ? 3 : 0)) * WW +
-                                         (size_t)S::NS * EX + S::MEQN * T * T + 2 * NTR;
+  static constexpr int BUF = (S::MEQN + (S::CAPA ? 3 : 0)) * WW;   // one staged tile (q + aux)
+  static constexpr size_t smem_doubles = (size_t)2 * BUF + (size_t)S::NC * WW + (size_t)S::NS * EX +
+                                         S::MEQN * T * T + 2 * NTR;
   static constexpr size_t smem_bytes = smem_doubles * sizeof(double);
 };
 
-// second-order correction, CFL and transverse splits of one edge (phase 2 of a sweep)
+// fluctuations + second-order correction F~ (limiter on the upwind neighbour's unlimited wave)
+// + CFL of one edge (phase 2 of a sweep)
 template <class S, int D>
-__device__ __forceinline__ void edge_phase2(const double* sc, const double* scm, const double* scp,
-                                            int st, const StepArgs& A, AuxCell ar, double rl, double rr,
-                                            AuxCell recvL, AuxCell nextL, AuxCell recvR, AuxCell nextR,
-                                            double& cfl, double* Lv, double* Rv, double* bmL, double* bpL,
-                                            double* bmR, double* bpR) {
+__device__ __forceinline__ void edge_correction(const double* sc, const double* scm, const double* scp,
+                                                int st, const StepArgs& A, AuxCell ar, double rl, double rr,
+                                                double& cfl, double* am, double* ap, double* F) {
   constexpr int MEQN = S::MEQN;
-  double am[MEQN], ap[MEQN], F[MEQN];
   S::template fluct<D>(sc, st, A.sp, ar, am, ap);
 #pragma unroll
   for (int k = 0; k < MEQN; ++k) F[k] = 0.0;
@@ -88,183 +121,252 @@ __device__ __forceinline__ void edge_phase2(const double* sc, const double* scm,
       }
     }
   }
-  const double m3 = A.method3 == 2 ? 1.0 : 0.0;
-#pragma unroll
-  for (int k = 0; k < MEQN; ++k) { Lv[k] = am[k] + F[k]; Rv[k] = ap[k] - F[k]; }
+}
+
+// transverse split of X = A-+dq (+-F~ for method3 = 2) entering `recv`
+template <class S, int D>
+__device__ __forceinline__ void edge_transverse(const double* sc, int st, const StepArgs& A, const double* X,
+                                                AuxCell recv, AuxCell next, double* bm, double* bp) {
   if (A.method3 >= 1) {
-    double XL[MEQN], XR[MEQN];
-#pragma unroll
-    for (int k = 0; k < MEQN; ++k) { XL[k] = am[k] + m3 * F[k]; XR[k] = ap[k] - m3 * F[k]; }
-    S::template transverse<D>(sc, st, A.sp, XL, recvL, nextL, bmL, bpL);
-    S::template transverse<D>(sc, st, A.sp, XR, recvR, nextR, bmR, bpR);
+    S::template transverse<D>(sc, st, A.sp, X, recv, next, bm, bp);
   } else {
 #pragma unroll
-    for (int k = 0; k < MEQN; ++k) bmL[k] = bpL[k] = bmR[k] = bpR[k] = 0.0;
+    for (int k = 0; k < S::MEQN; ++k) bm[k] = bp[k] = 0.0;
   }
 }
 
+// issue the bulk copies staging tile `tile` (q window + aux window) into buf, on barrier bar.
+// Called by all 32 lanes of warp 0: lane 0 arms the barrier, the lanes split the row copies.
+template <class S, int T>
+__device__ __forceinline__ void stage_tile(const StepArgs& A, int64_t tile, double* buf, uint64_t* bar,
+                                           int lane) {
+  using Sh = StepShape<S, T>;
+  constexpr int MEQN = S::MEQN, W = Sh::W, WW = Sh::WW;
+  const int tiles2 = A.tiles * A.tiles;
+  const int64_t patch = tile / tiles2;
+  const int t = (int)(tile - patch * tiles2);
+  const int tx = t % A.tiles, ty = t / A.tiles;
+  const int n = A.m + 4, n2 = n * n;
+  constexpr uint32_t bytes = (uint32_t)Sh::BUF * sizeof(double);
+  if (lane == 0) mbar_expect_tx(bar, bytes);
+  __syncwarp();
+  if (A.tiles == 1) {        // the window is the whole padded patch: one contiguous copy each
+    if (lane == 0) bulk_g2s(buf, A.qold + patch * (int64_t)MEQN * n2, MEQN * WW * sizeof(double), bar);
+    if (S::CAPA && lane == 1) bulk_g2s(buf + MEQN * WW, A.aux + patch * 3ll * n2, 3 * WW * sizeof(double), bar);
+  } else {                   // one row copy per (component, window row), spread over the lanes
+    const double* qb = A.qold + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T) * n + tx * T;
+#pragma unroll 1
+    for (int r = lane; r < MEQN * W; r += 32) {
+      const int k = r / W, b = r - k * W;
+      bulk_g2s(buf + r * W, qb + (int64_t)k * n2 + b * n, W * sizeof(double), bar);
+    }
+    if (S::CAPA) {
+      const double* ab = A.aux + patch * 3ll * n2 + (int64_t)(ty * T) * n + tx * T;
+#pragma unroll 1
+      for (int r = lane; r < 3 * W; r += 32) {
+        const int k = r / W, b = r - k * W;
+        bulk_g2s(buf + MEQN * WW + r * W, ab + (int64_t)k * n2 + b * n, W * sizeof(double), bar);
+      }
+    }
+  }
+}
+
+// Persistent CTAs: each loops over tiles blockIdx.x, + gridDim.x, ...; the next tile's window is
+// bulk-copied (TMA engine) into the other staging buffer while the current one is computed.
 template <class S, int T, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A) {
+__global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int64_t ntiles) {
   using Sh = StepShape<S, T>;
   constexpr int MEQN = S::MEQN, W = Sh::W, WW = Sh::WW, EX = Sh::EX, E2 = Sh::E2;
   static_assert(E2 <= NT, "one round of corrections per sweep (single-writer L/R phases)");
-  extern __shared__ double sm[];
-  double* sq = sm;                                   // [MEQN][W][W]
-  double* scl = sq + MEQN * WW;                      // [NC][W][W] per-cell derived fields
-  double* sa = scl + S::NC * WW;                     // [3][W][W] aux (capacity form)
-  double* scr = sa + (S::CAPA ? 3 * WW : 0);         // [NS][EX] per-edge scratch
+  extern __shared__ __align__(128) double sm[];
+  double* sbuf = sm;                                 // 2 x [MEQN + 3 aux][W][W] staging buffers
+  double* scl = sbuf + 2 * Sh::BUF;                  // [NC][W][W] per-cell derived fields
+  double* scr = scl + S::NC * WW;                    // [NS][EX] per-edge scratch
   double* dq = scr + S::NS * EX;                     // [MEQN][T][T]
   double* ta = dq + MEQN * T * T;                    // x: up / y: right
   double* tb = ta + Sh::NTR;                         // x: down / y: left
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ double wmax[(NT + 31) / 32];
 
   const int tid = threadIdx.x;
   const int tiles2 = A.tiles * A.tiles;
-  const int64_t patch = blockIdx.x / tiles2;
-  const int tile = blockIdx.x - (int)(patch * tiles2);
-  const int tx = tile % A.tiles, ty = tile / A.tiles;
   const int n = A.m + 4, n2 = n * n;
-  const double* qb = A.qold + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T) * n + tx * T;
-
-  for (int t = tid; t < MEQN * WW; t += NT) {
-    const int k = t / WW, r = t - k * WW, b = r / W, a = r - b * W;
-    sq[t] = qb[(int64_t)k * n2 + b * n + a];
-  }
-  if (S::CAPA) {
-    const double* ab = A.aux + patch * 3ll * n2 + (int64_t)(ty * T) * n + tx * T;
-    for (int t = tid; t < 3 * WW; t += NT) {
-      const int k = t / WW, r = t - k * WW, b = r / W, a = r - b * W;
-      sa[t] = ab[(int64_t)k * n2 + b * n + a];
-    }
-  }
-  if (S::NC > 0) {
-    __syncthreads();
-    for (int t = tid; t < WW; t += NT) S::precompute(sq + t, WW, A.sp, scl + t, WW);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_proxy_async();
   }
   __syncthreads();
-
-  const double dx = ldexp(A.dx0, -(int)A.level[patch]);
-  const double dtdx = A.dt / dx;   // square cells: dt/dy = dt/dx
-  auto widx = [](int i, int j) { return (j + 1) * W + (i + 1); };   // tile-local 1-based cell
-  auto auxc = [&](int i, int j) { return AuxCell{sa + widx(i, j), WW}; };
-  auto rcell = [&](int i, int j) { return S::CAPA ? dtdx / sa[widx(i, j)] : dtdx; };
+  if (tid < 32 && (int64_t)blockIdx.x < ntiles) stage_tile<S, T>(A, blockIdx.x, sbuf, &bars[0], tid);
+  uint32_t phase = 0;   // bit b = parity to wait for on buffer b
   double cfl = 0.0;
-
-  // =============================== x-sweep ===============================
-  for (int e = tid; e < EX; e += NT) {       // edge i (cells i-1 | i), row j
-    const int i = e % (T + 3), j = e / (T + 3);
-    double ql[MEQN], qr[MEQN];
-#pragma unroll
-    for (int k = 0; k < MEQN; ++k) { ql[k] = sq[k * WW + widx(i - 1, j)]; qr[k] = sq[k * WW + widx(i, j)]; }
-    S::template riemann<1>(ql, qr, scl + widx(i - 1, j), scl + widx(i, j), WW, auxc(i - 1, j), auxc(i, j),
-                           A.sp, scr + e, EX);
-  }
-  __syncthreads();
-  {
-    const int e2 = tid;
-    const bool v = e2 < E2;
-    const int i = v ? 1 + e2 % (T + 1) : 1, j = v ? e2 / (T + 1) : 0;
-    double Lv[MEQN], Rv[MEQN], bmL[MEQN], bpL[MEQN], bmR[MEQN], bpR[MEQN];
-    const double rl = rcell(i - 1, j), rr = rcell(i, j);
-    if (v) {
-      const int e = j * (T + 3) + i;
-      edge_phase2<S, 1>(scr + e, scr + e - 1, scr + e + 1, EX, A, auxc(i, j), rl, rr, auxc(i - 1, j),
-                        auxc(i - 1, j + 1), auxc(i, j), auxc(i, j + 1), cfl, Lv, Rv, bmL, bpL, bmR, bpR);
-      if (i - 1 >= 1) {   // L part -> left cell (i-1, j): first writer
-#pragma unroll
-        for (int k = 0; k < MEQN; ++k) {
-          if (j >= 1 && j <= T) dq[(k * T + (j - 1)) * T + (i - 2)] = -rl * Lv[k];
-          ta[(k * (T + 2) + j) * T + (i - 2)] = -0.5 * rl * bpL[k];
-          tb[(k * (T + 2) + j) * T + (i - 2)] = -0.5 * rl * bmL[k];
-        }
-      }
-    }
-    __syncthreads();
-    if (v && i <= T) {    // R part -> right cell (i, j)
-#pragma unroll
-      for (int k = 0; k < MEQN; ++k) {
-        if (j >= 1 && j <= T) dq[(k * T + (j - 1)) * T + (i - 1)] -= rr * Rv[k];
-        ta[(k * (T + 2) + j) * T + (i - 1)] -= 0.5 * rr * bpR[k];
-        tb[(k * (T + 2) + j) * T + (i - 1)] -= 0.5 * rr * bmR[k];
-      }
-    }
-  }
-  __syncthreads();
-  // X3: G~(i, j+1/2) = up(i, j) + dn(i, j+1)
-  for (int t = tid; t < T * T; t += NT) {
-    const int i = 1 + t % T, j = 1 + t / T;
-    const double s = rcell(i, j);
-#pragma unroll
-    for (int k = 0; k < MEQN; ++k) {
-      const double* up = ta + k * (T + 2) * T;
-      const double* dn = tb + k * (T + 2) * T;
-      const double gt = up[j * T + (i - 1)] + dn[(j + 1) * T + (i - 1)];
-      const double gb = up[(j - 1) * T + (i - 1)] + dn[j * T + (i - 1)];
-      dq[(k * T + (j - 1)) * T + (i - 1)] -= s * (gt - gb);
-    }
-  }
-  __syncthreads();
-
-  // =============================== y-sweep ===============================
-  for (int e = tid; e < EX; e += NT) {       // column i, edge j (cells j-1 | j)
-    const int i = e % (T + 2), j = e / (T + 2);
-    double ql[MEQN], qr[MEQN];
-#pragma unroll
-    for (int k = 0; k < MEQN; ++k) { ql[k] = sq[k * WW + widx(i, j - 1)]; qr[k] = sq[k * WW + widx(i, j)]; }
-    S::template riemann<2>(ql, qr, scl + widx(i, j - 1), scl + widx(i, j), WW, auxc(i, j - 1), auxc(i, j),
-                           A.sp, scr + e, EX);
-  }
-  __syncthreads();
-  {
-    const int e2 = tid;
-    const bool v = e2 < E2;
-    const int i = v ? e2 % (T + 2) : 0, j = v ? 1 + e2 / (T + 2) : 1;
-    double Lv[MEQN], Rv[MEQN], bmL[MEQN], bpL[MEQN], bmR[MEQN], bpR[MEQN];
-    const double sl = rcell(i, j - 1), sr = rcell(i, j);
-    if (v) {
-      const int e = j * (T + 2) + i;
-      edge_phase2<S, 2>(scr + e, scr + e - (T + 2), scr + e + (T + 2), EX, A, auxc(i, j), sl, sr,
-                        auxc(i, j - 1), auxc(i + 1, j - 1), auxc(i, j), auxc(i + 1, j), cfl, Lv, Rv, bmL,
-                        bpL, bmR, bpR);
-      if (j - 1 >= 1) {   // L part -> lower cell (i, j-1)
-#pragma unroll
-        for (int k = 0; k < MEQN; ++k) {
-          if (i >= 1 && i <= T) dq[(k * T + (j - 2)) * T + (i - 1)] -= sl * Lv[k];
-          ta[(k * T + (j - 2)) * (T + 2) + i] = -0.5 * sl * bpL[k];
-          tb[(k * T + (j - 2)) * (T + 2) + i] = -0.5 * sl * bmL[k];
-        }
-      }
-    }
-    __syncthreads();
-    if (v && j <= T) {    // R part -> upper cell (i, j)
-#pragma unroll
-      for (int k = 0; k < MEQN; ++k) {
-        if (i >= 1 && i <= T) dq[(k * T + (j - 1)) * T + (i - 1)] -= sr * Rv[k];
-        ta[(k * T + (j - 1)) * (T + 2) + i] -= 0.5 * sr * bpR[k];
-        tb[(k * T + (j - 1)) * (T + 2) + i] -= 0.5 * sr * bmR[k];
-      }
-    }
-  }
-  __syncthreads();
-  // Y3: F~(i+1/2, j) = right(i, j) + left(i+1, j); q_new = q + dq
-  double* ob = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + 2) * n + tx * T + 2;
   bool bad = false;
-  for (int t = tid; t < MEQN * T * T; t += NT) {
-    const int k = t / (T * T), r = t - k * T * T;
-    const int i = 1 + r % T, j = 1 + r / T;
-    const double rc = rcell(i, j);
-    const double* rt = ta + k * T * (T + 2);
-    const double* lf = tb + k * T * (T + 2);
-    const double fr = rt[(j - 1) * (T + 2) + i] + lf[(j - 1) * (T + 2) + i + 1];
-    const double fl = rt[(j - 1) * (T + 2) + i - 1] + lf[(j - 1) * (T + 2) + i];
-    const double val = sq[k * WW + widx(i, j)] + (dq[t] - rc * (fr - fl));
-    bad |= !isfinite(val);
-    ob[(int64_t)k * n2 + (int64_t)(j - 1) * n + (i - 1)] = val;
+
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int b = it & 1;
+    const int64_t next = tile + gridDim.x;
+    if (tid < 32 && next < ntiles) {   // the other buffer was released by the previous tile's last barrier
+      fence_proxy_async();
+      stage_tile<S, T>(A, next, sbuf + (b ^ 1) * Sh::BUF, &bars[b ^ 1], tid);
+    }
+    double* sq = sbuf + b * Sh::BUF;                 // [MEQN][W][W]
+    double* sa = sq + MEQN * WW;                     // [3][W][W] aux (capacity form)
+    const int64_t patch = tile / tiles2;
+    const int tt = (int)(tile - patch * tiles2);
+    const int tx = tt % A.tiles, ty = tt / A.tiles;
+    const double dx = ldexp(A.dx0, -(int)A.level[patch]);
+    const double dtdx = A.dt / dx;   // square cells: dt/dy = dt/dx
+    mbar_wait(&bars[b], (phase >> b) & 1u);
+    phase ^= 1u << b;
+
+    auto widx = [](int i, int j) { return (j + 1) * W + (i + 1); };   // tile-local 1-based cell
+    auto auxc = [&](int i, int j) { return AuxCell{sa + widx(i, j), WW}; };
+    auto rcell = [&](int i, int j) { return S::CAPA ? dtdx / sa[widx(i, j)] : dtdx; };
+
+    if (S::NC > 0) {
+      const int tid = opaque(threadIdx.x);
+      for (int t = tid; t < WW; t += NT) S::precompute(sq + t, WW, A.sp, scl + t, WW);
+      __syncthreads();
+    }
+    // =============================== x-sweep ===============================
+    for (int e = opaque(threadIdx.x); e < EX; e += NT) {       // edge i (cells i-1 | i), row j
+      const int i = e % (T + 3), j = e / (T + 3);
+      double ql[MEQN], qr[MEQN];
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) { ql[k] = sq[k * WW + widx(i - 1, j)]; qr[k] = sq[k * WW + widx(i, j)]; }
+      S::template riemann<1>(ql, qr, scl + widx(i - 1, j), scl + widx(i, j), WW, auxc(i - 1, j), auxc(i, j),
+                             A.sp, scr + e, EX);
+    }
+    __syncthreads();
+    {
+      const int e2 = opaque(threadIdx.x);
+      const bool v = e2 < E2;
+      const int i = v ? 1 + e2 % (T + 1) : 1, j = v ? e2 / (T + 1) : 0;
+      double Rv[MEQN], bmR[MEQN], bpR[MEQN];
+      const double rl = rcell(i - 1, j), rr = rcell(i, j);
+      if (v) {
+        const int e = j * (T + 3) + i;
+        double am[MEQN], ap[MEQN], F[MEQN], X[MEQN], bm[MEQN], bp[MEQN];
+        edge_correction<S, 1>(scr + e, scr + e - 1, scr + e + 1, EX, A, auxc(i, j), rl, rr, cfl, am, ap, F);
+        const double m3 = A.method3 == 2 ? 1.0 : 0.0;
+        if (i - 1 >= 1) {   // L part -> left cell (i-1, j): first writer
+#pragma unroll
+          for (int k = 0; k < MEQN; ++k) X[k] = am[k] + m3 * F[k];
+          edge_transverse<S, 1>(scr + e, EX, A, X, auxc(i - 1, j), auxc(i - 1, j + 1), bm, bp);
+#pragma unroll
+          for (int k = 0; k < MEQN; ++k) {
+            if (j >= 1 && j <= T) dq[(k * T + (j - 1)) * T + (i - 2)] = -rl * (am[k] + F[k]);
+            ta[(k * (T + 2) + j) * T + (i - 2)] = -0.5 * rl * bp[k];
+            tb[(k * (T + 2) + j) * T + (i - 2)] = -0.5 * rl * bm[k];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) { X[k] = ap[k] - m3 * F[k]; Rv[k] = ap[k] - F[k]; }
+        edge_transverse<S, 1>(scr + e, EX, A, X, auxc(i, j), auxc(i, j + 1), bmR, bpR);
+      }
+      __syncthreads();
+      if (v && i <= T) {    // R part -> right cell (i, j)
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) {
+          if (j >= 1 && j <= T) dq[(k * T + (j - 1)) * T + (i - 1)] -= rr * Rv[k];
+          ta[(k * (T + 2) + j) * T + (i - 1)] -= 0.5 * rr * bpR[k];
+          tb[(k * (T + 2) + j) * T + (i - 1)] -= 0.5 * rr * bmR[k];
+        }
+      }
+    }
+    __syncthreads();
+    // X3: G~(i, j+1/2) = up(i, j) + dn(i, j+1)
+    for (int t = opaque(threadIdx.x); t < T * T; t += NT) {
+      const int i = 1 + t % T, j = 1 + t / T;
+      const double s = rcell(i, j);
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) {
+        const double* up = ta + k * (T + 2) * T;
+        const double* dn = tb + k * (T + 2) * T;
+        const double gt = up[j * T + (i - 1)] + dn[(j + 1) * T + (i - 1)];
+        const double gb = up[(j - 1) * T + (i - 1)] + dn[j * T + (i - 1)];
+        dq[(k * T + (j - 1)) * T + (i - 1)] -= s * (gt - gb);
+      }
+    }
+    __syncthreads();
+    // =============================== y-sweep ===============================
+    for (int e = opaque(threadIdx.x); e < EX; e += NT) {       // column i, edge j (cells j-1 | j)
+      const int i = e % (T + 2), j = e / (T + 2);
+      double ql[MEQN], qr[MEQN];
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) { ql[k] = sq[k * WW + widx(i, j - 1)]; qr[k] = sq[k * WW + widx(i, j)]; }
+      S::template riemann<2>(ql, qr, scl + widx(i, j - 1), scl + widx(i, j), WW, auxc(i, j - 1), auxc(i, j),
+                             A.sp, scr + e, EX);
+    }
+    __syncthreads();
+    {
+      const int e2 = opaque(threadIdx.x);
+      const bool v = e2 < E2;
+      const int i = v ? e2 % (T + 2) : 0, j = v ? 1 + e2 / (T + 2) : 1;
+      double Rv[MEQN], bmR[MEQN], bpR[MEQN];
+      const double sl = rcell(i, j - 1), sr = rcell(i, j);
+      if (v) {
+        const int e = j * (T + 2) + i;
+        double am[MEQN], ap[MEQN], F[MEQN], X[MEQN], bm[MEQN], bp[MEQN];
+        edge_correction<S, 2>(scr + e, scr + e - (T + 2), scr + e + (T + 2), EX, A, auxc(i, j), sl, sr, cfl,
+                              am, ap, F);
+        const double m3 = A.method3 == 2 ? 1.0 : 0.0;
+        if (j - 1 >= 1) {   // L part -> lower cell (i, j-1)
+#pragma unroll
+          for (int k = 0; k < MEQN; ++k) X[k] = am[k] + m3 * F[k];
+          edge_transverse<S, 2>(scr + e, EX, A, X, auxc(i, j - 1), auxc(i + 1, j - 1), bm, bp);
+#pragma unroll
+          for (int k = 0; k < MEQN; ++k) {
+            if (i >= 1 && i <= T) dq[(k * T + (j - 2)) * T + (i - 1)] -= sl * (am[k] + F[k]);
+            ta[(k * T + (j - 2)) * (T + 2) + i] = -0.5 * sl * bp[k];
+            tb[(k * T + (j - 2)) * (T + 2) + i] = -0.5 * sl * bm[k];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) { X[k] = ap[k] - m3 * F[k]; Rv[k] = ap[k] - F[k]; }
+        edge_transverse<S, 2>(scr + e, EX, A, X, auxc(i, j), auxc(i + 1, j), bmR, bpR);
+      }
+      __syncthreads();
+      if (v && j <= T) {    // R part -> upper cell (i, j)
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) {
+          if (i >= 1 && i <= T) dq[(k * T + (j - 1)) * T + (i - 1)] -= sr * Rv[k];
+          ta[(k * T + (j - 1)) * (T + 2) + i] -= 0.5 * sr * bpR[k];
+          tb[(k * T + (j - 1)) * (T + 2) + i] -= 0.5 * sr * bmR[k];
+        }
+      }
+    }
+    __syncthreads();
+    // Y3: F~(i+1/2, j) = right(i, j) + left(i+1, j); q_new = q + dq  (one thread per cell)
+    {
+      const int t = opaque(threadIdx.x);
+      if (t < T * T) {
+        const int i = 1 + t % T, j = 1 + t / T;
+        const double rc = rcell(i, j);
+        double* o = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + 1 + j) * n + tx * T + 1 + i;
+        const double* rt = ta + (j - 1) * (T + 2) + i;   // right(i, j) of component 0
+        const double* lf = tb + (j - 1) * (T + 2) + i;   // left(i, j)
+        const double* qs = sq + widx(i, j);
+        const double* d = dq + (j - 1) * T + (i - 1);
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) {
+          const int c = k * T * (T + 2);
+          const double fr = rt[c] + lf[c + 1];
+          const double fl = rt[c - 1] + lf[c];
+          const double val = qs[k * WW] + (d[k * T * T] - rc * (fr - fl));
+          bad |= !isfinite(val);
+          o[(int64_t)k * n2] = val;
+        }
+      }
+    }
+    __syncthreads();   // staging buffer b and the work arrays are free for the next tile
   }
+
   // a non-finite updated state makes the step's CFL +inf (fc_step -> FC_ENONFINITE)
   if (__syncthreads_or(bad)) cfl = __longlong_as_double(0x7ff0000000000000ll);
   if (cfl != cfl) cfl = __longlong_as_double(0x7ff0000000000000ll);
   for (int o = 16; o > 0; o >>= 1) cfl = fmax(cfl, __shfl_xor_sync(0xffffffffu, cfl, o));
-  __shared__ double wmax[(NT + 31) / 32];
   if ((tid & 31) == 0) wmax[tid >> 5] = cfl;
   __syncthreads();
   if (tid == 0) {
@@ -278,21 +380,34 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A) {
 template <class S, int T, int NT, int MINB>
 static int launch_step_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   const size_t smem = StepShape<S, T>::smem_bytes;
-  static bool configured = false;
-  if (!configured) {
+  static int resident = 0;   // CTAs that fit on the device at once (persistent grid)
+  if (!resident) {
     cudaFuncSetAttribute(k_step<S, T, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_step<S, T, NT, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    configured = true;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<S, T, NT, MINB>, NT, smem);
+    resident = sms * (per_sm > 0 ? per_sm : 1);
   }
-  const int64_t grid = npatch * a.tiles * a.tiles;
-  k_step<S, T, NT, MINB><<<(unsigned)grid, NT, smem, st>>>(a);
+  const int64_t ntiles = npatch * a.tiles * a.tiles;
+  const int64_t grid = ntiles < resident ? ntiles : resident;
+  k_step<S, T, NT, MINB><<<(unsigned)grid, NT, smem, st>>>(a, ntiles);
   return 1;
 }
 
 template <class S>
 static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
-  constexpr int MB16 = (S::MEQN >= 3) ? 2 : 4;
-  if (a.m % 16 == 0) return launch_step_t<S, 16, 320 + 32, MB16>(a, npatch, st);
+  // CTAs per SM requested from ptxas for the 16 x 16 tile (register budget 65536 / (352 MB));
+  // FC_STEP_MINB overrides it for tuning experiments
+  static const int env_mb = getenv("FC_STEP_MINB") ? atoi(getenv("FC_STEP_MINB")) : 0;
+  const int mb = env_mb ? env_mb : ((S::MEQN >= 3) ? 2 : 3);
+  if (a.m % 16 == 0) {
+    if (mb == 1) return launch_step_t<S, 16, 352, 1>(a, npatch, st);
+    if (mb == 2) return launch_step_t<S, 16, 352, 2>(a, npatch, st);
+    if (mb == 3) return launch_step_t<S, 16, 352, 3>(a, npatch, st);
+    return launch_step_t<S, 16, 352, 4>(a, npatch, st);
+  }
   if (a.m % 8 == 0) return launch_step_t<S, 8, 128, 4>(a, npatch, st);
   if (a.m % 4 == 0) return launch_step_t<S, 4, 64, 8>(a, npatch, st);
   if (a.m % 2 == 0) return launch_step_t<S, 2, 32, 8>(a, npatch, st);

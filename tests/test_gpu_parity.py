@@ -34,9 +34,13 @@ def assert_parity(w, qg, qo, cg, co, mass_rtol=1e-13):
 
 
 # ---- ghost fill ---------------------------------------------------------------------------------
+from workloads.cubed_sphere import c4_workload
+
+
 def _ring_cases():
     rng = np.random.default_rng(1308147 + 11)
-    out = [c1(), c2(), c3(level=2, m=8), c3(level=1, m=32), c5(level=2, m=16)]
+    out = [c1(), c2(), c3(level=2, m=8), c3(level=1, m=32), c5(level=2, m=16),
+           c4_workload(base_level=2, m=8), c4_workload(base_level=2, m=8, uniform=True)]
     for name, conn in (("walls", F.walled_unit_square(F.WALL)), ("brick", F.brick(3, 2, bc=F.OUTFLOW)),
                        ("reversed", F.brick(2, 1, bc=F.OUTFLOW, reversed_x_links=(0,))),
                        ("periodic", F.periodic_unit_square())):
@@ -65,6 +69,7 @@ def test_ghost_rings_bitwise(w, rng):
 
 # ---- full runs vs the oracle ----------------------------------------------------------------------
 RUNS = [c1(), c2(), c3(level=3, m=32), c5(level=3, m=16), c5(level=2, m=8),
+        c4_workload(base_level=2, m=16, steps=100), c4_workload(base_level=2, m=8, uniform=True, steps=60),
         c1(level=2, m=24, steps=30), c1(level=1, m=20, steps=30), c1(level=1, m=6, steps=30)]
 
 
@@ -152,12 +157,12 @@ def _sample_ids(w, rng, extra):
     return np.array(sorted(i for i in ids if 0 <= i < P), np.int64)
 
 
-@pytest.mark.parametrize("name", ["C5", "C3"])
+@pytest.mark.parametrize("name", ["C5", "C3", "C4"])
 def test_full_size_first_step_sampled(name, rng):
     """BASELINE.json's full sizes in the launch configuration bench.py times: one step from the IC
     on the GPU, checked on sampled patches (random + shock/bubble/wall-adjacent ones) against
     the oracle's per-patch step built from the same IC."""
-    w = c5() if name == "C5" else c3()
+    w = {"C5": c5, "C3": c3, "C4": c4_workload}[name]()
     f = gpu_forest(w)
     f.set_q(np.ascontiguousarray(w.q0))
     rc, cfl = f.step(w.dt0)
@@ -167,11 +172,14 @@ def test_full_size_first_step_sampled(name, rng):
     if name == "C5":
         extra = np.nonzero((np.abs(X + h / 2 - 1.29) < 0.01) | (np.abs(X + h / 2 - 1.3) < 0.02) |
                            (y0 == 0) | (x0 + h >= 1.0 - 1e-12))[0][:64]
+    elif name == "C4":   # patches at tree corners / faces and at level jumps
+        corner = ((x0 == 0) | (x0 + h >= 1 - 1e-12)) & ((y0 == 0) | (y0 + h >= 1 - 1e-12))
+        extra = np.concatenate([np.nonzero(corner)[0], np.nonzero(np.diff(w.forest.levels) != 0)[0][:40]])
     else:
         extra = np.nonzero((x0 == 0) | (y0 == 0) | (np.abs(np.hypot(x0 + h / 2 - 0.5, y0 + h / 2 - 0.5) - 0.2) < 0.03))[0][:64]
     ids = _sample_ids(w, rng, extra.tolist())
     of = oracle.forest_for(w)
-    qo, co = of.step_sample(oracle.problem_for(w), w.q0, w.dt0, 1.0 / w.m, ids)
+    qo, co = of.step_sample(oracle.problem_for(w), w.q0, w.dt0, 1.0 / w.m, ids, aux=w.aux)
     for k in range(w.meqn):
         scale = max(np.abs(qo[:, k]).max(), 1e-300)
         err = np.abs(qg[ids, k] - qo[:, k]).max()

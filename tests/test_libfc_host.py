@@ -34,8 +34,12 @@ def oracle_table(levels, tree_ids, conn, m):
     return oracle.OracleForest(levels, tree_ids, conn, m).ghost_table()
 
 
+from workloads.cubed_sphere import c4_workload
+
+
 @pytest.mark.parametrize("w", [c1(), c1(level=3, m=4), c2(), c3(level=2, m=8), c3(level=1, m=32),
-                               c5(level=2, m=8), c5(level=1, m=16)], ids=lambda w: w.name)
+                               c5(level=2, m=8), c5(level=1, m=16), c4_workload(),
+                               c4_workload(base_level=2, m=8, uniform=True)], ids=lambda w: w.name)
 def test_table_bit_exact_configs(w):
     _, t = host_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m)
     o = oracle_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m)
