@@ -173,6 +173,11 @@ int fc_local_range(fc_forest* f, int64_t* first, int64_t* count);
  * rank receives per step (counts[nranks]).  Works on host-only handles. */
 int fc_halo_counts(fc_forest* f, int64_t* counts);
 
+/* The remote cells this rank requests from `peer` in halo round 1 (interior cells) or 2 (ring cells
+ * read by interpolation slopes): keys global_patch * n^2 + padded cell index, ascending.
+ * *len = count; FC_EINVAL if cap < count.  Works on host-only handles (multi-rank plan tests). */
+int fc_halo_requests(fc_forest* f, int peer, int round, int64_t* buf, int64_t cap, int64_t* len);
+
 /* Write a fresh 128-byte ncclUniqueId into out (call on rank 0, broadcast to the others). */
 int fc_nccl_unique_id(void* out);
 

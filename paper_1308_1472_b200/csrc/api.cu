@@ -408,6 +408,16 @@ int fc_halo_counts(fc_forest* f, int64_t* counts) {
   return FC_OK;
 }
 
+int fc_halo_requests(fc_forest* f, int peer, int round, int64_t* buf, int64_t cap, int64_t* len) {
+  if (!f || !len) return fail(FC_EINVAL, "null argument");
+  if (peer < 0 || peer >= f->pl.nranks || (round != 1 && round != 2)) return fail(FC_EINVAL, "bad peer/round");
+  const auto& v = round == 1 ? f->pl.halo.need1[peer] : f->pl.halo.need2[peer];
+  *len = (int64_t)v.size();
+  if (cap < *len || (!buf && *len)) return fail(FC_EINVAL, "buffer too small");
+  if (*len) std::memcpy(buf, v.data(), v.size() * sizeof(int64_t));
+  return FC_OK;
+}
+
 int fc_get_ghost_table(fc_forest* f, int which, int32_t* buf, int64_t cap, int64_t* len) {
   if (!f || !len) return fail(FC_EINVAL, "null argument");
   if (which != FC_TABLE_EXPANDED) return fail(FC_EINVAL, "unknown table kind");

@@ -31,7 +31,7 @@ ERRNAMES = {0: "FC_OK", -1: "FC_EINVAL", -2: "FC_ETILING", -3: "FC_ECONN", -4: "
 EXPORTS = ["fc_forest_create", "fc_forest_destroy", "fc_set_problem", "fc_set_aux", "fc_set_q",
            "fc_ghost_fill", "fc_step", "fc_get_q", "fc_get_q_padded", "fc_get_ghost_table",
            "fc_set_stream", "fc_set_timing", "fc_get_stats", "fc_reset_stats", "fc_local_range",
-           "fc_halo_counts", "fc_nccl_unique_id", "fc_last_error"]
+           "fc_halo_counts", "fc_halo_requests", "fc_nccl_unique_id", "fc_last_error"]
 
 
 class FcError(RuntimeError):
@@ -91,6 +91,7 @@ def lib():
         L.fc_reset_stats.argtypes = [P]
         L.fc_local_range.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.fc_halo_counts.argtypes = [P, P]
+        L.fc_halo_requests.argtypes = [P, C.c_int, C.c_int, P, C.c_int64, C.POINTER(C.c_int64)]
         L.fc_nccl_unique_id.argtypes = [P]
         L.fc_last_error.restype = C.c_char_p
         _lib = L
@@ -214,6 +215,14 @@ class Forest:
 
     def reset_stats(self):
         _check(lib().fc_reset_stats(self.h), "fc_reset_stats")
+
+    def halo_requests(self, peer: int, round_: int) -> np.ndarray:
+        n = C.c_int64()
+        lib().fc_halo_requests(self.h, peer, round_, None, 0, C.byref(n))
+        buf = np.empty(max(1, n.value), np.int64)
+        _check(lib().fc_halo_requests(self.h, peer, round_, buf.ctypes.data_as(C.c_void_p), n.value,
+                                      C.byref(n)), "fc_halo_requests")
+        return buf[:n.value]
 
     def halo_counts(self) -> np.ndarray:
         out = np.zeros(self.nranks, np.int64)
