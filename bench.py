@@ -54,6 +54,28 @@ def make_workload(name: str):
     raise SystemExit(f"unknown workload {name}")
 
 
+def algorithmic_flops(name: str):
+    """fp64 flops per cell-update of the method, counted on the oracle's own code
+    (tools/count_flops.py -> profiles/algorithmic_flops.json)."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "profiles", "algorithmic_flops.json")))[name])
+    except Exception:
+        return None
+
+
+def fp64_peak_tflops(pk) -> float:
+    """B200 fp64 (non-tensor) peak from unit counts: 148 SMs x 64 FMA lanes x 2 flops x clock."""
+    return 148 * 64 * 2 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+
+
+def profile_summary(name: str):
+    """Per-launch DRAM traffic of the update kernel from the committed ncu capture, if any."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "step_kernel_traffic.json")))[name]
+    except Exception:
+        return None
+
+
 def bytes_per_cell_update(w) -> int:
     """Compulsory (algorithmic) HBM bytes per cell-update: q read + q written + aux read."""
     return 16 * w.meqn + 8 * w.maux
@@ -245,41 +267,68 @@ def main():
             dt = w.next_dt(dt, cfl)
         return dt, cfls
 
-    # ---- device-resident timed run ----
-    f.set_q(qdev)
-    dt, _ = steps(args.warmup, w.dt0)
-    f.reset_stats()
-    f.set_timing(True)
-    clocks = Clocks(list(range(max(1, world)))) if rank == 0 else None
-    barrier()
-    torch.cuda.synchronize()
-    if clocks:
-        clocks.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    dt, cfls = steps(args.steps, dt)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    clk = clocks.stop() if clocks else None
-    ms = allmax(ev0.elapsed_time(ev1))
-    st = f.stats()
-    f.set_timing(False)
-    value = cells_total * args.steps / (ms / 1000.0)
+    def set_mode(skip: int):
+        f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject, skip)
 
-    # dominant kernel: the fused update (avg launch time from CUDA events on the lib's stream)
+    def timed(skip: int, monitor: bool):
+        """W warm-up + K timed steps from the IC (device-resident inputs)."""
+        set_mode(skip)
+        f.set_q(qdev)
+        dt, _ = steps(args.warmup, w.dt0)
+        f.reset_stats()
+        f.set_timing(True)
+        clocks = Clocks(list(range(max(1, world)))) if (rank == 0 and monitor) else None
+        barrier()
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.start()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        dt, cfls = steps(args.steps, dt)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        clk = clocks.stop() if clocks else None
+        ms = allmax(ev0.elapsed_time(ev1))
+        st = f.stats()
+        f.set_timing(False)
+        return ms, st, clk, cfls
+
+    # ---- device-resident timed runs: default (exact quiescent-tile shortcut on), full update ----
+    ms, st, clk, cfls = timed(1, True)
+    value = cells_total * args.steps / (ms / 1000.0)
+    ms_full, st_full, _, _ = timed(0, False)
+    value_full = cells_total * args.steps / (ms_full / 1000.0)
+    set_mode(1)
+
     pk, pk_src = peaks()
+    bpc = bytes_per_cell_update(w)
+    hbm_peak = float(pk["hbm_gbs"])
+    flops = algorithmic_flops(args.workload)
+    fp64_peak = fp64_peak_tflops(pk)
+    prof = profile_summary(args.workload)
+    kernel = {"C5": "k_step<EulerRoe,16,352,2>", "C3": "k_step<SweRoe,16,352,2>"}[args.workload]
+    # dominant kernel of the timed step: the fused update (launch time from CUDA events on the
+    # library's stream); with quiescent tiles skipped it streams q through HBM
     step_ms = st["ms_step"] / max(1, st["step_kernel_launches"])
     ghost_ms = st["ms_ghost"] / max(1, st["steps"])
-    bpc = bytes_per_cell_update(w)
     ach_gbs = local_cells * bpc / (step_ms / 1000.0) / 1e9
-    hbm_peak = float(pk["hbm_gbs"])
     roofline = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm_peak, "unit": "GB/s",
-                "frac": ach_gbs / hbm_peak, "traffic": None,
-                "kernel": "k_step<EulerRoe,16,320>" if args.workload == "C5" else "k_step",
-                "algorithmic_bytes_per_cell_update": bpc, "launch_ms": step_ms,
-                "peak_source": f"{pk_src} MEASURED_PEAKS.json hbm_gbs",
-                "note": "fp64-ALU-bound kernel: see roofline_alu in DESIGN.md; HBM fraction is the metric's own figure"}
+                "frac": ach_gbs / hbm_peak,
+                "traffic": prof.get("dram_bytes_per_launch") if prof else None,
+                "kernel": kernel + " (quiescent-tile shortcut on)", "launch_ms": step_ms,
+                "algorithmic_bytes_per_cell_update": bpc,
+                "peak_source": f"{pk_src} MEASURED_PEAKS.json hbm_gbs (copy)"}
+    # the full update (no shortcut) is bound by the fp64 pipe: algorithmic flops per cell-update
+    # counted on the oracle's own code
+    step_ms_full = st_full["ms_step"] / max(1, st_full["step_kernel_launches"])
+    ach_tf = local_cells * flops / (step_ms_full / 1000.0) / 1e12 if flops else None
+    roofline_alu = {"bound": "alu", "achieved": ach_tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": (ach_tf / fp64_peak) if ach_tf else None, "kernel": kernel + " (full update)",
+                    "launch_ms": step_ms_full, "algorithmic_flops_per_cell_update": flops,
+                    "peak_source": "derived: 148 SMs x 64 fp64 FMA lanes x 2 flops x sm_max_mhz "
+                                   f"({pk.get('sm_max_mhz', 1965.0)} MHz, {pk_src} MEASURED_PEAKS.json)",
+                    "flops_source": "profiles/algorithmic_flops.json (oracle's own ops, tools/count_flops.py)"}
 
     # ---- end-to-end through the public API with host buffers ----
     e2e = None
@@ -318,9 +367,12 @@ def main():
                            "parallelism": f"morton-shard x{world}" + (" (NCCL halo)" if world > 1 else ""),
                            "l2": "state 2 x %.2f GB >> 126 MB L2 (no flush needed)" % (P * w.meqn * (w.m + 4) ** 2 * 8 / 1e9),
                            "dt_policy": "Clawpack variable dt (0.9 / CFL)", "final_cfl": cfls[-1]},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "roofline_alu_full_update": roofline_alu,
+                "value_full_update": value_full, "ms_per_step_full_update": ms_full / args.steps,
+                "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": st["kernel_launches"],
-                "phase_ms_per_step": {"ghost": ghost_ms, "update": step_ms, "cfl_allreduce": st["ms_comm"] / max(1, st["steps"])},
+                "phase_ms_per_step": {"ghost": ghost_ms, "update": step_ms, "cfl_allreduce": st["ms_comm"] / max(1, st["steps"]),
+                                      "update_full": step_ms_full},
                 "clocks": clk}
         print(json.dumps(line), flush=True)
     f.close()

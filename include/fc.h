@@ -91,6 +91,9 @@ typedef struct {
   int32_t method2;              /* 1: first order; 2: + limited second-order corrections */
   int32_t method3;              /* 0: no transverse; 1: transverse of A+-dq; 2: also of the corrections */
   double cfl_reject;            /* fc_step rejects (FC_ECFL) when max CFL exceeds this (e.g. 1.0) */
+  int32_t skip_quiescent;       /* 1: exact shortcut for tiles whose 2-cell-haloed window holds one
+                                   uniform state (all waves are exactly 0, so q_new = q bitwise and only
+                                   the CFL is evaluated); 0: always run the full update */
 } fc_problem;
 
 typedef struct {

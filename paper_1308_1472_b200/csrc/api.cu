@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -26,7 +27,12 @@ int launch_scatter(const double* src, double* q, int64_t P, int meqn, int m, cud
 int launch_gather(const double* q, double* dst, int64_t P, int meqn, int m, cudaStream_t st);
 int launch_step(int kind, const double* qold, double* qnew, const double* aux, const int8_t* level,
                 int64_t npatch, int m, double dt, double dx0, double p0, double p1, int limiter,
-                int method2, int method3, unsigned long long* cfl_bits, cudaStream_t st);
+                int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
+                const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits, cudaStream_t st);
+int launch_filter(int kind, const double* qold, double* qnew, int npatch, int m, uint8_t* uflag, double* uval,
+                  const int32_t* nbr, const uint8_t* negmask, const int8_t* level, double dt, double dx0,
+                  double p0, double p1, int32_t* active, int32_t* nactive, unsigned long long* cfl_bits,
+                  cudaStream_t st);
 }  // namespace fc
 
 using namespace fc;
@@ -69,6 +75,15 @@ struct fc_forest {
   unsigned long long* d_cfl = nullptr;
   double* h_cfl = nullptr;
   DevList copy, avg, bcx, bcy, corner3;
+  // fused ring gather (uniform same-level forests, one tile per patch): ring never written
+  bool fused = false;
+  int32_t* d_ring = nullptr;
+  uint8_t* d_bcflag = nullptr;
+  // quiescent-patch filter (fused path): neighbour table, wall mask, flags, states, active list
+  int32_t *d_nbr = nullptr, *d_active = nullptr, *d_nactive = nullptr;
+  uint8_t *d_negmask = nullptr, *d_uflag = nullptr;
+  double* d_uval = nullptr;
+  int32_t h_nactive = 0;
   std::vector<DevList> interp, bcx_l, bcy_l;
   fc_problem prob{};
   bool has_problem = false, has_q = false, has_aux = false;
@@ -240,6 +255,9 @@ static void destroy(fc_forest* f) {
     cudaSetDevice(f->device);
     if (f->stream) cudaStreamSynchronize(f->stream);
     cudaFree(f->qold); cudaFree(f->qnew); cudaFree(f->aux); cudaFree(f->d_level); cudaFree(f->d_cfl);
+    cudaFree(f->d_ring); cudaFree(f->d_bcflag);
+    cudaFree(f->d_nbr); cudaFree(f->d_active); cudaFree(f->d_nactive); cudaFree(f->d_negmask);
+    cudaFree(f->d_uflag); cudaFree(f->d_uval);
     if (f->h_cfl) cudaFreeHost(f->h_cfl);
     free_list(f->copy); free_list(f->avg); free_list(f->bcx); free_list(f->bcy); free_list(f->corner3);
     for (auto& l : f->interp) free_list(l);
@@ -336,6 +354,32 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
       return fail(rc, m);
     }
   }
+  // fused ring gather: every ghost record COPY/BC and one 2-tile-free patch per tile (m <= 16)
+  {
+    const int T = (pl.m % 16 == 0) ? 16 : ((pl.m % 8 == 0) ? 8 : ((pl.m % 4 == 0) ? 4 : 2));
+    const char* env = getenv("FC_FUSED_RING");
+    const bool allow = !env || atoi(env) != 0;
+    if (allow && pl.uniform_same && T == pl.m) {
+      RingSources rs;
+      rc = plan_ring_sources(f->pl, pl.meqn, rs, err);
+      if (rc) { destroy(f); return fail(rc, err); }
+      if ((e = cudaMalloc(&f->d_ring, rs.src.size() * sizeof(int32_t))) != cudaSuccess) return cuda_fail(e, "cudaMalloc ring");
+      if ((e = cudaMalloc(&f->d_bcflag, std::max<size_t>(1, rs.bcflag.size()))) != cudaSuccess) return cuda_fail(e, "cudaMalloc bcflag");
+      cudaMemcpy(f->d_ring, rs.src.data(), rs.src.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+      cudaMemcpy(f->d_bcflag, rs.bcflag.data(), rs.bcflag.size(), cudaMemcpyHostToDevice);
+      const size_t Pl1 = std::max<int64_t>(1, f->Pl);
+      if ((e = cudaMalloc(&f->d_nbr, Pl1 * 8 * sizeof(int32_t))) != cudaSuccess ||
+          (e = cudaMalloc(&f->d_active, Pl1 * sizeof(int32_t))) != cudaSuccess ||
+          (e = cudaMalloc(&f->d_nactive, sizeof(int32_t))) != cudaSuccess ||
+          (e = cudaMalloc(&f->d_negmask, Pl1)) != cudaSuccess || (e = cudaMalloc(&f->d_uflag, Pl1)) != cudaSuccess ||
+          (e = cudaMalloc(&f->d_uval, Pl1 * pl.meqn * sizeof(double))) != cudaSuccess)
+        return cuda_fail(e, "cudaMalloc filter");
+      cudaMemcpy(f->d_nbr, rs.nbr.data(), rs.nbr.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+      cudaMemcpy(f->d_negmask, rs.negmask.data(), rs.negmask.size(), cudaMemcpyHostToDevice);
+      f->fused = true;
+      f->st.uniform_fast_path = 1;
+    }
+  }
   if (pl.nranks > 1) {
     rc = setup_halo(f, d->nccl_id);
     if (rc) { std::string m = g_err; destroy(f); return fail(rc, m); }
@@ -361,6 +405,7 @@ int fc_set_problem(fc_forest* f, const fc_problem* pr) {
   if ((pr->kind == FC_SWE_ROE || pr->kind == FC_EULER_ROE) && !(pr->p0 > 0.0))
     return fail(FC_EINVAL, "g / gamma must be positive");
   if (pr->kind == FC_EULER_ROE && !(pr->p0 > 1.0)) return fail(FC_EINVAL, "gamma must exceed 1");
+  if (pr->skip_quiescent != 0 && pr->skip_quiescent != 1) return fail(FC_EINVAL, "skip_quiescent must be 0 or 1");
   f->prob = *pr;
   f->has_problem = true;
   return FC_OK;
@@ -499,13 +544,31 @@ int fc_step(fc_forest* f, double dt, double* max_cfl) {
   if (!(dt > 0.0) || !std::isfinite(dt)) return fail(FC_EINVAL, "dt must be positive and finite");
   CK(cudaSetDevice(f->device));
   if (f->timing) CK(cudaEventRecord(f->ev[0], f->stream));
-  int rc = ghost_fill_internal(f);
+  // fused ring gather + quiescent filter when skipping is on (rings never written); otherwise the
+  // ghost kernels fill the rings and every tile is bulk-copied whole (faster for the full update)
+  const bool use_fused = f->fused && f->prob.skip_quiescent && f->prob.kind != FC_ADV_EDGEVEL_CAPA;
+  int rc = use_fused ? halo_round(f, 0) : ghost_fill_internal(f);
   if (rc) return rc;
   if (f->timing) CK(cudaEventRecord(f->ev[1], f->stream));
   CK(cudaMemsetAsync(f->d_cfl, 0, sizeof(unsigned long long), f->stream));
   const fc_problem& p = f->prob;
+  // fused path + quiescent skipping: copy/classify + activity filter, then the step over the
+  // active patches only (the in-kernel window check is then redundant)
+  bool filtered = false;
+  if (use_fused) {
+    CK(cudaMemsetAsync(f->d_nactive, 0, sizeof(int32_t), f->stream));
+    const int fr = launch_filter(p.kind, f->qold, f->qnew, (int)f->Pl, f->pl.m, f->d_uflag, f->d_uval, f->d_nbr,
+                                 f->d_negmask, f->d_level, dt, f->pl.dx0, p.p0, p.p1, f->d_active, f->d_nactive,
+                                 f->d_cfl, f->stream);
+    if (fr > 0) {
+      f->st.kernel_launches += fr;
+      filtered = true;
+    }
+  }
   int lr = launch_step(p.kind, f->qold, f->qnew, f->aux, f->d_level, f->Pl, f->pl.m, dt, f->pl.dx0,
-                       p.p0, p.p1, p.limiter, p.method2, p.method3, f->d_cfl, f->stream);
+                       p.p0, p.p1, p.limiter, p.method2, p.method3, filtered ? 0 : p.skip_quiescent,
+                       use_fused ? f->d_ring : nullptr, f->d_bcflag, filtered ? f->d_active : nullptr,
+                       filtered ? f->d_nactive : nullptr, f->d_cfl, f->stream);
   if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
   f->st.kernel_launches += lr;
   f->st.step_kernel_launches += lr;

@@ -84,9 +84,23 @@ struct Plan {
   int lmin_local = 0, lmax_local = 0;
 };
 
+// Fused ring gather (forests whose ghost records are all COPY / BCX / BCY, one tile per patch):
+// per local patch, G entries in ring storage order: >= 0 = source offset of component 0 (local or
+// halo slot, as in the ghost lists); < 0 = -1 - ((window_src << 3) | (negated_comp << 1) | is_y)
+// for a physical-boundary cell filled from the patch's own window.  bcflag[p]: bit 0 BCX, bit 1 BCY.
+struct RingSources {
+  std::vector<int32_t> src;
+  std::vector<uint8_t> bcflag;
+  // activity test: the <= 8 distinct patches the ring reads (local ids; -2 = a remote patch,
+  // -1 = unused) and a mask of components a wall negates (they must vanish for a quiescent patch)
+  std::vector<int32_t> nbr;     // [Pl][8]
+  std::vector<uint8_t> negmask; // [Pl]
+};
+
 // planner entry points (plan.cpp); return FC_OK or an FC_E* code with err set
 int plan_build(const fc_forest_desc* d, Plan& pl, std::string& err);
 // build typed lists for `meqn` (component stride n^2); halo slots from pl.halo
 int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err);
+int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& err);
 
 }  // namespace fc

@@ -460,4 +460,53 @@ int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err) {
   return FC_OK;
 }
 
+int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& err) {
+  const int m = pl.m, n = pl.n;
+  const int64_t n2 = (int64_t)n * n, S = (int64_t)meqn * n2;
+  const int64_t Pl = pl.p1 - pl.p0, G = n2 - (int64_t)m * m;
+  rs.src.assign((size_t)Pl * G, 0);
+  rs.bcflag.assign((size_t)Pl, 0);
+  rs.nbr.assign((size_t)Pl * 8, -1);
+  rs.negmask.assign((size_t)Pl, 0);
+  for (int64_t lp = 0; lp < Pl; ++lp) {
+    int nn = 0;
+    auto add_nbr = [&](int32_t id) {
+      for (int k = 0; k < nn; ++k)
+        if (rs.nbr[lp * 8 + k] == id) return true;
+      if (nn >= 8) return false;
+      rs.nbr[lp * 8 + nn++] = id;
+      return true;
+    };
+    for (int64_t r = 0; r < G; ++r) {
+      const int32_t* o = pl.table.data() + (lp * G + r) * REC;
+      int32_t v;
+      if (o[0] == OP_COPY) {
+        const int64_t cell = (int64_t)(o[3] + 1) * n + (o[2] + 1);
+        const int64_t q = o[1];
+        if (!add_nbr((q >= pl.p0 && q < pl.p1) ? (int32_t)(q - pl.p0) : -2)) { err = "more than 8 ring neighbours"; return FC_EUNSUP; }
+        if (q >= pl.p0 && q < pl.p1) {
+          v = (int32_t)((q - pl.p0) * S + cell);
+        } else {
+          auto it = pl.halo.slot.find((q * n2 + cell) * 2);
+          if (it == pl.halo.slot.end()) { err = "missing halo slot"; return FC_EINVAL; }
+          const int64_t h = it->second;
+          v = (int32_t)((Pl + h / n2) * S + h % n2);
+        }
+      } else if (o[0] == OP_BCX || o[0] == OP_BCY) {
+        const int win = (o[3] + 1) * n + (o[2] + 1);
+        const int isy = o[0] == OP_BCY;
+        const int neg = (o[4] == FC_BC_WALL && meqn >= 3) ? (isy ? 2 : 1) : 0;
+        v = -1 - ((win << 3) | (neg << 1) | isy);
+        rs.bcflag[lp] |= (uint8_t)(isy ? 2 : 1);
+        if (neg) rs.negmask[lp] |= (uint8_t)(1u << neg);
+      } else {
+        err = "ring gather needs COPY/BC records only";
+        return FC_EUNSUP;
+      }
+      rs.src[lp * G + r] = v;
+    }
+  }
+  return FC_OK;
+}
+
 }  // namespace fc

@@ -36,6 +36,11 @@ struct AuxCell {
 
 __device__ __forceinline__ double dmin0(double s) { return s < 0.0 ? s : 0.0; }
 __device__ __forceinline__ double dmax0(double s) { return s > 0.0 ? s : 0.0; }
+// (min(s,0), max(s,0)) with one compare: the negative part is s - max(s,0), exact
+__device__ __forceinline__ void split0(double s, double& sm, double& sp) {
+  sp = s > 0.0 ? s : 0.0;
+  sm = s - sp;
+}
 
 // 1/x: SFU seed (MUFU.RCP64H, ~2^-22) + two Newton steps -> ~1 ulp (x normal, nonzero)
 __device__ __forceinline__ double fast_rcp(double x) {
@@ -59,9 +64,16 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
 }
 
 // ----------------------------------------------------------------------------------------------
+// CFL of a tile whose staged window holds one uniform state q (component stride qs): the max over
+// the tile's edges of max(r s, -r s) over the waves, which for a uniform state is r (|u_n| + c).
+// Block-uniform result (every thread returns the same value, or its share for AdvEdgeCapa).
 struct AdvConst {
   static constexpr int MEQN = 1, MW = 1, NS = 1, NC = 0;
   static constexpr bool CAPA = false;
+  __device__ static double quiescent_cfl(const double*, int, const SolverParams& P, const double*, double dtdx,
+                                         int, int, int, int) {
+    return dtdx * fmax(fabs(P.p0), fabs(P.p1));
+  }
   __device__ static void precompute(const double*, int, const SolverParams&, double*, int) {}
   template <int D>
   __device__ static void riemann(const double* ql, const double* qr, const double*, const double*,
@@ -96,6 +108,22 @@ struct AdvConst {
 struct AdvEdgeCapa {
   static constexpr int MEQN = 1, MW = 1, NS = 1, NC = 0;
   static constexpr bool CAPA = true;
+  // edge velocities vary per edge: each thread scans a share of the tile's x- and y-edges
+  __device__ static double quiescent_cfl(const double*, int WW, const SolverParams&, const double* sa,
+                                         double dtdx, int T, int W, int tid, int NT) {
+    double c = 0.0;
+    for (int e = tid; e < (T + 1) * (T + 2); e += NT) {
+      const int i = 1 + e % (T + 1), j = e / (T + 1);          // x-edge i of row j
+      const int r = (j + 1) * W + (i + 1);
+      const double s = sa[WW + r];
+      c = fmax(c, fmax(dtdx / sa[r] * s, -dtdx / sa[r - 1] * s));
+      const int ii = e % (T + 2), jj = 1 + e / (T + 2);          // y-edge jj of column ii
+      const int rr = (jj + 1) * W + (ii + 1);
+      const double sy = sa[2 * WW + rr];
+      c = fmax(c, fmax(dtdx / sa[rr] * sy, -dtdx / sa[rr - W] * sy));
+    }
+    return c;
+  }
   __device__ static void precompute(const double*, int, const SolverParams&, double*, int) {}
   template <int D>
   __device__ static void riemann(const double* ql, const double* qr, const double*, const double*,
@@ -136,6 +164,12 @@ struct AdvEdgeCapa {
 struct SweRoe {
   static constexpr int MEQN = 3, MW = 3, NS = 7, NC = 3;
   static constexpr bool CAPA = false;
+  __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, const double*,
+                                         double dtdx, int, int, int, int) {
+    const double h = q[0], ih = 1.0 / h;
+    const double c = sqrt(P.p0 * h);
+    return dtdx * (fmax(fabs(q[qs] * ih), fabs(q[2 * qs] * ih)) + c);
+  }
   // cell fields: sqrt(h), u, v
   __device__ static void precompute(const double* q, int qs, const SolverParams&, double* c, int cs) {
     const double h = q[0];
@@ -211,9 +245,12 @@ struct SweRoe {
     const double b1 = ((vn + c) * X[0] - X[nd]) * i2c;
     const double b2 = X[td] - vt * X[0];
     const double b3 = ((c - vn) * X[0] + X[nd]) * i2c;
-    const double l1 = vn - c, l2 = vn, l3 = vn + c;
-    const double m1 = dmin0(l1) * b1, m2 = dmin0(l2) * b2, m3 = dmin0(l3) * b3;
-    const double p1 = dmax0(l1) * b1, p2 = dmax0(l2) * b2, p3 = dmax0(l3) * b3;
+    double l1m, l1p, l2m, l2p, l3m, l3p;
+    split0(vn - c, l1m, l1p);
+    split0(vn, l2m, l2p);
+    split0(vn + c, l3m, l3p);
+    const double m1 = l1m * b1, m2 = l2m * b2, m3 = l3m * b3;
+    const double p1 = l1p * b1, p2 = l2p * b2, p3 = l3p * b3;
     bm[0] = m1 + m3;
     bm[nd] = m1 * (vn - c) + m3 * (vn + c);
     bm[td] = (m1 + m3) * vt + m2;
@@ -232,6 +269,14 @@ struct SweRoe {
 struct EulerRoe {
   static constexpr int MEQN = 4, MW = 4, NS = 13, NC = 5;
   static constexpr bool CAPA = false;
+  __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, const double*,
+                                         double dtdx, int, int, int, int) {
+    const double rho = q[0], ir = 1.0 / rho;
+    const double u = q[qs] * ir, v = q[2 * qs] * ir;
+    const double p = (P.p0 - 1.0) * (q[3 * qs] - 0.5 * rho * (u * u + v * v));
+    const double c = sqrt(P.p0 * p * ir);
+    return dtdx * (fmax(fabs(u), fabs(v)) + c);
+  }
   // cell fields: sqrt(rho), u, v, H, c
   __device__ static void precompute(const double* q, int qs, const SolverParams& P, double* c, int cs) {
     const double gam = P.p0, gm1 = gam - 1.0;
@@ -354,6 +399,16 @@ struct EulerRoe {
     const double sg = p == 0 ? -1.0 : 1.0;
     W[0] = a; W[nd] = a * (un + sg * c); W[td] = a * vt; W[3] = a * (H + sg * un * c);
   }
+  // A-dq from the scratch (Harten-Hyman fixed), A+dq = sum_p s_p W_p - A-dq
+  template <int D>
+  __device__ static void fluct_w(const double* sc, int st, const double (*W)[4], const double* s,
+                                 double* am, double* ap) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      am[k] = sc[(9 + k) * st];
+      ap[k] = s[0] * W[0][k] + s[1] * W[1][k] + s[2] * W[2][k] + s[3] * W[3][k] - am[k];
+    }
+  }
   template <int D>
   __device__ static void fluct(const double* sc, int st, const SolverParams& P, AuxCell ar,
                                double* am, double* ap) {
@@ -383,11 +438,14 @@ struct EulerRoe {
     const double b2 = gm1 * (ic * ic) * ((H - vn * vn - vt * vt) * X[0] + vn * X[nd] + vt * X[td] - X[3]);
     const double b4 = (X[nd] + (c - vn) * X[0] - c * b2) * (0.5 * ic);
     const double b1 = X[0] - b2 - b4;
-    const double l1 = vn - c, l2 = vn, l4 = vn + c;
     const double ek = 0.5 * (vn * vn + vt * vt);
     // B-X and B+X: sum over waves of min/max(lambda, 0) b r
-    const double m1 = dmin0(l1) * b1, m2 = dmin0(l2) * b2, m3 = dmin0(l2) * b3, m4 = dmin0(l4) * b4;
-    const double p1 = dmax0(l1) * b1, p2 = dmax0(l2) * b2, p3 = dmax0(l2) * b3, p4 = dmax0(l4) * b4;
+    double l1m, l1p, l2m, l2p, l4m, l4p;
+    split0(vn - c, l1m, l1p);
+    split0(vn, l2m, l2p);
+    split0(vn + c, l4m, l4p);
+    const double m1 = l1m * b1, m2 = l2m * b2, m3 = l2m * b3, m4 = l4m * b4;
+    const double p1 = l1p * b1, p2 = l2p * b2, p3 = l2p * b3, p4 = l4p * b4;
     bm[0] = m1 + m2 + m4;
     bm[nd] = m1 * (vn - c) + m2 * vn + m4 * (vn + c);
     bm[td] = (m1 + m2 + m4) * vt + m3;

@@ -26,6 +26,22 @@
 
 namespace fc {
 
+// wave limiters as one branch-free form phi = max(lo, min(c1 + c2 theta, c3, c4 theta)):
+//   MC     (lo, c1, c2, c3, c4) = (0, 1/2, 1/2, 2, 2)   -> max(0, min((1+t)/2, 2, 2t))
+//   minmod                        (0, 1,   0,   1, 1)   -> max(0, min(1, t))
+//   none                          (1, 1,   0,   1, 1)   -> 1
+struct LimiterCoef {
+  double lo, c1, c2, c3, c4;
+};
+__host__ __device__ inline LimiterCoef limiter_coef(int lim) {
+  if (lim == 2) return {0.0, 0.5, 0.5, 2.0, 2.0};
+  if (lim == 1) return {0.0, 1.0, 0.0, 1.0, 1.0};
+  return {1.0, 1.0, 0.0, 1.0, 1.0};
+}
+__device__ __forceinline__ double limiter_phi(const LimiterCoef& L, double th) {
+  return fmax(L.lo, fmin(fmin(fma(L.c2, th, L.c1), L.c3), L.c4 * th));
+}
+
 struct StepArgs {
   const double* __restrict__ qold;
   double* __restrict__ qnew;
@@ -34,15 +50,15 @@ struct StepArgs {
   double dt, dx0;
   SolverParams sp;
   int limiter, method2, method3;
+  int skip_quiescent;                 // exact shortcut for tiles whose staged window is uniform
+  const int32_t* __restrict__ ring;   // fused ring gather (RingSources.src) or null: ring in q_old
+  const uint8_t* __restrict__ bcflag; // per patch: bit 0 BCX, bit 1 BCY entries present
+  const int32_t* __restrict__ active; // active-patch list (quiescent patches filtered out) or null
+  const int32_t* __restrict__ nactive;
+  LimiterCoef lim;
   int m, tiles;                       // tiles per side
   unsigned long long* cfl_bits;
 };
-
-__device__ __forceinline__ double limiter_phi(int lim, double th) {
-  if (lim == 2) return fmax(0.0, fmin(fmin(0.5 * (1.0 + th), 2.0), 2.0 * th));
-  if (lim == 1) return fmax(0.0, fmin(1.0, th));
-  return 1.0;
-}
 
 // ---- TMA bulk copies + mbarrier (sm_90+ / sm_100a) -------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -75,6 +91,13 @@ __device__ __forceinline__ int opaque(int x) {
   asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
   return y;
 }
+// 8-byte async global -> shared copy (LDGSTS), completion tracked with cp.async groups
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 template <class S, int T>
@@ -90,34 +113,63 @@ struct StepShape {
   static constexpr size_t smem_bytes = smem_doubles * sizeof(double);
 };
 
+// default A-+dq from the waves: sum_p min/max(s_p, 0) W_p (Euler overrides: Harten-Hyman A-dq)
+template <class S, int D, class = void>
+struct FluctFromWaves {
+  __device__ static void run(const double*, int, const double (*W)[S::MEQN], const double* s, double* am,
+                             double* ap) {
+#pragma unroll
+    for (int k = 0; k < S::MEQN; ++k) { am[k] = 0.0; ap[k] = 0.0; }
+#pragma unroll
+    for (int p = 0; p < S::MW; ++p) {
+      double sm, sp;
+      split0(s[p], sm, sp);
+#pragma unroll
+      for (int k = 0; k < S::MEQN; ++k) { am[k] = fma(sm, W[p][k], am[k]); ap[k] = fma(sp, W[p][k], ap[k]); }
+    }
+  }
+};
+template <int D>
+struct FluctFromWaves<EulerRoe, D, void> {
+  __device__ static void run(const double* sc, int st, const double (*W)[4], const double* s, double* am,
+                             double* ap) {
+    EulerRoe::fluct_w<D>(sc, st, W, s, am, ap);
+  }
+};
+
 // fluctuations + second-order correction F~ (limiter on the upwind neighbour's unlimited wave)
-// + CFL of one edge (phase 2 of a sweep)
+// + CFL of one edge (phase 2 of a sweep).  Waves are reconstructed once; the limiter is
+// branch-free (a zero wave contributes c phi W = 0 whatever phi is).
 template <class S, int D>
 __device__ __forceinline__ void edge_correction(const double* sc, const double* scm, const double* scp,
                                                 int st, const StepArgs& A, AuxCell ar, double rl, double rr,
                                                 double& cfl, double* am, double* ap, double* F) {
   constexpr int MEQN = S::MEQN;
-  S::template fluct<D>(sc, st, A.sp, ar, am, ap);
-#pragma unroll
-  for (int k = 0; k < MEQN; ++k) F[k] = 0.0;
-  const double rav = 0.5 * (rl + rr);
+  double W[S::MW][MEQN], s[S::MW];
 #pragma unroll
   for (int p = 0; p < S::MW; ++p) {
-    const double s = S::template speed<D>(sc, st, p, A.sp, ar);
-    cfl = fmax(cfl, fmax(rr * s, -rl * s));
-    if (A.method2 == 2) {
-      double Wp[MEQN], WI[MEQN];
-      S::template wave<D>(sc, st, p, A.sp, Wp);
-      S::template wave<D>(s > 0.0 ? scm : scp, st, p, A.sp, WI);
-      double wn2 = 0.0, dot = 0.0;
+    S::template wave<D>(sc, st, p, A.sp, W[p]);
+    s[p] = S::template speed<D>(sc, st, p, A.sp, ar);
+    cfl = fmax(cfl, fmax(rr * s[p], -rl * s[p]));
+  }
+  FluctFromWaves<S, D>::run(sc, st, W, s, am, ap);
 #pragma unroll
-      for (int k = 0; k < MEQN; ++k) { wn2 = fma(Wp[k], Wp[k], wn2); dot = fma(WI[k], Wp[k], dot); }
-      if (wn2 != 0.0) {
-        const double phi = limiter_phi(A.limiter, dot * fast_rcp(wn2));
-        const double as = fabs(s);
+  for (int k = 0; k < MEQN; ++k) F[k] = 0.0;
+  if (A.method2 == 2) {
+    const double rav = 0.5 * (rl + rr);
+#pragma unroll
+    for (int p = 0; p < S::MW; ++p) {
+      double WI[MEQN];
+      S::template wave<D>(s[p] > 0.0 ? scm : scp, st, p, A.sp, WI);
+      double wn2 = W[p][0] * W[p][0], dot = WI[0] * W[p][0];
+#pragma unroll
+      for (int k = 1; k < MEQN; ++k) { wn2 = fma(W[p][k], W[p][k], wn2); dot = fma(WI[k], W[p][k], dot); }
+      if (wn2 != 0.0) {   // a zero wave adds nothing (also skips the limiter in quiescent flow)
+        const double phi = limiter_phi(A.lim, dot * fast_rcp(wn2));
+        const double as = fabs(s[p]);
         const double c = 0.5 * as * (1.0 - as * rav) * phi;
 #pragma unroll
-        for (int k = 0; k < MEQN; ++k) F[k] = fma(c, Wp[k], F[k]);
+        for (int k = 0; k < MEQN; ++k) F[k] = fma(c, W[p][k], F[k]);
       }
     }
   }
@@ -138,15 +190,33 @@ __device__ __forceinline__ void edge_transverse(const double* sc, int st, const 
 // issue the bulk copies staging tile `tile` (q window + aux window) into buf, on barrier bar.
 // Called by all 32 lanes of warp 0: lane 0 arms the barrier, the lanes split the row copies.
 template <class S, int T>
-__device__ __forceinline__ void stage_tile(const StepArgs& A, int64_t tile, double* buf, uint64_t* bar,
+__device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* buf, uint64_t* bar,
                                            int lane) {
   using Sh = StepShape<S, T>;
   constexpr int MEQN = S::MEQN, W = Sh::W, WW = Sh::WW;
-  const int tiles2 = A.tiles * A.tiles;
-  const int64_t patch = tile / tiles2;
-  const int t = (int)(tile - patch * tiles2);
-  const int tx = t % A.tiles, ty = t / A.tiles;
+  int patch = tile, tx = 0, ty = 0;
+  if (A.tiles > 1) {
+    const int tiles2 = A.tiles * A.tiles;
+    patch = tile / tiles2;
+    const int t = tile - patch * tiles2;
+    ty = t / A.tiles;
+    tx = t - ty * A.tiles;
+  }
   const int n = A.m + 4, n2 = n * n;
+  if (A.ring) {              // fused ring gather: the TMA brings the m x m interior rows only
+    constexpr uint32_t qbytes = (uint32_t)MEQN * T * T * sizeof(double);
+    constexpr uint32_t abytes = S::CAPA ? (uint32_t)3 * WW * sizeof(double) : 0u;
+    if (lane == 0) mbar_expect_tx(bar, qbytes + abytes);
+    __syncwarp();
+    const double* qb = A.qold + (int64_t)patch * MEQN * n2;
+#pragma unroll 1
+    for (int r = lane; r < MEQN * T; r += 32) {
+      const int k = r / T, row = r - k * T;
+      bulk_g2s(buf + k * WW + (row + 2) * W + 2, qb + (int64_t)k * n2 + (row + 2) * n + 2, T * sizeof(double), bar);
+    }
+    if (S::CAPA && lane == 0) bulk_g2s(buf + MEQN * WW, A.aux + (int64_t)patch * 3 * n2, abytes, bar);
+    return;
+  }
   constexpr uint32_t bytes = (uint32_t)Sh::BUF * sizeof(double);
   if (lane == 0) mbar_expect_tx(bar, bytes);
   __syncwarp();
@@ -171,13 +241,65 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int64_t tile, doub
   }
 }
 
+// window index (padded index, W = n) of ring cell r in ring storage order (j = -1..m+2 outer,
+// i = -1..m+2 inner, interior skipped)
+template <int T>
+__device__ __forceinline__ int ring_window_index(int r) {
+  constexpr int n = T + 4;
+  if (r < 2 * n) return r;                                   // rows j = -1, 0
+  r -= 2 * n;
+  if (r < 4 * T) {                                           // rows 1..m: i = -1, 0, m+1, m+2
+    const int j = r / 4 + 1, c = r % 4;
+    const int i = c < 2 ? c - 1 : T + c - 1;
+    return (j + 1) * n + (i + 1);
+  }
+  r -= 4 * T;
+  return (T + 2) * n + r;                                    // rows j = m+1, m+2
+}
+
+// issue the cp.async copies of the ring cells of `tile` (COPY sources) into buf; one group
+template <class S, int T, int NT>
+__device__ __forceinline__ void gather_ring(const StepArgs& A, int tile, double* buf) {
+  using Sh = StepShape<S, T>;
+  constexpr int MEQN = S::MEQN, WW = Sh::WW, G = WW - T * T;
+  const int n2 = WW;
+  const int32_t* rs = A.ring + (int64_t)tile * G;
+  for (int e = opaque(threadIdx.x); e < G * MEQN; e += NT) {
+    const int k = e / G, r = e - k * G;
+    const int32_t v = __ldg(rs + r);
+    if (v >= 0) cp_async8(buf + k * WW + ring_window_index<T>(r), A.qold + v + (int64_t)k * n2);
+  }
+}
+
+// physical-boundary ring cells of the staged window, x faces (is_y = 0) then y faces (is_y = 1)
+template <class S, int T, int NT>
+__device__ __forceinline__ void window_bc(const StepArgs& A, int tile, double* sq, int is_y) {
+  using Sh = StepShape<S, T>;
+  constexpr int MEQN = S::MEQN, WW = Sh::WW, G = WW - T * T;
+  const int32_t* rs = A.ring + (int64_t)tile * G;
+  for (int r = opaque(threadIdx.x); r < G; r += NT) {
+    const int32_t v = __ldg(rs + r);
+    if (v >= 0) continue;
+    const int code = -1 - v;
+    if ((code & 1) != is_y) continue;
+    const int src = code >> 3, neg = (code >> 1) & 3, dst = ring_window_index<T>(r);
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) {
+      const double x = sq[k * WW + src];
+      sq[k * WW + dst] = (neg != 0 && k == neg) ? -x : x;
+    }
+  }
+}
+
 // Persistent CTAs: each loops over tiles blockIdx.x, + gridDim.x, ...; the next tile's window is
 // bulk-copied (TMA engine) into the other staging buffer while the current one is computed.
 template <class S, int T, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int64_t ntiles) {
+__global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int ntiles) {
   using Sh = StepShape<S, T>;
   constexpr int MEQN = S::MEQN, W = Sh::W, WW = Sh::WW, EX = Sh::EX, E2 = Sh::E2;
   static_assert(E2 <= NT, "one round of corrections per sweep (single-writer L/R phases)");
+  if (A.active) ntiles = *A.nactive;   // tiles of the active list only (tile = patch)
+  auto tile_of = [&](int k) { return A.active ? A.active[k] : k; };
   extern __shared__ __align__(128) double sm[];
   double* sbuf = sm;                                 // 2 x [MEQN + 3 aux][W][W] staging buffers
   double* scl = sbuf + 2 * Sh::BUF;                  // [NC][W][W] per-cell derived fields
@@ -197,32 +319,73 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int64_t ntiles) {
     fence_proxy_async();
   }
   __syncthreads();
-  if (tid < 32 && (int64_t)blockIdx.x < ntiles) stage_tile<S, T>(A, blockIdx.x, sbuf, &bars[0], tid);
+  if (tid < 32 && (int)blockIdx.x < ntiles) stage_tile<S, T>(A, tile_of(blockIdx.x), sbuf, &bars[0], tid);
+  if (A.ring) {
+    if ((int)blockIdx.x < ntiles) gather_ring<S, T, NT>(A, tile_of(blockIdx.x), sbuf);
+    cp_async_commit();
+  }
   uint32_t phase = 0;   // bit b = parity to wait for on buffer b
   double cfl = 0.0;
   bool bad = false;
 
   int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+  for (int kt = blockIdx.x; kt < ntiles; kt += gridDim.x, ++it) {
     const int b = it & 1;
-    const int64_t next = tile + gridDim.x;
-    if (tid < 32 && next < ntiles) {   // the other buffer was released by the previous tile's last barrier
+    const int tile = tile_of(kt);
+    const int knext = kt + gridDim.x;
+    if (tid < 32 && knext < ntiles) {  // the other buffer was released by the previous tile's last barrier
       fence_proxy_async();
-      stage_tile<S, T>(A, next, sbuf + (b ^ 1) * Sh::BUF, &bars[b ^ 1], tid);
+      stage_tile<S, T>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF, &bars[b ^ 1], tid);
+    }
+    if (A.ring) {                      // this thread's ring cells of the next tile: one cp.async group
+      if (knext < ntiles) gather_ring<S, T, NT>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF);
+      cp_async_commit();
     }
     double* sq = sbuf + b * Sh::BUF;                 // [MEQN][W][W]
     double* sa = sq + MEQN * WW;                     // [3][W][W] aux (capacity form)
-    const int64_t patch = tile / tiles2;
-    const int tt = (int)(tile - patch * tiles2);
-    const int tx = tt % A.tiles, ty = tt / A.tiles;
+    int patch = tile, tx = 0, ty = 0;
+    if (A.tiles > 1) {
+      patch = tile / tiles2;
+      const int tt = tile - patch * tiles2;
+      ty = tt / A.tiles;
+      tx = tt - ty * A.tiles;
+    }
     const double dx = ldexp(A.dx0, -(int)A.level[patch]);
     const double dtdx = A.dt / dx;   // square cells: dt/dy = dt/dx
     mbar_wait(&bars[b], (phase >> b) & 1u);
     phase ^= 1u << b;
+    if (A.ring) {                      // this tile's ring: wait for all but the newest group,
+      cp_async_wait<1>();              // make every thread's copies visible, then the BCs
+      __syncthreads();
+      const uint8_t bc = A.bcflag[patch];
+      if (bc & 1) { window_bc<S, T, NT>(A, tile, sq, 0); __syncthreads(); }
+      if (bc & 2) { window_bc<S, T, NT>(A, tile, sq, 1); __syncthreads(); }
+    }
 
     auto widx = [](int i, int j) { return (j + 1) * W + (i + 1); };   // tile-local 1-based cell
     auto auxc = [&](int i, int j) { return AuxCell{sa + widx(i, j), WW}; };
     auto rcell = [&](int i, int j) { return S::CAPA ? dtdx / sa[widx(i, j)] : dtdx; };
+
+    // Quiescent tile: if every staged cell (interior + 2-cell halo) holds the same state, every
+    // Riemann problem of the tile has a zero jump, so all waves, fluctuations, corrections and
+    // transverse terms are exactly 0 and q_new = q bitwise (the oracle computes q - 0 - 0).  Only
+    // the CFL remains: the max over the tile's edges of the wave speeds, taken from the state.
+    if (A.skip_quiescent) {
+      bool diff = false;
+      for (int t = opaque(threadIdx.x); t < MEQN * WW; t += NT) diff |= sq[t] != sq[(t / WW) * WW];
+      if (!__syncthreads_or(diff)) {
+        cfl = fmax(cfl, S::quiescent_cfl(sq, WW, A.sp, sa, dtdx, T, W, opaque(threadIdx.x), NT));
+        const int t = opaque(threadIdx.x);
+        if (t < T * T) {
+          const int i = 1 + t % T, j = 1 + t / T;
+          double* o = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + 1 + j) * n + tx * T + 1 + i;
+#pragma unroll
+          for (int k = 0; k < MEQN; ++k) o[(int64_t)k * n2] = sq[k * WW];
+        }
+        __syncthreads();
+        continue;
+      }
+    }
 
     if (S::NC > 0) {
       const int tid = opaque(threadIdx.x);
@@ -276,6 +439,9 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int64_t ntiles) {
       }
     }
     __syncthreads();
+    // =============================== y-sweep ===============================
+    // X3 (fold the x-sweep's transverse G~ into dq) shares this phase with the y Riemann solves:
+    // it reads ta/tb and updates dq, Y1 reads sq/scl and writes scr, so no barrier between them.
     // X3: G~(i, j+1/2) = up(i, j) + dn(i, j+1)
     for (int t = opaque(threadIdx.x); t < T * T; t += NT) {
       const int i = 1 + t % T, j = 1 + t / T;
@@ -289,8 +455,6 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int64_t ntiles) {
         dq[(k * T + (j - 1)) * T + (i - 1)] -= s * (gt - gb);
       }
     }
-    __syncthreads();
-    // =============================== y-sweep ===============================
     for (int e = opaque(threadIdx.x); e < EX; e += NT) {       // column i, edge j (cells j-1 | j)
       const int i = e % (T + 2), j = e / (T + 2);
       double ql[MEQN], qr[MEQN];
@@ -377,6 +541,138 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int64_t ntiles) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// Quiescent-patch filter for the fused (ring-gather) path, three kernels per step:
+//   k_copy_classify  q_new interior = q_old interior (streaming, 16-byte accesses) and, per patch,
+//                    "interior uniform" + its state;
+//   k_activity       a patch is quiescent iff it is uniform, every patch its ring reads is uniform
+//                    with the same state, and no wall negates a non-zero component of it: then its
+//                    staged window is uniform, every wave of its update is exactly 0 and q_new = q
+//                    (already copied); its CFL comes from the state.  Others go to the active list;
+//   k_step           over the active list only.
+template <int MEQN, int T>
+__global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict__ qold, double* __restrict__ qnew,
+                                                       int npatch, uint8_t* __restrict__ uflag,
+                                                       double* __restrict__ uval) {
+  constexpr int n = T + 4, n2 = n * n, H = T / 2;      // H = double2 per interior row
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < npatch; p += warps) {
+    const double* src = qold + (int64_t)p * MEQN * n2;
+    double* dst = qnew + (int64_t)p * MEQN * n2;
+    bool diff = false;
+    double v0k = 0.0;
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) {
+      const double v0 = __ldg(src + k * n2 + 2 * n + 2);
+      if (lane == k) v0k = v0;
+#pragma unroll 2
+      for (int e = lane; e < T * H; e += 32) {
+        const int row = e / H, c2 = e - row * H;
+        const int off = k * n2 + (row + 2) * n + 2 + 2 * c2;
+        const double2 x = __ldg(reinterpret_cast<const double2*>(src + off));
+        *reinterpret_cast<double2*>(dst + off) = x;
+        diff |= (x.x != v0) | (x.y != v0);
+      }
+    }
+    const bool uni = !__any_sync(0xffffffffu, diff);
+    if (lane == 0) uflag[p] = uni ? 1 : 0;
+    if (lane < MEQN) uval[(int64_t)p * MEQN + lane] = v0k;
+  }
+}
+
+template <class S>
+__global__ void __launch_bounds__(256) k_activity(int npatch, const uint8_t* __restrict__ uflag,
+                                                  const double* __restrict__ uval, const int32_t* __restrict__ nbr,
+                                                  const uint8_t* __restrict__ negmask, const int8_t* __restrict__ level,
+                                                  double dt, double dx0, SolverParams sp, int32_t* __restrict__ active,
+                                                  int32_t* __restrict__ nactive, unsigned long long* cfl_bits) {
+  constexpr int MEQN = S::MEQN;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  double cfl = 0.0;
+  bool act = false;
+  if (p < npatch) {
+    bool q = uflag[p] != 0;
+    double v[MEQN];
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) v[k] = uval[(int64_t)p * MEQN + k];
+    const uint8_t nm = negmask[p];
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k)
+      if (((nm >> k) & 1) && v[k] != 0.0) q = false;
+#pragma unroll
+    for (int s = 0; s < 8 && q; ++s) {
+      const int32_t o = nbr[(int64_t)p * 8 + s];
+      if (o == -1) continue;
+      if (o < 0 || !uflag[o]) { q = false; break; }
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k)
+        if (uval[(int64_t)o * MEQN + k] != v[k]) q = false;
+    }
+    if (q) {
+      const double dtdx = dt / ldexp(dx0, -(int)level[p]);
+      cfl = S::quiescent_cfl(v, 1, sp, nullptr, dtdx, 0, 0, 0, 1);
+    } else {
+      act = true;
+    }
+  }
+  // warp-aggregated append to the active list
+  const unsigned mask = __ballot_sync(0xffffffffu, act);
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == 0 && mask) base = atomicAdd(nactive, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (act) active[base + __popc(mask & ((1u << lane) - 1u))] = p;
+  if (cfl != cfl) cfl = __longlong_as_double(0x7ff0000000000000ll);
+  for (int o = 16; o > 0; o >>= 1) cfl = fmax(cfl, __shfl_xor_sync(0xffffffffu, cfl, o));
+  __shared__ double wmax[8];
+  if (lane == 0) wmax[threadIdx.x >> 5] = cfl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double c = wmax[0];
+    for (int w = 1; w < 8; ++w) c = fmax(c, wmax[w]);
+    if (c > 0.0) atomicMax(cfl_bits, (unsigned long long)__double_as_longlong(c));
+  }
+}
+
+template <class S>
+static int launch_filter_s(const double* qold, double* qnew, int npatch, int m, uint8_t* uflag, double* uval,
+                           const int32_t* nbr, const uint8_t* negmask, const int8_t* level, double dt,
+                           double dx0, SolverParams sp, int32_t* active, int32_t* nactive,
+                           unsigned long long* cfl_bits, cudaStream_t st) {
+  const int blocks_copy = 148 * 8;
+  switch (m) {
+    case 16: k_copy_classify<S::MEQN, 16><<<blocks_copy, 256, 0, st>>>(qold, qnew, npatch, uflag, uval); break;
+    case 8: k_copy_classify<S::MEQN, 8><<<blocks_copy, 256, 0, st>>>(qold, qnew, npatch, uflag, uval); break;
+    case 4: k_copy_classify<S::MEQN, 4><<<blocks_copy, 256, 0, st>>>(qold, qnew, npatch, uflag, uval); break;
+    default: return -1;
+  }
+  k_activity<S><<<(npatch + 255) / 256, 256, 0, st>>>(npatch, uflag, uval, nbr, negmask, level, dt, dx0, sp,
+                                                       active, nactive, cfl_bits);
+  return 2;
+}
+
+int launch_filter(int kind, const double* qold, double* qnew, int npatch, int m, uint8_t* uflag, double* uval,
+                  const int32_t* nbr, const uint8_t* negmask, const int8_t* level, double dt, double dx0,
+                  double p0, double p1, int32_t* active, int32_t* nactive, unsigned long long* cfl_bits,
+                  cudaStream_t st) {
+  SolverParams sp;
+  sp.p0 = p0;
+  sp.p1 = p1;
+  switch (kind) {
+    case FC_ADV_CONST:
+      return launch_filter_s<AdvConst>(qold, qnew, npatch, m, uflag, uval, nbr, negmask, level, dt, dx0, sp,
+                                       active, nactive, cfl_bits, st);
+    case FC_SWE_ROE:
+      return launch_filter_s<SweRoe>(qold, qnew, npatch, m, uflag, uval, nbr, negmask, level, dt, dx0, sp,
+                                     active, nactive, cfl_bits, st);
+    case FC_EULER_ROE:
+      return launch_filter_s<EulerRoe>(qold, qnew, npatch, m, uflag, uval, nbr, negmask, level, dt, dx0, sp,
+                                       active, nactive, cfl_bits, st);
+  }
+  return -1;   // capacity form: edge-dependent CFL, no patch filter
+}
+
+// ---------------------------------------------------------------------------------------------
 template <class S, int T, int NT, int MINB>
 static int launch_step_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   const size_t smem = StepShape<S, T>::smem_bytes;
@@ -391,8 +687,9 @@ static int launch_step_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
     resident = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int64_t ntiles = npatch * a.tiles * a.tiles;
-  const int64_t grid = ntiles < resident ? ntiles : resident;
-  k_step<S, T, NT, MINB><<<(unsigned)grid, NT, smem, st>>>(a, ntiles);
+  if (ntiles >= (1ll << 31)) return -1;
+  const int64_t grid = ntiles < resident ? ntiles : resident;   // (active list: at most ntiles)
+  k_step<S, T, NT, MINB><<<(unsigned)grid, NT, smem, st>>>(a, (int)ntiles);
   return 1;
 }
 
@@ -416,12 +713,19 @@ static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
 
 int launch_step(int kind, const double* qold, double* qnew, const double* aux, const int8_t* level,
                 int64_t npatch, int m, double dt, double dx0, double p0, double p1, int limiter,
-                int method2, int method3, unsigned long long* cfl_bits, cudaStream_t st) {
+                int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
+                const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits, cudaStream_t st) {
   if (npatch <= 0) return 0;
   StepArgs a;
   a.qold = qold; a.qnew = qnew; a.aux = aux; a.level = level;
   a.dt = dt; a.dx0 = dx0; a.sp.p0 = p0; a.sp.p1 = p1;
   a.limiter = limiter; a.method2 = method2; a.method3 = method3;
+  a.skip_quiescent = skip_quiescent;
+  a.ring = ring;
+  a.bcflag = bcflag;
+  a.active = active;
+  a.nactive = nactive;
+  a.lim = limiter_coef(limiter);
   a.m = m;
   const int T = (m % 16 == 0) ? 16 : ((m % 8 == 0) ? 8 : ((m % 4 == 0) ? 4 : 2));
   a.tiles = m / T;

@@ -50,7 +50,8 @@ class ForestDesc(C.Structure):
 
 class Problem(C.Structure):
     _fields_ = [("kind", C.c_int32), ("p0", C.c_double), ("p1", C.c_double), ("limiter", C.c_int32),
-                ("method2", C.c_int32), ("method3", C.c_int32), ("cfl_reject", C.c_double)]
+                ("method2", C.c_int32), ("method3", C.c_int32), ("cfl_reject", C.c_double),
+                ("skip_quiescent", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -156,8 +157,8 @@ class Forest:
 
     # -- calls -----------------------------------------------------------------------------------
     def set_problem(self, kind, p0=0.0, p1=0.0, limiter=FC_LIM_MC, method2=2, method3=2,
-                    cfl_reject=1.0):
-        pr = Problem(kind, p0, p1, limiter, method2, method3, cfl_reject)
+                    cfl_reject=1.0, skip_quiescent=1):
+        pr = Problem(kind, p0, p1, limiter, method2, method3, cfl_reject, skip_quiescent)
         _check(lib().fc_set_problem(self.h, C.byref(pr)), "fc_set_problem")
 
     def set_aux(self, aux):
@@ -230,21 +231,24 @@ class Forest:
         return out
 
 
-def forest_for(w, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id=None) -> Forest:
+def forest_for(w, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id=None,
+               skip_quiescent: int = 1) -> Forest:
     """Handle for a workloads.Workload, with its problem (and aux, for local patches) set."""
     f = Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0,
                device, rank, nranks, nccl_id)
     if device >= 0:
-        f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject)
+        f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject,
+                      skip_quiescent)
         if w.aux is not None:
             f.set_aux(np.ascontiguousarray(w.aux[f.first:f.first + f.count]))
     return f
 
 
-def run(w, steps: int | None = None, dt_list=None, device: int = 0, f: Forest | None = None):
+def run(w, steps: int | None = None, dt_list=None, device: int = 0, f: Forest | None = None,
+        skip_quiescent: int = 1):
     """Run the workload's dt policy on the GPU (same policy as the oracle's driver).
     Returns (q [P][meqn][m][m], cfls, dts)."""
-    f = f or forest_for(w, device)
+    f = f or forest_for(w, device, skip_quiescent=skip_quiescent)
     f.set_q(np.ascontiguousarray(w.q0[f.first:f.first + f.count]))
     steps = w.steps if steps is None else steps
     dt = w.dt0

@@ -73,11 +73,24 @@ RUNS = [c1(), c2(), c3(level=3, m=32), c5(level=3, m=16), c5(level=2, m=8),
         c1(level=2, m=24, steps=30), c1(level=1, m=20, steps=30), c1(level=1, m=6, steps=30)]
 
 
+@pytest.mark.parametrize("skip", [1, 0], ids=["quiescent_skip", "full_update"])
 @pytest.mark.parametrize("w", RUNS, ids=lambda w: w.name)
-def test_parity_against_oracle(w):
+def test_parity_against_oracle(w, skip):
     qo, co, do = oracle.run(w)
-    qg, cg, dg = fc.run(w, dt_list=do)
+    qg, cg, dg = fc.run(w, dt_list=do, skip_quiescent=skip)
     assert_parity(w, qg, qo, cg, co)
+
+
+@pytest.mark.parametrize("w", [c5(level=3, m=16, steps=40), c3(level=2, m=32, steps=40),
+                               c4_workload(base_level=2, m=16, steps=40)], ids=lambda w: w.name)
+def test_quiescent_shortcut_is_exact(w):
+    """The quiescent-tile shortcut (uniform staged window -> q_new = q, CFL from the state) gives
+    bitwise the same state as the full update, and the same CFLs up to rounding."""
+    _, _, do = oracle.run(w, steps=w.steps)
+    q1, c1_, _ = fc.run(w, dt_list=do, skip_quiescent=1)
+    q0, c0_, _ = fc.run(w, dt_list=do, skip_quiescent=0)
+    np.testing.assert_array_equal(q1, q0)
+    np.testing.assert_allclose(c1_, c0_, rtol=1e-14, atol=0)
 
 
 def test_parity_c2_levels_and_dt_policy_on_gpu():
