@@ -553,30 +553,41 @@ template <int MEQN, int T>
 __global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict__ qold, double* __restrict__ qnew,
                                                        int npatch, uint8_t* __restrict__ uflag,
                                                        double* __restrict__ uval) {
-  constexpr int n = T + 4, n2 = n * n, H = T / 2;      // H = double2 per interior row
+  // One warp per patch.  Per component the padded rows 2..m+1 form one contiguous, 16-byte aligned
+  // block of m*n doubles: it is copied whole (the two ring columns on each side of q_new are
+  // scratch), so every DRAM sector is read and written in full -- no partial-sector
+  // read-modify-write.  Uniformity is tested on the interior columns only.
+  constexpr int n = T + 4, n2 = n * n, RP = n / 2;          // double2 per padded row
+  constexpr int E = MEQN * T * RP, NE = (E + 31) / 32;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < npatch; p += warps) {
-    const double* src = qold + (int64_t)p * MEQN * n2;
-    double* dst = qnew + (int64_t)p * MEQN * n2;
-    bool diff = false;
-    double v0k = 0.0;
+    const double* src = qold + (int64_t)p * MEQN * n2 + 2 * n;
+    double* dst = qnew + (int64_t)p * MEQN * n2 + 2 * n;
+    double2 x[NE];
 #pragma unroll
-    for (int k = 0; k < MEQN; ++k) {
-      const double v0 = __ldg(src + k * n2 + 2 * n + 2);
-      if (lane == k) v0k = v0;
-#pragma unroll 2
-      for (int e = lane; e < T * H; e += 32) {
-        const int row = e / H, c2 = e - row * H;
-        const int off = k * n2 + (row + 2) * n + 2 + 2 * c2;
-        const double2 x = __ldg(reinterpret_cast<const double2*>(src + off));
-        *reinterpret_cast<double2*>(dst + off) = x;
-        diff |= (x.x != v0) | (x.y != v0);
+    for (int u = 0; u < NE; ++u) {
+      const int e = lane + 32 * u;
+      const int k = e / (T * RP), r = e - k * (T * RP);
+      if (e < E) x[u] = __ldcs(reinterpret_cast<const double2*>(src + k * n2) + r);
+    }
+    double v0[MEQN];
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) v0[k] = __ldg(src + k * n2 + 2);
+    bool diff = false;
+#pragma unroll
+    for (int u = 0; u < NE; ++u) {
+      const int e = lane + 32 * u;
+      if (e < E) {
+        const int k = e / (T * RP), r = e - k * (T * RP);
+        __stcs(reinterpret_cast<double2*>(dst + k * n2) + r, x[u]);
+        const int c = r % RP;                               // pair index in the row: 1..RP-2 interior
+        if (c >= 1 && c <= RP - 2) diff |= (x[u].x != v0[k]) | (x[u].y != v0[k]);
       }
     }
     const bool uni = !__any_sync(0xffffffffu, diff);
     if (lane == 0) uflag[p] = uni ? 1 : 0;
-    if (lane < MEQN) uval[(int64_t)p * MEQN + lane] = v0k;
+    if (lane < MEQN) uval[(int64_t)p * MEQN + lane] = v0[lane < MEQN ? lane : 0];
   }
 }
 
