@@ -316,7 +316,9 @@ def main():
     roofline = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach_gbs / hbm_peak,
                 "traffic": prof.get("dram_bytes_per_launch") if prof else None,
-                "kernel": kernel + " (quiescent-tile shortcut on)", "launch_ms": step_ms,
+                "kernel": ("update phase of fc_step: k_copy_classify (dominant: streams q_old -> q_new and "
+                           "classifies patches) + k_activity + " + kernel + " on the active patches"),
+                "launch_ms": step_ms,
                 "algorithmic_bytes_per_cell_update": bpc,
                 "peak_source": f"{pk_src} MEASURED_PEAKS.json hbm_gbs (copy)"}
     # the full update (no shortcut) is bound by the fp64 pipe: algorithmic flops per cell-update
