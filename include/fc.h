@@ -81,7 +81,8 @@ typedef struct {
   double tree_dx0;              /* tree edge length (a level-l cell is tree_dx0 2^-l / m wide) */
   int32_t device;               /* CUDA device ordinal; -1 = host-only planning handle (tables only) */
   int32_t rank, nranks;         /* this process among nranks (1 = single GPU) */
-  const void* nccl_id;          /* 128-byte ncclUniqueId when nranks > 1 (fc_nccl_unique_id on rank 0) */
+  const void* nccl_id;          /* 128-byte ncclUniqueId when nranks > 1 (fc_nccl_unique_id on rank 0);
+                                   NULL with nranks > 1 selects the manual halo transport (below) */
 } fc_forest_desc;
 
 typedef struct {
@@ -180,6 +181,27 @@ int fc_halo_counts(fc_forest* f, int64_t* counts);
  * read by interpolation slopes): keys global_patch * n^2 + padded cell index, ascending.
  * *len = count; FC_EINVAL if cap < count.  Works on host-only handles (multi-rank plan tests). */
 int fc_halo_requests(fc_forest* f, int peer, int round, int64_t* buf, int64_t cap, int64_t* len);
+
+/* ---- staged step with a caller-provided halo transport ---------------------------------------
+ * A handle created with nranks > 1 and nccl_id == NULL uses a *manual* halo transport: no NCCL
+ * communicator is created and fc_step / fc_ghost_fill return FC_ESTATE; the caller instead
+ *   (once)  passes every peer's requests (fc_halo_requests of the peer, `peer` = this rank) with
+ *           fc_halo_set_requests and calls fc_halo_finalize;
+ *   (step)  round 1: fc_halo_pack on every rank, copies recv[recv_off[s]..] <- send_s[send_off_s[me]..]
+ *           between ranks (fc_halo_buffers: device pointers, offsets in doubles, [nranks + 1]),
+ *           fc_halo_unpack; fc_step_local(phase 1) (ghost phases A, C); round 2 likewise (ring cells
+ *           read by interpolation); fc_step_local(phase 2) (ghost phase B, update, this rank's CFL);
+ *           fc_commit with the max of the ranks' CFLs.
+ * fc_step on an NCCL handle is exactly this sequence with ncclSend/Recv as the transport and
+ * ncclAllReduce(max) for the CFL (PAPER.md:264-272 [§4]: exchange, then local neighbour work).
+ * Used to test the sharded data path with several rank handles in one process. */
+int fc_halo_set_requests(fc_forest* f, int round, int peer, const int64_t* keys, int64_t n);
+int fc_halo_finalize(fc_forest* f);
+int fc_halo_buffers(fc_forest* f, int round, void** send, void** recv, int64_t* send_off, int64_t* recv_off);
+int fc_halo_pack(fc_forest* f, int round);      /* synchronous */
+int fc_halo_unpack(fc_forest* f, int round);    /* synchronous */
+int fc_step_local(fc_forest* f, double dt, int phase, double* local_cfl);
+int fc_commit(fc_forest* f, double global_cfl); /* FC_ECFL / FC_ENONFINITE as fc_step */
 
 /* Write a fresh 128-byte ncclUniqueId into out (call on rank 0, broadcast to the others). */
 int fc_nccl_unique_id(void* out);

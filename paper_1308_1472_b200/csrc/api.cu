@@ -89,6 +89,8 @@ struct fc_forest {
   bool has_problem = false, has_q = false, has_aux = false;
   // halo
   ncclComm_t comm = nullptr;
+  bool manual = false;                 // nranks > 1 without an NCCL id: the caller moves halo data
+  std::vector<std::vector<int64_t>> peer_req[2];   // requests this rank serves, per round and peer
   // per round: concatenated pack / unpack index lists and per-peer counts
   int32_t *d_pack[2] = {nullptr, nullptr}, *d_unpack[2] = {nullptr, nullptr};
   int64_t npack[2] = {0, 0}, nunpack[2] = {0, 0};
@@ -114,16 +116,61 @@ static void free_list(DevList& l) {
   l.d = nullptr;
 }
 
-// one-time NCCL exchange of halo requests -> pack / unpack lists
+// pack / unpack lists and buffers from the requests this rank serves (f->peer_req) and its own
+// requests (pl.halo.need1/need2); shared by the NCCL and the manual transports
+static int build_halo_lists(fc_forest* f) {
+  Plan& pl = f->pl;
+  const int R = pl.nranks;
+  const int64_t n2 = (int64_t)pl.n * pl.n;
+  const int64_t S = (int64_t)pl.meqn * n2;
+  for (int round = 0; round < 2; ++round) {
+    const auto& need = round == 0 ? pl.halo.need1 : pl.halo.need2;
+    f->send_cnt[round].assign(R, 0);
+    f->recv_cnt[round].assign(R, 0);
+    std::vector<int32_t> pack, unpack;
+    for (int s = 0; s < R; ++s) {
+      f->recv_cnt[round][s] = (int64_t)need[s].size();
+      f->send_cnt[round][s] = (int64_t)f->peer_req[round][s].size();
+      for (int64_t key : f->peer_req[round][s]) {
+        const int64_t q = key / n2, cell = key % n2;
+        if (q < pl.p0 || q >= pl.p1) return fail(FC_EINVAL, "halo request for a patch this rank does not own");
+        pack.push_back((int32_t)((q - pl.p0) * S + cell));
+      }
+      for (int64_t key : need[s]) {   // my requests, in slot order
+        const int64_t h = pl.halo.slot.at(key * 2 + round);
+        unpack.push_back((int32_t)((f->Pl + h / n2) * S + h % n2));
+      }
+    }
+    cudaFree(f->d_pack[round]);
+    cudaFree(f->d_unpack[round]);
+    f->d_pack[round] = f->d_unpack[round] = nullptr;
+    f->npack[round] = (int64_t)pack.size();
+    f->nunpack[round] = (int64_t)unpack.size();
+    if (!pack.empty()) {
+      CK(cudaMalloc(&f->d_pack[round], pack.size() * sizeof(int32_t)));
+      CK(cudaMemcpy(f->d_pack[round], pack.data(), pack.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    if (!unpack.empty()) {
+      CK(cudaMalloc(&f->d_unpack[round], unpack.size() * sizeof(int32_t)));
+      CK(cudaMemcpy(f->d_unpack[round], unpack.data(), unpack.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+  }
+  cudaFree(f->d_sendbuf);
+  cudaFree(f->d_recvbuf);
+  const int64_t maxs = std::max(f->npack[0], f->npack[1]), maxr = std::max(f->nunpack[0], f->nunpack[1]);
+  CK(cudaMalloc(&f->d_sendbuf, std::max<int64_t>(1, maxs) * pl.meqn * sizeof(double)));
+  CK(cudaMalloc(&f->d_recvbuf, std::max<int64_t>(1, maxr) * pl.meqn * sizeof(double)));
+  f->st.halo_cells = f->nunpack[0] + f->nunpack[1];
+  return FC_OK;
+}
+
+// one-time NCCL exchange of halo requests (counts all-gathered, then per-peer send/recv)
 static int setup_halo(fc_forest* f, const void* nccl_id) {
   Plan& pl = f->pl;
   const int R = pl.nranks, me = pl.rank;
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof(id));
   NK(ncclCommInitRank(&f->comm, R, id, me));
-  const int64_t n2 = (int64_t)pl.n * pl.n;
-  const int64_t S = (int64_t)pl.meqn * n2;
-  // counts matrix: row r = what rank r needs from each peer, rounds 1 and 2
   std::vector<int64_t> mine(2 * R), all((size_t)2 * R * R);
   for (int s = 0; s < R; ++s) {
     mine[s] = (int64_t)pl.halo.need1[s].size();
@@ -139,22 +186,14 @@ static int setup_halo(fc_forest* f, const void* nccl_id) {
   cudaFree(d_mine);
   cudaFree(d_all);
   for (int round = 0; round < 2; ++round) {
-    f->send_cnt[round].assign(R, 0);
-    f->recv_cnt[round].assign(R, 0);
-    for (int s = 0; s < R; ++s) {
-      f->recv_cnt[round][s] = mine[round * R + s];          // I need from s
-      f->send_cnt[round][s] = all[(size_t)s * 2 * R + round * R + me];  // s needs from me
-    }
-    // send my requests to the owners, receive the peers' requests
     const auto& need = round == 0 ? pl.halo.need1 : pl.halo.need2;
-    std::vector<int64_t> req_out, req_in;
-    std::vector<int64_t> off_out(R + 1, 0), off_in(R + 1, 0);
+    std::vector<int64_t> cnt_in(R), off_out(R + 1, 0), off_in(R + 1, 0), req_out;
     for (int s = 0; s < R; ++s) {
+      cnt_in[s] = all[(size_t)s * 2 * R + round * R + me];   // s needs from me
       off_out[s + 1] = off_out[s] + (int64_t)need[s].size();
-      off_in[s + 1] = off_in[s] + f->send_cnt[round][s];
+      off_in[s + 1] = off_in[s] + cnt_in[s];
       req_out.insert(req_out.end(), need[s].begin(), need[s].end());
     }
-    req_in.resize(off_in[R]);
     int64_t *d_out = nullptr, *d_in = nullptr;
     CK(cudaMalloc(&d_out, std::max<int64_t>(1, off_out[R]) * sizeof(int64_t)));
     CK(cudaMalloc(&d_in, std::max<int64_t>(1, off_in[R]) * sizeof(int64_t)));
@@ -164,51 +203,35 @@ static int setup_halo(fc_forest* f, const void* nccl_id) {
     for (int s = 0; s < R; ++s) {
       if (s == me) continue;
       if (need[s].size()) NK(ncclSend(d_out + off_out[s], need[s].size(), ncclInt64, s, f->comm, f->stream));
-      if (f->send_cnt[round][s]) NK(ncclRecv(d_in + off_in[s], f->send_cnt[round][s], ncclInt64, s, f->comm, f->stream));
+      if (cnt_in[s]) NK(ncclRecv(d_in + off_in[s], cnt_in[s], ncclInt64, s, f->comm, f->stream));
     }
     NK(ncclGroupEnd());
     CK(cudaStreamSynchronize(f->stream));
-    if (off_in[R])
-      CK(cudaMemcpy(req_in.data(), d_in, off_in[R] * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    std::vector<int64_t> req_in(off_in[R]);
+    if (off_in[R]) CK(cudaMemcpy(req_in.data(), d_in, off_in[R] * sizeof(int64_t), cudaMemcpyDeviceToHost));
     cudaFree(d_out);
     cudaFree(d_in);
-    // pack list: requested (global patch, cell) -> local offset of component 0
-    std::vector<int32_t> pack(off_in[R]), unpack;
-    for (int64_t k = 0; k < off_in[R]; ++k) {
-      const int64_t q = req_in[k] / n2, cell = req_in[k] % n2;
-      if (q < pl.p0 || q >= pl.p1) return fail(FC_EINVAL, "halo request for a patch this rank does not own");
-      pack[k] = (int32_t)((q - pl.p0) * S + cell);
-    }
-    // unpack list: my requests in slot order
-    for (int s = 0; s < R; ++s)
-      for (int64_t key : need[s]) {
-        const int64_t h = pl.halo.slot.at(key * 2 + round);
-        unpack.push_back((int32_t)((f->Pl + h / n2) * S + h % n2));
-      }
-    f->npack[round] = (int64_t)pack.size();
-    f->nunpack[round] = (int64_t)unpack.size();
-    if (!pack.empty()) {
-      CK(cudaMalloc(&f->d_pack[round], pack.size() * sizeof(int32_t)));
-      CK(cudaMemcpy(f->d_pack[round], pack.data(), pack.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    }
-    if (!unpack.empty()) {
-      CK(cudaMalloc(&f->d_unpack[round], unpack.size() * sizeof(int32_t)));
-      CK(cudaMemcpy(f->d_unpack[round], unpack.data(), unpack.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    }
+    f->peer_req[round].assign(R, {});
+    for (int s = 0; s < R; ++s) f->peer_req[round][s].assign(req_in.begin() + off_in[s], req_in.begin() + off_in[s + 1]);
   }
-  const int64_t maxs = std::max(f->npack[0], f->npack[1]), maxr = std::max(f->nunpack[0], f->nunpack[1]);
-  CK(cudaMalloc(&f->d_sendbuf, std::max<int64_t>(1, maxs) * pl.meqn * sizeof(double)));
-  CK(cudaMalloc(&f->d_recvbuf, std::max<int64_t>(1, maxr) * pl.meqn * sizeof(double)));
-  f->st.halo_cells = f->nunpack[0] + f->nunpack[1];
-  return FC_OK;
+  return build_halo_lists(f);
 }
 
-static int halo_round(fc_forest* f, int round) {
-  if (f->pl.nranks <= 1) return FC_OK;
-  const int R = f->pl.nranks, me = f->pl.rank, meqn = f->pl.meqn;
-  const int n2 = f->pl.n * f->pl.n;
-  f->st.kernel_launches += launch_pack(f->qold, f->d_pack[round], f->npack[round], meqn, n2, f->d_sendbuf, f->stream);
+// ---- halo transfer pieces (round: 0 = interior cells, 1 = ring cells read by interpolation) ----
+static int halo_pack(fc_forest* f, int round) {
+  f->st.kernel_launches += launch_pack(f->qold, f->d_pack[round], f->npack[round], f->pl.meqn,
+                                       f->pl.n * f->pl.n, f->d_sendbuf, f->stream);
   CK(cudaGetLastError());
+  return FC_OK;
+}
+static int halo_unpack(fc_forest* f, int round) {
+  f->st.kernel_launches += launch_unpack(f->qold, f->d_unpack[round], f->nunpack[round], f->pl.meqn,
+                                         f->pl.n * f->pl.n, f->d_recvbuf, f->stream);
+  CK(cudaGetLastError());
+  return FC_OK;
+}
+static int halo_nccl(fc_forest* f, int round) {
+  const int R = f->pl.nranks, me = f->pl.rank, meqn = f->pl.meqn;
   NK(ncclGroupStart());
   int64_t so = 0, ro = 0;
   for (int s = 0; s < R; ++s) {
@@ -219,33 +242,100 @@ static int halo_round(fc_forest* f, int round) {
     ro += rc;
   }
   NK(ncclGroupEnd());
-  f->st.kernel_launches += launch_unpack(f->qold, f->d_unpack[round], f->nunpack[round], meqn, n2, f->d_recvbuf, f->stream);
+  return FC_OK;
+}
+
+// one NCCL halo round (pack -> grouped send/recv -> unpack); no-op on one rank
+static int halo_round(fc_forest* f, int round) {
+  if (f->pl.nranks <= 1) return FC_OK;
+  if (f->manual) return fail(FC_ESTATE, "manual halo transport: use the staged step calls");
+  int rc;
+  if ((rc = halo_pack(f, round)) || (rc = halo_nccl(f, round)) || (rc = halo_unpack(f, round))) return rc;
+  return FC_OK;
+}
+
+static bool has_round2(const fc_forest* f) { return f->npack[1] || f->nunpack[1]; }
+
+static bool use_fused(const fc_forest* f) {
+  return f->fused && f->prob.skip_quiescent && f->prob.kind != FC_ADV_EDGEVEL_CAPA;
+}
+
+static void run_ghost(fc_forest* f, int op, const DevList& l) {
+  f->st.kernel_launches += launch_ghost(op, f->qold, l.d, l.nrec, f->pl.meqn, f->pl.n * f->pl.n, f->stream);
+}
+
+// ghost phases that only need halo round 1: A (copy, average) -> C (BC x then y)
+static int ghost_phase_ac(fc_forest* f) {
+  run_ghost(f, OP_COPY, f->copy);
+  run_ghost(f, OP_AVG4, f->avg);
+  run_ghost(f, 4, f->bcx);
+  run_ghost(f, 4, f->bcy);
+  CK(cudaGetLastError());
+  return FC_OK;
+}
+
+// ghost phases after halo round 2: per level B (interpolate) -> C, then CORNER3
+static int ghost_phase_b(fc_forest* f) {
+  for (size_t l = 0; l < f->interp.size(); ++l) {
+    if (!f->interp[l].nrec) continue;
+    run_ghost(f, OP_INTERP, f->interp[l]);
+    run_ghost(f, 4, f->bcx_l[l]);
+    run_ghost(f, 4, f->bcy_l[l]);
+  }
+  run_ghost(f, 6, f->corner3);
   CK(cudaGetLastError());
   return FC_OK;
 }
 
 static int ghost_fill_internal(fc_forest* f) {
-  const int meqn = f->pl.meqn, n2 = f->pl.n * f->pl.n;
   int rc;
-  if ((rc = halo_round(f, 0))) return rc;
-  auto run = [&](int op, const DevList& l) {
-    f->st.kernel_launches += launch_ghost(op, f->qold, l.d, l.nrec, meqn, n2, f->stream);
-  };
-  run(OP_COPY, f->copy);
-  run(OP_AVG4, f->avg);
-  run(4, f->bcx);
-  run(4, f->bcy);
-  CK(cudaGetLastError());
-  if (f->npack[1] || f->nunpack[1])
-    if ((rc = halo_round(f, 1))) return rc;
-  for (size_t l = 0; l < f->interp.size(); ++l) {
-    if (!f->interp[l].nrec) continue;
-    run(OP_INTERP, f->interp[l]);
-    run(4, f->bcx_l[l]);
-    run(4, f->bcy_l[l]);
+  if ((rc = halo_round(f, 0)) || (rc = ghost_phase_ac(f))) return rc;
+  if (has_round2(f) && (rc = halo_round(f, 1))) return rc;
+  return ghost_phase_b(f);
+}
+
+// the update after the ghost data are in place: quiescent filter (fused path) + step kernel,
+// leaving this rank's CFL max in d_cfl
+static int update_local(fc_forest* f, double dt) {
+  CK(cudaMemsetAsync(f->d_cfl, 0, sizeof(unsigned long long), f->stream));
+  const fc_problem& p = f->prob;
+  const bool fused = use_fused(f);
+  bool filtered = false;
+  if (fused) {   // copy/classify + activity filter, then the step over the active patches only
+    CK(cudaMemsetAsync(f->d_nactive, 0, sizeof(int32_t), f->stream));
+    const int fr = launch_filter(p.kind, f->qold, f->qnew, (int)f->Pl, f->pl.m, f->d_uflag, f->d_uval, f->d_nbr,
+                                 f->d_negmask, f->d_level, dt, f->pl.dx0, p.p0, p.p1, f->d_active, f->d_nactive,
+                                 f->d_cfl, f->stream);
+    if (fr > 0) {
+      f->st.kernel_launches += fr;
+      filtered = true;
+    }
   }
-  run(6, f->corner3);
+  int lr = launch_step(p.kind, f->qold, f->qnew, f->aux, f->d_level, f->Pl, f->pl.m, dt, f->pl.dx0,
+                       p.p0, p.p1, p.limiter, p.method2, p.method3, filtered ? 0 : p.skip_quiescent,
+                       fused ? f->d_ring : nullptr, f->d_bcflag, filtered ? f->d_active : nullptr,
+                       filtered ? f->d_nactive : nullptr, f->d_cfl, f->stream);
+  if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
+  f->st.kernel_launches += lr;
+  f->st.step_kernel_launches += lr;
   CK(cudaGetLastError());
+  return FC_OK;
+}
+
+static int check_step_args(fc_forest* f, double dt) {
+  if (!f) return fail(FC_EINVAL, "null handle");
+  if (f->host_only || !f->has_q || !f->has_problem) return fail(FC_ESTATE, "set problem and q first");
+  if (f->pl.maux > 0 && !f->has_aux) return fail(FC_ESTATE, "set aux first");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(FC_EINVAL, "dt must be positive and finite");
+  return FC_OK;
+}
+
+// commit rule shared by fc_step and fc_commit
+static int commit(fc_forest* f, double cfl) {
+  if (!std::isfinite(cfl)) return fail(FC_ENONFINITE, "CFL is not finite");
+  if (cfl > f->prob.cfl_reject) return fail(FC_ECFL, "CFL above cfl_reject; step not committed");
+  std::swap(f->qold, f->qnew);
+  f->st.steps += 1;
   return FC_OK;
 }
 
@@ -300,7 +390,7 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
     *out = f;
     return FC_OK;
   }
-  if (d->nranks > 1 && !d->nccl_id) { delete f; return fail(FC_EINVAL, "nranks > 1 needs nccl_id"); }
+  f->manual = d->nranks > 1 && !d->nccl_id;   // no NCCL id: the caller transports halo data
   f->host_only = false;
   f->device = d->device;
   const Plan& pl = f->pl;
@@ -381,7 +471,12 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
     }
   }
   if (pl.nranks > 1) {
-    rc = setup_halo(f, d->nccl_id);
+    if (f->manual) {
+      for (int r = 0; r < 2; ++r) f->peer_req[r].assign(pl.nranks, {});
+      rc = build_halo_lists(f);   // receive side now; send side after fc_halo_set_requests + finalize
+    } else {
+      rc = setup_halo(f, d->nccl_id);
+    }
     if (rc) { std::string m = g_err; destroy(f); return fail(rc, m); }
   }
   *out = f;
@@ -530,6 +625,7 @@ int fc_get_q_padded(fc_forest* f, double* q, int where) {
 int fc_ghost_fill(fc_forest* f) {
   if (!f) return fail(FC_EINVAL, "null handle");
   if (f->host_only || !f->has_q) return fail(FC_ESTATE, "no state");
+  if (f->manual) return fail(FC_ESTATE, "manual halo transport: use the staged calls");
   CK(cudaSetDevice(f->device));
   int rc = ghost_fill_internal(f);
   if (rc) return rc;
@@ -538,41 +634,17 @@ int fc_ghost_fill(fc_forest* f) {
 }
 
 int fc_step(fc_forest* f, double dt, double* max_cfl) {
-  if (!f) return fail(FC_EINVAL, "null handle");
-  if (f->host_only || !f->has_q || !f->has_problem) return fail(FC_ESTATE, "set problem and q first");
-  if (f->pl.maux > 0 && !f->has_aux) return fail(FC_ESTATE, "set aux first");
-  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(FC_EINVAL, "dt must be positive and finite");
+  int rc = check_step_args(f, dt);
+  if (rc) return rc;
+  if (f->manual) return fail(FC_ESTATE, "manual halo transport: use fc_halo_* / fc_step_local / fc_commit");
   CK(cudaSetDevice(f->device));
   if (f->timing) CK(cudaEventRecord(f->ev[0], f->stream));
   // fused ring gather + quiescent filter when skipping is on (rings never written); otherwise the
   // ghost kernels fill the rings and every tile is bulk-copied whole (faster for the full update)
-  const bool use_fused = f->fused && f->prob.skip_quiescent && f->prob.kind != FC_ADV_EDGEVEL_CAPA;
-  int rc = use_fused ? halo_round(f, 0) : ghost_fill_internal(f);
+  rc = use_fused(f) ? halo_round(f, 0) : ghost_fill_internal(f);
   if (rc) return rc;
   if (f->timing) CK(cudaEventRecord(f->ev[1], f->stream));
-  CK(cudaMemsetAsync(f->d_cfl, 0, sizeof(unsigned long long), f->stream));
-  const fc_problem& p = f->prob;
-  // fused path + quiescent skipping: copy/classify + activity filter, then the step over the
-  // active patches only (the in-kernel window check is then redundant)
-  bool filtered = false;
-  if (use_fused) {
-    CK(cudaMemsetAsync(f->d_nactive, 0, sizeof(int32_t), f->stream));
-    const int fr = launch_filter(p.kind, f->qold, f->qnew, (int)f->Pl, f->pl.m, f->d_uflag, f->d_uval, f->d_nbr,
-                                 f->d_negmask, f->d_level, dt, f->pl.dx0, p.p0, p.p1, f->d_active, f->d_nactive,
-                                 f->d_cfl, f->stream);
-    if (fr > 0) {
-      f->st.kernel_launches += fr;
-      filtered = true;
-    }
-  }
-  int lr = launch_step(p.kind, f->qold, f->qnew, f->aux, f->d_level, f->Pl, f->pl.m, dt, f->pl.dx0,
-                       p.p0, p.p1, p.limiter, p.method2, p.method3, filtered ? 0 : p.skip_quiescent,
-                       use_fused ? f->d_ring : nullptr, f->d_bcflag, filtered ? f->d_active : nullptr,
-                       filtered ? f->d_nactive : nullptr, f->d_cfl, f->stream);
-  if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
-  f->st.kernel_launches += lr;
-  f->st.step_kernel_launches += lr;
-  CK(cudaGetLastError());
+  if ((rc = update_local(f, dt))) return rc;
   if (f->timing) CK(cudaEventRecord(f->ev[2], f->stream));
   if (f->pl.nranks > 1)
     NK(ncclAllReduce(f->d_cfl, f->d_cfl, 1, ncclDouble, ncclMax, f->comm, f->stream));
@@ -590,11 +662,89 @@ int fc_step(fc_forest* f, double dt, double* max_cfl) {
   }
   const double cfl = *f->h_cfl;
   if (max_cfl) *max_cfl = cfl;
-  if (!std::isfinite(cfl)) return fail(FC_ENONFINITE, "CFL is not finite");
-  if (cfl > p.cfl_reject) return fail(FC_ECFL, "CFL above cfl_reject; step not committed");
-  std::swap(f->qold, f->qnew);
-  f->st.steps += 1;
+  return commit(f, cfl);
+}
+
+// ---- staged step for a caller-provided halo transport (manual mode) ---------------------------
+int fc_halo_set_requests(fc_forest* f, int round, int peer, const int64_t* keys, int64_t n) {
+  if (!f || (n && !keys)) return fail(FC_EINVAL, "null argument");
+  if (!f->manual) return fail(FC_ESTATE, "not a manual-transport handle");
+  if (round != 1 && round != 2) return fail(FC_EINVAL, "round must be 1 or 2");
+  if (peer < 0 || peer >= f->pl.nranks) return fail(FC_EINVAL, "bad peer");
+  if (f->peer_req[round - 1].size() != (size_t)f->pl.nranks) f->peer_req[round - 1].assign(f->pl.nranks, {});
+  f->peer_req[round - 1][peer].assign(keys, keys + n);
   return FC_OK;
+}
+
+int fc_halo_finalize(fc_forest* f) {
+  if (!f) return fail(FC_EINVAL, "null handle");
+  if (!f->manual) return fail(FC_ESTATE, "not a manual-transport handle");
+  CK(cudaSetDevice(f->device));
+  for (int r = 0; r < 2; ++r)
+    if (f->peer_req[r].size() != (size_t)f->pl.nranks) f->peer_req[r].assign(f->pl.nranks, {});
+  return build_halo_lists(f);
+}
+
+int fc_halo_buffers(fc_forest* f, int round, void** send, void** recv, int64_t* send_off, int64_t* recv_off) {
+  if (!f || !send || !recv || !send_off || !recv_off) return fail(FC_EINVAL, "null argument");
+  if (f->host_only || f->pl.nranks <= 1) return fail(FC_ESTATE, "no halo on this handle");
+  if (round != 1 && round != 2) return fail(FC_EINVAL, "round must be 1 or 2");
+  const int r = round - 1, R = f->pl.nranks, meqn = f->pl.meqn;
+  *send = f->d_sendbuf;
+  *recv = f->d_recvbuf;
+  send_off[0] = recv_off[0] = 0;
+  for (int s = 0; s < R; ++s) {
+    send_off[s + 1] = send_off[s] + (f->send_cnt[r].empty() ? 0 : f->send_cnt[r][s]) * meqn;
+    recv_off[s + 1] = recv_off[s] + (f->recv_cnt[r].empty() ? 0 : f->recv_cnt[r][s]) * meqn;
+  }
+  return FC_OK;
+}
+
+int fc_halo_pack(fc_forest* f, int round) {
+  if (!f || (round != 1 && round != 2)) return fail(FC_EINVAL, "bad argument");
+  if (f->host_only || !f->has_q) return fail(FC_ESTATE, "no state");
+  CK(cudaSetDevice(f->device));
+  int rc = halo_pack(f, round - 1);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(f->stream));
+  return FC_OK;
+}
+
+int fc_halo_unpack(fc_forest* f, int round) {
+  if (!f || (round != 1 && round != 2)) return fail(FC_EINVAL, "bad argument");
+  if (f->host_only || !f->has_q) return fail(FC_ESTATE, "no state");
+  CK(cudaSetDevice(f->device));
+  int rc = halo_unpack(f, round - 1);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(f->stream));
+  return FC_OK;
+}
+
+int fc_step_local(fc_forest* f, double dt, int phase, double* local_cfl) {
+  int rc = check_step_args(f, dt);
+  if (rc) return rc;
+  CK(cudaSetDevice(f->device));
+  if (phase == 1) {
+    if (!use_fused(f) && (rc = ghost_phase_ac(f))) return rc;
+  } else if (phase == 2) {
+    if (!use_fused(f) && (rc = ghost_phase_b(f))) return rc;
+    if ((rc = update_local(f, dt))) return rc;
+    CK(cudaMemcpyAsync(f->h_cfl, f->d_cfl, sizeof(double), cudaMemcpyDeviceToHost, f->stream));
+    if (local_cfl) {
+      CK(cudaStreamSynchronize(f->stream));
+      *local_cfl = *f->h_cfl;
+    }
+  } else {
+    return fail(FC_EINVAL, "phase must be 1 or 2");
+  }
+  CK(cudaStreamSynchronize(f->stream));
+  return FC_OK;
+}
+
+int fc_commit(fc_forest* f, double global_cfl) {
+  if (!f) return fail(FC_EINVAL, "null handle");
+  if (f->host_only || !f->has_q) return fail(FC_ESTATE, "no state");
+  return commit(f, global_cfl);
 }
 
 }  // extern "C"

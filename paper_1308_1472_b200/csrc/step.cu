@@ -650,6 +650,7 @@ static int launch_filter_s(const double* qold, double* qnew, int npatch, int m, 
                            const int32_t* nbr, const uint8_t* negmask, const int8_t* level, double dt,
                            double dx0, SolverParams sp, int32_t* active, int32_t* nactive,
                            unsigned long long* cfl_bits, cudaStream_t st) {
+  if (npatch <= 0) return 0;
   const int blocks_copy = 148 * 8;
   switch (m) {
     case 16: k_copy_classify<S::MEQN, 16><<<blocks_copy, 256, 0, st>>>(qold, qnew, npatch, uflag, uval); break;

@@ -31,7 +31,9 @@ ERRNAMES = {0: "FC_OK", -1: "FC_EINVAL", -2: "FC_ETILING", -3: "FC_ECONN", -4: "
 EXPORTS = ["fc_forest_create", "fc_forest_destroy", "fc_set_problem", "fc_set_aux", "fc_set_q",
            "fc_ghost_fill", "fc_step", "fc_get_q", "fc_get_q_padded", "fc_get_ghost_table",
            "fc_set_stream", "fc_set_timing", "fc_get_stats", "fc_reset_stats", "fc_local_range",
-           "fc_halo_counts", "fc_halo_requests", "fc_nccl_unique_id", "fc_last_error"]
+           "fc_halo_counts", "fc_halo_requests", "fc_halo_set_requests", "fc_halo_finalize",
+           "fc_halo_buffers", "fc_halo_pack", "fc_halo_unpack", "fc_step_local", "fc_commit",
+           "fc_nccl_unique_id", "fc_last_error"]
 
 
 class FcError(RuntimeError):
@@ -93,6 +95,13 @@ def lib():
         L.fc_local_range.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.fc_halo_counts.argtypes = [P, P]
         L.fc_halo_requests.argtypes = [P, C.c_int, C.c_int, P, C.c_int64, C.POINTER(C.c_int64)]
+        L.fc_halo_set_requests.argtypes = [P, C.c_int, C.c_int, P, C.c_int64]
+        L.fc_halo_finalize.argtypes = [P]
+        L.fc_halo_buffers.argtypes = [P, C.c_int, C.POINTER(P), C.POINTER(P), P, P]
+        L.fc_halo_pack.argtypes = [P, C.c_int]
+        L.fc_halo_unpack.argtypes = [P, C.c_int]
+        L.fc_step_local.argtypes = [P, C.c_double, C.c_int, C.POINTER(C.c_double)]
+        L.fc_commit.argtypes = [P, C.c_double]
         L.fc_nccl_unique_id.argtypes = [P]
         L.fc_last_error.restype = C.c_char_p
         _lib = L
@@ -224,6 +233,40 @@ class Forest:
         _check(lib().fc_halo_requests(self.h, peer, round_, buf.ctypes.data_as(C.c_void_p), n.value,
                                       C.byref(n)), "fc_halo_requests")
         return buf[:n.value]
+
+    # -- manual halo transport (staged step) --------------------------------------------------
+    def halo_set_requests(self, round_: int, peer: int, keys: np.ndarray):
+        keys = np.ascontiguousarray(keys, np.int64)
+        _check(lib().fc_halo_set_requests(self.h, round_, peer, keys.ctypes.data_as(C.c_void_p), len(keys)),
+               "fc_halo_set_requests")
+
+    def halo_finalize(self):
+        _check(lib().fc_halo_finalize(self.h), "fc_halo_finalize")
+
+    def halo_buffers(self, round_: int):
+        s, r = C.c_void_p(), C.c_void_p()
+        so = np.zeros(self.nranks + 1, np.int64)
+        ro = np.zeros(self.nranks + 1, np.int64)
+        _check(lib().fc_halo_buffers(self.h, round_, C.byref(s), C.byref(r), so.ctypes.data_as(C.c_void_p),
+                                     ro.ctypes.data_as(C.c_void_p)), "fc_halo_buffers")
+        return s.value, r.value, so, ro
+
+    def halo_pack(self, round_: int):
+        _check(lib().fc_halo_pack(self.h, round_), "fc_halo_pack")
+
+    def halo_unpack(self, round_: int):
+        _check(lib().fc_halo_unpack(self.h, round_), "fc_halo_unpack")
+
+    def step_local(self, dt: float, phase: int) -> float:
+        c = C.c_double(0.0)
+        _check(lib().fc_step_local(self.h, dt, phase, C.byref(c)), "fc_step_local")
+        return c.value
+
+    def commit(self, global_cfl: float) -> int:
+        rc = lib().fc_commit(self.h, global_cfl)
+        if rc not in (FC_OK, FC_ECFL):
+            _check(rc, "fc_commit")
+        return rc
 
     def halo_counts(self) -> np.ndarray:
         out = np.zeros(self.nranks, np.int64)

@@ -70,7 +70,8 @@ def test_ghost_rings_bitwise(w, rng):
 # ---- full runs vs the oracle ----------------------------------------------------------------------
 RUNS = [c1(), c2(), c3(level=3, m=32), c5(level=3, m=16), c5(level=2, m=8),
         c4_workload(base_level=2, m=16, steps=100), c4_workload(base_level=2, m=8, uniform=True, steps=60),
-        c1(level=2, m=24, steps=30), c1(level=1, m=20, steps=30), c1(level=1, m=6, steps=30)]
+        c1(level=2, m=24, steps=30), c1(level=1, m=20, steps=30), c1(level=1, m=6, steps=30),
+        c1(level=0, m=16, steps=30), c1(level=3, m=4, steps=30), c5(level=0, m=8, steps=30)]
 
 
 @pytest.mark.parametrize("skip", [1, 0], ids=["quiescent_skip", "full_update"])

@@ -1,0 +1,99 @@
+"""The sharded (multi-GPU) data path on one GPU: R rank handles in one process with the manual
+halo transport (include/fc.h "staged step"), halo buffers moved between the ranks with plain
+device copies in place of ncclSend/ncclRecv, the CFL max taken over the ranks.  Everything else --
+request exchange, pack / unpack lists, halo slots in virtual patches, round-2 exchange of coarse
+ring cells for interpolation, the fused ring gather through halo slots, remote neighbours in the
+quiescent filter -- is the production code.  The concatenated result must equal the one-rank run
+bitwise (shard-count invariance) and the oracle within tolerance."""
+import ctypes as C
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1308_1472_b200 import fc
+from workloads.configs import c2, c3, c5
+from workloads.cubed_sphere import c4_workload
+
+pytestmark = pytest.mark.gpu
+
+_cudart = None
+
+
+def d2d(dst: int, src: int, nbytes: int):
+    global _cudart
+    if _cudart is None:
+        import nvidia.cuda_runtime as cr
+        path = sorted(glob.glob(os.path.join(os.path.dirname(cr.__file__), "lib", "libcudart.so*")))[0]
+        _cudart = C.CDLL(path)
+        _cudart.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+    if nbytes:
+        assert _cudart.cudaMemcpy(C.c_void_p(int(dst)), C.c_void_p(int(src)), int(nbytes), 3) == 0
+
+
+def run_sharded(w, R, dts, skip):
+    hs = []
+    for r in range(R):
+        f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0, 0, r, R, None)
+        f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject, skip)
+        if w.aux is not None:
+            f.set_aux(np.ascontiguousarray(w.aux[f.first:f.first + f.count]))
+        hs.append(f)
+    for rnd in (1, 2):
+        for r in range(R):
+            for s in range(R):
+                if s != r:
+                    hs[s].halo_set_requests(rnd, r, hs[r].halo_requests(s, rnd))
+    for f in hs:
+        f.halo_finalize()
+        f.set_q(np.ascontiguousarray(w.q0[f.first:f.first + f.count]))
+
+    def exchange(rnd):
+        for f in hs:
+            f.halo_pack(rnd)
+        bufs = [f.halo_buffers(rnd) for f in hs]
+        for r in range(R):
+            _, recv, _, roff = bufs[r]
+            for s in range(R):
+                if s == r:
+                    continue
+                send, _, soff, _ = bufs[s]
+                n = roff[s + 1] - roff[s]
+                assert n == soff[r + 1] - soff[r]
+                d2d(recv + 8 * roff[s], send + 8 * soff[r], 8 * n)
+        for f in hs:
+            f.halo_unpack(rnd)
+
+    cfls = []
+    for dt in dts:
+        exchange(1)
+        for f in hs:
+            f.step_local(dt, 1)
+        exchange(2)
+        c = max(f.step_local(dt, 2) for f in hs)
+        for f in hs:
+            assert f.commit(c) == fc.FC_OK
+        cfls.append(c)
+    q = np.concatenate([f.get_q() for f in hs if f.count], axis=0)
+    for f in hs:
+        f.close()
+    return q, np.array(cfls)
+
+
+CASES = [c2(steps=30), c5(level=2, m=16, steps=30), c3(level=2, m=32, steps=30),
+         c4_workload(base_level=2, m=8, steps=30)]
+
+
+@pytest.mark.parametrize("skip", [1, 0], ids=["quiescent_skip", "full_update"])
+@pytest.mark.parametrize("R", [2, 3, 4])
+@pytest.mark.parametrize("w", CASES, ids=lambda w: w.name)
+def test_sharded_equals_single_rank_bitwise(w, R, skip):
+    qo, co, do = oracle.run(w)
+    q1, c1_, _ = fc.run(w, dt_list=do, skip_quiescent=skip)
+    qr, cr = run_sharded(w, R, do, skip)
+    np.testing.assert_array_equal(qr, q1)
+    np.testing.assert_array_equal(cr, c1_)
+    for k in range(w.meqn):
+        assert np.abs(qr[:, k] - qo[:, k]).max() <= 1e-12 * np.abs(qo[:, k]).max()

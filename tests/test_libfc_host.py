@@ -129,3 +129,24 @@ def test_sharded_tables_and_halo_plan(nranks):
                 has = any(lo <= q < hi for q in srcs)
                 assert (counts[s] > 0) == has, (w.name, r, s)
             del owners
+
+
+def test_more_ranks_than_patches():
+    """Ranks past the patch count own empty Morton ranges (the Fig. 3 "idle processors" case)."""
+    w = c1(level=1, m=8)          # 4 patches
+    o = oracle_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m)
+    seen = 0
+    for r in range(8):
+        f, t = host_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, rank=r, nranks=8)
+        assert f.count == ((r + 1) * 4) // 8 - (r * 4) // 8
+        np.testing.assert_array_equal(t, o[f.first:f.first + f.count])
+        seen += f.count
+    assert seen == 4
+
+
+def test_single_patch_forest_tables():
+    """A one-leaf periodic tree: every ghost cell copies from the patch itself (wrap-around)."""
+    w = c1(level=0, m=8)
+    _, t = host_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m)
+    assert (t[..., 0] == 1).all() and (t[..., 1] == 0).all()
+    np.testing.assert_array_equal(t, oracle_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m))
