@@ -10,6 +10,16 @@
 
 namespace fc {
 
+// Storage of a padded patch in device memory: rows of n = m + 4 doubles (row j + 1 holds cell row j,
+// j = -1..m+2) with the columns rotated so that cell i (1-based, -1..m+2) sits at column (i - 1) mod n:
+// the m interior cells of a row occupy its first m doubles -- whole, aligned 32-byte sectors -- and
+// the 4 ghost columns (right m+1, m+2, then left -1, 0) share the last 32 bytes.  Interior-only
+// traffic (the quiescent copy, TMA interior rows) then touches no partial sector.  The ABI's padded
+// arrays (fc_get_q_padded, aux) keep the natural layout (j + 1) n + (i + 1).
+inline int qcell(int i, int j, int n) { return (j + 1) * n + ((i - 1 + n) % n); }
+// natural padded index -> storage index
+inline int qcell_of_natural(int cell, int n) { return qcell(cell % n - 1, cell / n - 1, n); }
+
 // ghost-record ops (canonical EXPANDED table, include/fc.h)
 enum Op : int32_t { OP_NONE = 0, OP_COPY = 1, OP_AVG4 = 2, OP_INTERP = 3, OP_BCX = 4, OP_BCY = 5, OP_CORNER3 = 6 };
 constexpr int REC = 8;

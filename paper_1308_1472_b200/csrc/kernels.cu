@@ -108,7 +108,7 @@ __global__ void k_scatter_interior(const double* __restrict__ src, double* __res
     const int64_t r = t / m;
     const int j = (int)(r % m);
     const int64_t pk = r / m;
-    q[pk * n * n + (int64_t)(j + 2) * n + (i + 2)] = src[t];
+    q[pk * n * n + (int64_t)(j + 2) * n + i] = src[t];   // rotated storage: cell i+1 at column i
   }
 }
 
@@ -122,7 +122,17 @@ __global__ void k_gather_interior(const double* __restrict__ q, double* __restri
     const int64_t r = t / m;
     const int j = (int)(r % m);
     const int64_t pk = r / m;
-    dst[t] = q[pk * n * n + (int64_t)(j + 2) * n + (i + 2)];
+    dst[t] = q[pk * n * n + (int64_t)(j + 2) * n + i];
+  }
+}
+
+// storage (rotated columns) -> natural padded layout, one n x n block per (patch, component)
+__global__ void k_unrotate(const double* __restrict__ q, double* __restrict__ dst, int64_t nblocks, int n) {
+  const int64_t tot = nblocks * n * n;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t % n);          // natural column = i + 1
+    const int64_t rb = t - c;
+    dst[t] = q[rb + (c - 2 + n) % n];    // storage column (i - 1) mod n
   }
 }
 
@@ -162,6 +172,12 @@ int launch_unpack(double* q, const int32_t* idx, int64_t cnt, int meqn, int n2, 
 int launch_scatter(const double* src, double* q, int64_t P, int meqn, int m, cudaStream_t st) {
   if (P <= 0) return 0;
   k_scatter_interior<<<148 * 8, 256, 0, st>>>(src, q, P, meqn, m);
+  return 1;
+}
+
+int launch_unrotate(const double* q, double* dst, int64_t nblocks, int n, cudaStream_t st) {
+  if (nblocks <= 0) return 0;
+  k_unrotate<<<148 * 8, 256, 0, st>>>(q, dst, nblocks, n);
   return 1;
 }
 

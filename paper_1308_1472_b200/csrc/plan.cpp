@@ -389,8 +389,8 @@ int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err) {
   gl.bcy_l.assign(pl.lmax + 1, {});
   bool any_interp = false;
   auto off = [&](int64_t q, int i, int j, int round) -> int32_t {
-    const int64_t cell = (int64_t)(j + 1) * n + (i + 1);
-    if (q >= pl.p0 && q < pl.p1) return (int32_t)((q - pl.p0) * S + cell);
+    const int64_t cell = (int64_t)(j + 1) * n + (i + 1);   // natural index: halo keys
+    if (q >= pl.p0 && q < pl.p1) return (int32_t)((q - pl.p0) * S + qcell(i, j, n));
     const int64_t key = (q * n2 + cell) * 2 + (round - 1);
     auto it = pl.halo.slot.find(key);
     if (it == pl.halo.slot.end()) return -1;
@@ -404,7 +404,7 @@ int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err) {
       for (int i = -1; i <= m + 2; ++i) {
         if (!is_ring(m, i, j)) continue;
         const int32_t* o = pl.table.data() + (lp * G + r++) * REC;
-        const int32_t dst = (int32_t)(lp * S + (int64_t)(j + 1) * n + (i + 1));
+        const int32_t dst = (int32_t)(lp * S + qcell(i, j, n));
         switch (o[0]) {
           case OP_COPY: {
             int32_t s = off(o[1], o[2], o[3], 1);
@@ -433,7 +433,7 @@ int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err) {
           }
           case OP_BCX:
           case OP_BCY: {
-            const int32_t s = (int32_t)(lp * S + (int64_t)(o[3] + 1) * n + (o[2] + 1));
+            const int32_t s = (int32_t)(lp * S + qcell(o[2], o[3], n));
             const int32_t neg = (o[4] == FC_BC_WALL && meqn >= 3) ? (o[0] == OP_BCX ? 1 : 2) : -1;
             auto& v = o[0] == OP_BCX ? gl.bcx : gl.bcy;
             v.insert(v.end(), {dst, s, neg});
@@ -442,8 +442,8 @@ int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err) {
             break;
           }
           case OP_CORNER3: {
-            const int32_t a = (int32_t)(lp * S + (int64_t)(o[3] + 1) * n + (o[2] + 1));
-            const int32_t b = (int32_t)(lp * S + (int64_t)(o[7] + 1) * n + (o[6] + 1));
+            const int32_t a = (int32_t)(lp * S + qcell(o[2], o[3], n));
+            const int32_t b = (int32_t)(lp * S + qcell(o[6], o[7], n));
             gl.corner3.insert(gl.corner3.end(), {dst, a, b});
             break;
           }
@@ -481,11 +481,11 @@ int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& er
       const int32_t* o = pl.table.data() + (lp * G + r) * REC;
       int32_t v;
       if (o[0] == OP_COPY) {
-        const int64_t cell = (int64_t)(o[3] + 1) * n + (o[2] + 1);
+        const int64_t cell = (int64_t)(o[3] + 1) * n + (o[2] + 1);   // natural: halo key
         const int64_t q = o[1];
         if (!add_nbr((q >= pl.p0 && q < pl.p1) ? (int32_t)(q - pl.p0) : -2)) { err = "more than 8 ring neighbours"; return FC_EUNSUP; }
         if (q >= pl.p0 && q < pl.p1) {
-          v = (int32_t)((q - pl.p0) * S + cell);
+          v = (int32_t)((q - pl.p0) * S + qcell(o[2], o[3], n));
         } else {
           auto it = pl.halo.slot.find((q * n2 + cell) * 2);
           if (it == pl.halo.slot.end()) { err = "missing halo slot"; return FC_EINVAL; }

@@ -212,7 +212,8 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
 #pragma unroll 1
     for (int r = lane; r < MEQN * T; r += 32) {
       const int k = r / T, row = r - k * T;
-      bulk_g2s(buf + k * WW + (row + 2) * W + 2, qb + (int64_t)k * n2 + (row + 2) * n + 2, T * sizeof(double), bar);
+      // rotated storage: the m interior cells of a row are its first m doubles
+      bulk_g2s(buf + k * WW + (row + 2) * W + 2, qb + (int64_t)k * n2 + (row + 2) * n, T * sizeof(double), bar);
     }
     if (S::CAPA && lane == 0) bulk_g2s(buf + MEQN * WW, A.aux + (int64_t)patch * 3 * n2, abytes, bar);
     return;
@@ -220,16 +221,28 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
   constexpr uint32_t bytes = (uint32_t)Sh::BUF * sizeof(double);
   if (lane == 0) mbar_expect_tx(bar, bytes);
   __syncwarp();
-  if (A.tiles == 1) {        // the window is the whole padded patch: one contiguous copy each
+  if (A.tiles == 1) {        // the window is the whole (rotated) padded patch: one contiguous copy;
+                             // the kernel un-rotates its rows in shared memory
     if (lane == 0) bulk_g2s(buf, A.qold + patch * (int64_t)MEQN * n2, MEQN * WW * sizeof(double), bar);
-    if (S::CAPA && lane == 1) bulk_g2s(buf + MEQN * WW, A.aux + patch * 3ll * n2, 3 * WW * sizeof(double), bar);
-  } else {                   // one row copy per (component, window row), spread over the lanes
-    const double* qb = A.qold + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T) * n + tx * T;
+  } else {                   // q: per (component, window row) the storage row is rotated (cell i at
+                             // column (i-1) mod n), so a window row is one piece, or two for the
+                             // leftmost tile (ghost cells -1, 0 live at the end of the storage row)
+    const double* qb = A.qold + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T) * n;
 #pragma unroll 1
     for (int r = lane; r < MEQN * W; r += 32) {
       const int k = r / W, b = r - k * W;
-      bulk_g2s(buf + r * W, qb + (int64_t)k * n2 + b * n, W * sizeof(double), bar);
+      const double* row = qb + (int64_t)k * n2 + b * n;
+      if (tx == 0) {
+        bulk_g2s(buf + r * W, row + (n - 2), 2 * sizeof(double), bar);
+        bulk_g2s(buf + r * W + 2, row, (W - 2) * sizeof(double), bar);
+      } else {
+        bulk_g2s(buf + r * W, row + tx * T - 2, W * sizeof(double), bar);
+      }
     }
+  }
+  if (A.tiles == 1) {        // aux (natural layout): the window is the whole padded patch
+    if (S::CAPA && lane == 1) bulk_g2s(buf + MEQN * WW, A.aux + patch * 3ll * n2, 3 * WW * sizeof(double), bar);
+  } else {
     if (S::CAPA) {
       const double* ab = A.aux + patch * 3ll * n2 + (int64_t)(ty * T) * n + tx * T;
 #pragma unroll 1
@@ -354,6 +367,17 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int ntiles) {
     const double dtdx = A.dt / dx;   // square cells: dt/dy = dt/dx
     mbar_wait(&bars[b], (phase >> b) & 1u);
     phase ^= 1u << b;
+    if (!A.ring && A.tiles == 1) {     // rotated rows -> natural window rows (cell i at column i+1)
+      for (int r = opaque(threadIdx.x); r < MEQN * W; r += NT) {
+        double* row = sq + r * W;
+        const double a = row[W - 2], c = row[W - 1];
+#pragma unroll
+        for (int k = W - 1; k >= 2; --k) row[k] = row[k - 2];
+        row[0] = a;
+        row[1] = c;
+      }
+      __syncthreads();
+    }
     if (A.ring) {                      // this tile's ring: wait for all but the newest group,
       cp_async_wait<1>();              // make every thread's copies visible, then the BCs
       __syncthreads();
@@ -378,7 +402,7 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int ntiles) {
         const int t = opaque(threadIdx.x);
         if (t < T * T) {
           const int i = 1 + t % T, j = 1 + t / T;
-          double* o = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + 1 + j) * n + tx * T + 1 + i;
+          double* o = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + 1 + j) * n + tx * T + i - 1;
 #pragma unroll
           for (int k = 0; k < MEQN; ++k) o[(int64_t)k * n2] = sq[k * WW];
         }
@@ -508,7 +532,7 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int ntiles) {
       if (t < T * T) {
         const int i = 1 + t % T, j = 1 + t / T;
         const double rc = rcell(i, j);
-        double* o = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + 1 + j) * n + tx * T + 1 + i;
+        double* o = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + 1 + j) * n + tx * T + i - 1;
         const double* rt = ta + (j - 1) * (T + 2) + i;   // right(i, j) of component 0
         const double* lf = tb + (j - 1) * (T + 2) + i;   // left(i, j)
         const double* qs = sq + widx(i, j);
@@ -553,12 +577,11 @@ template <int MEQN, int T>
 __global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict__ qold, double* __restrict__ qnew,
                                                        int npatch, uint8_t* __restrict__ uflag,
                                                        double* __restrict__ uval) {
-  // One warp per patch.  Per component the padded rows 2..m+1 form one contiguous, 16-byte aligned
-  // block of m*n doubles: it is copied whole (the two ring columns on each side of q_new are
-  // scratch), so every DRAM sector is read and written in full -- no partial-sector
-  // read-modify-write.  Uniformity is tested on the interior columns only.
-  constexpr int n = T + 4, n2 = n * n, RP = n / 2;          // double2 per padded row
-  constexpr int E = MEQN * T * RP, NE = (E + 31) / 32;
+  // One warp per patch.  In the rotated storage the m interior cells of each row are the row's first
+  // m doubles (whole, aligned 32-byte sectors): exactly the interior is copied, so DRAM traffic is
+  // the compulsory read + write of q, with no partial-sector read-modify-write.
+  constexpr int n = T + 4, n2 = n * n, H = T / 2;           // double2 per interior row
+  constexpr int E = MEQN * T * H, NE = (E + 31) / 32;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < npatch; p += warps) {
@@ -568,21 +591,20 @@ __global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict_
 #pragma unroll
     for (int u = 0; u < NE; ++u) {
       const int e = lane + 32 * u;
-      const int k = e / (T * RP), r = e - k * (T * RP);
-      if (e < E) x[u] = __ldcs(reinterpret_cast<const double2*>(src + k * n2) + r);
+      const int k = e / (T * H), r = e - k * (T * H), row = r / H, c2 = r - row * H;
+      if (e < E) x[u] = __ldcs(reinterpret_cast<const double2*>(src + k * n2 + row * n) + c2);
     }
     double v0[MEQN];
 #pragma unroll
-    for (int k = 0; k < MEQN; ++k) v0[k] = __ldg(src + k * n2 + 2);
+    for (int k = 0; k < MEQN; ++k) v0[k] = __ldg(src + k * n2);
     bool diff = false;
 #pragma unroll
     for (int u = 0; u < NE; ++u) {
       const int e = lane + 32 * u;
       if (e < E) {
-        const int k = e / (T * RP), r = e - k * (T * RP);
-        __stcs(reinterpret_cast<double2*>(dst + k * n2) + r, x[u]);
-        const int c = r % RP;                               // pair index in the row: 1..RP-2 interior
-        if (c >= 1 && c <= RP - 2) diff |= (x[u].x != v0[k]) | (x[u].y != v0[k]);
+        const int k = e / (T * H), r = e - k * (T * H), row = r / H, c2 = r - row * H;
+        __stcs(reinterpret_cast<double2*>(dst + k * n2 + row * n) + c2, x[u]);
+        diff |= (x[u].x != v0[k]) | (x[u].y != v0[k]);
       }
     }
     const bool uni = !__any_sync(0xffffffffu, diff);
