@@ -302,7 +302,10 @@ static int update_local(fc_forest* f, double dt) {
   const fc_problem& p = f->prob;
   const bool fused = use_fused(f);
   bool filtered = false;
-  if (fused) {   // copy/classify + activity filter, then the step over the active patches only
+  // (tiny forests skip the filter: its two extra launches cost more than the tiles they save; the
+  // step kernel's own quiescent-window check still applies)
+  if (p.skip_quiescent && p.kind != FC_ADV_EDGEVEL_CAPA && (f->Pl >= 512 || fused)) {
+    // copy/classify + activity filter, then the step over the active patches' tiles only
     CK(cudaMemsetAsync(f->d_nactive, 0, sizeof(int32_t), f->stream));
     const int fr = launch_filter(p.kind, f->qold, f->qnew, (int)f->Pl, f->pl.m, f->d_uflag, f->d_uval, f->d_nbr,
                                  f->d_negmask, f->d_level, dt, f->pl.dx0, p.p0, p.p1, f->d_active, f->d_nactive,
@@ -470,6 +473,21 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
       f->fused = true;
       f->st.uniform_fast_path = 1;
     }
+  }
+  if (!f->d_nbr) {   // quiescent-filter tables for the ring (non-fused) path: any forest
+    std::vector<int32_t> nbr;
+    std::vector<uint8_t> nm;
+    rc = plan_activity(f->pl, pl.meqn, nbr, nm, err);
+    if (rc) { destroy(f); return fail(rc, err); }
+    const size_t Pl1 = std::max<int64_t>(1, f->Pl);
+    if ((e = cudaMalloc(&f->d_nbr, Pl1 * 8 * sizeof(int32_t))) != cudaSuccess ||
+        (e = cudaMalloc(&f->d_active, Pl1 * sizeof(int32_t))) != cudaSuccess ||
+        (e = cudaMalloc(&f->d_nactive, sizeof(int32_t))) != cudaSuccess ||
+        (e = cudaMalloc(&f->d_negmask, Pl1)) != cudaSuccess || (e = cudaMalloc(&f->d_uflag, Pl1)) != cudaSuccess ||
+        (e = cudaMalloc(&f->d_uval, Pl1 * pl.meqn * sizeof(double))) != cudaSuccess)
+      return cuda_fail(e, "cudaMalloc filter");
+    if (!nbr.empty()) cudaMemcpy(f->d_nbr, nbr.data(), nbr.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (!nm.empty()) cudaMemcpy(f->d_negmask, nm.data(), nm.size(), cudaMemcpyHostToDevice);
   }
   if (pl.nranks > 1) {
     if (f->manual) {

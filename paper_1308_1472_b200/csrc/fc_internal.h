@@ -112,5 +112,9 @@ int plan_build(const fc_forest_desc* d, Plan& pl, std::string& err);
 // build typed lists for `meqn` (component stride n^2); halo slots from pl.halo
 int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err);
 int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& err);
+// activity tables for the quiescent filter on any forest: nbr [Pl][8] / negmask [Pl] as in
+// RingSources; a patch with an AVG4 / INTERP / CORNER3 ghost record is always active (nbr[0] = -2)
+int plan_activity(const Plan& pl, int meqn, std::vector<int32_t>& nbr, std::vector<uint8_t>& negmask,
+                  std::string& err);
 
 }  // namespace fc

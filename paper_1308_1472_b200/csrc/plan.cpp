@@ -460,6 +460,41 @@ int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err) {
   return FC_OK;
 }
 
+int plan_activity(const Plan& pl, int meqn, std::vector<int32_t>& nbr, std::vector<uint8_t>& negmask,
+                  std::string& err) {
+  const int64_t n2 = (int64_t)pl.n * pl.n, G = n2 - (int64_t)pl.m * pl.m;
+  const int64_t Pl = pl.p1 - pl.p0;
+  nbr.assign((size_t)Pl * 8, -1);
+  negmask.assign((size_t)Pl, 0);
+  for (int64_t lp = 0; lp < Pl; ++lp) {
+    int nn = 0;
+    bool always = false;
+    for (int64_t r = 0; r < G && !always; ++r) {
+      const int32_t* o = pl.table.data() + (lp * G + r) * REC;
+      if (o[0] == OP_COPY) {
+        const int64_t q = o[1];
+        const int32_t id = (q >= pl.p0 && q < pl.p1) ? (int32_t)(q - pl.p0) : -2;
+        bool found = false;
+        for (int k = 0; k < nn; ++k) found |= nbr[lp * 8 + k] == id;
+        if (!found) {
+          if (nn >= 8 || id == -2) { always = true; break; }
+          nbr[lp * 8 + nn++] = id;
+        }
+      } else if (o[0] == OP_BCX || o[0] == OP_BCY) {
+        if (o[4] == FC_BC_WALL && meqn >= 3) negmask[lp] |= (uint8_t)(1u << (o[0] == OP_BCY ? 2 : 1));
+      } else {
+        always = true;   // averaged / interpolated / corner ghosts: not tested, always updated
+      }
+    }
+    if (always) {
+      for (int k = 0; k < 8; ++k) nbr[lp * 8 + k] = -1;
+      nbr[lp * 8] = -2;
+    }
+  }
+  (void)err;
+  return FC_OK;
+}
+
 int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& err) {
   const int m = pl.m, n = pl.n;
   const int64_t n2 = (int64_t)n * n, S = (int64_t)meqn * n2;

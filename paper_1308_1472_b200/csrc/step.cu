@@ -311,8 +311,13 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int ntiles) {
   using Sh = StepShape<S, T>;
   constexpr int MEQN = S::MEQN, W = Sh::W, WW = Sh::WW, EX = Sh::EX, E2 = Sh::E2;
   static_assert(E2 <= NT, "one round of corrections per sweep (single-writer L/R phases)");
-  if (A.active) ntiles = *A.nactive;   // tiles of the active list only (tile = patch)
-  auto tile_of = [&](int k) { return A.active ? A.active[k] : k; };
+  const int tiles2_ = A.tiles * A.tiles;
+  if (A.active) ntiles = *A.nactive * tiles2_;   // the tiles of the active patches only
+  auto tile_of = [&](int k) {
+    if (!A.active) return k;
+    const int a = k / tiles2_;
+    return A.active[a] * tiles2_ + (k - a * tiles2_);
+  };
   extern __shared__ __align__(128) double sm[];
   double* sbuf = sm;                                 // 2 x [MEQN + 3 aux][W][W] staging buffers
   double* scl = sbuf + 2 * Sh::BUF;                  // [NC][W][W] per-cell derived fields
@@ -577,34 +582,38 @@ template <int MEQN, int T>
 __global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict__ qold, double* __restrict__ qnew,
                                                        int npatch, uint8_t* __restrict__ uflag,
                                                        double* __restrict__ uval) {
-  // One warp per patch.  In the rotated storage the m interior cells of each row are the row's first
-  // m doubles (whole, aligned 32-byte sectors): exactly the interior is copied, so DRAM traffic is
-  // the compulsory read + write of q, with no partial-sector read-modify-write.
+  // One warp per patch (T = m here).  In the rotated storage the m interior cells of each row are
+  // the row's first m doubles (whole, aligned 32-byte sectors): exactly the interior is copied, so
+  // DRAM traffic is the compulsory read + write of q, with no partial-sector read-modify-write.
+  // Each lane issues up to 16 16-byte loads before using any.
   constexpr int n = T + 4, n2 = n * n, H = T / 2;           // double2 per interior row
-  constexpr int E = MEQN * T * H, NE = (E + 31) / 32;
+  constexpr int E = MEQN * T * H, NE = (E + 31) / 32, NC = NE < 16 ? NE : 16;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < npatch; p += warps) {
     const double* src = qold + (int64_t)p * MEQN * n2 + 2 * n;
     double* dst = qnew + (int64_t)p * MEQN * n2 + 2 * n;
-    double2 x[NE];
-#pragma unroll
-    for (int u = 0; u < NE; ++u) {
-      const int e = lane + 32 * u;
-      const int k = e / (T * H), r = e - k * (T * H), row = r / H, c2 = r - row * H;
-      if (e < E) x[u] = __ldcs(reinterpret_cast<const double2*>(src + k * n2 + row * n) + c2);
-    }
     double v0[MEQN];
 #pragma unroll
     for (int k = 0; k < MEQN; ++k) v0[k] = __ldg(src + k * n2);
     bool diff = false;
+#pragma unroll 1
+    for (int base = 0; base < E; base += 32 * NC) {
+      double2 x[NC];
 #pragma unroll
-    for (int u = 0; u < NE; ++u) {
-      const int e = lane + 32 * u;
-      if (e < E) {
+      for (int u = 0; u < NC; ++u) {
+        const int e = base + lane + 32 * u;
         const int k = e / (T * H), r = e - k * (T * H), row = r / H, c2 = r - row * H;
-        __stcs(reinterpret_cast<double2*>(dst + k * n2 + row * n) + c2, x[u]);
-        diff |= (x[u].x != v0[k]) | (x[u].y != v0[k]);
+        if (e < E) x[u] = __ldcs(reinterpret_cast<const double2*>(src + k * n2 + row * n) + c2);
+      }
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const int e = base + lane + 32 * u;
+        if (e < E) {
+          const int k = e / (T * H), r = e - k * (T * H), row = r / H, c2 = r - row * H;
+          __stcs(reinterpret_cast<double2*>(dst + k * n2 + row * n) + c2, x[u]);
+          diff |= (x[u].x != v0[k]) | (x[u].y != v0[k]);
+        }
       }
     }
     const bool uni = !__any_sync(0xffffffffu, diff);
@@ -675,6 +684,7 @@ static int launch_filter_s(const double* qold, double* qnew, int npatch, int m, 
   if (npatch <= 0) return 0;
   const int blocks_copy = 148 * 8;
   switch (m) {
+    case 32: k_copy_classify<S::MEQN, 32><<<blocks_copy, 256, 0, st>>>(qold, qnew, npatch, uflag, uval); break;
     case 16: k_copy_classify<S::MEQN, 16><<<blocks_copy, 256, 0, st>>>(qold, qnew, npatch, uflag, uval); break;
     case 8: k_copy_classify<S::MEQN, 8><<<blocks_copy, 256, 0, st>>>(qold, qnew, npatch, uflag, uval); break;
     case 4: k_copy_classify<S::MEQN, 4><<<blocks_copy, 256, 0, st>>>(qold, qnew, npatch, uflag, uval); break;
