@@ -304,7 +304,7 @@ static int update_local(fc_forest* f, double dt) {
   bool filtered = false;
   // (tiny forests skip the filter: its two extra launches cost more than the tiles they save; the
   // step kernel's own quiescent-window check still applies)
-  if (p.skip_quiescent && p.kind != FC_ADV_EDGEVEL_CAPA && (f->Pl >= 512 || fused)) {
+  if (p.skip_quiescent && p.kind != FC_ADV_EDGEVEL_CAPA && f->Pl >= 512) {
     // copy/classify + activity filter, then the step over the active patches' tiles only
     CK(cudaMemsetAsync(f->d_nactive, 0, sizeof(int32_t), f->stream));
     const int fr = launch_filter(p.kind, f->qold, f->qnew, (int)f->Pl, f->pl.m, f->d_uflag, f->d_uval, f->d_nbr,
