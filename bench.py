@@ -20,9 +20,7 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -83,59 +81,75 @@ def bytes_per_cell_update(w) -> int:
 
 # ---------------------------------------------------------------------------------------------
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Clock / throttle sampling during the timed region (the B200_PROFILING.md clocks line:
+    clocks.sm, clocks.max.sm, power.draw, clocks_event_reasons.{hw_slowdown, hw_thermal_slowdown,
+    sw_thermal_slowdown, sw_power_cap}).  NVML is polled from a thread every `period` s: the timed
+    region (~0.1-1 s) is shorter than nvidia-smi's own start-up, so `nvidia-smi -lms` saw nothing.
+    Each rank samples its own GPU (found by UUID); rank 0 reports the samples of every rank."""
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, gpus):
-        self.gpus = gpus
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
+    def __init__(self, device: int, period: float = 0.005):
+        import threading
+        import pynvml as nv
+        import torch
+        self.nv = nv
+        nv.nvmlInit()
+        self.h = None
+        try:
+            uid = str(torch.cuda.get_device_properties(device).uuid)
+            self.h = nv.nvmlDeviceGetHandleByUUID(uid if uid.startswith("GPU-") else "GPU-" + uid)
+        except Exception:
+            self.h = nv.nvmlDeviceGetHandleByIndex(device)
+        self.bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                     "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                     "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                     "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        self.period = period
+        self.rows = []
+        self.stop_ev = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        try:
+            pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+        except Exception:
+            pw = None
+        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.rows.append((sm, mx, pw, [k for k, b in self.bits.items() if rs & b]))
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self._sample()
+            except Exception:
+                pass
+            self.stop_ev.wait(self.period)
 
     def start(self):
-        try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.p = None
+        self.th.start()
 
     def stop(self):
-        if self.p is None:
-            return None
-        self.p.terminate()
+        self.stop_ev.set()
+        self.th.join(timeout=5)
         try:
-            self.p.wait(timeout=5)
+            self._sample()           # at least one sample even for a very short region
         except Exception:
-            self.p.kill()
-        self.f.flush()
-        rows = []
-        for line in open(self.f.name):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                idx = int(parts[0])
-            except ValueError:
-                continue
-            if idx not in self.gpus:
-                continue
-            rows.append(parts)
-        os.unlink(self.f.name)
+            pass
+        return self.rows
+
+    @staticmethod
+    def summary(rows):
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for k, nm in enumerate(names):
-                if r[5 + k].lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(rows),
-                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())
-                if any(r[3].replace(".", "").isdigit() for r in rows) else None}
+        sm = [r[0] for r in rows]
+        pw = [r[2] for r in rows if r[2] is not None]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in rows),
+                "sm_mhz_min": min(sm), "reasons": sorted({x for r in rows for x in r[3]}),
+                "samples": len(rows), "power_w_max": max(pw) if pw else None,
+                "source": "NVML polled every 5 ms during the timed region (all ranks)"}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -277,7 +291,12 @@ def main():
         dt, _ = steps(args.warmup, w.dt0)
         f.reset_stats()
         f.set_timing(True)
-        clocks = Clocks(list(range(max(1, world)))) if (rank == 0 and monitor) else None
+        clocks = None
+        if monitor:
+            try:
+                clocks = Clocks(local)
+            except Exception as e:   # NVML unavailable: reported as no samples
+                print(f"[bench] clock sampling unavailable: {e}", file=sys.stderr)
         barrier()
         torch.cuda.synchronize()
         if clocks:
@@ -288,7 +307,12 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        clk = clocks.stop() if clocks else None
+        rows = clocks.stop() if clocks else []
+        if world > 1 and monitor:
+            allrows = [None] * world
+            dist.all_gather_object(allrows, rows)
+            rows = [r for rr in allrows for r in (rr or [])]
+        clk = Clocks.summary(rows) if monitor else None
         ms = allmax(ev0.elapsed_time(ev1))
         st = f.stats()
         f.set_timing(False)

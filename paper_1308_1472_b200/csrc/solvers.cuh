@@ -8,7 +8,8 @@
 // Interface used by k_step (step.cu):
 //   NC          per-cell derived fields precomputed once per staged cell (shared by the 4 edges
 //               of the cell in both sweeps): Euler {sqrt(rho), u, v, H, c}; SWE {sqrt(h), u, v}
-//   NS          per-edge scratch written by the normal solve (phase 1) and read in phase 2:
+//   NS          per-edge scratch written by the normal solve (phase 1) and read in phase 2
+//               (NSA >= NS allocated: slots PB..PB+MEQN-1 receive the edge's L part in phase 2):
 //               AdvConst / AdvEdgeCapa {dq}; SweRoe {a1..a3, u, v, c, 1/c};
 //               EulerRoe {a1..a4, u, v, H, c, 1/c, A-dq (Harten-Hyman fixed)} (A+dq = sum s W - A-dq)
 //   riemann<D>  normal solve on one edge (D = 1: x, normal momentum = component 1; D = 2: y)
@@ -68,8 +69,8 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
 // the tile's edges of max(r s, -r s) over the waves, which for a uniform state is r (|u_n| + c).
 // Block-uniform result (every thread returns the same value, or its share for AdvEdgeCapa).
 struct AdvConst {
-  static constexpr int MEQN = 1, MW = 1, NS = 1, NC = 0;
-  static constexpr bool CAPA = false;
+  static constexpr int MEQN = 1, MW = 1, NS = 1, NC = 0, PB = NS, NSA = PB + MEQN;
+  static constexpr bool CAPA = false, AM_STORED = false;
   __device__ static double quiescent_cfl(const double*, int, const SolverParams& P, const double*, double dtdx,
                                          int, int, int, int) {
     return dtdx * fmax(fabs(P.p0), fabs(P.p1));
@@ -106,8 +107,8 @@ struct AdvConst {
 
 // ----------------------------------------------------------------------------------------------
 struct AdvEdgeCapa {
-  static constexpr int MEQN = 1, MW = 1, NS = 1, NC = 0;
-  static constexpr bool CAPA = true;
+  static constexpr int MEQN = 1, MW = 1, NS = 1, NC = 0, PB = NS, NSA = PB + MEQN;
+  static constexpr bool CAPA = true, AM_STORED = false;
   // edge velocities vary per edge: each thread scans a share of the tile's x- and y-edges
   __device__ static double quiescent_cfl(const double*, int WW, const SolverParams&, const double* sa,
                                          double dtdx, int T, int W, int tid, int NT) {
@@ -162,8 +163,8 @@ struct AdvEdgeCapa {
 // a1 = ((u+c) dh - dn)/(2c), a2 = dt - vt dh, a3 = ((c-u) dh + dn)/(2c); r1 = (1, u-c, v),
 // r2 = (0, 0, 1)_t, r3 = (1, u+c, v); speeds u-c, u, u+c (normal/tangential per direction).
 struct SweRoe {
-  static constexpr int MEQN = 3, MW = 3, NS = 7, NC = 3;
-  static constexpr bool CAPA = false;
+  static constexpr int MEQN = 3, MW = 3, NS = 7, NC = 3, PB = NS, NSA = PB + MEQN;
+  static constexpr bool CAPA = false, AM_STORED = false;
   __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, const double*,
                                          double dtdx, int, int, int, int) {
     const double h = q[0], ih = 1.0 / h;
@@ -267,8 +268,9 @@ struct SweRoe {
 // r1 = (1, un-c, vt, H - un c), r2 = (1, un, vt, (un^2+vt^2)/2), r3 = (0, 0, 1, vt)_t,
 // r4 = (1, un+c, vt, H + un c); speeds un-c, un, un, un+c.
 struct EulerRoe {
-  static constexpr int MEQN = 4, MW = 4, NS = 13, NC = 5;
-  static constexpr bool CAPA = false;
+  // PB: the edge's L part (A-dq + F~) overwrites its A-dq slots once they are consumed
+  static constexpr int MEQN = 4, MW = 4, NS = 13, NC = 5, PB = 9, NSA = NS;
+  static constexpr bool CAPA = false, AM_STORED = true;
   __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, const double*,
                                          double dtdx, int, int, int, int) {
     const double rho = q[0], ir = 1.0 / rho;

@@ -58,6 +58,7 @@ struct StepArgs {
   LimiterCoef lim;
   int m, tiles;                       // tiles per side
   unsigned long long* cfl_bits;
+  double* fbuf;                       // method3 = 1 only: per-CTA F~ of each correction edge [MEQN][E2]
 };
 
 // ---- TMA bulk copies + mbarrier (sm_90+ / sm_100a) -------------------------------------------
@@ -108,70 +109,68 @@ struct StepShape {
   static constexpr int E2 = (T + 1) * (T + 2);   // edges with corrections / transverse
   static constexpr int NTR = S::MEQN * T * (T + 2);
   static constexpr int BUF = (S::MEQN + (S::CAPA ? 3 : 0)) * WW;   // one staged tile (q + aux)
-  static constexpr size_t smem_doubles = (size_t)2 * BUF + (size_t)S::NC * WW + (size_t)S::NS * EX +
-                                         S::MEQN * T * T + 2 * NTR;
+  static constexpr size_t smem_doubles = (size_t)2 * BUF + (size_t)S::NC * WW + (size_t)S::NSA * EX +
+                                         (size_t)S::MEQN * E2 + S::MEQN * T * T + 2 * NTR;
   static constexpr size_t smem_bytes = smem_doubles * sizeof(double);
 };
 
-// default A-+dq from the waves: sum_p min/max(s_p, 0) W_p (Euler overrides: Harten-Hyman A-dq)
-template <class S, int D, class = void>
-struct FluctFromWaves {
-  __device__ static void run(const double*, int, const double (*W)[S::MEQN], const double* s, double* am,
-                             double* ap) {
-#pragma unroll
-    for (int k = 0; k < S::MEQN; ++k) { am[k] = 0.0; ap[k] = 0.0; }
-#pragma unroll
-    for (int p = 0; p < S::MW; ++p) {
-      double sm, sp;
-      split0(s[p], sm, sp);
-#pragma unroll
-      for (int k = 0; k < S::MEQN; ++k) { am[k] = fma(sm, W[p][k], am[k]); ap[k] = fma(sp, W[p][k], ap[k]); }
-    }
-  }
-};
-template <int D>
-struct FluctFromWaves<EulerRoe, D, void> {
-  __device__ static void run(const double* sc, int st, const double (*W)[4], const double* s, double* am,
-                             double* ap) {
-    EulerRoe::fluct_w<D>(sc, st, W, s, am, ap);
-  }
-};
-
-// fluctuations + second-order correction F~ (limiter on the upwind neighbour's unlimited wave)
-// + CFL of one edge (phase 2 of a sweep).  Waves are reconstructed once; the limiter is
-// branch-free (a zero wave contributes c phi W = 0 whatever phi is).
+// Phase 2a of a sweep, one correction edge: fluctuations A-+dq, second-order correction F~ (MC /
+// minmod limiter on the upwind neighbour's *unlimited* wave) and the edge CFL.
+// Waves are reconstructed one at a time from the compact scratch (no wave array stays live):
+// A-dq = sum_p min(s_p,0) W_p, A+dq = sum_p max(s_p,0) W_p, or, for Euler, A-dq is the Harten-Hyman
+// fixed value stored by the normal solve and A+dq = sum_p s_p W_p - A-dq.  Out: P = A-dq + F~ (the
+// edge's L part, entering the cell on its low side), Q = A+dq - F~ (R part), F = F~.
 template <class S, int D>
 __device__ __forceinline__ void edge_correction(const double* sc, const double* scm, const double* scp,
                                                 int st, const StepArgs& A, AuxCell ar, double rl, double rr,
-                                                double& cfl, double* am, double* ap, double* F) {
+                                                double& cfl, double* P, double* Q, double* F) {
   constexpr int MEQN = S::MEQN;
-  double W[S::MW][MEQN], s[S::MW];
+  double am[MEQN], ap[MEQN];
+#pragma unroll
+  for (int k = 0; k < MEQN; ++k) {
+    am[k] = 0.0;   // (Euler: the stored A-dq is read after the wave loop, fewer live registers)
+    ap[k] = 0.0;
+    F[k] = 0.0;
+  }
+  const double rav = 0.5 * (rl + rr);
 #pragma unroll
   for (int p = 0; p < S::MW; ++p) {
-    S::template wave<D>(sc, st, p, A.sp, W[p]);
-    s[p] = S::template speed<D>(sc, st, p, A.sp, ar);
-    cfl = fmax(cfl, fmax(rr * s[p], -rl * s[p]));
-  }
-  FluctFromWaves<S, D>::run(sc, st, W, s, am, ap);
+    double W[MEQN];
+    S::template wave<D>(sc, st, p, A.sp, W);
+    const double s = S::template speed<D>(sc, st, p, A.sp, ar);
+    cfl = fmax(cfl, fmax(rr * s, -rl * s));
+    if (S::AM_STORED) {
 #pragma unroll
-  for (int k = 0; k < MEQN; ++k) F[k] = 0.0;
-  if (A.method2 == 2) {
-    const double rav = 0.5 * (rl + rr);
+      for (int k = 0; k < MEQN; ++k) ap[k] = fma(s, W[k], ap[k]);
+    } else {
+      double sm, sp;
+      split0(s, sm, sp);
 #pragma unroll
-    for (int p = 0; p < S::MW; ++p) {
+      for (int k = 0; k < MEQN; ++k) { am[k] = fma(sm, W[k], am[k]); ap[k] = fma(sp, W[k], ap[k]); }
+    }
+    if (A.method2 == 2) {
       double WI[MEQN];
-      S::template wave<D>(s[p] > 0.0 ? scm : scp, st, p, A.sp, WI);
-      double wn2 = W[p][0] * W[p][0], dot = WI[0] * W[p][0];
+      S::template wave<D>(s > 0.0 ? scm : scp, st, p, A.sp, WI);
+      double wn2 = W[0] * W[0], dot = WI[0] * W[0];
 #pragma unroll
-      for (int k = 1; k < MEQN; ++k) { wn2 = fma(W[p][k], W[p][k], wn2); dot = fma(WI[k], W[p][k], dot); }
+      for (int k = 1; k < MEQN; ++k) { wn2 = fma(W[k], W[k], wn2); dot = fma(WI[k], W[k], dot); }
       if (wn2 != 0.0) {   // a zero wave adds nothing (also skips the limiter in quiescent flow)
         const double phi = limiter_phi(A.lim, dot * fast_rcp(wn2));
-        const double as = fabs(s[p]);
+        const double as = fabs(s);
         const double c = 0.5 * as * (1.0 - as * rav) * phi;
 #pragma unroll
-        for (int k = 0; k < MEQN; ++k) F[k] = fma(c, W[p][k], F[k]);
+        for (int k = 0; k < MEQN; ++k) F[k] = fma(c, W[k], F[k]);
       }
     }
+  }
+#pragma unroll
+  for (int k = 0; k < MEQN; ++k) {
+    if (S::AM_STORED) {
+      am[k] = sc[(S::PB + k) * st];
+      ap[k] -= am[k];
+    }
+    P[k] = am[k] + F[k];
+    Q[k] = ap[k] - F[k];
   }
 }
 
@@ -306,11 +305,18 @@ __device__ __forceinline__ void window_bc(const StepArgs& A, int tile, double* s
 
 // Persistent CTAs: each loops over tiles blockIdx.x, + gridDim.x, ...; the next tile's window is
 // bulk-copied (TMA engine) into the other staging buffer while the current one is computed.
+// register cap for MINB resident CTAs of NT threads.  Registers are split between the 4 SM
+// sub-partitions: the one holding ceil(warps / 4) warps bounds the per-thread count (8-register units)
+constexpr int step_maxnreg(int nt, int minb) {
+  return (16384 / (((nt * minb / 32) + 3) / 4 * 32)) / 8 * 8 > 255 ? 255
+                                                                 : (16384 / (((nt * minb / 32) + 3) / 4 * 32)) / 8 * 8;
+}
+
 template <class S, int T, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int ntiles) {
+__global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step(StepArgs A, int ntiles) {
   using Sh = StepShape<S, T>;
   constexpr int MEQN = S::MEQN, W = Sh::W, WW = Sh::WW, EX = Sh::EX, E2 = Sh::E2;
-  static_assert(E2 <= NT, "one round of corrections per sweep (single-writer L/R phases)");
+  static_assert(E2 <= NT && T * (T + 2) <= NT, "one round of edges / receiving cells per phase");
   const int tiles2_ = A.tiles * A.tiles;
   if (A.active) ntiles = *A.nactive * tiles2_;   // the tiles of the active patches only
   auto tile_of = [&](int k) {
@@ -321,10 +327,12 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int ntiles) {
   extern __shared__ __align__(128) double sm[];
   double* sbuf = sm;                                 // 2 x [MEQN + 3 aux][W][W] staging buffers
   double* scl = sbuf + 2 * Sh::BUF;                  // [NC][W][W] per-cell derived fields
-  double* scr = scl + S::NC * WW;                    // [NS][EX] per-edge scratch
-  double* dq = scr + S::NS * EX;                     // [MEQN][T][T]
+  double* scr = scl + S::NC * WW;                    // [NSA][EX] per-edge scratch
+  double* qrp = scr + S::NSA * EX;                   // [MEQN][E2] per-edge R part (A+dq - F~)
+  double* dq = qrp + MEQN * E2;                      // [MEQN][T][T]
   double* ta = dq + MEQN * T * T;                    // x: up / y: right
   double* tb = ta + Sh::NTR;                         // x: down / y: left
+  double* fb = A.fbuf ? A.fbuf + (int64_t)blockIdx.x * MEQN * E2 : nullptr;
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ double wmax[(NT + 31) / 32];
 
@@ -431,39 +439,57 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int ntiles) {
                              A.sp, scr + e, EX);
     }
     __syncthreads();
+    // X2a: fluctuations, limited correction F~ and CFL per correction edge (i in 1..T+1, row j)
     {
       const int e2 = opaque(threadIdx.x);
-      const bool v = e2 < E2;
-      const int i = v ? 1 + e2 % (T + 1) : 1, j = v ? e2 / (T + 1) : 0;
-      double Rv[MEQN], bmR[MEQN], bpR[MEQN];
-      const double rl = rcell(i - 1, j), rr = rcell(i, j);
-      if (v) {
+      if (e2 < E2) {
+        const int i = 1 + e2 % (T + 1), j = e2 / (T + 1);
         const int e = j * (T + 3) + i;
-        double am[MEQN], ap[MEQN], F[MEQN], X[MEQN], bm[MEQN], bp[MEQN];
-        edge_correction<S, 1>(scr + e, scr + e - 1, scr + e + 1, EX, A, auxc(i, j), rl, rr, cfl, am, ap, F);
-        const double m3 = A.method3 == 2 ? 1.0 : 0.0;
-        if (i - 1 >= 1) {   // L part -> left cell (i-1, j): first writer
+        double P[MEQN], Q[MEQN], F[MEQN];
+        edge_correction<S, 1>(scr + e, scr + e - 1, scr + e + 1, EX, A, auxc(i, j), rcell(i - 1, j), rcell(i, j),
+                              cfl, P, Q, F);
 #pragma unroll
-          for (int k = 0; k < MEQN; ++k) X[k] = am[k] + m3 * F[k];
-          edge_transverse<S, 1>(scr + e, EX, A, X, auxc(i - 1, j), auxc(i - 1, j + 1), bm, bp);
+        for (int k = 0; k < MEQN; ++k) { scr[(S::PB + k) * EX + e] = P[k]; qrp[k * E2 + e2] = Q[k]; }
+        if (A.method3 == 1) {   // transverse of A-+dq alone: keep F~ (CTA-private global scratch)
+#pragma unroll
+          for (int k = 0; k < MEQN; ++k) fb[k * E2 + e2] = F[k];
+        }
+      }
+    }
+    __syncthreads();
+    // X2b: one thread per receiving cell (i in 1..T, row j in 0..T+1): the L part of its right edge
+    // and the R part of its left edge -> dq (interior rows) and the transverse split of both into
+    // the y-edge accumulators up (ta) / down (tb).  Single writer per cell: no atomics, no zero fill.
+    {
+      const int t = opaque(threadIdx.x);
+      if (t < T * (T + 2)) {
+        const int i = 1 + t % T, j = t / T;
+        const int er = j * (T + 3) + i + 1, el = er - 1, e2l = j * (T + 1) + (i - 1);
+        const double r = rcell(i, j);
+        double XL[MEQN], XR[MEQN], bm[MEQN], bp[MEQN], bmR[MEQN], bpR[MEQN];
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) { XL[k] = scr[(S::PB + k) * EX + er]; XR[k] = qrp[k * E2 + e2l]; }
+        if (j >= 1 && j <= T) {
 #pragma unroll
           for (int k = 0; k < MEQN; ++k) {
-            if (j >= 1 && j <= T) dq[(k * T + (j - 1)) * T + (i - 2)] = -rl * (am[k] + F[k]);
-            ta[(k * (T + 2) + j) * T + (i - 2)] = -0.5 * rl * bp[k];
-            tb[(k * (T + 2) + j) * T + (i - 2)] = -0.5 * rl * bm[k];
+            double d = -r * XL[k];
+            d -= r * XR[k];
+            dq[(k * T + (j - 1)) * T + (i - 1)] = d;
           }
         }
+        if (A.method3 == 1) {
 #pragma unroll
-        for (int k = 0; k < MEQN; ++k) { X[k] = ap[k] - m3 * F[k]; Rv[k] = ap[k] - F[k]; }
-        edge_transverse<S, 1>(scr + e, EX, A, X, auxc(i, j), auxc(i, j + 1), bmR, bpR);
-      }
-      __syncthreads();
-      if (v && i <= T) {    // R part -> right cell (i, j)
+          for (int k = 0; k < MEQN; ++k) { XL[k] -= fb[k * E2 + e2l + 1]; XR[k] += fb[k * E2 + e2l]; }
+        }
+        edge_transverse<S, 1>(scr + er, EX, A, XL, auxc(i, j), auxc(i, j + 1), bm, bp);
+        edge_transverse<S, 1>(scr + el, EX, A, XR, auxc(i, j), auxc(i, j + 1), bmR, bpR);
 #pragma unroll
         for (int k = 0; k < MEQN; ++k) {
-          if (j >= 1 && j <= T) dq[(k * T + (j - 1)) * T + (i - 1)] -= rr * Rv[k];
-          ta[(k * (T + 2) + j) * T + (i - 1)] -= 0.5 * rr * bpR[k];
-          tb[(k * (T + 2) + j) * T + (i - 1)] -= 0.5 * rr * bmR[k];
+          double u = -0.5 * r * bp[k], d = -0.5 * r * bm[k];
+          u -= 0.5 * r * bpR[k];
+          d -= 0.5 * r * bmR[k];
+          ta[(k * (T + 2) + j) * T + (i - 1)] = u;
+          tb[(k * (T + 2) + j) * T + (i - 1)] = d;
         }
       }
     }
@@ -493,40 +519,58 @@ __global__ void __launch_bounds__(NT, MINB) k_step(StepArgs A, int ntiles) {
                              A.sp, scr + e, EX);
     }
     __syncthreads();
+    // Y2a: per correction edge j in 1..T+1 of column i in 0..T+1
     {
       const int e2 = opaque(threadIdx.x);
-      const bool v = e2 < E2;
-      const int i = v ? e2 % (T + 2) : 0, j = v ? 1 + e2 / (T + 2) : 1;
-      double Rv[MEQN], bmR[MEQN], bpR[MEQN];
-      const double sl = rcell(i, j - 1), sr = rcell(i, j);
-      if (v) {
+      if (e2 < E2) {
+        const int i = e2 % (T + 2), j = 1 + e2 / (T + 2);
         const int e = j * (T + 2) + i;
-        double am[MEQN], ap[MEQN], F[MEQN], X[MEQN], bm[MEQN], bp[MEQN];
-        edge_correction<S, 2>(scr + e, scr + e - (T + 2), scr + e + (T + 2), EX, A, auxc(i, j), sl, sr, cfl,
-                              am, ap, F);
-        const double m3 = A.method3 == 2 ? 1.0 : 0.0;
-        if (j - 1 >= 1) {   // L part -> lower cell (i, j-1)
+        double P[MEQN], Q[MEQN], F[MEQN];
+        edge_correction<S, 2>(scr + e, scr + e - (T + 2), scr + e + (T + 2), EX, A, auxc(i, j), rcell(i, j - 1),
+                              rcell(i, j), cfl, P, Q, F);
 #pragma unroll
-          for (int k = 0; k < MEQN; ++k) X[k] = am[k] + m3 * F[k];
-          edge_transverse<S, 2>(scr + e, EX, A, X, auxc(i, j - 1), auxc(i + 1, j - 1), bm, bp);
+        for (int k = 0; k < MEQN; ++k) { scr[(S::PB + k) * EX + e] = P[k]; qrp[k * E2 + e2] = Q[k]; }
+        if (A.method3 == 1) {
+#pragma unroll
+          for (int k = 0; k < MEQN; ++k) fb[k * E2 + e2] = F[k];
+        }
+      }
+    }
+    __syncthreads();
+    // Y2b: one thread per receiving cell (column i in 0..T+1, j in 1..T): L part of its top edge, R
+    // part of its bottom edge -> dq (interior columns), transverse into the x-edge accumulators
+    // right (ta) / left (tb)
+    {
+      const int t = opaque(threadIdx.x);
+      if (t < T * (T + 2)) {
+        const int i = t % (T + 2), j = 1 + t / (T + 2);
+        const int et = (j + 1) * (T + 2) + i, eb = et - (T + 2), e2b = (j - 1) * (T + 2) + i;
+        const double r = rcell(i, j);
+        double XL[MEQN], XR[MEQN], bm[MEQN], bp[MEQN], bmR[MEQN], bpR[MEQN];
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) { XL[k] = scr[(S::PB + k) * EX + et]; XR[k] = qrp[k * E2 + e2b]; }
+        if (i >= 1 && i <= T) {
 #pragma unroll
           for (int k = 0; k < MEQN; ++k) {
-            if (i >= 1 && i <= T) dq[(k * T + (j - 2)) * T + (i - 1)] -= sl * (am[k] + F[k]);
-            ta[(k * T + (j - 2)) * (T + 2) + i] = -0.5 * sl * bp[k];
-            tb[(k * T + (j - 2)) * (T + 2) + i] = -0.5 * sl * bm[k];
+            double d = dq[(k * T + (j - 1)) * T + (i - 1)];
+            d -= r * XL[k];
+            d -= r * XR[k];
+            dq[(k * T + (j - 1)) * T + (i - 1)] = d;
           }
         }
+        if (A.method3 == 1) {
 #pragma unroll
-        for (int k = 0; k < MEQN; ++k) { X[k] = ap[k] - m3 * F[k]; Rv[k] = ap[k] - F[k]; }
-        edge_transverse<S, 2>(scr + e, EX, A, X, auxc(i, j), auxc(i + 1, j), bmR, bpR);
-      }
-      __syncthreads();
-      if (v && j <= T) {    // R part -> upper cell (i, j)
+          for (int k = 0; k < MEQN; ++k) { XL[k] -= fb[k * E2 + e2b + (T + 2)]; XR[k] += fb[k * E2 + e2b]; }
+        }
+        edge_transverse<S, 2>(scr + et, EX, A, XL, auxc(i, j), auxc(i + 1, j), bm, bp);
+        edge_transverse<S, 2>(scr + eb, EX, A, XR, auxc(i, j), auxc(i + 1, j), bmR, bpR);
 #pragma unroll
         for (int k = 0; k < MEQN; ++k) {
-          if (i >= 1 && i <= T) dq[(k * T + (j - 1)) * T + (i - 1)] -= sr * Rv[k];
-          ta[(k * T + (j - 1)) * (T + 2) + i] -= 0.5 * sr * bpR[k];
-          tb[(k * T + (j - 1)) * (T + 2) + i] -= 0.5 * sr * bmR[k];
+          double u = -0.5 * r * bp[k], d = -0.5 * r * bm[k];
+          u -= 0.5 * r * bpR[k];
+          d -= 0.5 * r * bmR[k];
+          ta[(k * T + (j - 1)) * (T + 2) + i] = u;
+          tb[(k * T + (j - 1)) * (T + 2) + i] = d;
         }
       }
     }
@@ -733,7 +777,15 @@ static int launch_step_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   const int64_t ntiles = npatch * a.tiles * a.tiles;
   if (ntiles >= (1ll << 31)) return -1;
   const int64_t grid = ntiles < resident ? ntiles : resident;   // (active list: at most ntiles)
-  k_step<S, T, NT, MINB><<<(unsigned)grid, NT, smem, st>>>(a, (int)ntiles);
+  StepArgs b = a;
+  b.fbuf = nullptr;
+  if (a.method3 == 1) {      // F~ scratch for the (rare) method3 = 1 transverse variant, kept for the
+    static double* fbuf = nullptr;   // process lifetime (one per instantiation, resident CTAs x E2)
+    if (!fbuf && cudaMalloc(&fbuf, (size_t)resident * S::MEQN * StepShape<S, T>::E2 * sizeof(double)) != cudaSuccess)
+      return -1;
+    b.fbuf = fbuf;
+  }
+  k_step<S, T, NT, MINB><<<(unsigned)grid, NT, smem, st>>>(b, (int)ntiles);
   return 1;
 }
 

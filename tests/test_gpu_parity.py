@@ -82,6 +82,27 @@ def test_parity_against_oracle(w, skip):
     assert_parity(w, qg, qo, cg, co)
 
 
+VARIANTS = [(1, 2, oracle.LIM_MC), (2, 1, oracle.LIM_MC), (2, 0, oracle.LIM_MC),
+            (2, 2, oracle.LIM_MINMOD), (2, 2, oracle.LIM_NONE)]
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=lambda v: f"m2_{v[0]}_m3_{v[1]}_lim{v[2]}")
+@pytest.mark.parametrize("w", [c5(level=2, m=16, steps=20), c3(level=1, m=32, steps=20), c2(steps=20),
+                               c4_workload(base_level=1, m=16, steps=20)], ids=lambda w: w.name)
+def test_parity_method_variants(w, variant):
+    """method2 = 1 (no F~), method3 = 1 (transverse of A-+dq alone) / 0 (none), minmod and no
+    limiter: every variant of the update (SURVEY §8(b) fc_set_problem) against the
+    oracle, full update and quiescent shortcut."""
+    import dataclasses
+    w = dataclasses.replace(w, method2=variant[0], method3=variant[1], limiter=variant[2])
+    if variant[1] == 0:   # without transverse terms the unsplit scheme is stable only to CFL 1/2
+        w = dataclasses.replace(w, dt0=0.5 * w.dt0, cfl_target=0.45)
+    qo, co, do = oracle.run(w)
+    for skip in (0, 1):
+        qg, cg, _ = fc.run(w, dt_list=do, skip_quiescent=skip)
+        assert_parity(w, qg, qo, cg, co)
+
+
 @pytest.mark.parametrize("w", [c5(level=3, m=16, steps=40), c3(level=2, m=32, steps=40),
                                c4_workload(base_level=2, m=16, steps=40)], ids=lambda w: w.name)
 def test_quiescent_shortcut_is_exact(w):

@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--level", type=int, default=None)
     ap.add_argument("--m", type=int, default=None)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--skip", type=int, default=1, help="skip_quiescent (0 = full update of every tile)")
     a = ap.parse_args()
     from workloads.configs import make_config
     from paper_1308_1472_b200 import fc
@@ -24,7 +25,7 @@ def main():
     if a.m is not None:
         kw["m"] = a.m
     w = make_config(a.config, **kw)
-    q, cfl, dts = fc.run(w, steps=a.steps)
+    q, cfl, dts = fc.run(w, steps=a.steps, skip_quiescent=a.skip)
     print(f"{w.name}: {a.steps} steps, cells {w.cells}, cfl {cfl[-1]:.6f}")
 
 
