@@ -108,7 +108,9 @@ struct StepShape {
   static constexpr int EX = (T + 3) * (T + 2);   // edges per sweep (incl. limiter neighbours)
   static constexpr int E2 = (T + 1) * (T + 2);   // edges with corrections / transverse
   static constexpr int NTR = S::MEQN * T * (T + 2);
-  static constexpr int BUF = (S::MEQN + (S::CAPA ? 3 : 0)) * WW;   // one staged tile (q + aux)
+  // one staged tile: q [MEQN][W][W] (+2 doubles: the single-copy whole-patch staging lands at +2,
+  // see stage_tile) then aux [3][W][W] at offset MEQN WW + 2
+  static constexpr int BUF = S::MEQN * WW + 2 + (S::CAPA ? 3 : 0) * WW;
   static constexpr size_t smem_doubles = (size_t)2 * BUF + (size_t)S::NC * WW + (size_t)S::NSA * EX +
                                          (size_t)S::MEQN * E2 + S::MEQN * T * T + 2 * NTR;
   static constexpr size_t smem_bytes = smem_doubles * sizeof(double);
@@ -214,15 +216,18 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
       // rotated storage: the m interior cells of a row are its first m doubles
       bulk_g2s(buf + k * WW + (row + 2) * W + 2, qb + (int64_t)k * n2 + (row + 2) * n, T * sizeof(double), bar);
     }
-    if (S::CAPA && lane == 0) bulk_g2s(buf + MEQN * WW, A.aux + (int64_t)patch * 3 * n2, abytes, bar);
+    if (S::CAPA && lane == 0) bulk_g2s(buf + MEQN * WW + 2, A.aux + (int64_t)patch * 3 * n2, abytes, bar);
     return;
   }
-  constexpr uint32_t bytes = (uint32_t)Sh::BUF * sizeof(double);
+  constexpr uint32_t bytes = (uint32_t)(Sh::BUF - 2) * sizeof(double);
   if (lane == 0) mbar_expect_tx(bar, bytes);
   __syncwarp();
-  if (A.tiles == 1) {        // the window is the whole (rotated) padded patch: one contiguous copy;
-                             // the kernel un-rotates its rows in shared memory
-    if (lane == 0) bulk_g2s(buf, A.qold + patch * (int64_t)MEQN * n2, MEQN * WW * sizeof(double), bar);
+  if (A.tiles == 1) {        // the window is the whole padded patch: one contiguous copy of its
+                             // rotated storage to buf + 2.  Storage row r holds cells 1..m+2 then the
+                             // ghosts -1, 0 (column (i-1) mod n), so at +2 every cell i >= 1 lands at
+                             // its natural window position and the ghost pair of flattened row R
+                             // lands at the start of row R+1: the kernel reads ghosts there (gsh)
+    if (lane == 0) bulk_g2s(buf + 2, A.qold + patch * (int64_t)MEQN * n2, MEQN * WW * sizeof(double), bar);
   } else {                   // q: per (component, window row) the storage row is rotated (cell i at
                              // column (i-1) mod n), so a window row is one piece, or two for the
                              // leftmost tile (ghost cells -1, 0 live at the end of the storage row)
@@ -240,14 +245,14 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
     }
   }
   if (A.tiles == 1) {        // aux (natural layout): the window is the whole padded patch
-    if (S::CAPA && lane == 1) bulk_g2s(buf + MEQN * WW, A.aux + patch * 3ll * n2, 3 * WW * sizeof(double), bar);
+    if (S::CAPA && lane == 1) bulk_g2s(buf + MEQN * WW + 2, A.aux + patch * 3ll * n2, 3 * WW * sizeof(double), bar);
   } else {
     if (S::CAPA) {
       const double* ab = A.aux + patch * 3ll * n2 + (int64_t)(ty * T) * n + tx * T;
 #pragma unroll 1
       for (int r = lane; r < 3 * W; r += 32) {
         const int k = r / W, b = r - k * W;
-        bulk_g2s(buf + MEQN * WW + r * W, ab + (int64_t)k * n2 + b * n, W * sizeof(double), bar);
+        bulk_g2s(buf + MEQN * WW + 2 + r * W, ab + (int64_t)k * n2 + b * n, W * sizeof(double), bar);
       }
     }
   }
@@ -339,6 +344,7 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
   const int tid = threadIdx.x;
   const int tiles2 = A.tiles * A.tiles;
   const int n = A.m + 4, n2 = n * n;
+  const int gsh = (!A.ring && A.tiles == 1) ? W : 0;   // see stage_tile / qidx
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -359,16 +365,24 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
     const int b = it & 1;
     const int tile = tile_of(kt);
     const int knext = kt + gridDim.x;
-    if (tid < 32 && knext < ntiles) {  // the other buffer was released by the previous tile's last barrier
-      fence_proxy_async();
-      stage_tile<S, T>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF, &bars[b ^ 1], tid);
-    }
-    if (A.ring) {                      // this thread's ring cells of the next tile: one cp.async group
-      if (knext < ntiles) gather_ring<S, T, NT>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF);
-      cp_async_commit();
-    }
+    // Staging of the next tile into the other buffer.  That buffer was read by the previous tile up
+    // to its last phase, so this is issued right after this tile's first barrier (every thread has
+    // left the previous tile by then); no end-of-tile barrier is needed.
+    bool issued = false;
+    auto issue_next = [&]() {
+      if (issued) return;
+      issued = true;
+      if (tid < 32 && knext < ntiles) {
+        fence_proxy_async();
+        stage_tile<S, T>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF, &bars[b ^ 1], tid);
+      }
+      if (A.ring) {                    // this thread's ring cells of the next tile: one cp.async group
+        if (knext < ntiles) gather_ring<S, T, NT>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF);
+        cp_async_commit();
+      }
+    };
     double* sq = sbuf + b * Sh::BUF;                 // [MEQN][W][W]
-    double* sa = sq + MEQN * WW;                     // [3][W][W] aux (capacity form)
+    double* sa = sq + MEQN * WW + 2;                 // [3][W][W] aux (capacity form)
     int patch = tile, tx = 0, ty = 0;
     if (A.tiles > 1) {
       patch = tile / tiles2;
@@ -380,26 +394,18 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
     const double dtdx = A.dt / dx;   // square cells: dt/dy = dt/dx
     mbar_wait(&bars[b], (phase >> b) & 1u);
     phase ^= 1u << b;
-    if (!A.ring && A.tiles == 1) {     // rotated rows -> natural window rows (cell i at column i+1)
-      for (int r = opaque(threadIdx.x); r < MEQN * W; r += NT) {
-        double* row = sq + r * W;
-        const double a = row[W - 2], c = row[W - 1];
-#pragma unroll
-        for (int k = W - 1; k >= 2; --k) row[k] = row[k - 2];
-        row[0] = a;
-        row[1] = c;
-      }
+    if (A.ring) {                      // this tile's ring: wait for this thread's copies, make every
+      cp_async_wait<0>();              // thread's copies visible, then the BCs
       __syncthreads();
-    }
-    if (A.ring) {                      // this tile's ring: wait for all but the newest group,
-      cp_async_wait<1>();              // make every thread's copies visible, then the BCs
-      __syncthreads();
+      issue_next();
       const uint8_t bc = A.bcflag[patch];
       if (bc & 1) { window_bc<S, T, NT>(A, tile, sq, 0); __syncthreads(); }
       if (bc & 2) { window_bc<S, T, NT>(A, tile, sq, 1); __syncthreads(); }
     }
 
     auto widx = [](int i, int j) { return (j + 1) * W + (i + 1); };   // tile-local 1-based cell
+    // staged-q index: single-copy staging keeps the left ghost pair of each row one row down
+    auto qidx = [&](int i, int j) { return widx(i, j) + (i < 1 ? gsh : 0); };
     auto auxc = [&](int i, int j) { return AuxCell{sa + widx(i, j), WW}; };
     auto rcell = [&](int i, int j) { return S::CAPA ? dtdx / sa[widx(i, j)] : dtdx; };
 
@@ -409,36 +415,42 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
     // the CFL remains: the max over the tile's edges of the wave speeds, taken from the state.
     if (A.skip_quiescent) {
       bool diff = false;
-      for (int t = opaque(threadIdx.x); t < MEQN * WW; t += NT) diff |= sq[t] != sq[(t / WW) * WW];
-      if (!__syncthreads_or(diff)) {
-        cfl = fmax(cfl, S::quiescent_cfl(sq, WW, A.sp, sa, dtdx, T, W, opaque(threadIdx.x), NT));
+      // (with the shifted ghosts the cells of component k occupy [k WW + s0, (k+1) WW + s0))
+      const int s0 = gsh ? 2 : 0;
+      for (int t = opaque(threadIdx.x); t < MEQN * WW; t += NT)
+        diff |= sq[t + s0] != sq[(t / WW) * WW + 2 * W + 2];
+      const bool uniform = !__syncthreads_or(diff);
+      issue_next();
+      if (uniform) {
+        cfl = fmax(cfl, S::quiescent_cfl(sq + 2 * W + 2, WW, A.sp, sa, dtdx, T, W, opaque(threadIdx.x), NT));
         const int t = opaque(threadIdx.x);
         if (t < T * T) {
           const int i = 1 + t % T, j = 1 + t / T;
           double* o = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + 1 + j) * n + tx * T + i - 1;
 #pragma unroll
-          for (int k = 0; k < MEQN; ++k) o[(int64_t)k * n2] = sq[k * WW];
+          for (int k = 0; k < MEQN; ++k) o[(int64_t)k * n2] = sq[k * WW + 2 * W + 2];
         }
-        __syncthreads();
         continue;
       }
     }
 
     if (S::NC > 0) {
       const int tid = opaque(threadIdx.x);
-      for (int t = tid; t < WW; t += NT) S::precompute(sq + t, WW, A.sp, scl + t, WW);
+      for (int t = tid; t < WW; t += NT) S::precompute(sq + t + (t % W < 2 ? gsh : 0), WW, A.sp, scl + t, WW);
       __syncthreads();
+      issue_next();
     }
     // =============================== x-sweep ===============================
     for (int e = opaque(threadIdx.x); e < EX; e += NT) {       // edge i (cells i-1 | i), row j
       const int i = e % (T + 3), j = e / (T + 3);
       double ql[MEQN], qr[MEQN];
 #pragma unroll
-      for (int k = 0; k < MEQN; ++k) { ql[k] = sq[k * WW + widx(i - 1, j)]; qr[k] = sq[k * WW + widx(i, j)]; }
+      for (int k = 0; k < MEQN; ++k) { ql[k] = sq[k * WW + qidx(i - 1, j)]; qr[k] = sq[k * WW + qidx(i, j)]; }
       S::template riemann<1>(ql, qr, scl + widx(i - 1, j), scl + widx(i, j), WW, auxc(i - 1, j), auxc(i, j),
                              A.sp, scr + e, EX);
     }
     __syncthreads();
+    issue_next();                      // (solvers without per-cell precompute)
     // X2a: fluctuations, limited correction F~ and CFL per correction edge (i in 1..T+1, row j)
     {
       const int e2 = opaque(threadIdx.x);
@@ -514,7 +526,7 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
       const int i = e % (T + 2), j = e / (T + 2);
       double ql[MEQN], qr[MEQN];
 #pragma unroll
-      for (int k = 0; k < MEQN; ++k) { ql[k] = sq[k * WW + widx(i, j - 1)]; qr[k] = sq[k * WW + widx(i, j)]; }
+      for (int k = 0; k < MEQN; ++k) { ql[k] = sq[k * WW + qidx(i, j - 1)]; qr[k] = sq[k * WW + qidx(i, j)]; }
       S::template riemann<2>(ql, qr, scl + widx(i, j - 1), scl + widx(i, j), WW, auxc(i, j - 1), auxc(i, j),
                              A.sp, scr + e, EX);
     }
@@ -597,7 +609,8 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
         }
       }
     }
-    __syncthreads();   // staging buffer b and the work arrays are free for the next tile
+    // no barrier: the next tile's phases touch ta/tb/dq (read above) only after two barriers, and
+    // this buffer is re-staged only after the next tile's first barrier (issue_next)
   }
 
   // a non-finite updated state makes the step's CFL +inf (fc_step -> FC_ENONFINITE)
