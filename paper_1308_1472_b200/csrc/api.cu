@@ -25,7 +25,7 @@ int launch_pack(const double* q, const int32_t* idx, int64_t cnt, int meqn, int 
 int launch_unpack(double* q, const int32_t* idx, int64_t cnt, int meqn, int n2, const double* buf, cudaStream_t st);
 int launch_scatter(const double* src, double* q, int64_t P, int meqn, int m, cudaStream_t st);
 int launch_gather(const double* q, double* dst, int64_t P, int meqn, int m, cudaStream_t st);
-int launch_unrotate(const double* q, double* dst, int64_t nblocks, int n, cudaStream_t st);
+int launch_unpack_padded(const double* q, double* dst, int64_t nblocks, int n, cudaStream_t st);
 int launch_step(int kind, const double* qold, double* qnew, const double* aux, const int8_t* level,
                 int64_t npatch, int m, double dt, double dx0, double p0, double p1, int limiter,
                 int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
@@ -638,7 +638,7 @@ int fc_get_q_padded(fc_forest* f, double* q, int where) {
   const size_t bytes = (size_t)f->Pl * f->pl.meqn * f->pl.n * f->pl.n * sizeof(double);
   // storage -> natural padded layout (q_new is free scratch between steps)
   double* dst = where == FC_DEVICE ? q : f->qnew;
-  f->st.kernel_launches += launch_unrotate(f->qold, dst, f->Pl * f->pl.meqn, f->pl.n, f->stream);
+  f->st.kernel_launches += launch_unpack_padded(f->qold, dst, f->Pl * f->pl.meqn, f->pl.n, f->stream);
   CK(cudaGetLastError());
   if (where != FC_DEVICE) CK(cudaMemcpyAsync(q, f->qnew, bytes, cudaMemcpyDeviceToHost, f->stream));
   CK(cudaStreamSynchronize(f->stream));

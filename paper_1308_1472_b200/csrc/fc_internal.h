@@ -10,13 +10,31 @@
 
 namespace fc {
 
-// Storage of a padded patch in device memory: rows of n = m + 4 doubles (row j + 1 holds cell row j,
-// j = -1..m+2) with the columns rotated so that cell i (1-based, -1..m+2) sits at column (i - 1) mod n:
-// the m interior cells of a row occupy its first m doubles -- whole, aligned 32-byte sectors -- and
-// the 4 ghost columns (right m+1, m+2, then left -1, 0) share the last 32 bytes.  Interior-only
-// traffic (the quiescent copy, TMA interior rows) then touches no partial sector.  The ABI's padded
+#ifdef __CUDACC__
+#define FC_HD __host__ __device__
+#else
+#define FC_HD
+#endif
+
+// Storage of a padded patch in device memory, per (patch, component) block of n^2 doubles
+// (n = m + 4): the m x m interior first, dense and row-major (cell (i, j), i, j = 1..m, at
+// (j - 1) m + (i - 1)), then the 8m + 16 ghost cells in ring order (rows j = -1..m+2 outer, columns
+// i = -1..m+2 inner, interior skipped) -- the order of the ring tables.  Interior-only traffic (the
+// quiescent copy, interior staging) then streams whole contiguous 2 KB blocks: B200's DRAM fetch
+// granule made a strided interior (128 of every 160 bytes) cost the full rows (measured with
+// tools/dram_pattern.cu: 16 of 20 doubles per row reads 100% of the bytes).  The ABI's padded
 // arrays (fc_get_q_padded, aux) keep the natural layout (j + 1) n + (i + 1).
-inline int qcell(int i, int j, int n) { return (j + 1) * n + ((i - 1 + n) % n); }
+FC_HD inline int ring_index(int i, int j, int m) {
+  const int n = m + 4;
+  if (j <= 0) return (j + 1) * n + (i + 1);
+  if (j <= m) return 2 * n + 4 * (j - 1) + (i <= 0 ? i + 1 : i - m + 1);
+  return 2 * n + 4 * m + (j - m - 1) * n + (i + 1);
+}
+FC_HD inline int qcell(int i, int j, int n) {
+  const int m = n - 4;
+  if (i >= 1 && i <= m && j >= 1 && j <= m) return (j - 1) * m + (i - 1);
+  return m * m + ring_index(i, j, m);
+}
 // natural padded index -> storage index
 inline int qcell_of_natural(int cell, int n) { return qcell(cell % n - 1, cell / n - 1, n); }
 

@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #include "../../include/fc.h"
+#include "fc_internal.h"
 
 namespace fc {
 
@@ -108,7 +109,7 @@ __global__ void k_scatter_interior(const double* __restrict__ src, double* __res
     const int64_t r = t / m;
     const int j = (int)(r % m);
     const int64_t pk = r / m;
-    q[pk * n * n + (int64_t)(j + 2) * n + i] = src[t];   // rotated storage: cell i+1 at column i
+    q[pk * n * n + (int64_t)j * m + i] = src[t];   // dense interior first (fc_internal.h qcell)
   }
 }
 
@@ -122,17 +123,18 @@ __global__ void k_gather_interior(const double* __restrict__ q, double* __restri
     const int64_t r = t / m;
     const int j = (int)(r % m);
     const int64_t pk = r / m;
-    dst[t] = q[pk * n * n + (int64_t)(j + 2) * n + i];
+    dst[t] = q[pk * n * n + (int64_t)j * m + i];
   }
 }
 
-// storage (rotated columns) -> natural padded layout, one n x n block per (patch, component)
-__global__ void k_unrotate(const double* __restrict__ q, double* __restrict__ dst, int64_t nblocks, int n) {
+// storage (interior + ring, qcell) -> natural padded layout, one n x n block per (patch, component)
+__global__ void k_unpack_padded(const double* __restrict__ q, double* __restrict__ dst, int64_t nblocks, int n) {
   const int64_t tot = nblocks * n * n;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(t % n);          // natural column = i + 1
-    const int64_t rb = t - c;
-    dst[t] = q[rb + (c - 2 + n) % n];    // storage column (i - 1) mod n
+    const int c = (int)(t % n);                 // natural column = i + 1
+    const int64_t rr = t / n;
+    const int r = (int)(rr % n);                // natural row = j + 1
+    dst[t] = q[(rr - r) * n + qcell(c - 1, r - 1, n)];
   }
 }
 
@@ -175,9 +177,9 @@ int launch_scatter(const double* src, double* q, int64_t P, int meqn, int m, cud
   return 1;
 }
 
-int launch_unrotate(const double* q, double* dst, int64_t nblocks, int n, cudaStream_t st) {
+int launch_unpack_padded(const double* q, double* dst, int64_t nblocks, int n, cudaStream_t st) {
   if (nblocks <= 0) return 0;
-  k_unrotate<<<148 * 8, 256, 0, st>>>(q, dst, nblocks, n);
+  k_unpack_padded<<<148 * 8, 256, 0, st>>>(q, dst, nblocks, n);
   return 1;
 }
 

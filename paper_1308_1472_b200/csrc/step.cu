@@ -22,6 +22,7 @@
 #include <stdlib.h>
 
 #include "../../include/fc.h"
+#include "fc_internal.h"
 #include "solvers.cuh"
 
 namespace fc {
@@ -213,8 +214,8 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
 #pragma unroll 1
     for (int r = lane; r < MEQN * T; r += 32) {
       const int k = r / T, row = r - k * T;
-      // rotated storage: the m interior cells of a row are its first m doubles
-      bulk_g2s(buf + k * WW + (row + 2) * W + 2, qb + (int64_t)k * n2 + (row + 2) * n, T * sizeof(double), bar);
+      // storage (qcell): the interior is dense, row `row` at row * m
+      bulk_g2s(buf + k * WW + (row + 2) * W + 2, qb + (int64_t)k * n2 + row * T, T * sizeof(double), bar);
     }
     if (S::CAPA && lane == 0) bulk_g2s(buf + MEQN * WW + 2, A.aux + (int64_t)patch * 3 * n2, abytes, bar);
     return;
@@ -223,24 +224,27 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
   if (lane == 0) mbar_expect_tx(bar, bytes);
   __syncwarp();
   if (A.tiles == 1) {        // the window is the whole padded patch: one contiguous copy of its
-                             // rotated storage to buf + 2.  Storage row r holds cells 1..m+2 then the
-                             // ghosts -1, 0 (column (i-1) mod n), so at +2 every cell i >= 1 lands at
-                             // its natural window position and the ghost pair of flattened row R
-                             // lands at the start of row R+1: the kernel reads ghosts there (gsh)
-    if (lane == 0) bulk_g2s(buf + 2, A.qold + patch * (int64_t)MEQN * n2, MEQN * WW * sizeof(double), bar);
-  } else {                   // q: per (component, window row) the storage row is rotated (cell i at
-                             // column (i-1) mod n), so a window row is one piece, or two for the
-                             // leftmost tile (ghost cells -1, 0 live at the end of the storage row)
-    const double* qb = A.qold + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T) * n;
+                             // storage blocks (dense interior + ring, qcell); the kernel reads them
+                             // through qidx
+    if (lane == 0) bulk_g2s(buf, A.qold + patch * (int64_t)MEQN * n2, MEQN * WW * sizeof(double), bar);
+  } else {                   // q: per (component, window row): a ghost row is one piece of the ring
+                             // area; an interior row is its interior run plus the ghost pair of an
+                             // edge tile (ring area) -- into the natural window
+    const int m = A.m, mm = m * m;
+    const double* qb = A.qold + patch * (int64_t)MEQN * n2;
 #pragma unroll 1
     for (int r = lane; r < MEQN * W; r += 32) {
       const int k = r / W, b = r - k * W;
-      const double* row = qb + (int64_t)k * n2 + b * n;
-      if (tx == 0) {
-        bulk_g2s(buf + r * W, row + (n - 2), 2 * sizeof(double), bar);
-        bulk_g2s(buf + r * W + 2, row, (W - 2) * sizeof(double), bar);
+      const int j = ty * T + b - 1, i0 = tx * T - 1;
+      const double* blk = qb + (int64_t)k * n2;
+      double* dst = buf + r * W;
+      if (j <= 0 || j > m) {
+        bulk_g2s(dst, blk + mm + ring_index(i0, j, m), W * sizeof(double), bar);
       } else {
-        bulk_g2s(buf + r * W, row + tx * T - 2, W * sizeof(double), bar);
+        const int ia = i0 < 1 ? 1 : i0, ib = i0 + W - 1 > m ? m : i0 + W - 1;   // interior run
+        bulk_g2s(dst + (ia - i0), blk + (j - 1) * m + (ia - 1), (ib - ia + 1) * sizeof(double), bar);
+        if (i0 < 1) bulk_g2s(dst, blk + mm + ring_index(-1, j, m), 2 * sizeof(double), bar);
+        if (i0 + W - 1 > m) bulk_g2s(dst + (m + 1 - i0), blk + mm + ring_index(m + 1, j, m), 2 * sizeof(double), bar);
       }
     }
   }
@@ -344,7 +348,7 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
   const int tid = threadIdx.x;
   const int tiles2 = A.tiles * A.tiles;
   const int n = A.m + 4, n2 = n * n;
-  const int gsh = (!A.ring && A.tiles == 1) ? W : 0;   // see stage_tile / qidx
+  const bool dense = !A.ring && A.tiles == 1;   // staged window = storage blocks (see stage_tile)
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -404,8 +408,12 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
     }
 
     auto widx = [](int i, int j) { return (j + 1) * W + (i + 1); };   // tile-local 1-based cell
-    // staged-q index: single-copy staging keeps the left ghost pair of each row one row down
-    auto qidx = [&](int i, int j) { return widx(i, j) + (i < 1 ? gsh : 0); };
+    // staged-q index: the single-copy staging (dense) keeps the storage blocks (qcell)
+    auto qidx = [&](int i, int j) {
+      if (!dense) return widx(i, j);
+      if ((unsigned)(i - 1) < (unsigned)T && (unsigned)(j - 1) < (unsigned)T) return (j - 1) * T + (i - 1);
+      return T * T + ring_index(i, j, T);
+    };
     auto auxc = [&](int i, int j) { return AuxCell{sa + widx(i, j), WW}; };
     auto rcell = [&](int i, int j) { return S::CAPA ? dtdx / sa[widx(i, j)] : dtdx; };
 
@@ -415,20 +423,17 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
     // the CFL remains: the max over the tile's edges of the wave speeds, taken from the state.
     if (A.skip_quiescent) {
       bool diff = false;
-      // (with the shifted ghosts the cells of component k occupy [k WW + s0, (k+1) WW + s0))
-      const int s0 = gsh ? 2 : 0;
-      for (int t = opaque(threadIdx.x); t < MEQN * WW; t += NT)
-        diff |= sq[t + s0] != sq[(t / WW) * WW + 2 * W + 2];
+      for (int t = opaque(threadIdx.x); t < MEQN * WW; t += NT) diff |= sq[t] != sq[(t / WW) * WW + qidx(1, 1)];
       const bool uniform = !__syncthreads_or(diff);
       issue_next();
       if (uniform) {
-        cfl = fmax(cfl, S::quiescent_cfl(sq + 2 * W + 2, WW, A.sp, sa, dtdx, T, W, opaque(threadIdx.x), NT));
+        cfl = fmax(cfl, S::quiescent_cfl(sq + qidx(1, 1), WW, A.sp, sa, dtdx, T, W, opaque(threadIdx.x), NT));
         const int t = opaque(threadIdx.x);
         if (t < T * T) {
           const int i = 1 + t % T, j = 1 + t / T;
-          double* o = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + 1 + j) * n + tx * T + i - 1;
+          double* o = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + j - 1) * A.m + tx * T + i - 1;
 #pragma unroll
-          for (int k = 0; k < MEQN; ++k) o[(int64_t)k * n2] = sq[k * WW + 2 * W + 2];
+          for (int k = 0; k < MEQN; ++k) o[(int64_t)k * n2] = sq[k * WW + qidx(1, 1)];
         }
         continue;
       }
@@ -436,7 +441,7 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
 
     if (S::NC > 0) {
       const int tid = opaque(threadIdx.x);
-      for (int t = tid; t < WW; t += NT) S::precompute(sq + t + (t % W < 2 ? gsh : 0), WW, A.sp, scl + t, WW);
+      for (int t = tid; t < WW; t += NT) S::precompute(sq + qidx(t % W - 1, t / W - 1), WW, A.sp, scl + t, WW);
       __syncthreads();
       issue_next();
     }
@@ -593,10 +598,10 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
       if (t < T * T) {
         const int i = 1 + t % T, j = 1 + t / T;
         const double rc = rcell(i, j);
-        double* o = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + 1 + j) * n + tx * T + i - 1;
+        double* o = A.qnew + patch * (int64_t)MEQN * n2 + (int64_t)(ty * T + j - 1) * A.m + tx * T + i - 1;
         const double* rt = ta + (j - 1) * (T + 2) + i;   // right(i, j) of component 0
         const double* lf = tb + (j - 1) * (T + 2) + i;   // left(i, j)
-        const double* qs = sq + widx(i, j);
+        const double* qs = sq + qidx(i, j);
         const double* d = dq + (j - 1) * T + (i - 1);
 #pragma unroll
         for (int k = 0; k < MEQN; ++k) {
@@ -639,17 +644,16 @@ template <int MEQN, int T>
 __global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict__ qold, double* __restrict__ qnew,
                                                        int npatch, uint8_t* __restrict__ uflag,
                                                        double* __restrict__ uval) {
-  // One warp per patch (T = m here).  In the rotated storage the m interior cells of each row are
-  // the row's first m doubles (whole, aligned 32-byte sectors): exactly the interior is copied, so
-  // DRAM traffic is the compulsory read + write of q, with no partial-sector read-modify-write.
-  // Each lane issues up to 16 16-byte loads before using any.
-  constexpr int n = T + 4, n2 = n * n, H = T / 2;           // double2 per interior row
-  constexpr int E = MEQN * T * H, NE = (E + 31) / 32, NC = NE < 16 ? NE : 16;
+  // One warp per patch (T = m here).  The storage keeps each (patch, component) interior as one
+  // dense m x m block (qcell): exactly the interior is copied, contiguous 16-byte accesses, so DRAM
+  // traffic is the compulsory read + write of q.  Each lane issues up to 16 loads before using any.
+  constexpr int n = T + 4, n2 = n * n, H = T * T / 2;       // double2 per interior block
+  constexpr int E = MEQN * H, NE = (E + 31) / 32, NC = NE < 16 ? NE : 16;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < npatch; p += warps) {
-    const double* src = qold + (int64_t)p * MEQN * n2 + 2 * n;
-    double* dst = qnew + (int64_t)p * MEQN * n2 + 2 * n;
+    const double* src = qold + (int64_t)p * MEQN * n2;
+    double* dst = qnew + (int64_t)p * MEQN * n2;
     double v0[MEQN];
 #pragma unroll
     for (int k = 0; k < MEQN; ++k) v0[k] = __ldg(src + k * n2);
@@ -660,15 +664,15 @@ __global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict_
 #pragma unroll
       for (int u = 0; u < NC; ++u) {
         const int e = base + lane + 32 * u;
-        const int k = e / (T * H), r = e - k * (T * H), row = r / H, c2 = r - row * H;
-        if (e < E) x[u] = __ldcs(reinterpret_cast<const double2*>(src + k * n2 + row * n) + c2);
+        const int k = e / H, c2 = e - k * H;
+        if (e < E) x[u] = __ldcs(reinterpret_cast<const double2*>(src + k * n2) + c2);
       }
 #pragma unroll
       for (int u = 0; u < NC; ++u) {
         const int e = base + lane + 32 * u;
         if (e < E) {
-          const int k = e / (T * H), r = e - k * (T * H), row = r / H, c2 = r - row * H;
-          __stcs(reinterpret_cast<double2*>(dst + k * n2 + row * n) + c2, x[u]);
+          const int k = e / H, c2 = e - k * H;
+          __stcs(reinterpret_cast<double2*>(dst + k * n2) + c2, x[u]);
           diff |= (x[u].x != v0[k]) | (x[u].y != v0[k]);
         }
       }
