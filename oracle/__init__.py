@@ -41,7 +41,7 @@ def build(force: bool = False) -> str:
 
 class Problem(C.Structure):
     _fields_ = [("kind", C.c_int), ("p0", C.c_double), ("p1", C.c_double), ("limiter", C.c_int),
-                ("method2", C.c_int), ("method3", C.c_int)]
+                ("method2", C.c_int), ("method3", C.c_int), ("reflux", C.c_int)]
 
 
 _lib = None
@@ -68,6 +68,10 @@ def lib():
         L.orc_step_patch.argtypes = [C.POINTER(Problem), C.c_int, C.c_int, P, P, C.c_double,
                                      C.c_double, C.c_double, P]
         L.orc_step_patch.restype = C.c_double
+        L.orc_step_patch_faces.argtypes = [C.POINTER(Problem), C.c_int, C.c_int, P, P, C.c_double,
+                                           C.c_double, C.c_double, P, P]
+        L.orc_step_patch_faces.restype = C.c_double
+        L.orc_flux.argtypes = [C.POINTER(Problem), C.c_int, P, C.c_double, P]
         L.orc_limiter.argtypes = [C.c_int, C.c_double]
         L.orc_limiter.restype = C.c_double
         L.orc_meqn.argtypes = [C.c_int]
@@ -81,9 +85,9 @@ def _p(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def problem(kind, params=(0.0, 0.0), limiter=LIM_MC, method2=2, method3=2) -> Problem:
+def problem(kind, params=(0.0, 0.0), limiter=LIM_MC, method2=2, method3=2, reflux=0) -> Problem:
     return Problem(int(kind), float(params[0]), float(params[1]), int(limiter), int(method2),
-                   int(method3))
+                   int(method3), int(reflux))
 
 
 def meqn(kind: int) -> int:
@@ -246,7 +250,7 @@ def forest_for(w) -> OracleForest:
 
 
 def problem_for(w) -> Problem:
-    return problem(w.kind, w.params, w.limiter, w.method2, w.method3)
+    return problem(w.kind, w.params, w.limiter, w.method2, w.method3, getattr(w, "reflux", 0))
 
 
 def run(w, steps: int | None = None, dt_list=None, nthreads: int = 1, forest=None):

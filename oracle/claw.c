@@ -276,11 +276,44 @@ int orc_rpt2(const orc_problem* pr, int ixy, const double* ql, const double* qr,
   return ORC_OK;
 }
 
+/* ---- physical flux ------------------------------------------------------------------------------ */
+/* f(q) along axis ixy (1: x, 2: y) of the conservation law q_t + f(q)_x + g(q)_y = 0 that the
+ * wave-propagation method discretises (PAPER.md:168-178 [§3]; LeVeque 2002 ch. 4, 13-14).  For the
+ * advective (colour-equation) form with edge velocities the flux through an edge is the edge
+ * velocity times the state ("u_e+ Q_l + u_e- Q_r + F~").  Used by the reflux. */
+void orc_flux(const orc_problem* pr, int ixy, const double* q, double uedge, double* f) {
+  const int nd = ixy, td = 3 - ixy;
+  switch (pr->kind) {
+    case ORC_ADV_CONST: f[0] = (ixy == 1 ? pr->p0 : pr->p1) * q[0]; return;
+    case ORC_ADV_EDGEVEL_CAPA: f[0] = uedge * q[0]; return;
+    case ORC_SWE_ROE: {
+      const double un = q[nd] / q[0];
+      f[0] = q[nd];
+      f[nd] = q[nd] * un + 0.5 * pr->p0 * q[0] * q[0];
+      f[td] = q[td] * un;
+      return;
+    }
+    default: {
+      const double p = euler_p(pr->p0, q), un = q[nd] / q[0];
+      f[0] = q[nd];
+      f[nd] = q[nd] * un + p;
+      f[td] = q[td] * un;
+      f[3] = (q[3] + p) * un;
+      return;
+    }
+  }
+}
+
 /* ---- one patch -------------------------------------------------------------------------------- */
 static int g_step_error = 0;   /* first solver error seen by orc_step_patch (physical guard) */
 
 double orc_step_patch(const orc_problem* pr, int m, int meqn, const double* qp, const double* auxp,
                       double dt, double dx, double dy, double* qnew) {
+  return orc_step_patch_faces(pr, m, meqn, qp, auxp, dt, dx, dy, qnew, NULL);
+}
+
+double orc_step_patch_faces(const orc_problem* pr, int m, int meqn, const double* qp, const double* auxp,
+                            double dt, double dx, double dy, double* qnew, double* face) {
   const int n = ORC_N(m), nn = n * n, mw = orc_mwaves(pr->kind);
   const size_t A = (size_t)meqn * nn;
   double* amx = (double*)calloc(6 * A, sizeof(double));
@@ -417,6 +450,32 @@ double orc_step_patch(const orc_problem* pr, int m, int meqn, const double* qp, 
         double b = E(apy, k, i, j) + E(amy, k, i, j + 1) + E(gy, k, i, j + 1) - E(gy, k, i, j);
         qnew[(size_t)k * nn + ORC_IDX(m, i, j)] = Q(k, i, j) - r * a - s * b;
       }
+  /* face fluxes for the coarse/fine reflux, per face (0: -x, 1: +x, 2: -y,
+   * 3: +y) and boundary edge, in outward form: the total flux the update applied through the
+   * edge, F = f(Q_l) + A-dq + F~ = f(Q_r) - A+dq + F~ (F~ including the other sweep's transverse
+   * terms), signed along the face's outward normal.  With Q_own the adjacent interior cell:
+   *   high faces (+x, +y):  out = f(Q_own) + A-dq + F~;   low faces (-x, -y):  out = A+dq - F~ - f(Q_own). */
+  if (face) {
+    double fq[4], tmp[3];
+    for (int e = 0; e < m; ++e) {
+      const int c = e + 1;
+      double* o0 = face + ((size_t)0 * m + e) * meqn;
+      double* o1 = face + ((size_t)1 * m + e) * meqn;
+      double* o2 = face + ((size_t)2 * m + e) * meqn;
+      double* o3 = face + ((size_t)3 * m + e) * meqn;
+      double ql_[4], qh_[4];
+      for (int k = 0; k < meqn; ++k) { ql_[k] = Q(k, 1, c); qh_[k] = Q(k, m, c); }
+      orc_flux(pr, 1, ql_, AUXP(1, c, tmp)[1], fq);
+      for (int k = 0; k < meqn; ++k) o0[k] = (E(apx, k, 1, c) - E(fx, k, 1, c)) - fq[k];
+      orc_flux(pr, 1, qh_, AUXP(m + 1, c, tmp)[1], fq);
+      for (int k = 0; k < meqn; ++k) o1[k] = fq[k] + (E(amx, k, m + 1, c) + E(fx, k, m + 1, c));
+      for (int k = 0; k < meqn; ++k) { ql_[k] = Q(k, c, 1); qh_[k] = Q(k, c, m); }
+      orc_flux(pr, 2, ql_, AUXP(c, 1, tmp)[2], fq);
+      for (int k = 0; k < meqn; ++k) o2[k] = (E(apy, k, c, 1) - E(gy, k, c, 1)) - fq[k];
+      orc_flux(pr, 2, qh_, AUXP(c, m + 1, tmp)[2], fq);
+      for (int k = 0; k < meqn; ++k) o3[k] = fq[k] + (E(amy, k, c, m + 1) + E(gy, k, c, m + 1));
+    }
+  }
 #undef Q
 #undef E
 #undef AUXP
@@ -435,16 +494,27 @@ int orc_step(const orc_forest* f, const orc_problem* pr, double* qpad, const dou
   g_step_error = 0;
   double cfl = 0.0;
   (void)nthreads;
+  double* faces = NULL;
+  const size_t FS = (size_t)4 * m * meqn;
+  if (pr->reflux) {
+    faces = (double*)malloc((size_t)f->P * FS * sizeof(double));
+    if (!faces) return ORC_ENOMEM;
+  }
 #ifdef _OPENMP
 #pragma omp parallel for schedule(static) reduction(max : cfl) num_threads(nthreads > 0 ? nthreads : 1)
 #endif
   for (int64_t p = 0; p < f->P; ++p) {
     double h = ldexp(dx0, -f->level[p]);
-    double c = orc_step_patch(pr, m, meqn, qpad + p * S, aux ? aux + p * SA : NULL, dt, h, h,
-                              qout + p * S);
+    double c = orc_step_patch_faces(pr, m, meqn, qpad + p * S, aux ? aux + p * SA : NULL, dt, h, h,
+                                    qout + p * S, faces ? faces + p * FS : NULL);
     if (c > cfl || c != c) cfl = c;
   }
   *cfl_out = cfl;
+  if (faces) {
+    int rr = g_step_error ? g_step_error : orc_reflux(f, pr, faces, aux, dt, dx0, qout);
+    free(faces);
+    return rr;
+  }
   return g_step_error;
 }
 

@@ -16,6 +16,7 @@
  * physical face crossed means PHYS.  The leaf containing the point is found by Morton-range
  * search (no neighbour logic), and the op follows from its level.
  */
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 #include "oracle.h"
@@ -290,4 +291,81 @@ const int32_t* orc_cached_table(const orc_forest* fc, int* rc) {
   *rc = orc_ghost_table(f, f->table);
   if (*rc) { free(f->table); f->table = NULL; return NULL; }
   return f->table;
+}
+
+/* ---- coarse/fine reflux (PAPER.md:279-282 [§4]) ------------------------------ */
+/* fine cell of the finer neighbour at the point (X, Y) of tree t (a fine-cell centre); -1 if the
+ * leaf there is not one level finer than l */
+static int fine_cell(const orc_forest* f, int t, int64_t X, int64_t Y, int l, int64_t sh, int64_t* L,
+                     int* i, int* j) {
+  const int m = f->m;
+  *L = locate(f, t, X, Y);
+  if (f->level[*L] != l + 1) return -1;
+  *i = (int)(((X - f->x[*L] * 2 * m) / sh + 1) / 2);
+  *j = (int)(((Y - f->y[*L] * 2 * m) / sh + 1) / 2);
+  return 0;
+}
+
+int orc_reflux(const orc_forest* f, const orc_problem* pr, const double* faces, const double* aux,
+               double dt, double dx0, double* qout) {
+  const int m = f->m, meqn = orc_meqn(pr->kind), n = ORC_N(m);
+  const size_t S = (size_t)meqn * n * n, SA = (size_t)3 * n * n, FS = (size_t)4 * m * meqn;
+  for (int64_t p = 0; p < f->P; ++p) {
+    const int l = f->level[p];
+    if (l >= f->lmax) continue;                       /* no finer neighbour possible */
+    const int64_t s = 1ll << (f->lmax - l);           /* half a cell of p; s / 2 = half a fine cell */
+    const int64_t sh = s / 2;
+    const int64_t X0 = f->x[p] * 2 * m, Y0 = f->y[p] * 2 * m;
+    const double dx = ldexp(dx0, -l);
+    for (int sf = 0; sf < 4; ++sf) {
+      for (int c = 0; c < m; ++c) {
+        const double* oc = faces + p * FS + ((size_t)sf * m + c) * meqn;
+        const double* of[2];
+        int ok = 1;
+        for (int h = 0; h < 2 && ok; ++h) {          /* the two fine edges covering coarse edge c */
+          const int64_t tau = 2 * s * c + (h ? 3 * sh : sh);
+          int64_t Lc[2];
+          int ic[2], jc[2];
+          for (int d = 0; d < 2 && ok; ++d) {        /* fine cells at depth 1 and 2 behind the face */
+            const int64_t dep = d ? 3 * sh : sh;
+            int64_t X, Y;
+            switch (sf) {
+              case 0: X = X0 - dep; Y = Y0 + tau; break;
+              case 1: X = X0 + 2 * m * s + dep; Y = Y0 + tau; break;
+              case 2: X = X0 + tau; Y = Y0 - dep; break;
+              default: X = X0 + tau; Y = Y0 + 2 * m * s + dep; break;
+            }
+            int t = f->tree[p];
+            const int axis = sf < 2 ? 0 : 1, fo = out_face(f, X, Y, axis);
+            if (fo >= 0) {
+              const int code = f->t2f[4 * t + fo], nf = code & 3, rev = code >> 2;
+              const int t_from = t;
+              if (cross(f, &t, &X, &Y, fo)) { ok = 0; break; }   /* physical face */
+              if (meqn > 1 && t != t_from && !(nf == (fo ^ 1) && !rev)) return ORC_EUNSUP;
+            }
+            if (fine_cell(f, t, X, Y, l, sh, &Lc[d], &ic[d], &jc[d])) { ok = 0; break; }
+          }
+          if (!ok) break;
+          if (Lc[0] != Lc[1]) return ORC_EBALANCE;
+          const int di = ic[1] - ic[0], dj = jc[1] - jc[0];   /* inward normal in the fine frame */
+          int ff, fe;
+          if (di == 1 && dj == 0 && ic[0] == 1) { ff = 0; fe = jc[0] - 1; }
+          else if (di == -1 && dj == 0 && ic[0] == m) { ff = 1; fe = jc[0] - 1; }
+          else if (di == 0 && dj == 1 && jc[0] == 1) { ff = 2; fe = ic[0] - 1; }
+          else if (di == 0 && dj == -1 && jc[0] == m) { ff = 3; fe = ic[0] - 1; }
+          else return ORC_EBALANCE;
+          of[h] = faces + Lc[0] * FS + ((size_t)ff * m + fe) * meqn;
+        }
+        if (!ok) continue;                            /* not a coarse/fine edge */
+        const int ci = sf == 0 ? 1 : (sf == 1 ? m : c + 1), cj = sf < 2 ? c + 1 : (sf == 2 ? 1 : m);
+        const double kap = aux ? aux[p * SA + ORC_IDX(m, ci, cj)] : 1.0;
+        const double r = dt / (kap * dx);
+        for (int k = 0; k < meqn; ++k) {
+          const double corr = oc[k] + 0.5 * (of[0][k] + of[1][k]);
+          qout[p * S + (size_t)k * n * n + ORC_IDX(m, ci, cj)] += r * corr;
+        }
+      }
+    }
+  }
+  return ORC_OK;
 }

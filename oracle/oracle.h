@@ -43,6 +43,7 @@ typedef struct {
   int limiter;     /* ORC_LIM_* */
   int method2;     /* 1: first order, 2: + limited second-order corrections */
   int method3;     /* 0: none, 1: transverse of A+-dq, 2: transverse of A+-dq -+ F~ */
+  int reflux;      /* 1: conservative coarse/fine flux correction after the update (orc_reflux) */
 } orc_problem;
 
 int orc_forest_create(int64_t num_patches, const int8_t* levels, const int32_t* tree_ids,
@@ -82,6 +83,22 @@ int orc_build_padded_sample(const orc_forest* f, const double* q, int meqn, int6
 /* single-patch update on a padded patch (ring already filled) -> patch CFL */
 double orc_step_patch(const orc_problem* pr, int m, int meqn, const double* qp, const double* auxp,
                       double dt, double dx, double dy, double* qnew);
+
+/* orc_step_patch plus the applied boundary-edge fluxes face[4][m][meqn] (faces -x, +x, -y, +y;
+ * edge e = cell row / column e+1 of the face), in outward form (see claw.c); face may be NULL */
+double orc_step_patch_faces(const orc_problem* pr, int m, int meqn, const double* qp, const double* auxp,
+                            double dt, double dx, double dy, double* qnew, double* face);
+/* Conservative coarse/fine flux correction ("reflux"; PAPER.md:279-282 [§4]):
+ * every coarse cell C adjacent to a face whose neighbour is one level finer gets, per such face,
+ *   Q_C += dt / (kappa_C dx_C) (out_C + (out_f1 + out_f2) / 2)
+ * -- its own applied flux replaced by the mean of the two fine fluxes through the same face
+ * (fine edges found by point location across the connectivity), all in outward form.  faces =
+ * [P][4][m][meqn] from orc_step_patch_faces of the same step; qout updated in place.  Systems
+ * (meqn > 1) across non-aligned tree links are not supported (ORC_EUNSUP). */
+int orc_reflux(const orc_forest* f, const orc_problem* pr, const double* faces, const double* aux,
+               double dt, double dx0, double* qout);
+/* physical flux along axis ixy of state q (uedge: edge velocity, advective form) */
+void orc_flux(const orc_problem* pr, int ixy, const double* q, double uedge, double* f);
 
 /* pieces exposed for the pin tests */
 double orc_limiter(int limiter, double theta);

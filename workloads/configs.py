@@ -45,6 +45,7 @@ class Workload:
     method2: int = 2
     method3: int = 2
     cfl_reject: float = 1.0
+    reflux: int = 0          # conservative coarse/fine flux correction
     mbc: int = 2
     info: dict = field(default_factory=dict)
     ic: object = None        # ic(forest, m, p0, p1) -> q0[p1-p0] (analytic, deterministic)
