@@ -95,6 +95,14 @@ typedef struct {
   int32_t skip_quiescent;       /* 1: exact shortcut for tiles whose 2-cell-haloed window holds one
                                    uniform state (all waves are exactly 0, so q_new = q bitwise and only
                                    the CFL is evaluated); 0: always run the full update */
+  int32_t reflux;               /* 1: conservative coarse/fine flux correction after the update
+                                   (PAPER.md:279-282): every coarse cell next to a
+                                   face whose neighbour is one level finer has the flux it applied
+                                   through that face replaced by the mean of the two fine fluxes, so
+                                   sum kappa q is conserved across coarse/fine faces.  No-op on
+                                   conforming meshes.  FC_EUNSUP (at fc_set_problem) for systems
+                                   (meqn > 1) across rotated tree links and for coarse/fine pairs
+                                   split between ranks.  0: off (the paper's global-dt step) */
 } fc_problem;
 
 typedef struct {

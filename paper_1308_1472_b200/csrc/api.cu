@@ -29,7 +29,10 @@ int launch_unpack_padded(const double* q, double* dst, int64_t nblocks, int n, c
 int launch_step(int kind, const double* qold, double* qnew, const double* aux, const int8_t* level,
                 int64_t npatch, int m, double dt, double dx0, double p0, double p1, int limiter,
                 int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
-                const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits, cudaStream_t st);
+                const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits,
+                const int32_t* rslot, double* freg, cudaStream_t st);
+int launch_reflux(const int32_t* cells, int64_t ncells, const double* freg, double* qnew, const double* aux,
+                  const int8_t* level, double dt, double dx0, int meqn, int n2, cudaStream_t st);
 int launch_filter(int kind, const double* qold, double* qnew, int npatch, int m, uint8_t* uflag, double* uval,
                   const int32_t* nbr, const uint8_t* negmask, const int8_t* level, double dt, double dx0,
                   double p0, double p1, int32_t* active, int32_t* nactive, unsigned long long* cfl_bits,
@@ -85,6 +88,12 @@ struct fc_forest {
   uint8_t *d_negmask = nullptr, *d_uflag = nullptr;
   double* d_uval = nullptr;
   int32_t h_nactive = 0;
+  // coarse/fine reflux (built at the first fc_set_problem asking for it)
+  bool reflux_planned = false;
+  int32_t* d_rslot = nullptr;          // [Pl] flux-register slot or -1
+  int32_t* d_rcells = nullptr;         // [ncells][RFX]
+  int64_t nrcells = 0;
+  double* d_freg = nullptr;            // [slots][4][m][meqn] applied face fluxes (outward)
   std::vector<DevList> interp, bcx_l, bcy_l;
   fc_problem prob{};
   bool has_problem = false, has_q = false, has_aux = false;
@@ -301,6 +310,7 @@ static int update_local(fc_forest* f, double dt) {
   CK(cudaMemsetAsync(f->d_cfl, 0, sizeof(unsigned long long), f->stream));
   const fc_problem& p = f->prob;
   const bool fused = use_fused(f);
+  const bool reflux = p.reflux && f->nrcells > 0;
   bool filtered = false;
   // (tiny forests skip the filter: its two extra launches cost more than the tiles they save; the
   // step kernel's own quiescent-window check still applies)
@@ -318,11 +328,17 @@ static int update_local(fc_forest* f, double dt) {
   int lr = launch_step(p.kind, f->qold, f->qnew, f->aux, f->d_level, f->Pl, f->pl.m, dt, f->pl.dx0,
                        p.p0, p.p1, p.limiter, p.method2, p.method3, filtered ? 0 : p.skip_quiescent,
                        fused ? f->d_ring : nullptr, f->d_bcflag, filtered ? f->d_active : nullptr,
-                       filtered ? f->d_nactive : nullptr, f->d_cfl, f->stream);
+                       filtered ? f->d_nactive : nullptr, f->d_cfl, reflux ? f->d_rslot : nullptr,
+                       reflux ? f->d_freg : nullptr, f->stream);
   if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
   f->st.kernel_launches += lr;
   f->st.step_kernel_launches += lr;
   CK(cudaGetLastError());
+  if (reflux) {   // coarse cells next to finer faces: applied flux -> mean of the fine fluxes
+    f->st.kernel_launches += launch_reflux(f->d_rcells, f->nrcells, f->d_freg, f->qnew, f->aux, f->d_level, dt,
+                                           f->pl.dx0, f->pl.meqn, f->pl.n * f->pl.n, f->stream);
+    CK(cudaGetLastError());
+  }
   return FC_OK;
 }
 
@@ -352,6 +368,7 @@ static void destroy(fc_forest* f) {
     cudaFree(f->d_ring); cudaFree(f->d_bcflag);
     cudaFree(f->d_nbr); cudaFree(f->d_active); cudaFree(f->d_nactive); cudaFree(f->d_negmask);
     cudaFree(f->d_uflag); cudaFree(f->d_uval);
+    cudaFree(f->d_rslot); cudaFree(f->d_rcells); cudaFree(f->d_freg);
     if (f->h_cfl) cudaFreeHost(f->h_cfl);
     free_list(f->copy); free_list(f->avg); free_list(f->bcx); free_list(f->bcy); free_list(f->corner3);
     for (auto& l : f->interp) free_list(l);
@@ -520,6 +537,26 @@ int fc_set_problem(fc_forest* f, const fc_problem* pr) {
     return fail(FC_EINVAL, "g / gamma must be positive");
   if (pr->kind == FC_EULER_ROE && !(pr->p0 > 1.0)) return fail(FC_EINVAL, "gamma must exceed 1");
   if (pr->skip_quiescent != 0 && pr->skip_quiescent != 1) return fail(FC_EINVAL, "skip_quiescent must be 0 or 1");
+  if (pr->reflux != 0 && pr->reflux != 1) return fail(FC_EINVAL, "reflux must be 0 or 1");
+  if (pr->reflux && !f->reflux_planned) {
+    RefluxPlan rf;
+    std::string err;
+    int rc = plan_reflux(f->pl, f->pl.meqn, rf, err);
+    if (rc) return fail(rc, err);
+    if (!f->host_only) {
+      CK(cudaSetDevice(f->device));
+      const int64_t Pl1 = std::max<int64_t>(1, f->Pl);
+      CK(cudaMalloc(&f->d_rslot, Pl1 * sizeof(int32_t)));
+      if (f->Pl) CK(cudaMemcpy(f->d_rslot, rf.slot.data(), f->Pl * sizeof(int32_t), cudaMemcpyHostToDevice));
+      f->nrcells = (int64_t)rf.cells.size() / RFX;
+      if (f->nrcells) {
+        CK(cudaMalloc(&f->d_rcells, rf.cells.size() * sizeof(int32_t)));
+        CK(cudaMemcpy(f->d_rcells, rf.cells.data(), rf.cells.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&f->d_freg, (size_t)rf.nslots * 4 * f->pl.m * f->pl.meqn * sizeof(double)));
+      }
+    }
+    f->reflux_planned = true;
+  }
   f->prob = *pr;
   f->has_problem = true;
   return FC_OK;

@@ -135,4 +135,19 @@ int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& er
 int plan_activity(const Plan& pl, int meqn, std::vector<int32_t>& nbr, std::vector<uint8_t>& negmask,
                   std::string& err);
 
+// Coarse/fine reflux.  slot[lp] >= 0 for local patches with a face whose
+// neighbour is one level coarser or finer: the step kernel records, for each of their 4 faces and
+// m boundary edges, the applied flux in outward form into reg[((slot * 4 + face) * m + edge) *
+// meqn + k].  cells: one record per coarse cell next to >= 1 finer face, RFX ints each:
+// {q offset (storage, component 0), aux offset of kappa (natural, -1 = none), local patch,
+//  number of faces (1 or 2), then per face (ascending face order) {RO_coarse, RO_fine1, RO_fine2}}
+// with RO = register offset of component 0 of that (slot, face, edge).
+constexpr int RFX = 10;
+struct RefluxPlan {
+  std::vector<int32_t> slot;
+  int32_t nslots = 0;
+  std::vector<int32_t> cells;
+};
+int plan_reflux(const Plan& pl, int meqn, RefluxPlan& rf, std::string& err);
+
 }  // namespace fc

@@ -13,6 +13,8 @@
 // (tree, level, x, y), after composing face-crossing isometries; cells are then expanded through
 // that direction's affine map.  The two must produce bit-identical tables (tests/).
 #include <algorithm>
+#include <array>
+#include <map>
 #include <cstring>
 #include <tuple>
 
@@ -540,6 +542,115 @@ int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& er
       }
       rs.src[lp * G + r] = v;
     }
+  }
+  return FC_OK;
+}
+
+}  // namespace fc
+
+namespace fc {
+
+// Reflux pairing.  For every local patch p and face direction whose neighbour is
+// FINER: each coarse edge c of the face is covered by two fine edges, at tangential positions
+// c + 1/4 and c + 3/4 of a coarse cell.  The fine cells at depth 1 and 2 behind those positions are
+// located through the face transform of dir_info; their difference is the inward normal of the
+// fine patch's face, which gives the fine face and edge index in the fine patch's own frame.
+int plan_reflux(const Plan& pl, int meqn, RefluxPlan& rf, std::string& err) {
+  const int m = pl.m, n = pl.n;
+  const int64_t m2 = 2 * (int64_t)m, n2 = (int64_t)n * n, S = (int64_t)meqn * n2;
+  const int64_t Pl = pl.p1 - pl.p0;
+  static const int FD[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};
+  rf.slot.assign((size_t)Pl, -1);
+  rf.nslots = 0;
+  rf.cells.clear();
+  // slots: every local patch with a coarser or finer face neighbour
+  std::vector<std::array<DirKind, 4>> kinds((size_t)Pl);
+  std::vector<std::array<DirInfo, 4>> dirs((size_t)Pl);
+  for (int64_t lp = 0; lp < Pl; ++lp) {
+    bool cf = false;
+    for (int s = 0; s < 4; ++s) {
+      int rc = dir_info(pl, pl.p0 + lp, FD[s][0], FD[s][1], dirs[lp][s], err);
+      if (rc) return rc;
+      kinds[lp][s] = dirs[lp][s].kind;
+      cf |= kinds[lp][s] == D_FINER || kinds[lp][s] == D_COARSER;
+    }
+    if (cf) rf.slot[lp] = rf.nslots++;
+  }
+  auto RO = [&](int32_t slot, int face, int e) { return (int32_t)((((int64_t)slot * 4 + face) * m + e) * meqn); };
+  std::map<int64_t, std::vector<int32_t>> cells;   // coarse cell (lp, i, j) -> face triples
+  for (int64_t lp = 0; lp < Pl; ++lp) {
+    const int64_t p = pl.p0 + lp;
+    const Leaf& L = pl.leaves[p];
+    const int64_t sz = 1ll << (pl.lmax - L.level), h = sz, hh = h / 2;   // half a coarse / fine cell
+    const int64_t X0 = L.x * m2, Y0 = L.y * m2, W = m2 * sz;
+    for (int s = 0; s < 4; ++s) {
+      if (kinds[lp][s] != D_FINER) continue;
+      const DirInfo& D = dirs[lp][s];
+      if (meqn > 1 && !(D.T.r00 == 1 && D.T.r11 == 1 && D.T.r01 == 0 && D.T.r10 == 0)) {
+        err = "reflux of a system across a rotated tree link is not supported";
+        return FC_EUNSUP;
+      }
+      for (int c = 0; c < m; ++c) {
+        int32_t ro[2];
+        for (int hf = 0; hf < 2; ++hf) {
+          const int64_t tau = 2 * h * c + (hf ? 3 * hh : hh);
+          int64_t leaf[2];
+          int ic[2], jc[2];
+          for (int d = 0; d < 2; ++d) {
+            const int64_t dep = d ? 3 * hh : hh;
+            int64_t X, Y;
+            switch (s) {
+              case 0: X = X0 - dep; Y = Y0 + tau; break;
+              case 1: X = X0 + W + dep; Y = Y0 + tau; break;
+              case 2: X = X0 + tau; Y = Y0 - dep; break;
+              default: X = X0 + tau; Y = Y0 + W + dep; break;
+            }
+            int64_t cx, cy;
+            apply(D.T, X, Y, cx, cy);
+            const int64_t csz = sz / 2, cw = m2 * csz;
+            const int64_t id = find_leaf(pl, D.T.tree, L.level + 1, (cx / cw) * csz, (cy / cw) * csz);
+            if (id < 0) { err = "reflux: fine neighbour not found"; return FC_EBALANCE; }
+            const Leaf& N = pl.leaves[id];
+            leaf[d] = id;
+            ic[d] = (int)(((cx - N.x * m2) / hh + 1) / 2);
+            jc[d] = (int)(((cy - N.y * m2) / hh + 1) / 2);
+          }
+          if (leaf[0] != leaf[1]) { err = "reflux: fine edge pair split"; return FC_EBALANCE; }
+          const int di = ic[1] - ic[0], dj = jc[1] - jc[0];
+          int ff, fe;
+          if (di == 1 && dj == 0 && ic[0] == 1) { ff = 0; fe = jc[0] - 1; }
+          else if (di == -1 && dj == 0 && ic[0] == m) { ff = 1; fe = jc[0] - 1; }
+          else if (di == 0 && dj == 1 && jc[0] == 1) { ff = 2; fe = ic[0] - 1; }
+          else if (di == 0 && dj == -1 && jc[0] == m) { ff = 3; fe = ic[0] - 1; }
+          else { err = "reflux: fine face not found"; return FC_EBALANCE; }
+          const int64_t q = leaf[0];
+          if (q < pl.p0 || q >= pl.p1) {
+            err = "reflux across a rank boundary is not supported";
+            return FC_EUNSUP;
+          }
+          const int32_t fs = rf.slot[q - pl.p0];
+          if (fs < 0) { err = "reflux: fine patch without a flux slot"; return FC_EINVAL; }
+          ro[hf] = RO(fs, ff, fe);
+        }
+        const int ci = s == 0 ? 1 : (s == 1 ? m : c + 1), cj = s < 2 ? c + 1 : (s == 2 ? 1 : m);
+        auto& v = cells[(lp * (m + 2) + cj) * (m + 2) + ci];
+        v.push_back(RO(rf.slot[lp], s, c));
+        v.push_back(ro[0]);
+        v.push_back(ro[1]);
+      }
+    }
+  }
+  for (auto& kv : cells) {
+    const int64_t key = kv.first;
+    const int ci = (int)(key % (m + 2)), cj = (int)((key / (m + 2)) % (m + 2));
+    const int64_t lp = key / ((int64_t)(m + 2) * (m + 2));
+    const int nf = (int)kv.second.size() / 3;
+    if (nf < 1 || nf > 2) { err = "reflux: bad face count"; return FC_EINVAL; }
+    int32_t r[RFX] = {(int32_t)(lp * S + qcell(ci, cj, n)),
+                      pl.maux ? (int32_t)(lp * pl.maux * n2 + (int64_t)(cj + 1) * n + (ci + 1)) : -1,
+                      (int32_t)lp, nf, 0, 0, 0, 0, 0, 0};
+    for (int k = 0; k < 3 * nf; ++k) r[4 + k] = kv.second[k];
+    rf.cells.insert(rf.cells.end(), r, r + RFX);
   }
   return FC_OK;
 }

@@ -75,6 +75,11 @@ struct AdvConst {
                                          int, int, int, int) {
     return dtdx * fmax(fabs(P.p0), fabs(P.p1));
   }
+  // physical flux along axis D (coarse/fine reflux records)
+  template <int D>
+  __device__ static void flux(const double* q, int, double, const SolverParams& P, double* f) {
+    f[0] = (D == 1 ? P.p0 : P.p1) * q[0];
+  }
   __device__ static void precompute(const double*, int, const SolverParams&, double*, int) {}
   template <int D>
   __device__ static void riemann(const double* ql, const double* qr, const double*, const double*,
@@ -125,6 +130,11 @@ struct AdvEdgeCapa {
     }
     return c;
   }
+  // advective form: the flux through an edge is its normal velocity times the state
+  template <int D>
+  __device__ static void flux(const double* q, int, double uedge, const SolverParams&, double* f) {
+    f[0] = uedge * q[0];
+  }
   __device__ static void precompute(const double*, int, const SolverParams&, double*, int) {}
   template <int D>
   __device__ static void riemann(const double* ql, const double* qr, const double*, const double*,
@@ -170,6 +180,14 @@ struct SweRoe {
     const double h = q[0], ih = 1.0 / h;
     const double c = sqrt(P.p0 * h);
     return dtdx * (fmax(fabs(q[qs] * ih), fabs(q[2 * qs] * ih)) + c);
+  }
+  template <int D>
+  __device__ static void flux(const double* q, int qs, double, const SolverParams& P, double* f) {
+    constexpr int nd = D, td = 3 - D;
+    const double un = q[nd * qs] / q[0];
+    f[0] = q[nd * qs];
+    f[nd] = q[nd * qs] * un + 0.5 * P.p0 * q[0] * q[0];
+    f[td] = q[td * qs] * un;
   }
   // cell fields: sqrt(h), u, v
   __device__ static void precompute(const double* q, int qs, const SolverParams&, double* c, int cs) {
@@ -278,6 +296,17 @@ struct EulerRoe {
     const double p = (P.p0 - 1.0) * (q[3 * qs] - 0.5 * rho * (u * u + v * v));
     const double c = sqrt(P.p0 * p * ir);
     return dtdx * (fmax(fabs(u), fabs(v)) + c);
+  }
+  template <int D>
+  __device__ static void flux(const double* q, int qs, double, const SolverParams& P, double* f) {
+    constexpr int nd = D, td = 3 - D;
+    const double rho = q[0], mx = q[qs], my = q[2 * qs], E = q[3 * qs];
+    const double p = (P.p0 - 1.0) * (E - 0.5 * (mx * mx + my * my) / rho);
+    const double un = q[nd * qs] / rho;
+    f[0] = q[nd * qs];
+    f[nd] = q[nd * qs] * un + p;
+    f[td] = q[td * qs] * un;
+    f[3] = (E + p) * un;
   }
   // cell fields: sqrt(rho), u, v, H, c
   __device__ static void precompute(const double* q, int qs, const SolverParams& P, double* c, int cs) {

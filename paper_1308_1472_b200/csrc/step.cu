@@ -60,6 +60,8 @@ struct StepArgs {
   int m, tiles;                       // tiles per side
   unsigned long long* cfl_bits;
   double* fbuf;                       // method3 = 1 only: per-CTA F~ of each correction edge [MEQN][E2]
+  const int32_t* __restrict__ rslot;  // reflux: per patch flux-register slot (-1: none) or null
+  double* freg;                       // reflux: [slot][4 faces][m edges][MEQN] applied fluxes, outward
 };
 
 // ---- TMA bulk copies + mbarrier (sm_90+ / sm_100a) -------------------------------------------
@@ -321,7 +323,7 @@ constexpr int step_maxnreg(int nt, int minb) {
                                                                  : (16384 / (((nt * minb / 32) + 3) / 4 * 32)) / 8 * 8;
 }
 
-template <class S, int T, int NT, int MINB>
+template <class S, int T, int NT, int MINB, bool RF>
 __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step(StepArgs A, int ntiles) {
   using Sh = StepShape<S, T>;
   constexpr int MEQN = S::MEQN, W = Sh::W, WW = Sh::WW, EX = Sh::EX, E2 = Sh::E2;
@@ -395,6 +397,9 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
       tx = tt - ty * A.tiles;
     }
     const double dx = ldexp(A.dx0, -(int)A.level[patch]);
+    // coarse/fine reflux: this patch records the fluxes it applies through its 4 faces
+    const int slot = RF ? A.rslot[patch] : -1;   // RF: compiled with the reflux records
+    auto reg = [&](int face, int e) { return A.freg + (((int64_t)slot * 4 + face) * A.m + e) * MEQN; };
     const double dtdx = A.dt / dx;   // square cells: dt/dy = dt/dx
     mbar_wait(&bars[b], (phase >> b) & 1u);
     phase ^= 1u << b;
@@ -421,7 +426,7 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
     // Riemann problem of the tile has a zero jump, so all waves, fluctuations, corrections and
     // transverse terms are exactly 0 and q_new = q bitwise (the oracle computes q - 0 - 0).  Only
     // the CFL remains: the max over the tile's edges of the wave speeds, taken from the state.
-    if (A.skip_quiescent) {
+    if (A.skip_quiescent && !(RF && slot >= 0)) {
       bool diff = false;
       for (int t = opaque(threadIdx.x); t < MEQN * WW; t += NT) diff |= sq[t] != sq[(t / WW) * WW + qidx(1, 1)];
       const bool uniform = !__syncthreads_or(diff);
@@ -493,6 +498,18 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
             d -= r * XR[k];
             dq[(k * T + (j - 1)) * T + (i - 1)] = d;
           }
+          if (RF && slot >= 0) {   // x faces, part 1: A+dq - F~ (low face) / A-dq + F~ (high face)
+            if (tx == 0 && i == 1) {
+              double* g = reg(0, ty * T + j - 1);
+#pragma unroll
+              for (int k = 0; k < MEQN; ++k) g[k] = XR[k];
+            }
+            if (tx == A.tiles - 1 && i == T) {
+              double* g = reg(1, ty * T + j - 1);
+#pragma unroll
+              for (int k = 0; k < MEQN; ++k) g[k] = XL[k];
+            }
+          }
         }
         if (A.method3 == 1) {
 #pragma unroll
@@ -518,6 +535,12 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
     for (int t = opaque(threadIdx.x); t < T * T; t += NT) {
       const int i = 1 + t % T, j = 1 + t / T;
       const double s = rcell(i, j);
+      double* gl = nullptr;
+      double* gh = nullptr;
+      if (RF && slot >= 0) {   // y faces, part 1: the x-sweep's transverse flux at the face
+        if (ty == 0 && j == 1) gl = reg(2, tx * T + i - 1);
+        if (ty == A.tiles - 1 && j == T) gh = reg(3, tx * T + i - 1);
+      }
 #pragma unroll
       for (int k = 0; k < MEQN; ++k) {
         const double* up = ta + k * (T + 2) * T;
@@ -525,6 +548,8 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
         const double gt = up[j * T + (i - 1)] + dn[(j + 1) * T + (i - 1)];
         const double gb = up[(j - 1) * T + (i - 1)] + dn[j * T + (i - 1)];
         dq[(k * T + (j - 1)) * T + (i - 1)] -= s * (gt - gb);
+        if (gl) gl[k] = -gb;
+        if (gh) gh[k] = gt;
       }
     }
     for (int e = opaque(threadIdx.x); e < EX; e += NT) {       // column i, edge j (cells j-1 | j)
@@ -574,6 +599,22 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
             d -= r * XR[k];
             dq[(k * T + (j - 1)) * T + (i - 1)] = d;
           }
+          if (RF && slot >= 0) {   // y faces, part 2: fluctuation + F~ and the physical flux (outward)
+            if (ty == 0 && j == 1) {
+              double fq[MEQN];
+              S::template flux<2>(sq + qidx(i, 1), WW, S::CAPA ? sa[2 * WW + widx(i, 1)] : 0.0, A.sp, fq);
+              double* g = reg(2, tx * T + i - 1);
+#pragma unroll
+              for (int k = 0; k < MEQN; ++k) g[k] = (g[k] + XR[k]) - fq[k];
+            }
+            if (ty == A.tiles - 1 && j == T) {
+              double fq[MEQN];
+              S::template flux<2>(sq + qidx(i, T), WW, S::CAPA ? sa[2 * WW + widx(i, T + 1)] : 0.0, A.sp, fq);
+              double* g = reg(3, tx * T + i - 1);
+#pragma unroll
+              for (int k = 0; k < MEQN; ++k) g[k] = fq[k] + (XL[k] + g[k]);
+            }
+          }
         }
         if (A.method3 == 1) {
 #pragma unroll
@@ -604,6 +645,20 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
         const double* qs = sq + qidx(i, j);
         const double* d = dq + (j - 1) * T + (i - 1);
 #pragma unroll
+        double* gl = nullptr;
+        double* gh = nullptr;
+        double fql[MEQN], fqh[MEQN];
+        if (RF && slot >= 0) {   // x faces, part 2: the y-sweep's transverse flux and the physical flux
+          if (tx == 0 && i == 1) {
+            gl = reg(0, ty * T + j - 1);
+            S::template flux<1>(qs, WW, S::CAPA ? sa[WW + widx(1, j)] : 0.0, A.sp, fql);
+          }
+          if (tx == A.tiles - 1 && i == T) {
+            gh = reg(1, ty * T + j - 1);
+            S::template flux<1>(qs, WW, S::CAPA ? sa[WW + widx(T + 1, j)] : 0.0, A.sp, fqh);
+          }
+        }
+#pragma unroll
         for (int k = 0; k < MEQN; ++k) {
           const int c = k * T * (T + 2);
           const double fr = rt[c] + lf[c + 1];
@@ -611,6 +666,8 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
           const double val = qs[k * WW] + (d[k * T * T] - rc * (fr - fl));
           bad |= !isfinite(val);
           o[(int64_t)k * n2] = val;
+          if (gl) gl[k] = (gl[k] - fl) - fql[k];
+          if (gh) gh[k] = fqh[k] + (gh[k] + fr);
         }
       }
     }
@@ -778,17 +835,17 @@ int launch_filter(int kind, const double* qold, double* qnew, int npatch, int m,
 }
 
 // ---------------------------------------------------------------------------------------------
-template <class S, int T, int NT, int MINB>
+template <class S, int T, int NT, int MINB, bool RF>
 static int launch_step_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   const size_t smem = StepShape<S, T>::smem_bytes;
   static int resident = 0;   // CTAs that fit on the device at once (persistent grid)
   if (!resident) {
-    cudaFuncSetAttribute(k_step<S, T, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_step<S, T, NT, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_step<S, T, NT, MINB, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_step<S, T, NT, MINB, RF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<S, T, NT, MINB>, NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<S, T, NT, MINB, RF>, NT, smem);
     resident = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int64_t ntiles = npatch * a.tiles * a.tiles;
@@ -802,34 +859,44 @@ static int launch_step_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
       return -1;
     b.fbuf = fbuf;
   }
-  k_step<S, T, NT, MINB><<<(unsigned)grid, NT, smem, st>>>(b, (int)ntiles);
+  k_step<S, T, NT, MINB, RF><<<(unsigned)grid, NT, smem, st>>>(b, (int)ntiles);
   return 1;
+}
+
+template <class S, int T, int NT, int MINB>
+static int launch_step_r(const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  return a.rslot ? launch_step_t<S, T, NT, MINB, true>(a, npatch, st) : launch_step_t<S, T, NT, MINB, false>(a, npatch, st);
 }
 
 template <class S>
 static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   // CTAs per SM requested from ptxas for the 16 x 16 tile (register budget 65536 / (352 MB));
-  // FC_STEP_MINB overrides it for tuning experiments
+  // FC_STEP_MINB overrides it for tuning experiments (without reflux records)
   static const int env_mb = getenv("FC_STEP_MINB") ? atoi(getenv("FC_STEP_MINB")) : 0;
-  const int mb = env_mb ? env_mb : ((S::MEQN >= 3) ? 2 : 3);
+  constexpr int dmb = (S::MEQN >= 3) ? 2 : 3;
+  const int mb = env_mb ? env_mb : dmb;
   if (a.m % 16 == 0) {
-    if (mb == 1) return launch_step_t<S, 16, 352, 1>(a, npatch, st);
-    if (mb == 2) return launch_step_t<S, 16, 352, 2>(a, npatch, st);
-    if (mb == 3) return launch_step_t<S, 16, 352, 3>(a, npatch, st);
-    return launch_step_t<S, 16, 352, 4>(a, npatch, st);
+    if (a.rslot || mb == dmb) return launch_step_r<S, 16, 352, dmb>(a, npatch, st);
+    if (mb == 1) return launch_step_t<S, 16, 352, 1, false>(a, npatch, st);
+    if (mb == 2) return launch_step_t<S, 16, 352, 2, false>(a, npatch, st);
+    if (mb == 3) return launch_step_t<S, 16, 352, 3, false>(a, npatch, st);
+    return launch_step_t<S, 16, 352, 4, false>(a, npatch, st);
   }
-  if (a.m % 8 == 0) return launch_step_t<S, 8, 128, 4>(a, npatch, st);
-  if (a.m % 4 == 0) return launch_step_t<S, 4, 64, 8>(a, npatch, st);
-  if (a.m % 2 == 0) return launch_step_t<S, 2, 32, 8>(a, npatch, st);
+  if (a.m % 8 == 0) return launch_step_r<S, 8, 128, 4>(a, npatch, st);
+  if (a.m % 4 == 0) return launch_step_r<S, 4, 64, 8>(a, npatch, st);
+  if (a.m % 2 == 0) return launch_step_r<S, 2, 32, 8>(a, npatch, st);
   return -1;
 }
 
 int launch_step(int kind, const double* qold, double* qnew, const double* aux, const int8_t* level,
                 int64_t npatch, int m, double dt, double dx0, double p0, double p1, int limiter,
                 int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
-                const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits, cudaStream_t st) {
+                const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits,
+                const int32_t* rslot, double* freg, cudaStream_t st) {
   if (npatch <= 0) return 0;
   StepArgs a;
+  a.rslot = rslot;
+  a.freg = freg;
   a.qold = qold; a.qnew = qnew; a.aux = aux; a.level = level;
   a.dt = dt; a.dx0 = dx0; a.sp.p0 = p0; a.sp.p1 = p1;
   a.limiter = limiter; a.method2 = method2; a.method3 = method3;
@@ -850,6 +917,41 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
     case FC_EULER_ROE: return launch_step_s<EulerRoe>(a, npatch, st);
   }
   return -1;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Coarse/fine reflux: one thread per coarse cell next to a
+// finer face; per face (ascending face order) Q_C += dt / (kappa dx) (out_C + (out_f1 + out_f2)/2),
+// i.e. the flux the coarse cell applied is replaced by the mean of the two fine fluxes (all in
+// outward form, recorded by k_step).  Runs after k_step on q_new, before the commit.
+__global__ void __launch_bounds__(128) k_reflux(const int32_t* __restrict__ cells, int64_t ncells,
+                                                const double* __restrict__ freg, double* __restrict__ qnew,
+                                                const double* __restrict__ aux, const int8_t* __restrict__ level,
+                                                double dt, double dx0, int meqn, int n2) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ncells; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t* r = cells + t * RFX;
+    const double kap = r[1] >= 0 ? aux[r[1]] : 1.0;
+    const double rr = dt / (kap * ldexp(dx0, -(int)level[r[2]]));
+    double* q = qnew + r[0];
+    for (int f = 0; f < r[3]; ++f) {
+      const double* oc = freg + r[4 + 3 * f];
+      const double* f1 = freg + r[5 + 3 * f];
+      const double* f2 = freg + r[6 + 3 * f];
+      for (int k = 0; k < meqn; ++k) {
+        const double corr = oc[k] + 0.5 * (f1[k] + f2[k]);
+        q[(int64_t)k * n2] += rr * corr;
+      }
+    }
+  }
+}
+
+int launch_reflux(const int32_t* cells, int64_t ncells, const double* freg, double* qnew, const double* aux,
+                  const int8_t* level, double dt, double dx0, int meqn, int n2, cudaStream_t st) {
+  if (ncells <= 0) return 0;
+  const int64_t blocks = (ncells + 127) / 128;
+  k_reflux<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(cells, ncells, freg, qnew, aux, level,
+                                                                              dt, dx0, meqn, n2);
+  return 1;
 }
 
 }  // namespace fc

@@ -53,7 +53,7 @@ class ForestDesc(C.Structure):
 class Problem(C.Structure):
     _fields_ = [("kind", C.c_int32), ("p0", C.c_double), ("p1", C.c_double), ("limiter", C.c_int32),
                 ("method2", C.c_int32), ("method3", C.c_int32), ("cfl_reject", C.c_double),
-                ("skip_quiescent", C.c_int32)]
+                ("skip_quiescent", C.c_int32), ("reflux", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -166,8 +166,8 @@ class Forest:
 
     # -- calls -----------------------------------------------------------------------------------
     def set_problem(self, kind, p0=0.0, p1=0.0, limiter=FC_LIM_MC, method2=2, method3=2,
-                    cfl_reject=1.0, skip_quiescent=1):
-        pr = Problem(kind, p0, p1, limiter, method2, method3, cfl_reject, skip_quiescent)
+                    cfl_reject=1.0, skip_quiescent=1, reflux=0):
+        pr = Problem(kind, p0, p1, limiter, method2, method3, cfl_reject, skip_quiescent, reflux)
         _check(lib().fc_set_problem(self.h, C.byref(pr)), "fc_set_problem")
 
     def set_aux(self, aux):
@@ -281,7 +281,7 @@ def forest_for(w, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id=None,
                device, rank, nranks, nccl_id)
     if device >= 0:
         f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject,
-                      skip_quiescent)
+                      skip_quiescent, getattr(w, "reflux", 0))
         if w.aux is not None:
             f.set_aux(np.ascontiguousarray(w.aux[f.first:f.first + f.count]))
     return f

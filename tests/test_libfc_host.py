@@ -150,3 +150,28 @@ def test_single_patch_forest_tables():
     _, t = host_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m)
     assert (t[..., 0] == 1).all() and (t[..., 1] == 0).all()
     np.testing.assert_array_equal(t, oracle_table(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m))
+
+
+# ---- coarse/fine reflux planning -----------------------------------------------
+def test_reflux_plan_accepts_single_rank_amr_and_rejects_split_pairs():
+    """fc_set_problem(reflux = 1) plans the coarse/fine flux pairing on the host: accepted on one
+    rank for C2 and the cubed sphere; with Morton shards that cut a coarse/fine pair it reports
+    FC_EUNSUP (the fine fluxes would live on another rank); conforming forests always pass."""
+    from workloads.cubed_sphere import c4_workload
+    for w in (c2(), c4_workload(base_level=2, m=8, steps=1)):
+        f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, device=-1)
+        f.set_problem(w.kind, w.params[0], w.params[1], reflux=1)
+    w = c2()
+    codes = []
+    for r in range(3):
+        f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, 1, device=-1, rank=r, nranks=3)
+        try:
+            f.set_problem(w.kind, w.params[0], w.params[1], reflux=1)
+            codes.append(0)
+        except fc.FcError as e:
+            codes.append(e.code)
+    assert fc.FC_EUNSUP in codes
+    w = c5(level=2, m=8)
+    for r in range(3):
+        f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, 4, device=-1, rank=r, nranks=3)
+        f.set_problem(w.kind, w.params[0], w.params[1], reflux=1)
