@@ -13,7 +13,7 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["forest.c", "ghost.c", "claw.c"]
+SOURCES = ["forest.c", "ghost.c", "claw.c", "subcycle.c"]
 LIB = os.path.join(HERE, "liboracle.so")
 
 OK, EINVAL, ETILING, ECONN, EBALANCE, ENOMEM, EUNSUP, EPHYS = 0, -1, -2, -3, -4, -5, -6, -7
@@ -72,6 +72,8 @@ def lib():
                                            C.c_double, C.c_double, P, P]
         L.orc_step_patch_faces.restype = C.c_double
         L.orc_flux.argtypes = [C.POINTER(Problem), C.c_int, P, C.c_double, P]
+        L.orc_step_subcycled.argtypes = [P, C.POINTER(Problem), P, P, C.c_double, C.c_double, P,
+                                         C.POINTER(C.c_double)]
         L.orc_limiter.argtypes = [C.c_int, C.c_double]
         L.orc_limiter.restype = C.c_double
         L.orc_meqn.argtypes = [C.c_int]
@@ -222,6 +224,19 @@ class OracleForest:
             raise RuntimeError(f"orc_step -> {rc}")
         return out, cfl.value
 
+    def step_subcycled(self, pr: Problem, qpad: np.ndarray, dt_coarse: float, dx0: float, aux=None):
+        """One sub-cycled step (per-level dt, time-interpolated coarse ghosts; subcycle.c) of the
+        coarsest level by dt_coarse -> (qout padded, interiors valid; cfl)."""
+        qpad = np.ascontiguousarray(qpad, np.float64)
+        out = np.empty_like(qpad)
+        cfl = C.c_double()
+        ap = None if aux is None else np.ascontiguousarray(aux, np.float64)
+        rc = lib().orc_step_subcycled(self.h, C.byref(pr), _p(qpad), None if ap is None else _p(ap),
+                                      dt_coarse, dx0, _p(out), C.byref(cfl))
+        if rc:
+            raise RuntimeError(f"orc_step_subcycled -> {rc}")
+        return out, cfl.value
+
     def step_sample(self, pr: Problem, q: np.ndarray, dt: float, dx0: float, ids, aux=None):
         q = np.ascontiguousarray(q, np.float64)
         ids = np.ascontiguousarray(ids, np.int64)
@@ -271,6 +286,35 @@ def run(w, steps: int | None = None, dt_list=None, nthreads: int = 1, forest=Non
             # Clawpack retake with dt * target / cfl (state unchanged)
             dt = dt * w.cfl_target / cfl
             out, cfl = f.step(pr, qp, dt, dx0, w.aux, nthreads)
+        cfls.append(cfl)
+        dts.append(dt)
+        qp = out
+        if dt_list is None:
+            dt = w.next_dt(dt, cfl)
+    m = w.m
+    return np.ascontiguousarray(qp[:, :, 2:m + 2, 2:m + 2]), np.array(cfls), np.array(dts)
+
+
+def run_subcycled(w, steps: int | None = None, dt_list=None, forest=None):
+    """Sub-cycled driver (subcycle.c): each step advances the coarsest level by dt_coarse and every
+    finer level l by dt_coarse 2^-(l - lmin).  dt_coarse starts at w.dt0 * 2^(lmax - lmin) (the
+    workload's dt0 is the finest level's) and follows the workload's policy on the returned CFL.
+    Returns (q [P][meqn][m][m], cfls, dt_coarse list)."""
+    f = forest or forest_for(w)
+    pr = problem_for(w)
+    steps = w.steps if steps is None else steps
+    qp = f.pad(w.q0)
+    dx0 = 1.0 / w.m
+    lv = w.forest.levels
+    dt = w.dt0 * 2.0 ** (int(lv.max()) - int(lv.min()))
+    cfls, dts = [], []
+    for n in range(steps):
+        if dt_list is not None:
+            dt = dt_list[n]
+        out, cfl = f.step_subcycled(pr, qp, dt, dx0, w.aux)
+        if cfl > w.cfl_reject and dt_list is None:
+            dt = dt * w.cfl_target / cfl
+            out, cfl = f.step_subcycled(pr, qp, dt, dx0, w.aux)
         cfls.append(cfl)
         dts.append(dt)
         qp = out

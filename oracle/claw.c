@@ -306,6 +306,11 @@ void orc_flux(const orc_problem* pr, int ixy, const double* q, double uedge, dou
 
 /* ---- one patch -------------------------------------------------------------------------------- */
 static int g_step_error = 0;   /* first solver error seen by orc_step_patch (physical guard) */
+int orc_take_step_error(void) {
+  int e = g_step_error;
+  g_step_error = 0;
+  return e;
+}
 
 double orc_step_patch(const orc_problem* pr, int m, int meqn, const double* qp, const double* auxp,
                       double dt, double dx, double dy, double* qnew) {

@@ -308,11 +308,22 @@ static int fine_cell(const orc_forest* f, int t, int64_t X, int64_t Y, int l, in
 
 int orc_reflux(const orc_forest* f, const orc_problem* pr, const double* faces, const double* aux,
                double dt, double dx0, double* qout) {
+  return orc_reflux_ex(f, pr, faces, faces, 1.0, dt, -1, aux, dx0, qout);
+}
+
+/* the reflux of coarse patches of level `level` (all levels if < 0), with the coarse records
+ * weighted by wc and the fine ones taken from faces_f:
+ *   Q_C += dtr / (kappa dx) (wc out_C + (F_1 + F_2) / 2)
+ * global dt: faces_f = faces_c, wc = 1, dtr = dt;  sub-cycling: faces_f = dt-weighted fine sums
+ * over the fine sub-steps, wc = dt_coarse, dtr = 1 */
+int orc_reflux_ex(const orc_forest* f, const orc_problem* pr, const double* faces, const double* faces_f,
+                  double wc, double dtr, int level, const double* aux, double dx0, double* qout) {
   const int m = f->m, meqn = orc_meqn(pr->kind), n = ORC_N(m);
   const size_t S = (size_t)meqn * n * n, SA = (size_t)3 * n * n, FS = (size_t)4 * m * meqn;
   for (int64_t p = 0; p < f->P; ++p) {
     const int l = f->level[p];
     if (l >= f->lmax) continue;                       /* no finer neighbour possible */
+    if (level >= 0 && l != level) continue;
     const int64_t s = 1ll << (f->lmax - l);           /* half a cell of p; s / 2 = half a fine cell */
     const int64_t sh = s / 2;
     const int64_t X0 = f->x[p] * 2 * m, Y0 = f->y[p] * 2 * m;
@@ -354,14 +365,14 @@ int orc_reflux(const orc_forest* f, const orc_problem* pr, const double* faces, 
           else if (di == 0 && dj == 1 && jc[0] == 1) { ff = 2; fe = ic[0] - 1; }
           else if (di == 0 && dj == -1 && jc[0] == m) { ff = 3; fe = ic[0] - 1; }
           else return ORC_EBALANCE;
-          of[h] = faces + Lc[0] * FS + ((size_t)ff * m + fe) * meqn;
+          of[h] = faces_f + Lc[0] * FS + ((size_t)ff * m + fe) * meqn;
         }
         if (!ok) continue;                            /* not a coarse/fine edge */
         const int ci = sf == 0 ? 1 : (sf == 1 ? m : c + 1), cj = sf < 2 ? c + 1 : (sf == 2 ? 1 : m);
         const double kap = aux ? aux[p * SA + ORC_IDX(m, ci, cj)] : 1.0;
-        const double r = dt / (kap * dx);
+        const double r = dtr / (kap * dx);
         for (int k = 0; k < meqn; ++k) {
-          const double corr = oc[k] + 0.5 * (of[0][k] + of[1][k]);
+          const double corr = wc * oc[k] + 0.5 * (of[0][k] + of[1][k]);
           qout[p * S + (size_t)k * n * n + ORC_IDX(m, ci, cj)] += r * corr;
         }
       }

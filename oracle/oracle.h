@@ -97,6 +97,21 @@ double orc_step_patch_faces(const orc_problem* pr, int m, int meqn, const double
  * (meqn > 1) across non-aligned tree links are not supported (ORC_EUNSUP). */
 int orc_reflux(const orc_forest* f, const orc_problem* pr, const double* faces, const double* aux,
                double dt, double dx0, double* qout);
+/* general form (coarse patches of one level, weighted records), see forest.c */
+int orc_reflux_ex(const orc_forest* f, const orc_problem* pr, const double* faces, const double* faces_f,
+                  double wc, double dtr, int level, const double* aux, double dx0, double* qout);
+/* Sub-cycled step (PAPER.md:201-202 [§3] "when sub-cycling, time accurate data between coarse grids
+ * is used to fill in ghost cells for fine grids"; PAPER.md:277-290 [§4] one exchange per level,
+ * coarse-to-fine recursion, correction factors propagated back): level l advances with
+ * dt_l = dt_coarse 2^-(l - lmin); advance(l, t): ghost fill at time t of a snapshot in which every
+ * patch of level >= l holds its current state and every coarser patch the linear interpolation in
+ * time between its last two states, update of the level-l patches, then two advances of level
+ * l+1 at t and t + dt_{l+1}, then (reflux on) the level-l / level-(l+1) flux correction with the
+ * coarse flux x dt_l against the fine fluxes x dt_{l+1} summed over both sub-steps.  Times are
+ * integer ticks of the finest sub-step, so the interpolation weights are exact dyadic numbers.
+ * qpad [P][meqn][n][n] in (interiors used), qout interiors out; *cfl = max over all updates. */
+int orc_step_subcycled(const orc_forest* f, const orc_problem* pr, const double* qpad, const double* aux,
+                       double dt_coarse, double dx0, double* qout, double* cfl);
 /* physical flux along axis ixy of state q (uedge: edge velocity, advective form) */
 void orc_flux(const orc_problem* pr, int ixy, const double* q, double uedge, double* f);
 

@@ -17,6 +17,8 @@ struct orc_forest {
 };
 
 const int32_t* orc_cached_table(const orc_forest* f, int* rc);
+/* first solver error since the last call (physical-state guard of orc_step_patch), then clear */
+int orc_take_step_error(void);
 
 /* padded index of 1-based cell (i, j), i, j in [-1, m+2], in an n x n array (x fastest) */
 #define ORC_N(m) ((m) + 4)
