@@ -152,6 +152,17 @@ int fc_ghost_fill(fc_forest* f);
  * NaN/Inf or the updated state is not finite (state unchanged).  Synchronises the handle's stream (the CFL is returned to the host). */
 int fc_step(fc_forest* f, double dt, double* max_cfl);
 
+/* One sub-cycled step (PAPER.md:201-202 [§3] "when sub-cycling, time accurate data between coarse
+ * grids is used to fill in ghost cells for fine grids", PAPER.md:277-290 [§4] one exchange per
+ * level, coarse-to-fine recursion): the coarsest level of the forest advances by
+ * dt_coarse and level l by dt_coarse 2^-(l - lmin), each level after a ghost fill (halo exchange
+ * included) in which coarser patches hold their state interpolated linearly in time; with
+ * fc_problem.reflux the coarse/fine fluxes are balanced over the fine sub-steps.  *max_cfl = max over
+ * all level updates; commit / FC_ECFL / FC_ENONFINITE as fc_step.  On a one-level forest this is
+ * fc_step(dt_coarse).  FC_ESTATE on a manual-transport handle.  Extra device memory: two state-sized
+ * buffers, allocated at the first call. */
+int fc_step_subcycled(fc_forest* f, double dt_coarse, double* max_cfl);
+
 /* Interior q_old -> q[P_local][meqn][m][m].  Synchronous. */
 int fc_get_q(fc_forest* f, double* q, int where);
 

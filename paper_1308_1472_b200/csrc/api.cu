@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -31,8 +32,13 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
                 int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
                 const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits,
                 const int32_t* rslot, double* freg, cudaStream_t st);
-int launch_reflux(const int32_t* cells, int64_t ncells, const double* freg, double* qnew, const double* aux,
-                  const int8_t* level, double dt, double dx0, int meqn, int n2, cudaStream_t st);
+int launch_reflux(const int32_t* cells, int64_t ncells, const double* freg, const double* ffine, double* qnew,
+                  const double* aux, const int8_t* level, double wc, double dtr, double dx0, int meqn, int n2,
+                  cudaStream_t st);
+int launch_sub_snapshot(const double* cur, double* old, double* snap, const int8_t* level, int64_t P, int meqn,
+                        int m, int n2, int l, const double* alpha, int lmin, cudaStream_t st);
+int launch_sub_accumulate(const int32_t* list, int64_t n, const int32_t* rslot, const double* rec, double* acc,
+                          int fs, double dt, int add, cudaStream_t st);
 int launch_filter(int kind, const double* qold, double* qnew, int npatch, int m, uint8_t* uflag, double* uval,
                   const int32_t* nbr, const uint8_t* negmask, const int8_t* level, double dt, double dx0,
                   double p0, double p1, int32_t* active, int32_t* nactive, unsigned long long* cfl_bits,
@@ -94,6 +100,17 @@ struct fc_forest {
   int32_t* d_rcells = nullptr;         // [ncells][RFX]
   int64_t nrcells = 0;
   double* d_freg = nullptr;            // [slots][4][m][meqn] applied face fluxes (outward)
+  int32_t nslots = 0;
+  std::vector<int64_t> rcell_off;      // reflux cells sorted by coarse level: [level - glmin] offsets
+  // sub-cycling (fc_step_subcycled): levels [glmin, glmax] of the whole forest, per-level local lists
+  int glmin = 0, glmax = 0;
+  bool sub_ready = false;
+  double *d_sub_old = nullptr, *d_sub_snap = nullptr, *d_facc = nullptr;
+  std::vector<int32_t*> d_lvl;         // per level: local patch ids
+  std::vector<int64_t> n_lvl;
+  int32_t* d_lvl_cnt = nullptr;        // per level: count (device, for k_step's active list)
+  int64_t sub_tick_old[32] = {}, sub_tick_new[32] = {};
+  double sub_dt0 = 0.0;
   std::vector<DevList> interp, bcx_l, bcy_l;
   fc_problem prob{};
   bool has_problem = false, has_q = false, has_aux = false;
@@ -335,8 +352,8 @@ static int update_local(fc_forest* f, double dt) {
   f->st.step_kernel_launches += lr;
   CK(cudaGetLastError());
   if (reflux) {   // coarse cells next to finer faces: applied flux -> mean of the fine fluxes
-    f->st.kernel_launches += launch_reflux(f->d_rcells, f->nrcells, f->d_freg, f->qnew, f->aux, f->d_level, dt,
-                                           f->pl.dx0, f->pl.meqn, f->pl.n * f->pl.n, f->stream);
+    f->st.kernel_launches += launch_reflux(f->d_rcells, f->nrcells, f->d_freg, f->d_freg, f->qnew, f->aux,
+                                           f->d_level, 1.0, dt, f->pl.dx0, f->pl.meqn, f->pl.n * f->pl.n, f->stream);
     CK(cudaGetLastError());
   }
   return FC_OK;
@@ -369,6 +386,8 @@ static void destroy(fc_forest* f) {
     cudaFree(f->d_nbr); cudaFree(f->d_active); cudaFree(f->d_nactive); cudaFree(f->d_negmask);
     cudaFree(f->d_uflag); cudaFree(f->d_uval);
     cudaFree(f->d_rslot); cudaFree(f->d_rcells); cudaFree(f->d_freg);
+    cudaFree(f->d_sub_old); cudaFree(f->d_sub_snap); cudaFree(f->d_facc); cudaFree(f->d_lvl_cnt);
+    for (auto* d : f->d_lvl) cudaFree(d);
     if (f->h_cfl) cudaFreeHost(f->h_cfl);
     free_list(f->copy); free_list(f->avg); free_list(f->bcx); free_list(f->bcy); free_list(f->corner3);
     for (auto& l : f->interp) free_list(l);
@@ -405,6 +424,12 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
   if (rc) { delete f; return fail(rc, err); }
   f->Pl = f->pl.p1 - f->pl.p0;
   f->st.local_patches = f->Pl;
+  f->glmin = 127;
+  f->glmax = -1;
+  for (const Leaf& L : f->pl.leaves) {   // levels of the whole forest (same on every rank)
+    f->glmin = std::min(f->glmin, (int)L.level);
+    f->glmax = std::max(f->glmax, (int)L.level);
+  }
   f->st.uniform_fast_path = 0;
   if (d->device < 0) {           // host-only planning handle: tables and plans, no device work
     f->host_only = true;
@@ -543,6 +568,21 @@ int fc_set_problem(fc_forest* f, const fc_problem* pr) {
     std::string err;
     int rc = plan_reflux(f->pl, f->pl.meqn, rf, err);
     if (rc) return fail(rc, err);
+    {   // cells grouped by the coarse patch's level (sub-cycling refluxes one level pair at a time)
+      const int64_t nc = (int64_t)rf.cells.size() / RFX;
+      std::vector<int64_t> idx(nc);
+      for (int64_t i = 0; i < nc; ++i) idx[i] = i;
+      auto lev = [&](int64_t i) { return (int)f->pl.leaves[f->pl.p0 + rf.cells[i * RFX + 2]].level; };
+      std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return lev(a) < lev(b); });
+      std::vector<int32_t> sorted(rf.cells.size());
+      for (int64_t i = 0; i < nc; ++i)
+        std::copy(rf.cells.begin() + idx[i] * RFX, rf.cells.begin() + (idx[i] + 1) * RFX, sorted.begin() + i * RFX);
+      rf.cells.swap(sorted);
+      f->rcell_off.assign(f->glmax - f->glmin + 2, 0);
+      for (int64_t i = 0; i < nc; ++i) f->rcell_off[lev(i) - f->glmin + 1] += 1;
+      for (size_t l = 1; l < f->rcell_off.size(); ++l) f->rcell_off[l] += f->rcell_off[l - 1];
+      f->nslots = rf.nslots;
+    }
     if (!f->host_only) {
       CK(cudaSetDevice(f->device));
       const int64_t Pl1 = std::max<int64_t>(1, f->Pl);
@@ -717,6 +757,116 @@ int fc_step(fc_forest* f, double dt, double* max_cfl) {
     cudaEventElapsedTime(&b, f->ev[1], f->ev[2]);
     cudaEventElapsedTime(&c, f->ev[2], f->ev[3]);
     f->st.ms_ghost += a;
+    f->st.ms_step += b;
+    f->st.ms_comm += c;
+  }
+  const double cfl = *f->h_cfl;
+  if (max_cfl) *max_cfl = cfl;
+  return commit(f, cfl);
+}
+
+// ---- sub-cycled step ---------------------------------
+// Level l advances with dt_l = dt_coarse 2^-(l - glmin) in a coarse-to-fine recursion; the ghost
+// fill of level l at each of its start times runs on a snapshot in which coarser patches hold their
+// state interpolated linearly in time (exact dyadic weights from integer ticks).  Buffers: q_old =
+// the committed state (untouched until the commit), q_new = the working state (all levels at their
+// current times), d_sub_old = each level's state at the start of its current step, d_sub_snap = the
+// snapshot with its rings (the ghost fill and the halo exchange run on it).
+static int sub_prepare(fc_forest* f) {
+  if (f->sub_ready) return FC_OK;
+  const int NL = f->glmax - f->glmin + 1;
+  if (NL > 30) return fail(FC_EUNSUP, "more than 30 refinement levels");
+  CK(cudaMalloc(&f->d_sub_old, f->state_doubles * sizeof(double)));
+  CK(cudaMalloc(&f->d_sub_snap, f->state_doubles * sizeof(double)));
+  CK(cudaMemset(f->d_sub_snap, 0, f->state_doubles * sizeof(double)));
+  std::vector<std::vector<int32_t>> lists(NL);
+  for (int64_t lp = 0; lp < f->Pl; ++lp) lists[f->pl.leaves[f->pl.p0 + lp].level - f->glmin].push_back((int32_t)lp);
+  std::vector<int32_t> cnt(NL);
+  f->d_lvl.assign(NL, nullptr);
+  f->n_lvl.assign(NL, 0);
+  for (int l = 0; l < NL; ++l) {
+    f->n_lvl[l] = (int64_t)lists[l].size();
+    cnt[l] = (int32_t)lists[l].size();
+    CK(cudaMalloc(&f->d_lvl[l], std::max<size_t>(1, lists[l].size()) * sizeof(int32_t)));
+    if (!lists[l].empty())
+      CK(cudaMemcpy(f->d_lvl[l], lists[l].data(), lists[l].size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  CK(cudaMalloc(&f->d_lvl_cnt, NL * sizeof(int32_t)));
+  CK(cudaMemcpy(f->d_lvl_cnt, cnt.data(), NL * sizeof(int32_t), cudaMemcpyHostToDevice));
+  f->sub_ready = true;
+  return FC_OK;
+}
+
+static int sub_advance(fc_forest* f, int l, int64_t tick, int sub) {
+  const fc_problem& p = f->prob;
+  const int li = l - f->glmin, m = f->pl.m, meqn = f->pl.meqn, n2 = f->pl.n * f->pl.n;
+  const int64_t len = 1ll << (f->glmax - l);
+  const double dt = std::ldexp(f->sub_dt0, -li);
+  const bool reflux = p.reflux && f->nrcells > 0;
+  double alpha[32] = {};
+  for (int c = f->glmin; c < l; ++c)
+    alpha[c - f->glmin] = (double)(tick - f->sub_tick_old[c - f->glmin]) /
+                          (double)(f->sub_tick_new[c - f->glmin] - f->sub_tick_old[c - f->glmin]);
+  f->st.kernel_launches += launch_sub_snapshot(f->qnew, f->d_sub_old, f->d_sub_snap, f->d_level, f->Pl, meqn, m, n2,
+                                               l, alpha, f->glmin, f->stream);
+  CK(cudaGetLastError());
+  double* committed = f->qold;       // the ghost fill (and its halo exchange) runs on the snapshot
+  f->qold = f->d_sub_snap;
+  int rc = ghost_fill_internal(f);
+  f->qold = committed;
+  if (rc) return rc;
+  if (f->n_lvl[li] > 0) {
+    int lr = launch_step(p.kind, f->d_sub_snap, f->qnew, f->aux, f->d_level, f->n_lvl[li], m, dt, f->pl.dx0, p.p0,
+                         p.p1, p.limiter, p.method2, p.method3, p.skip_quiescent, nullptr, f->d_bcflag, f->d_lvl[li],
+                         f->d_lvl_cnt + li, f->d_cfl, reflux ? f->d_rslot : nullptr, reflux ? f->d_freg : nullptr,
+                         f->stream);
+    if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
+    f->st.kernel_launches += lr;
+    f->st.step_kernel_launches += lr;
+    CK(cudaGetLastError());
+    if (reflux)
+      f->st.kernel_launches += launch_sub_accumulate(f->d_lvl[li], f->n_lvl[li], f->d_rslot, f->d_freg, f->d_facc,
+                                                     4 * m * meqn, dt, sub, f->stream);
+  }
+  f->sub_tick_old[li] = tick;
+  f->sub_tick_new[li] = tick + len;
+  if (l < f->glmax) {
+    if ((rc = sub_advance(f, l + 1, tick, 0))) return rc;
+    if ((rc = sub_advance(f, l + 1, tick + len / 2, 1))) return rc;
+    if (reflux) {
+      const int64_t a = f->rcell_off[li], b = f->rcell_off[li + 1];
+      f->st.kernel_launches += launch_reflux(f->d_rcells + a * RFX, b - a, f->d_freg, f->d_facc, f->qnew, f->aux,
+                                             f->d_level, dt, 1.0, f->pl.dx0, meqn, n2, f->stream);
+      CK(cudaGetLastError());
+    }
+  }
+  return FC_OK;
+}
+
+int fc_step_subcycled(fc_forest* f, double dt_coarse, double* max_cfl) {
+  int rc = check_step_args(f, dt_coarse);
+  if (rc) return rc;
+  if (f->manual) return fail(FC_ESTATE, "manual halo transport: sub-cycling needs the NCCL transport");
+  if (f->glmin == f->glmax) return fc_step(f, dt_coarse, max_cfl);   // one level: the global step
+  CK(cudaSetDevice(f->device));
+  if ((rc = sub_prepare(f))) return rc;
+  if (f->prob.reflux && f->nrcells > 0 && !f->d_facc)
+    CK(cudaMalloc(&f->d_facc, (size_t)std::max<int32_t>(1, f->nslots) * 4 * f->pl.m * f->pl.meqn * sizeof(double)));
+  if (f->timing) CK(cudaEventRecord(f->ev[0], f->stream));
+  CK(cudaMemsetAsync(f->d_cfl, 0, sizeof(unsigned long long), f->stream));
+  CK(cudaMemcpyAsync(f->qnew, f->qold, f->state_doubles * sizeof(double), cudaMemcpyDeviceToDevice, f->stream));
+  f->sub_dt0 = dt_coarse;
+  if ((rc = sub_advance(f, f->glmin, 0, 0))) return rc;
+  if (f->timing) CK(cudaEventRecord(f->ev[2], f->stream));
+  if (f->pl.nranks > 1)
+    NK(ncclAllReduce(f->d_cfl, f->d_cfl, 1, ncclDouble, ncclMax, f->comm, f->stream));
+  if (f->timing) CK(cudaEventRecord(f->ev[3], f->stream));
+  CK(cudaMemcpyAsync(f->h_cfl, f->d_cfl, sizeof(double), cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  if (f->timing) {
+    float b = 0.f, c = 0.f;
+    cudaEventElapsedTime(&b, f->ev[0], f->ev[2]);
+    cudaEventElapsedTime(&c, f->ev[2], f->ev[3]);
     f->st.ms_step += b;
     f->st.ms_comm += c;
   }

@@ -924,33 +924,101 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
 // finer face; per face (ascending face order) Q_C += dt / (kappa dx) (out_C + (out_f1 + out_f2)/2),
 // i.e. the flux the coarse cell applied is replaced by the mean of the two fine fluxes (all in
 // outward form, recorded by k_step).  Runs after k_step on q_new, before the commit.
+// General form Q_C += dtr / (kappa dx) (wc out_C + (F_1 + F_2)/2) with the fine F from ffine:
+// global dt: ffine = freg, wc = 1, dtr = dt; sub-cycling: ffine = the dt-weighted fine sums over
+// the two fine sub-steps, wc = dt of the coarse level, dtr = 1.
 __global__ void __launch_bounds__(128) k_reflux(const int32_t* __restrict__ cells, int64_t ncells,
-                                                const double* __restrict__ freg, double* __restrict__ qnew,
-                                                const double* __restrict__ aux, const int8_t* __restrict__ level,
-                                                double dt, double dx0, int meqn, int n2) {
+                                                const double* __restrict__ freg, const double* __restrict__ ffine,
+                                                double* __restrict__ qnew, const double* __restrict__ aux,
+                                                const int8_t* __restrict__ level, double wc, double dtr, double dx0,
+                                                int meqn, int n2) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ncells; t += (int64_t)gridDim.x * blockDim.x) {
     const int32_t* r = cells + t * RFX;
     const double kap = r[1] >= 0 ? aux[r[1]] : 1.0;
-    const double rr = dt / (kap * ldexp(dx0, -(int)level[r[2]]));
+    const double rr = dtr / (kap * ldexp(dx0, -(int)level[r[2]]));
     double* q = qnew + r[0];
     for (int f = 0; f < r[3]; ++f) {
       const double* oc = freg + r[4 + 3 * f];
-      const double* f1 = freg + r[5 + 3 * f];
-      const double* f2 = freg + r[6 + 3 * f];
+      const double* f1 = ffine + r[5 + 3 * f];
+      const double* f2 = ffine + r[6 + 3 * f];
       for (int k = 0; k < meqn; ++k) {
-        const double corr = oc[k] + 0.5 * (f1[k] + f2[k]);
+        const double corr = wc * oc[k] + 0.5 * (f1[k] + f2[k]);
         q[(int64_t)k * n2] += rr * corr;
       }
     }
   }
 }
 
-int launch_reflux(const int32_t* cells, int64_t ncells, const double* freg, double* qnew, const double* aux,
-                  const int8_t* level, double dt, double dx0, int meqn, int n2, cudaStream_t st) {
+int launch_reflux(const int32_t* cells, int64_t ncells, const double* freg, const double* ffine, double* qnew,
+                  const double* aux, const int8_t* level, double wc, double dtr, double dx0, int meqn, int n2,
+                  cudaStream_t st) {
   if (ncells <= 0) return 0;
   const int64_t blocks = (ncells + 127) / 128;
-  k_reflux<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(cells, ncells, freg, qnew, aux, level,
-                                                                              dt, dx0, meqn, n2);
+  k_reflux<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 128, 0, st>>>(cells, ncells, freg, ffine, qnew, aux,
+                                                                              level, wc, dtr, dx0, meqn, n2);
+  return 1;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Sub-cycling, driven by fc_step_subcycled (api.cu).
+// Snapshot for the ghost fill of level l at one time: patches of level >= l hold their current
+// interior, coarser ones (1 - a) Q_old + a Q_new with a the exact dyadic weight of their level
+// (separately rounded products, as the oracle); level-l patches also save Q_old := current.
+struct SubAlpha {
+  double a[32];
+  int lmin;
+};
+__global__ void k_sub_snapshot(const double* __restrict__ cur, double* __restrict__ old, double* __restrict__ snap,
+                               const int8_t* __restrict__ level, int64_t P, int meqn, int mm, int n2, int l,
+                               SubAlpha al) {
+  const int64_t per = (int64_t)meqn * mm, tot = P * per;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = t / per;
+    const int r = (int)(t - p * per), k = r / mm, c = r - k * mm;
+    const int64_t o = (p * meqn + k) * n2 + c;     // dense interior (qcell)
+    const int lp = level[p];
+    if (lp >= l) {
+      const double v = cur[o];
+      snap[o] = v;
+      if (lp == l) old[o] = v;
+    } else {
+      const double a = al.a[lp - al.lmin];
+      snap[o] = __dadd_rn(__dmul_rn(1.0 - a, old[o]), __dmul_rn(a, cur[o]));
+    }
+  }
+}
+
+// fine-side reflux sums: acc = dt rec (first sub-step of the parent's step) or acc + dt rec
+__global__ void k_sub_accumulate(const int32_t* __restrict__ list, int64_t n, const int32_t* __restrict__ rslot,
+                                 const double* __restrict__ rec, double* __restrict__ acc, int fs, double dt,
+                                 int add) {
+  const int64_t tot = n * fs;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / fs;
+    const int e = (int)(t - i * fs);
+    const int32_t slot = rslot[list[i]];
+    if (slot < 0) continue;
+    const int64_t o = (int64_t)slot * fs + e;
+    const double v = __dmul_rn(dt, rec[o]);
+    acc[o] = add ? __dadd_rn(acc[o], v) : v;
+  }
+}
+
+int launch_sub_snapshot(const double* cur, double* old, double* snap, const int8_t* level, int64_t P, int meqn,
+                        int m, int n2, int l, const double* alpha, int lmin, cudaStream_t st) {
+  if (P <= 0) return 0;
+  SubAlpha al;
+  for (int i = 0; i < 32; ++i) al.a[i] = alpha[i];
+  al.lmin = lmin;
+  k_sub_snapshot<<<148 * 8, 256, 0, st>>>(cur, old, snap, level, P, meqn, m * m, n2, l, al);
+  return 1;
+}
+
+int launch_sub_accumulate(const int32_t* list, int64_t n, const int32_t* rslot, const double* rec, double* acc,
+                          int fs, double dt, int add, cudaStream_t st) {
+  if (n <= 0) return 0;
+  const int64_t tot = n * fs, blocks = (tot + 255) / 256;
+  k_sub_accumulate<<<(unsigned)(blocks < 148 * 8 ? blocks : 148 * 8), 256, 0, st>>>(list, n, rslot, rec, acc, fs, dt, add);
   return 1;
 }
 

@@ -33,7 +33,7 @@ EXPORTS = ["fc_forest_create", "fc_forest_destroy", "fc_set_problem", "fc_set_au
            "fc_set_stream", "fc_set_timing", "fc_get_stats", "fc_reset_stats", "fc_local_range",
            "fc_halo_counts", "fc_halo_requests", "fc_halo_set_requests", "fc_halo_finalize",
            "fc_halo_buffers", "fc_halo_pack", "fc_halo_unpack", "fc_step_local", "fc_commit",
-           "fc_nccl_unique_id", "fc_last_error"]
+           "fc_nccl_unique_id", "fc_last_error", "fc_step_subcycled"]
 
 
 class FcError(RuntimeError):
@@ -85,6 +85,7 @@ def lib():
         L.fc_set_q.argtypes = [P, P, C.c_int]
         L.fc_ghost_fill.argtypes = [P]
         L.fc_step.argtypes = [P, C.c_double, C.POINTER(C.c_double)]
+        L.fc_step_subcycled.argtypes = [P, C.c_double, C.POINTER(C.c_double)]
         L.fc_get_q.argtypes = [P, P, C.c_int]
         L.fc_get_q_padded.argtypes = [P, P, C.c_int]
         L.fc_get_ghost_table.argtypes = [P, C.c_int, P, C.c_int64, C.POINTER(C.c_int64)]
@@ -187,6 +188,14 @@ class Forest:
         rc = lib().fc_step(self.h, dt, C.byref(cfl))
         if rc not in (FC_OK, FC_ECFL) or (raise_on_reject and rc != FC_OK):
             _check(rc, "fc_step")
+        return rc, cfl.value
+
+    def step_subcycled(self, dt_coarse: float, raise_on_reject: bool = True):
+        """One sub-cycled step (coarsest level by dt_coarse, finer levels by halves); (rc, cfl)."""
+        cfl = C.c_double(0.0)
+        rc = lib().fc_step_subcycled(self.h, dt_coarse, C.byref(cfl))
+        if rc not in (FC_OK, FC_ECFL) or (raise_on_reject and rc != FC_OK):
+            _check(rc, "fc_step_subcycled")
         return rc, cfl.value
 
     def get_q(self, out=None):
@@ -303,6 +312,30 @@ def run(w, steps: int | None = None, dt_list=None, device: int = 0, f: Forest | 
         if rc == FC_ECFL:
             dt = dt * w.cfl_target / cfl
             rc, cfl = f.step(dt)
+        cfls.append(cfl)
+        dts.append(dt)
+        if dt_list is None:
+            dt = w.next_dt(dt, cfl)
+    return f.get_q(), np.array(cfls), np.array(dts)
+
+
+def run_subcycled(w, steps: int | None = None, dt_list=None, device: int = 0, f: Forest | None = None,
+                  skip_quiescent: int = 1):
+    """Sub-cycled driver (same policy as oracle.run_subcycled): dt_coarse starts at
+    w.dt0 * 2^(lmax - lmin).  Returns (q, cfls, dt_coarse list)."""
+    f = f or forest_for(w, device, skip_quiescent=skip_quiescent)
+    f.set_q(np.ascontiguousarray(w.q0[f.first:f.first + f.count]))
+    steps = w.steps if steps is None else steps
+    lv = w.forest.levels
+    dt = w.dt0 * 2.0 ** (int(lv.max()) - int(lv.min()))
+    cfls, dts = [], []
+    for n in range(steps):
+        if dt_list is not None:
+            dt = dt_list[n]
+        rc, cfl = f.step_subcycled(dt, raise_on_reject=dt_list is not None)
+        if rc == FC_ECFL:
+            dt = dt * w.cfl_target / cfl
+            rc, cfl = f.step_subcycled(dt)
         cfls.append(cfl)
         dts.append(dt)
         if dt_list is None:
