@@ -13,7 +13,7 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["forest.c", "ghost.c", "claw.c", "subcycle.c"]
+SOURCES = ["forest.c", "ghost.c", "claw.c", "subcycle.c", "regrid.c"]
 LIB = os.path.join(HERE, "liboracle.so")
 
 OK, EINVAL, ETILING, ECONN, EBALANCE, ENOMEM, EUNSUP, EPHYS = 0, -1, -2, -3, -4, -5, -6, -7
@@ -72,6 +72,7 @@ def lib():
                                            C.c_double, C.c_double, P, P]
         L.orc_step_patch_faces.restype = C.c_double
         L.orc_flux.argtypes = [C.POINTER(Problem), C.c_int, P, C.c_double, P]
+        L.orc_regrid.argtypes = [P, P, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, P, P, P, P, P]
         L.orc_step_subcycled.argtypes = [P, C.POINTER(Problem), P, P, C.c_double, C.c_double, P,
                                          C.POINTER(C.c_double)]
         L.orc_limiter.argtypes = [C.c_int, C.c_double]
@@ -236,6 +237,24 @@ class OracleForest:
         if rc:
             raise RuntimeError(f"orc_step_subcycled -> {rc}")
         return out, cfl.value
+
+    def regrid(self, qpad: np.ndarray, refine_threshold: float, coarsen_threshold: float,
+               min_level: int, max_level: int):
+        """Regrid (regrid.c) from a ghost-filled padded state -> (levels, tree_ids, q interiors, src)."""
+        qpad = np.ascontiguousarray(qpad, np.float64)
+        P, meq = qpad.shape[0], qpad.shape[1]
+        m = self.m
+        nl = np.zeros(4 * P, np.int8)
+        nt = np.zeros(4 * P, np.int32)
+        qo = np.zeros((4 * P, meq, m, m))
+        src = np.zeros((4 * P, 6), np.int32)
+        npn = C.c_int64()
+        rc = lib().orc_regrid(self.h, _p(qpad), meq, refine_threshold, coarsen_threshold, min_level, max_level,
+                              C.byref(npn), _p(nl), _p(nt), _p(qo), _p(src))
+        if rc:
+            raise RuntimeError(f"orc_regrid -> {rc}")
+        k = npn.value
+        return nl[:k].copy(), nt[:k].copy(), qo[:k].copy(), src[:k].copy()
 
     def step_sample(self, pr: Problem, q: np.ndarray, dt: float, dx0: float, ids, aux=None):
         q = np.ascontiguousarray(q, np.float64)

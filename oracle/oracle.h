@@ -112,6 +112,16 @@ int orc_reflux_ex(const orc_forest* f, const orc_problem* pr, const double* face
  * qpad [P][meqn][n][n] in (interiors used), qout interiors out; *cfl = max over all updates. */
 int orc_step_subcycled(const orc_forest* f, const orc_problem* pr, const double* qpad, const double* aux,
                        double dt_coarse, double dx0, double* qout, double* cfl);
+/* Dynamic regrid of the forest (regrid.c): tag by
+ * max - min of component 0, refine above refine_threshold (level < max_level), 2:1 balance by
+ * refinement, coarsen complete families below coarsen_threshold (level > min_level) whose
+ * neighbours allow it; new leaves in Morton order with the data interpolated (limited, minmod,
+ * from the ghost-filled qpad) or averaged.  Outputs (capacity 4P): new_levels, new_trees,
+ * qout[new_P][meqn][m][m], and if src != NULL src[new_P][6] = {kind (1 copy, 2 child, 3 parent),
+ * old patch (first child for a parent), child index, 0, 0, 0}. */
+int orc_regrid(const orc_forest* f, const double* qpad, int meqn, double refine_threshold,
+               double coarsen_threshold, int min_level, int max_level, int64_t* new_P, int8_t* new_levels,
+               int32_t* new_trees, double* qout, int32_t* src);
 /* physical flux along axis ixy of state q (uedge: edge velocity, advective form) */
 void orc_flux(const orc_problem* pr, int ixy, const double* q, double uedge, double* f);
 
