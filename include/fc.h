@@ -163,6 +163,26 @@ int fc_step(fc_forest* f, double dt, double* max_cfl);
  * buffers, allocated at the first call. */
 int fc_step_subcycled(fc_forest* f, double dt_coarse, double* max_cfl);
 
+/* Dynamic regrid (PAPER.md:148-155 [§2] 2:1 balanced refinement, PAPER.md:207-211 [§3] "interpolation
+ * from coarse grids to newly created fine grids, and the averaging of fine grid data to a newly
+ * created underlying coarse grid").  Tag: max - min of component 0 over each patch.
+ * Refine when above refine_threshold (level < max_level), then refine neighbours as needed for the
+ * face and corner 2:1 balance; coarsen a complete family of 4 siblings (level > min_level) when all
+ * are below coarsen_threshold, none is refined and no outside neighbour would end more than one
+ * level finer.  Data: copied, limited (minmod) interpolation from the ghost-filled parent (the ghost
+ * fill's formula), or the 2x2 average.  *out is a NEW handle on the new forest (same connectivity,
+ * m, meqn, device, problem; q set; aux NOT set: the capacity form needs fc_set_aux on the new mesh,
+ * see fc_get_leaves); the old handle is unchanged and stays valid.  One rank only (FC_EUNSUP). */
+typedef struct {
+  double refine_threshold, coarsen_threshold;
+  int32_t min_level, max_level;
+} fc_regrid_params;
+int fc_regrid(fc_forest* f, const fc_regrid_params* rp, fc_forest** out);
+
+/* The forest's leaves in global Morton order: levels[P], tree_ids[P] (either may be NULL; both NULL
+ * = size query); *num_patches = P.  FC_EINVAL if cap < P. */
+int fc_get_leaves(fc_forest* f, int8_t* levels, int32_t* tree_ids, int64_t cap, int64_t* num_patches);
+
 /* Interior q_old -> q[P_local][meqn][m][m].  Synchronous. */
 int fc_get_q(fc_forest* f, double* q, int where);
 

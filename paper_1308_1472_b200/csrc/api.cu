@@ -39,6 +39,9 @@ int launch_sub_snapshot(const double* cur, double* old, double* snap, const int8
                         int m, int n2, int l, const double* alpha, int lmin, cudaStream_t st);
 int launch_sub_accumulate(const int32_t* list, int64_t n, const int32_t* rslot, const double* rec, double* acc,
                           int fs, double dt, int add, cudaStream_t st);
+int launch_regrid_tag(const double* q, int64_t P, int meqn, int m, double* tag, cudaStream_t st);
+int launch_regrid_transfer(const double* qo, double* qn, const int32_t* src, int64_t NP, int meqn, int m,
+                           cudaStream_t st);
 int launch_filter(int kind, const double* qold, double* qnew, int npatch, int m, uint8_t* uflag, double* uval,
                   const int32_t* nbr, const uint8_t* negmask, const int8_t* level, double dt, double dx0,
                   double p0, double p1, int32_t* active, int32_t* nactive, unsigned long long* cfl_bits,
@@ -873,6 +876,79 @@ int fc_step_subcycled(fc_forest* f, double dt_coarse, double* max_cfl) {
   const double cfl = *f->h_cfl;
   if (max_cfl) *max_cfl = cfl;
   return commit(f, cfl);
+}
+
+// ---- dynamic regrid -------------------------------
+int fc_regrid(fc_forest* f, const fc_regrid_params* rp, fc_forest** out) {
+  if (!f || !rp || !out) return fail(FC_EINVAL, "null argument");
+  *out = nullptr;
+  if (f->host_only || !f->has_q || !f->has_problem) return fail(FC_ESTATE, "set problem and q first");
+  if (f->pl.nranks != 1) return fail(FC_EUNSUP, "regrid runs on one rank (no repartition / migration yet)");
+  if (rp->min_level < 0 || rp->max_level < rp->min_level || rp->max_level > 28)
+    return fail(FC_EINVAL, "regrid level bounds out of range");
+  CK(cudaSetDevice(f->device));
+  int rc = ghost_fill_internal(f);                 // the interpolation slopes read the parents' rings
+  if (rc) return rc;
+  const int m = f->pl.m, meqn = f->pl.meqn;
+  double* d_tag = nullptr;
+  CK(cudaMalloc(&d_tag, std::max<int64_t>(1, f->Pl) * sizeof(double)));
+  f->st.kernel_launches += launch_regrid_tag(f->qold, f->Pl, meqn, m, d_tag, f->stream);
+  std::vector<double> tag(f->Pl);
+  CK(cudaMemcpyAsync(tag.data(), d_tag, f->Pl * sizeof(double), cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  cudaFree(d_tag);
+  std::vector<int8_t> lv;
+  std::vector<int32_t> tr, src;
+  std::string err;
+  if ((rc = plan_regrid(f->pl, tag.data(), rp->refine_threshold, rp->coarsen_threshold, rp->min_level,
+                        rp->max_level, lv, tr, src, err)))
+    return fail(rc, err);
+  fc_forest_desc d{};
+  d.num_patches = (int64_t)lv.size();
+  d.levels = lv.data();
+  d.tree_ids = tr.data();
+  d.num_trees = f->pl.T;
+  d.tree_to_tree = f->pl.t2t.data();
+  d.tree_to_face = f->pl.t2f.data();
+  d.face_bc = f->pl.fbc.data();
+  d.m = m;
+  d.mbc = 2;
+  d.meqn = meqn;
+  d.maux = f->pl.maux;
+  d.tree_dx0 = f->pl.dx0 * m;
+  d.device = f->device;
+  d.rank = 0;
+  d.nranks = 1;
+  d.nccl_id = nullptr;
+  fc_forest* g = nullptr;
+  if ((rc = fc_forest_create(&d, &g))) return rc;
+  if ((rc = fc_set_problem(g, &f->prob))) { fc_forest_destroy(g); return rc; }
+  int32_t* d_src = nullptr;
+  if (cudaMalloc(&d_src, src.size() * sizeof(int32_t)) != cudaSuccess ||
+      cudaMemcpy(d_src, src.data(), src.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d_src);
+    fc_forest_destroy(g);
+    return fail(FC_ECUDA, "regrid: source records");
+  }
+  g->st.kernel_launches += launch_regrid_transfer(f->qold, g->qold, d_src, g->Pl, meqn, m, f->stream);
+  cudaError_t e = cudaStreamSynchronize(f->stream);
+  cudaFree(d_src);
+  if (e != cudaSuccess) { fc_forest_destroy(g); return fail(FC_ECUDA, std::string("regrid transfer: ") + cudaGetErrorString(e)); }
+  g->has_q = true;
+  *out = g;
+  return FC_OK;
+}
+
+int fc_get_leaves(fc_forest* f, int8_t* levels, int32_t* tree_ids, int64_t cap, int64_t* num_patches) {
+  if (!f || !num_patches) return fail(FC_EINVAL, "null argument");
+  *num_patches = f->pl.P;
+  if (!levels && !tree_ids) return FC_OK;        // size query
+  if (cap < f->pl.P) return fail(FC_EINVAL, "capacity below the number of patches");
+  for (int64_t p = 0; p < f->pl.P; ++p) {
+    if (levels) levels[p] = (int8_t)f->pl.leaves[p].level;
+    if (tree_ids) tree_ids[p] = f->pl.leaves[p].tree;
+  }
+  return FC_OK;
 }
 
 // ---- staged step for a caller-provided halo transport (manual mode) ---------------------------

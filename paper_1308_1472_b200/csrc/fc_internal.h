@@ -149,5 +149,10 @@ struct RefluxPlan {
   std::vector<int32_t> cells;
 };
 int plan_reflux(const Plan& pl, int meqn, RefluxPlan& rf, std::string& err);
+// Dynamic regrid (one rank): new leaves in Morton order and per new leaf {kind (1 copy, 2 child,
+// 3 parent), old patch (first child for a parent), child index}; tag[p] = max - min of component 0
+int plan_regrid(const Plan& pl, const double* tag, double refine_threshold, double coarsen_threshold,
+                int min_level, int max_level, std::vector<int8_t>& new_levels, std::vector<int32_t>& new_trees,
+                std::vector<int32_t>& src, std::string& err);
 
 }  // namespace fc

@@ -189,4 +189,77 @@ int launch_gather(const double* q, double* dst, int64_t P, int meqn, int m, cuda
   return 1;
 }
 
+// ---- dynamic regrid --------------------------------------------------------
+// tag: max - min of component 0 over each patch interior (one warp per patch)
+__global__ void k_regrid_tag(const double* __restrict__ q, int64_t P, int meqn, int m, double* __restrict__ tag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int n = m + 4, mm = m * m;
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P; p += warps) {
+    const double* b = q + p * meqn * n * n;     // dense interior of component 0 (qcell)
+    double lo = b[0], hi = b[0];
+    for (int c = lane; c < mm; c += 32) { lo = fmin(lo, b[c]); hi = fmax(hi, b[c]); }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) tag[p] = hi - lo;
+  }
+}
+
+__device__ __forceinline__ double rg_minmod(double a, double b) {
+  if (a > 0.0 && b > 0.0) return a < b ? a : b;
+  if (a < 0.0 && b < 0.0) return a > b ? a : b;
+  return 0.0;
+}
+
+// new state from the old one (ghost rings filled): src[np][3] = {kind, old patch, child}
+//   1 copy; 2 child k of the old patch: limited (minmod) interpolation, the ghost fill's formula;
+//   3 parent of the 4 old patches from the given one: ((a + b) + (c + d)) / 4 per coarse cell
+__global__ void k_regrid_transfer(const double* __restrict__ qo, double* __restrict__ qn,
+                                  const int32_t* __restrict__ src, int64_t NP, int meqn, int m) {
+  const int n = m + 4, n2 = n * n, mm = m * m, h = m / 2;
+  const int64_t tot = NP * meqn * mm;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t np = t / ((int64_t)meqn * mm);
+    const int r = (int)(t - np * meqn * mm), e = r / mm, c = r - e * mm;
+    const int i = 1 + c % m, j = 1 + c / m;
+    const int32_t* s = src + np * 3;
+    double v;
+    if (s[0] == 1) {
+      v = qo[((int64_t)s[1] * meqn + e) * n2 + qcell(i, j, n)];
+    } else if (s[0] == 2) {
+      const double* Q = qo + ((int64_t)s[1] * meqn + e) * n2;
+      const int ox = s[2] & 1, oy = s[2] >> 1;
+      const int I = ox * h + (i + 1) / 2, J = oy * h + (j + 1) / 2;
+      const double sgx = (i & 1) ? -1.0 : 1.0, sgy = (j & 1) ? -1.0 : 1.0;
+      const double cc = Q[qcell(I, J, n)];
+      const double sx = rg_minmod(Q[qcell(I + 1, J, n)] - cc, cc - Q[qcell(I - 1, J, n)]);
+      const double sy = rg_minmod(Q[qcell(I, J + 1, n)] - cc, cc - Q[qcell(I, J - 1, n)]);
+      v = __dadd_rn(cc, 0.25 * __dadd_rn(__dmul_rn(sgx, sx), __dmul_rn(sgy, sy)));
+    } else {
+      const int k = (i > h) + 2 * (j > h);
+      const int a = 2 * (i - (i > h) * h), b = 2 * (j - (j > h) * h);
+      const double* Q = qo + ((int64_t)(s[1] + k) * meqn + e) * n2;
+      v = __dadd_rn(__dadd_rn(Q[qcell(a - 1, b - 1, n)], Q[qcell(a, b - 1, n)]),
+                    __dadd_rn(Q[qcell(a - 1, b, n)], Q[qcell(a, b, n)])) * 0.25;
+    }
+    qn[(np * meqn + e) * n2 + (j - 1) * m + (i - 1)] = v;
+  }
+}
+
+int launch_regrid_tag(const double* q, int64_t P, int meqn, int m, double* tag, cudaStream_t st) {
+  if (P <= 0) return 0;
+  const int64_t blocks = (P * 32 + 255) / 256;
+  k_regrid_tag<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(q, P, meqn, m, tag);
+  return 1;
+}
+
+int launch_regrid_transfer(const double* qo, double* qn, const int32_t* src, int64_t NP, int meqn, int m,
+                           cudaStream_t st) {
+  if (NP <= 0) return 0;
+  k_regrid_transfer<<<148 * 8, 256, 0, st>>>(qo, qn, src, NP, meqn, m);
+  return 1;
+}
+
 }  // namespace fc

@@ -656,3 +656,117 @@ int plan_reflux(const Plan& pl, int meqn, RefluxPlan& rf, std::string& err) {
 }
 
 }  // namespace fc
+
+namespace fc {
+
+// ---- dynamic regrid ----------------------------
+// Leaf containing a point (fine units, possibly outside its tree: crossed through the face maps,
+// both orders at a corner).  Up to 2 leaves (3-tree corners); -1 entries otherwise.
+static int leaves_at(const Plan& pl, int t, int64_t X, int64_t Y, int64_t out[2]) {
+  const int64_t m2 = 2 * (int64_t)pl.m, E = m2 << pl.lmax;
+  int cnt = 0;
+  for (int first = 0; first < 2; ++first) {
+    int tt = t;
+    int64_t x = X, y = Y;
+    bool phys = false;
+    for (int pass = 0; pass < 2 && !phys; ++pass) {
+      const int axis = pass == 0 ? first : 1 - first;
+      const int face = axis == 0 ? (x < 0 ? 0 : (x >= E ? 1 : -1)) : (y < 0 ? 2 : (y >= E ? 3 : -1));
+      if (face < 0) continue;
+      Affine A;
+      if (!cross_map(pl, tt, face, E, A)) { phys = true; break; }
+      int64_t nx, ny;
+      apply(A, x, y, nx, ny);
+      x = nx; y = ny; tt = A.tree;
+    }
+    if (phys || x < 0 || y < 0 || x >= E || y >= E) continue;
+    int64_t id = -1;
+    for (int l = pl.lmax; l >= 0 && id < 0; --l) {
+      const int64_t sz = 1ll << (pl.lmax - l);
+      id = find_leaf(pl, tt, l, (x / m2) / sz * sz, (y / m2) / sz * sz);
+    }
+    if (id >= 0 && !(cnt == 1 && out[0] == id)) out[cnt++] = id;
+  }
+  return cnt;
+}
+
+int plan_regrid(const Plan& pl, const double* tag, double refine_threshold, double coarsen_threshold,
+                int min_level, int max_level, std::vector<int8_t>& new_levels, std::vector<int32_t>& new_trees,
+                std::vector<int32_t>& src, std::string& err) {
+  if (pl.nranks != 1) { err = "regrid runs on one rank"; return FC_EUNSUP; }
+  if (max_level > 28 || min_level < 0) { err = "regrid levels out of range"; return FC_EINVAL; }
+  const int64_t P = pl.P, m2 = 2 * (int64_t)pl.m;
+  std::vector<uint8_t> refine((size_t)P, 0), coarsen((size_t)P, 0);
+  for (int64_t p = 0; p < P; ++p) refine[p] = tag[p] > refine_threshold && pl.leaves[p].level < max_level;
+  auto newlev = [&](int64_t q) { return pl.leaves[q].level + refine[q]; };
+  // refinement until 2:1 balanced: a leaf going to l+1 lifts face / corner neighbours at <= l-1
+  for (bool changed = true; changed;) {
+    changed = false;
+    for (int64_t p = 0; p < P; ++p) {
+      if (!refine[p]) continue;
+      const Leaf& L = pl.leaves[p];
+      const int64_t S = m2 << (pl.lmax - L.level), X0 = L.x * m2, Y0 = L.y * m2;
+      for (int dj = -1; dj <= 1; ++dj)
+        for (int di = -1; di <= 1; ++di) {
+          if (!di && !dj) continue;
+          const int64_t X = di < 0 ? X0 - 1 : (di > 0 ? X0 + S : X0 + S / 2);
+          const int64_t Y = dj < 0 ? Y0 - 1 : (dj > 0 ? Y0 + S : Y0 + S / 2);
+          int64_t q[2];
+          const int c = leaves_at(pl, L.tree, X, Y, q);
+          for (int k = 0; k < c; ++k)
+            if (newlev(q[k]) <= L.level - 1) { refine[q[k]] = 1; changed = true; }
+        }
+    }
+  }
+  // coarsening of complete families whose outside neighbours all stay at <= l
+  for (int64_t p = 0; p + 3 < P; ++p) {
+    const Leaf& L = pl.leaves[p];
+    if (L.level <= min_level || L.level == 0) continue;
+    const int64_t sz = 1ll << (pl.lmax - L.level);
+    if ((L.x / sz) % 2 || (L.y / sz) % 2) continue;
+    bool ok = true;
+    for (int k = 0; k < 4 && ok; ++k) {
+      const Leaf& c = pl.leaves[p + k];
+      ok = c.tree == L.tree && c.level == L.level && c.x == L.x + (k & 1) * sz && c.y == L.y + (k >> 1) * sz &&
+           !refine[p + k] && tag[p + k] < coarsen_threshold;
+    }
+    for (int k = 0; k < 4 && ok; ++k) {
+      const Leaf& c = pl.leaves[p + k];
+      const int64_t S = m2 * sz, X0 = c.x * m2, Y0 = c.y * m2;
+      for (int dj = -1; dj <= 1 && ok; ++dj)
+        for (int di = -1; di <= 1 && ok; ++di) {
+          if (!di && !dj) continue;
+          for (int h = 0; h < ((di && dj) ? 1 : 2) && ok; ++h) {
+            const int64_t along = h ? 3 * S / 4 : S / 4;
+            const int64_t X = di < 0 ? X0 - 1 : (di > 0 ? X0 + S : X0 + along);
+            const int64_t Y = dj < 0 ? Y0 - 1 : (dj > 0 ? Y0 + S : Y0 + along);
+            int64_t q[2];
+            const int cnt = leaves_at(pl, L.tree, X, Y, q);
+            for (int j = 0; j < cnt; ++j)
+              if (!(q[j] >= p && q[j] < p + 4) && newlev(q[j]) > L.level) ok = false;
+          }
+        }
+    }
+    if (ok) { coarsen[p] = 1; p += 3; }
+  }
+  new_levels.clear(); new_trees.clear(); src.clear();
+  for (int64_t p = 0; p < P; ++p) {
+    const Leaf& L = pl.leaves[p];
+    if (refine[p]) {
+      for (int k = 0; k < 4; ++k) {
+        new_levels.push_back((int8_t)(L.level + 1)); new_trees.push_back(L.tree);
+        src.insert(src.end(), {2, (int32_t)p, k});
+      }
+    } else if (coarsen[p]) {
+      new_levels.push_back((int8_t)(L.level - 1)); new_trees.push_back(L.tree);
+      src.insert(src.end(), {3, (int32_t)p, 0});
+      p += 3;
+    } else {
+      new_levels.push_back((int8_t)L.level); new_trees.push_back(L.tree);
+      src.insert(src.end(), {1, (int32_t)p, 0});
+    }
+  }
+  return FC_OK;
+}
+
+}  // namespace fc

@@ -33,7 +33,7 @@ EXPORTS = ["fc_forest_create", "fc_forest_destroy", "fc_set_problem", "fc_set_au
            "fc_set_stream", "fc_set_timing", "fc_get_stats", "fc_reset_stats", "fc_local_range",
            "fc_halo_counts", "fc_halo_requests", "fc_halo_set_requests", "fc_halo_finalize",
            "fc_halo_buffers", "fc_halo_pack", "fc_halo_unpack", "fc_step_local", "fc_commit",
-           "fc_nccl_unique_id", "fc_last_error", "fc_step_subcycled"]
+           "fc_nccl_unique_id", "fc_last_error", "fc_step_subcycled", "fc_regrid", "fc_get_leaves"]
 
 
 class FcError(RuntimeError):
@@ -54,6 +54,11 @@ class Problem(C.Structure):
     _fields_ = [("kind", C.c_int32), ("p0", C.c_double), ("p1", C.c_double), ("limiter", C.c_int32),
                 ("method2", C.c_int32), ("method3", C.c_int32), ("cfl_reject", C.c_double),
                 ("skip_quiescent", C.c_int32), ("reflux", C.c_int32)]
+
+
+class RegridParams(C.Structure):
+    _fields_ = [("refine_threshold", C.c_double), ("coarsen_threshold", C.c_double),
+                ("min_level", C.c_int32), ("max_level", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -86,6 +91,8 @@ def lib():
         L.fc_ghost_fill.argtypes = [P]
         L.fc_step.argtypes = [P, C.c_double, C.POINTER(C.c_double)]
         L.fc_step_subcycled.argtypes = [P, C.c_double, C.POINTER(C.c_double)]
+        L.fc_regrid.argtypes = [P, C.POINTER(RegridParams), C.POINTER(P)]
+        L.fc_get_leaves.argtypes = [P, P, P, C.c_int64, C.POINTER(C.c_int64)]
         L.fc_get_q.argtypes = [P, P, C.c_int]
         L.fc_get_q_padded.argtypes = [P, P, C.c_int]
         L.fc_get_ghost_table.argtypes = [P, C.c_int, P, C.c_int64, C.POINTER(C.c_int64)]
@@ -197,6 +204,31 @@ class Forest:
         if rc not in (FC_OK, FC_ECFL) or (raise_on_reject and rc != FC_OK):
             _check(rc, "fc_step_subcycled")
         return rc, cfl.value
+
+    def regrid(self, refine_threshold: float, coarsen_threshold: float, min_level: int, max_level: int):
+        """Dynamic regrid (fc_regrid) -> a new Forest on the new mesh (problem and q carried over;
+        aux must be set again for the capacity form).  This handle stays valid."""
+        rp = RegridParams(refine_threshold, coarsen_threshold, min_level, max_level)
+        h = C.c_void_p()
+        _check(lib().fc_regrid(self.h, C.byref(rp), C.byref(h)), "fc_regrid")
+        g = Forest.__new__(Forest)
+        g.h = h
+        g._keep, g._nid = [], None
+        g.m, g.meqn, g.maux, g.n = self.m, self.meqn, self.maux, self.n
+        first, count = C.c_int64(), C.c_int64()
+        _check(lib().fc_local_range(h, C.byref(first), C.byref(count)), "fc_local_range")
+        g.first, g.count, g.nranks = first.value, count.value, 1
+        return g
+
+    def leaves(self):
+        """(levels int8[P], tree_ids int32[P]) of the forest in global Morton order."""
+        n = C.c_int64()
+        _check(lib().fc_get_leaves(self.h, None, None, 0, C.byref(n)), "fc_get_leaves")
+        lv = np.zeros(n.value, np.int8)
+        tr = np.zeros(n.value, np.int32)
+        _check(lib().fc_get_leaves(self.h, lv.ctypes.data_as(C.c_void_p), tr.ctypes.data_as(C.c_void_p),
+                                   n.value, C.byref(n)), "fc_get_leaves")
+        return lv, tr
 
     def get_q(self, out=None):
         if out is None:
