@@ -14,7 +14,7 @@ import pytest
 
 import oracle
 from paper_1308_1472_b200 import fc
-from workloads.configs import c2, c3, c5
+from workloads.configs import c1, c2, c3, c5
 from workloads.cubed_sphere import c4_workload
 
 pytestmark = pytest.mark.gpu
@@ -97,3 +97,16 @@ def test_sharded_equals_single_rank_bitwise(w, R, skip):
     np.testing.assert_array_equal(cr, c1_)
     for k in range(w.meqn):
         assert np.abs(qr[:, k] - qo[:, k]).max() <= 1e-12 * np.abs(qo[:, k]).max()
+
+
+@pytest.mark.parametrize("R", [5, 8])
+@pytest.mark.parametrize("w", [c1(), c5(level=2, m=16, steps=20),
+                               c2(steps=20)], ids=lambda w: w.name)
+def test_sharded_eight_ranks_bitwise(w, R):
+    """8 shards (C1: 2 patches per rank, periodic wraps and corner-only peers) and an
+    uneven 5-way cut, bitwise equal to one rank."""
+    _, _, do = oracle.run(w)
+    q1, c1_, _ = fc.run(w, dt_list=do)
+    qr, cr = run_sharded(w, R, do, 1)
+    np.testing.assert_array_equal(qr, q1)
+    np.testing.assert_array_equal(cr, c1_)
