@@ -6,7 +6,9 @@ update + CFL reduction) on 1..8 B200s, plus roofline, end-to-end and oracle base
     python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port P bench.py --gpus N --steps K --warmup W
 
-One "step" = one fc_step: ghost fill (incl. the NCCL halo exchange for N > 1), the update of every
+One "step" = one fc_step: ghost fill (for N > 1 the remote ring cells are read inside the update
+kernel from the owner GPU's memory over NVLink -- the peer-memory halo, `--halo nccl` for the NCCL
+send/recv exchange instead), the update of every
 local patch, the global CFL max-allreduce and the CFL read-back that drives the next dt (the
 Clawpack variable-dt rule of the workload).  The workload is BASELINE.json configs[4] (C5: Euler
 shock-bubble on a 4-tree brick, level 8, m = 16, 262,144 patches, 67.1M cells) -- the config
@@ -222,6 +224,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-patches", type=int, default=256)
+    ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: peer-memory halo in the fused gather (default) or NCCL send/recv")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -259,8 +263,35 @@ def main():
         obj = [fc.fc_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0,
-                  local, rank, world, nccl_id)
+    # N > 1: peer-memory halo (the fused ring gather reads neighbours' cells from the owner GPU over
+    # NVLink, CUDA IPC mapped at creation) unless --halo nccl; falls back to the NCCL halo exchange
+    # if the IPC mapping is refused
+    halo = "none"
+    if world > 1:
+        halo = args.halo
+        f, why = None, ""
+        try:
+            f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0,
+                          local, rank, world, nccl_id, halo_p2p=1 if halo == "p2p" else 0)
+        except fc.FcError as e:
+            if halo != "p2p":
+                raise
+            why = str(e)
+        ok = torch.tensor([1 if f is not None else 0], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)            # the decision is collective
+        if int(ok.item()) == 0:
+            print(f"[bench] rank {rank}: peer-memory halo unavailable ({why or 'on another rank'}); NCCL halo",
+                  file=sys.stderr)
+            if f is not None:
+                f.close()
+            halo = "nccl (p2p refused)"
+            obj = [fc.fc_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0,
+                          local, rank, world, obj[0], halo_p2p=0)
+    else:
+        f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0,
+                      local, rank, world, nccl_id)
     assert (f.first, f.count) == (p0, p1 - p0)
     f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject)
     q0 = torch.from_numpy(w.q0_range(p0, p1)).pin_memory()
@@ -390,7 +421,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": WORKLOADS[args.workload], "patches": P, "cells": cells_total,
-                           "parallelism": f"morton-shard x{world}" + (" (NCCL halo)" if world > 1 else ""),
+                           "parallelism": f"morton-shard x{world}" + (f" (halo: {halo})" if world > 1 else ""),
                            "l2": "state 2 x %.2f GB >> 126 MB L2 (no flush needed)" % (P * w.meqn * (w.m + 4) ** 2 * 8 / 1e9),
                            "dt_policy": "Clawpack variable dt (0.9 / CFL)", "final_cfl": cfls[-1]},
                 "roofline": roofline, "roofline_alu_full_update": roofline_alu,

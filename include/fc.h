@@ -83,6 +83,12 @@ typedef struct {
   int32_t rank, nranks;         /* this process among nranks (1 = single GPU) */
   const void* nccl_id;          /* 128-byte ncclUniqueId when nranks > 1 (fc_nccl_unique_id on rank 0);
                                    NULL with nranks > 1 selects the manual halo transport (below) */
+  int32_t halo_p2p;             /* 1 (nranks > 1, uniform forests, fused ring gather): ring cells owned
+                                   by other ranks are read inside the update kernel straight from the
+                                   owners' state buffers in peer memory (CUDA IPC over NVLink; in manual
+                                   mode wired with fc_p2p_set_peer) -- no pack / ncclSend/Recv / unpack
+                                   pass (PAPER.md:264-272's ghost exchange fused into the gather); the
+                                   CFL allreduce orders the steps across ranks.  0: halo exchange */
 } fc_forest_desc;
 
 typedef struct {
@@ -241,6 +247,14 @@ int fc_halo_pack(fc_forest* f, int round);      /* synchronous */
 int fc_halo_unpack(fc_forest* f, int round);    /* synchronous */
 int fc_step_local(fc_forest* f, double dt, int phase, double* local_cfl);
 int fc_commit(fc_forest* f, double global_cfl); /* FC_ECFL / FC_ENONFINITE as fc_step */
+
+/* Peer-memory halo (halo_p2p = 1).  fc_p2p_buffers: this handle's two state buffers (device
+ * pointers, fixed for its lifetime; they alternate as q_old / q_new) and *parity = which one is
+ * q_old now (0 or 1; all ranks commit in lockstep, so the parity is global).  fc_p2p_set_peer
+ * (manual transport only; NCCL handles exchange CUDA IPC handles at creation): register rank
+ * `peer`'s two buffers as mapped in this process. */
+int fc_p2p_buffers(fc_forest* f, void** buf0, void** buf1, int32_t* parity);
+int fc_p2p_set_peer(fc_forest* f, int32_t peer, void* buf0, void* buf1);
 
 /* Write a fresh 128-byte ncclUniqueId into out (call on rank 0, broadcast to the others). */
 int fc_nccl_unique_id(void* out);

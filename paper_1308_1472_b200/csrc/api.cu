@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -31,7 +32,8 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
                 int64_t npatch, int m, double dt, double dx0, double p0, double p1, int limiter,
                 int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
                 const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits,
-                const int32_t* rslot, double* freg, cudaStream_t st);
+                const int32_t* rslot, double* freg, const uint8_t* rpeer, const double* const* peerq,
+                cudaStream_t st);
 int launch_reflux(const int32_t* cells, int64_t ncells, const double* freg, const double* ffine, double* qnew,
                   const double* aux, const int8_t* level, double wc, double dtr, double dx0, int meqn, int n2,
                   cudaStream_t st);
@@ -117,6 +119,13 @@ struct fc_forest {
   std::vector<DevList> interp, bcx_l, bcy_l;
   fc_problem prob{};
   bool has_problem = false, has_q = false, has_aux = false;
+  // peer-memory halo (halo_p2p, fused path): ring cells of other ranks read from their buffers
+  bool p2p = false;
+  uint8_t* d_rpeer = nullptr;          // [Pl][G] 0 = local, k = rank k-1
+  double* buf[2] = {nullptr, nullptr}; // this rank's two state buffers (q_old = buf[parity])
+  int parity = 0;
+  std::vector<std::array<double*, 2>> peer_buf;   // per rank: its two buffers mapped here
+  std::vector<bool> peer_ipc;          // opened through CUDA IPC (closed on destroy)
   // halo
   ncclComm_t comm = nullptr;
   bool manual = false;                 // nranks > 1 without an NCCL id: the caller moves halo data
@@ -247,6 +256,36 @@ static int setup_halo(fc_forest* f, const void* nccl_id) {
   return build_halo_lists(f);
 }
 
+// peer-memory halo over NCCL ranks: all-gather the CUDA IPC handles of every rank's two state
+// buffers, open the other ranks' (peer access over NVLink), then an allreduce as a barrier
+static int setup_p2p_ipc(fc_forest* f) {
+  const int R = f->pl.nranks, me = f->pl.rank;
+  cudaIpcMemHandle_t mine[2];
+  CK(cudaIpcGetMemHandle(&mine[0], f->buf[0]));
+  CK(cudaIpcGetMemHandle(&mine[1], f->buf[1]));
+  const size_t hb = sizeof(mine);
+  char *d_mine = nullptr, *d_all = nullptr;
+  CK(cudaMalloc(&d_mine, hb));
+  CK(cudaMalloc(&d_all, hb * R));
+  CK(cudaMemcpy(d_mine, mine, hb, cudaMemcpyHostToDevice));
+  NK(ncclAllGather(d_mine, d_all, hb, ncclUint8, f->comm, f->stream));
+  std::vector<cudaIpcMemHandle_t> all(2 * R);
+  CK(cudaMemcpyAsync(all.data(), d_all, hb * R, cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  cudaFree(d_mine);
+  cudaFree(d_all);
+  for (int r = 0; r < R; ++r) {
+    if (r == me) continue;
+    for (int b = 0; b < 2; ++b) {
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, all[2 * r + b], cudaIpcMemLazyEnablePeerAccess));
+      f->peer_buf[r][b] = (double*)p;
+    }
+    f->peer_ipc[r] = true;
+  }
+  return FC_OK;
+}
+
 // ---- halo transfer pieces (round: 0 = interior cells, 1 = ring cells read by interpolation) ----
 static int halo_pack(fc_forest* f, int round) {
   f->st.kernel_launches += launch_pack(f->qold, f->d_pack[round], f->npack[round], f->pl.meqn,
@@ -331,6 +370,11 @@ static int update_local(fc_forest* f, double dt) {
   const fc_problem& p = f->prob;
   const bool fused = use_fused(f);
   const bool reflux = p.reflux && f->nrcells > 0;
+  std::array<const double*, 16> peerq{};   // peers' current q_old (peer-memory halo)
+  if (fused && f->p2p) {
+    if (f->pl.nranks > 16) return fail(FC_EUNSUP, "peer-memory halo supports at most 16 ranks");
+    for (int r = 0; r < f->pl.nranks; ++r) peerq[r] = f->peer_buf[r][f->parity];
+  }
   bool filtered = false;
   // (tiny forests skip the filter: its two extra launches cost more than the tiles they save; the
   // step kernel's own quiescent-window check still applies)
@@ -349,7 +393,8 @@ static int update_local(fc_forest* f, double dt) {
                        p.p0, p.p1, p.limiter, p.method2, p.method3, filtered ? 0 : p.skip_quiescent,
                        fused ? f->d_ring : nullptr, f->d_bcflag, filtered ? f->d_active : nullptr,
                        filtered ? f->d_nactive : nullptr, f->d_cfl, reflux ? f->d_rslot : nullptr,
-                       reflux ? f->d_freg : nullptr, f->stream);
+                       reflux ? f->d_freg : nullptr, (fused && f->p2p) ? f->d_rpeer : nullptr, peerq.data(),
+                       f->stream);
   if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
   f->st.kernel_launches += lr;
   f->st.step_kernel_launches += lr;
@@ -375,6 +420,7 @@ static int commit(fc_forest* f, double cfl) {
   if (!std::isfinite(cfl)) return fail(FC_ENONFINITE, "CFL is not finite");
   if (cfl > f->prob.cfl_reject) return fail(FC_ECFL, "CFL above cfl_reject; step not committed");
   std::swap(f->qold, f->qnew);
+  f->parity ^= 1;
   f->st.steps += 1;
   return FC_OK;
 }
@@ -389,6 +435,10 @@ static void destroy(fc_forest* f) {
     cudaFree(f->d_nbr); cudaFree(f->d_active); cudaFree(f->d_nactive); cudaFree(f->d_negmask);
     cudaFree(f->d_uflag); cudaFree(f->d_uval);
     cudaFree(f->d_rslot); cudaFree(f->d_rcells); cudaFree(f->d_freg);
+    cudaFree(f->d_rpeer);
+    for (size_t r = 0; r < f->peer_ipc.size(); ++r)
+      if (f->peer_ipc[r])
+        for (double* p : f->peer_buf[r]) if (p) cudaIpcCloseMemHandle(p);
     cudaFree(f->d_sub_old); cudaFree(f->d_sub_snap); cudaFree(f->d_facc); cudaFree(f->d_lvl_cnt);
     for (auto* d : f->d_lvl) cudaFree(d);
     if (f->h_cfl) cudaFreeHost(f->h_cfl);
@@ -459,6 +509,8 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
   f->state_doubles = (size_t)(f->Pl + f->Pv) * pl.meqn * n2;
   if ((e = cudaMalloc(&f->qold, f->state_doubles * sizeof(double))) != cudaSuccess) return cuda_fail(e, "cudaMalloc q_old");
   if ((e = cudaMalloc(&f->qnew, f->state_doubles * sizeof(double))) != cudaSuccess) return cuda_fail(e, "cudaMalloc q_new");
+  f->buf[0] = f->qold;
+  f->buf[1] = f->qnew;
   cudaMemset(f->qold, 0, f->state_doubles * sizeof(double));
   cudaMemset(f->qnew, 0, f->state_doubles * sizeof(double));
   if (pl.maux > 0) {
@@ -500,8 +552,15 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
     const bool allow = !env || atoi(env) != 0;
     if (allow && pl.uniform_same && T == pl.m) {
       RingSources rs;
-      rc = plan_ring_sources(f->pl, pl.meqn, rs, err);
+      f->p2p = d->halo_p2p != 0 && pl.nranks > 1;
+      rc = plan_ring_sources(f->pl, pl.meqn, rs, err, f->p2p);
       if (rc) { destroy(f); return fail(rc, err); }
+      if (f->p2p) {
+        if ((e = cudaMalloc(&f->d_rpeer, rs.peer.size())) != cudaSuccess) return cuda_fail(e, "cudaMalloc ring peers");
+        cudaMemcpy(f->d_rpeer, rs.peer.data(), rs.peer.size(), cudaMemcpyHostToDevice);
+        f->peer_buf.assign(pl.nranks, {nullptr, nullptr});
+        f->peer_ipc.assign(pl.nranks, false);
+      }
       if ((e = cudaMalloc(&f->d_ring, rs.src.size() * sizeof(int32_t))) != cudaSuccess) return cuda_fail(e, "cudaMalloc ring");
       if ((e = cudaMalloc(&f->d_bcflag, std::max<size_t>(1, rs.bcflag.size()))) != cudaSuccess) return cuda_fail(e, "cudaMalloc bcflag");
       cudaMemcpy(f->d_ring, rs.src.data(), rs.src.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
@@ -540,6 +599,7 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
       rc = build_halo_lists(f);   // receive side now; send side after fc_halo_set_requests + finalize
     } else {
       rc = setup_halo(f, d->nccl_id);
+      if (!rc && f->p2p) rc = setup_p2p_ipc(f);
     }
     if (rc) { std::string m = g_err; destroy(f); return fail(rc, m); }
   }
@@ -692,6 +752,8 @@ int fc_set_q(fc_forest* f, const double* q, int where) {
   }
   f->st.kernel_launches += launch_scatter(src, f->qold, f->Pl, meqn, m, f->stream);
   CK(cudaGetLastError());
+  if (f->p2p && f->comm)   // peers read this state directly: every rank's upload before any step
+    NK(ncclAllReduce(f->d_cfl, f->d_cfl, 1, ncclDouble, ncclMax, f->comm, f->stream));
   CK(cudaStreamSynchronize(f->stream));
   f->has_q = true;
   return FC_OK;
@@ -744,7 +806,8 @@ int fc_step(fc_forest* f, double dt, double* max_cfl) {
   if (f->timing) CK(cudaEventRecord(f->ev[0], f->stream));
   // fused ring gather + quiescent filter when skipping is on (rings never written); otherwise the
   // ghost kernels fill the rings and every tile is bulk-copied whole (faster for the full update)
-  rc = use_fused(f) ? halo_round(f, 0) : ghost_fill_internal(f);
+  // (peer-memory halo: the fused gather reads other ranks' cells itself; no exchange pass)
+  rc = use_fused(f) ? (f->p2p ? FC_OK : halo_round(f, 0)) : ghost_fill_internal(f);
   if (rc) return rc;
   if (f->timing) CK(cudaEventRecord(f->ev[1], f->stream));
   if ((rc = update_local(f, dt))) return rc;
@@ -822,7 +885,7 @@ static int sub_advance(fc_forest* f, int l, int64_t tick, int sub) {
     int lr = launch_step(p.kind, f->d_sub_snap, f->qnew, f->aux, f->d_level, f->n_lvl[li], m, dt, f->pl.dx0, p.p0,
                          p.p1, p.limiter, p.method2, p.method3, p.skip_quiescent, nullptr, f->d_bcflag, f->d_lvl[li],
                          f->d_lvl_cnt + li, f->d_cfl, reflux ? f->d_rslot : nullptr, reflux ? f->d_freg : nullptr,
-                         f->stream);
+                         nullptr, nullptr, f->stream);
     if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
     f->st.kernel_launches += lr;
     f->st.step_kernel_launches += lr;
@@ -1024,6 +1087,24 @@ int fc_step_local(fc_forest* f, double dt, int phase, double* local_cfl) {
     return fail(FC_EINVAL, "phase must be 1 or 2");
   }
   CK(cudaStreamSynchronize(f->stream));
+  return FC_OK;
+}
+
+int fc_p2p_buffers(fc_forest* f, void** buf0, void** buf1, int32_t* parity) {
+  if (!f || !buf0 || !buf1 || !parity) return fail(FC_EINVAL, "null argument");
+  if (f->host_only) return fail(FC_ESTATE, "host-only handle");
+  *buf0 = f->buf[0];
+  *buf1 = f->buf[1];
+  *parity = f->parity;
+  return FC_OK;
+}
+
+int fc_p2p_set_peer(fc_forest* f, int32_t peer, void* buf0, void* buf1) {
+  if (!f) return fail(FC_EINVAL, "null handle");
+  if (!f->p2p) return fail(FC_ESTATE, "not a peer-memory-halo handle (halo_p2p = 0 or not the fused path)");
+  if (!f->manual) return fail(FC_ESTATE, "NCCL handles map their peers at creation");
+  if (peer < 0 || peer >= f->pl.nranks || peer == f->pl.rank || !buf0 || !buf1) return fail(FC_EINVAL, "bad peer");
+  f->peer_buf[peer] = {(double*)buf0, (double*)buf1};
   return FC_OK;
 }
 

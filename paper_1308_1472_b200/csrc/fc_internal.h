@@ -118,6 +118,9 @@ struct Plan {
 // for a physical-boundary cell filled from the patch's own window.  bcflag[p]: bit 0 BCX, bit 1 BCY.
 struct RingSources {
   std::vector<int32_t> src;
+  // peer-memory halo (p2p): 0 = src is an offset in this rank's state, k > 0 = in rank k-1's
+  // local state (its own patch numbering); empty without p2p (remote cells use halo slots)
+  std::vector<uint8_t> peer;
   std::vector<uint8_t> bcflag;
   // activity test: the <= 8 distinct patches the ring reads (local ids; -2 = a remote patch,
   // -1 = unused) and a mask of components a wall negates (they must vanish for a quiescent patch)
@@ -129,7 +132,7 @@ struct RingSources {
 int plan_build(const fc_forest_desc* d, Plan& pl, std::string& err);
 // build typed lists for `meqn` (component stride n^2); halo slots from pl.halo
 int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err);
-int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& err);
+int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& err, bool p2p = false);
 // activity tables for the quiescent filter on any forest: nbr [Pl][8] / negmask [Pl] as in
 // RingSources; a patch with an AVG4 / INTERP / CORNER3 ghost record is always active (nbr[0] = -2)
 int plan_activity(const Plan& pl, int meqn, std::vector<int32_t>& nbr, std::vector<uint8_t>& negmask,

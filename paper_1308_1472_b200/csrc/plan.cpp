@@ -497,7 +497,7 @@ int plan_activity(const Plan& pl, int meqn, std::vector<int32_t>& nbr, std::vect
   return FC_OK;
 }
 
-int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& err) {
+int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& err, bool p2p) {
   const int m = pl.m, n = pl.n;
   const int64_t n2 = (int64_t)n * n, S = (int64_t)meqn * n2;
   const int64_t Pl = pl.p1 - pl.p0, G = n2 - (int64_t)m * m;
@@ -505,6 +505,10 @@ int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& er
   rs.bcflag.assign((size_t)Pl, 0);
   rs.nbr.assign((size_t)Pl * 8, -1);
   rs.negmask.assign((size_t)Pl, 0);
+  if (p2p) {
+    if (pl.nranks > 255) { err = "peer-memory halo supports at most 255 ranks"; return FC_EUNSUP; }
+    rs.peer.assign((size_t)Pl * G, 0);
+  }
   for (int64_t lp = 0; lp < Pl; ++lp) {
     int nn = 0;
     auto add_nbr = [&](int32_t id) {
@@ -523,6 +527,10 @@ int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& er
         if (!add_nbr((q >= pl.p0 && q < pl.p1) ? (int32_t)(q - pl.p0) : -2)) { err = "more than 8 ring neighbours"; return FC_EUNSUP; }
         if (q >= pl.p0 && q < pl.p1) {
           v = (int32_t)((q - pl.p0) * S + qcell(o[2], o[3], n));
+        } else if (p2p) {   // the owner's own state: its local patch index, same block layout
+          const int64_t ow = owner_of(pl, q), first = (ow * pl.P) / pl.nranks;
+          v = (int32_t)((q - first) * S + qcell(o[2], o[3], n));
+          rs.peer[lp * G + r] = (uint8_t)(ow + 1);
         } else {
           auto it = pl.halo.slot.find((q * n2 + cell) * 2);
           if (it == pl.halo.slot.end()) { err = "missing halo slot"; return FC_EINVAL; }

@@ -62,6 +62,8 @@ struct StepArgs {
   double* fbuf;                       // method3 = 1 only: per-CTA F~ of each correction edge [MEQN][E2]
   const int32_t* __restrict__ rslot;  // reflux: per patch flux-register slot (-1: none) or null
   double* freg;                       // reflux: [slot][4 faces][m edges][MEQN] applied fluxes, outward
+  const uint8_t* __restrict__ rpeer;  // peer-memory halo: owner of each ring source (0 = this rank)
+  const double* peerq[16];            // peer-memory halo: rank r's current q_old (peer pointer)
 };
 
 // ---- TMA bulk copies + mbarrier (sm_90+ / sm_100a) -------------------------------------------
@@ -287,10 +289,16 @@ __device__ __forceinline__ void gather_ring(const StepArgs& A, int tile, double*
   constexpr int MEQN = S::MEQN, WW = Sh::WW, G = WW - T * T;
   const int n2 = WW;
   const int32_t* rs = A.ring + (int64_t)tile * G;
+  const uint8_t* rp = A.rpeer ? A.rpeer + (int64_t)tile * G : nullptr;
   for (int e = opaque(threadIdx.x); e < G * MEQN; e += NT) {
     const int k = e / G, r = e - k * G;
     const int32_t v = __ldg(rs + r);
-    if (v >= 0) cp_async8(buf + k * WW + ring_window_index<T>(r), A.qold + v + (int64_t)k * n2);
+    if (v >= 0) {
+      // peer-memory halo: a cell of another rank is copied straight from its buffer over NVLink
+      const int ow = rp ? __ldg(rp + r) : 0;
+      const double* base = ow ? A.peerq[ow - 1] : A.qold;
+      cp_async8(buf + k * WW + ring_window_index<T>(r), base + v + (int64_t)k * n2);
+    }
   }
 }
 
@@ -892,11 +900,14 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
                 int64_t npatch, int m, double dt, double dx0, double p0, double p1, int limiter,
                 int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
                 const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits,
-                const int32_t* rslot, double* freg, cudaStream_t st) {
+                const int32_t* rslot, double* freg, const uint8_t* rpeer, const double* const* peerq,
+                cudaStream_t st) {
   if (npatch <= 0) return 0;
   StepArgs a;
   a.rslot = rslot;
   a.freg = freg;
+  a.rpeer = rpeer;
+  for (int r = 0; r < 16; ++r) a.peerq[r] = peerq ? peerq[r] : nullptr;
   a.qold = qold; a.qnew = qnew; a.aux = aux; a.level = level;
   a.dt = dt; a.dx0 = dx0; a.sp.p0 = p0; a.sp.p1 = p1;
   a.limiter = limiter; a.method2 = method2; a.method3 = method3;

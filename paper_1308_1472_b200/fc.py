@@ -33,7 +33,8 @@ EXPORTS = ["fc_forest_create", "fc_forest_destroy", "fc_set_problem", "fc_set_au
            "fc_set_stream", "fc_set_timing", "fc_get_stats", "fc_reset_stats", "fc_local_range",
            "fc_halo_counts", "fc_halo_requests", "fc_halo_set_requests", "fc_halo_finalize",
            "fc_halo_buffers", "fc_halo_pack", "fc_halo_unpack", "fc_step_local", "fc_commit",
-           "fc_nccl_unique_id", "fc_last_error", "fc_step_subcycled", "fc_regrid", "fc_get_leaves"]
+           "fc_nccl_unique_id", "fc_last_error", "fc_step_subcycled", "fc_regrid", "fc_get_leaves",
+           "fc_p2p_buffers", "fc_p2p_set_peer"]
 
 
 class FcError(RuntimeError):
@@ -47,7 +48,8 @@ class ForestDesc(C.Structure):
                 ("num_trees", C.c_int32), ("tree_to_tree", C.c_void_p), ("tree_to_face", C.c_void_p),
                 ("face_bc", C.c_void_p), ("m", C.c_int32), ("mbc", C.c_int32), ("meqn", C.c_int32),
                 ("maux", C.c_int32), ("tree_dx0", C.c_double), ("device", C.c_int32),
-                ("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_id", C.c_void_p)]
+                ("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_id", C.c_void_p),
+                ("halo_p2p", C.c_int32)]
 
 
 class Problem(C.Structure):
@@ -93,6 +95,8 @@ def lib():
         L.fc_step_subcycled.argtypes = [P, C.c_double, C.POINTER(C.c_double)]
         L.fc_regrid.argtypes = [P, C.POINTER(RegridParams), C.POINTER(P)]
         L.fc_get_leaves.argtypes = [P, P, P, C.c_int64, C.POINTER(C.c_int64)]
+        L.fc_p2p_buffers.argtypes = [P, C.POINTER(P), C.POINTER(P), C.POINTER(C.c_int32)]
+        L.fc_p2p_set_peer.argtypes = [P, C.c_int32, P, P]
         L.fc_get_q.argtypes = [P, P, C.c_int]
         L.fc_get_q_padded.argtypes = [P, P, C.c_int]
         L.fc_get_ghost_table.argtypes = [P, C.c_int, P, C.c_int64, C.POINTER(C.c_int64)]
@@ -142,7 +146,7 @@ class Forest:
 
     def __init__(self, levels, tree_ids, conn, m: int, meqn: int, maux: int = 0,
                  tree_dx0: float = 1.0, device: int = 0, rank: int = 0, nranks: int = 1,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, halo_p2p: int = 0):
         self._keep = [np.ascontiguousarray(levels, np.int8), np.ascontiguousarray(tree_ids, np.int32),
                       np.ascontiguousarray(conn.tree_to_tree, np.int32),
                       np.ascontiguousarray(conn.tree_to_face, np.int8),
@@ -151,7 +155,7 @@ class Forest:
         self._nid = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         d = ForestDesc(len(lv), lv.ctypes.data, tr.ctypes.data, len(t2t) // 4, t2t.ctypes.data,
                        t2f.ctypes.data, fbc.ctypes.data, m, 2, meqn, maux, tree_dx0, device, rank,
-                       nranks, C.cast(self._nid, C.c_void_p) if self._nid else None)
+                       nranks, C.cast(self._nid, C.c_void_p) if self._nid else None, halo_p2p)
         h = C.c_void_p()
         _check(lib().fc_forest_create(C.byref(d), C.byref(h)), "fc_forest_create")
         self.h = h
@@ -219,6 +223,15 @@ class Forest:
         _check(lib().fc_local_range(h, C.byref(first), C.byref(count)), "fc_local_range")
         g.first, g.count, g.nranks = first.value, count.value, 1
         return g
+
+    def p2p_buffers(self):
+        """(buf0, buf1, parity): this rank's two state buffers (device addresses) and which is q_old."""
+        b0, b1, par = C.c_void_p(), C.c_void_p(), C.c_int32()
+        _check(lib().fc_p2p_buffers(self.h, C.byref(b0), C.byref(b1), C.byref(par)), "fc_p2p_buffers")
+        return b0.value, b1.value, par.value
+
+    def p2p_set_peer(self, peer: int, buf0: int, buf1: int):
+        _check(lib().fc_p2p_set_peer(self.h, peer, C.c_void_p(buf0), C.c_void_p(buf1)), "fc_p2p_set_peer")
 
     def leaves(self):
         """(levels int8[P], tree_ids int32[P]) of the forest in global Morton order."""

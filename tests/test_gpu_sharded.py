@@ -110,3 +110,45 @@ def test_sharded_eight_ranks_bitwise(w, R):
     qr, cr = run_sharded(w, R, do, 1)
     np.testing.assert_array_equal(qr, q1)
     np.testing.assert_array_equal(cr, c1_)
+
+
+# ---- peer-memory halo (halo_p2p): the fused gather reads other ranks' buffers directly -----------
+def run_sharded_p2p(w, R, dts):
+    """R rank handles with halo_p2p = 1 wired to each other's state buffers (same device: the peer
+    pointers are plain device pointers here, CUDA IPC mappings with NCCL); no halo pass at all."""
+    hs = [fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0, 0, r, R, None,
+                    halo_p2p=1) for r in range(R)]
+    for f in hs:
+        f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject, 1)
+    bufs = [f.p2p_buffers() for f in hs]
+    for r, f in enumerate(hs):
+        for s in range(R):
+            if s != r:
+                f.p2p_set_peer(s, bufs[s][0], bufs[s][1])
+        f.set_q(np.ascontiguousarray(w.q0[f.first:f.first + f.count]))
+    cfls = []
+    for dt in dts:
+        for f in hs:
+            f.step_local(dt, 1)
+        c = max(f.step_local(dt, 2) for f in hs)
+        for f in hs:
+            assert f.commit(c) == fc.FC_OK
+        cfls.append(c)
+    assert len({f.p2p_buffers()[2] for f in hs}) == 1           # parities in lockstep
+    q = np.concatenate([f.get_q() for f in hs if f.count], axis=0)
+    for f in hs:
+        f.close()
+    return q, np.array(cfls)
+
+
+@pytest.mark.parametrize("R", [2, 3, 4, 8])
+@pytest.mark.parametrize("w", [c1(), c5(level=2, m=16, steps=30), c5(level=3, m=16, steps=10),
+                               c5(level=4, m=16, steps=8)], ids=lambda w: w.name)
+def test_peer_memory_halo_equals_single_rank_bitwise(w, R):
+    """(C5 level 4 at 2 ranks: 512 patches per rank, so the quiescent filter runs with remote
+    neighbours always active)"""
+    _, _, do = oracle.run(w)
+    q1, c1_, _ = fc.run(w, dt_list=do)
+    qr, cr = run_sharded_p2p(w, R, do)
+    np.testing.assert_array_equal(qr, q1)
+    np.testing.assert_array_equal(cr, c1_)
