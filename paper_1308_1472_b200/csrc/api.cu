@@ -47,7 +47,7 @@ int launch_regrid_transfer(const double* qo, double* qn, const int32_t* src, int
 int launch_filter(int kind, const double* qold, double* qnew, int npatch, int m, uint8_t* uflag, double* uval,
                   const int32_t* nbr, const uint8_t* negmask, const int8_t* level, double dt, double dx0,
                   double p0, double p1, int32_t* active, int32_t* nactive, unsigned long long* cfl_bits,
-                  cudaStream_t st);
+                  cudaStream_t st, cudaEvent_t ev_before_copy, cudaEvent_t ev_after_copy);
 }  // namespace fc
 
 using namespace fc;
@@ -139,6 +139,7 @@ struct fc_forest {
   fc_stats st{};
   bool timing = false;
   cudaEvent_t ev[6] = {};
+  bool copy_timed = false;             // ev[4] / ev[5] bracket the quiescent copy of this step
 };
 
 static int to_dev(fc_forest* f, const std::vector<int32_t>& v, int rec, DevList& out) {
@@ -383,10 +384,11 @@ static int update_local(fc_forest* f, double dt) {
     CK(cudaMemsetAsync(f->d_nactive, 0, sizeof(int32_t), f->stream));
     const int fr = launch_filter(p.kind, f->qold, f->qnew, (int)f->Pl, f->pl.m, f->d_uflag, f->d_uval, f->d_nbr,
                                  f->d_negmask, f->d_level, dt, f->pl.dx0, p.p0, p.p1, f->d_active, f->d_nactive,
-                                 f->d_cfl, f->stream);
+                                 f->d_cfl, f->stream, f->timing ? f->ev[4] : nullptr, f->timing ? f->ev[5] : nullptr);
     if (fr > 0) {
       f->st.kernel_launches += fr;
       filtered = true;
+      f->copy_timed = f->timing;
     }
   }
   int lr = launch_step(p.kind, f->qold, f->qnew, f->aux, f->d_level, f->Pl, f->pl.m, dt, f->pl.dx0,
@@ -688,7 +690,8 @@ int fc_reset_stats(fc_forest* f) {
   if (!f) return fail(FC_EINVAL, "null handle");
   f->st.kernel_launches = 0;
   f->st.steps = 0;
-  f->st.ms_ghost = f->st.ms_step = f->st.ms_comm = 0.0;
+  f->st.ms_ghost = f->st.ms_step = f->st.ms_comm = f->st.ms_copy = 0.0;
+  f->st.copy_launches = 0;
   f->st.step_kernel_launches = 0;
   return FC_OK;
 }
@@ -822,6 +825,13 @@ int fc_step(fc_forest* f, double dt, double* max_cfl) {
     cudaEventElapsedTime(&a, f->ev[0], f->ev[1]);
     cudaEventElapsedTime(&b, f->ev[1], f->ev[2]);
     cudaEventElapsedTime(&c, f->ev[2], f->ev[3]);
+    if (f->copy_timed) {
+      float d = 0.f;
+      cudaEventElapsedTime(&d, f->ev[4], f->ev[5]);
+      f->st.ms_copy += d;
+      f->st.copy_launches += 1;
+      f->copy_timed = false;
+    }
     f->st.ms_ghost += a;
     f->st.ms_step += b;
     f->st.ms_comm += c;

@@ -806,9 +806,10 @@ template <class S>
 static int launch_filter_s(const double* qold, double* qnew, int npatch, int m, uint8_t* uflag, double* uval,
                            const int32_t* nbr, const uint8_t* negmask, const int8_t* level, double dt,
                            double dx0, SolverParams sp, int32_t* active, int32_t* nactive,
-                           unsigned long long* cfl_bits, cudaStream_t st) {
+                           unsigned long long* cfl_bits, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1) {
   if (npatch <= 0) return 0;
   const int blocks_copy = 148 * 8;
+  if (e0) cudaEventRecord(e0, st);
   switch (m) {
     case 32: k_copy_classify<S::MEQN, 32><<<blocks_copy, 256, 0, st>>>(qold, qnew, npatch, uflag, uval); break;
     case 16: k_copy_classify<S::MEQN, 16><<<blocks_copy, 256, 0, st>>>(qold, qnew, npatch, uflag, uval); break;
@@ -816,6 +817,7 @@ static int launch_filter_s(const double* qold, double* qnew, int npatch, int m, 
     case 4: k_copy_classify<S::MEQN, 4><<<blocks_copy, 256, 0, st>>>(qold, qnew, npatch, uflag, uval); break;
     default: return -1;
   }
+  if (e1) cudaEventRecord(e1, st);
   k_activity<S><<<(npatch + 255) / 256, 256, 0, st>>>(npatch, uflag, uval, nbr, negmask, level, dt, dx0, sp,
                                                        active, nactive, cfl_bits);
   return 2;
@@ -824,20 +826,20 @@ static int launch_filter_s(const double* qold, double* qnew, int npatch, int m, 
 int launch_filter(int kind, const double* qold, double* qnew, int npatch, int m, uint8_t* uflag, double* uval,
                   const int32_t* nbr, const uint8_t* negmask, const int8_t* level, double dt, double dx0,
                   double p0, double p1, int32_t* active, int32_t* nactive, unsigned long long* cfl_bits,
-                  cudaStream_t st) {
+                  cudaStream_t st, cudaEvent_t ev_before_copy, cudaEvent_t ev_after_copy) {
   SolverParams sp;
   sp.p0 = p0;
   sp.p1 = p1;
   switch (kind) {
     case FC_ADV_CONST:
       return launch_filter_s<AdvConst>(qold, qnew, npatch, m, uflag, uval, nbr, negmask, level, dt, dx0, sp,
-                                       active, nactive, cfl_bits, st);
+                                       active, nactive, cfl_bits, st, ev_before_copy, ev_after_copy);
     case FC_SWE_ROE:
       return launch_filter_s<SweRoe>(qold, qnew, npatch, m, uflag, uval, nbr, negmask, level, dt, dx0, sp,
-                                     active, nactive, cfl_bits, st);
+                                     active, nactive, cfl_bits, st, ev_before_copy, ev_after_copy);
     case FC_EULER_ROE:
       return launch_filter_s<EulerRoe>(qold, qnew, npatch, m, uflag, uval, nbr, negmask, level, dt, dx0, sp,
-                                       active, nactive, cfl_bits, st);
+                                       active, nactive, cfl_bits, st, ev_before_copy, ev_after_copy);
   }
   return -1;   // capacity form: edge-dependent CFL, no patch filter
 }
