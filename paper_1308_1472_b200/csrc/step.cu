@@ -132,6 +132,37 @@ __device__ __forceinline__ void edge_correction(const double* sc, const double* 
                                                 int st, const StepArgs& A, AuxCell ar, double rl, double rr,
                                                 double& cfl, double* P, double* Q, double* F) {
   constexpr int MEQN = S::MEQN;
+  if constexpr (MEQN == 1 && S::MW == 1) {
+    // scalar: the limited correction phi(W_I / W) W evaluated division-free as
+    // sign(W) min(|c1 W + c2 W_I|, c3 |W|, c4 |W_I|) when W and W_I share a sign (else lo W) --
+    // equal in exact arithmetic; the phased kernel is issue-bound on scalars, so the reciprocal's
+    // MUFU + Newton steps per edge are worth removing
+    const double W = sc[0];
+    const double s = S::template speed<D>(sc, st, 0, A.sp, ar);
+    cfl = fmax(cfl, fmax(rr * s, -rl * s));
+    double sm, sp;
+    split0(s, sm, sp);
+    double f = 0.0;
+    if (A.method2 == 2 && W != 0.0) {
+      const double WI = (s > 0.0 ? scm : scp)[0];
+      const LimiterCoef& L = A.lim;
+      double phiw;
+      if (L.lo == 1.0) {
+        phiw = W;
+      } else if ((W > 0.0 && WI > 0.0) || (W < 0.0 && WI < 0.0)) {
+        const double mag = fmin(fmin(fabs(fma(L.c1, W, L.c2 * WI)), L.c3 * fabs(W)), L.c4 * fabs(WI));
+        phiw = W > 0.0 ? mag : -mag;
+      } else {
+        phiw = 0.0;
+      }
+      const double as = fabs(s), rav = 0.5 * (rl + rr);
+      f = 0.5 * as * (1.0 - as * rav) * phiw;
+    }
+    F[0] = f;
+    P[0] = sm * W + f;
+    Q[0] = sp * W - f;
+    return;
+  }
   double am[MEQN], ap[MEQN];
 #pragma unroll
   for (int k = 0; k < MEQN; ++k) {
