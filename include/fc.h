@@ -171,6 +171,14 @@ int fc_step(fc_forest* f, double dt, double* max_cfl);
  * buffers, allocated at the first call. */
 int fc_step_subcycled(fc_forest* f, double dt_coarse, double* max_cfl);
 
+/* nsteps global steps with a fixed dt (the advection configs' policy), as one CUDA graph per step
+ * replayed back to back with no host round trip (the per-step CFL goes to a device history;
+ * cfls[nsteps] receives it if not NULL, *max_cfl its maximum).  Same kernels and results as
+ * nsteps x fc_step(dt).  If any step's CFL exceeds cfl_reject (FC_ECFL) or is not finite
+ * (FC_ENONFINITE) the whole run is undone (state restored).  One rank (FC_EUNSUP otherwise).  The
+ * graphs are captured at the first call and again when dt or nsteps' capacity changes. */
+int fc_run(fc_forest* f, double dt, int64_t nsteps, double* cfls, double* max_cfl);
+
 /* Dynamic regrid (PAPER.md:148-155 [§2] 2:1 balanced refinement, PAPER.md:207-211 [§3] "interpolation
  * from coarse grids to newly created fine grids, and the averaging of fine grid data to a newly
  * created underlying coarse grid").  Tag: max - min of component 0 over each patch.

@@ -41,6 +41,7 @@ int launch_sub_snapshot(const double* cur, double* old, double* snap, const int8
                         int m, int n2, int l, const double* alpha, int lmin, cudaStream_t st);
 int launch_sub_accumulate(const int32_t* list, int64_t n, const int32_t* rslot, const double* rec, double* acc,
                           int fs, double dt, int add, cudaStream_t st);
+int launch_cfl_hist(const unsigned long long* cfl_bits, double* hist, int64_t* idx, cudaStream_t st);
 int launch_regrid_tag(const double* q, int64_t P, int meqn, int m, double* tag, cudaStream_t st);
 int launch_regrid_transfer(const double* qo, double* qn, const int32_t* src, int64_t NP, int meqn, int m,
                            cudaStream_t st);
@@ -116,6 +117,14 @@ struct fc_forest {
   int32_t* d_lvl_cnt = nullptr;        // per level: count (device, for k_step's active list)
   int64_t sub_tick_old[32] = {}, sub_tick_new[32] = {};
   double sub_dt0 = 0.0;
+  // fc_run: one CUDA graph per buffer parity for a fixed dt, the CFL history, a rollback copy
+  cudaGraphExec_t run_exec[2] = {nullptr, nullptr};
+  double run_dt = 0.0;
+  double* d_hist = nullptr;
+  int64_t hist_cap = 0;
+  int64_t* d_hist_idx = nullptr;
+  double* d_backup = nullptr;
+  int64_t run_launches = 0;            // kernels per captured step
   std::vector<DevList> interp, bcx_l, bcy_l;
   fc_problem prob{};
   bool has_problem = false, has_q = false, has_aux = false;
@@ -438,6 +447,8 @@ static void destroy(fc_forest* f) {
     cudaFree(f->d_uflag); cudaFree(f->d_uval);
     cudaFree(f->d_rslot); cudaFree(f->d_rcells); cudaFree(f->d_freg);
     cudaFree(f->d_rpeer);
+    for (auto& g : f->run_exec) if (g) cudaGraphExecDestroy(g);
+    cudaFree(f->d_hist); cudaFree(f->d_hist_idx); cudaFree(f->d_backup);
     for (size_t r = 0; r < f->peer_ipc.size(); ++r)
       if (f->peer_ipc[r])
         for (double* p : f->peer_buf[r]) if (p) cudaIpcCloseMemHandle(p);
@@ -839,6 +850,101 @@ int fc_step(fc_forest* f, double dt, double* max_cfl) {
   const double cfl = *f->h_cfl;
   if (max_cfl) *max_cfl = cfl;
   return commit(f, cfl);
+}
+
+// ---- multi-step fixed-dt run in CUDA graphs ---------------------------------------------------------
+// The device part of one step (ghost fill or fused gather, quiescent filter, update, CFL into the
+// history) is captured once per buffer parity and replayed nsteps times with no host round trip;
+// the CFLs are checked at the end.  If any exceeds cfl_reject (or is not finite) the run is undone
+// from a copy of the starting state.  Semantics = nsteps x fc_step(dt) without retakes.
+static int run_capture(fc_forest* f, double dt) {
+  const int64_t kl = f->st.kernel_launches, skl = f->st.step_kernel_launches;   // capture is not a launch
+  const bool timing = f->timing;   // no timing events inside the graphs
+  f->timing = false;
+  for (int par = 0; par < 2; ++par) {
+    if (f->run_exec[par]) { cudaGraphExecDestroy(f->run_exec[par]); f->run_exec[par] = nullptr; }
+    double* qo = f->buf[par];
+    double* qn = f->buf[par ^ 1];
+    double* save_o = f->qold;
+    double* save_n = f->qnew;
+    f->qold = qo;
+    f->qnew = qn;
+    CK(cudaStreamBeginCapture(f->stream, cudaStreamCaptureModeRelaxed));
+    int rc = use_fused(f) ? FC_OK : ghost_fill_internal(f);
+    if (!rc) rc = update_local(f, dt);
+    if (!rc) launch_cfl_hist(f->d_cfl, f->d_hist, f->d_hist_idx, f->stream);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(f->stream, &g);
+    f->qold = save_o;
+    f->qnew = save_n;
+    if (rc) { if (g) cudaGraphDestroy(g); f->timing = timing; return rc; }
+    if (ec != cudaSuccess) { f->timing = timing; return fail(FC_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ec)); }
+    const cudaError_t ei = cudaGraphInstantiate(&f->run_exec[par], g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) { f->timing = timing; return fail(FC_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)); }
+  }
+  f->timing = timing;
+  f->copy_timed = false;
+  f->run_launches = (f->st.kernel_launches - kl) / 2 + 1;   // + the CFL history kernel
+  f->st.kernel_launches = kl;
+  f->st.step_kernel_launches = skl;
+  f->run_dt = dt;
+  return FC_OK;
+}
+
+int fc_run(fc_forest* f, double dt, int64_t nsteps, double* cfls, double* max_cfl) {
+  int rc = check_step_args(f, dt);
+  if (rc) return rc;
+  if (nsteps < 0) return fail(FC_EINVAL, "nsteps < 0");
+  if (f->pl.nranks != 1) return fail(FC_EUNSUP, "fc_run runs on one rank");
+  if (max_cfl) *max_cfl = 0.0;
+  if (nsteps == 0) return FC_OK;
+  CK(cudaSetDevice(f->device));
+  if (f->hist_cap < nsteps) {
+    cudaFree(f->d_hist);
+    f->d_hist = nullptr;
+    CK(cudaMalloc(&f->d_hist, nsteps * sizeof(double)));
+    f->hist_cap = nsteps;
+    if (f->run_exec[0]) { cudaGraphExecDestroy(f->run_exec[0]); f->run_exec[0] = nullptr; }   // re-capture
+    if (f->run_exec[1]) { cudaGraphExecDestroy(f->run_exec[1]); f->run_exec[1] = nullptr; }
+  }
+  if (!f->d_hist_idx) CK(cudaMalloc(&f->d_hist_idx, sizeof(int64_t)));
+  if (!f->d_backup) CK(cudaMalloc(&f->d_backup, f->state_doubles * sizeof(double)));
+  if (!f->run_exec[0] || f->run_dt != dt) {   // (relaxed capture: one-time kernel setup may run inside)
+    if ((rc = run_capture(f, dt))) return rc;
+  }
+  const int par0 = f->parity;
+  double* start = f->qold;
+  CK(cudaMemcpyAsync(f->d_backup, start, f->state_doubles * sizeof(double), cudaMemcpyDeviceToDevice, f->stream));
+  CK(cudaMemsetAsync(f->d_hist_idx, 0, sizeof(int64_t), f->stream));
+  for (int64_t i = 0; i < nsteps; ++i) {
+    CK(cudaGraphLaunch(f->run_exec[f->parity], f->stream));
+    std::swap(f->qold, f->qnew);
+    f->parity ^= 1;
+  }
+  std::vector<double> h(nsteps);
+  CK(cudaMemcpyAsync(h.data(), f->d_hist, nsteps * sizeof(double), cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  double mx = 0.0;
+  bool bad = false, over = false;
+  for (int64_t i = 0; i < nsteps; ++i) {
+    if (cfls) cfls[i] = h[i];
+    if (!std::isfinite(h[i])) bad = true;
+    else if (h[i] > f->prob.cfl_reject) over = true;
+    if (h[i] > mx || h[i] != h[i]) mx = h[i];
+  }
+  if (max_cfl) *max_cfl = mx;
+  f->st.kernel_launches += nsteps * f->run_launches;
+  f->st.step_kernel_launches += nsteps;
+  if (bad || over) {   // undo: the starting state back into the buffer that held it
+    if (f->parity != par0) { std::swap(f->qold, f->qnew); f->parity = par0; }
+    CK(cudaMemcpyAsync(f->qold, f->d_backup, f->state_doubles * sizeof(double), cudaMemcpyDeviceToDevice, f->stream));
+    CK(cudaStreamSynchronize(f->stream));
+    return bad ? fail(FC_ENONFINITE, "CFL not finite in the run; state restored")
+               : fail(FC_ECFL, "CFL above cfl_reject in the run; state restored");
+  }
+  f->st.steps += nsteps;
+  return FC_OK;
 }
 
 // ---- sub-cycled step ---------------------------------

@@ -189,6 +189,19 @@ int launch_gather(const double* q, double* dst, int64_t P, int meqn, int m, cuda
   return 1;
 }
 
+// ---- multi-step runs (fc_run): the step's CFL (IEEE bits from the atomicMax) into a history slot
+__global__ void k_cfl_hist(const unsigned long long* __restrict__ cfl_bits, double* __restrict__ hist,
+                           int64_t* __restrict__ idx) {
+  const int64_t i = *idx;
+  hist[i] = __longlong_as_double((long long)*cfl_bits);
+  *idx = i + 1;
+}
+
+int launch_cfl_hist(const unsigned long long* cfl_bits, double* hist, int64_t* idx, cudaStream_t st) {
+  k_cfl_hist<<<1, 1, 0, st>>>(cfl_bits, hist, idx);
+  return 1;
+}
+
 // ---- dynamic regrid --------------------------------------------------------
 // tag: max - min of component 0 over each patch interior (one warp per patch)
 __global__ void k_regrid_tag(const double* __restrict__ q, int64_t P, int meqn, int m, double* __restrict__ tag) {

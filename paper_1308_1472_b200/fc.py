@@ -34,7 +34,7 @@ EXPORTS = ["fc_forest_create", "fc_forest_destroy", "fc_set_problem", "fc_set_au
            "fc_halo_counts", "fc_halo_requests", "fc_halo_set_requests", "fc_halo_finalize",
            "fc_halo_buffers", "fc_halo_pack", "fc_halo_unpack", "fc_step_local", "fc_commit",
            "fc_nccl_unique_id", "fc_last_error", "fc_step_subcycled", "fc_regrid", "fc_get_leaves",
-           "fc_p2p_buffers", "fc_p2p_set_peer"]
+           "fc_p2p_buffers", "fc_p2p_set_peer", "fc_run"]
 
 
 class FcError(RuntimeError):
@@ -98,6 +98,7 @@ def lib():
         L.fc_get_leaves.argtypes = [P, P, P, C.c_int64, C.POINTER(C.c_int64)]
         L.fc_p2p_buffers.argtypes = [P, C.POINTER(P), C.POINTER(P), C.POINTER(C.c_int32)]
         L.fc_p2p_set_peer.argtypes = [P, C.c_int32, P, P]
+        L.fc_run.argtypes = [P, C.c_double, C.c_int64, P, C.POINTER(C.c_double)]
         L.fc_get_q.argtypes = [P, P, C.c_int]
         L.fc_get_q_padded.argtypes = [P, P, C.c_int]
         L.fc_get_ghost_table.argtypes = [P, C.c_int, P, C.c_int64, C.POINTER(C.c_int64)]
@@ -201,6 +202,15 @@ class Forest:
         if rc not in (FC_OK, FC_ECFL) or (raise_on_reject and rc != FC_OK):
             _check(rc, "fc_step")
         return rc, cfl.value
+
+    def run(self, dt: float, nsteps: int, raise_on_reject: bool = True):
+        """fc_run: nsteps fixed-dt steps replayed as CUDA graphs -> (rc, cfls[nsteps])."""
+        cfls = np.zeros(max(1, nsteps))
+        mx = C.c_double(0.0)
+        rc = lib().fc_run(self.h, dt, nsteps, cfls.ctypes.data_as(C.c_void_p), C.byref(mx))
+        if rc not in (FC_OK, FC_ECFL) or (raise_on_reject and rc != FC_OK):
+            _check(rc, "fc_run")
+        return rc, cfls[:nsteps]
 
     def step_subcycled(self, dt_coarse: float, raise_on_reject: bool = True):
         """One sub-cycled step (coarsest level by dt_coarse, finer levels by halves); (rc, cfl)."""
