@@ -21,6 +21,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "../../include/fc.h"
 #include "fc_internal.h"
 #include "solvers.cuh"
@@ -728,6 +730,228 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
 }
 
 // ---------------------------------------------------------------------------------------------
+// Scalar advection (AdvConst, AdvEdgeCapa): two phases per tile.  For a scalar the wave is the jump
+// and the limiter's upwind wave is another jump, so every edge computes everything it needs straight
+// from the staged window -- no separate Riemann phase -- and writes its L part (A-dq + F~, entering
+// the low cell), R part (A+dq - F~) and the four pre-scaled transverse contributions of those parts;
+// then every cell gathers its 2 x 2 edges' parts and the 8 transverse contributions around it.
+// 2 barriers per tile (3 with the window), each edge computed once: the phased k_step spent ~750
+// thread-instructions per scalar cell-update on 7 barrier-separated phases (issue-bound).
+template <class S, int T, int NT, bool RF>
+__global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
+  using Sh = StepShape<S, T>;
+  constexpr int W = Sh::W, WW = Sh::WW;
+  constexpr int NXE = (T + 1) * (T + 2), NE = 2 * NXE;   // x-edges a-1/2 (a = 1..T+1) of rows 0..T+1; y likewise
+  const int tiles2 = A.tiles * A.tiles;
+  if (A.active) ntiles = *A.nactive * tiles2;
+  auto tile_of = [&](int k) {
+    if (!A.active) return k;
+    const int a = k / tiles2;
+    return A.active[a] * tiles2 + (k - a * tiles2);
+  };
+  extern __shared__ __align__(128) double sm[];
+  double* sbuf = sm;                        // 2 staging buffers
+  double* win = sbuf + 2 * Sh::BUF;         // natural window (dense single-copy staging only)
+  double* rr = win + WW;                    // dt / (kappa dx) per window cell (capacity form)
+  double* ex = rr + WW;                     // [6][NXE]: dqL, dqR, L->up, L->down, R->up, R->down
+  double* ey = ex + 6 * NXE;                // [6][NXE]: dqL, dqR, L->left, L->right, R->left, R->right
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ double wmax[(NT + 31) / 32];
+  __shared__ int16_t umap[WW];              // natural window index -> dense storage index (qcell)
+  const int tid = threadIdx.x;
+  const int n = A.m + 4, n2 = n * n;
+  const bool dense = !A.ring && A.tiles == 1;
+  for (int t = tid; t < WW; t += NT) {
+    const int i = t % W - 1, j = t / W - 1;
+    umap[t] = (int16_t)(((unsigned)(i - 1) < (unsigned)T && (unsigned)(j - 1) < (unsigned)T)
+                            ? (j - 1) * T + (i - 1) : T * T + ring_index(i, j, T));
+  }
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_proxy_async();
+  }
+  __syncthreads();
+  if (tid < 32 && (int)blockIdx.x < ntiles) stage_tile<S, T>(A, tile_of(blockIdx.x), sbuf, &bars[0], tid);
+  if (A.ring) {
+    if ((int)blockIdx.x < ntiles) gather_ring<S, T, NT>(A, tile_of(blockIdx.x), sbuf);
+    cp_async_commit();
+  }
+  double cfl = 0.0;
+  bool bad = false;
+  const double m3 = A.method3 == 2 ? 1.0 : 0.0;
+  const bool trans = A.method3 >= 1, second = A.method2 == 2;
+  const LimiterCoef L = A.lim;
+  int it = 0;
+  for (int kt = blockIdx.x; kt < ntiles; kt += gridDim.x, ++it) {
+    const int b = it & 1;
+    const int tile = tile_of(kt);
+    const int knext = kt + gridDim.x;
+    bool issued = false;
+    auto issue_next = [&]() {
+      if (issued) return;
+      issued = true;
+      if (tid < 32 && knext < ntiles) {
+        fence_proxy_async();
+        stage_tile<S, T>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF, &bars[b ^ 1], tid);
+      }
+      if (A.ring) {
+        if (knext < ntiles) gather_ring<S, T, NT>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF);
+        cp_async_commit();
+      }
+    };
+    double* sq = sbuf + b * Sh::BUF;
+    double* sa = sq + WW + 2;
+    int patch = tile, tx = 0, ty = 0;
+    if (A.tiles > 1) {
+      patch = tile / tiles2;
+      const int tt = tile - patch * tiles2;
+      ty = tt / A.tiles;
+      tx = tt - ty * A.tiles;
+    }
+    const double dtdx = A.dt / ldexp(A.dx0, -(int)A.level[patch]);
+    const int slot = RF ? A.rslot[patch] : -1;
+    auto reg = [&](int face, int e) { return A.freg + (((int64_t)slot * 4 + face) * A.m + e); };
+    mbar_wait(&bars[b], (uint32_t)((it >> 1) & 1));
+    if (A.ring) {
+      cp_async_wait<0>();
+      __syncthreads();
+      issue_next();
+      const uint8_t bc = A.bcflag[patch];
+      if (bc & 1) { window_bc<S, T, NT>(A, tile, sq, 0); __syncthreads(); }
+      if (bc & 2) { window_bc<S, T, NT>(A, tile, sq, 1); __syncthreads(); }
+    }
+    // phase 0: natural window (un-permuting the dense staging), r per cell, uniformity
+    const double* wq = dense ? win : sq;
+    const double ref = dense ? sq[0] : sq[2 * W + 2];     // interior cell (1, 1)
+    bool diff = false;
+    for (int t = opaque(threadIdx.x); t < WW; t += NT) {
+      double v;
+      if (dense) {
+        v = sq[umap[t]];
+        win[t] = v;
+      } else {
+        v = sq[t];
+      }
+      if (S::CAPA) rr[t] = dtdx / sa[t];
+      diff |= v != ref;
+    }
+    const bool may_skip = A.skip_quiescent && !(RF && slot >= 0);
+    bool uniform = false;
+    if (may_skip) uniform = !__syncthreads_or(diff);
+    else __syncthreads();
+    issue_next();
+    if (uniform) {   // every jump is zero: q_new = q, CFL from the state
+      cfl = fmax(cfl, S::quiescent_cfl(sq, WW, A.sp, sa, dtdx, T, W, opaque(threadIdx.x), NT));
+      for (int t = opaque(threadIdx.x); t < T * T; t += NT) {
+        const int i = 1 + t % T, j = 1 + t / T;
+        A.qnew[patch * (int64_t)n2 + (int64_t)(ty * T + j - 1) * A.m + tx * T + i - 1] = ref;
+      }
+      __syncthreads();
+      continue;
+    }
+    auto Q = [&](int a, int c) { return wq[(c + 1) * W + (a + 1)]; };
+    auto R = [&](int a, int c) { return S::CAPA ? rr[(c + 1) * W + (a + 1)] : dtdx; };
+    auto UX = [&](int a, int c) { return S::CAPA ? sa[WW + (c + 1) * W + (a + 1)] : A.sp.p0; };
+    auto VY = [&](int a, int c) { return S::CAPA ? sa[2 * WW + (c + 1) * W + (a + 1)] : A.sp.p1; };
+    auto limited = [&](double w, double wi) {   // phi(w_i / w) w, division-free
+      if (L.lo == 1.0) return w;
+      if (!((w > 0.0 && wi > 0.0) || (w < 0.0 && wi < 0.0))) return 0.0;
+      const double mag = fmin(fmin(fabs(fma(L.c1, w, L.c2 * wi)), L.c3 * fabs(w)), L.c4 * fabs(wi));
+      return w > 0.0 ? mag : -mag;
+    };
+    // phase A: every edge once (x-edges then y-edges; the branch is warp-uniform but for one warp)
+    auto edge = [&](auto dir, int u) {
+      constexpr int D = decltype(dir)::value;
+      constexpr int dla = D == 1 ? -1 : 0, dlc = D == 1 ? 0 : -1;
+      const int a = D == 1 ? 1 + u % (T + 1) : u % (T + 2);
+      const int c = D == 1 ? u / (T + 1) : 1 + u / (T + 2);
+      // the edge joins cells lo = (a-1, c) | hi = (a, c) (x) or lo = (a, c-1) | hi = (a, c) (y)
+      const double* qh_p = wq + (c + 1) * W + (a + 1);
+      constexpr int step = D == 1 ? 1 : W;
+      const double qh = qh_p[0], ql = qh_p[-step];
+      const double w = qh - ql;
+      const double s = D == 1 ? UX(a, c) : VY(a, c);
+      const double rl = R(a + dla, c + dlc), rh = R(a, c);
+      const double sp = s > 0.0 ? s : 0.0, sn = s - sp;
+      double f = 0.0;
+      if (second && w != 0.0) {
+        const double wi = s > 0.0 ? ql - qh_p[-2 * step] : qh_p[step] - qh;
+        const double as = fabs(s);
+        f = 0.5 * as * (1.0 - as * (0.5 * (rl + rh))) * limited(w, wi);
+      }
+      if (S::CAPA) cfl = fmax(cfl, fmax(rh * s, -rl * s));
+      double* E = D == 1 ? ex : ey;
+      E[u] = sn * w + f;                 // dqL: enters the low cell
+      E[NXE + u] = sp * w - f;           // dqR: enters the high cell
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+      if (trans) {
+        const double xl = sn * w + m3 * f, xr = sp * w - m3 * f;
+        if (D == 1) {    // into G~ at the y-edges of the receiving cells (own bottom / top velocities)
+          t0 = -0.5 * rl * fmax(VY(a - 1, c + 1), 0.0) * xl;   // L -> up of (a-1, c)
+          t1 = -0.5 * rl * fmin(VY(a - 1, c), 0.0) * xl;       // L -> down
+          t2 = -0.5 * rh * fmax(VY(a, c + 1), 0.0) * xr;       // R -> up of (a, c)
+          t3 = -0.5 * rh * fmin(VY(a, c), 0.0) * xr;           // R -> down
+        } else {         // into F~ at the x-edges of the receiving cells (own left / right velocities)
+          t0 = -0.5 * rl * fmin(UX(a, c - 1), 0.0) * xl;       // L -> left of (a, c-1)
+          t1 = -0.5 * rl * fmax(UX(a + 1, c - 1), 0.0) * xl;   // L -> right
+          t2 = -0.5 * rh * fmin(UX(a, c), 0.0) * xr;           // R -> left of (a, c)
+          t3 = -0.5 * rh * fmax(UX(a + 1, c), 0.0) * xr;       // R -> right
+        }
+      }
+      E[2 * NXE + u] = t0;
+      E[3 * NXE + u] = t1;
+      E[4 * NXE + u] = t2;
+      E[5 * NXE + u] = t3;
+    };
+    if (!S::CAPA)   // constant velocities: the CFL is r max(|u|, |v|) on every edge
+      cfl = fmax(cfl, fmax(fmax(dtdx * A.sp.p0, -dtdx * A.sp.p0), fmax(dtdx * A.sp.p1, -dtdx * A.sp.p1)));
+    for (int t = opaque(threadIdx.x); t < NE; t += NT) {
+      if (t < NXE) edge(std::integral_constant<int, 1>{}, t);
+      else edge(std::integral_constant<int, 2>{}, t - NXE);
+    }
+    __syncthreads();
+    // phase B: every cell gathers its edges
+    for (int t = opaque(threadIdx.x); t < T * T; t += NT) {
+      const int i = 1 + t % T, j = 1 + t / T;
+      auto xi = [](int a, int c) { return c * (T + 1) + (a - 1); };
+      auto yi = [](int a, int c) { return (c - 1) * (T + 2) + a; };
+      const double Gt = ex[4 * NXE + xi(i, j)] + ex[2 * NXE + xi(i + 1, j)] + ex[5 * NXE + xi(i, j + 1)] +
+                        ex[3 * NXE + xi(i + 1, j + 1)];
+      const double Gb = ex[4 * NXE + xi(i, j - 1)] + ex[2 * NXE + xi(i + 1, j - 1)] + ex[5 * NXE + xi(i, j)] +
+                        ex[3 * NXE + xi(i + 1, j)];
+      const double Fr = ey[3 * NXE + yi(i, j + 1)] + ey[5 * NXE + yi(i, j)] + ey[2 * NXE + yi(i + 1, j + 1)] +
+                        ey[4 * NXE + yi(i + 1, j)];
+      const double Fl = ey[3 * NXE + yi(i - 1, j + 1)] + ey[5 * NXE + yi(i - 1, j)] + ey[2 * NXE + yi(i, j + 1)] +
+                        ey[4 * NXE + yi(i, j)];
+      const double dxR = ex[NXE + xi(i, j)], dxL = ex[xi(i + 1, j)];
+      const double dyR = ey[NXE + yi(i, j)], dyL = ey[yi(i, j + 1)];
+      const double r0 = R(i, j), q0 = Q(i, j);
+      const double val = q0 - r0 * (dxR + dxL + Fr - Fl) - r0 * (dyR + dyL + Gt - Gb);
+      bad |= !isfinite(val);
+      A.qnew[patch * (int64_t)n2 + (int64_t)(ty * T + j - 1) * A.m + tx * T + i - 1] = val;
+      if (RF && slot >= 0) {   // applied face fluxes, outward (reflux records)
+        if (tx == 0 && i == 1) *reg(0, ty * T + j - 1) = (dxR - Fl) - UX(1, j) * q0;
+        if (tx == A.tiles - 1 && i == T) *reg(1, ty * T + j - 1) = UX(T + 1, j) * q0 + (dxL + Fr);
+        if (ty == 0 && j == 1) *reg(2, tx * T + i - 1) = (dyR - Gb) - VY(i, 1) * q0;
+        if (ty == A.tiles - 1 && j == T) *reg(3, tx * T + i - 1) = VY(i, T + 1) * q0 + (dyL + Gt);
+      }
+    }
+    __syncthreads();   // the window, r and the edge arrays are rewritten by the next tile
+  }
+  if (__syncthreads_or(bad)) cfl = __longlong_as_double(0x7ff0000000000000ll);
+  if (cfl != cfl) cfl = __longlong_as_double(0x7ff0000000000000ll);
+  for (int o = 16; o > 0; o >>= 1) cfl = fmax(cfl, __shfl_xor_sync(0xffffffffu, cfl, o));
+  if ((tid & 31) == 0) wmax[tid >> 5] = cfl;
+  __syncthreads();
+  if (tid == 0) {
+    double c = wmax[0];
+    for (int w = 1; w < (NT + 31) / 32; ++w) c = fmax(c, wmax[w]);
+    atomicMax(A.cfl_bits, (unsigned long long)__double_as_longlong(c));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Quiescent-patch filter for the fused (ring-gather) path, three kernels per step:
 //   k_copy_classify  q_new interior = q_old interior (streaming, 16-byte accesses) and, per patch,
 //                    "interior uniform" + its state;
@@ -904,6 +1128,34 @@ static int launch_step_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   return 1;
 }
 
+template <class S, int T, bool RF>
+static int launch_sc_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  constexpr int NT = T * T < 32 ? 32 : T * T;
+  constexpr int NXE = (T + 1) * (T + 2);
+  const size_t smem = ((size_t)2 * StepShape<S, T>::BUF + 2 * (size_t)StepShape<S, T>::WW + 12 * (size_t)NXE) *
+                      sizeof(double);
+  static int resident = 0;
+  if (!resident) {
+    cudaFuncSetAttribute(k_step_sc<S, T, NT, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_step_sc<S, T, NT, RF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_sc<S, T, NT, RF>, NT, smem);
+    resident = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int64_t ntiles = npatch * a.tiles * a.tiles;
+  if (ntiles >= (1ll << 31)) return -1;
+  const int64_t grid = ntiles < resident ? ntiles : resident;
+  k_step_sc<S, T, NT, RF><<<(unsigned)grid, NT, smem, st>>>(a, (int)ntiles);
+  return 1;
+}
+
+template <class S, int T>
+static int launch_sc(const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  return a.rslot ? launch_sc_t<S, T, true>(a, npatch, st) : launch_sc_t<S, T, false>(a, npatch, st);
+}
+
 template <class S, int T, int NT, int MINB>
 static int launch_step_r(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   return a.rslot ? launch_step_t<S, T, NT, MINB, true>(a, npatch, st) : launch_step_t<S, T, NT, MINB, false>(a, npatch, st);
@@ -914,6 +1166,16 @@ static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   // CTAs per SM requested from ptxas for the 16 x 16 tile (register budget 65536 / (352 MB));
   // FC_STEP_MINB overrides it for tuning experiments (without reflux records)
   static const int env_mb = getenv("FC_STEP_MINB") ? atoi(getenv("FC_STEP_MINB")) : 0;
+  // scalar solvers: the two-phase kernel (FC_SCALAR_PHASED=1 keeps the generic phased k_step)
+  static const bool phased = getenv("FC_SCALAR_PHASED") && atoi(getenv("FC_SCALAR_PHASED"));
+  if constexpr (S::MEQN == 1) {
+    if (!phased) {
+      if (a.m % 16 == 0) return launch_sc<S, 16>(a, npatch, st);
+      if (a.m % 8 == 0) return launch_sc<S, 8>(a, npatch, st);
+      if (a.m % 4 == 0) return launch_sc<S, 4>(a, npatch, st);
+      if (a.m % 2 == 0) return launch_sc<S, 2>(a, npatch, st);
+    }
+  }
   constexpr int dmb = (S::MEQN >= 3) ? 2 : 3;
   const int mb = env_mb ? env_mb : dmb;
   if (a.m % 16 == 0) {
