@@ -781,7 +781,9 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
   bool bad = false;
   const double m3 = A.method3 == 2 ? 1.0 : 0.0;
   const bool trans = A.method3 >= 1, second = A.method2 == 2;
-  const LimiterCoef L = A.lim;
+  const bool nolim = A.lim.lo == 1.0;
+  const double lc1 = A.lim.c1, lc2 = A.lim.c2, lc3 = A.lim.c3, lc4 = A.lim.c4;
+  const double u0 = A.sp.p0, v0 = A.sp.p1;
   int it = 0;
   for (int kt = blockIdx.x; kt < ntiles; kt += gridDim.x, ++it) {
     const int b = it & 1;
@@ -852,14 +854,21 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
     }
     auto Q = [&](int a, int c) { return wq[(c + 1) * W + (a + 1)]; };
     auto R = [&](int a, int c) { return S::CAPA ? rr[(c + 1) * W + (a + 1)] : dtdx; };
-    auto UX = [&](int a, int c) { return S::CAPA ? sa[WW + (c + 1) * W + (a + 1)] : A.sp.p0; };
-    auto VY = [&](int a, int c) { return S::CAPA ? sa[2 * WW + (c + 1) * W + (a + 1)] : A.sp.p1; };
-    auto limited = [&](double w, double wi) {   // phi(w_i / w) w, division-free
-      if (L.lo == 1.0) return w;
-      if (!((w > 0.0 && wi > 0.0) || (w < 0.0 && wi < 0.0))) return 0.0;
-      const double mag = fmin(fmin(fabs(fma(L.c1, w, L.c2 * wi)), L.c3 * fabs(w)), L.c4 * fabs(wi));
-      return w > 0.0 ? mag : -mag;
+    auto UX = [&](int a, int c) { return S::CAPA ? sa[WW + (c + 1) * W + (a + 1)] : u0; };
+    auto VY = [&](int a, int c) { return S::CAPA ? sa[2 * WW + (c + 1) * W + (a + 1)] : v0; };
+    // phi(w_i / w) w, division-free and branch-free (lo = 1: no limiter)
+    auto limited = [&](double w, double wi) {
+      const bool same = (w > 0.0 && wi > 0.0) || (w < 0.0 && wi < 0.0);
+      const double mag = fmin(fmin(fabs(fma(lc1, w, lc2 * wi)), lc3 * fabs(w)), lc4 * fabs(wi));
+      return nolim ? w : (same ? copysign(mag, w) : 0.0);
     };
+    // per-tile constants of the constant-velocity solver
+    const double spx = u0 > 0.0 ? u0 : 0.0, snx = u0 - spx, spy = v0 > 0.0 ? v0 : 0.0, sny = v0 - spy;
+    const double cfx = second ? 0.5 * fabs(u0) * (1.0 - fabs(u0) * dtdx) : 0.0;
+    const double cfy = second ? 0.5 * fabs(v0) * (1.0 - fabs(v0) * dtdx) : 0.0;
+    const double ht = trans ? -0.5 * dtdx : 0.0;
+    const double kup = ht * (v0 > 0.0 ? v0 : 0.0), kdown = ht * (v0 < 0.0 ? v0 : 0.0);
+    const double kleft = ht * (u0 < 0.0 ? u0 : 0.0), kright = ht * (u0 > 0.0 ? u0 : 0.0);
     // phase A: every edge once (x-edges then y-edges; the branch is warp-uniform but for one warp)
     auto edge = [&](auto dir, int u) {
       constexpr int D = decltype(dir)::value;
@@ -871,41 +880,56 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
       constexpr int step = D == 1 ? 1 : W;
       const double qh = qh_p[0], ql = qh_p[-step];
       const double w = qh - ql;
-      const double s = D == 1 ? UX(a, c) : VY(a, c);
-      const double rl = R(a + dla, c + dlc), rh = R(a, c);
-      const double sp = s > 0.0 ? s : 0.0, sn = s - sp;
-      double f = 0.0;
-      if (second && w != 0.0) {
-        const double wi = s > 0.0 ? ql - qh_p[-2 * step] : qh_p[step] - qh;
+      double s, sp, sn, cf, rl, rh;
+      if (S::CAPA) {
+        s = D == 1 ? UX(a, c) : VY(a, c);
+        rl = R(a + dla, c + dlc);
+        rh = R(a, c);
+        sp = s > 0.0 ? s : 0.0;
+        sn = s - sp;
         const double as = fabs(s);
-        f = 0.5 * as * (1.0 - as * (0.5 * (rl + rh))) * limited(w, wi);
+        cf = second ? 0.5 * as * (1.0 - as * (0.5 * (rl + rh))) : 0.0;
+        cfl = fmax(cfl, fmax(rh * s, -rl * s));
+      } else {   // per-tile constants
+        s = D == 1 ? u0 : v0;
+        sp = D == 1 ? spx : spy;
+        sn = D == 1 ? snx : sny;
+        cf = D == 1 ? cfx : cfy;
+        rl = rh = dtdx;
       }
-      if (S::CAPA) cfl = fmax(cfl, fmax(rh * s, -rl * s));
+      const double wi = s > 0.0 ? ql - qh_p[-2 * step] : qh_p[step] - qh;
+      const double f = cf * limited(w, wi);
       double* E = D == 1 ? ex : ey;
       E[u] = sn * w + f;                 // dqL: enters the low cell
       E[NXE + u] = sp * w - f;           // dqR: enters the high cell
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-      if (trans) {
-        const double xl = sn * w + m3 * f, xr = sp * w - m3 * f;
+      const double xl = sn * w + m3 * f, xr = sp * w - m3 * f;
+      double k0, k1, k2, k3;             // -1/2 r B+- of the receiving cells, 0 without transverse
+      if (S::CAPA) {
+        const double h = trans ? -0.5 : 0.0;
         if (D == 1) {    // into G~ at the y-edges of the receiving cells (own bottom / top velocities)
-          t0 = -0.5 * rl * fmax(VY(a - 1, c + 1), 0.0) * xl;   // L -> up of (a-1, c)
-          t1 = -0.5 * rl * fmin(VY(a - 1, c), 0.0) * xl;       // L -> down
-          t2 = -0.5 * rh * fmax(VY(a, c + 1), 0.0) * xr;       // R -> up of (a, c)
-          t3 = -0.5 * rh * fmin(VY(a, c), 0.0) * xr;           // R -> down
+          k0 = h * rl * fmax(VY(a - 1, c + 1), 0.0);   // L -> up of (a-1, c)
+          k1 = h * rl * fmin(VY(a - 1, c), 0.0);       // L -> down
+          k2 = h * rh * fmax(VY(a, c + 1), 0.0);       // R -> up of (a, c)
+          k3 = h * rh * fmin(VY(a, c), 0.0);           // R -> down
         } else {         // into F~ at the x-edges of the receiving cells (own left / right velocities)
-          t0 = -0.5 * rl * fmin(UX(a, c - 1), 0.0) * xl;       // L -> left of (a, c-1)
-          t1 = -0.5 * rl * fmax(UX(a + 1, c - 1), 0.0) * xl;   // L -> right
-          t2 = -0.5 * rh * fmin(UX(a, c), 0.0) * xr;           // R -> left of (a, c)
-          t3 = -0.5 * rh * fmax(UX(a + 1, c), 0.0) * xr;       // R -> right
+          k0 = h * rl * fmin(UX(a, c - 1), 0.0);       // L -> left of (a, c-1)
+          k1 = h * rl * fmax(UX(a + 1, c - 1), 0.0);   // L -> right
+          k2 = h * rh * fmin(UX(a, c), 0.0);           // R -> left of (a, c)
+          k3 = h * rh * fmax(UX(a + 1, c), 0.0);       // R -> right
         }
+      } else {
+        k0 = D == 1 ? kup : kleft;
+        k1 = D == 1 ? kdown : kright;
+        k2 = k0;
+        k3 = k1;
       }
-      E[2 * NXE + u] = t0;
-      E[3 * NXE + u] = t1;
-      E[4 * NXE + u] = t2;
-      E[5 * NXE + u] = t3;
+      E[2 * NXE + u] = k0 * xl;
+      E[3 * NXE + u] = k1 * xl;
+      E[4 * NXE + u] = k2 * xr;
+      E[5 * NXE + u] = k3 * xr;
     };
     if (!S::CAPA)   // constant velocities: the CFL is r max(|u|, |v|) on every edge
-      cfl = fmax(cfl, fmax(fmax(dtdx * A.sp.p0, -dtdx * A.sp.p0), fmax(dtdx * A.sp.p1, -dtdx * A.sp.p1)));
+      cfl = fmax(cfl, fmax(fmax(dtdx * u0, -dtdx * u0), fmax(dtdx * v0, -dtdx * v0)));
     for (int t = opaque(threadIdx.x); t < NE; t += NT) {
       if (t < NXE) edge(std::integral_constant<int, 1>{}, t);
       else edge(std::integral_constant<int, 2>{}, t - NXE);
