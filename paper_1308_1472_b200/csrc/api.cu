@@ -100,6 +100,12 @@ struct fc_forest {
   uint8_t *d_negmask = nullptr, *d_uflag = nullptr;
   double* d_uval = nullptr;
   int32_t h_nactive = 0;
+  // adaptive quiescent filter: skipped (the full update runs; both are exact) while most patches
+  // are active, re-probed every 16 steps
+  int32_t* h_nact = nullptr;           // pinned: active patches of the last filtered step
+  double active_frac = 0.0;
+  int probe_countdown = 0;
+  bool filtered_last = false;
   // coarse/fine reflux (built at the first fc_set_problem asking for it)
   bool reflux_planned = false;
   int32_t* d_rslot = nullptr;          // [Pl] flux-register slot or -1
@@ -388,7 +394,10 @@ static int update_local(fc_forest* f, double dt) {
   bool filtered = false;
   // (tiny forests skip the filter: its two extra launches cost more than the tiles they save; the
   // step kernel's own quiescent-window check still applies)
-  if (p.skip_quiescent && p.kind != FC_ADV_EDGEVEL_CAPA && f->Pl >= 512) {
+  f->filtered_last = false;
+  const bool want_filter = p.skip_quiescent && p.kind != FC_ADV_EDGEVEL_CAPA && f->Pl >= 512;
+  const bool probe = f->probe_countdown <= 0;
+  if (want_filter && !(f->active_frac >= 0.75 && !probe)) {
     // copy/classify + activity filter, then the step over the active patches' tiles only
     CK(cudaMemsetAsync(f->d_nactive, 0, sizeof(int32_t), f->stream));
     const int fr = launch_filter(p.kind, f->qold, f->qnew, (int)f->Pl, f->pl.m, f->d_uflag, f->d_uval, f->d_nbr,
@@ -399,6 +408,8 @@ static int update_local(fc_forest* f, double dt) {
       filtered = true;
       f->copy_timed = f->timing;
     }
+  } else if (want_filter) {
+    f->probe_countdown -= 1;
   }
   int lr = launch_step(p.kind, f->qold, f->qnew, f->aux, f->d_level, f->Pl, f->pl.m, dt, f->pl.dx0,
                        p.p0, p.p1, p.limiter, p.method2, p.method3, filtered ? 0 : p.skip_quiescent,
@@ -410,12 +421,24 @@ static int update_local(fc_forest* f, double dt) {
   f->st.kernel_launches += lr;
   f->st.step_kernel_launches += lr;
   CK(cudaGetLastError());
+  if (filtered) {   // active count for the adaptive filter (read after the step's synchronisation)
+    CK(cudaMemcpyAsync(f->h_nact, f->d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, f->stream));
+    f->filtered_last = true;
+  }
   if (reflux) {   // coarse cells next to finer faces: applied flux -> mean of the fine fluxes
     f->st.kernel_launches += launch_reflux(f->d_rcells, f->nrcells, f->d_freg, f->d_freg, f->qnew, f->aux,
                                            f->d_level, 1.0, dt, f->pl.dx0, f->pl.meqn, f->pl.n * f->pl.n, f->stream);
     CK(cudaGetLastError());
   }
   return FC_OK;
+}
+
+// after a step's stream synchronisation: the active fraction seen by the quiescent filter
+static void note_activity(fc_forest* f) {
+  if (!f->filtered_last) return;
+  f->active_frac = f->Pl > 0 ? (double)*f->h_nact / (double)f->Pl : 0.0;
+  if (f->active_frac >= 0.75) f->probe_countdown = 16;
+  f->filtered_last = false;
 }
 
 static int check_step_args(fc_forest* f, double dt) {
@@ -455,6 +478,7 @@ static void destroy(fc_forest* f) {
     cudaFree(f->d_sub_old); cudaFree(f->d_sub_snap); cudaFree(f->d_facc); cudaFree(f->d_lvl_cnt);
     for (auto* d : f->d_lvl) cudaFree(d);
     if (f->h_cfl) cudaFreeHost(f->h_cfl);
+    if (f->h_nact) cudaFreeHost(f->h_nact);
     free_list(f->copy); free_list(f->avg); free_list(f->bcx); free_list(f->bcy); free_list(f->corner3);
     for (auto& l : f->interp) free_list(l);
     for (auto& l : f->bcx_l) free_list(l);
@@ -536,6 +560,7 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
   cudaMemcpy(f->d_level, lv.data(), f->Pl, cudaMemcpyHostToDevice);
   if ((e = cudaMalloc(&f->d_cfl, sizeof(unsigned long long))) != cudaSuccess) return cuda_fail(e, "cudaMalloc cfl");
   if ((e = cudaMallocHost(&f->h_cfl, sizeof(double))) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+  if ((e = cudaMallocHost(&f->h_nact, sizeof(int32_t))) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
   for (auto& ev : f->ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
   rc = plan_lists(f->pl, pl.meqn, f->gl, err);
@@ -831,6 +856,7 @@ int fc_step(fc_forest* f, double dt, double* max_cfl) {
   if (f->timing) CK(cudaEventRecord(f->ev[3], f->stream));
   CK(cudaMemcpyAsync(f->h_cfl, f->d_cfl, sizeof(double), cudaMemcpyDeviceToHost, f->stream));
   CK(cudaStreamSynchronize(f->stream));
+  note_activity(f);
   if (f->timing) {
     float a = 0.f, b = 0.f, c = 0.f;
     cudaEventElapsedTime(&a, f->ev[0], f->ev[1]);
@@ -1203,6 +1229,7 @@ int fc_step_local(fc_forest* f, double dt, int phase, double* local_cfl) {
     return fail(FC_EINVAL, "phase must be 1 or 2");
   }
   CK(cudaStreamSynchronize(f->stream));
+  note_activity(f);
   return FC_OK;
 }
 
