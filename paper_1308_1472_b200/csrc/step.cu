@@ -737,6 +737,11 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
 // then every cell gathers its 2 x 2 edges' parts and the 8 transverse contributions around it.
 // 2 barriers per tile (3 with the window), each edge computed once: the phased k_step spent ~750
 // thread-instructions per scalar cell-update on 7 barrier-separated phases (issue-bound).
+// staging depth of the scalar kernel: NB - 1 tiles in flight ahead.  Constant-velocity tiles are
+// 3.2 KB and quick to update, so more are kept in flight; capacity-form tiles carry 3 aux fields
+// and deeper staging would cost CTAs per SM (measured: T2 -4 % time at 4, T4 +18 % at 4)
+template <class S>
+__host__ __device__ constexpr int sc_nbuf() { return S::CAPA ? 2 : 4; }
 template <class S, int T, int NT, bool RF>
 __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
   using Sh = StepShape<S, T>;
@@ -749,13 +754,14 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
     const int a = k / tiles2;
     return A.active[a] * tiles2 + (k - a * tiles2);
   };
+  constexpr int NB = sc_nbuf<S>();          // staging depth: NB - 1 tiles in flight ahead
   extern __shared__ __align__(128) double sm[];
-  double* sbuf = sm;                        // 2 staging buffers
-  double* win = sbuf + 2 * Sh::BUF;         // natural window (dense single-copy staging only)
+  double* sbuf = sm;                        // NB staging buffers
+  double* win = sbuf + NB * Sh::BUF;        // natural window (dense single-copy staging only)
   double* rr = win + WW;                    // dt / (kappa dx) per window cell (capacity form)
   double* ex = rr + WW;                     // [6][NXE]: dqL, dqR, L->up, L->down, R->up, R->down
   double* ey = ex + 6 * NXE;                // [6][NXE]: dqL, dqR, L->left, L->right, R->left, R->right
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[NB];
   __shared__ double wmax[(NT + 31) / 32];
   __shared__ int16_t umap[WW];              // natural window index -> dense storage index (qcell)
   const int tid = threadIdx.x;
@@ -767,15 +773,17 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
                             ? (j - 1) * T + (i - 1) : T * T + ring_index(i, j, T));
   }
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int q = 0; q < NB; ++q) mbar_init(&bars[q], 1);
     fence_proxy_async();
   }
   __syncthreads();
-  if (tid < 32 && (int)blockIdx.x < ntiles) stage_tile<S, T>(A, tile_of(blockIdx.x), sbuf, &bars[0], tid);
-  if (A.ring) {
-    if ((int)blockIdx.x < ntiles) gather_ring<S, T, NT>(A, tile_of(blockIdx.x), sbuf);
-    cp_async_commit();
+  for (int q = 0; q < NB - 1; ++q) {
+    const int k0 = blockIdx.x + q * gridDim.x;
+    if (tid < 32 && k0 < ntiles) stage_tile<S, T>(A, tile_of(k0), sbuf + q * Sh::BUF, &bars[q], tid);
+    if (A.ring) {
+      if (k0 < ntiles) gather_ring<S, T, NT>(A, tile_of(k0), sbuf + q * Sh::BUF);
+      cp_async_commit();
+    }
   }
   double cfl = 0.0;
   bool bad = false;
@@ -786,19 +794,19 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
   const double u0 = A.sp.p0, v0 = A.sp.p1;
   int it = 0;
   for (int kt = blockIdx.x; kt < ntiles; kt += gridDim.x, ++it) {
-    const int b = it & 1;
+    const int b = it % NB, bn = (it + NB - 1) % NB;
     const int tile = tile_of(kt);
-    const int knext = kt + gridDim.x;
+    const int knext = kt + (NB - 1) * gridDim.x;
     bool issued = false;
     auto issue_next = [&]() {
       if (issued) return;
       issued = true;
       if (tid < 32 && knext < ntiles) {
         fence_proxy_async();
-        stage_tile<S, T>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF, &bars[b ^ 1], tid);
+        stage_tile<S, T>(A, tile_of(knext), sbuf + bn * Sh::BUF, &bars[bn], tid);
       }
       if (A.ring) {
-        if (knext < ntiles) gather_ring<S, T, NT>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF);
+        if (knext < ntiles) gather_ring<S, T, NT>(A, tile_of(knext), sbuf + bn * Sh::BUF);
         cp_async_commit();
       }
     };
@@ -814,9 +822,9 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
     const double dtdx = A.dt / ldexp(A.dx0, -(int)A.level[patch]);
     const int slot = RF ? A.rslot[patch] : -1;
     auto reg = [&](int face, int e) { return A.freg + (((int64_t)slot * 4 + face) * A.m + e); };
-    mbar_wait(&bars[b], (uint32_t)((it >> 1) & 1));
+    mbar_wait(&bars[b], (uint32_t)((it / NB) & 1));
     if (A.ring) {
-      cp_async_wait<0>();
+      cp_async_wait<NB - 2>();
       __syncthreads();
       issue_next();
       const uint8_t bc = A.bcflag[patch];
@@ -1156,8 +1164,8 @@ template <class S, int T, bool RF>
 static int launch_sc_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   constexpr int NT = T * T < 32 ? 32 : T * T;
   constexpr int NXE = (T + 1) * (T + 2);
-  const size_t smem = ((size_t)2 * StepShape<S, T>::BUF + 2 * (size_t)StepShape<S, T>::WW + 12 * (size_t)NXE) *
-                      sizeof(double);
+  const size_t smem = ((size_t)sc_nbuf<S>() * StepShape<S, T>::BUF + 2 * (size_t)StepShape<S, T>::WW +
+                       12 * (size_t)NXE) * sizeof(double);
   static int resident = 0;
   if (!resident) {
     cudaFuncSetAttribute(k_step_sc<S, T, NT, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
