@@ -543,7 +543,8 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
   f->stream = f->own_stream;
   const int64_t nhalo = pl.halo.n1 + pl.halo.n2;
   f->Pv = (nhalo + n2 - 1) / n2;
-  f->state_doubles = (size_t)(f->Pl + f->Pv) * pl.meqn * n2;
+  // (at least one block: an empty rank still has mappable buffers for the peer-memory halo)
+  f->state_doubles = (size_t)std::max<int64_t>(1, f->Pl + f->Pv) * pl.meqn * n2;
   if ((e = cudaMalloc(&f->qold, f->state_doubles * sizeof(double))) != cudaSuccess) return cuda_fail(e, "cudaMalloc q_old");
   if ((e = cudaMalloc(&f->qnew, f->state_doubles * sizeof(double))) != cudaSuccess) return cuda_fail(e, "cudaMalloc q_new");
   f->buf[0] = f->qold;

@@ -220,3 +220,19 @@ def test_full_size_first_step_sampled(name, rng):
         err = np.abs(qg[ids, k] - qo[:, k]).max()
         assert err <= 1e-12 * max(scale, np.abs(qo).max() if scale == 1e-300 else scale), (k, err)
     assert cfl >= co.max() * (1 - 1e-12) and cfl <= 1.0
+
+
+def test_zero_velocity_is_a_fixed_point():
+    """Degenerate advection u = v = 0: no wave moves, the state is unchanged bitwise and every CFL
+    is 0 (both kernels: constant velocity and capacity form with zero edge velocities)."""
+    import dataclasses
+    from workloads.cubed_sphere import c4_workload
+    w = dataclasses.replace(c2(steps=5), params=(0.0, 0.0))
+    q, c, _ = fc.run(w)
+    np.testing.assert_array_equal(q, w.q0)
+    assert (c == 0.0).all()
+    s = c4_workload(base_level=1, m=8, steps=3)
+    s.aux[:, 1:] = 0.0
+    q, c, _ = fc.run(s)
+    np.testing.assert_array_equal(q, s.q0)
+    assert (c == 0.0).all()

@@ -152,3 +152,19 @@ def test_peer_memory_halo_equals_single_rank_bitwise(w, R):
     qr, cr = run_sharded_p2p(w, R, do)
     np.testing.assert_array_equal(qr, q1)
     np.testing.assert_array_equal(cr, c1_)
+
+
+@pytest.mark.parametrize("R", [2, 3])
+def test_empty_ranks_bitwise(R):
+    """More ranks than patches (a one-patch periodic forest): the ranks past the patch count own
+    empty Morton ranges and take part in every stage with nothing to do (Fig. 3's idle
+    processors), for both halo transports."""
+    w = c1(level=0, m=16, steps=10)
+    _, _, do = oracle.run(w)
+    q1, c1_, _ = fc.run(w, dt_list=do)
+    qr, cr = run_sharded(w, R, do, 1)
+    np.testing.assert_array_equal(qr, q1)
+    np.testing.assert_array_equal(cr, c1_)
+    qp, cp = run_sharded_p2p(w, R, do)
+    np.testing.assert_array_equal(qp, q1)
+    np.testing.assert_array_equal(cp, c1_)
