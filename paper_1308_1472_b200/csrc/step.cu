@@ -1151,10 +1151,14 @@ static int launch_step_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   StepArgs b = a;
   b.fbuf = nullptr;
   if (a.method3 == 1) {      // F~ scratch for the (rare) method3 = 1 transverse variant, kept for the
-    static double* fbuf = nullptr;   // process lifetime (one per instantiation, resident CTAs x E2)
-    if (!fbuf && cudaMalloc(&fbuf, (size_t)resident * S::MEQN * StepShape<S, T>::E2 * sizeof(double)) != cudaSuccess)
+    static double* fbuf[64] = {};    // process lifetime, one per device (resident CTAs x E2)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return -1;
+    if (!fbuf[dev] &&
+        cudaMalloc(&fbuf[dev], (size_t)resident * S::MEQN * StepShape<S, T>::E2 * sizeof(double)) != cudaSuccess)
       return -1;
-    b.fbuf = fbuf;
+    b.fbuf = fbuf[dev];
   }
   k_step<S, T, NT, MINB, RF><<<(unsigned)grid, NT, smem, st>>>(b, (int)ntiles);
   return 1;
