@@ -37,7 +37,8 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
 int launch_reflux(const int32_t* cells, int64_t ncells, const double* freg, const double* ffine, double* qnew,
                   const double* aux, const int8_t* level, double wc, double dtr, double dx0, int meqn, int n2,
                   cudaStream_t st);
-int launch_sub_snapshot(const double* cur, double* old, double* snap, const int8_t* level, int64_t P, int meqn,
+int launch_sub_snapshot(const double* cur, double* old, double* snap, const int8_t* level, const int32_t* list,
+                        int64_t P, int meqn,
                         int m, int n2, int l, const double* alpha, int lmin, cudaStream_t st);
 int launch_sub_accumulate(const int32_t* list, int64_t n, const int32_t* rslot, const double* rec, double* acc,
                           int fs, double dt, int add, cudaStream_t st);
@@ -76,6 +77,14 @@ static int fail(int code, const std::string& msg) {
 struct DevList {
   int32_t* d = nullptr;
   int64_t nrec = 0;
+};
+
+// the ghost lists of one fill: the whole forest's, or (sub-cycling) the part a level-l fill needs
+struct FillLists {
+  DevList copy, avg, bcx, bcy, corner3;
+  std::vector<DevList> interp, bcx_l, bcy_l;
+  int32_t* d_snap = nullptr;           // (sub-cycling) the patches whose snapshot the fill reads
+  int64_t n_snap = 0;
 };
 
 struct fc_forest {
@@ -122,6 +131,8 @@ struct fc_forest {
   std::vector<int64_t> n_lvl;
   int32_t* d_lvl_cnt = nullptr;        // per level: count (device, for k_step's active list)
   int64_t sub_tick_old[32] = {}, sub_tick_new[32] = {};
+  std::vector<FillLists> sub_fill;     // per level (single rank): restricted fills + snapshot lists
+  const FillLists* fill_sel = nullptr; // when set, the ghost phases run these lists
   double sub_dt0 = 0.0;
   // fc_run: one CUDA graph per buffer parity for a fixed dt, the CFL history, a rollback copy
   cudaGraphExec_t run_exec[2] = {nullptr, nullptr};
@@ -351,23 +362,28 @@ static void run_ghost(fc_forest* f, int op, const DevList& l) {
 
 // ghost phases that only need halo round 1: A (copy, average) -> C (BC x then y)
 static int ghost_phase_ac(fc_forest* f) {
-  run_ghost(f, OP_COPY, f->copy);
-  run_ghost(f, OP_AVG4, f->avg);
-  run_ghost(f, 4, f->bcx);
-  run_ghost(f, 4, f->bcy);
+  const FillLists* s = f->fill_sel;
+  run_ghost(f, OP_COPY, s ? s->copy : f->copy);
+  run_ghost(f, OP_AVG4, s ? s->avg : f->avg);
+  run_ghost(f, 4, s ? s->bcx : f->bcx);
+  run_ghost(f, 4, s ? s->bcy : f->bcy);
   CK(cudaGetLastError());
   return FC_OK;
 }
 
 // ghost phases after halo round 2: per level B (interpolate) -> C, then CORNER3
 static int ghost_phase_b(fc_forest* f) {
-  for (size_t l = 0; l < f->interp.size(); ++l) {
-    if (!f->interp[l].nrec) continue;
-    run_ghost(f, OP_INTERP, f->interp[l]);
-    run_ghost(f, 4, f->bcx_l[l]);
-    run_ghost(f, 4, f->bcy_l[l]);
+  const FillLists* s = f->fill_sel;
+  const auto& interp = s ? s->interp : f->interp;
+  const auto& bcx_l = s ? s->bcx_l : f->bcx_l;
+  const auto& bcy_l = s ? s->bcy_l : f->bcy_l;
+  for (size_t l = 0; l < interp.size(); ++l) {
+    if (!interp[l].nrec) continue;
+    run_ghost(f, OP_INTERP, interp[l]);
+    run_ghost(f, 4, bcx_l[l]);
+    run_ghost(f, 4, bcy_l[l]);
   }
-  run_ghost(f, 6, f->corner3);
+  run_ghost(f, 6, s ? s->corner3 : f->corner3);
   CK(cudaGetLastError());
   return FC_OK;
 }
@@ -477,6 +493,13 @@ static void destroy(fc_forest* f) {
         for (double* p : f->peer_buf[r]) if (p) cudaIpcCloseMemHandle(p);
     cudaFree(f->d_sub_old); cudaFree(f->d_sub_snap); cudaFree(f->d_facc); cudaFree(f->d_lvl_cnt);
     for (auto* d : f->d_lvl) cudaFree(d);
+    for (auto& s : f->sub_fill) {
+      free_list(s.copy); free_list(s.avg); free_list(s.bcx); free_list(s.bcy); free_list(s.corner3);
+      for (auto& l : s.interp) free_list(l);
+      for (auto& l : s.bcx_l) free_list(l);
+      for (auto& l : s.bcy_l) free_list(l);
+      cudaFree(s.d_snap);
+    }
     if (f->h_cfl) cudaFreeHost(f->h_cfl);
     if (f->h_nact) cudaFreeHost(f->h_nact);
     free_list(f->copy); free_list(f->avg); free_list(f->bcx); free_list(f->bcy); free_list(f->corner3);
@@ -978,8 +1001,8 @@ int fc_run(fc_forest* f, double dt, int64_t nsteps, double* cfls, double* max_cf
 // Level l advances with dt_l = dt_coarse 2^-(l - glmin) in a coarse-to-fine recursion; the ghost
 // fill of level l at each of its start times runs on a snapshot in which coarser patches hold their
 // state interpolated linearly in time (exact dyadic weights from integer ticks).  Buffers: q_old =
-// the committed state (untouched until the commit), q_new = the working state (all levels at their
-// current times), d_sub_old = each level's state at the start of its current step, d_sub_snap = the
+// the committed state (untouched until the commit), q_new = the working state (each patch's
+// interior written by its level's first step; all levels at their current times), d_sub_old = each level's state at the start of its current step, d_sub_snap = the
 // snapshot with its rings (the ghost fill and the halo exchange run on it).
 static int sub_prepare(fc_forest* f) {
   if (f->sub_ready) return FC_OK;
@@ -1002,6 +1025,60 @@ static int sub_prepare(fc_forest* f) {
   }
   CK(cudaMalloc(&f->d_lvl_cnt, NL * sizeof(int32_t)));
   CK(cudaMemcpy(f->d_lvl_cnt, cnt.data(), NL * sizeof(int32_t), cudaMemcpyHostToDevice));
+  // Restricted fills (one rank; a remote coarse patch's ring would need its owner's closure): the
+  // level-l fill only has to produce the rings of D_l = the level-l patches plus, recursively, every
+  // patch an INTERP record of D_l reads (its ring feeds the slopes), and the snapshot only has to
+  // hold N_l = D_l plus every patch a record of D_l reads.  The records kept are exactly the full
+  // fill's records for D_l's cells, in the same order, so the rings of D_l are bitwise those of the
+  // full fill; other rings and snapshot cells are stale and nothing of level l reads them.
+  const char* full = std::getenv("FC_SUB_FULL_FILL");
+  if (f->pl.nranks == 1 && !(full && full[0] == '1')) {
+    const Plan& pl = f->pl;
+    const int64_t Pl = f->Pl, G = (int64_t)pl.n * pl.n - (int64_t)pl.m * pl.m;
+    auto sources = [&](int64_t lp, auto&& fn) {       // (op, source local patch) of lp's records
+      for (int64_t r = 0; r < G; ++r) {
+        const int32_t* o = pl.table.data() + (lp * G + r) * REC;
+        if (o[0] == OP_COPY || o[0] == OP_AVG4 || o[0] == OP_INTERP) fn(o[0], (int64_t)o[1] - pl.p0);
+      }
+    };
+    f->sub_fill.resize(NL);
+    for (int l = 0; l < NL; ++l) {
+      std::vector<uint8_t> D(Pl, 0), N(Pl, 0);
+      std::vector<int64_t> work(lists[l].begin(), lists[l].end());
+      for (int64_t lp : work) D[lp] = 1;
+      while (!work.empty()) {
+        const int64_t lp = work.back();
+        work.pop_back();
+        sources(lp, [&](int op, int64_t q) {
+          if (op == OP_INTERP && !D[q]) { D[q] = 1; work.push_back(q); }
+        });
+      }
+      std::vector<int32_t> snap;
+      for (int64_t lp = 0; lp < Pl; ++lp)
+        if (D[lp]) { N[lp] = 1; sources(lp, [&](int, int64_t q) { N[q] = 1; }); }
+      for (int64_t lp = 0; lp < Pl; ++lp) if (N[lp]) snap.push_back((int32_t)lp);
+      GhostLists gl;
+      std::string err;
+      int rc = plan_lists(pl, pl.meqn, gl, err, &D);
+      if (rc) return fail(rc, err);
+      FillLists& s = f->sub_fill[l];
+      if ((rc = to_dev(f, gl.copy, 2, s.copy)) || (rc = to_dev(f, gl.avg, 5, s.avg)) ||
+          (rc = to_dev(f, gl.bcx, 3, s.bcx)) || (rc = to_dev(f, gl.bcy, 3, s.bcy)) ||
+          (rc = to_dev(f, gl.corner3, 3, s.corner3)))
+        return rc;
+      s.interp.resize(gl.interp.size());
+      s.bcx_l.resize(gl.interp.size());
+      s.bcy_l.resize(gl.interp.size());
+      for (size_t k = 0; k < gl.interp.size(); ++k)
+        if ((rc = to_dev(f, gl.interp[k], 8, s.interp[k])) || (rc = to_dev(f, gl.bcx_l[k], 3, s.bcx_l[k])) ||
+            (rc = to_dev(f, gl.bcy_l[k], 3, s.bcy_l[k])))
+          return rc;
+      s.n_snap = (int64_t)snap.size();
+      CK(cudaMalloc(&s.d_snap, std::max<size_t>(1, snap.size()) * sizeof(int32_t)));
+      if (!snap.empty())
+        CK(cudaMemcpy(s.d_snap, snap.data(), snap.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+  }
   f->sub_ready = true;
   return FC_OK;
 }
@@ -1016,12 +1093,18 @@ static int sub_advance(fc_forest* f, int l, int64_t tick, int sub) {
   for (int c = f->glmin; c < l; ++c)
     alpha[c - f->glmin] = (double)(tick - f->sub_tick_old[c - f->glmin]) /
                           (double)(f->sub_tick_new[c - f->glmin] - f->sub_tick_old[c - f->glmin]);
-  f->st.kernel_launches += launch_sub_snapshot(f->qnew, f->d_sub_old, f->d_sub_snap, f->d_level, f->Pl, meqn, m, n2,
-                                               l, alpha, f->glmin, f->stream);
+  const FillLists* sel = f->sub_fill.empty() ? nullptr : &f->sub_fill[li];
+  // at tick 0 no patch has stepped yet: the current state is the committed one (and the weights
+  // of the coarser levels are 0), so q_new is never read before each patch's step has written it
+  f->st.kernel_launches += launch_sub_snapshot(tick == 0 ? f->qold : f->qnew, f->d_sub_old, f->d_sub_snap, f->d_level,
+                                               sel ? sel->d_snap : nullptr, sel ? sel->n_snap : f->Pl, meqn, m,
+                                               n2, l, alpha, f->glmin, f->stream);
   CK(cudaGetLastError());
   double* committed = f->qold;       // the ghost fill (and its halo exchange) runs on the snapshot
   f->qold = f->d_sub_snap;
+  f->fill_sel = sel;
   int rc = ghost_fill_internal(f);
+  f->fill_sel = nullptr;
   f->qold = committed;
   if (rc) return rc;
   if (f->n_lvl[li] > 0) {
@@ -1063,7 +1146,6 @@ int fc_step_subcycled(fc_forest* f, double dt_coarse, double* max_cfl) {
     CK(cudaMalloc(&f->d_facc, (size_t)std::max<int32_t>(1, f->nslots) * 4 * f->pl.m * f->pl.meqn * sizeof(double)));
   if (f->timing) CK(cudaEventRecord(f->ev[0], f->stream));
   CK(cudaMemsetAsync(f->d_cfl, 0, sizeof(unsigned long long), f->stream));
-  CK(cudaMemcpyAsync(f->qnew, f->qold, f->state_doubles * sizeof(double), cudaMemcpyDeviceToDevice, f->stream));
   f->sub_dt0 = dt_coarse;
   if ((rc = sub_advance(f, f->glmin, 0, 0))) return rc;
   if (f->timing) CK(cudaEventRecord(f->ev[2], f->stream));

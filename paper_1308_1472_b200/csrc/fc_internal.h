@@ -131,7 +131,8 @@ struct RingSources {
 // planner entry points (plan.cpp); return FC_OK or an FC_E* code with err set
 int plan_build(const fc_forest_desc* d, Plan& pl, std::string& err);
 // build typed lists for `meqn` (component stride n^2); halo slots from pl.halo
-int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err);
+int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err,
+               const std::vector<uint8_t>* dst_mask = nullptr);
 int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& err, bool p2p = false);
 // activity tables for the quiescent filter on any forest: nbr [Pl][8] / negmask [Pl] as in
 // RingSources; a patch with an AVG4 / INTERP / CORNER3 ghost record is always active (nbr[0] = -2)

@@ -378,7 +378,7 @@ int plan_build(const fc_forest_desc* d, Plan& pl, std::string& err) {
   return FC_OK;
 }
 
-int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err) {
+int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err, const std::vector<uint8_t>* dst_mask) {
   const int m = pl.m, n = pl.n;
   const int64_t n2 = (int64_t)n * n, S = (int64_t)meqn * n2;
   const int64_t Pl = pl.p1 - pl.p0, G = n2 - (int64_t)m * m;
@@ -400,6 +400,7 @@ int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err) {
     return (int32_t)((Pl + h / n2) * S + h % n2);
   };
   for (int64_t lp = 0; lp < Pl; ++lp) {
+    if (dst_mask && !(*dst_mask)[lp]) continue;   // (sub-cycling: only the rings a level fill needs)
     const int lvl = pl.leaves[pl.p0 + lp].level;
     int r = 0;
     for (int j = -1; j <= m + 2; ++j)

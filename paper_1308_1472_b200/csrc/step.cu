@@ -1311,12 +1311,13 @@ struct SubAlpha {
   int lmin;
 };
 __global__ void k_sub_snapshot(const double* __restrict__ cur, double* __restrict__ old, double* __restrict__ snap,
-                               const int8_t* __restrict__ level, int64_t P, int meqn, int mm, int n2, int l,
-                               SubAlpha al) {
+                               const int8_t* __restrict__ level, const int32_t* __restrict__ list, int64_t P,
+                               int meqn, int mm, int n2, int l, SubAlpha al) {
   const int64_t per = (int64_t)meqn * mm, tot = P * per;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = t / per;
-    const int r = (int)(t - p * per), k = r / mm, c = r - k * mm;
+    const int64_t i = t / per;
+    const int r = (int)(t - i * per), k = r / mm, c = r - k * mm;
+    const int64_t p = list ? (int64_t)list[i] : i;
     const int64_t o = (p * meqn + k) * n2 + c;     // dense interior (qcell)
     const int lp = level[p];
     if (lp >= l) {
@@ -1346,13 +1347,13 @@ __global__ void k_sub_accumulate(const int32_t* __restrict__ list, int64_t n, co
   }
 }
 
-int launch_sub_snapshot(const double* cur, double* old, double* snap, const int8_t* level, int64_t P, int meqn,
-                        int m, int n2, int l, const double* alpha, int lmin, cudaStream_t st) {
+int launch_sub_snapshot(const double* cur, double* old, double* snap, const int8_t* level, const int32_t* list,
+                        int64_t P, int meqn, int m, int n2, int l, const double* alpha, int lmin, cudaStream_t st) {
   if (P <= 0) return 0;
   SubAlpha al;
   for (int i = 0; i < 32; ++i) al.a[i] = alpha[i];
   al.lmin = lmin;
-  k_sub_snapshot<<<148 * 8, 256, 0, st>>>(cur, old, snap, level, P, meqn, m * m, n2, l, al);
+  k_sub_snapshot<<<148 * 8, 256, 0, st>>>(cur, old, snap, level, list, P, meqn, m * m, n2, l, al);
   return 1;
 }
 

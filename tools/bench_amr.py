@@ -5,7 +5,7 @@ within 0.25 of (0.5, 0.5)).  For each mode: device time (CUDA events on the libr
 advance the solution by one coarse dt = 2 fine dt, i.e. 2 x fc_step(dt_f) or 1 x
 fc_step_subcycled(2 dt_f), averaged over K such intervals after W warm-ups.
 
-    python tools/bench_amr.py [--base 8] [--m 16] [--steps 20] [--warmup 3]
+    python tools/bench_amr.py [--base 8] [--m 16] [--steps 20] [--warmup 3] [--radius 0.25]
 """
 import argparse
 import json
@@ -21,18 +21,19 @@ def main():
     ap.add_argument("--m", type=int, default=16)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--radius", type=float, default=0.25, help="refined disc radius of the C2 rule")
     a = ap.parse_args()
     import numpy as np
     import torch
     from paper_1308_1472_b200 import fc
     from workloads.configs import c2
-    w = c2(base_level=a.base, m=a.m)
+    w = c2(base_level=a.base, m=a.m, radius=a.radius)
     lv = w.forest.levels
     cells = w.num_patches * a.m * a.m
     fine_cells = int((lv == lv.max()).sum()) * a.m * a.m
     stream = torch.cuda.current_stream()
     dtf = w.dt0
-    out = {"workload": f"T2: C2 physics, L{a.base}/L{a.base + 1}, m={a.m}", "patches": w.num_patches, "cells": cells,
+    out = {"workload": f"T2: C2 physics, L{a.base}/L{a.base + 1}, m={a.m}, radius {a.radius}", "patches": w.num_patches, "cells": cells,
            "fine_cells": fine_cells}
     for mode in ("global", "subcycled"):
         for reflux in (0, 1):
