@@ -38,16 +38,17 @@ def _deps():
         glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "fc.h"), __file__]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    lib = out or LIB
+    if not force and os.path.exists(lib):
+        t = os.path.getmtime(lib)
         if all(os.path.getmtime(d) <= t for d in _deps()):
-            return LIB
+            return lib
     inc, libdir = nccl_dirs()
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
            "-cudart", "static", f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}",
-           "-Xptxas", "-v" if verbose else "-O3",
+           "-Xptxas", "-v" if verbose else "-O3", *[f"-D{d}" for d in defines],
            "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES] + \
           [f"-L{libdir}", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{libdir}"]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -56,10 +57,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libfc.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv)
-    print(LIB)
+    # tuning builds: --define NAME=VALUE ... --out PATH (FC_LIB_PATH=PATH loads it)
+    defs = [sys.argv[i + 1] for i, a in enumerate(sys.argv) if a == "--define"]
+    outs = [sys.argv[i + 1] for i, a in enumerate(sys.argv) if a == "--out"]
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, defines=defs,
+                out=outs[0] if outs else None))

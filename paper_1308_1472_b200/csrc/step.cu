@@ -103,6 +103,9 @@ __device__ __forceinline__ int opaque(int x) {
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -984,6 +987,302 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// Constant-velocity scalar advection (the C1/C2/T1/T2 physics), register sweep.  With the same
+// speeds (u, v) on every edge, the parts k_step_sc gathers per cell regroup as
+//   q_new = q - r [ Xf + Yf + k_right (Y - Y_{i-1}) + k_left (Y_{i+1} - Y)
+//                           + k_up (X - X_{j-1}) + k_down (X_{j+1} - X) ]
+// where, per cell, Xf = dqR(i-1/2) + dqL(i+1/2) are the parts of its two x-edges that enter it
+// (A+dq - F~ from the left edge, A-dq + F~ from the right one), X the same with the correction
+// weighted by (method3 == 2) (what the transverse solve splits), Yf / Y along y, r = dt / dx and
+// k_* = -r/2 max/min(u or v, 0) (0 without transverse terms): the same sums, re-associated
+// (reading 24).  A warp holds PW = 32 / LP patches, LP = T/2 + 1 lanes each; lane k of a
+// patch owns columns 2k, 2k+1 (0..T+1) and sweeps rows 0..T+1 once with its columns' 4-row windows,
+// the X of the two rows below and the last y-edge's parts in registers; a neighbouring column's
+// parts come by shuffle.  Every edge is computed once, by one lane; no shared-memory scratch and
+// no barrier in the sweep.  Each CTA is one warp with its own double-buffered staging (whole
+// padded patches by one bulk copy each, or, on the fused ring path, the interior rows by bulk copy
+// and the ring by cp.async from the sources) into the natural (T+4)^2 window, so that a lane's
+// reads are fixed offsets from its columns' base addresses.
+#ifndef CV_UNROLL
+#define CV_UNROLL 0
+#endif
+#ifndef CV_ILIM
+#define CV_ILIM 0
+#endif
+template <int T>
+struct CvShape {
+  static constexpr int W = T + 4, WW = W * W, LP = T / 2 + 1, PW = 32 / LP;
+};
+
+template <int T, int SX, int SY, bool MT2, int NB>
+__global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
+  using C = CvShape<T>;
+  constexpr int W = C::W, WW = C::WW, LP = C::LP, PW = C::PW, G = WW - T * T;
+  extern __shared__ __align__(128) double sm[];     // [NB][PW][WW]
+  __shared__ __align__(8) uint64_t bars[NB];
+  const int lane = threadIdx.x;
+  if (A.active) npatch = *A.nactive;
+  const int ngroups = (npatch + PW - 1) / PW;
+  const bool ring = A.ring != nullptr;
+  auto patch_of = [&](int idx) { return A.active ? A.active[idx] : idx; };
+  auto stage = [&](int g, int s) {
+    double* buf = sm + (size_t)s * PW * WW;
+    const int i0 = g * PW, cnt = min(PW, npatch - i0);
+    if (lane == 0)
+      mbar_expect_tx(&bars[s], (uint32_t)cnt * (ring ? T * T : T * T + 4 * W) * (uint32_t)sizeof(double));
+    __syncwarp();
+    if (!ring) {   // padded patch (dense interior, then the ring) -> natural window: interior rows and
+                   // the two ghost-row pairs by bulk copy, the side pairs of rows 1..T by 16-byte cp.async
+      const int mp = lane < cnt ? patch_of(i0 + lane) : 0;
+#pragma unroll
+      for (int q = 0; q < PW; ++q) {
+        const int patch = __shfl_sync(0xffffffffu, mp, q);
+        if (q >= cnt) break;
+        const double* qb = A.qold + (int64_t)patch * WW;
+        double* b = buf + q * WW;
+        if (lane < T) bulk_g2s(b + (lane + 2) * W + 2, qb + lane * T, T * sizeof(double), &bars[s]);
+        else if (lane == T) bulk_g2s(b, qb + T * T, 2 * W * sizeof(double), &bars[s]);
+        else if (lane == T + 1) bulk_g2s(b + (T + 2) * W, qb + T * T + 2 * W + 4 * T, 2 * W * sizeof(double), &bars[s]);
+        if (lane < 2 * T) {
+          const int j = 1 + (lane >> 1), side = lane & 1;
+          cp_async16(b + (j + 1) * W + (side ? T + 2 : 0), qb + T * T + 2 * W + 4 * (j - 1) + 2 * side);
+        }
+      }
+      cp_async_commit();
+      return;
+    }
+    // fused ring gather: all the group's source offsets are loaded first (one latency, not one per
+    // patch), then the interior rows go by bulk copy and the ring cells by cp.async
+    constexpr int NR = (G + 31) / 32;
+    int pt[PW];
+    int32_t src[PW][NR];
+    uint8_t own[PW][NR];
+#pragma unroll
+    for (int q = 0; q < PW; ++q) pt[q] = q < cnt ? patch_of(i0 + q) : -1;
+#pragma unroll
+    for (int q = 0; q < PW; ++q)
+#pragma unroll
+      for (int t = 0; t < NR; ++t) {
+        const int r = lane + 32 * t;
+        const bool ok = pt[q] >= 0 && r < G;
+        src[q][t] = ok ? __ldg(A.ring + (int64_t)pt[q] * G + r) : -1;
+        own[q][t] = (ok && A.rpeer) ? __ldg(A.rpeer + (int64_t)pt[q] * G + r) : 0;
+      }
+#pragma unroll
+    for (int q = 0; q < PW; ++q) {
+      if (pt[q] < 0) continue;
+      double* b = buf + q * WW;
+      if (lane < T) bulk_g2s(b + (lane + 2) * W + 2, A.qold + (int64_t)pt[q] * WW + lane * T, T * sizeof(double), &bars[s]);
+#pragma unroll
+      for (int t = 0; t < NR; ++t) {
+        const int r = lane + 32 * t;
+        if (src[q][t] >= 0) cp_async8(b + ring_window_index<T>(r), (own[q][t] ? A.peerq[own[q][t] - 1] : A.qold) + src[q][t]);
+      }
+    }
+    cp_async_commit();
+  };
+  if (lane == 0) {
+    for (int q = 0; q < NB; ++q) mbar_init(&bars[q], 1);
+    fence_proxy_async();
+  }
+  __syncwarp();
+  for (int q = 0; q < (NB > 1 ? NB - 1 : 1); ++q) {
+    const int g = blockIdx.x + q * gridDim.x;
+    if (g < ngroups) stage(g, q);
+    else cp_async_commit();
+  }
+  // lane -> (patch slot, columns c0 = 2k, c0 + 1); the 5 columns it reads: c0 - 1 .. c0 + 3 (the
+  // last clamped into the window: it only feeds the unused edge T + 3/2)
+  const int p = lane / LP, k = lane - p * LP, c0 = 2 * k;
+  const double u0 = A.sp.p0, v0 = A.sp.p1;
+  const bool trans = A.method3 >= 1, second = A.method2 == 2;
+  const double lc1 = A.lim.c1, lc2 = A.lim.c2, lc3 = A.lim.c3, lc4 = A.lim.c4;
+  // phi(wi / w) w of the MC / minmod limiter (launched for those only), division- and branch-free:
+  // with s the sign of w, s max(0, min(s (c1 w + c2 wi), c3 |w|, s c4 wi)) (s x: a sign-bit flip)
+#if CV_ILIM
+  // the min / max on the bit patterns as signed 64-bit integers: the order of non-negative doubles,
+  // and every negative double (sign bit set) is a negative integer, clamped to +0
+  auto limited = [&](double w, double wi) {
+    const long long sw = __double_as_longlong(w) & (long long)0x8000000000000000ull;
+    const long long a = __double_as_longlong(fma(lc1, w, lc2 * wi)) ^ sw;
+    const long long c = __double_as_longlong(lc4 * wi) ^ sw;
+    const long long b = __double_as_longlong(lc3 * fabs(w));
+    long long mm = a < b ? a : b;
+    mm = mm < c ? mm : c;
+    mm = mm > 0 ? mm : 0;
+    return __longlong_as_double(mm ^ sw);
+  };
+#else
+  auto limited = [&](double w, double wi) {
+    const long long sw = __double_as_longlong(w) & (long long)0x8000000000000000ull;
+    const double a = __longlong_as_double(__double_as_longlong(fma(lc1, w, lc2 * wi)) ^ sw);
+    const double c = __longlong_as_double(__double_as_longlong(lc4 * wi) ^ sw);
+    const double b = lc3 * fabs(w);
+    double mm = a < b ? a : b;
+    mm = mm < c ? mm : c;
+    mm = mm > 0.0 ? mm : 0.0;
+    return __longlong_as_double(__double_as_longlong(mm) ^ sw);
+  };
+#endif
+  double cfl = 0.0;
+  double chk = 0.0;                     // sum of 0 * q_new: NaN iff some q_new is not finite
+  int it = 0;
+  for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
+    const int b = it % NB;
+    const int cnt = min(PW, npatch - g * PW);
+    // this group's patch ids, levels and boundary flags (loads in flight during the wait)
+    const int mypatch = lane < cnt ? patch_of(g * PW + lane) : 0;
+    const int mylevel = A.level[mypatch];
+    const int mybc = (ring && lane < cnt) ? A.bcflag[mypatch] : 0;
+    mbar_wait(&bars[b], (uint32_t)((it / NB) & 1));
+    cp_async_wait<(NB > 1 ? NB - 2 : 0)>();
+    __syncwarp();
+    // the next group's staging: NB - 1 groups ahead, or (NB = 1) after this group's sweep
+    auto issue_next = [&]() {
+      const int gn = g + (NB > 1 ? NB - 1 : 1) * gridDim.x, bn = (it + NB - 1) % NB;
+      if (gn < ngroups) {
+        fence_proxy_async();
+        stage(gn, bn);
+      } else {
+        cp_async_commit();
+      }
+    };
+    if (NB > 1) issue_next();
+    double* gbuf = sm + (size_t)b * PW * WW;
+    if (ring) {   // physical-boundary ring cells: x faces, then y faces
+      for (unsigned todo = __ballot_sync(0xffffffffu, mybc != 0); todo; todo &= todo - 1) {
+        const int q = __ffs(todo) - 1;
+        const int patch = __shfl_sync(0xffffffffu, mypatch, q);
+        const int bc = __shfl_sync(0xffffffffu, mybc, q);
+        const int32_t* rs = A.ring + (int64_t)patch * G;
+        double* sq = gbuf + q * WW;
+        for (int is_y = 0; is_y < 2; ++is_y) {
+          if (!(bc & (1 << is_y))) continue;
+          for (int r = lane; r < G; r += 32) {
+            const int32_t v = __ldg(rs + r);
+            if (v >= 0) continue;
+            const int code = -1 - v;
+            if ((code & 1) != is_y) continue;
+            sq[ring_window_index<T>(r)] = sq[code >> 3];   // (one component: no momentum to negate)
+          }
+          __syncwarp();
+        }
+      }
+    }
+    const bool live = p < cnt;
+    const int patch = __shfl_sync(0xffffffffu, mypatch, live ? p : 0);
+    const int level = __shfl_sync(0xffffffffu, mylevel, live ? p : 0);
+    const double* sq = gbuf + (live ? p : 0) * WW;
+    const double* col[5];   // column c0 - 1 + e of window row -1
+#pragma unroll
+    for (int e = 0; e < 5; ++e) col[e] = sq + min(c0 - 1 + e, T + 2) + 1;
+    auto ld = [&](int e, int j) { return col[e][(j + 1) * W]; };
+    const double r = A.dt / ldexp(A.dx0, -level);
+    if (live) cfl = fmax(cfl, fmax(fmax(r * u0, -r * u0), fmax(r * v0, -r * v0)));
+    const double cfx = second ? 0.5 * fabs(u0) * (1.0 - fabs(u0) * r) : 0.0;
+    const double cfy = second ? 0.5 * fabs(v0) * (1.0 - fabs(v0) * r) : 0.0;
+    const double ht = trans ? -0.5 * r : 0.0;
+    // k_up / k_down / k_left / k_right with the signs fixed by SX, SY
+    const double kx = ht * u0, ky = ht * v0;   // (SX > 0: k_right = kx, k_left = 0; SX < 0: k_left = kx)
+    const double m3 = A.method3 == 2 ? 1.0 : 0.0;
+    double* out = A.qnew + (int64_t)patch * WW;
+    // edge parts: dqL (into the low cell), dqR (into the high cell), xl / xr (their transverse
+    // parts: the correction weighted by m3)
+    auto edge = [&](double w, double wi, double s, double cf, double& dL, double& dR, double& xl, double& xr,
+                    auto sgn) {
+      constexpr int SG = decltype(sgn)::value;
+      const double f = cf * limited(w, wi);
+      if (SG > 0) {
+        dL = f;
+        dR = fma(s, w, -f);
+        if (MT2) { xl = dL; xr = dR; }
+        else { xl = m3 * f; xr = fma(s, w, -(m3 * f)); }
+      } else {
+        dL = fma(s, w, f);
+        dR = -f;
+        if (MT2) { xl = dL; xr = dR; }
+        else { xl = fma(s, w, m3 * f); xr = -(m3 * f); }
+      }
+    };
+    using SXc = std::integral_constant<int, SX>;
+    using SYc = std::integral_constant<int, SY>;
+    double qa[4], qb[4];                  // columns c0, c0 + 1: rows j-1 .. j+2
+    qa[1] = ld(1, -1); qa[2] = ld(1, 0); qa[3] = ld(1, 1);
+    qb[1] = ld(2, -1); qb[2] = ld(2, 0); qb[3] = ld(2, 1);
+    qa[0] = qb[0] = 0.0;
+    double Xa1 = 0, Xa2 = 0, Xb1 = 0, Xb2 = 0;       // X(c, j-1), X(c, j-2)
+    double Xfa = 0, Xfb = 0;                         // Xf(c, j-1)
+    double Ya = 0, Yb = 0, Yl = 0, Yr = 0, Yfa = 0, Yfb = 0;   // Y(c0 / c0+1 / c0-1 / c0+2, j-1), Yf
+    double yra = 0, yrb = 0, dRya = 0, dRyb = 0, wya = 0, wyb = 0;   // last y-edge's parts, its jump
+    // one row j of the sweep; F: which parts exist at this j (peeled first / last rows)
+    constexpr int LD = 1, UPD = 2, YE = 4, YS = 8, J0 = 16;
+    auto iter = [&](int j, auto flags) {
+      constexpr int F = decltype(flags)::value;
+      qa[0] = qa[1]; qa[1] = qa[2]; qa[2] = qa[3];
+      qb[0] = qb[1]; qb[1] = qb[2]; qb[2] = qb[3];
+      if (F & LD) { qa[3] = ld(1, j + 2); qb[3] = ld(2, j + 2); }
+      // x-edges c0 + 1/2 and c0 + 3/2 of row j
+      const double qm = ld(0, j), qc = ld(3, j), qd = ld(4, j);
+      const double w0 = qb[1] - qa[1], w1 = qc - qb[1];
+      const double wi0 = SX > 0 ? qa[1] - qm : w1, wi1 = SX > 0 ? w0 : qd - qc;
+      double dL0, dR0, xl0, xr0, dL1, dR1, xl1, xr1;
+      edge(w0, wi0, u0, cfx, dL0, dR0, xl0, xr0, SXc{});
+      edge(w1, wi1, u0, cfx, dL1, dR1, xl1, xr1, SXc{});
+      const double xrL = __shfl_up_sync(0xffffffffu, xr1, 1);
+      const double dRL = MT2 ? xrL : __shfl_up_sync(0xffffffffu, dR1, 1);
+      const double Xa = xrL + xl0, Xb = xr0 + xl1;
+      const double Xfa0 = MT2 ? Xa : dRL + dL0, Xfb0 = MT2 ? Xb : dR0 + dL1;
+      if (F & UPD) {   // update of row j - 1
+        const int jr = j - 1;
+        const double ta = Xfa + Yfa + (SX > 0 ? kx * (Ya - Yl) : kx * (Yb - Ya)) +
+                          (SY > 0 ? ky * (Xa1 - Xa2) : ky * (Xa - Xa1));
+        const double tb = Xfb + Yfb + (SX > 0 ? kx * (Yb - Ya) : kx * (Yr - Yb)) +
+                          (SY > 0 ? ky * (Xb1 - Xb2) : ky * (Xb - Xb1));
+        const double va = fma(-r, ta, qa[0]), vb = fma(-r, tb, qb[0]);
+        if (live && c0 >= 1) out[(jr - 1) * T + c0 - 1] = va;
+        if (live && c0 + 1 <= T) out[(jr - 1) * T + c0] = vb;
+        chk = fma(va, 0.0, fma(vb, 0.0, chk));
+      }
+      if (F & YE) {    // y-edges (c, j + 1/2)
+        const double wa = qa[2] - qa[1], wb = qb[2] - qb[1];
+        const double wia = SY > 0 ? ((F & J0) ? qa[1] - qa[0] : wya) : qa[3] - qa[2];
+        const double wib = SY > 0 ? ((F & J0) ? qb[1] - qb[0] : wyb) : qb[3] - qb[2];
+        double dLa, dRa, yla, yra_, dLb, dRb, ylb, yrb_;
+        edge(wa, wia, v0, cfy, dLa, dRa, yla, yra_, SYc{});
+        edge(wb, wib, v0, cfy, dLb, dRb, ylb, yrb_, SYc{});
+        if (F & YS) {
+          Ya = yra + yla; Yb = yrb + ylb;
+          Yfa = MT2 ? Ya : dRya + dLa; Yfb = MT2 ? Yb : dRyb + dLb;
+          Yl = __shfl_up_sync(0xffffffffu, Yb, 1);
+          Yr = __shfl_down_sync(0xffffffffu, Ya, 1);
+        }
+        yra = yra_; yrb = yrb_; dRya = dRa; dRyb = dRb; wya = wa; wyb = wb;
+      }
+      Xa2 = Xa1; Xa1 = Xa; Xb2 = Xb1; Xb1 = Xb; Xfa = Xfa0; Xfb = Xfb0;
+    };
+    iter(0, std::integral_constant<int, LD | YE | J0>{});
+    iter(1, std::integral_constant<int, LD | YE | YS>{});
+#if CV_UNROLL == 1
+#pragma unroll 1
+#elif CV_UNROLL == 2
+#pragma unroll 2
+#elif CV_UNROLL == 3
+#pragma unroll 3
+#else
+#pragma unroll
+#endif
+    for (int j = 2; j <= T; ++j) iter(j, std::integral_constant<int, LD | UPD | YE | YS>{});
+    iter(T + 1, std::integral_constant<int, UPD>{});
+    __syncwarp();   // the staging buffer is refilled by a later group
+    if (NB == 1) issue_next();
+  }
+  const bool bad = __any_sync(0xffffffffu, chk != chk);
+  if (bad || cfl != cfl) cfl = __longlong_as_double(0x7ff0000000000000ll);
+  for (int o = 16; o > 0; o >>= 1) cfl = fmax(cfl, __shfl_xor_sync(0xffffffffu, cfl, o));
+  if (lane == 0) atomicMax(A.cfl_bits, (unsigned long long)__double_as_longlong(cfl));
+}
+
+// ---------------------------------------------------------------------------------------------
 // Quiescent-patch filter for the fused (ring-gather) path, three kernels per step:
 //   k_copy_classify  q_new interior = q_old interior (streaming, 16-byte accesses) and, per patch,
 //                    "interior uniform" + its state;
@@ -1187,6 +1486,42 @@ static int launch_sc_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   return 1;
 }
 
+#ifndef CV_NB
+#define CV_NB 1
+#endif
+template <int T, int SX, int SY, bool MT2>
+static int launch_cv_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  constexpr int NB = CV_NB;
+  using C = CvShape<T>;
+  const size_t smem = (size_t)NB * C::PW * C::WW * sizeof(double);
+  static int resident = 0;
+  if (!resident) {
+    cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_cv<T, SX, SY, MT2, NB>, 32, smem);
+    resident = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  if (npatch >= (1ll << 31)) return -1;
+  const int64_t groups = (npatch + C::PW - 1) / C::PW;
+  const int64_t grid = groups < resident ? groups : resident;
+  k_step_cv<T, SX, SY, MT2, NB><<<(unsigned)grid, 32, smem, st>>>(a, (int)npatch);
+  return 1;
+}
+
+template <int T>
+static int launch_cv(const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  const bool px = a.sp.p0 > 0.0, py = a.sp.p1 > 0.0, mt2 = a.method3 == 2;
+  if (mt2) {
+    if (px) return py ? launch_cv_t<T, 1, 1, true>(a, npatch, st) : launch_cv_t<T, 1, -1, true>(a, npatch, st);
+    return py ? launch_cv_t<T, -1, 1, true>(a, npatch, st) : launch_cv_t<T, -1, -1, true>(a, npatch, st);
+  }
+  if (px) return py ? launch_cv_t<T, 1, 1, false>(a, npatch, st) : launch_cv_t<T, 1, -1, false>(a, npatch, st);
+  return py ? launch_cv_t<T, -1, 1, false>(a, npatch, st) : launch_cv_t<T, -1, -1, false>(a, npatch, st);
+}
+
 template <class S, int T>
 static int launch_sc(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   return a.rslot ? launch_sc_t<S, T, true>(a, npatch, st) : launch_sc_t<S, T, false>(a, npatch, st);
@@ -1204,6 +1539,15 @@ static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   static const int env_mb = getenv("FC_STEP_MINB") ? atoi(getenv("FC_STEP_MINB")) : 0;
   // scalar solvers: the two-phase kernel (FC_SCALAR_PHASED=1 keeps the generic phased k_step)
   static const bool phased = getenv("FC_SCALAR_PHASED") && atoi(getenv("FC_SCALAR_PHASED"));
+  // constant-velocity advection on whole 8 x 8 / 16 x 16 patches: the register-sweep kernel
+  // (FC_SCALAR_CV=0 keeps k_step_sc; reflux records are written by k_step_sc)
+  static const bool cv = !(getenv("FC_SCALAR_CV") && atoi(getenv("FC_SCALAR_CV")) == 0);
+  if constexpr (std::is_same<S, AdvConst>::value) {
+    if (cv && !phased && !a.rslot && a.tiles == 1 && a.limiter != 0) {
+      if (a.m == 16) return launch_cv<16>(a, npatch, st);
+      if (a.m == 8) return launch_cv<8>(a, npatch, st);
+    }
+  }
   if constexpr (S::MEQN == 1) {
     if (!phased) {
       if (a.m % 16 == 0) return launch_sc<S, 16>(a, npatch, st);

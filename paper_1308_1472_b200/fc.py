@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfc.so")
+LIB_PATH = os.environ.get("FC_LIB_PATH") or os.path.join(HERE, "libfc.so")   # (override: tuning builds)
 
 FC_OK, FC_EINVAL, FC_ETILING, FC_ECONN, FC_EBALANCE, FC_ECUDA, FC_ENCCL, FC_ENOMEM, FC_ESTATE, \
     FC_ECFL, FC_ENONFINITE, FC_EUNSUP = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9, -10, -11

@@ -99,3 +99,16 @@ def test_one_level_subcycling_is_fc_step():
     qb, cb, _ = fc.run_subcycled(w)
     np.testing.assert_array_equal(qa, qb)
     np.testing.assert_array_equal(ca, cb)
+
+
+@pytest.mark.parametrize("w", [CASES[1], CASES[3], CASES[4]], ids=lambda w: w.name)
+def test_per_level_fills_bitwise_equal_whole_forest_fills(w, monkeypatch):
+    """The restricted per-level ghost fills and snapshots (the default on one rank) produce the
+    same state bitwise as whole-forest passes (FC_SUB_FULL_FILL=1, read when a handle first
+    sub-cycles): the records kept for the cells level l reads are the full fill's, in order."""
+    w = dataclasses.replace(w, reflux=1)
+    qa, ca, _ = fc.run_subcycled(w)
+    monkeypatch.setenv("FC_SUB_FULL_FILL", "1")
+    qb, cb, _ = fc.run_subcycled(w)
+    np.testing.assert_array_equal(qa, qb)
+    np.testing.assert_array_equal(ca, cb)
