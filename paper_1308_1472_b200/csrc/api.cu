@@ -37,8 +37,8 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
 int launch_reflux(const int32_t* cells, int64_t ncells, const double* freg, const double* ffine, double* qnew,
                   const double* aux, const int8_t* level, double wc, double dtr, double dx0, int meqn, int n2,
                   cudaStream_t st);
-int launch_sub_snapshot(const double* cur, double* old, double* snap, const int8_t* level, const int32_t* list,
-                        int64_t P, int meqn,
+int launch_sub_snapshot(const double* cur, double* old, const double* old0, double* snap, const int8_t* level,
+                        const int32_t* list, int64_t P, int meqn,
                         int m, int n2, int l, const double* alpha, int lmin, cudaStream_t st);
 int launch_sub_accumulate(const int32_t* list, int64_t n, const int32_t* rslot, const double* rec, double* acc,
                           int fs, double dt, int add, cudaStream_t st);
@@ -1094,21 +1094,28 @@ static int sub_advance(fc_forest* f, int l, int64_t tick, int sub) {
     alpha[c - f->glmin] = (double)(tick - f->sub_tick_old[c - f->glmin]) /
                           (double)(f->sub_tick_new[c - f->glmin] - f->sub_tick_old[c - f->glmin]);
   const FillLists* sel = f->sub_fill.empty() ? nullptr : &f->sub_fill[li];
-  // at tick 0 no patch has stepped yet: the current state is the committed one (and the weights
-  // of the coarser levels are 0), so q_new is never read before each patch's step has written it
-  f->st.kernel_launches += launch_sub_snapshot(tick == 0 ? f->qold : f->qnew, f->d_sub_old, f->d_sub_snap, f->d_level,
-                                               sel ? sel->d_snap : nullptr, sel ? sel->n_snap : f->Pl, meqn, m,
-                                               n2, l, alpha, f->glmin, f->stream);
-  CK(cudaGetLastError());
+  // The coarsest level steps once, from the committed state: its fill runs on q_old itself (whose
+  // rings are scratch) and q_old doubles as its start-of-step state, so no snapshot is taken.
+  // Finer levels: at tick 0 no patch has stepped yet, the current state is the committed one (and
+  // the weights of the coarser levels are 0), so q_new is never read before each patch's step has
+  // written it.
+  const bool coarsest = l == f->glmin;
+  if (!coarsest) {
+    f->st.kernel_launches += launch_sub_snapshot(tick == 0 ? f->qold : f->qnew, f->d_sub_old, f->qold, f->d_sub_snap,
+                                                 f->d_level, sel ? sel->d_snap : nullptr, sel ? sel->n_snap : f->Pl,
+                                                 meqn, m, n2, l, alpha, f->glmin, f->stream);
+    CK(cudaGetLastError());
+  }
   double* committed = f->qold;       // the ghost fill (and its halo exchange) runs on the snapshot
-  f->qold = f->d_sub_snap;
+  double* src = coarsest ? f->qold : f->d_sub_snap;
+  f->qold = src;
   f->fill_sel = sel;
   int rc = ghost_fill_internal(f);
   f->fill_sel = nullptr;
   f->qold = committed;
   if (rc) return rc;
   if (f->n_lvl[li] > 0) {
-    int lr = launch_step(p.kind, f->d_sub_snap, f->qnew, f->aux, f->d_level, f->n_lvl[li], m, dt, f->pl.dx0, p.p0,
+    int lr = launch_step(p.kind, src, f->qnew, f->aux, f->d_level, f->n_lvl[li], m, dt, f->pl.dx0, p.p0,
                          p.p1, p.limiter, p.method2, p.method3, p.skip_quiescent, nullptr, f->d_bcflag, f->d_lvl[li],
                          f->d_lvl_cnt + li, f->d_cfl, reflux ? f->d_rslot : nullptr, reflux ? f->d_freg : nullptr,
                          nullptr, nullptr, f->stream);

@@ -1014,7 +1014,7 @@ struct CvShape {
   static constexpr int W = T + 4, WW = W * W, LP = T / 2 + 1, PW = 32 / LP;
 };
 
-template <int T, int SX, int SY, bool MT2, int NB>
+template <int T, int SX, int SY, bool MT2, int NB, bool RF>
 __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
   using C = CvShape<T>;
   constexpr int W = C::W, WW = C::WW, LP = C::LP, PW = C::PW, G = WW - T * T;
@@ -1133,6 +1133,7 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
     // this group's patch ids, levels and boundary flags (loads in flight during the wait)
     const int mypatch = lane < cnt ? patch_of(g * PW + lane) : 0;
     const int mylevel = A.level[mypatch];
+    const int myslot = RF ? A.rslot[mypatch] : -1;
     const int mybc = (ring && lane < cnt) ? A.bcflag[mypatch] : 0;
     mbar_wait(&bars[b], (uint32_t)((it / NB) & 1));
     cp_async_wait<(NB > 1 ? NB - 2 : 0)>();
@@ -1172,6 +1173,9 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
     const bool live = p < cnt;
     const int patch = __shfl_sync(0xffffffffu, mypatch, live ? p : 0);
     const int level = __shfl_sync(0xffffffffu, mylevel, live ? p : 0);
+    const int slot = RF ? __shfl_sync(0xffffffffu, myslot, live ? p : 0) : -1;
+    const bool rec = RF && live && slot >= 0;   // reflux records: applied face fluxes, outward
+    double* reg = RF ? A.freg + (int64_t)(slot < 0 ? 0 : slot) * 4 * T : nullptr;   // [face][T]
     const double* sq = gbuf + (live ? p : 0) * WW;
     const double* col[5];   // column c0 - 1 + e of window row -1
 #pragma unroll
@@ -1214,6 +1218,7 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
     double Xfa = 0, Xfb = 0;                         // Xf(c, j-1)
     double Ya = 0, Yb = 0, Yl = 0, Yr = 0, Yfa = 0, Yfb = 0;   // Y(c0 / c0+1 / c0-1 / c0+2, j-1), Yf
     double yra = 0, yrb = 0, dRya = 0, dRyb = 0, wya = 0, wyb = 0;   // last y-edge's parts, its jump
+    double dR0p = 0, dL0p = 0, dRh_a = 0, dRh_b = 0, dLt_a = 0, dLt_b = 0;   // (reflux records only)
     // one row j of the sweep; F: which parts exist at this j (peeled first / last rows)
     constexpr int LD = 1, UPD = 2, YE = 4, YS = 8, J0 = 16;
     auto iter = [&](int j, auto flags) {
@@ -1242,6 +1247,18 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
         if (live && c0 >= 1) out[(jr - 1) * T + c0 - 1] = va;
         if (live && c0 + 1 <= T) out[(jr - 1) * T + c0] = vb;
         chk = fma(va, 0.0, fma(vb, 0.0, chk));
+        if (RF && rec) {   // the same face fluxes k_step_sc records (F~ / G~ transverse at the face)
+          if (k == 0) reg[jr - 1] = (dR0p - kx * (SX > 0 ? Ya : Yb)) - u0 * qb[0];                 // x-low, i = 1
+          if (k == LP - 1) reg[T + jr - 1] = u0 * qa[0] + (dL0p + kx * (SX > 0 ? Ya : Yb));       // x-high, i = T
+          if (jr == 1) {                                                                          // y-low, j = 1
+            if (c0 >= 1) reg[2 * T + c0 - 1] = (dRh_a - ky * (SY > 0 ? Xa2 : Xa1)) - v0 * qa[0];
+            if (c0 + 1 <= T) reg[2 * T + c0] = (dRh_b - ky * (SY > 0 ? Xb2 : Xb1)) - v0 * qb[0];
+          }
+          if (jr == T) {                                                                          // y-high, j = T
+            if (c0 >= 1) reg[3 * T + c0 - 1] = v0 * qa[0] + (dLt_a + ky * (SY > 0 ? Xa1 : Xa));
+            if (c0 + 1 <= T) reg[3 * T + c0] = v0 * qb[0] + (dLt_b + ky * (SY > 0 ? Xb1 : Xb));
+          }
+        }
       }
       if (F & YE) {    // y-edges (c, j + 1/2)
         const double wa = qa[2] - qa[1], wb = qb[2] - qb[1];
@@ -1257,8 +1274,13 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
           Yr = __shfl_down_sync(0xffffffffu, Ya, 1);
         }
         yra = yra_; yrb = yrb_; dRya = dRa; dRyb = dRb; wya = wa; wyb = wb;
+        if (RF) {
+          if (F & J0) { dRh_a = dRa; dRh_b = dRb; }
+          dLt_a = dLa; dLt_b = dLb;
+        }
       }
       Xa2 = Xa1; Xa1 = Xa; Xb2 = Xb1; Xb1 = Xb; Xfa = Xfa0; Xfb = Xfb0;
+      if (RF) { dR0p = dR0; dL0p = dL0; }
     };
     iter(0, std::integral_constant<int, LD | YE | J0>{});
     iter(1, std::integral_constant<int, LD | YE | YS>{});
@@ -1489,31 +1511,35 @@ static int launch_sc_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
 #ifndef CV_NB
 #define CV_NB 1
 #endif
-template <int T, int SX, int SY, bool MT2>
+template <int T, int SX, int SY, bool MT2, bool RF = false>
 static int launch_cv_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   constexpr int NB = CV_NB;
   using C = CvShape<T>;
   const size_t smem = (size_t)NB * C::PW * C::WW * sizeof(double);
   static int resident = 0;
   if (!resident) {
-    cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB, RF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_cv<T, SX, SY, MT2, NB>, 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_cv<T, SX, SY, MT2, NB, RF>, 32, smem);
     resident = sms * (per_sm > 0 ? per_sm : 1);
   }
   if (npatch >= (1ll << 31)) return -1;
   const int64_t groups = (npatch + C::PW - 1) / C::PW;
   const int64_t grid = groups < resident ? groups : resident;
-  k_step_cv<T, SX, SY, MT2, NB><<<(unsigned)grid, 32, smem, st>>>(a, (int)npatch);
+  k_step_cv<T, SX, SY, MT2, NB, RF><<<(unsigned)grid, 32, smem, st>>>(a, (int)npatch);
   return 1;
 }
 
 template <int T>
 static int launch_cv(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   const bool px = a.sp.p0 > 0.0, py = a.sp.p1 > 0.0, mt2 = a.method3 == 2;
+  if (a.rslot) {   // reflux records (method3 = 2 only; others go to k_step_sc)
+    if (px) return py ? launch_cv_t<T, 1, 1, true, true>(a, npatch, st) : launch_cv_t<T, 1, -1, true, true>(a, npatch, st);
+    return py ? launch_cv_t<T, -1, 1, true, true>(a, npatch, st) : launch_cv_t<T, -1, -1, true, true>(a, npatch, st);
+  }
   if (mt2) {
     if (px) return py ? launch_cv_t<T, 1, 1, true>(a, npatch, st) : launch_cv_t<T, 1, -1, true>(a, npatch, st);
     return py ? launch_cv_t<T, -1, 1, true>(a, npatch, st) : launch_cv_t<T, -1, -1, true>(a, npatch, st);
@@ -1540,10 +1566,10 @@ static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   // scalar solvers: the two-phase kernel (FC_SCALAR_PHASED=1 keeps the generic phased k_step)
   static const bool phased = getenv("FC_SCALAR_PHASED") && atoi(getenv("FC_SCALAR_PHASED"));
   // constant-velocity advection on whole 8 x 8 / 16 x 16 patches: the register-sweep kernel
-  // (FC_SCALAR_CV=0 keeps k_step_sc; reflux records are written by k_step_sc)
+  // (FC_SCALAR_CV=0 keeps k_step_sc; reflux records need method3 = 2 here)
   static const bool cv = !(getenv("FC_SCALAR_CV") && atoi(getenv("FC_SCALAR_CV")) == 0);
   if constexpr (std::is_same<S, AdvConst>::value) {
-    if (cv && !phased && !a.rslot && a.tiles == 1 && a.limiter != 0) {
+    if (cv && !phased && (!a.rslot || a.method3 == 2) && a.tiles == 1 && a.limiter != 0) {
       if (a.m == 16) return launch_cv<16>(a, npatch, st);
       if (a.m == 8) return launch_cv<8>(a, npatch, st);
     }
@@ -1654,7 +1680,8 @@ struct SubAlpha {
   double a[32];
   int lmin;
 };
-__global__ void k_sub_snapshot(const double* __restrict__ cur, double* __restrict__ old, double* __restrict__ snap,
+__global__ void k_sub_snapshot(const double* __restrict__ cur, double* __restrict__ old,
+                               const double* __restrict__ old0, double* __restrict__ snap,
                                const int8_t* __restrict__ level, const int32_t* __restrict__ list, int64_t P,
                                int meqn, int mm, int n2, int l, SubAlpha al) {
   const int64_t per = (int64_t)meqn * mm, tot = P * per;
@@ -1670,7 +1697,8 @@ __global__ void k_sub_snapshot(const double* __restrict__ cur, double* __restric
       if (lp == l) old[o] = v;
     } else {
       const double a = al.a[lp - al.lmin];
-      snap[o] = __dadd_rn(__dmul_rn(1.0 - a, old[o]), __dmul_rn(a, cur[o]));
+      const double ov = lp == al.lmin ? old0[o] : old[o];   // the coarsest level starts at q_old
+      snap[o] = __dadd_rn(__dmul_rn(1.0 - a, ov), __dmul_rn(a, cur[o]));
     }
   }
 }
@@ -1691,13 +1719,14 @@ __global__ void k_sub_accumulate(const int32_t* __restrict__ list, int64_t n, co
   }
 }
 
-int launch_sub_snapshot(const double* cur, double* old, double* snap, const int8_t* level, const int32_t* list,
-                        int64_t P, int meqn, int m, int n2, int l, const double* alpha, int lmin, cudaStream_t st) {
+int launch_sub_snapshot(const double* cur, double* old, const double* old0, double* snap, const int8_t* level,
+                        const int32_t* list, int64_t P, int meqn, int m, int n2, int l, const double* alpha, int lmin,
+                        cudaStream_t st) {
   if (P <= 0) return 0;
   SubAlpha al;
   for (int i = 0; i < 32; ++i) al.a[i] = alpha[i];
   al.lmin = lmin;
-  k_sub_snapshot<<<148 * 8, 256, 0, st>>>(cur, old, snap, level, list, P, meqn, m * m, n2, l, al);
+  k_sub_snapshot<<<148 * 8, 256, 0, st>>>(cur, old, old0, snap, level, list, P, meqn, m * m, n2, l, al);
   return 1;
 }
 
