@@ -120,7 +120,8 @@ typedef struct {
   int64_t step_kernel_launches; /* launches of the update kernel counted in ms_step */
   int64_t local_patches;        /* patches owned by this rank */
   int64_t halo_cells;           /* remote cells received per step (all rounds) */
-  int32_t uniform_fast_path;    /* 1 if the fused gather path (no ring writes) is used */
+  int32_t uniform_fast_path;    /* fused gather path (no ring writes): 1 uniform forest, 2 AMR forest
+                                   (two-hop: computed AVG/INTERP ghosts), 0 ghost kernels */
   int32_t pad_;
   double ms_copy;               /* accumulated device time in the quiescent copy/classify kernel (part of ms_step) */
   int64_t copy_launches;        /* launches counted in ms_copy */

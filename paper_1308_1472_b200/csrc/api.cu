@@ -33,7 +33,9 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
                 int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
                 const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits,
                 const int32_t* rslot, double* freg, const uint8_t* rpeer, const double* const* peerq,
-                cudaStream_t st);
+                const double* cg, cudaStream_t st);
+int launch_cg(int op, const double* q, double* cg, const int32_t* list, int64_t nrec, int meqn, int n2,
+              cudaStream_t st);
 int launch_reflux(const int32_t* cells, int64_t ncells, const double* freg, const double* ffine, double* qnew,
                   const double* aux, const int8_t* level, double wc, double dtr, double dx0, int meqn, int n2,
                   cudaStream_t st);
@@ -147,7 +149,11 @@ struct fc_forest {
   bool has_problem = false, has_q = false, has_aux = false;
   // peer-memory halo (halo_p2p, fused path): ring cells of other ranks read from their buffers
   bool p2p = false;
-  uint8_t* d_rpeer = nullptr;          // [Pl][G] 0 = local, k = rank k-1
+  uint8_t* d_rpeer = nullptr;          // [Pl][G] 0 = local, k = rank k-1, 255 = computed ghost
+  bool amr_fused = false;              // fused ring gather on an AMR forest (computed ghosts)
+  double* d_cg = nullptr;              // computed ghosts (AVG4 / INTERP ring cells), plan_ring_amr
+  DevList cg_avg;
+  std::vector<DevList> cg_interp;      // per level
   double* buf[2] = {nullptr, nullptr}; // this rank's two state buffers (q_old = buf[parity])
   int parity = 0;
   std::vector<std::array<double*, 2>> peer_buf;   // per rank: its two buffers mapped here
@@ -407,6 +413,13 @@ static int update_local(fc_forest* f, double dt) {
     if (f->pl.nranks > 16) return fail(FC_EUNSUP, "peer-memory halo supports at most 16 ranks");
     for (int r = 0; r < f->pl.nranks; ++r) peerq[r] = f->peer_buf[r][f->parity];
   }
+  if (fused && f->amr_fused) {   // computed ghosts of the AMR ring gather: averages, then per level
+    const int n2 = f->pl.n * f->pl.n;
+    f->st.kernel_launches += launch_cg(2, f->qold, f->d_cg, f->cg_avg.d, f->cg_avg.nrec, f->pl.meqn, n2, f->stream);
+    for (auto& l : f->cg_interp)
+      f->st.kernel_launches += launch_cg(3, f->qold, f->d_cg, l.d, l.nrec, f->pl.meqn, n2, f->stream);
+    CK(cudaGetLastError());
+  }
   bool filtered = false;
   // (tiny forests skip the filter: its two extra launches cost more than the tiles they save; the
   // step kernel's own quiescent-window check still applies)
@@ -431,8 +444,8 @@ static int update_local(fc_forest* f, double dt) {
                        p.p0, p.p1, p.limiter, p.method2, p.method3, filtered ? 0 : p.skip_quiescent,
                        fused ? f->d_ring : nullptr, f->d_bcflag, filtered ? f->d_active : nullptr,
                        filtered ? f->d_nactive : nullptr, f->d_cfl, reflux ? f->d_rslot : nullptr,
-                       reflux ? f->d_freg : nullptr, (fused && f->p2p) ? f->d_rpeer : nullptr, peerq.data(),
-                       f->stream);
+                       reflux ? f->d_freg : nullptr, (fused && (f->p2p || f->amr_fused)) ? f->d_rpeer : nullptr,
+                       peerq.data(), f->d_cg, f->stream);
   if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
   f->st.kernel_launches += lr;
   f->st.step_kernel_launches += lr;
@@ -486,6 +499,9 @@ static void destroy(fc_forest* f) {
     cudaFree(f->d_uflag); cudaFree(f->d_uval);
     cudaFree(f->d_rslot); cudaFree(f->d_rcells); cudaFree(f->d_freg);
     cudaFree(f->d_rpeer);
+    cudaFree(f->d_cg);
+    free_list(f->cg_avg);
+    for (auto& l : f->cg_interp) free_list(l);
     for (auto& g : f->run_exec) if (g) cudaGraphExecDestroy(g);
     cudaFree(f->d_hist); cudaFree(f->d_hist_idx); cudaFree(f->d_backup);
     for (size_t r = 0; r < f->peer_ipc.size(); ++r)
@@ -638,6 +654,29 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
       cudaMemcpy(f->d_negmask, rs.negmask.data(), rs.negmask.size(), cudaMemcpyHostToDevice);
       f->fused = true;
       f->st.uniform_fast_path = 1;
+    } else if (allow && !pl.uniform_same && T == pl.m && pl.nranks == 1) {
+      // AMR forest: fused two-hop gather (plan_ring_amr); unsupported forests keep the ghost kernels
+      RingSources rs;
+      RingAmr ra;
+      std::string why;
+      if (plan_ring_amr(f->pl, pl.meqn, rs, ra, why) == FC_OK) {
+        const int64_t S = (int64_t)pl.meqn * pl.n * pl.n;
+        if ((e = cudaMalloc(&f->d_rpeer, rs.peer.size())) != cudaSuccess ||
+            (e = cudaMalloc(&f->d_ring, rs.src.size() * sizeof(int32_t))) != cudaSuccess ||
+            (e = cudaMalloc(&f->d_bcflag, std::max<size_t>(1, rs.bcflag.size()))) != cudaSuccess ||
+            (e = cudaMalloc(&f->d_cg, (size_t)std::max<int64_t>(1, ra.ncg_patches) * S * sizeof(double))) != cudaSuccess)
+          return cuda_fail(e, "cudaMalloc AMR ring");
+        cudaMemcpy(f->d_rpeer, rs.peer.data(), rs.peer.size(), cudaMemcpyHostToDevice);
+        cudaMemcpy(f->d_ring, rs.src.data(), rs.src.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(f->d_bcflag, rs.bcflag.data(), rs.bcflag.size(), cudaMemcpyHostToDevice);
+        if ((rc = to_dev(f, ra.avg, 5, f->cg_avg))) { destroy(f); return fail(rc, g_err); }
+        f->cg_interp.resize(ra.interp.size());
+        for (size_t l = 0; l < ra.interp.size(); ++l)
+          if ((rc = to_dev(f, ra.interp[l], 8, f->cg_interp[l]))) { destroy(f); return fail(rc, g_err); }
+        f->fused = true;
+        f->amr_fused = true;
+        f->st.uniform_fast_path = 2;
+      }
     }
   }
   if (!f->d_nbr) {   // quiescent-filter tables for the ring (non-fused) path: any forest
@@ -1118,7 +1157,7 @@ static int sub_advance(fc_forest* f, int l, int64_t tick, int sub) {
     int lr = launch_step(p.kind, src, f->qnew, f->aux, f->d_level, f->n_lvl[li], m, dt, f->pl.dx0, p.p0,
                          p.p1, p.limiter, p.method2, p.method3, p.skip_quiescent, nullptr, f->d_bcflag, f->d_lvl[li],
                          f->d_lvl_cnt + li, f->d_cfl, reflux ? f->d_rslot : nullptr, reflux ? f->d_freg : nullptr,
-                         nullptr, nullptr, f->stream);
+                         nullptr, nullptr, nullptr, f->stream);
     if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
     f->st.kernel_launches += lr;
     f->st.step_kernel_launches += lr;

@@ -134,6 +134,13 @@ int plan_build(const fc_forest_desc* d, Plan& pl, std::string& err);
 int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err,
                const std::vector<uint8_t>* dst_mask = nullptr);
 int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& err, bool p2p = false);
+// fused two-hop ring gather on AMR forests: computed-ghost (AVG4 / INTERP) lists and slot count
+struct RingAmr {
+  std::vector<int32_t> avg;                  // {dst slot offset, 4 q_old offsets}
+  std::vector<std::vector<int32_t>> interp;  // per level: {dst slot offset, 5 refs, sigx, sigy}
+  int64_t ncg_patches = 0;                   // computed-ghost buffer size in n^2-cell virtual patches
+};
+int plan_ring_amr(const Plan& pl, int meqn, RingSources& rs, RingAmr& ra, std::string& err);
 // activity tables for the quiescent filter on any forest: nbr [Pl][8] / negmask [Pl] as in
 // RingSources; a patch with an AVG4 / INTERP / CORNER3 ghost record is always active (nbr[0] = -2)
 int plan_activity(const Plan& pl, int meqn, std::vector<int32_t>& nbr, std::vector<uint8_t>& negmask,

@@ -59,6 +59,39 @@ __global__ void k_ghost_interp(double* __restrict__ q, const int32_t* __restrict
   }
 }
 
+// computed ghosts of the fused AMR ring gather (plan_ring_amr): the same arithmetic as
+// k_ghost_avg / k_ghost_interp, written into slots of the computed-ghost buffer cg; a source
+// reference v >= 0 is q[v], v < 0 is cg[-1 - v]
+__global__ void k_cg_avg(const double* __restrict__ q, double* __restrict__ cg, const int32_t* __restrict__ L,
+                         int64_t nrec, int meqn, int n2) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrec) return;
+  const int32_t* o = L + 5 * r;
+  for (int k = 0; k < meqn; ++k) {
+    const int64_t c = (int64_t)k * n2;
+    const double a = __dadd_rn(q[o[1] + c], q[o[2] + c]);
+    const double b = __dadd_rn(q[o[3] + c], q[o[4] + c]);
+    cg[o[0] + c] = __dmul_rn(__dadd_rn(a, b), 0.25);
+  }
+}
+
+__global__ void k_cg_interp(const double* __restrict__ q, double* __restrict__ cg, const int32_t* __restrict__ L,
+                            int64_t nrec, int meqn, int n2) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrec) return;
+  const int32_t* o = L + 8 * r;
+  const double sgx = (double)o[6], sgy = (double)o[7];
+  for (int k = 0; k < meqn; ++k) {
+    const int64_t c = (int64_t)k * n2;
+    auto rd = [&](int32_t v) { return v >= 0 ? q[v + c] : cg[(-1 - (int64_t)v) + c]; };
+    const double qc = rd(o[1]);
+    const double sx = minmod(__dsub_rn(rd(o[3]), qc), __dsub_rn(qc, rd(o[2])));
+    const double sy = minmod(__dsub_rn(rd(o[5]), qc), __dsub_rn(qc, rd(o[4])));
+    const double t = __dadd_rn(__dmul_rn(sgx, sx), __dmul_rn(sgy, sy));
+    cg[o[0] + c] = __dadd_rn(qc, __dmul_rn(0.25, t));
+  }
+}
+
 __global__ void k_ghost_bc(double* __restrict__ q, const int32_t* __restrict__ L, int64_t nrec,
                            int meqn, int n2) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -154,6 +187,15 @@ int launch_ghost(int op, double* q, const int32_t* list, int64_t nrec, int meqn,
     case 6: k_ghost_corner3<<<nblk(nrec, B), B, 0, st>>>(q, list, nrec, meqn, n2); break;
     default: return -1;
   }
+  return 1;
+}
+
+int launch_cg(int op, const double* q, double* cg, const int32_t* list, int64_t nrec, int meqn, int n2,
+              cudaStream_t st) {
+  if (nrec <= 0) return 0;
+  const int B = 256;
+  if (op == 2) k_cg_avg<<<nblk(nrec, B), B, 0, st>>>(q, cg, list, nrec, meqn, n2);
+  else k_cg_interp<<<nblk(nrec, B), B, 0, st>>>(q, cg, list, nrec, meqn, n2);
   return 1;
 }
 

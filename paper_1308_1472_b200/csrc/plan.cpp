@@ -555,6 +555,107 @@ int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& er
   return FC_OK;
 }
 
+// Fused two-hop ring gather for AMR forests (one rank, one tile per patch).  The
+// rings are never written: COPY ring cells are gathered by the step kernel straight from their
+// source cells; AVG4 and INTERP ring cells get a slot in a "computed ghost" buffer (virtual patches
+// of n^2 cells, the same component stride as the state) that two small kernels fill first -- the
+// averages from the fine interiors, then per level (ascending) the interpolations, whose slope
+// stencil reads the coarse patch's interior or, one hop further, the source of the coarse patch's
+// ring cell (a COPY source cell, or another computed slot).  Every value is the one the ghost
+// kernels would have written into the ring, with the same arithmetic.  Slope stencils that reach a
+// physical-boundary ring cell, and CORNER3 records, are not supported (FC_EUNSUP: the caller
+// keeps the ghost kernels).  Source references in the lists: >= 0 an offset in q_old, < 0 the
+// computed slot offset -1 - v.  In rs.src the computed cells have peer code 255.
+int plan_ring_amr(const Plan& pl, int meqn, RingSources& rs, RingAmr& ra, std::string& err) {
+  const int m = pl.m, n = pl.n;
+  const int64_t n2 = (int64_t)n * n, S = (int64_t)meqn * n2;
+  const int64_t Pl = pl.p1 - pl.p0, G = n2 - (int64_t)m * m;
+  if (pl.nranks != 1) { err = "AMR ring gather: one rank only"; return FC_EUNSUP; }
+  rs.src.assign((size_t)Pl * G, 0);
+  rs.peer.assign((size_t)Pl * G, 0);
+  rs.bcflag.assign((size_t)Pl, 0);
+  rs.nbr.clear();
+  rs.negmask.clear();
+  ra = RingAmr();
+  ra.interp.assign(pl.lmax + 1, {});
+  std::vector<int64_t> slot((size_t)Pl * G, -1);
+  int64_t ncg = 0;
+  for (int64_t i = 0; i < Pl * G; ++i) {
+    const int op = pl.table[i * REC];
+    if (op == OP_AVG4 || op == OP_INTERP) slot[i] = ncg++;
+    if (op == OP_CORNER3) { err = "AMR ring gather: CORNER3 ghosts"; return FC_EUNSUP; }
+  }
+  ra.ncg_patches = (ncg + n2 - 1) / n2;
+  if ((Pl + ra.ncg_patches) * S >= (1ll << 31)) { err = "AMR ring gather: state too large"; return FC_EUNSUP; }
+  auto cgoff = [&](int64_t g) { return (int32_t)((g / n2) * S + g % n2); };
+  auto interior = [&](int64_t q, int i, int j) -> int32_t {   // q global, (i, j) interior
+    return (int32_t)((q - pl.p0) * S + qcell(i, j, n));
+  };
+  // a cell (I, J) of local patch q (interior or ring) as a source reference
+  auto ref = [&](int64_t q, int I, int J, int32_t& v) -> bool {
+    if (I >= 1 && I <= m && J >= 1 && J <= m) { v = interior(q, I, J); return true; }
+    const int64_t i = (q - pl.p0) * G + ring_index(I, J, m);
+    const int32_t* o = pl.table.data() + i * REC;
+    if (o[0] == OP_COPY) {
+      if (o[2] < 1 || o[2] > m || o[3] < 1 || o[3] > m) return false;
+      v = interior(o[1], o[2], o[3]);
+      return true;
+    }
+    if (o[0] == OP_AVG4 || o[0] == OP_INTERP) { v = -1 - cgoff(slot[i]); return true; }
+    return false;   // a physical-boundary (or corner) ring cell
+  };
+  for (int64_t lp = 0; lp < Pl; ++lp) {
+    const int lvl = pl.leaves[pl.p0 + lp].level;
+    for (int64_t r = 0; r < G; ++r) {
+      const int64_t i = lp * G + r;
+      const int32_t* o = pl.table.data() + i * REC;
+      int32_t v = 0;
+      switch (o[0]) {
+        case OP_COPY:
+          if (o[2] < 1 || o[2] > m || o[3] < 1 || o[3] > m) { err = "AMR ring gather: copy from a ghost"; return FC_EUNSUP; }
+          v = interior(o[1], o[2], o[3]);
+          break;
+        case OP_BCX:
+        case OP_BCY: {
+          const int win = (o[3] + 1) * n + (o[2] + 1);
+          const int isy = o[0] == OP_BCY;
+          const int neg = (o[4] == FC_BC_WALL && meqn >= 3) ? (isy ? 2 : 1) : 0;
+          v = -1 - ((win << 3) | (neg << 1) | isy);
+          rs.bcflag[lp] |= (uint8_t)(isy ? 2 : 1);
+          break;
+        }
+        case OP_AVG4: {
+          const int I = o[2], J = o[3];
+          if (I < 1 || I + 1 > m || J < 1 || J + 1 > m) { err = "AMR ring gather: average outside the interior"; return FC_EUNSUP; }
+          v = cgoff(slot[i]);
+          rs.peer[i] = 255;
+          ra.avg.insert(ra.avg.end(), {v, interior(o[1], I, J), interior(o[1], I + 1, J), interior(o[1], I, J + 1),
+                                       interior(o[1], I + 1, J + 1)});
+          break;
+        }
+        case OP_INTERP: {
+          const int I = o[2], J = o[3];
+          int32_t c[5];
+          if (!ref(o[1], I, J, c[0]) || !ref(o[1], I - 1, J, c[1]) || !ref(o[1], I + 1, J, c[2]) ||
+              !ref(o[1], I, J - 1, c[3]) || !ref(o[1], I, J + 1, c[4])) {
+            err = "AMR ring gather: interpolation slope reads a boundary ghost";
+            return FC_EUNSUP;
+          }
+          v = cgoff(slot[i]);
+          rs.peer[i] = 255;
+          ra.interp[lvl].insert(ra.interp[lvl].end(), {v, c[0], c[1], c[2], c[3], c[4], o[4], o[5]});
+          break;
+        }
+        default:
+          err = "AMR ring gather: unexpected ghost op";
+          return FC_EUNSUP;
+      }
+      rs.src[i] = v;
+    }
+  }
+  return FC_OK;
+}
+
 }  // namespace fc
 
 namespace fc {

@@ -66,7 +66,12 @@ struct StepArgs {
   double* freg;                       // reflux: [slot][4 faces][m edges][MEQN] applied fluxes, outward
   const uint8_t* __restrict__ rpeer;  // peer-memory halo: owner of each ring source (0 = this rank)
   const double* peerq[16];            // peer-memory halo: rank r's current q_old (peer pointer)
+  const double* cg;                   // fused AMR ring gather: computed ghosts (ring peer code 255)
 };
+// base of a ring source: this rank's q_old, a peer's (code k = rank k - 1), the computed ghosts (255)
+__device__ __forceinline__ const double* ring_base(const StepArgs& A, int ow) {
+  return ow == 0 ? A.qold : (ow == 255 ? A.cg : A.peerq[ow - 1]);
+}
 
 // ---- TMA bulk copies + mbarrier (sm_90+ / sm_100a) -------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -332,7 +337,7 @@ __device__ __forceinline__ void gather_ring(const StepArgs& A, int tile, double*
     if (v >= 0) {
       // peer-memory halo: a cell of another rank is copied straight from its buffer over NVLink
       const int ow = rp ? __ldg(rp + r) : 0;
-      const double* base = ow ? A.peerq[ow - 1] : A.qold;
+      const double* base = ring_base(A, ow);
       cp_async8(buf + k * WW + ring_window_index<T>(r), base + v + (int64_t)k * n2);
     }
   }
@@ -1076,7 +1081,7 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
 #pragma unroll
       for (int t = 0; t < NR; ++t) {
         const int r = lane + 32 * t;
-        if (src[q][t] >= 0) cp_async8(b + ring_window_index<T>(r), (own[q][t] ? A.peerq[own[q][t] - 1] : A.qold) + src[q][t]);
+        if (src[q][t] >= 0) cp_async8(b + ring_window_index<T>(r), ring_base(A, own[q][t]) + src[q][t]);
       }
     }
     cp_async_commit();
@@ -1602,9 +1607,10 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
                 int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
                 const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits,
                 const int32_t* rslot, double* freg, const uint8_t* rpeer, const double* const* peerq,
-                cudaStream_t st) {
+                const double* cg, cudaStream_t st) {
   if (npatch <= 0) return 0;
   StepArgs a;
+  a.cg = cg;
   a.rslot = rslot;
   a.freg = freg;
   a.rpeer = rpeer;
