@@ -53,6 +53,7 @@ extern "C" {
 #define FC_ADV_EDGEVEL_CAPA 1 /* kappa q_t + (u~ q)_xi + (v~ q)_eta advective form; aux = {kappa, u~ (left edge), v~ (bottom edge)}; meqn 1, maux 3 */
 #define FC_SWE_ROE 2          /* shallow water (h, hu, hv), p0 = g; meqn 3 */
 #define FC_EULER_ROE 3        /* Euler (rho, rho u, rho v, E), p0 = gamma, p1 != 0: Harten-Hyman entropy fix; meqn 4 */
+#define FC_EULER_HLLE 4       /* Euler, HLLE two-wave solver (Roe transverse), p0 = gamma; meqn 4 */
 
 #define FC_LIM_NONE 0
 #define FC_LIM_MINMOD 1

@@ -18,7 +18,7 @@ LIB = os.path.join(HERE, "liboracle.so")
 
 OK, EINVAL, ETILING, ECONN, EBALANCE, ENOMEM, EUNSUP, EPHYS = 0, -1, -2, -3, -4, -5, -6, -7
 OP_NONE, OP_COPY, OP_AVG4, OP_INTERP, OP_BCX, OP_BCY, OP_CORNER3 = range(7)
-ADV_CONST, ADV_EDGEVEL_CAPA, SWE_ROE, EULER_ROE = 0, 1, 2, 3
+ADV_CONST, ADV_EDGEVEL_CAPA, SWE_ROE, EULER_ROE, EULER_HLLE = 0, 1, 2, 3, 4
 LIM_NONE, LIM_MINMOD, LIM_MC = 0, 1, 2
 REC = 8
 

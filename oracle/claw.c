@@ -15,7 +15,8 @@
  *   Q_ij -= r_ij [A+dq_{i-1/2} + A-dq_{i+1/2} + F~_{i+1/2} - F~_{i-1/2}]
  *         + s_ij [B+dq_{j-1/2} + B-dq_{j+1/2} + G~_{j+1/2} - G~_{j-1/2}],  r = dt/(kappa dx).
  * Solvers: scalar advection (constant / edge velocities with capacity), shallow-water Roe,
- * Euler Roe with the Harten-Hyman entropy fix (SURVEY §8(c.5) "Solvers").
+ * Euler Roe with the Harten-Hyman entropy fix (SURVEY §8(c.5) "Solvers"); Euler HLLE (SURVEY §8(f)
+ * #4: Einfeldt's two-wave solver, LeVeque 2002 §15.3.7) with the Roe transverse solver.
  */
 #include <math.h>
 #include <stdlib.h>
@@ -27,7 +28,7 @@ int orc_meqn(int kind) {
   switch (kind) {
     case ORC_ADV_CONST: case ORC_ADV_EDGEVEL_CAPA: return 1;
     case ORC_SWE_ROE: return 3;
-    case ORC_EULER_ROE: return 4;
+    case ORC_EULER_ROE: case ORC_EULER_HLLE: return 4;
   }
   return 0;
 }
@@ -36,6 +37,7 @@ int orc_mwaves(int kind) {
     case ORC_ADV_CONST: case ORC_ADV_EDGEVEL_CAPA: return 1;
     case ORC_SWE_ROE: return 3;
     case ORC_EULER_ROE: return 4;
+    case ORC_EULER_HLLE: return 2;
   }
   return 0;
 }
@@ -127,6 +129,44 @@ static void eig_euler(double gam, const roe_t* R, int nd, const double* X, doubl
   lam[0] = vn - c; lam[1] = vn; lam[2] = vn; lam[3] = vn + c;
 }
 
+/* ---- Euler HLLE -------------------------------------------------------------
+ * Einfeldt's HLLE solver in LeVeque's wave form (Finite Volume Methods for Hyperbolic Problems,
+ * 2002, §15.3.7): two waves through one middle state Q*, with speeds
+ *   s1 = min(u_l - c_l, u^ - c^),   s2 = max(u_r + c_r, u^ + c^)
+ * (u^, c^ the Roe-averaged normal velocity and sound speed, u_l, c_l / u_r, c_r those of the two
+ * states), and Q* fixed by conservation, s1 (Q* - Q_l) + s2 (Q_r - Q*) = f(Q_r) - f(Q_l):
+ *   W1 = Q* - Q_l = (f(Q_r) - f(Q_l) - s2 (Q_r - Q_l)) / (s1 - s2),   W2 = (Q_r - Q_l) - W1,
+ * A-dq = min(s1,0) W1 + min(s2,0) W2, A+dq = max(s1,0) W1 + max(s2,0) W2 (reading 25). */
+static int rp_hlle(const orc_problem* pr, int ixy, const double* ql, const double* qr, double* waves,
+                   double* s, double* amdq, double* apdq) {
+  const double gam = pr->p0;
+  const int nd = ixy;
+  roe_t R;
+  int rc = euler_roe(gam, ql, qr, &R);
+  if (rc) return rc;
+  const double un = (nd == 1) ? R.u : R.v;
+  const double ul = ql[nd] / ql[0], cl = sqrt(gam * euler_p(gam, ql) / ql[0]);
+  const double ur = qr[nd] / qr[0], cr = sqrt(gam * euler_p(gam, qr) / qr[0]);
+  const double s1 = dmin(ul - cl, un - R.c);
+  const double s2 = dmax(ur + cr, un + R.c);
+  double fl[4], fr[4];
+  orc_flux(pr, ixy, ql, 0.0, fl);
+  orc_flux(pr, ixy, qr, 0.0, fr);
+  for (int k = 0; k < 4; ++k) {
+    const double dq = qr[k] - ql[k];
+    const double w1 = ((fr[k] - fl[k]) - s2 * dq) / (s1 - s2);
+    waves[k] = w1;
+    waves[4 + k] = dq - w1;
+  }
+  s[0] = s1;
+  s[1] = s2;
+  for (int k = 0; k < 4; ++k) {
+    amdq[k] = dmin(s1, 0.0) * waves[k] + dmin(s2, 0.0) * waves[4 + k];
+    apdq[k] = dmax(s1, 0.0) * waves[k] + dmax(s2, 0.0) * waves[4 + k];
+  }
+  return ORC_OK;
+}
+
 /* ---- normal Riemann solver -------------------------------------------------------------------- */
 int orc_rpn2(const orc_problem* pr, int ixy, const double* ql, const double* qr,
              const double* auxl, const double* auxr, double* waves, double* s, double* amdq,
@@ -164,6 +204,7 @@ int orc_rpn2(const orc_problem* pr, int ixy, const double* ql, const double* qr,
     }
     return ORC_OK;
   }
+  if (pr->kind == ORC_EULER_HLLE) return rp_hlle(pr, ixy, ql, qr, waves, s, amdq, apdq);
   /* Euler */
   const double gam = pr->p0;
   int rc = euler_roe(gam, ql, qr, &R);

@@ -31,7 +31,7 @@ enum { ORC_OK = 0, ORC_EINVAL = -1, ORC_ETILING = -2, ORC_ECONN = -3, ORC_EBALAN
 enum { ORC_OP_NONE = 0, ORC_OP_COPY = 1, ORC_OP_AVG4 = 2, ORC_OP_INTERP = 3, ORC_OP_BCX = 4,
        ORC_OP_BCY = 5, ORC_OP_CORNER3 = 6 };
 
-enum { ORC_ADV_CONST = 0, ORC_ADV_EDGEVEL_CAPA = 1, ORC_SWE_ROE = 2, ORC_EULER_ROE = 3 };
+enum { ORC_ADV_CONST = 0, ORC_ADV_EDGEVEL_CAPA = 1, ORC_SWE_ROE = 2, ORC_EULER_ROE = 3, ORC_EULER_HLLE = 4 };
 enum { ORC_LIM_NONE = 0, ORC_LIM_MINMOD = 1, ORC_LIM_MC = 2 };
 enum { ORC_BC_OUTFLOW = 0, ORC_BC_WALL = 1 };
 

@@ -715,16 +715,16 @@ int fc_forest_destroy(fc_forest* f) {
 
 int fc_set_problem(fc_forest* f, const fc_problem* pr) {
   if (!f || !pr) return fail(FC_EINVAL, "null argument");
-  static const int meqn_of[4] = {1, 1, 3, 4}, maux_of[4] = {0, 3, 0, 0};
-  if (pr->kind < 0 || pr->kind > 3) return fail(FC_EINVAL, "unknown problem kind");
+  static const int meqn_of[5] = {1, 1, 3, 4, 4}, maux_of[5] = {0, 3, 0, 0, 0};
+  if (pr->kind < 0 || pr->kind > 4) return fail(FC_EINVAL, "unknown problem kind");
   if (meqn_of[pr->kind] != f->pl.meqn || maux_of[pr->kind] != f->pl.maux)
     return fail(FC_EINVAL, "meqn/maux of the forest do not match the problem kind");
   if (pr->limiter < 0 || pr->limiter > 2 || pr->method2 < 1 || pr->method2 > 2 || pr->method3 < 0 ||
       pr->method3 > 2)
     return fail(FC_EINVAL, "limiter/method out of range");
-  if ((pr->kind == FC_SWE_ROE || pr->kind == FC_EULER_ROE) && !(pr->p0 > 0.0))
+  if ((pr->kind == FC_SWE_ROE || pr->kind == FC_EULER_ROE || pr->kind == FC_EULER_HLLE) && !(pr->p0 > 0.0))
     return fail(FC_EINVAL, "g / gamma must be positive");
-  if (pr->kind == FC_EULER_ROE && !(pr->p0 > 1.0)) return fail(FC_EINVAL, "gamma must exceed 1");
+  if ((pr->kind == FC_EULER_ROE || pr->kind == FC_EULER_HLLE) && !(pr->p0 > 1.0)) return fail(FC_EINVAL, "gamma must exceed 1");
   if (pr->skip_quiescent != 0 && pr->skip_quiescent != 1) return fail(FC_EINVAL, "skip_quiescent must be 0 or 1");
   if (pr->reflux != 0 && pr->reflux != 1) return fail(FC_EINVAL, "reflux must be 0 or 1");
   if (pr->reflux && !f->reflux_planned) {

@@ -461,9 +461,13 @@ struct EulerRoe {
   template <int D>
   __device__ static void transverse(const double* sc, int st, const SolverParams& P, const double* X,
                                     AuxCell, AuxCell, double* bm, double* bp) {
+    roe_transverse<D>(sc[4 * st], sc[5 * st], sc[6 * st], sc[7 * st], sc[8 * st], P.p0 - 1.0, X, bm, bp);
+  }
+  // B-X and B+X of the Roe matrix (u, v, H, c, 1/c) along the transverse direction of sweep D
+  template <int D>
+  __device__ static void roe_transverse(double u, double v, double H, double c, double ic, double gm1,
+                                        const double* X, double* bm, double* bp) {
     constexpr int nd = 3 - D, td = D;
-    const double gm1 = P.p0 - 1.0;
-    const double u = sc[4 * st], v = sc[5 * st], H = sc[6 * st], c = sc[7 * st], ic = sc[8 * st];
     const double vn = nd == 1 ? u : v, vt = nd == 1 ? v : u;
     const double b3 = X[td] - vt * X[0];
     const double b2 = gm1 * (ic * ic) * ((H - vn * vn - vt * vt) * X[0] + vn * X[nd] + vt * X[td] - X[3]);
@@ -485,6 +489,84 @@ struct EulerRoe {
     bp[nd] = p1 * (vn - c) + p2 * vn + p4 * (vn + c);
     bp[td] = (p1 + p2 + p4) * vt + p3;
     bp[3] = p1 * (H - vn * c) + p2 * ek + p3 * vt + p4 * (H + vn * c);
+  }
+};
+
+// ----------------------------------------------------------------------------------------------
+// Euler, HLLE (Einfeldt; LeVeque 2002 §15.3.7; the oracle's rp_hlle): two waves
+// through one middle state, s1 = min(u_l - c_l, u^ - c^), s2 = max(u_r + c_r, u^ + c^),
+// W1 = (f(Q_r) - f(Q_l) - s2 dQ) / (s1 - s2), W2 = dQ - W1; the transverse solve is the Roe one
+// (reading 25).  Scratch: W1, W2, s1, s2, Roe u, v, H, c, 1/c.
+struct EulerHlle {
+  static constexpr int MEQN = 4, MW = 2, NS = 15, NC = 5, PB = NS, NSA = PB + MEQN;
+  static constexpr bool CAPA = false, AM_STORED = false;
+  __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, const double* a,
+                                         double dtdx, int i0, int i1, int i2, int i3) {
+    return EulerRoe::quiescent_cfl(q, qs, P, a, dtdx, i0, i1, i2, i3);
+  }
+  template <int D>
+  __device__ static void flux(const double* q, int qs, double ue, const SolverParams& P, double* f) {
+    EulerRoe::flux<D>(q, qs, ue, P, f);
+  }
+  __device__ static void precompute(const double* q, int qs, const SolverParams& P, double* c, int cs) {
+    EulerRoe::precompute(q, qs, P, c, cs);   // sqrt(rho), u, v, H, c
+  }
+  template <int D>
+  __device__ static void riemann(const double* ql, const double* qr, const double* cl, const double* cr,
+                                 int cs, AuxCell, AuxCell, const SolverParams& P, double* sc, int st) {
+    constexpr int nd = D;
+    const double gm1 = P.p0 - 1.0;
+    const double wl = cl[0], wr = cr[0];
+    const double inv = fast_rcp(wl + wr);
+    const double al = wl * inv, ar = wr * inv;
+    const double u = al * cl[cs] + ar * cr[cs];
+    const double v = al * cl[2 * cs] + ar * cr[2 * cs];
+    const double H = al * cl[3 * cs] + ar * cr[3 * cs];
+    const double c2 = gm1 * (H - 0.5 * (u * u + v * v));
+    const double ic = fast_rsqrt(c2);
+    const double c = c2 * ic;
+    const double un = nd == 1 ? u : v;
+    const double s1 = fmin(cl[nd * cs] - cl[4 * cs], un - c);
+    const double s2 = fmax(cr[nd * cs] + cr[4 * cs], un + c);
+    double fl[4], fr[4];
+    EulerRoe::flux<D>(ql, 1, 0.0, P, fl);
+    EulerRoe::flux<D>(qr, 1, 0.0, P, fr);
+    const double r12 = fast_rcp(s1 - s2);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double dq = qr[k] - ql[k];
+      const double w1 = ((fr[k] - fl[k]) - s2 * dq) * r12;
+      sc[k * st] = w1;
+      sc[(4 + k) * st] = dq - w1;
+    }
+    sc[8 * st] = s1; sc[9 * st] = s2;
+    sc[10 * st] = u; sc[11 * st] = v; sc[12 * st] = H; sc[13 * st] = c; sc[14 * st] = ic;
+  }
+  template <int D>
+  __device__ static double speed(const double* sc, int st, int p, const SolverParams&, AuxCell) {
+    return sc[(8 + p) * st];
+  }
+  template <int D>
+  __device__ static void wave(const double* sc, int st, int p, const SolverParams&, double* W) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) W[k] = sc[(4 * p + k) * st];
+  }
+  template <int D>
+  __device__ static void fluct(const double* sc, int st, const SolverParams&, AuxCell, double* am, double* ap) {
+    double m1, p1, m2, p2;
+    split0(sc[8 * st], m1, p1);
+    split0(sc[9 * st], m2, p2);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      am[k] = m1 * sc[k * st] + m2 * sc[(4 + k) * st];
+      ap[k] = p1 * sc[k * st] + p2 * sc[(4 + k) * st];
+    }
+  }
+  template <int D>
+  __device__ static void transverse(const double* sc, int st, const SolverParams& P, const double* X,
+                                    AuxCell, AuxCell, double* bm, double* bp) {
+    EulerRoe::roe_transverse<D>(sc[10 * st], sc[11 * st], sc[12 * st], sc[13 * st], sc[14 * st], P.p0 - 1.0, X,
+                                bm, bp);
   }
 };
 

@@ -1453,6 +1453,9 @@ int launch_filter(int kind, const double* qold, double* qnew, int npatch, int m,
     case FC_EULER_ROE:
       return launch_filter_s<EulerRoe>(qold, qnew, npatch, m, uflag, uval, nbr, negmask, level, dt, dx0, sp,
                                        active, nactive, cfl_bits, st, ev_before_copy, ev_after_copy);
+    case FC_EULER_HLLE:
+      return launch_filter_s<EulerHlle>(qold, qnew, npatch, m, uflag, uval, nbr, negmask, level, dt, dx0, sp,
+                                        active, nactive, cfl_bits, st, ev_before_copy, ev_after_copy);
   }
   return -1;   // capacity form: edge-dependent CFL, no patch filter
 }
@@ -1587,7 +1590,8 @@ static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
       if (a.m % 2 == 0) return launch_sc<S, 2>(a, npatch, st);
     }
   }
-  constexpr int dmb = (S::MEQN >= 3) ? 2 : 3;
+  // (HLLE's 15-slot edge scratch leaves shared memory for one 16 x 16 CTA per SM)
+  constexpr int dmb = std::is_same<S, EulerHlle>::value ? 1 : ((S::MEQN >= 3) ? 2 : 3);
   const int mb = env_mb ? env_mb : dmb;
   if (a.m % 16 == 0) {
     if (a.rslot || mb == dmb) return launch_step_r<S, 16, 352, dmb>(a, npatch, st);
@@ -1633,6 +1637,7 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
     case FC_ADV_EDGEVEL_CAPA: return launch_step_s<AdvEdgeCapa>(a, npatch, st);
     case FC_SWE_ROE: return launch_step_s<SweRoe>(a, npatch, st);
     case FC_EULER_ROE: return launch_step_s<EulerRoe>(a, npatch, st);
+    case FC_EULER_HLLE: return launch_step_s<EulerHlle>(a, npatch, st);
   }
   return -1;
 }

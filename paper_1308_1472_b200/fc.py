@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("FC_LIB_PATH") or os.path.join(HERE, "libfc.so")   # (
 FC_OK, FC_EINVAL, FC_ETILING, FC_ECONN, FC_EBALANCE, FC_ECUDA, FC_ENCCL, FC_ENOMEM, FC_ESTATE, \
     FC_ECFL, FC_ENONFINITE, FC_EUNSUP = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9, -10, -11
 FC_HOST, FC_DEVICE = 0, 1
-FC_ADV_CONST, FC_ADV_EDGEVEL_CAPA, FC_SWE_ROE, FC_EULER_ROE = 0, 1, 2, 3
+FC_ADV_CONST, FC_ADV_EDGEVEL_CAPA, FC_SWE_ROE, FC_EULER_ROE, FC_EULER_HLLE = 0, 1, 2, 3, 4
 FC_LIM_NONE, FC_LIM_MINMOD, FC_LIM_MC = 0, 1, 2
 FC_TABLE_EXPANDED = 1
 

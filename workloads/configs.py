@@ -20,7 +20,7 @@ from .forests import (Forest, OUTFLOW, WALL, brick, cell_centres, forest_refined
 
 # problem kinds / limiters (numbering shared by DESIGN.md, include/fc.h and oracle/oracle.h,
 # which each define them independently)
-ADV_CONST, ADV_EDGEVEL_CAPA, SWE_ROE, EULER_ROE = 0, 1, 2, 3
+ADV_CONST, ADV_EDGEVEL_CAPA, SWE_ROE, EULER_ROE, EULER_HLLE = 0, 1, 2, 3, 4
 LIM_NONE, LIM_MINMOD, LIM_MC = 0, 1, 2
 
 CONFIG_NAMES = ("C1", "C2", "C3", "C4", "C5")
