@@ -181,6 +181,31 @@ def oracle_rate(w, seconds: float, sample_patches: int = 256, seed: int = 130814
     return cells / el, el, reps, len(ids)
 
 
+def oracle_rate_openmp(seconds: float):
+    """The oracle's whole-forest step (orc_step, its OpenMP loop over patches) on all host cores,
+    on C5's physics and patch size at level 5 (4,096 patches, 1.05 M cells: the full C5 forest
+    would take minutes per step): ghost fill + one update per repetition, until `seconds`."""
+    import oracle
+    from workloads.configs import c5
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    w = c5(level=5, m=16, steps=1)
+    f = oracle.forest_for(w)
+    pr = oracle.problem_for(w)
+    qp = f.pad(w.q0)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        f.step(pr, qp, w.dt0, 1.0 / w.m, None, cores)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    cells = w.num_patches * w.m * w.m
+    return {"value": cells * reps / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{reps} x whole-forest steps (ghost fill + update, OpenMP over patches) of C5 physics "
+                      f"at level 5 ({w.num_patches} patches, {cells} cells), {el:.1f} s"}
+
+
 def run_reference(args):
     """--impl reference: the oracle timed on the host (rank 0 only under torchrun)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -427,6 +452,8 @@ def main():
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{reps} x one-step updates of {ns} random {w.name} patches ({ns * w.m * w.m} cells) "
                          f"from the IC, ring built from neighbours, {el:.1f} s single-threaded"}
+        if args.workload == "C5":         # the oracle with OpenMP on all host cores too
+            cpu["openmp"] = oracle_rate_openmp(max(1.0, args.cpu_seconds / 3))
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
