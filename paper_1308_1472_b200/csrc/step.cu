@@ -1249,9 +1249,10 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
         const double tb = Xfb + Yfb + (SX > 0 ? kx * (Yb - Ya) : kx * (Yr - Yb)) +
                           (SY > 0 ? ky * (Xb1 - Xb2) : ky * (Xb - Xb1));
         const double va = fma(-r, ta, qa[0]), vb = fma(-r, tb, qb[0]);
-        if (live && c0 >= 1) out[(jr - 1) * T + c0 - 1] = va;
-        if (live && c0 + 1 <= T) out[(jr - 1) * T + c0] = vb;
-        chk = fma(va, 0.0, fma(vb, 0.0, chk));
+        const bool sa_ = live && c0 >= 1, sb_ = live && c0 + 1 <= T;
+        if (sa_) out[(jr - 1) * T + c0 - 1] = va;
+        if (sb_) out[(jr - 1) * T + c0] = vb;
+        chk = fma(sa_ ? va : 0.0, 0.0, fma(sb_ ? vb : 0.0, 0.0, chk));
         if (RF && rec) {   // the same face fluxes k_step_sc records (F~ / G~ transverse at the face)
           if (k == 0) reg[jr - 1] = (dR0p - kx * (SX > 0 ? Ya : Yb)) - u0 * qb[0];                 // x-low, i = 1
           if (k == LP - 1) reg[T + jr - 1] = u0 * qa[0] + (dL0p + kx * (SX > 0 ? Ya : Yb));       // x-high, i = T
@@ -1301,6 +1302,221 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
     for (int j = 2; j <= T; ++j) iter(j, std::integral_constant<int, LD | UPD | YE | YS>{});
     iter(T + 1, std::integral_constant<int, UPD>{});
     __syncwarp();   // the staging buffer is refilled by a later group
+    if (NB == 1) issue_next();
+  }
+  const bool bad = __any_sync(0xffffffffu, chk != chk);
+  if (bad || cfl != cfl) cfl = __longlong_as_double(0x7ff0000000000000ll);
+  for (int o = 16; o > 0; o >>= 1) cfl = fmax(cfl, __shfl_xor_sync(0xffffffffu, cfl, o));
+  if (lane == 0) atomicMax(A.cfl_bits, (unsigned long long)__double_as_longlong(cfl));
+}
+
+// ---------------------------------------------------------------------------------------------
+// Capacity-form advection with edge velocities (C4 / T4 physics), register sweep: the layout of
+// k_step_cv (PW patches per warp, lane k owns columns 2k, 2k+1, one pass over rows 0..T+1), with
+// per-edge speeds and per-cell r = dt / (kappa dx).  The transverse parts regroup per cell as
+//   U = h r max(v_top, 0) X,  D = h r min(v_bot, 0) X,  R = h r max(u_right, 0) Y,  L = h r min(u_left, 0) Y
+// (h = -1/2, X / Y as in k_step_cv; the receiving cell's own edge velocities, PAPER.md:168-171 /
+// reading 24), and
+//   q_new = q - r [Xf + Yf + R + L_{i+1} - R_{i-1} - L + U + D_{j+1} - U_{j-1} - D].
+// q is staged in shared memory as in k_step_cv; the three aux fields are read from global memory
+// one row ahead (read-only path), kappa's reciprocal is formed once per cell.  CFL: every x-edge
+// i - 1/2, i = 1..T+1, of rows 0..T+1 and every y-edge of columns 0..T+1 (k_step_sc's set).
+#ifndef CVC_MINB
+#define CVC_MINB 16
+#endif
+#ifndef CVC_UNROLL
+#define CVC_UNROLL 1
+#endif
+template <int T, bool MT2, int NB>
+__global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatch) {
+  using C = CvShape<T>;
+  constexpr int W = C::W, WW = C::WW, LP = C::LP, PW = C::PW;
+  extern __shared__ __align__(128) double sm[];     // [NB][PW][WW]
+  __shared__ __align__(8) uint64_t bars[NB];
+  const int lane = threadIdx.x;
+  if (A.active) npatch = *A.nactive;
+  const int ngroups = (npatch + PW - 1) / PW;
+  auto patch_of = [&](int idx) { return A.active ? A.active[idx] : idx; };
+  auto stage = [&](int g, int s) {   // padded patches -> natural windows (as k_step_cv, dense path)
+    double* buf = sm + (size_t)s * PW * WW;
+    const int i0 = g * PW, cnt = min(PW, npatch - i0);
+    if (lane == 0) mbar_expect_tx(&bars[s], (uint32_t)cnt * (T * T + 4 * W) * (uint32_t)sizeof(double));
+    __syncwarp();
+    const int mp = lane < cnt ? patch_of(i0 + lane) : 0;
+#pragma unroll
+    for (int q = 0; q < PW; ++q) {
+      const int patch = __shfl_sync(0xffffffffu, mp, q);
+      if (q >= cnt) break;
+      const double* qb = A.qold + (int64_t)patch * WW;
+      double* b = buf + q * WW;
+      if (lane < T) bulk_g2s(b + (lane + 2) * W + 2, qb + lane * T, T * sizeof(double), &bars[s]);
+      else if (lane == T) bulk_g2s(b, qb + T * T, 2 * W * sizeof(double), &bars[s]);
+      else if (lane == T + 1) bulk_g2s(b + (T + 2) * W, qb + T * T + 2 * W + 4 * T, 2 * W * sizeof(double), &bars[s]);
+      if (lane < 2 * T) {
+        const int j = 1 + (lane >> 1), side = lane & 1;
+        cp_async16(b + (j + 1) * W + (side ? T + 2 : 0), qb + T * T + 2 * W + 4 * (j - 1) + 2 * side);
+      }
+    }
+    cp_async_commit();
+  };
+  if (lane == 0) {
+    for (int q = 0; q < NB; ++q) mbar_init(&bars[q], 1);
+    fence_proxy_async();
+  }
+  __syncwarp();
+  for (int q = 0; q < (NB > 1 ? NB - 1 : 1); ++q) {
+    const int g = blockIdx.x + q * gridDim.x;
+    if (g < ngroups) stage(g, q);
+    else cp_async_commit();
+  }
+  const int p = lane / LP, k = lane - p * LP, c0 = 2 * k;
+  const bool trans = A.method3 >= 1, second = A.method2 == 2;
+  const double m3 = A.method3 == 2 ? 1.0 : 0.0, h = trans ? -0.5 : 0.0;
+  const double lc1 = A.lim.c1, lc2 = A.lim.c2, lc3 = A.lim.c3, lc4 = A.lim.c4;
+  auto limited = [&](double w, double wi) {   // as k_step_cv (MC / minmod)
+    const long long sw = __double_as_longlong(w) & (long long)0x8000000000000000ull;
+    const double a = __longlong_as_double(__double_as_longlong(fma(lc1, w, lc2 * wi)) ^ sw);
+    const double c = __longlong_as_double(__double_as_longlong(lc4 * wi) ^ sw);
+    const double b = lc3 * fabs(w);
+    double mm = a < b ? a : b;
+    mm = mm < c ? mm : c;
+    mm = mm > 0.0 ? mm : 0.0;
+    return __longlong_as_double(__double_as_longlong(mm) ^ sw);
+  };
+  double cfl = 0.0, chk = 0.0;
+  int it = 0;
+  for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
+    const int b = it % NB;
+    const int cnt = min(PW, npatch - g * PW);
+    const int mypatch = lane < cnt ? patch_of(g * PW + lane) : 0;
+    const int mylevel = A.level[mypatch];
+    mbar_wait(&bars[b], (uint32_t)((it / NB) & 1));
+    cp_async_wait<(NB > 1 ? NB - 2 : 0)>();
+    __syncwarp();
+    auto issue_next = [&]() {
+      const int gn = g + (NB > 1 ? NB - 1 : 1) * gridDim.x, bn = (it + NB - 1) % NB;
+      if (gn < ngroups) {
+        fence_proxy_async();
+        stage(gn, bn);
+      } else {
+        cp_async_commit();
+      }
+    };
+    if (NB > 1) issue_next();
+    const bool live = p < cnt;
+    const int patch = __shfl_sync(0xffffffffu, mypatch, live ? p : 0);
+    const int level = __shfl_sync(0xffffffffu, mylevel, live ? p : 0);
+    const double* sq = sm + ((size_t)b * PW + (live ? p : 0)) * WW;
+    const double* col[5];
+#pragma unroll
+    for (int e = 0; e < 5; ++e) col[e] = sq + min(c0 - 1 + e, T + 2) + 1;
+    auto ld = [&](int e, int j) { return col[e][(j + 1) * W]; };
+    // aux (natural [3][W][W]): kappa, u~ (left edge of the cell), v~ (bottom edge)
+    const double* ax = A.aux + (int64_t)patch * 3 * WW;
+    const int ca = c0 + 1, cb = min(c0 + 2, T + 2);   // natural column offsets of c0 and c0 + 1 (+1)
+    auto kap = [&](int cc, int j) { return __ldg(ax + (j + 1) * W + cc); };
+    auto uu = [&](int cc, int j) { return __ldg(ax + WW + (j + 1) * W + cc); };
+    auto vv = [&](int cc, int j) { return __ldg(ax + 2 * WW + (j + 1) * W + cc); };
+    const double dtdx = A.dt / ldexp(A.dx0, -level);
+    double* out = A.qnew + (int64_t)patch * WW;
+    // edge parts from (w, upwind candidates, speed, r of the low / high cell); CFL when counted
+    auto edge = [&](double w, double wup_lo, double wup_hi, double s, double rl, double rh, bool count,
+                    double& dL, double& dR, double& xl, double& xr) {
+      if (count && live) cfl = fmax(cfl, fmax(rh * s, -rl * s));
+      const double as = fabs(s);
+      const double cf = second ? 0.5 * as * (1.0 - as * (0.5 * (rl + rh))) : 0.0;
+      const double f = cf * limited(w, s > 0.0 ? wup_lo : wup_hi);
+      const double sp = s > 0.0 ? s : 0.0, sn = s - sp;
+      dL = fma(sn, w, f);
+      dR = fma(sp, w, -f);
+      if (MT2) { xl = dL; xr = dR; }
+      else { xl = fma(sn, w, m3 * f); xr = fma(sp, w, -(m3 * f)); }
+    };
+    double qa[4], qb[4];
+    qa[1] = ld(1, -1); qa[2] = ld(1, 0); qa[3] = ld(1, 1);
+    qb[1] = ld(2, -1); qb[2] = ld(2, 0); qb[3] = ld(2, 1);
+    qa[0] = qb[0] = 0.0;
+    double ra = dtdx * fast_rcp(kap(ca, 0)), rb = dtdx * fast_rcp(kap(cb, 0));   // r at row j (j = 0)
+    double Ua1 = 0, Ua2 = 0, Ub1 = 0, Ub2 = 0, Da1 = 0, Db1 = 0;   // U(j-1), U(j-2), D(j-1)
+    double Xfa = 0, Xfb = 0, Yfa = 0, Yfb = 0, Ra = 0, Rb = 0, La = 0, Lb = 0, Rl = 0, Lr = 0;
+    double yra = 0, yrb = 0, dRya = 0, dRyb = 0, wya = 0, wyb = 0, vba = 0, vbb = 0;   // last y-edge
+    double ra1 = 0, rb1 = 0;                                        // r(j - 1)
+    vba = vv(ca, 0); vbb = vv(cb, 0);                                // v~ at the bottom of row 0
+    // aux one row ahead of its use (global-load latency): u~ of the row, v~ and kappa of the row above
+    const int cu2 = min(c0 + 3, T + 3);
+    double u1c = uu(ca + 1, 0), u2c = uu(cu2, 0), vtca = vv(ca, 1), vtcb = vv(cb, 1), kca = kap(ca, 1),
+           kcb = kap(cb, 1);
+    constexpr int LD = 1, UPD = 2, YE = 4, YS = 8, J0 = 16;
+    auto iter = [&](int j, auto flags) {
+      constexpr int F = decltype(flags)::value;
+      qa[0] = qa[1]; qa[1] = qa[2]; qa[2] = qa[3];
+      qb[0] = qb[1]; qb[1] = qb[2]; qb[2] = qb[3];
+      if (F & LD) { qa[3] = ld(1, j + 2); qb[3] = ld(2, j + 2); }
+      const double u1 = u1c, u2 = u2c;
+      double vta = 0, vtb = 0, ra_n = 0, rb_n = 0;
+      if (F & YE) {
+        vta = vtca; vtb = vtcb;
+        ra_n = dtdx * fast_rcp(kca); rb_n = dtdx * fast_rcp(kcb);
+      }
+      if (j + 1 <= T + 1) { u1c = uu(ca + 1, j + 1); u2c = uu(cu2, j + 1); }   // (the next row's)
+      if (j + 2 <= T + 1) { vtca = vv(ca, j + 2); vtcb = vv(cb, j + 2); kca = kap(ca, j + 2); kcb = kap(cb, j + 2); }
+      const double rc = __shfl_down_sync(0xffffffffu, ra, 1);          // r of column c0 + 2
+      const double uL = __shfl_up_sync(0xffffffffu, u2, 1);            // u~ at c0 - 1/2 (left lane)
+      // x-edges c0 + 1/2, c0 + 3/2 of row j (the second one of the last lane is outside the set)
+      const double qm = ld(0, j), qc = ld(3, j), qd = ld(4, j);
+      const double w0 = qb[1] - qa[1], w1 = qc - qb[1];
+      double dL0, dR0, xl0, xr0, dL1, dR1, xl1, xr1;
+      edge(w0, qa[1] - qm, w1, u1, ra, rb, true, dL0, dR0, xl0, xr0);
+      edge(w1, w0, qd - qc, u2, rb, rc, k < LP - 1, dL1, dR1, xl1, xr1);
+      const double xrL = __shfl_up_sync(0xffffffffu, xr1, 1);
+      const double dRL = MT2 ? xrL : __shfl_up_sync(0xffffffffu, dR1, 1);
+      const double Xa = xrL + xl0, Xb = xr0 + xl1;
+      const double Xfa0 = MT2 ? Xa : dRL + dL0, Xfb0 = MT2 ? Xb : dR0 + dL1;
+      // U(j) needs v~ at the top of row j (the y-edge j + 1/2), D(j) the bottom one
+      const double Ua = h * ra * fmax(F & YE ? vta : 0.0, 0.0) * Xa, Ub = h * rb * fmax(F & YE ? vtb : 0.0, 0.0) * Xb;
+      const double Da = h * ra * fmin(vba, 0.0) * Xa, Db = h * rb * fmin(vbb, 0.0) * Xb;
+      if (F & UPD) {   // row j - 1
+        const int jr = j - 1;
+        const double ta = Xfa + Yfa + (Ra + Lb - Rl - La) + (Ua1 + Da - Ua2 - Da1);
+        const double tb = Xfb + Yfb + (Rb + Lr - Ra - Lb) + (Ub1 + Db - Ub2 - Db1);
+        const double va = fma(-ra1, ta, qa[0]), vb = fma(-rb1, tb, qb[0]);
+        const bool sa_ = live && c0 >= 1, sb_ = live && c0 + 1 <= T;
+        if (sa_) out[(jr - 1) * T + c0 - 1] = va;
+        if (sb_) out[(jr - 1) * T + c0] = vb;
+        chk = fma(sa_ ? va : 0.0, 0.0, fma(sb_ ? vb : 0.0, 0.0, chk));
+      }
+      if (F & YE) {    // y-edges (c, j + 1/2)
+        const double wa = qa[2] - qa[1], wb = qb[2] - qb[1];
+        const double wla = (F & J0) ? qa[1] - qa[0] : wya, wlb = (F & J0) ? qb[1] - qb[0] : wyb;
+        double dLa, dRa, yla, yra_, dLb, dRb, ylb, yrb_;
+        edge(wa, wla, qa[3] - qa[2], vta, ra, ra_n, true, dLa, dRa, yla, yra_);
+        edge(wb, wlb, qb[3] - qb[2], vtb, rb, rb_n, true, dLb, dRb, ylb, yrb_);
+        if (F & YS) {
+          const double Ya = yra + yla, Yb = yrb + ylb;
+          Yfa = MT2 ? Ya : dRya + dLa; Yfb = MT2 ? Yb : dRyb + dLb;
+          Ra = h * ra * fmax(u1, 0.0) * Ya; Rb = h * rb * fmax(u2, 0.0) * Yb;
+          La = h * ra * fmin(uL, 0.0) * Ya; Lb = h * rb * fmin(u1, 0.0) * Yb;
+          Rl = __shfl_up_sync(0xffffffffu, Rb, 1);      // R of column c0 - 1
+          Lr = __shfl_down_sync(0xffffffffu, La, 1);    // L of column c0 + 2
+        }
+        yra = yra_; yrb = yrb_; dRya = dRa; dRyb = dRb; wya = wa; wyb = wb;
+      }
+      Ua2 = Ua1; Ua1 = Ua; Ub2 = Ub1; Ub1 = Ub; Da1 = Da; Db1 = Db; Xfa = Xfa0; Xfb = Xfb0;
+      ra1 = ra; rb1 = rb;
+      if (F & YE) { ra = ra_n; rb = rb_n; vba = vta; vbb = vtb; }
+    };
+    iter(0, std::integral_constant<int, LD | YE | J0>{});
+    iter(1, std::integral_constant<int, LD | YE | YS>{});
+#if CVC_UNROLL == 1
+#pragma unroll 1
+#elif CVC_UNROLL == 2
+#pragma unroll 2
+#else
+#pragma unroll
+#endif
+    for (int j = 2; j <= T; ++j) iter(j, std::integral_constant<int, LD | UPD | YE | YS>{});
+    iter(T + 1, std::integral_constant<int, UPD>{});
+    __syncwarp();
     if (NB == 1) issue_next();
   }
   const bool bad = __any_sync(0xffffffffu, chk != chk);
@@ -1541,6 +1757,28 @@ static int launch_cv_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   return 1;
 }
 
+template <int T, bool MT2>
+static int launch_cvc_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  constexpr int NB = CV_NB;
+  using C = CvShape<T>;
+  const size_t smem = (size_t)NB * C::PW * C::WW * sizeof(double);
+  static int resident = 0;
+  if (!resident) {
+    cudaFuncSetAttribute(k_step_cvc<T, MT2, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_step_cvc<T, MT2, NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_cvc<T, MT2, NB>, 32, smem);
+    resident = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  if (npatch >= (1ll << 31)) return -1;
+  const int64_t groups = (npatch + C::PW - 1) / C::PW;
+  const int64_t grid = groups < resident ? groups : resident;
+  k_step_cvc<T, MT2, NB><<<(unsigned)grid, 32, smem, st>>>(a, (int)npatch);
+  return 1;
+}
+
 template <int T>
 static int launch_cv(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   const bool px = a.sp.p0 > 0.0, py = a.sp.p1 > 0.0, mt2 = a.method3 == 2;
@@ -1580,6 +1818,13 @@ static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
     if (cv && !phased && (!a.rslot || a.method3 == 2) && a.tiles == 1 && a.limiter != 0) {
       if (a.m == 16) return launch_cv<16>(a, npatch, st);
       if (a.m == 8) return launch_cv<8>(a, npatch, st);
+    }
+  }
+  if constexpr (std::is_same<S, AdvEdgeCapa>::value) {   // capacity form: the same sweep, aux from global
+    if (cv && !phased && !a.rslot && !a.ring && a.tiles == 1 && a.limiter != 0) {
+      const bool mt2 = a.method3 == 2;
+      if (a.m == 16) return mt2 ? launch_cvc_t<16, true>(a, npatch, st) : launch_cvc_t<16, false>(a, npatch, st);
+      if (a.m == 8) return mt2 ? launch_cvc_t<8, true>(a, npatch, st) : launch_cvc_t<8, false>(a, npatch, st);
     }
   }
   if constexpr (S::MEQN == 1) {
