@@ -358,8 +358,12 @@ static int halo_round(fc_forest* f, int round) {
 
 static bool has_round2(const fc_forest* f) { return f->npack[1] || f->nunpack[1]; }
 
+// the fused ring gather (no ring writes): default mode, and the full-update mode for constant-
+// velocity advection (measured: T1 full 1.00 -> 0.67 ms, T2 0.27 -> 0.22 ms; for Euler the gather
+// of every patch's ring in the 352-thread k_step costs more than the ghost kernels: C5 full 9.5 ->
+// 10.3 ms).  FC_FUSED_RING=0 at creation keeps the ghost kernels; the capacity form always does.
 static bool use_fused(const fc_forest* f) {
-  return f->fused && f->prob.skip_quiescent && f->prob.kind != FC_ADV_EDGEVEL_CAPA;
+  return f->fused && f->prob.kind != FC_ADV_EDGEVEL_CAPA && (f->prob.skip_quiescent || f->prob.kind == FC_ADV_CONST);
 }
 
 static void run_ghost(fc_forest* f, int op, const DevList& l) {
