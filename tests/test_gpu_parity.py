@@ -236,3 +236,17 @@ def test_zero_velocity_is_a_fixed_point():
     q, c, _ = fc.run(s)
     np.testing.assert_array_equal(q, s.q0)
     assert (c == 0.0).all()
+
+
+@pytest.mark.parametrize("uv", [(-0.7, 0.45), (0.3, -0.9), (-0.6, -0.8)])
+@pytest.mark.parametrize("m", [8, 16])
+@pytest.mark.parametrize("reflux", [0, 1])
+def test_constant_velocity_signs_against_oracle(uv, m, reflux):
+    """The register-sweep kernel is instantiated per sign of (u, v): every sign combination on an AMR
+    forest (C2 rule) at m = 8 and 16, with and without the reflux records, both update modes."""
+    import dataclasses
+    w = dataclasses.replace(c2(base_level=2, m=m, steps=12), params=uv, reflux=reflux)
+    qo, co, do = oracle.run(w)
+    for skip in (1, 0):
+        qg, cg, _ = fc.run(w, dt_list=do, skip_quiescent=skip)
+        assert_parity(w, qg, qo, cg, co)
