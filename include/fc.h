@@ -260,6 +260,23 @@ int fc_halo_unpack(fc_forest* f, int round);    /* synchronous */
 int fc_step_local(fc_forest* f, double dt, int phase, double* local_cfl);
 int fc_commit(fc_forest* f, double global_cfl); /* FC_ECFL / FC_ENONFINITE as fc_step */
 
+/* ---- reflux across rank cuts (SURVEY §8(f) #1 on shards) --------------------
+ * With reflux = 1 on a sharded forest, a coarse cell whose finer face neighbours live on another
+ * rank needs their recorded face fluxes.  fc_set_problem plans it: this rank requests each such
+ * fine face from its owner (fc_reflux_requests: keys global_fine_patch * 4 + face, in the order
+ * of this rank's remote-face records; works on host-only handles).  NCCL handles exchange the
+ * requests inside fc_set_problem (collective: every rank calls it) and the records inside fc_step
+ * (after the update kernel, before the correction).  Manual transport: pass every peer's requests
+ * with fc_reflux_set_requests (`peer` = the requesting rank) and call fc_reflux_finalize once; per
+ * step, after fc_step_local(phase 2) (which packs this rank's served records), copy
+ * recv[recv_off[s]..] <- send_s[send_off_s[me]..] between ranks (fc_reflux_buffers: device
+ * pointers, offsets in doubles, [nranks + 1]), then fc_step_local(phase 3) applies the correction,
+ * then fc_commit.  Sub-cycled steps with cross-rank pairs return FC_EUNSUP. */
+int fc_reflux_requests(fc_forest* f, int peer, int64_t* buf, int64_t cap, int64_t* len);
+int fc_reflux_set_requests(fc_forest* f, int peer, const int64_t* keys, int64_t n);
+int fc_reflux_finalize(fc_forest* f);
+int fc_reflux_buffers(fc_forest* f, void** send, void** recv, int64_t* send_off, int64_t* recv_off);
+
 /* Peer-memory halo (halo_p2p = 1).  fc_p2p_buffers: this handle's two state buffers (device
  * pointers, fixed for its lifetime; they alternate as q_old / q_new) and *parity = which one is
  * q_old now (0 or 1; all ranks commit in lockstep, so the parity is global).  fc_p2p_set_peer

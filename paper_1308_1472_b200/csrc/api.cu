@@ -122,8 +122,16 @@ struct fc_forest {
   int32_t* d_rslot = nullptr;          // [Pl] flux-register slot or -1
   int32_t* d_rcells = nullptr;         // [ncells][RFX]
   int64_t nrcells = 0;
-  double* d_freg = nullptr;            // [slots][4][m][meqn] applied face fluxes (outward)
+  double* d_freg = nullptr;            // [4 slots + remote faces][m][meqn] applied face fluxes (outward)
   int32_t nslots = 0;
+  // reflux across rank cuts: fine faces requested from / served to other ranks (keys q * 4 + face)
+  std::vector<std::vector<int64_t>> rf_req, rf_serve;
+  std::vector<int32_t> h_rslot;
+  int64_t rf_nremote = 0, rf_npack = 0;
+  int32_t* d_rf_pack = nullptr;        // freg offsets (doubles) of the records this rank sends
+  double* d_rf_send = nullptr;
+  std::vector<int64_t> rf_send_off, rf_recv_off;   // [R + 1], doubles
+  bool rf_ready = true;                // manual transport: false until fc_reflux_finalize
   std::vector<int64_t> rcell_off;      // reflux cells sorted by coarse level: [level - glmin] offsets
   // sub-cycling (fc_step_subcycled): levels [glmin, glmax] of the whole forest, per-level local lists
   int glmin = 0, glmax = 0;
@@ -405,13 +413,46 @@ static int ghost_fill_internal(fc_forest* f) {
   return ghost_phase_b(f);
 }
 
+// coarse cells next to finer faces: applied flux -> mean of the fine fluxes
+static int apply_reflux(fc_forest* f, double dt) {
+  if (f->nrcells <= 0) return FC_OK;
+  f->st.kernel_launches += launch_reflux(f->d_rcells, f->nrcells, f->d_freg, f->d_freg, f->qnew, f->aux, f->d_level,
+                                         1.0, dt, f->pl.dx0, f->pl.meqn, f->pl.n * f->pl.n, f->stream);
+  CK(cudaGetLastError());
+  return FC_OK;
+}
+
+// pack the fine-face records other ranks requested; with NCCL send them and receive this rank's
+// requests straight into the remote-face region of freg (the manual transport moves them itself)
+static int reflux_exchange(fc_forest* f) {
+  const int R = f->pl.nranks, me = f->pl.rank;
+  const int64_t rec = (int64_t)f->pl.m * f->pl.meqn;
+  if (f->rf_npack) {
+    f->st.kernel_launches += launch_pack(f->d_freg, f->d_rf_pack, f->rf_npack, 1, 0, f->d_rf_send, f->stream);
+    CK(cudaGetLastError());
+  }
+  if (f->manual) return FC_OK;
+  double* remote = f->d_freg + 4 * (int64_t)f->nslots * rec;
+  NK(ncclGroupStart());
+  for (int s = 0; s < R; ++s) {
+    if (s == me) continue;
+    const int64_t ns = f->rf_send_off[s + 1] - f->rf_send_off[s], nr = f->rf_recv_off[s + 1] - f->rf_recv_off[s];
+    if (ns) NK(ncclSend(f->d_rf_send + f->rf_send_off[s], ns, ncclDouble, s, f->comm, f->stream));
+    if (nr) NK(ncclRecv(remote + f->rf_recv_off[s], nr, ncclDouble, s, f->comm, f->stream));
+  }
+  NK(ncclGroupEnd());
+  return FC_OK;
+}
+
 // the update after the ghost data are in place: quiescent filter (fused path) + step kernel,
 // leaving this rank's CFL max in d_cfl
 static int update_local(fc_forest* f, double dt) {
   CK(cudaMemsetAsync(f->d_cfl, 0, sizeof(unsigned long long), f->stream));
   const fc_problem& p = f->prob;
   const bool fused = use_fused(f);
-  const bool reflux = p.reflux && f->nrcells > 0;
+  const bool reflux = p.reflux && f->nrcells > 0;          // this rank applies corrections
+  const bool records = p.reflux && (f->nrcells > 0 || f->rf_npack > 0);   // and / or serves records
+  if (p.reflux && !f->rf_ready) return fail(FC_ESTATE, "reflux requests not finalized (fc_reflux_finalize)");
   std::array<const double*, 16> peerq{};   // peers' current q_old (peer-memory halo)
   if (fused && f->p2p) {
     if (f->pl.nranks > 16) return fail(FC_EUNSUP, "peer-memory halo supports at most 16 ranks");
@@ -447,8 +488,8 @@ static int update_local(fc_forest* f, double dt) {
   int lr = launch_step(p.kind, f->qold, f->qnew, f->aux, f->d_level, f->Pl, f->pl.m, dt, f->pl.dx0,
                        p.p0, p.p1, p.limiter, p.method2, p.method3, filtered ? 0 : p.skip_quiescent,
                        fused ? f->d_ring : nullptr, f->d_bcflag, filtered ? f->d_active : nullptr,
-                       filtered ? f->d_nactive : nullptr, f->d_cfl, reflux ? f->d_rslot : nullptr,
-                       reflux ? f->d_freg : nullptr, (fused && (f->p2p || f->amr_fused)) ? f->d_rpeer : nullptr,
+                       filtered ? f->d_nactive : nullptr, f->d_cfl, records ? f->d_rslot : nullptr,
+                       records ? f->d_freg : nullptr, (fused && (f->p2p || f->amr_fused)) ? f->d_rpeer : nullptr,
                        peerq.data(), f->d_cg, f->stream);
   if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
   f->st.kernel_launches += lr;
@@ -458,11 +499,11 @@ static int update_local(fc_forest* f, double dt) {
     CK(cudaMemcpyAsync(f->h_nact, f->d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, f->stream));
     f->filtered_last = true;
   }
-  if (reflux) {   // coarse cells next to finer faces: applied flux -> mean of the fine fluxes
-    f->st.kernel_launches += launch_reflux(f->d_rcells, f->nrcells, f->d_freg, f->d_freg, f->qnew, f->aux,
-                                           f->d_level, 1.0, dt, f->pl.dx0, f->pl.meqn, f->pl.n * f->pl.n, f->stream);
-    CK(cudaGetLastError());
+  if (p.reflux && f->pl.nranks > 1) {   // fine-face records for other ranks' coarse cells
+    int rc = reflux_exchange(f);
+    if (rc) return rc;
   }
+  if (reflux && !f->manual) return apply_reflux(f, dt);   // (manual transport: fc_step_local phase 3)
   return FC_OK;
 }
 
@@ -502,6 +543,7 @@ static void destroy(fc_forest* f) {
     cudaFree(f->d_nbr); cudaFree(f->d_active); cudaFree(f->d_nactive); cudaFree(f->d_negmask);
     cudaFree(f->d_uflag); cudaFree(f->d_uval);
     cudaFree(f->d_rslot); cudaFree(f->d_rcells); cudaFree(f->d_freg);
+    cudaFree(f->d_rf_pack); cudaFree(f->d_rf_send);
     cudaFree(f->d_rpeer);
     cudaFree(f->d_cg);
     free_list(f->cg_avg);
@@ -533,6 +575,80 @@ static void destroy(fc_forest* f) {
     if (f->own_stream) cudaStreamDestroy(f->own_stream);
   }
   delete f;
+}
+
+// reflux across rank cuts: pack list (freg offsets of the served records) and the per-peer send /
+// receive offsets, from rf_serve (requests this rank serves) and rf_req (its own requests)
+static int build_reflux_lists(fc_forest* f) {
+  const int R = f->pl.nranks;
+  const int64_t rec = (int64_t)f->pl.m * f->pl.meqn;
+  std::vector<int32_t> pack;
+  f->rf_send_off.assign(R + 1, 0);
+  f->rf_recv_off.assign(R + 1, 0);
+  for (int s = 0; s < R; ++s) {
+    for (int64_t key : f->rf_serve[s]) {
+      const int64_t q = key / 4, face = key % 4;
+      if (q < f->pl.p0 || q >= f->pl.p1) return fail(FC_EINVAL, "reflux request for a patch this rank does not own");
+      const int32_t slot = f->h_rslot[q - f->pl.p0];
+      if (slot < 0) return fail(FC_EINVAL, "reflux request for a patch without flux records");
+      for (int64_t e = 0; e < rec; ++e) pack.push_back((int32_t)((slot * 4 + face) * rec + e));
+    }
+    f->rf_send_off[s + 1] = (int64_t)pack.size();
+    f->rf_recv_off[s + 1] = f->rf_recv_off[s] + (int64_t)f->rf_req[s].size() * rec;
+  }
+  cudaFree(f->d_rf_pack);
+  cudaFree(f->d_rf_send);
+  f->d_rf_pack = nullptr;
+  f->d_rf_send = nullptr;
+  f->rf_npack = (int64_t)pack.size();
+  CK(cudaMalloc(&f->d_rf_send, std::max<int64_t>(1, f->rf_npack) * sizeof(double)));
+  if (f->rf_npack) {
+    CK(cudaMalloc(&f->d_rf_pack, pack.size() * sizeof(int32_t)));
+    CK(cudaMemcpy(f->d_rf_pack, pack.data(), pack.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  f->rf_ready = true;
+  return FC_OK;
+}
+
+// one-time NCCL exchange of the reflux requests (counts all-gathered, then per-peer send/recv)
+static int reflux_exchange_requests(fc_forest* f) {
+  const int R = f->pl.nranks, me = f->pl.rank;
+  std::vector<int64_t> mine(R), all((size_t)R * R);
+  for (int s = 0; s < R; ++s) mine[s] = (int64_t)f->rf_req[s].size();
+  int64_t *d_mine = nullptr, *d_all = nullptr;
+  CK(cudaMalloc(&d_mine, R * sizeof(int64_t)));
+  CK(cudaMalloc(&d_all, all.size() * sizeof(int64_t)));
+  CK(cudaMemcpy(d_mine, mine.data(), R * sizeof(int64_t), cudaMemcpyHostToDevice));
+  NK(ncclAllGather(d_mine, d_all, R, ncclInt64, f->comm, f->stream));
+  CK(cudaMemcpyAsync(all.data(), d_all, all.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  cudaFree(d_mine);
+  cudaFree(d_all);
+  std::vector<int64_t> off_out(R + 1, 0), off_in(R + 1, 0), out;
+  for (int s = 0; s < R; ++s) {
+    off_out[s + 1] = off_out[s] + (int64_t)f->rf_req[s].size();
+    off_in[s + 1] = off_in[s] + all[(size_t)s * R + me];
+    out.insert(out.end(), f->rf_req[s].begin(), f->rf_req[s].end());
+  }
+  int64_t *d_out = nullptr, *d_in = nullptr;
+  CK(cudaMalloc(&d_out, std::max<int64_t>(1, off_out[R]) * sizeof(int64_t)));
+  CK(cudaMalloc(&d_in, std::max<int64_t>(1, off_in[R]) * sizeof(int64_t)));
+  if (off_out[R]) CK(cudaMemcpy(d_out, out.data(), off_out[R] * sizeof(int64_t), cudaMemcpyHostToDevice));
+  NK(ncclGroupStart());
+  for (int s = 0; s < R; ++s) {
+    if (s == me) continue;
+    if (off_out[s + 1] > off_out[s]) NK(ncclSend(d_out + off_out[s], off_out[s + 1] - off_out[s], ncclInt64, s, f->comm, f->stream));
+    if (off_in[s + 1] > off_in[s]) NK(ncclRecv(d_in + off_in[s], off_in[s + 1] - off_in[s], ncclInt64, s, f->comm, f->stream));
+  }
+  NK(ncclGroupEnd());
+  CK(cudaStreamSynchronize(f->stream));
+  std::vector<int64_t> in(off_in[R]);
+  if (off_in[R]) CK(cudaMemcpy(in.data(), d_in, off_in[R] * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  cudaFree(d_out);
+  cudaFree(d_in);
+  f->rf_serve.assign(R, {});
+  for (int s = 0; s < R; ++s) f->rf_serve[s].assign(in.begin() + off_in[s], in.begin() + off_in[s + 1]);
+  return build_reflux_lists(f);
 }
 
 extern "C" {
@@ -751,17 +867,32 @@ int fc_set_problem(fc_forest* f, const fc_problem* pr) {
       for (size_t l = 1; l < f->rcell_off.size(); ++l) f->rcell_off[l] += f->rcell_off[l - 1];
       f->nslots = rf.nslots;
     }
+    f->rf_req = rf.req;
+    f->rf_nremote = rf.nremote;
+    f->h_rslot = rf.slot;
+    f->nrcells = (int64_t)rf.cells.size() / RFX;
     if (!f->host_only) {
       CK(cudaSetDevice(f->device));
       const int64_t Pl1 = std::max<int64_t>(1, f->Pl);
       CK(cudaMalloc(&f->d_rslot, Pl1 * sizeof(int32_t)));
       if (f->Pl) CK(cudaMemcpy(f->d_rslot, rf.slot.data(), f->Pl * sizeof(int32_t), cudaMemcpyHostToDevice));
-      f->nrcells = (int64_t)rf.cells.size() / RFX;
       if (f->nrcells) {
         CK(cudaMalloc(&f->d_rcells, rf.cells.size() * sizeof(int32_t)));
         CK(cudaMemcpy(f->d_rcells, rf.cells.data(), rf.cells.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-        CK(cudaMalloc(&f->d_freg, (size_t)rf.nslots * 4 * f->pl.m * f->pl.meqn * sizeof(double)));
       }
+      const int64_t faces = 4 * (int64_t)rf.nslots + rf.nremote;
+      CK(cudaMalloc(&f->d_freg, (size_t)std::max<int64_t>(1, faces) * f->pl.m * f->pl.meqn * sizeof(double)));
+      if (f->pl.nranks > 1) {   // who serves whom: NCCL exchange now, or the caller (manual transport)
+        if (f->manual) {
+          f->rf_serve.assign(f->pl.nranks, {});
+          f->rf_ready = false;
+        } else {
+          int rc2 = reflux_exchange_requests(f);
+          if (rc2) return rc2;
+        }
+      }
+    } else {
+      f->nrcells = (int64_t)rf.cells.size() / RFX;
     }
     f->reflux_planned = true;
   }
@@ -1189,6 +1320,8 @@ int fc_step_subcycled(fc_forest* f, double dt_coarse, double* max_cfl) {
   int rc = check_step_args(f, dt_coarse);
   if (rc) return rc;
   if (f->manual) return fail(FC_ESTATE, "manual halo transport: sub-cycling needs the NCCL transport");
+  if (f->prob.reflux && (f->rf_nremote > 0 || f->rf_npack > 0))
+    return fail(FC_EUNSUP, "sub-cycled reflux across rank cuts is not supported");
   if (f->glmin == f->glmax) return fc_step(f, dt_coarse, max_cfl);   // one level: the global step
   CK(cudaSetDevice(f->device));
   if ((rc = sub_prepare(f))) return rc;
@@ -1289,6 +1422,46 @@ int fc_get_leaves(fc_forest* f, int8_t* levels, int32_t* tree_ids, int64_t cap, 
   return FC_OK;
 }
 
+// ---- reflux across rank cuts ----------------------------------------------------------------
+int fc_reflux_requests(fc_forest* f, int peer, int64_t* buf, int64_t cap, int64_t* len) {
+  if (!f || !len) return fail(FC_EINVAL, "null argument");
+  if (peer < 0 || peer >= f->pl.nranks) return fail(FC_EINVAL, "bad peer");
+  if (!f->reflux_planned) return fail(FC_ESTATE, "set a problem with reflux = 1 first");
+  const auto& v = f->rf_req[peer];
+  *len = (int64_t)v.size();
+  if (buf && cap >= *len) std::copy(v.begin(), v.end(), buf);
+  else if (buf && *len) return fail(FC_EINVAL, "buffer too small");
+  return FC_OK;
+}
+
+int fc_reflux_set_requests(fc_forest* f, int peer, const int64_t* keys, int64_t n) {
+  if (!f || (n && !keys)) return fail(FC_EINVAL, "null argument");
+  if (!f->manual) return fail(FC_ESTATE, "not a manual-transport handle");
+  if (!f->reflux_planned) return fail(FC_ESTATE, "set a problem with reflux = 1 first");
+  if (peer < 0 || peer >= f->pl.nranks) return fail(FC_EINVAL, "bad peer");
+  f->rf_serve[peer].assign(keys, keys + n);
+  return FC_OK;
+}
+
+int fc_reflux_finalize(fc_forest* f) {
+  if (!f) return fail(FC_EINVAL, "null handle");
+  if (!f->manual) return fail(FC_ESTATE, "not a manual-transport handle");
+  if (!f->reflux_planned) return fail(FC_ESTATE, "set a problem with reflux = 1 first");
+  CK(cudaSetDevice(f->device));
+  return build_reflux_lists(f);
+}
+
+int fc_reflux_buffers(fc_forest* f, void** send, void** recv, int64_t* send_off, int64_t* recv_off) {
+  if (!f || !send || !recv || !send_off || !recv_off) return fail(FC_EINVAL, "null argument");
+  if (f->host_only || !f->reflux_planned || f->rf_send_off.size() != (size_t)f->pl.nranks + 1)
+    return fail(FC_ESTATE, "no reflux exchange on this handle");
+  *send = f->d_rf_send;
+  *recv = f->d_freg + 4 * (int64_t)f->nslots * f->pl.m * f->pl.meqn;
+  std::copy(f->rf_send_off.begin(), f->rf_send_off.end(), send_off);
+  std::copy(f->rf_recv_off.begin(), f->rf_recv_off.end(), recv_off);
+  return FC_OK;
+}
+
 // ---- staged step for a caller-provided halo transport (manual mode) ---------------------------
 int fc_halo_set_requests(fc_forest* f, int round, int peer, const int64_t* keys, int64_t n) {
   if (!f || (n && !keys)) return fail(FC_EINVAL, "null argument");
@@ -1350,6 +1523,8 @@ int fc_step_local(fc_forest* f, double dt, int phase, double* local_cfl) {
   CK(cudaSetDevice(f->device));
   if (phase == 1) {
     if (!use_fused(f) && (rc = ghost_phase_ac(f))) return rc;
+  } else if (phase == 3) {   // after the caller moved the reflux records: apply the reflux
+    if (f->prob.reflux && (rc = apply_reflux(f, dt))) return rc;
   } else if (phase == 2) {
     if (!use_fused(f) && (rc = ghost_phase_b(f))) return rc;
     if ((rc = update_local(f, dt))) return rc;
@@ -1359,7 +1534,7 @@ int fc_step_local(fc_forest* f, double dt, int phase, double* local_cfl) {
       *local_cfl = *f->h_cfl;
     }
   } else {
-    return fail(FC_EINVAL, "phase must be 1 or 2");
+    return fail(FC_EINVAL, "phase must be 1, 2 or 3");
   }
   CK(cudaStreamSynchronize(f->stream));
   note_activity(f);

@@ -158,6 +158,10 @@ struct RefluxPlan {
   std::vector<int32_t> slot;
   int32_t nslots = 0;
   std::vector<int32_t> cells;
+  // fine faces owned by other ranks: per owner rank the keys (fine patch global id * 4 + face) in
+  // remote-face order; remote face r (owner-major) lives at face index 4 nslots + r of freg
+  std::vector<std::vector<int64_t>> req;
+  int64_t nremote = 0;
 };
 int plan_reflux(const Plan& pl, int meqn, RefluxPlan& rf, std::string& err);
 // Dynamic regrid (one rank): new leaves in Morton order and per new leaf {kind (1 copy, 2 child,

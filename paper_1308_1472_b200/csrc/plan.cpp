@@ -673,6 +673,11 @@ int plan_reflux(const Plan& pl, int meqn, RefluxPlan& rf, std::string& err) {
   rf.slot.assign((size_t)Pl, -1);
   rf.nslots = 0;
   rf.cells.clear();
+  rf.req.assign(pl.nranks, {});
+  rf.nremote = 0;
+  std::vector<std::map<int64_t, int64_t>> rmap(pl.nranks);   // per owner: key -> index in its list
+  struct Fix { int64_t cell; int pos; int owner; int64_t key; int fe; };
+  std::vector<Fix> fixes;                                     // remote references, resolved at the end
   // slots: every local patch with a coarser or finer face neighbour
   std::vector<std::array<DirKind, 4>> kinds((size_t)Pl);
   std::vector<std::array<DirInfo, 4>> dirs((size_t)Pl);
@@ -734,20 +739,43 @@ int plan_reflux(const Plan& pl, int meqn, RefluxPlan& rf, std::string& err) {
           else if (di == 0 && dj == -1 && jc[0] == m) { ff = 3; fe = ic[0] - 1; }
           else { err = "reflux: fine face not found"; return FC_EBALANCE; }
           const int64_t q = leaf[0];
-          if (q < pl.p0 || q >= pl.p1) {
-            err = "reflux across a rank boundary is not supported";
-            return FC_EUNSUP;
+          if (q < pl.p0 || q >= pl.p1) {   // the fine face is another rank's: requested from it
+            const int ow = (int)owner_of(pl, q);
+            const int64_t key = q * 4 + ff;
+            auto it = rmap[ow].find(key);
+            if (it == rmap[ow].end()) it = rmap[ow].emplace(key, (int64_t)rmap[ow].size()).first;
+            ro[hf] = -1 - (int32_t)fixes.size();
+            fixes.push_back({0, 0, ow, key, fe});
+            continue;
           }
           const int32_t fs = rf.slot[q - pl.p0];
           if (fs < 0) { err = "reflux: fine patch without a flux slot"; return FC_EINVAL; }
           ro[hf] = RO(fs, ff, fe);
         }
         const int ci = s == 0 ? 1 : (s == 1 ? m : c + 1), cj = s < 2 ? c + 1 : (s == 2 ? 1 : m);
-        auto& v = cells[(lp * (m + 2) + cj) * (m + 2) + ci];
+        const int64_t ck = (lp * (m + 2) + cj) * (m + 2) + ci;
+        auto& v = cells[ck];
         v.push_back(RO(rf.slot[lp], s, c));
-        v.push_back(ro[0]);
-        v.push_back(ro[1]);
+        for (int hf = 0; hf < 2; ++hf) {
+          if (ro[hf] < 0) { fixes[-1 - ro[hf]].cell = ck; fixes[-1 - ro[hf]].pos = (int)v.size(); }
+          v.push_back(ro[hf]);
+        }
       }
+    }
+  }
+  // remote faces: owner-major, each owner's keys in first-reference order
+  {
+    std::vector<int64_t> base(pl.nranks + 1, 0);
+    for (int o = 0; o < pl.nranks; ++o) {
+      rf.req[o].assign(rmap[o].size(), 0);
+      for (auto& kv : rmap[o]) rf.req[o][kv.second] = kv.first;
+      base[o + 1] = base[o] + (int64_t)rmap[o].size();
+    }
+    rf.nremote = base[pl.nranks];
+    if ((4 * (int64_t)rf.nslots + rf.nremote) * m * meqn >= (1ll << 31)) { err = "reflux: too many flux records"; return FC_EUNSUP; }
+    for (const Fix& x : fixes) {
+      const int64_t r = base[x.owner] + rmap[x.owner].at(x.key);
+      cells[x.cell][x.pos] = (int32_t)(((4 * (int64_t)rf.nslots + r) * m + x.fe) * meqn);
     }
   }
   for (auto& kv : cells) {

@@ -34,7 +34,8 @@ EXPORTS = ["fc_forest_create", "fc_forest_destroy", "fc_set_problem", "fc_set_au
            "fc_halo_counts", "fc_halo_requests", "fc_halo_set_requests", "fc_halo_finalize",
            "fc_halo_buffers", "fc_halo_pack", "fc_halo_unpack", "fc_step_local", "fc_commit",
            "fc_nccl_unique_id", "fc_last_error", "fc_step_subcycled", "fc_regrid", "fc_get_leaves",
-           "fc_p2p_buffers", "fc_p2p_set_peer", "fc_run"]
+           "fc_p2p_buffers", "fc_p2p_set_peer", "fc_run", "fc_reflux_requests", "fc_reflux_set_requests",
+           "fc_reflux_finalize", "fc_reflux_buffers"]
 
 
 class FcError(RuntimeError):
@@ -112,6 +113,10 @@ def lib():
         L.fc_halo_set_requests.argtypes = [P, C.c_int, C.c_int, P, C.c_int64]
         L.fc_halo_finalize.argtypes = [P]
         L.fc_halo_buffers.argtypes = [P, C.c_int, C.POINTER(P), C.POINTER(P), P, P]
+        L.fc_reflux_requests.argtypes = [P, C.c_int, P, C.c_int64, C.POINTER(C.c_int64)]
+        L.fc_reflux_set_requests.argtypes = [P, C.c_int, P, C.c_int64]
+        L.fc_reflux_finalize.argtypes = [P]
+        L.fc_reflux_buffers.argtypes = [P, C.POINTER(P), C.POINTER(P), P, P]
         L.fc_halo_pack.argtypes = [P, C.c_int]
         L.fc_halo_unpack.argtypes = [P, C.c_int]
         L.fc_step_local.argtypes = [P, C.c_double, C.c_int, C.POINTER(C.c_double)]
@@ -307,6 +312,30 @@ class Forest:
 
     def halo_finalize(self):
         _check(lib().fc_halo_finalize(self.h), "fc_halo_finalize")
+
+    def reflux_requests(self, peer: int) -> np.ndarray:
+        n = C.c_int64()
+        _check(lib().fc_reflux_requests(self.h, peer, None, 0, C.byref(n)), "fc_reflux_requests")
+        buf = np.zeros(max(1, n.value), np.int64)
+        _check(lib().fc_reflux_requests(self.h, peer, buf.ctypes.data_as(C.c_void_p), len(buf), C.byref(n)),
+               "fc_reflux_requests")
+        return buf[:n.value]
+
+    def reflux_set_requests(self, peer: int, keys: np.ndarray):
+        keys = np.ascontiguousarray(keys, np.int64)
+        _check(lib().fc_reflux_set_requests(self.h, peer, keys.ctypes.data_as(C.c_void_p), len(keys)),
+               "fc_reflux_set_requests")
+
+    def reflux_finalize(self):
+        _check(lib().fc_reflux_finalize(self.h), "fc_reflux_finalize")
+
+    def reflux_buffers(self):
+        s, r = C.c_void_p(), C.c_void_p()
+        so = np.zeros(self.nranks + 1, np.int64)
+        ro = np.zeros(self.nranks + 1, np.int64)
+        _check(lib().fc_reflux_buffers(self.h, C.byref(s), C.byref(r), so.ctypes.data_as(C.c_void_p),
+                                       ro.ctypes.data_as(C.c_void_p)), "fc_reflux_buffers")
+        return s.value, r.value, so, ro
 
     def halo_buffers(self, round_: int):
         s, r = C.c_void_p(), C.c_void_p()

@@ -33,11 +33,11 @@ def d2d(dst: int, src: int, nbytes: int):
         assert _cudart.cudaMemcpy(C.c_void_p(int(dst)), C.c_void_p(int(src)), int(nbytes), 3) == 0
 
 
-def run_sharded(w, R, dts, skip):
+def run_sharded(w, R, dts, skip, reflux=0):
     hs = []
     for r in range(R):
         f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0, 0, r, R, None)
-        f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject, skip)
+        f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject, skip, reflux)
         if w.aux is not None:
             f.set_aux(np.ascontiguousarray(w.aux[f.first:f.first + f.count]))
         hs.append(f)
@@ -49,6 +49,24 @@ def run_sharded(w, R, dts, skip):
     for f in hs:
         f.halo_finalize()
         f.set_q(np.ascontiguousarray(w.q0[f.first:f.first + f.count]))
+    if reflux:   # fine faces of other ranks' coarse cells (fc_reflux_*)
+        for r in range(R):
+            for s in range(R):
+                if s != r:
+                    hs[s].reflux_set_requests(r, hs[r].reflux_requests(s))
+        for f in hs:
+            f.reflux_finalize()
+
+    def move(bufs):
+        for r in range(R):
+            _, recv, _, roff = bufs[r]
+            for s in range(R):
+                if s == r:
+                    continue
+                send, _, soff, _ = bufs[s]
+                n = roff[s + 1] - roff[s]
+                assert n == soff[r + 1] - soff[r]
+                d2d(recv + 8 * roff[s], send + 8 * soff[r], 8 * n)
 
     def exchange(rnd):
         for f in hs:
@@ -73,6 +91,10 @@ def run_sharded(w, R, dts, skip):
             f.step_local(dt, 1)
         exchange(2)
         c = max(f.step_local(dt, 2) for f in hs)
+        if reflux:
+            move([f.reflux_buffers() for f in hs])
+            for f in hs:
+                f.step_local(dt, 3)
         for f in hs:
             assert f.commit(c) == fc.FC_OK
         cfls.append(c)
@@ -168,3 +190,21 @@ def test_empty_ranks_bitwise(R):
     qp, cp = run_sharded_p2p(w, R, do)
     np.testing.assert_array_equal(qp, q1)
     np.testing.assert_array_equal(cp, c1_)
+
+
+@pytest.mark.parametrize("R", [2, 3, 4])
+@pytest.mark.parametrize("w", [c2(steps=20), "amr_euler"], ids=lambda w: w if isinstance(w, str) else w.name)
+def test_sharded_reflux_equals_single_rank_bitwise(w, R):
+    """Reflux across rank cuts (fc_reflux_*): the fine-face records of other ranks' patches are
+    requested once, packed after the update and moved between the ranks, then the correction is
+    applied -- bitwise the one-rank result, which conserves sum q area exactly."""
+    import dataclasses
+    if w == "amr_euler":
+        from test_gpu_subcycle import amr_euler
+        w = amr_euler(steps=8)
+    w = dataclasses.replace(w, reflux=1)
+    _, _, do = oracle.run(w)
+    q1, c1_, _ = fc.run(w, dt_list=do)
+    qr, cr = run_sharded(w, R, do, 1, reflux=1)
+    np.testing.assert_array_equal(qr, q1)
+    np.testing.assert_array_equal(cr, c1_)

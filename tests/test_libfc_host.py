@@ -153,25 +153,37 @@ def test_single_patch_forest_tables():
 
 
 # ---- coarse/fine reflux planning -----------------------------------------------
-def test_reflux_plan_accepts_single_rank_amr_and_rejects_split_pairs():
-    """fc_set_problem(reflux = 1) plans the coarse/fine flux pairing on the host: accepted on one
-    rank for C2 and the cubed sphere; with Morton shards that cut a coarse/fine pair it reports
-    FC_EUNSUP (the fine fluxes would live on another rank); conforming forests always pass."""
+def test_reflux_plan_single_rank_and_cross_rank_requests():
+    """fc_set_problem(reflux = 1) plans the coarse/fine flux pairing on the host: on one rank for C2
+    and the cubed sphere; with Morton shards that cut coarse/fine pairs each rank requests the fine
+    faces it needs from their owners (fc_reflux_requests): every requested fine patch is owned by
+    the peer asked, every face index is 0..3, no key repeats, and some pair of C2's three shards
+    does need one; conforming forests request nothing."""
     from workloads.cubed_sphere import c4_workload
     for w in (c2(), c4_workload(base_level=2, m=8, steps=1)):
         f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, device=-1)
         f.set_problem(w.kind, w.params[0], w.params[1], reflux=1)
+        assert len(f.reflux_requests(0)) == 0
     w = c2()
-    codes = []
-    for r in range(3):
-        f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, 1, device=-1, rank=r, nranks=3)
-        try:
-            f.set_problem(w.kind, w.params[0], w.params[1], reflux=1)
-            codes.append(0)
-        except fc.FcError as e:
-            codes.append(e.code)
-    assert fc.FC_EUNSUP in codes
+    R = 3
+    hs = [fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, 1, device=-1, rank=r, nranks=R)
+          for r in range(R)]
+    total = 0
+    for f in hs:
+        f.set_problem(w.kind, w.params[0], w.params[1], reflux=1)
+    for r, f in enumerate(hs):
+        for s in range(R):
+            keys = f.reflux_requests(s)
+            if s == r:
+                assert len(keys) == 0
+                continue
+            total += len(keys)
+            assert len(set(keys.tolist())) == len(keys)
+            q, face = keys // 4, keys % 4
+            assert ((q >= hs[s].first) & (q < hs[s].first + hs[s].count)).all() and ((face >= 0) & (face < 4)).all()
+    assert total > 0
     w = c5(level=2, m=8)
     for r in range(3):
         f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, 4, device=-1, rank=r, nranks=3)
         f.set_problem(w.kind, w.params[0], w.params[1], reflux=1)
+        assert all(len(f.reflux_requests(s)) == 0 for s in range(3))
