@@ -236,9 +236,13 @@ __device__ __forceinline__ void edge_transverse(const double* sc, int st, const 
 
 // issue the bulk copies staging tile `tile` (q window + aux window) into buf, on barrier bar.
 // Called by all 32 lanes of warp 0: lane 0 arms the barrier, the lanes split the row copies.
+// Issued by `nthr` threads (thread `lane` of them): one warp for the single-copy staging, the whole
+// CTA when the window comes in many row pieces (multi-tile patches, fused ring rows) -- a lone warp
+// issuing ~60-180 row copies per tile held the CTA at its next barrier (T3: 55 % barrier stalls).
+// Thread 0 arms the barrier with the window's bytes; the copies may complete before or after.
 template <class S, int T>
 __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* buf, uint64_t* bar,
-                                           int lane) {
+                                           int lane, int nthr = 32) {
   using Sh = StepShape<S, T>;
   constexpr int MEQN = S::MEQN, W = Sh::W, WW = Sh::WW;
   int patch = tile, tx = 0, ty = 0;
@@ -254,10 +258,9 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
     constexpr uint32_t qbytes = (uint32_t)MEQN * T * T * sizeof(double);
     constexpr uint32_t abytes = S::CAPA ? (uint32_t)3 * WW * sizeof(double) : 0u;
     if (lane == 0) mbar_expect_tx(bar, qbytes + abytes);
-    __syncwarp();
     const double* qb = A.qold + (int64_t)patch * MEQN * n2;
 #pragma unroll 1
-    for (int r = lane; r < MEQN * T; r += 32) {
+    for (int r = lane; r < MEQN * T; r += nthr) {
       const int k = r / T, row = r - k * T;
       // storage (qcell): the interior is dense, row `row` at row * m
       bulk_g2s(buf + k * WW + (row + 2) * W + 2, qb + (int64_t)k * n2 + row * T, T * sizeof(double), bar);
@@ -267,7 +270,6 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
   }
   constexpr uint32_t bytes = (uint32_t)(Sh::BUF - 2) * sizeof(double);
   if (lane == 0) mbar_expect_tx(bar, bytes);
-  __syncwarp();
   if (A.tiles == 1) {        // the window is the whole padded patch: one contiguous copy of its
                              // storage blocks (dense interior + ring, qcell); the kernel reads them
                              // through qidx
@@ -278,7 +280,7 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
     const int m = A.m, mm = m * m;
     const double* qb = A.qold + patch * (int64_t)MEQN * n2;
 #pragma unroll 1
-    for (int r = lane; r < MEQN * W; r += 32) {
+    for (int r = lane; r < MEQN * W; r += nthr) {
       const int k = r / W, b = r - k * W;
       const int j = ty * T + b - 1, i0 = tx * T - 1;
       const double* blk = qb + (int64_t)k * n2;
@@ -299,7 +301,7 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
     if (S::CAPA) {
       const double* ab = A.aux + patch * 3ll * n2 + (int64_t)(ty * T) * n + tx * T;
 #pragma unroll 1
-      for (int r = lane; r < 3 * W; r += 32) {
+      for (int r = lane; r < 3 * W; r += nthr) {
         const int k = r / W, b = r - k * W;
         bulk_g2s(buf + MEQN * WW + 2 + r * W, ab + (int64_t)k * n2 + b * n, W * sizeof(double), bar);
       }
@@ -406,7 +408,10 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
     fence_proxy_async();
   }
   __syncthreads();
-  if (tid < 32 && (int)blockIdx.x < ntiles) stage_tile<S, T>(A, tile_of(blockIdx.x), sbuf, &bars[0], tid);
+  const bool wide = A.ring || A.tiles > 1;          // many row pieces: the whole CTA issues them,
+  const int sid = wide ? (tid & 31) * (NT / 32) + (tid >> 5) : tid;   // consecutive rows on different warps
+  if ((tid < 32 || wide) && (int)blockIdx.x < ntiles)
+    stage_tile<S, T>(A, tile_of(blockIdx.x), sbuf, &bars[0], sid, wide ? NT : 32);
   if (A.ring) {
     if ((int)blockIdx.x < ntiles) gather_ring<S, T, NT>(A, tile_of(blockIdx.x), sbuf);
     cp_async_commit();
@@ -427,9 +432,9 @@ __global__ void __launch_bounds__(NT) __maxnreg__(step_maxnreg(NT, MINB)) k_step
     auto issue_next = [&]() {
       if (issued) return;
       issued = true;
-      if (tid < 32 && knext < ntiles) {
+      if ((tid < 32 || wide) && knext < ntiles) {
         fence_proxy_async();
-        stage_tile<S, T>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF, &bars[b ^ 1], tid);
+        stage_tile<S, T>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF, &bars[b ^ 1], sid, wide ? NT : 32);
       }
       if (A.ring) {                    // this thread's ring cells of the next tile: one cp.async group
         if (knext < ntiles) gather_ring<S, T, NT>(A, tile_of(knext), sbuf + (b ^ 1) * Sh::BUF);
@@ -775,6 +780,8 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
   const int tid = threadIdx.x;
   const int n = A.m + 4, n2 = n * n;
   const bool dense = !A.ring && A.tiles == 1;
+  const bool wide = A.ring || A.tiles > 1;          // many row pieces: the whole CTA issues them,
+  const int sid = wide ? (tid & 31) * (NT / 32) + (tid >> 5) : tid;   // consecutive rows on different warps
   for (int t = tid; t < WW; t += NT) {
     const int i = t % W - 1, j = t / W - 1;
     umap[t] = (int16_t)(((unsigned)(i - 1) < (unsigned)T && (unsigned)(j - 1) < (unsigned)T)
@@ -787,7 +794,7 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
   __syncthreads();
   for (int q = 0; q < NB - 1; ++q) {
     const int k0 = blockIdx.x + q * gridDim.x;
-    if (tid < 32 && k0 < ntiles) stage_tile<S, T>(A, tile_of(k0), sbuf + q * Sh::BUF, &bars[q], tid);
+    if ((tid < 32 || wide) && k0 < ntiles) stage_tile<S, T>(A, tile_of(k0), sbuf + q * Sh::BUF, &bars[q], sid, wide ? NT : 32);
     if (A.ring) {
       if (k0 < ntiles) gather_ring<S, T, NT>(A, tile_of(k0), sbuf + q * Sh::BUF);
       cp_async_commit();
@@ -809,9 +816,9 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
     auto issue_next = [&]() {
       if (issued) return;
       issued = true;
-      if (tid < 32 && knext < ntiles) {
+      if ((tid < 32 || wide) && knext < ntiles) {
         fence_proxy_async();
-        stage_tile<S, T>(A, tile_of(knext), sbuf + bn * Sh::BUF, &bars[bn], tid);
+        stage_tile<S, T>(A, tile_of(knext), sbuf + bn * Sh::BUF, &bars[bn], sid, wide ? NT : 32);
       }
       if (A.ring) {
         if (knext < ntiles) gather_ring<S, T, NT>(A, tile_of(knext), sbuf + bn * Sh::BUF);
