@@ -1282,17 +1282,29 @@ static int sub_advance(fc_forest* f, int l, int64_t tick, int sub) {
   }
   double* committed = f->qold;       // the ghost fill (and its halo exchange) runs on the snapshot
   double* src = coarsest ? f->qold : f->d_sub_snap;
-  f->qold = src;
-  f->fill_sel = sel;
-  int rc = ghost_fill_internal(f);
-  f->fill_sel = nullptr;
-  f->qold = committed;
-  if (rc) return rc;
+  // fused AMR gather (one rank): no ring writes -- the computed ghosts from this snapshot, and the
+  // step gathers every ring cell of the level's patches itself (their sources are all in N_l)
+  const bool fused = f->amr_fused && use_fused(f);
+  int rc = FC_OK;
+  if (fused) {
+    f->st.kernel_launches += launch_cg(2, src, f->d_cg, f->cg_avg.d, f->cg_avg.nrec, meqn, n2, f->stream);
+    for (auto& cl : f->cg_interp)
+      f->st.kernel_launches += launch_cg(3, src, f->d_cg, cl.d, cl.nrec, meqn, n2, f->stream);
+    CK(cudaGetLastError());
+  } else {
+    f->qold = src;
+    f->fill_sel = sel;
+    rc = ghost_fill_internal(f);
+    f->fill_sel = nullptr;
+    f->qold = committed;
+    if (rc) return rc;
+  }
   if (f->n_lvl[li] > 0) {
     int lr = launch_step(p.kind, src, f->qnew, f->aux, f->d_level, f->n_lvl[li], m, dt, f->pl.dx0, p.p0,
-                         p.p1, p.limiter, p.method2, p.method3, p.skip_quiescent, nullptr, f->d_bcflag, f->d_lvl[li],
-                         f->d_lvl_cnt + li, f->d_cfl, reflux ? f->d_rslot : nullptr, reflux ? f->d_freg : nullptr,
-                         nullptr, nullptr, nullptr, f->stream);
+                         p.p1, p.limiter, p.method2, p.method3, p.skip_quiescent, fused ? f->d_ring : nullptr,
+                         f->d_bcflag, f->d_lvl[li], f->d_lvl_cnt + li, f->d_cfl, reflux ? f->d_rslot : nullptr,
+                         reflux ? f->d_freg : nullptr, fused ? f->d_rpeer : nullptr, nullptr,
+                         fused ? f->d_cg : nullptr, f->stream);
     if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
     f->st.kernel_launches += lr;
     f->st.step_kernel_launches += lr;

@@ -66,3 +66,16 @@ def test_fused_amr_gather_in_cuda_graph_runs(monkeypatch):
         g.step(w.dt0)
     np.testing.assert_array_equal(qa, g.get_q())
     g.close()
+
+
+@pytest.mark.parametrize("w", [dataclasses.replace(c2(steps=6), reflux=1), three_levels(steps=4)],
+                         ids=lambda w: w.name)
+def test_fused_amr_gather_in_subcycled_steps(w, monkeypatch):
+    """Sub-cycling on one rank uses the fused gather too (computed ghosts from each level's
+    snapshot, no ring writes): bitwise the ghost-kernel sub-cycled run."""
+    monkeypatch.setenv("FC_FUSED_RING", "1")
+    qa, ca, _ = fc.run_subcycled(w)
+    monkeypatch.setenv("FC_FUSED_RING", "0")
+    qb, cb, _ = fc.run_subcycled(w)
+    np.testing.assert_array_equal(qa, qb)
+    np.testing.assert_array_equal(ca, cb)
