@@ -340,13 +340,16 @@ def main():
     def set_mode(skip: int):
         f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject, skip)
 
-    def timed(skip: int, monitor: bool):
-        """W warm-up + K timed steps from the IC (device-resident inputs)."""
+    def timed(skip: int, monitor: bool, instrument: bool):
+        """W warm-up + K timed steps from the IC (device-resident inputs).  instrument: the
+        library's own per-phase / per-kernel CUDA events on its stream (measured: they slow the C5
+        default step by ~14 %, so the headline pass runs without them and an identical instrumented
+        pass supplies the kernel durations)."""
         set_mode(skip)
         f.set_q(qdev)
         dt, _ = steps(args.warmup, w.dt0)
         f.reset_stats()
-        f.set_timing(True)
+        f.set_timing(instrument)
         clocks = None
         if monitor:
             try:
@@ -375,10 +378,12 @@ def main():
         return ms, st, clk, cfls
 
     # ---- device-resident timed runs: default (exact quiescent-tile shortcut on), full update ----
-    ms, st, clk, cfls = timed(1, True)
+    ms, _, clk, cfls = timed(1, True, False)
     value = cells_total * args.steps / (ms / 1000.0)
-    ms_full, st_full, _, _ = timed(0, False)
+    ms_i, st, _, _ = timed(1, False, True)          # instrumented twin: kernel / phase durations
+    ms_full, _, _, _ = timed(0, False, False)
     value_full = cells_total * args.steps / (ms_full / 1000.0)
+    _, st_full, _, _ = timed(0, False, True)
     set_mode(1)
 
     pk, pk_src = peaks()
@@ -408,7 +413,10 @@ def main():
                     "frac": ach_gbs / hbm_peak, "frac_vs_nominal_8000": ach_gbs / 8000.0,
                     "traffic": prof.get("copy_dram_bytes_per_launch") if prof else None,
                     "kernel": "k_copy_classify<4,16> (dominant: streams q_old -> q_new, classifies patches)",
-                    "launch_ms": copy_ms, "share_of_step": copy_ms / (ms / args.steps),
+                    "launch_ms": copy_ms, "share_of_step": copy_ms / (ms_i / args.steps),
+                    "timing": "kernel durations from CUDA events on the library stream in an instrumented "
+                              "twin of the timed region (same steps from the same state); the headline "
+                              "pass runs without the library's events",
                     "algorithmic_bytes_per_cell_update": bpc,
                     "peak_source": f"{pk_src} MEASURED_PEAKS.json hbm_gbs (copy)"}
     else:

@@ -180,6 +180,12 @@ struct fc_forest {
   bool timing = false;
   cudaEvent_t ev[6] = {};
   bool copy_timed = false;             // ev[4] / ev[5] bracket the quiescent copy of this step
+  // fc_step's timing events are read lazily (fc_get_stats): per step it only records events, so
+  // the instrumented loop runs at the uninstrumented pace (elapsed-time queries after each step's
+  // synchronisation kept the GPU idle: C5 0.92 -> 1.07 ms per step)
+  struct PendingTiming { cudaEvent_t e[6]; bool copy; };
+  std::vector<PendingTiming> t_pending;
+  std::vector<cudaEvent_t> t_pool, t_all;
 };
 
 static int to_dev(fc_forest* f, const std::vector<int32_t>& v, int rec, DevList& out) {
@@ -474,13 +480,15 @@ static int update_local(fc_forest* f, double dt) {
   if (want_filter && !(f->active_frac >= 0.75 && !probe)) {
     // copy/classify + activity filter, then the step over the active patches' tiles only
     CK(cudaMemsetAsync(f->d_nactive, 0, sizeof(int32_t), f->stream));
+    static const bool env_tc = !(getenv("FC_TIME_COPY") && atoi(getenv("FC_TIME_COPY")) == 0);
+    const bool time_copy = f->timing && env_tc;
     const int fr = launch_filter(p.kind, f->qold, f->qnew, (int)f->Pl, f->pl.m, f->d_uflag, f->d_uval, f->d_nbr,
                                  f->d_negmask, f->d_level, dt, f->pl.dx0, p.p0, p.p1, f->d_active, f->d_nactive,
-                                 f->d_cfl, f->stream, f->timing ? f->ev[4] : nullptr, f->timing ? f->ev[5] : nullptr);
+                                 f->d_cfl, f->stream, time_copy ? f->ev[4] : nullptr, time_copy ? f->ev[5] : nullptr);
     if (fr > 0) {
       f->st.kernel_launches += fr;
       filtered = true;
-      f->copy_timed = f->timing;
+      f->copy_timed = time_copy;
     }
   } else if (want_filter) {
     f->probe_countdown -= 1;
@@ -570,11 +578,32 @@ static void destroy(fc_forest* f) {
     for (auto& l : f->bcy_l) free_list(l);
     for (int r = 0; r < 2; ++r) { cudaFree(f->d_pack[r]); cudaFree(f->d_unpack[r]); }
     cudaFree(f->d_sendbuf); cudaFree(f->d_recvbuf);
-    for (auto& e : f->ev) if (e) cudaEventDestroy(e);
+    for (auto& e : f->t_all) cudaEventDestroy(e);
     if (f->comm) ncclCommDestroy(f->comm);
     if (f->own_stream) cudaStreamDestroy(f->own_stream);
   }
   delete f;
+}
+
+// accumulate the pending fc_step timing events into the stats and recycle them
+static void timing_drain(fc_forest* f) {
+  for (auto& p : f->t_pending) {
+    float a = 0.f, b = 0.f, c = 0.f;
+    cudaEventElapsedTime(&a, p.e[0], p.e[1]);
+    cudaEventElapsedTime(&b, p.e[1], p.e[2]);
+    cudaEventElapsedTime(&c, p.e[2], p.e[3]);
+    f->st.ms_ghost += a;
+    f->st.ms_step += b;
+    f->st.ms_comm += c;
+    if (p.copy) {
+      float d = 0.f;
+      cudaEventElapsedTime(&d, p.e[4], p.e[5]);
+      f->st.ms_copy += d;
+      f->st.copy_launches += 1;
+    }
+    for (int k = 0; k < 6; ++k) f->t_pool.push_back(p.e[k]);
+  }
+  f->t_pending.clear();
 }
 
 // reflux across rank cuts: pack list (freg offsets of the served records) and the per-peer send /
@@ -721,8 +750,10 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
   if ((e = cudaMalloc(&f->d_cfl, sizeof(unsigned long long))) != cudaSuccess) return cuda_fail(e, "cudaMalloc cfl");
   if ((e = cudaMallocHost(&f->h_cfl, sizeof(double))) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
   if ((e = cudaMallocHost(&f->h_nact, sizeof(int32_t))) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
-  for (auto& ev : f->ev)
+  for (auto& ev : f->ev) {
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+    f->t_all.push_back(ev);            // (every event the handle owns, destroyed once)
+  }
   rc = plan_lists(f->pl, pl.meqn, f->gl, err);
   if (rc) { destroy(f); return fail(rc, err); }
   if ((rc = to_dev(f, f->gl.copy, 2, f->copy)) || (rc = to_dev(f, f->gl.avg, 5, f->avg)) ||
@@ -916,12 +947,22 @@ int fc_set_timing(fc_forest* f, int on) {
 
 int fc_get_stats(fc_forest* f, fc_stats* out) {
   if (!f || !out) return fail(FC_EINVAL, "null argument");
+  if (!f->t_pending.empty()) {
+    CK(cudaSetDevice(f->device));
+    CK(cudaStreamSynchronize(f->stream));
+    timing_drain(f);
+  }
   *out = f->st;
   return FC_OK;
 }
 
 int fc_reset_stats(fc_forest* f) {
   if (!f) return fail(FC_EINVAL, "null handle");
+  if (!f->t_pending.empty()) {
+    CK(cudaSetDevice(f->device));
+    CK(cudaStreamSynchronize(f->stream));
+    timing_drain(f);   // (then zeroed below)
+  }
   f->st.kernel_launches = 0;
   f->st.steps = 0;
   f->st.ms_ghost = f->st.ms_step = f->st.ms_comm = f->st.ms_copy = 0.0;
@@ -1040,6 +1081,19 @@ int fc_step(fc_forest* f, double dt, double* max_cfl) {
   if (rc) return rc;
   if (f->manual) return fail(FC_ESTATE, "manual halo transport: use fc_halo_* / fc_step_local / fc_commit");
   CK(cudaSetDevice(f->device));
+  f->copy_timed = false;
+  if (f->timing) {   // fresh events for this step (read at fc_get_stats)
+    for (int k = 0; k < 6; ++k) {
+      if (f->t_pool.empty()) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        f->t_all.push_back(e);
+        f->t_pool.push_back(e);
+      }
+      f->ev[k] = f->t_pool.back();
+      f->t_pool.pop_back();
+    }
+  }
   if (f->timing) CK(cudaEventRecord(f->ev[0], f->stream));
   // fused ring gather + quiescent filter when skipping is on (rings never written); otherwise the
   // ghost kernels fill the rings and every tile is bulk-copied whole (faster for the full update)
@@ -1056,20 +1110,12 @@ int fc_step(fc_forest* f, double dt, double* max_cfl) {
   CK(cudaStreamSynchronize(f->stream));
   note_activity(f);
   if (f->timing) {
-    float a = 0.f, b = 0.f, c = 0.f;
-    cudaEventElapsedTime(&a, f->ev[0], f->ev[1]);
-    cudaEventElapsedTime(&b, f->ev[1], f->ev[2]);
-    cudaEventElapsedTime(&c, f->ev[2], f->ev[3]);
-    if (f->copy_timed) {
-      float d = 0.f;
-      cudaEventElapsedTime(&d, f->ev[4], f->ev[5]);
-      f->st.ms_copy += d;
-      f->st.copy_launches += 1;
-      f->copy_timed = false;
-    }
-    f->st.ms_ghost += a;
-    f->st.ms_step += b;
-    f->st.ms_comm += c;
+    fc_forest::PendingTiming p;
+    for (int k = 0; k < 6; ++k) p.e[k] = f->ev[k];
+    p.copy = f->copy_timed;
+    f->copy_timed = false;
+    f->t_pending.push_back(p);
+    if (f->t_pending.size() >= 4096) timing_drain(f);
   }
   const double cfl = *f->h_cfl;
   if (max_cfl) *max_cfl = cfl;
@@ -1077,6 +1123,7 @@ int fc_step(fc_forest* f, double dt, double* max_cfl) {
 }
 
 // ---- multi-step fixed-dt run in CUDA graphs ---------------------------------------------------------
+// (timing_drain: see fc_forest::t_pending)
 // The device part of one step (ghost fill or fused gather, quiescent filter, update, CFL into the
 // history) is captured once per buffer parity and replayed nsteps times with no host round trip;
 // the CFLs are checked at the end.  If any exceeds cfl_reject (or is not finite) the run is undone
@@ -1339,6 +1386,10 @@ int fc_step_subcycled(fc_forest* f, double dt_coarse, double* max_cfl) {
   if ((rc = sub_prepare(f))) return rc;
   if (f->prob.reflux && f->nrcells > 0 && !f->d_facc)
     CK(cudaMalloc(&f->d_facc, (size_t)std::max<int32_t>(1, f->nslots) * 4 * f->pl.m * f->pl.meqn * sizeof(double)));
+  if (f->timing && !f->t_pending.empty()) {   // (f->ev may be pending events of fc_step)
+    CK(cudaStreamSynchronize(f->stream));
+    timing_drain(f);
+  }
   if (f->timing) CK(cudaEventRecord(f->ev[0], f->stream));
   CK(cudaMemsetAsync(f->d_cfl, 0, sizeof(unsigned long long), f->stream));
   f->sub_dt0 = dt_coarse;
