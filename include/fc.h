@@ -197,6 +197,23 @@ typedef struct {
 } fc_regrid_params;
 int fc_regrid(fc_forest* f, const fc_regrid_params* rp, fc_forest** out);
 
+/* Multi-rank regrid (SURVEY §8(f) #3 "Morton repartition + NCCL migration").  On NCCL handles
+ * fc_regrid is collective: ghost fill with halo, local tags, all-gathered tags, the same global
+ * plan on every rank, a new handle partitioned by count over the same ranks (its NCCL id broadcast
+ * from rank 0), and migration of the old padded blocks each new patch reads from their old owners
+ * (grouped send/recv), then the transfer.  Manual transport, per rank: halo round 1,
+ * fc_regrid_fill(1), halo round 2, fc_regrid_fill(2) (rings filled); fc_regrid_tags (the local
+ * patches' tags, host); fc_regrid_begin with the concatenation of all ranks' tags (global patch
+ * order) -> the new handle; copy recv_g[recv_off[s]..] <- send_s[send_off_s[me]..] between ranks
+ * (fc_regrid_buffers(old, new): device pointers, offsets in doubles, [nranks + 1]; the own part is
+ * already in place); fc_regrid_finish(new).  The new handle then needs its halo requests (and
+ * reflux requests) set as any manual handle. */
+int fc_regrid_fill(fc_forest* f, int phase);
+int fc_regrid_tags(fc_forest* f, double* tags);
+int fc_regrid_begin(fc_forest* f, const double* global_tags, const fc_regrid_params* params, fc_forest** out);
+int fc_regrid_buffers(fc_forest* f, fc_forest* g, void** send, void** recv, int64_t* send_off, int64_t* recv_off);
+int fc_regrid_finish(fc_forest* g);
+
 /* The forest's leaves in global Morton order: levels[P], tree_ids[P] (either may be NULL; both NULL
  * = size query); *num_patches = P.  FC_EINVAL if cap < P. */
 int fc_get_leaves(fc_forest* f, int8_t* levels, int32_t* tree_ids, int64_t cap, int64_t* num_patches);

@@ -36,6 +36,7 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
                 const double* cg, cudaStream_t st);
 int launch_cg(int op, const double* q, double* cg, const int32_t* list, int64_t nrec, int meqn, int n2,
               cudaStream_t st);
+int launch_copy_blocks(const double* src, double* dst, const int32_t* ids, int64_t nb, int64_t S, cudaStream_t st);
 int launch_reflux(const int32_t* cells, int64_t ncells, const double* freg, const double* ffine, double* qnew,
                   const double* aux, const int8_t* level, double wc, double dtr, double dx0, int meqn, int n2,
                   cudaStream_t st);
@@ -132,6 +133,14 @@ struct fc_forest {
   double* d_rf_send = nullptr;
   std::vector<int64_t> rf_send_off, rf_recv_off;   // [R + 1], doubles
   bool rf_ready = true;                // manual transport: false until fc_reflux_finalize
+  // multi-rank regrid migration: old side (the blocks this rank sends, per new rank) and new side
+  // (the staged old blocks this rank's new patches read, per old owner, and their source records)
+  double* d_rg_send = nullptr;
+  std::vector<int64_t> rg_send_off;    // [R + 1], doubles
+  double* d_rg_stage = nullptr;
+  std::vector<int64_t> rg_recv_off;    // [R + 1], doubles
+  int32_t* d_rg_src = nullptr;
+  bool rg_pending = false;
   std::vector<int64_t> rcell_off;      // reflux cells sorted by coarse level: [level - glmin] offsets
   // sub-cycling (fc_step_subcycled): levels [glmin, glmax] of the whole forest, per-level local lists
   int glmin = 0, glmax = 0;
@@ -552,6 +561,7 @@ static void destroy(fc_forest* f) {
     cudaFree(f->d_uflag); cudaFree(f->d_uval);
     cudaFree(f->d_rslot); cudaFree(f->d_rcells); cudaFree(f->d_freg);
     cudaFree(f->d_rf_pack); cudaFree(f->d_rf_send);
+    cudaFree(f->d_rg_send); cudaFree(f->d_rg_stage); cudaFree(f->d_rg_src);
     cudaFree(f->d_rpeer);
     cudaFree(f->d_cg);
     free_list(f->cg_avg);
@@ -1413,14 +1423,17 @@ int fc_step_subcycled(fc_forest* f, double dt_coarse, double* max_cfl) {
 }
 
 // ---- dynamic regrid -------------------------------
+static int regrid_nccl(fc_forest* f, const fc_regrid_params* rp, fc_forest** out);
+
 int fc_regrid(fc_forest* f, const fc_regrid_params* rp, fc_forest** out) {
   if (!f || !rp || !out) return fail(FC_EINVAL, "null argument");
   *out = nullptr;
   if (f->host_only || !f->has_q || !f->has_problem) return fail(FC_ESTATE, "set problem and q first");
-  if (f->pl.nranks != 1) return fail(FC_EUNSUP, "regrid runs on one rank (no repartition / migration yet)");
   if (rp->min_level < 0 || rp->max_level < rp->min_level || rp->max_level > 28)
     return fail(FC_EINVAL, "regrid level bounds out of range");
+  if (f->manual) return fail(FC_ESTATE, "manual transport: use fc_regrid_fill / _tags / _begin / _finish");
   CK(cudaSetDevice(f->device));
+  if (f->pl.nranks > 1) return regrid_nccl(f, rp, out);
   int rc = ghost_fill_internal(f);                 // the interpolation slopes read the parents' rings
   if (rc) return rc;
   const int m = f->pl.m, meqn = f->pl.meqn;
@@ -1471,6 +1484,231 @@ int fc_regrid(fc_forest* f, const fc_regrid_params* rp, fc_forest** out) {
   g->has_q = true;
   *out = g;
   return FC_OK;
+}
+
+// ---- multi-rank regrid: the same global plan on every rank, Morton repartition by count of the
+// new leaves, migration of the old padded blocks each new patch reads (copy: its old patch; child:
+// the ghost-filled parent; parent: the 4 old children) from their old owners ----------------------
+static int regrid_local_tags(fc_forest* f, std::vector<double>& tag) {
+  const int m = f->pl.m, meqn = f->pl.meqn;
+  double* d_tag = nullptr;
+  CK(cudaMalloc(&d_tag, std::max<int64_t>(1, f->Pl) * sizeof(double)));
+  f->st.kernel_launches += launch_regrid_tag(f->qold, f->Pl, meqn, m, d_tag, f->stream);
+  tag.assign(f->Pl, 0.0);
+  if (f->Pl) CK(cudaMemcpyAsync(tag.data(), d_tag, f->Pl * sizeof(double), cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  cudaFree(d_tag);
+  return FC_OK;
+}
+
+// plan + new handle + migration buffers (old side packed, self part staged); g's transfer waits
+// for the other owners' blocks (regrid_finish)
+static int regrid_begin(fc_forest* f, const double* gtag, const fc_regrid_params* rp, const void* nccl_id,
+                        fc_forest** out) {
+  const int m = f->pl.m, meqn = f->pl.meqn, R = f->pl.nranks, me = f->pl.rank;
+  const int64_t S = (int64_t)meqn * f->pl.n * f->pl.n, Pold = f->pl.P;
+  std::vector<int8_t> lv;
+  std::vector<int32_t> tr, src;
+  std::string err;
+  int rc = plan_regrid(f->pl, gtag, rp->refine_threshold, rp->coarsen_threshold, rp->min_level, rp->max_level,
+                       lv, tr, src, err);
+  if (rc) return fail(rc, err);
+  const int64_t Pnew = (int64_t)lv.size();
+  fc_forest_desc d{};
+  d.num_patches = Pnew;
+  d.levels = lv.data();
+  d.tree_ids = tr.data();
+  d.num_trees = f->pl.T;
+  d.tree_to_tree = f->pl.t2t.data();
+  d.tree_to_face = f->pl.t2f.data();
+  d.face_bc = f->pl.fbc.data();
+  d.m = m;
+  d.mbc = 2;
+  d.meqn = meqn;
+  d.maux = f->pl.maux;
+  d.tree_dx0 = f->pl.dx0 * m;
+  d.device = f->device;
+  d.rank = me;
+  d.nranks = R;
+  d.nccl_id = nccl_id;
+  fc_forest* g = nullptr;
+  if ((rc = fc_forest_create(&d, &g))) return rc;
+  if ((rc = fc_set_problem(g, &f->prob))) { fc_forest_destroy(g); return rc; }
+  auto old_first = [&](int r) { return (int64_t)r * Pold / R; };
+  auto new_first = [&](int r) { return (int64_t)r * Pnew / R; };
+  auto old_owner = [&](int64_t j) {
+    int64_t r = j * R / Pold;
+    while (r > 0 && old_first((int)r) > j) --r;
+    while (r + 1 < R && old_first((int)r + 1) <= j) ++r;
+    return (int)r;
+  };
+  // the old blocks rank rr's new patches read, sorted (the 4 children of a parent are consecutive)
+  auto referenced = [&](int rr) {
+    std::vector<int32_t> ids;
+    for (int64_t i = new_first(rr); i < new_first(rr + 1); ++i) {
+      const int32_t* s = src.data() + i * 3;
+      if (s[0] == 3) for (int k = 0; k < 4; ++k) ids.push_back(s[1] + k);
+      else ids.push_back(s[1]);
+    }
+    std::sort(ids.begin(), ids.end());
+    ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+    return ids;
+  };
+  // new side: staging slots in old-id order = owner-major
+  const std::vector<int32_t> mine = referenced(me);
+  g->rg_recv_off.assign(R + 1, 0);
+  for (int32_t j : mine) g->rg_recv_off[old_owner(j) + 1] += S;
+  for (int r = 0; r < R; ++r) g->rg_recv_off[r + 1] += g->rg_recv_off[r];
+  std::vector<int32_t> lsrc(src.begin() + new_first(me) * 3, src.begin() + new_first(me + 1) * 3);
+  for (size_t i = 0; i < lsrc.size(); i += 3)
+    lsrc[i + 1] = (int32_t)(std::lower_bound(mine.begin(), mine.end(), lsrc[i + 1]) - mine.begin());
+  CK(cudaSetDevice(f->device));
+  CK(cudaMalloc(&g->d_rg_stage, std::max<size_t>(1, mine.size()) * S * sizeof(double)));
+  CK(cudaMalloc(&g->d_rg_src, std::max<size_t>(1, lsrc.size()) * sizeof(int32_t)));
+  if (!lsrc.empty()) CK(cudaMemcpy(g->d_rg_src, lsrc.data(), lsrc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  // old side: per new rank the blocks of mine it reads, packed (local ids)
+  std::vector<int32_t> ids;
+  f->rg_send_off.assign(R + 1, 0);
+  int64_t self_off = 0, self_n = 0;
+  for (int r = 0; r < R; ++r) {
+    const std::vector<int32_t> ref = r == me ? mine : referenced(r);
+    if (r == me) self_off = (int64_t)ids.size();
+    for (int32_t j : ref)
+      if (j >= f->pl.p0 && j < f->pl.p1) ids.push_back((int32_t)(j - f->pl.p0));
+    if (r == me) self_n = (int64_t)ids.size() - self_off;
+    f->rg_send_off[r + 1] = (int64_t)ids.size() * S;
+  }
+  cudaFree(f->d_rg_send);
+  f->d_rg_send = nullptr;
+  CK(cudaMalloc(&f->d_rg_send, std::max<size_t>(1, ids.size()) * S * sizeof(double)));
+  int32_t* d_ids = nullptr;
+  CK(cudaMalloc(&d_ids, std::max<size_t>(1, ids.size()) * sizeof(int32_t)));
+  if (!ids.empty()) CK(cudaMemcpy(d_ids, ids.data(), ids.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  f->st.kernel_launches += launch_copy_blocks(f->qold, f->d_rg_send, d_ids, (int64_t)ids.size(), S, f->stream);
+  if (self_n)   // this rank's own blocks go straight to its staging
+    CK(cudaMemcpyAsync(g->d_rg_stage + g->rg_recv_off[me], f->d_rg_send + self_off * S, self_n * S * sizeof(double),
+                       cudaMemcpyDeviceToDevice, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  cudaFree(d_ids);
+  g->rg_pending = true;
+  *out = g;
+  return FC_OK;
+}
+
+static int regrid_finish(fc_forest* g) {
+  if (!g->rg_pending) return fail(FC_ESTATE, "no regrid in progress on this handle");
+  CK(cudaSetDevice(g->device));
+  g->st.kernel_launches += launch_regrid_transfer(g->d_rg_stage, g->qold, g->d_rg_src, g->Pl, g->pl.meqn, g->pl.m,
+                                                  g->stream);
+  CK(cudaStreamSynchronize(g->stream));
+  cudaFree(g->d_rg_stage);
+  cudaFree(g->d_rg_src);
+  g->d_rg_stage = nullptr;
+  g->d_rg_src = nullptr;
+  g->rg_pending = false;
+  g->has_q = true;
+  return FC_OK;
+}
+
+// NCCL handles: every step of the above inside one collective call
+static int regrid_nccl(fc_forest* f, const fc_regrid_params* rp, fc_forest** out) {
+  const int R = f->pl.nranks, me = f->pl.rank;
+  int rc = ghost_fill_internal(f);                 // (halo rounds included)
+  if (rc) return rc;
+  std::vector<double> tag;
+  if ((rc = regrid_local_tags(f, tag))) return rc;
+  // all-gather the tags (padded to the largest shard)
+  int64_t maxpl = 0;
+  for (int r = 0; r < R; ++r) maxpl = std::max(maxpl, (int64_t)(r + 1) * f->pl.P / R - (int64_t)r * f->pl.P / R);
+  double *d_mine = nullptr, *d_all = nullptr;
+  CK(cudaMalloc(&d_mine, std::max<int64_t>(1, maxpl) * sizeof(double)));
+  CK(cudaMalloc(&d_all, std::max<int64_t>(1, maxpl) * R * sizeof(double)));
+  if (f->Pl) CK(cudaMemcpy(d_mine, tag.data(), f->Pl * sizeof(double), cudaMemcpyHostToDevice));
+  NK(ncclAllGather(d_mine, d_all, std::max<int64_t>(1, maxpl), ncclDouble, f->comm, f->stream));
+  std::vector<double> all((size_t)std::max<int64_t>(1, maxpl) * R), gtag(f->pl.P);
+  CK(cudaMemcpyAsync(all.data(), d_all, all.size() * sizeof(double), cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  cudaFree(d_mine);
+  cudaFree(d_all);
+  for (int r = 0; r < R; ++r) {
+    const int64_t a = (int64_t)r * f->pl.P / R, b = (int64_t)(r + 1) * f->pl.P / R;
+    std::copy(all.begin() + (size_t)r * std::max<int64_t>(1, maxpl), all.begin() + (size_t)r * std::max<int64_t>(1, maxpl) + (b - a),
+              gtag.begin() + a);
+  }
+  // a fresh NCCL id for the new handle's communicator, broadcast from rank 0 over the old one
+  char id[128] = {};
+  if (me == 0 && (rc = fc_nccl_unique_id(id))) return rc;
+  char* d_id = nullptr;
+  CK(cudaMalloc(&d_id, sizeof(id)));
+  CK(cudaMemcpy(d_id, id, sizeof(id), cudaMemcpyHostToDevice));
+  NK(ncclBroadcast(d_id, d_id, sizeof(id), ncclChar, 0, f->comm, f->stream));
+  CK(cudaMemcpyAsync(id, d_id, sizeof(id), cudaMemcpyDeviceToHost, f->stream));
+  CK(cudaStreamSynchronize(f->stream));
+  cudaFree(d_id);
+  fc_forest* g = nullptr;
+  if ((rc = regrid_begin(f, gtag.data(), rp, id, &g))) return rc;
+  NK(ncclGroupStart());
+  for (int s = 0; s < R; ++s) {
+    if (s == me) continue;
+    const int64_t ns = f->rg_send_off[s + 1] - f->rg_send_off[s], nr = g->rg_recv_off[s + 1] - g->rg_recv_off[s];
+    if (ns) NK(ncclSend(f->d_rg_send + f->rg_send_off[s], ns, ncclDouble, s, f->comm, f->stream));
+    if (nr) NK(ncclRecv(g->d_rg_stage + g->rg_recv_off[s], nr, ncclDouble, s, f->comm, f->stream));
+  }
+  NK(ncclGroupEnd());
+  CK(cudaStreamSynchronize(f->stream));
+  cudaFree(f->d_rg_send);
+  f->d_rg_send = nullptr;
+  if ((rc = regrid_finish(g))) { fc_forest_destroy(g); return rc; }
+  *out = g;
+  return FC_OK;
+}
+
+int fc_regrid_fill(fc_forest* f, int phase) {
+  if (!f) return fail(FC_EINVAL, "null handle");
+  if (!f->manual) return fail(FC_ESTATE, "not a manual-transport handle (fc_regrid does it all)");
+  if (f->host_only || !f->has_q) return fail(FC_ESTATE, "no state");
+  CK(cudaSetDevice(f->device));
+  int rc = phase == 1 ? ghost_phase_ac(f) : (phase == 2 ? ghost_phase_b(f) : fail(FC_EINVAL, "phase must be 1 or 2"));
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(f->stream));
+  return FC_OK;
+}
+
+int fc_regrid_tags(fc_forest* f, double* tags) {
+  if (!f || !tags) return fail(FC_EINVAL, "null argument");
+  if (f->host_only || !f->has_q) return fail(FC_ESTATE, "no state");
+  CK(cudaSetDevice(f->device));
+  std::vector<double> t;
+  int rc = regrid_local_tags(f, t);
+  if (rc) return rc;
+  std::copy(t.begin(), t.end(), tags);
+  return FC_OK;
+}
+
+int fc_regrid_begin(fc_forest* f, const double* global_tags, const fc_regrid_params* rp, fc_forest** out) {
+  if (!f || !global_tags || !rp || !out) return fail(FC_EINVAL, "null argument");
+  *out = nullptr;
+  if (!f->manual) return fail(FC_ESTATE, "not a manual-transport handle (fc_regrid does it all)");
+  if (f->host_only || !f->has_q || !f->has_problem) return fail(FC_ESTATE, "set problem and q first");
+  if (rp->min_level < 0 || rp->max_level < rp->min_level || rp->max_level > 28)
+    return fail(FC_EINVAL, "regrid level bounds out of range");
+  CK(cudaSetDevice(f->device));
+  return regrid_begin(f, global_tags, rp, nullptr, out);
+}
+
+int fc_regrid_buffers(fc_forest* f, fc_forest* g, void** send, void** recv, int64_t* send_off, int64_t* recv_off) {
+  if (!f || !g || !send || !recv || !send_off || !recv_off) return fail(FC_EINVAL, "null argument");
+  if (!g->rg_pending || f->rg_send_off.size() != (size_t)f->pl.nranks + 1) return fail(FC_ESTATE, "no regrid in progress");
+  *send = f->d_rg_send;
+  *recv = g->d_rg_stage;
+  std::copy(f->rg_send_off.begin(), f->rg_send_off.end(), send_off);
+  std::copy(g->rg_recv_off.begin(), g->rg_recv_off.end(), recv_off);
+  return FC_OK;
+}
+
+int fc_regrid_finish(fc_forest* g) {
+  if (!g) return fail(FC_EINVAL, "null handle");
+  return regrid_finish(g);
 }
 
 int fc_get_leaves(fc_forest* f, int8_t* levels, int32_t* tree_ids, int64_t cap, int64_t* num_patches) {

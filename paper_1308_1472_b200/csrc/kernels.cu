@@ -199,6 +199,22 @@ int launch_cg(int op, const double* q, double* cg, const int32_t* list, int64_t 
   return 1;
 }
 
+// whole padded patch blocks (S doubles each): dst block b = src block ids[b] (regrid migration)
+__global__ void k_copy_blocks(const double* __restrict__ src, double* __restrict__ dst,
+                              const int32_t* __restrict__ ids, int64_t nb, int64_t S) {
+  const int64_t tot = nb * S;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / S;
+    dst[t] = src[(int64_t)ids[b] * S + (t - b * S)];
+  }
+}
+
+int launch_copy_blocks(const double* src, double* dst, const int32_t* ids, int64_t nb, int64_t S, cudaStream_t st) {
+  if (nb <= 0) return 0;
+  k_copy_blocks<<<148 * 8, 256, 0, st>>>(src, dst, ids, nb, S);
+  return 1;
+}
+
 int launch_pack(const double* q, const int32_t* idx, int64_t cnt, int meqn, int n2, double* buf,
                 cudaStream_t st) {
   if (cnt <= 0) return 0;

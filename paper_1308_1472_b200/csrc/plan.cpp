@@ -831,7 +831,7 @@ static int leaves_at(const Plan& pl, int t, int64_t X, int64_t Y, int64_t out[2]
 int plan_regrid(const Plan& pl, const double* tag, double refine_threshold, double coarsen_threshold,
                 int min_level, int max_level, std::vector<int8_t>& new_levels, std::vector<int32_t>& new_trees,
                 std::vector<int32_t>& src, std::string& err) {
-  if (pl.nranks != 1) { err = "regrid runs on one rank"; return FC_EUNSUP; }
+  // (the plan is global: every rank runs it on the same leaves and the gathered tags)
   if (max_level > 28 || min_level < 0) { err = "regrid levels out of range"; return FC_EINVAL; }
   const int64_t P = pl.P, m2 = 2 * (int64_t)pl.m;
   std::vector<uint8_t> refine((size_t)P, 0), coarsen((size_t)P, 0);

@@ -35,7 +35,8 @@ EXPORTS = ["fc_forest_create", "fc_forest_destroy", "fc_set_problem", "fc_set_au
            "fc_halo_buffers", "fc_halo_pack", "fc_halo_unpack", "fc_step_local", "fc_commit",
            "fc_nccl_unique_id", "fc_last_error", "fc_step_subcycled", "fc_regrid", "fc_get_leaves",
            "fc_p2p_buffers", "fc_p2p_set_peer", "fc_run", "fc_reflux_requests", "fc_reflux_set_requests",
-           "fc_reflux_finalize", "fc_reflux_buffers"]
+           "fc_reflux_finalize", "fc_reflux_buffers", "fc_regrid_fill", "fc_regrid_tags", "fc_regrid_begin",
+           "fc_regrid_buffers", "fc_regrid_finish"]
 
 
 class FcError(RuntimeError):
@@ -117,6 +118,11 @@ def lib():
         L.fc_reflux_set_requests.argtypes = [P, C.c_int, P, C.c_int64]
         L.fc_reflux_finalize.argtypes = [P]
         L.fc_reflux_buffers.argtypes = [P, C.POINTER(P), C.POINTER(P), P, P]
+        L.fc_regrid_fill.argtypes = [P, C.c_int]
+        L.fc_regrid_tags.argtypes = [P, P]
+        L.fc_regrid_begin.argtypes = [P, P, C.POINTER(RegridParams), C.POINTER(P)]
+        L.fc_regrid_buffers.argtypes = [P, P, C.POINTER(P), C.POINTER(P), P, P]
+        L.fc_regrid_finish.argtypes = [P]
         L.fc_halo_pack.argtypes = [P, C.c_int]
         L.fc_halo_unpack.argtypes = [P, C.c_int]
         L.fc_step_local.argtypes = [P, C.c_double, C.c_int, C.POINTER(C.c_double)]
@@ -231,14 +237,7 @@ class Forest:
         rp = RegridParams(refine_threshold, coarsen_threshold, min_level, max_level)
         h = C.c_void_p()
         _check(lib().fc_regrid(self.h, C.byref(rp), C.byref(h)), "fc_regrid")
-        g = Forest.__new__(Forest)
-        g.h = h
-        g._keep, g._nid = [], None
-        g.m, g.meqn, g.maux, g.n = self.m, self.meqn, self.maux, self.n
-        first, count = C.c_int64(), C.c_int64()
-        _check(lib().fc_local_range(h, C.byref(first), C.byref(count)), "fc_local_range")
-        g.first, g.count, g.nranks = first.value, count.value, 1
-        return g
+        return self._wrap(h)
 
     def p2p_buffers(self):
         """(buf0, buf1, parity): this rank's two state buffers (device addresses) and which is q_old."""
@@ -312,6 +311,44 @@ class Forest:
 
     def halo_finalize(self):
         _check(lib().fc_halo_finalize(self.h), "fc_halo_finalize")
+
+    def _wrap(self, h):
+        g = Forest.__new__(Forest)
+        g.h = h
+        g._keep, g._nid = [], None
+        g.m, g.meqn, g.maux, g.n = self.m, self.meqn, self.maux, self.n
+        first, count = C.c_int64(), C.c_int64()
+        _check(lib().fc_local_range(h, C.byref(first), C.byref(count)), "fc_local_range")
+        g.first, g.count, g.nranks = first.value, count.value, self.nranks
+        return g
+
+    def regrid_fill(self, phase: int):
+        _check(lib().fc_regrid_fill(self.h, phase), "fc_regrid_fill")
+
+    def regrid_tags(self) -> np.ndarray:
+        t = np.zeros(max(1, self.count))
+        _check(lib().fc_regrid_tags(self.h, t.ctypes.data_as(C.c_void_p)), "fc_regrid_tags")
+        return t[:self.count]
+
+    def regrid_begin(self, global_tags: np.ndarray, refine_threshold: float, coarsen_threshold: float,
+                     min_level: int, max_level: int):
+        gt = np.ascontiguousarray(global_tags, np.float64)
+        rp = RegridParams(refine_threshold, coarsen_threshold, min_level, max_level)
+        h = C.c_void_p()
+        _check(lib().fc_regrid_begin(self.h, gt.ctypes.data_as(C.c_void_p), C.byref(rp), C.byref(h)),
+               "fc_regrid_begin")
+        return self._wrap(h)
+
+    def regrid_buffers(self, new):
+        s, r = C.c_void_p(), C.c_void_p()
+        so = np.zeros(self.nranks + 1, np.int64)
+        ro = np.zeros(self.nranks + 1, np.int64)
+        _check(lib().fc_regrid_buffers(self.h, new.h, C.byref(s), C.byref(r), so.ctypes.data_as(C.c_void_p),
+                                       ro.ctypes.data_as(C.c_void_p)), "fc_regrid_buffers")
+        return s.value, r.value, so, ro
+
+    def regrid_finish(self):
+        _check(lib().fc_regrid_finish(self.h), "fc_regrid_finish")
 
     def reflux_requests(self, peer: int) -> np.ndarray:
         n = C.c_int64()
