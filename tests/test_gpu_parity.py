@@ -250,3 +250,15 @@ def test_constant_velocity_signs_against_oracle(uv, m, reflux):
     for skip in (1, 0):
         qg, cg, _ = fc.run(w, dt_list=do, skip_quiescent=skip)
         assert_parity(w, qg, qo, cg, co)
+
+
+@pytest.mark.parametrize("w", [c5(level=1, m=4, steps=10), c5(level=1, m=12, steps=10), c5(level=0, m=24, steps=10),
+                               c3(level=1, m=6, steps=10), c3(level=1, m=20, steps=10)], ids=lambda w: w.name)
+def test_systems_ragged_tilings_against_oracle(w):
+    """Systems on patch sizes that tile as 4 x 4 (m = 4), 3 x 3 tiles of 4 (m = 12), 3 x 3 of 8
+    (m = 24), 3 x 3 of 2 (m = 6) and 5 x 5 of 4 (m = 20), with walls (SWE) and outflow (Euler):
+    both update modes against the oracle."""
+    qo, co, do = oracle.run(w)
+    for skip in (1, 0):
+        qg, cg, _ = fc.run(w, dt_list=do, skip_quiescent=skip)
+        assert_parity(w, qg, qo, cg, co)
