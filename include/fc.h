@@ -90,6 +90,9 @@ typedef struct {
                                    mode wired with fc_p2p_set_peer) -- no pack / ncclSend/Recv / unpack
                                    pass (PAPER.md:264-272's ghost exchange fused into the gather); the
                                    CFL allreduce orders the steps across ranks.  0: halo exchange */
+  const int64_t* partition;     /* optional [nranks + 1] Morton cut points (0 = p_0 <= p_1 ... <= p_R =
+                                   num_patches; rank r owns [p_r, p_{r+1})), identical on every rank;
+                                   NULL: by count, [floor(rP/R), floor((r+1)P/R)) */
 } fc_forest_desc;
 
 typedef struct {
@@ -194,6 +197,9 @@ int fc_run(fc_forest* f, double dt, int64_t nsteps, double* cfls, double* max_cf
 typedef struct {
   double refine_threshold, coarsen_threshold;
   int32_t min_level, max_level;
+  int32_t level_weights;        /* multi-rank: 1 = cut the new Morton order into equal sums of
+                                   2^(level - coarsest level) (the work of a sub-cycled step), 0 = by count */
+  int32_t pad_;
 } fc_regrid_params;
 int fc_regrid(fc_forest* f, const fc_regrid_params* rp, fc_forest** out);
 

@@ -1514,6 +1514,20 @@ static int regrid_begin(fc_forest* f, const double* gtag, const fc_regrid_params
                        lv, tr, src, err);
   if (rc) return fail(rc, err);
   const int64_t Pnew = (int64_t)lv.size();
+  // new Morton partition: by count, or (level_weights) equal sums of 2^(level - coarsest)
+  std::vector<int64_t> part(R + 1, 0);
+  if (rp->level_weights && R > 1) {
+    int lmin = 127;
+    for (int8_t l : lv) lmin = std::min(lmin, (int)l);
+    std::vector<double> cum(Pnew + 1, 0.0);
+    for (int64_t i = 0; i < Pnew; ++i) cum[i + 1] = cum[i] + std::ldexp(1.0, lv[i] - lmin);
+    for (int r = 1; r < R; ++r)   // first patch whose prefix weight reaches r / R of the total
+      part[r] = std::lower_bound(cum.begin(), cum.end(), cum[Pnew] * r / R) - cum.begin();
+    for (int r = 1; r < R; ++r) part[r] = std::max(part[r], part[r - 1]);
+  } else {
+    for (int r = 0; r <= R; ++r) part[r] = (int64_t)r * Pnew / R;
+  }
+  part[R] = Pnew;
   fc_forest_desc d{};
   d.num_patches = Pnew;
   d.levels = lv.data();
@@ -1531,17 +1545,17 @@ static int regrid_begin(fc_forest* f, const double* gtag, const fc_regrid_params
   d.rank = me;
   d.nranks = R;
   d.nccl_id = nccl_id;
+  d.partition = part.data();
   fc_forest* g = nullptr;
   if ((rc = fc_forest_create(&d, &g))) return rc;
   if ((rc = fc_set_problem(g, &f->prob))) { fc_forest_destroy(g); return rc; }
-  auto old_first = [&](int r) { return (int64_t)r * Pold / R; };
-  auto new_first = [&](int r) { return (int64_t)r * Pnew / R; };
+  auto old_first = [&](int r) { return f->pl.part[r]; };
+  auto new_first = [&](int r) { return part[r]; };
   auto old_owner = [&](int64_t j) {
-    int64_t r = j * R / Pold;
-    while (r > 0 && old_first((int)r) > j) --r;
-    while (r + 1 < R && old_first((int)r + 1) <= j) ++r;
-    return (int)r;
+    return (int)(std::upper_bound(f->pl.part.begin(), f->pl.part.end(), j) - f->pl.part.begin()) - 1;
   };
+  (void)old_first;
+  (void)Pold;
   // the old blocks rank rr's new patches read, sorted (the 4 children of a parent are consecutive)
   auto referenced = [&](int rr) {
     std::vector<int32_t> ids;
@@ -1619,7 +1633,7 @@ static int regrid_nccl(fc_forest* f, const fc_regrid_params* rp, fc_forest** out
   if ((rc = regrid_local_tags(f, tag))) return rc;
   // all-gather the tags (padded to the largest shard)
   int64_t maxpl = 0;
-  for (int r = 0; r < R; ++r) maxpl = std::max(maxpl, (int64_t)(r + 1) * f->pl.P / R - (int64_t)r * f->pl.P / R);
+  for (int r = 0; r < R; ++r) maxpl = std::max(maxpl, f->pl.part[r + 1] - f->pl.part[r]);
   double *d_mine = nullptr, *d_all = nullptr;
   CK(cudaMalloc(&d_mine, std::max<int64_t>(1, maxpl) * sizeof(double)));
   CK(cudaMalloc(&d_all, std::max<int64_t>(1, maxpl) * R * sizeof(double)));
@@ -1631,7 +1645,7 @@ static int regrid_nccl(fc_forest* f, const fc_regrid_params* rp, fc_forest** out
   cudaFree(d_mine);
   cudaFree(d_all);
   for (int r = 0; r < R; ++r) {
-    const int64_t a = (int64_t)r * f->pl.P / R, b = (int64_t)(r + 1) * f->pl.P / R;
+    const int64_t a = f->pl.part[r], b = f->pl.part[r + 1];
     std::copy(all.begin() + (size_t)r * std::max<int64_t>(1, maxpl), all.begin() + (size_t)r * std::max<int64_t>(1, maxpl) + (b - a),
               gtag.begin() + a);
   }

@@ -106,6 +106,7 @@ struct Plan {
   std::vector<int8_t> t2f, fbc;
   int rank = 0, nranks = 1;
   int64_t p0 = 0, p1 = 0;           // local range [p0, p1)
+  std::vector<int64_t> part;        // [nranks + 1] Morton cut points (rank r owns [part[r], part[r+1]))
   std::vector<int32_t> table;       // expanded records of local patches [Pl][G][8]
   HaloPlan halo;
   bool uniform_same = false;        // every ring cell is COPY/BC (no AVG/INTERP/CORNER3)

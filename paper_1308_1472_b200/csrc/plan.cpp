@@ -227,11 +227,8 @@ static int patch_records(const Plan& pl, int64_t p, int32_t* rec, std::string& e
   return FC_OK;
 }
 
-static int64_t owner_of(const Plan& pl, int64_t q) {
-  int64_t r = (q * pl.nranks) / pl.P;  // first guess, then fix up against the floor() ranges
-  while (r > 0 && (r * pl.P) / pl.nranks > q) --r;
-  while (r + 1 < pl.nranks && ((r + 1) * pl.P) / pl.nranks <= q) ++r;
-  return r;
+static int64_t owner_of(const Plan& pl, int64_t q) {   // the rank whose [part[r], part[r+1]) holds q
+  return (int64_t)(std::upper_bound(pl.part.begin(), pl.part.end(), q) - pl.part.begin()) - 1;
 }
 
 static inline bool is_ring(int m, int i, int j) { return !(i >= 1 && i <= m && j >= 1 && j <= m); }
@@ -293,8 +290,14 @@ int plan_build(const fc_forest_desc* d, Plan& pl, std::string& err) {
     if (c != full || p == first) { err = "tree not covered exactly"; return FC_ETILING; }
   }
   // local range and expanded table of local patches
-  pl.p0 = (pl.rank * pl.P) / pl.nranks;
-  pl.p1 = ((pl.rank + 1) * pl.P) / pl.nranks;
+  pl.part.assign(pl.nranks + 1, 0);
+  for (int r = 0; r <= pl.nranks; ++r)
+    pl.part[r] = d->partition ? d->partition[r] : ((int64_t)r * pl.P) / pl.nranks;
+  for (int r = 0; r < pl.nranks; ++r)
+    if (pl.part[r] > pl.part[r + 1]) { err = "partition not non-decreasing"; return FC_EINVAL; }
+  if (pl.part[0] != 0 || pl.part[pl.nranks] != pl.P) { err = "partition must cover 0..num_patches"; return FC_EINVAL; }
+  pl.p0 = pl.part[pl.rank];
+  pl.p1 = pl.part[pl.rank + 1];
   const int64_t Pl = pl.p1 - pl.p0, G = (int64_t)pl.n * pl.n - (int64_t)pl.m * pl.m;
   pl.table.assign((size_t)Pl * G * REC, 0);
   pl.uniform_same = true;
@@ -529,7 +532,7 @@ int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& er
         if (q >= pl.p0 && q < pl.p1) {
           v = (int32_t)((q - pl.p0) * S + qcell(o[2], o[3], n));
         } else if (p2p) {   // the owner's own state: its local patch index, same block layout
-          const int64_t ow = owner_of(pl, q), first = (ow * pl.P) / pl.nranks;
+          const int64_t ow = owner_of(pl, q), first = pl.part[ow];
           v = (int32_t)((q - first) * S + qcell(o[2], o[3], n));
           rs.peer[lp * G + r] = (uint8_t)(ow + 1);
         } else {

@@ -51,7 +51,7 @@ class ForestDesc(C.Structure):
                 ("face_bc", C.c_void_p), ("m", C.c_int32), ("mbc", C.c_int32), ("meqn", C.c_int32),
                 ("maux", C.c_int32), ("tree_dx0", C.c_double), ("device", C.c_int32),
                 ("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_id", C.c_void_p),
-                ("halo_p2p", C.c_int32)]
+                ("halo_p2p", C.c_int32), ("partition", C.c_void_p)]
 
 
 class Problem(C.Structure):
@@ -62,7 +62,8 @@ class Problem(C.Structure):
 
 class RegridParams(C.Structure):
     _fields_ = [("refine_threshold", C.c_double), ("coarsen_threshold", C.c_double),
-                ("min_level", C.c_int32), ("max_level", C.c_int32)]
+                ("min_level", C.c_int32), ("max_level", C.c_int32), ("level_weights", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -159,16 +160,19 @@ class Forest:
 
     def __init__(self, levels, tree_ids, conn, m: int, meqn: int, maux: int = 0,
                  tree_dx0: float = 1.0, device: int = 0, rank: int = 0, nranks: int = 1,
-                 nccl_id: bytes | None = None, halo_p2p: int = 0):
+                 nccl_id: bytes | None = None, halo_p2p: int = 0, partition=None):
         self._keep = [np.ascontiguousarray(levels, np.int8), np.ascontiguousarray(tree_ids, np.int32),
                       np.ascontiguousarray(conn.tree_to_tree, np.int32),
                       np.ascontiguousarray(conn.tree_to_face, np.int8),
                       np.ascontiguousarray(conn.face_bc, np.int8)]
         lv, tr, t2t, t2f, fbc = self._keep
+        part = None if partition is None else np.ascontiguousarray(partition, np.int64)
+        self._keep.append(part)
         self._nid = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         d = ForestDesc(len(lv), lv.ctypes.data, tr.ctypes.data, len(t2t) // 4, t2t.ctypes.data,
                        t2f.ctypes.data, fbc.ctypes.data, m, 2, meqn, maux, tree_dx0, device, rank,
-                       nranks, C.cast(self._nid, C.c_void_p) if self._nid else None, halo_p2p)
+                       nranks, C.cast(self._nid, C.c_void_p) if self._nid else None, halo_p2p,
+                       part.ctypes.data if part is not None else None)
         h = C.c_void_p()
         _check(lib().fc_forest_create(C.byref(d), C.byref(h)), "fc_forest_create")
         self.h = h
@@ -231,10 +235,11 @@ class Forest:
             _check(rc, "fc_step_subcycled")
         return rc, cfl.value
 
-    def regrid(self, refine_threshold: float, coarsen_threshold: float, min_level: int, max_level: int):
+    def regrid(self, refine_threshold: float, coarsen_threshold: float, min_level: int, max_level: int,
+               level_weights: int = 0):
         """Dynamic regrid (fc_regrid) -> a new Forest on the new mesh (problem and q carried over;
         aux must be set again for the capacity form).  This handle stays valid."""
-        rp = RegridParams(refine_threshold, coarsen_threshold, min_level, max_level)
+        rp = RegridParams(refine_threshold, coarsen_threshold, min_level, max_level, level_weights)
         h = C.c_void_p()
         _check(lib().fc_regrid(self.h, C.byref(rp), C.byref(h)), "fc_regrid")
         return self._wrap(h)
@@ -331,9 +336,9 @@ class Forest:
         return t[:self.count]
 
     def regrid_begin(self, global_tags: np.ndarray, refine_threshold: float, coarsen_threshold: float,
-                     min_level: int, max_level: int):
+                     min_level: int, max_level: int, level_weights: int = 0):
         gt = np.ascontiguousarray(global_tags, np.float64)
-        rp = RegridParams(refine_threshold, coarsen_threshold, min_level, max_level)
+        rp = RegridParams(refine_threshold, coarsen_threshold, min_level, max_level, level_weights)
         h = C.c_void_p()
         _check(lib().fc_regrid_begin(self.h, gt.ctypes.data_as(C.c_void_p), C.byref(rp), C.byref(h)),
                "fc_regrid_begin")

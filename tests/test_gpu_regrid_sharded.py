@@ -67,7 +67,7 @@ def step(hs, dt):
     return c
 
 
-def regrid(hs, prm):
+def regrid(hs, prm, weights=0):
     R = len(hs)
     halo(hs, 1)
     for f in hs:
@@ -76,7 +76,7 @@ def regrid(hs, prm):
     for f in hs:
         f.regrid_fill(2)
     tags = np.concatenate([f.regrid_tags() for f in hs])
-    gs = [f.regrid_begin(tags, *prm) for f in hs]
+    gs = [f.regrid_begin(tags, *prm, level_weights=weights) for f in hs]
     move([hs[r].regrid_buffers(gs[r]) for r in range(R)], R)
     for g in gs:
         g.regrid_finish()
@@ -140,3 +140,24 @@ def test_sharded_dynamic_amr_run_equals_one_rank(R):
     for h in hs:
         h.close()
     f.close()
+
+
+def test_sharded_regrid_level_weights():
+    """level_weights = 1: the new Morton cuts balance sum 2^(level - coarsest) (a sub-cycled step's
+    work) instead of the count; every rank's weight is within one patch of the ideal share, and the
+    state is the one-rank regrid's, bitwise."""
+    w, prm = c2(steps=1), (0.4, 0.01, 2, 5)
+    R = 3
+    one = fc.forest_for(w, 0)
+    one.set_q(np.ascontiguousarray(w.q0))
+    g1 = one.regrid(*prm)
+    lv, _ = g1.leaves()
+    hs = make_shards(w.forest.levels, w.forest.tree_ids, w.forest.conn, w, R)
+    for f in hs:
+        f.set_q(np.ascontiguousarray(w.q0[f.first:f.first + f.count]))
+    gs = regrid(hs, prm, weights=1)
+    wt = np.ldexp(1.0, lv.astype(np.int64) - int(lv.min()))
+    shares = [wt[g.first:g.first + g.count].sum() for g in gs]
+    assert abs(sum(shares) - wt.sum()) == 0 and max(shares) - min(shares) <= 2 * wt.max()
+    assert [g.first for g in gs] != [r * len(lv) // R for r in range(R)]    # not the count cut
+    np.testing.assert_array_equal(np.concatenate([g.get_q() for g in gs if g.count]), g1.get_q())

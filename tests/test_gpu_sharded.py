@@ -33,10 +33,11 @@ def d2d(dst: int, src: int, nbytes: int):
         assert _cudart.cudaMemcpy(C.c_void_p(int(dst)), C.c_void_p(int(src)), int(nbytes), 3) == 0
 
 
-def run_sharded(w, R, dts, skip, reflux=0):
+def run_sharded(w, R, dts, skip, reflux=0, partition=None):
     hs = []
     for r in range(R):
-        f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0, 0, r, R, None)
+        f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0, 0, r, R, None,
+                      partition=partition)
         f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject, skip, reflux)
         if w.aux is not None:
             f.set_aux(np.ascontiguousarray(w.aux[f.first:f.first + f.count]))
@@ -206,5 +207,17 @@ def test_sharded_reflux_equals_single_rank_bitwise(w, R):
     _, _, do = oracle.run(w)
     q1, c1_, _ = fc.run(w, dt_list=do)
     qr, cr = run_sharded(w, R, do, 1, reflux=1)
+    np.testing.assert_array_equal(qr, q1)
+    np.testing.assert_array_equal(cr, c1_)
+
+
+@pytest.mark.parametrize("w", [c2(steps=15), c5(level=2, m=16, steps=15)], ids=lambda w: w.name)
+def test_sharded_custom_partition_bitwise(w):
+    """fc_forest_desc.partition: uneven Morton cuts, one rank empty -- bitwise the one-rank run."""
+    P = w.num_patches
+    part = [0, P // 7, P // 7, P // 2 + 3, P]
+    _, _, do = oracle.run(w)
+    q1, c1_, _ = fc.run(w, dt_list=do)
+    qr, cr = run_sharded(w, 4, do, 1, partition=part)
     np.testing.assert_array_equal(qr, q1)
     np.testing.assert_array_equal(cr, c1_)

@@ -187,3 +187,20 @@ def test_reflux_plan_single_rank_and_cross_rank_requests():
         f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, 4, device=-1, rank=r, nranks=3)
         f.set_problem(w.kind, w.params[0], w.params[1], reflux=1)
         assert all(len(f.reflux_requests(s)) == 0 for s in range(3))
+
+
+def test_custom_partition_ranges_and_validation():
+    """fc_forest_desc.partition sets each rank's Morton range (empty ranks allowed); cut points
+    that decrease or do not cover 0..P are rejected with FC_EINVAL."""
+    w = c2()
+    P = w.num_patches
+    part = [0, 13, 13, 70, P]
+    for r in range(4):
+        f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, 1, device=-1, rank=r, nranks=4,
+                      partition=part)
+        assert (f.first, f.count) == (part[r], part[r + 1] - part[r])
+    for bad in ([0, 20, 10, 70, P], [0, 13, 13, 70, P - 1], [1, 13, 13, 70, P]):
+        with pytest.raises(fc.FcError) as e:
+            fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, 1, device=-1, rank=0, nranks=4,
+                      partition=bad)
+        assert e.value.code == fc.FC_EINVAL
