@@ -187,6 +187,7 @@ struct fc_forest {
   // instrumentation
   fc_stats st{};
   bool timing = false;
+  bool capturing = false;              // run_capture: the graphs skip the host read of the active count
   cudaEvent_t ev[6] = {};
   bool copy_timed = false;             // ev[4] / ev[5] bracket the quiescent copy of this step
   // fc_step's timing events are read lazily (fc_get_stats): per step it only records events, so
@@ -512,7 +513,7 @@ static int update_local(fc_forest* f, double dt) {
   f->st.kernel_launches += lr;
   f->st.step_kernel_launches += lr;
   CK(cudaGetLastError());
-  if (filtered) {   // active count for the adaptive filter (read after the step's synchronisation)
+  if (filtered && !f->capturing) {   // active count for the adaptive filter (read after the step's sync)
     CK(cudaMemcpyAsync(f->h_nact, f->d_nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, f->stream));
     f->filtered_last = true;
   }
@@ -1151,8 +1152,10 @@ static int run_capture(fc_forest* f, double dt) {
     f->qold = qo;
     f->qnew = qn;
     CK(cudaStreamBeginCapture(f->stream, cudaStreamCaptureModeRelaxed));
+    f->capturing = true;
     int rc = use_fused(f) ? FC_OK : ghost_fill_internal(f);
     if (!rc) rc = update_local(f, dt);
+    f->capturing = false;
     if (!rc) launch_cfl_hist(f->d_cfl, f->d_hist, f->d_hist_idx, f->stream);
     cudaGraph_t g = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(f->stream, &g);

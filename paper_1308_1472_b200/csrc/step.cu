@@ -1821,6 +1821,7 @@ static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   // constant-velocity advection on whole 8 x 8 / 16 x 16 patches: the register-sweep kernel
   // (FC_SCALAR_CV=0 keeps k_step_sc; reflux records need method3 = 2 here)
   static const bool cv = !(getenv("FC_SCALAR_CV") && atoi(getenv("FC_SCALAR_CV")) == 0);
+  // (the choice may not depend on the local patch count: results must not depend on the sharding)
   if constexpr (std::is_same<S, AdvConst>::value) {
     if (cv && !phased && (!a.rslot || a.method3 == 2) && a.tiles == 1 && a.limiter != 0) {
       if (a.m == 16) return launch_cv<16>(a, npatch, st);
