@@ -392,7 +392,7 @@ def main():
     flops = algorithmic_flops(args.workload)
     fp64_peak = fp64_peak_tflops(pk)
     prof = profile_summary(args.workload)
-    kernel = {"C5": "k_step<EulerRoe,16,352,2>", "C3": "k_step<SweRoe,16,352,2>"}[args.workload]
+    kernel = {"C5": "k_step<EulerRoe,16,384,2>", "C3": "k_step<SweRoe,16,384,2>"}[args.workload]
     # dominant kernel of the timed step: k_copy_classify (~70 % of the step; streams every cell's
     # q_old -> q_new, 64 algorithmic bytes per cell-update, and classifies the patches), timed with
     # CUDA events around its launches on the library's stream.  The whole update phase (copy +
