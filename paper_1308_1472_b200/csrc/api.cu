@@ -790,7 +790,7 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
     const int T = (pl.m % 16 == 0) ? 16 : ((pl.m % 8 == 0) ? 8 : ((pl.m % 4 == 0) ? 4 : 2));
     const char* env = getenv("FC_FUSED_RING");
     const bool allow = !env || atoi(env) != 0;
-    if (allow && pl.uniform_same && T == pl.m) {
+    if (allow && pl.uniform_same && pl.m % T == 0) {   // (multi-tile patches: gather_ring_tiles)
       RingSources rs;
       f->p2p = d->halo_p2p != 0 && pl.nranks > 1;
       rc = plan_ring_sources(f->pl, pl.meqn, rs, err, f->p2p);

@@ -254,6 +254,23 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
     tx = t - ty * A.tiles;
   }
   const int n = A.m + 4, n2 = n * n;
+  if (A.ring && A.tiles > 1) {   // fused ring gather, multi-tile patch: the window's part inside the
+                                 // patch interior by row copies (16-byte aligned: m, T even), the
+                                 // rest by gather_ring_tiles (constant-aux forms only)
+    const int m = A.m;
+    const int i_lo = max(1, tx * T - 1), i_hi = min(m, tx * T + T + 2);
+    const int j_lo = max(1, ty * T - 1), j_hi = min(m, ty * T + T + 2);
+    const int L = i_hi - i_lo + 1, R = j_hi - j_lo + 1;
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(MEQN * R * L) * (uint32_t)sizeof(double));
+    const double* qb = A.qold + (int64_t)patch * MEQN * n2;
+#pragma unroll 1
+    for (int r = lane; r < MEQN * R; r += nthr) {
+      const int k = r / R, j = j_lo + (r - k * R);
+      bulk_g2s(buf + k * WW + (j - ty * T + 1) * W + (i_lo - tx * T + 1), qb + (int64_t)k * n2 + (j - 1) * m + (i_lo - 1),
+               L * sizeof(double), bar);
+    }
+    return;
+  }
   if (A.ring) {              // fused ring gather: the TMA brings the m x m interior rows only
     constexpr uint32_t qbytes = (uint32_t)MEQN * T * T * sizeof(double);
     constexpr uint32_t abytes = S::CAPA ? (uint32_t)3 * WW * sizeof(double) : 0u;
@@ -325,9 +342,15 @@ __device__ __forceinline__ int ring_window_index(int r) {
   return (T + 2) * n + r;                                    // rows j = m+1, m+2
 }
 
+template <class S, int T, int NT>
+__device__ __forceinline__ void gather_ring_tiles(const StepArgs& A, int tile, double* buf);
+template <class S, int T, int NT>
+__device__ __forceinline__ void window_bc_tiles(const StepArgs& A, int tile, double* sq, int is_y);
+
 // issue the cp.async copies of the ring cells of `tile` (COPY sources) into buf; one group
 template <class S, int T, int NT>
 __device__ __forceinline__ void gather_ring(const StepArgs& A, int tile, double* buf) {
+  if (A.tiles > 1) { gather_ring_tiles<S, T, NT>(A, tile, buf); return; }
   using Sh = StepShape<S, T>;
   constexpr int MEQN = S::MEQN, WW = Sh::WW, G = WW - T * T;
   const int n2 = WW;
@@ -345,9 +368,55 @@ __device__ __forceinline__ void gather_ring(const StepArgs& A, int tile, double*
   }
 }
 
+// multi-tile patches (m = tiles x T): the window cells outside the patch interior are ring cells of
+// the patch; copy their sources (the patch's ring table), physical-boundary ones after the gather
+template <class S, int T, int NT>
+__device__ __forceinline__ void gather_ring_tiles(const StepArgs& A, int tile, double* buf) {
+  constexpr int MEQN = S::MEQN, W = T + 4, WW = W * W;
+  const int m = A.m, n = m + 4, n2 = n * n, G = n2 - m * m, tiles2 = A.tiles * A.tiles;
+  const int patch = tile / tiles2, tt = tile - patch * tiles2, ty = tt / A.tiles, tx = tt - ty * A.tiles;
+  const int32_t* rs = A.ring + (int64_t)patch * G;
+  const uint8_t* rp = A.rpeer ? A.rpeer + (int64_t)patch * G : nullptr;
+  for (int e = opaque(threadIdx.x); e < WW; e += NT) {
+    const int i = tx * T + e % W - 1, j = ty * T + e / W - 1;
+    if (i >= 1 && i <= m && j >= 1 && j <= m) continue;        // (row copies)
+    const int r = ring_index(i, j, m);
+    const int32_t v = __ldg(rs + r);
+    if (v < 0) continue;                                        // (physical boundary: window_bc_tiles)
+    const double* base = ring_base(A, rp ? __ldg(rp + r) : 0);
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) cp_async8(buf + k * WW + e, base + v + (int64_t)k * n2);
+  }
+}
+
+template <class S, int T, int NT>
+__device__ __forceinline__ void window_bc_tiles(const StepArgs& A, int tile, double* sq, int is_y) {
+  constexpr int MEQN = S::MEQN, W = T + 4, WW = W * W;
+  const int m = A.m, n = m + 4, n2 = n * n, G = n2 - m * m, tiles2 = A.tiles * A.tiles;
+  const int patch = tile / tiles2, tt = tile - patch * tiles2, ty = tt / A.tiles, tx = tt - ty * A.tiles;
+  const int32_t* rs = A.ring + (int64_t)patch * G;
+  for (int e = opaque(threadIdx.x); e < WW; e += NT) {
+    const int i = tx * T + e % W - 1, j = ty * T + e / W - 1;
+    if (i >= 1 && i <= m && j >= 1 && j <= m) continue;
+    const int32_t v = __ldg(rs + ring_index(i, j, m));
+    if (v >= 0) continue;
+    const int code = -1 - v;
+    if ((code & 1) != is_y) continue;
+    const int src = code >> 3, neg = (code >> 1) & 3;
+    const int si = src % n - 1, sj = src / n - 1;               // the patch cell it copies (natural)
+    const int ws = (sj - ty * T + 1) * W + (si - tx * T + 1);   // (within 2 cells: inside this window)
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) {
+      const double x = sq[k * WW + ws];
+      sq[k * WW + e] = (neg != 0 && k == neg) ? -x : x;
+    }
+  }
+}
+
 // physical-boundary ring cells of the staged window, x faces (is_y = 0) then y faces (is_y = 1)
 template <class S, int T, int NT>
 __device__ __forceinline__ void window_bc(const StepArgs& A, int tile, double* sq, int is_y) {
+  if (A.tiles > 1) { window_bc_tiles<S, T, NT>(A, tile, sq, is_y); return; }
   using Sh = StepShape<S, T>;
   constexpr int MEQN = S::MEQN, WW = Sh::WW, G = WW - T * T;
   const int32_t* rs = A.ring + (int64_t)tile * G;

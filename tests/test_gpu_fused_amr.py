@@ -11,7 +11,7 @@ import pytest
 
 from paper_1308_1472_b200 import fc
 from workloads import forests as F
-from workloads.configs import SWE_ROE, Workload, c2, c3_ic
+from workloads.configs import SWE_ROE, Workload, c2, c3, c3_ic
 
 from test_gpu_subcycle import amr_euler, three_levels
 
@@ -77,5 +77,18 @@ def test_fused_amr_gather_in_subcycled_steps(w, monkeypatch):
     qa, ca, _ = fc.run_subcycled(w)
     monkeypatch.setenv("FC_FUSED_RING", "0")
     qb, cb, _ = fc.run_subcycled(w)
+    np.testing.assert_array_equal(qa, qb)
+    np.testing.assert_array_equal(ca, cb)
+
+
+@pytest.mark.parametrize("w", [c3(level=2, m=32, steps=10), c3(level=1, m=20, steps=10)],
+                         ids=lambda w: w.name)
+def test_fused_gather_on_multi_tile_patches(w, monkeypatch):
+    """Uniform forests with m = tiles x T (m = 32: 2 x 2 tiles of 16; m = 20: 5 x 5 of 4), walls:
+    each tile's window takes its interior part by row copies and its ring part from the sources
+    (gather_ring_tiles, wall ghosts in shared memory) -- bitwise the ghost-kernel run."""
+    qa, ca, pa = run(w, monkeypatch, True)
+    qb, cb, pb = run(w, monkeypatch, False)
+    assert pa == 1 and pb == 0
     np.testing.assert_array_equal(qa, qb)
     np.testing.assert_array_equal(ca, cb)
