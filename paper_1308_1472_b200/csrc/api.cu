@@ -169,7 +169,7 @@ struct fc_forest {
   uint8_t* d_rpeer = nullptr;          // [Pl][G] 0 = local, k = rank k-1, 255 = computed ghost
   bool amr_fused = false;              // fused ring gather on an AMR forest (computed ghosts)
   double* d_cg = nullptr;              // computed ghosts (AVG4 / INTERP ring cells), plan_ring_amr
-  DevList cg_avg;
+  DevList cg_avg, cg_c3;
   std::vector<DevList> cg_interp;      // per level
   double* buf[2] = {nullptr, nullptr}; // this rank's two state buffers (q_old = buf[parity])
   int parity = 0;
@@ -387,7 +387,10 @@ static bool has_round2(const fc_forest* f) { return f->npack[1] || f->nunpack[1]
 // of every patch's ring in the 352-thread k_step costs more than the ghost kernels: C5 full 9.5 ->
 // 10.3 ms).  FC_FUSED_RING=0 at creation keeps the ghost kernels; the capacity form always does.
 static bool use_fused(const fc_forest* f) {
-  return f->fused && f->prob.kind != FC_ADV_EDGEVEL_CAPA && (f->prob.skip_quiescent || f->prob.kind == FC_ADV_CONST);
+  if (!f->fused) return false;
+  if (f->prob.kind == FC_ADV_EDGEVEL_CAPA)   // (aux staging of the fused multi-tile windows: not built)
+    return (f->pl.m == 16 || f->pl.m == 8) && (std::getenv("FC_FUSED_CAPA") == nullptr || std::atoi(std::getenv("FC_FUSED_CAPA")) != 0);
+  return f->prob.skip_quiescent || f->prob.kind == FC_ADV_CONST;
 }
 
 static void run_ghost(fc_forest* f, int op, const DevList& l) {
@@ -479,6 +482,7 @@ static int update_local(fc_forest* f, double dt) {
     f->st.kernel_launches += launch_cg(2, f->qold, f->d_cg, f->cg_avg.d, f->cg_avg.nrec, f->pl.meqn, n2, f->stream);
     for (auto& l : f->cg_interp)
       f->st.kernel_launches += launch_cg(3, f->qold, f->d_cg, l.d, l.nrec, f->pl.meqn, n2, f->stream);
+    f->st.kernel_launches += launch_cg(6, f->qold, f->d_cg, f->cg_c3.d, f->cg_c3.nrec, f->pl.meqn, n2, f->stream);
     CK(cudaGetLastError());
   }
   bool filtered = false;
@@ -566,6 +570,7 @@ static void destroy(fc_forest* f) {
     cudaFree(f->d_rpeer);
     cudaFree(f->d_cg);
     free_list(f->cg_avg);
+    free_list(f->cg_c3);
     for (auto& l : f->cg_interp) free_list(l);
     for (auto& g : f->run_exec) if (g) cudaGraphExecDestroy(g);
     cudaFree(f->d_hist); cudaFree(f->d_hist_idx); cudaFree(f->d_backup);
@@ -831,7 +836,10 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
         cudaMemcpy(f->d_rpeer, rs.peer.data(), rs.peer.size(), cudaMemcpyHostToDevice);
         cudaMemcpy(f->d_ring, rs.src.data(), rs.src.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
         cudaMemcpy(f->d_bcflag, rs.bcflag.data(), rs.bcflag.size(), cudaMemcpyHostToDevice);
-        if ((rc = to_dev(f, ra.avg, 5, f->cg_avg))) { destroy(f); return fail(rc, g_err); }
+        if ((rc = to_dev(f, ra.avg, 5, f->cg_avg)) || (rc = to_dev(f, ra.corner3, 3, f->cg_c3))) {
+          destroy(f);
+          return fail(rc, g_err);
+        }
         f->cg_interp.resize(ra.interp.size());
         for (size_t l = 0; l < ra.interp.size(); ++l)
           if ((rc = to_dev(f, ra.interp[l], 8, f->cg_interp[l]))) { destroy(f); return fail(rc, g_err); }
@@ -1350,6 +1358,7 @@ static int sub_advance(fc_forest* f, int l, int64_t tick, int sub) {
     f->st.kernel_launches += launch_cg(2, src, f->d_cg, f->cg_avg.d, f->cg_avg.nrec, meqn, n2, f->stream);
     for (auto& cl : f->cg_interp)
       f->st.kernel_launches += launch_cg(3, src, f->d_cg, cl.d, cl.nrec, meqn, n2, f->stream);
+    f->st.kernel_launches += launch_cg(6, src, f->d_cg, f->cg_c3.d, f->cg_c3.nrec, meqn, n2, f->stream);
     CK(cudaGetLastError());
   } else {
     f->qold = src;

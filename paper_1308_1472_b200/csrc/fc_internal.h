@@ -139,6 +139,7 @@ int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& er
 struct RingAmr {
   std::vector<int32_t> avg;                  // {dst slot offset, 4 q_old offsets}
   std::vector<std::vector<int32_t>> interp;  // per level: {dst slot offset, 5 refs, sigx, sigy}
+  std::vector<int32_t> corner3;              // {dst slot offset, 2 refs}: after every level
   int64_t ncg_patches = 0;                   // computed-ghost buffer size in n^2-cell virtual patches
 };
 int plan_ring_amr(const Plan& pl, int meqn, RingSources& rs, RingAmr& ra, std::string& err);

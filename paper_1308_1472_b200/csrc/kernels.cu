@@ -190,11 +190,24 @@ int launch_ghost(int op, double* q, const int32_t* list, int64_t nrec, int meqn,
   return 1;
 }
 
+__global__ void k_cg_corner3(const double* __restrict__ q, double* __restrict__ cg, const int32_t* __restrict__ L,
+                             int64_t nrec, int meqn, int n2) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrec) return;
+  const int32_t* o = L + 3 * r;
+  for (int k = 0; k < meqn; ++k) {
+    const int64_t c = (int64_t)k * n2;
+    auto rd = [&](int32_t v) { return v >= 0 ? q[v + c] : cg[(-1 - (int64_t)v) + c]; };
+    cg[o[0] + c] = __dmul_rn(0.5, __dadd_rn(rd(o[1]), rd(o[2])));   // (k_ghost_corner3's order)
+  }
+}
+
 int launch_cg(int op, const double* q, double* cg, const int32_t* list, int64_t nrec, int meqn, int n2,
               cudaStream_t st) {
   if (nrec <= 0) return 0;
   const int B = 256;
   if (op == 2) k_cg_avg<<<nblk(nrec, B), B, 0, st>>>(q, cg, list, nrec, meqn, n2);
+  else if (op == 6) k_cg_corner3<<<nblk(nrec, B), B, 0, st>>>(q, cg, list, nrec, meqn, n2);
   else k_cg_interp<<<nblk(nrec, B), B, 0, st>>>(q, cg, list, nrec, meqn, n2);
   return 1;
 }

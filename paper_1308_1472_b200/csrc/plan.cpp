@@ -566,8 +566,8 @@ int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& er
 // stencil reads the coarse patch's interior or, one hop further, the source of the coarse patch's
 // ring cell (a COPY source cell, or another computed slot).  Every value is the one the ghost
 // kernels would have written into the ring, with the same arithmetic.  Slope stencils that reach a
-// physical-boundary ring cell, and CORNER3 records, are not supported (FC_EUNSUP: the caller
-// keeps the ghost kernels).  Source references in the lists: >= 0 an offset in q_old, < 0 the
+// physical-boundary ring cell are not supported (FC_EUNSUP: the caller keeps the ghost kernels);
+// CORNER3 cells (cube corners) are computed last from the refs of their two face ghosts.  Source references in the lists: >= 0 an offset in q_old, < 0 the
 // computed slot offset -1 - v.  In rs.src the computed cells have peer code 255.
 int plan_ring_amr(const Plan& pl, int meqn, RingSources& rs, RingAmr& ra, std::string& err) {
   const int m = pl.m, n = pl.n;
@@ -585,8 +585,7 @@ int plan_ring_amr(const Plan& pl, int meqn, RingSources& rs, RingAmr& ra, std::s
   int64_t ncg = 0;
   for (int64_t i = 0; i < Pl * G; ++i) {
     const int op = pl.table[i * REC];
-    if (op == OP_AVG4 || op == OP_INTERP) slot[i] = ncg++;
-    if (op == OP_CORNER3) { err = "AMR ring gather: CORNER3 ghosts"; return FC_EUNSUP; }
+    if (op == OP_AVG4 || op == OP_INTERP || op == OP_CORNER3) slot[i] = ncg++;
   }
   ra.ncg_patches = (ncg + n2 - 1) / n2;
   if ((Pl + ra.ncg_patches) * S >= (1ll << 31)) { err = "AMR ring gather: state too large"; return FC_EUNSUP; }
@@ -647,6 +646,17 @@ int plan_ring_amr(const Plan& pl, int meqn, RingSources& rs, RingAmr& ra, std::s
           v = cgoff(slot[i]);
           rs.peer[i] = 255;
           ra.interp[lvl].insert(ra.interp[lvl].end(), {v, c[0], c[1], c[2], c[3], c[4], o[4], o[5]});
+          break;
+        }
+        case OP_CORNER3: {   // (3-tree cube corners) the mean of two of the patch's own face ghosts
+          int32_t a, b;
+          if (!ref(pl.p0 + lp, o[2], o[3], a) || !ref(pl.p0 + lp, o[6], o[7], b)) {
+            err = "AMR ring gather: corner ghost reads a boundary ghost";
+            return FC_EUNSUP;
+          }
+          v = cgoff(slot[i]);
+          rs.peer[i] = 255;
+          ra.corner3.insert(ra.corner3.end(), {v, a, b});
           break;
         }
         default:

@@ -1095,6 +1095,93 @@ struct CvShape {
   static constexpr int W = T + 4, WW = W * W, LP = T / 2 + 1, PW = 32 / LP;
 };
 
+// staging of one group of PW patches into natural (T+4)^2 windows for the register sweeps: the
+// padded patch (dense interior + ring) by row bulk copies and 16-byte side pairs, or, on the fused
+// ring path, the interior rows by bulk copy and the ring cells by cp.async from their sources (all
+// of the group's source offsets loaded first: one latency, not one per patch)
+#ifndef CV_STAGE_INLINE
+#define CV_STAGE_INLINE __forceinline__
+#endif
+template <int T>
+__device__ CV_STAGE_INLINE void cv_stage(const StepArgs& A, double* buf, uint64_t* bar, int lane, int i0, int cnt) {
+  using C = CvShape<T>;
+  constexpr int W = C::W, WW = C::WW, PW = C::PW, G = WW - T * T;
+  const bool ring = A.ring != nullptr;
+  auto patch_of = [&](int idx) { return A.active ? A.active[idx] : idx; };
+  if (lane == 0) mbar_expect_tx(bar, (uint32_t)cnt * (ring ? T * T : T * T + 4 * W) * (uint32_t)sizeof(double));
+  __syncwarp();
+  if (!ring) {
+    const int mp = lane < cnt ? patch_of(i0 + lane) : 0;
+#pragma unroll
+    for (int q = 0; q < PW; ++q) {
+      const int patch = __shfl_sync(0xffffffffu, mp, q);
+      if (q >= cnt) break;
+      const double* qb = A.qold + (int64_t)patch * WW;
+      double* b = buf + q * WW;
+      if (lane < T) bulk_g2s(b + (lane + 2) * W + 2, qb + lane * T, T * sizeof(double), bar);
+      else if (lane == T) bulk_g2s(b, qb + T * T, 2 * W * sizeof(double), bar);
+      else if (lane == T + 1) bulk_g2s(b + (T + 2) * W, qb + T * T + 2 * W + 4 * T, 2 * W * sizeof(double), bar);
+      if (lane < 2 * T) {
+        const int j = 1 + (lane >> 1), side = lane & 1;
+        cp_async16(b + (j + 1) * W + (side ? T + 2 : 0), qb + T * T + 2 * W + 4 * (j - 1) + 2 * side);
+      }
+    }
+    cp_async_commit();
+    return;
+  }
+  constexpr int NR = (G + 31) / 32;
+  int pt[PW];
+  int32_t src[PW][NR];
+  uint8_t own[PW][NR];
+#pragma unroll
+  for (int q = 0; q < PW; ++q) pt[q] = q < cnt ? patch_of(i0 + q) : -1;
+#pragma unroll
+  for (int q = 0; q < PW; ++q)
+#pragma unroll
+    for (int t = 0; t < NR; ++t) {
+      const int r = lane + 32 * t;
+      const bool ok = pt[q] >= 0 && r < G;
+      src[q][t] = ok ? __ldg(A.ring + (int64_t)pt[q] * G + r) : -1;
+      own[q][t] = (ok && A.rpeer) ? __ldg(A.rpeer + (int64_t)pt[q] * G + r) : 0;
+    }
+#pragma unroll
+  for (int q = 0; q < PW; ++q) {
+    if (pt[q] < 0) continue;
+    double* b = buf + q * WW;
+    if (lane < T) bulk_g2s(b + (lane + 2) * W + 2, A.qold + (int64_t)pt[q] * WW + lane * T, T * sizeof(double), bar);
+#pragma unroll
+    for (int t = 0; t < NR; ++t) {
+      const int r = lane + 32 * t;
+      if (src[q][t] >= 0) cp_async8(b + ring_window_index<T>(r), ring_base(A, own[q][t]) + src[q][t]);
+    }
+  }
+  cp_async_commit();
+}
+
+// fused ring path: the physical-boundary ring cells of the group's windows (x faces, then y faces)
+template <int T>
+__device__ __forceinline__ void cv_bcs(const StepArgs& A, double* gbuf, int mypatch, int mybc, int lane) {
+  constexpr int WW = CvShape<T>::WW, G = WW - T * T;
+  for (unsigned todo = __ballot_sync(0xffffffffu, mybc != 0); todo; todo &= todo - 1) {
+    const int q = __ffs(todo) - 1;
+    const int patch = __shfl_sync(0xffffffffu, mypatch, q);
+    const int bc = __shfl_sync(0xffffffffu, mybc, q);
+    const int32_t* rs = A.ring + (int64_t)patch * G;
+    double* sq = gbuf + q * WW;
+    for (int is_y = 0; is_y < 2; ++is_y) {
+      if (!(bc & (1 << is_y))) continue;
+      for (int r = lane; r < G; r += 32) {
+        const int32_t v = __ldg(rs + r);
+        if (v >= 0) continue;
+        const int code = -1 - v;
+        if ((code & 1) != is_y) continue;
+        sq[ring_window_index<T>(r)] = sq[code >> 3];   // (one component: no momentum to negate)
+      }
+      __syncwarp();
+    }
+  }
+}
+
 template <int T, int SX, int SY, bool MT2, int NB, bool RF>
 __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
   using C = CvShape<T>;
@@ -1106,62 +1193,7 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
   const int ngroups = (npatch + PW - 1) / PW;
   const bool ring = A.ring != nullptr;
   auto patch_of = [&](int idx) { return A.active ? A.active[idx] : idx; };
-  auto stage = [&](int g, int s) {
-    double* buf = sm + (size_t)s * PW * WW;
-    const int i0 = g * PW, cnt = min(PW, npatch - i0);
-    if (lane == 0)
-      mbar_expect_tx(&bars[s], (uint32_t)cnt * (ring ? T * T : T * T + 4 * W) * (uint32_t)sizeof(double));
-    __syncwarp();
-    if (!ring) {   // padded patch (dense interior, then the ring) -> natural window: interior rows and
-                   // the two ghost-row pairs by bulk copy, the side pairs of rows 1..T by 16-byte cp.async
-      const int mp = lane < cnt ? patch_of(i0 + lane) : 0;
-#pragma unroll
-      for (int q = 0; q < PW; ++q) {
-        const int patch = __shfl_sync(0xffffffffu, mp, q);
-        if (q >= cnt) break;
-        const double* qb = A.qold + (int64_t)patch * WW;
-        double* b = buf + q * WW;
-        if (lane < T) bulk_g2s(b + (lane + 2) * W + 2, qb + lane * T, T * sizeof(double), &bars[s]);
-        else if (lane == T) bulk_g2s(b, qb + T * T, 2 * W * sizeof(double), &bars[s]);
-        else if (lane == T + 1) bulk_g2s(b + (T + 2) * W, qb + T * T + 2 * W + 4 * T, 2 * W * sizeof(double), &bars[s]);
-        if (lane < 2 * T) {
-          const int j = 1 + (lane >> 1), side = lane & 1;
-          cp_async16(b + (j + 1) * W + (side ? T + 2 : 0), qb + T * T + 2 * W + 4 * (j - 1) + 2 * side);
-        }
-      }
-      cp_async_commit();
-      return;
-    }
-    // fused ring gather: all the group's source offsets are loaded first (one latency, not one per
-    // patch), then the interior rows go by bulk copy and the ring cells by cp.async
-    constexpr int NR = (G + 31) / 32;
-    int pt[PW];
-    int32_t src[PW][NR];
-    uint8_t own[PW][NR];
-#pragma unroll
-    for (int q = 0; q < PW; ++q) pt[q] = q < cnt ? patch_of(i0 + q) : -1;
-#pragma unroll
-    for (int q = 0; q < PW; ++q)
-#pragma unroll
-      for (int t = 0; t < NR; ++t) {
-        const int r = lane + 32 * t;
-        const bool ok = pt[q] >= 0 && r < G;
-        src[q][t] = ok ? __ldg(A.ring + (int64_t)pt[q] * G + r) : -1;
-        own[q][t] = (ok && A.rpeer) ? __ldg(A.rpeer + (int64_t)pt[q] * G + r) : 0;
-      }
-#pragma unroll
-    for (int q = 0; q < PW; ++q) {
-      if (pt[q] < 0) continue;
-      double* b = buf + q * WW;
-      if (lane < T) bulk_g2s(b + (lane + 2) * W + 2, A.qold + (int64_t)pt[q] * WW + lane * T, T * sizeof(double), &bars[s]);
-#pragma unroll
-      for (int t = 0; t < NR; ++t) {
-        const int r = lane + 32 * t;
-        if (src[q][t] >= 0) cp_async8(b + ring_window_index<T>(r), ring_base(A, own[q][t]) + src[q][t]);
-      }
-    }
-    cp_async_commit();
-  };
+  auto stage = [&](int g, int s) { cv_stage<T>(A, sm + (size_t)s * PW * WW, &bars[s], lane, g * PW, min(PW, npatch - g * PW)); };
   if (lane == 0) {
     for (int q = 0; q < NB; ++q) mbar_init(&bars[q], 1);
     fence_proxy_async();
@@ -1231,26 +1263,7 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
     };
     if (NB > 1) issue_next();
     double* gbuf = sm + (size_t)b * PW * WW;
-    if (ring) {   // physical-boundary ring cells: x faces, then y faces
-      for (unsigned todo = __ballot_sync(0xffffffffu, mybc != 0); todo; todo &= todo - 1) {
-        const int q = __ffs(todo) - 1;
-        const int patch = __shfl_sync(0xffffffffu, mypatch, q);
-        const int bc = __shfl_sync(0xffffffffu, mybc, q);
-        const int32_t* rs = A.ring + (int64_t)patch * G;
-        double* sq = gbuf + q * WW;
-        for (int is_y = 0; is_y < 2; ++is_y) {
-          if (!(bc & (1 << is_y))) continue;
-          for (int r = lane; r < G; r += 32) {
-            const int32_t v = __ldg(rs + r);
-            if (v >= 0) continue;
-            const int code = -1 - v;
-            if ((code & 1) != is_y) continue;
-            sq[ring_window_index<T>(r)] = sq[code >> 3];   // (one component: no momentum to negate)
-          }
-          __syncwarp();
-        }
-      }
-    }
+    if (ring) cv_bcs<T>(A, gbuf, mypatch, mybc, lane);
     const bool live = p < cnt;
     const int patch = __shfl_sync(0xffffffffu, mypatch, live ? p : 0);
     const int level = __shfl_sync(0xffffffffu, mylevel, live ? p : 0);
@@ -1398,7 +1411,7 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
 // one row ahead (read-only path), kappa's reciprocal is formed once per cell.  CFL: every x-edge
 // i - 1/2, i = 1..T+1, of rows 0..T+1 and every y-edge of columns 0..T+1 (k_step_sc's set).
 #ifndef CVC_MINB
-#define CVC_MINB 16
+#define CVC_MINB 12
 #endif
 #ifndef CVC_UNROLL
 #define CVC_UNROLL 1
@@ -1413,28 +1426,7 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
   if (A.active) npatch = *A.nactive;
   const int ngroups = (npatch + PW - 1) / PW;
   auto patch_of = [&](int idx) { return A.active ? A.active[idx] : idx; };
-  auto stage = [&](int g, int s) {   // padded patches -> natural windows (as k_step_cv, dense path)
-    double* buf = sm + (size_t)s * PW * WW;
-    const int i0 = g * PW, cnt = min(PW, npatch - i0);
-    if (lane == 0) mbar_expect_tx(&bars[s], (uint32_t)cnt * (T * T + 4 * W) * (uint32_t)sizeof(double));
-    __syncwarp();
-    const int mp = lane < cnt ? patch_of(i0 + lane) : 0;
-#pragma unroll
-    for (int q = 0; q < PW; ++q) {
-      const int patch = __shfl_sync(0xffffffffu, mp, q);
-      if (q >= cnt) break;
-      const double* qb = A.qold + (int64_t)patch * WW;
-      double* b = buf + q * WW;
-      if (lane < T) bulk_g2s(b + (lane + 2) * W + 2, qb + lane * T, T * sizeof(double), &bars[s]);
-      else if (lane == T) bulk_g2s(b, qb + T * T, 2 * W * sizeof(double), &bars[s]);
-      else if (lane == T + 1) bulk_g2s(b + (T + 2) * W, qb + T * T + 2 * W + 4 * T, 2 * W * sizeof(double), &bars[s]);
-      if (lane < 2 * T) {
-        const int j = 1 + (lane >> 1), side = lane & 1;
-        cp_async16(b + (j + 1) * W + (side ? T + 2 : 0), qb + T * T + 2 * W + 4 * (j - 1) + 2 * side);
-      }
-    }
-    cp_async_commit();
-  };
+  auto stage = [&](int g, int s) { cv_stage<T>(A, sm + (size_t)s * PW * WW, &bars[s], lane, g * PW, min(PW, npatch - g * PW)); };
   if (lane == 0) {
     for (int q = 0; q < NB; ++q) mbar_init(&bars[q], 1);
     fence_proxy_async();
@@ -1466,6 +1458,7 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
     const int cnt = min(PW, npatch - g * PW);
     const int mypatch = lane < cnt ? patch_of(g * PW + lane) : 0;
     const int mylevel = A.level[mypatch];
+    const int mybc = (A.ring && lane < cnt) ? A.bcflag[mypatch] : 0;
     mbar_wait(&bars[b], (uint32_t)((it / NB) & 1));
     cp_async_wait<(NB > 1 ? NB - 2 : 0)>();
     __syncwarp();
@@ -1479,6 +1472,7 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
       }
     };
     if (NB > 1) issue_next();
+    if (A.ring) cv_bcs<T>(A, sm + (size_t)b * PW * WW, mypatch, mybc, lane);
     const bool live = p < cnt;
     const int patch = __shfl_sync(0xffffffffu, mypatch, live ? p : 0);
     const int level = __shfl_sync(0xffffffffu, mylevel, live ? p : 0);
@@ -1898,7 +1892,7 @@ static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
     }
   }
   if constexpr (std::is_same<S, AdvEdgeCapa>::value) {   // capacity form: the same sweep, aux from global
-    if (cv && !phased && !a.rslot && !a.ring && a.tiles == 1 && a.limiter != 0) {
+    if (cv && !phased && !a.rslot && a.tiles == 1 && a.limiter != 0) {
       const bool mt2 = a.method3 == 2;
       if (a.m == 16) return mt2 ? launch_cvc_t<16, true>(a, npatch, st) : launch_cvc_t<16, false>(a, npatch, st);
       if (a.m == 8) return mt2 ? launch_cvc_t<8, true>(a, npatch, st) : launch_cvc_t<8, false>(a, npatch, st);
