@@ -92,3 +92,17 @@ def test_fused_gather_on_multi_tile_patches(w, monkeypatch):
     assert pa == 1 and pb == 0
     np.testing.assert_array_equal(qa, qb)
     np.testing.assert_array_equal(ca, cb)
+
+
+@pytest.mark.parametrize("uniform", [False, True], ids=["band", "uniform"])
+def test_fused_gather_capacity_form_on_the_cubed_sphere(uniform, monkeypatch):
+    """The capacity form (C4 physics) on the cubed sphere takes the fused path: its CORNER3 ghosts
+    at the 8 cube vertices are computed ghosts (the mean of two face ghosts' sources) -- bitwise the
+    ghost-kernel run, AMR band and uniform sphere."""
+    from workloads.cubed_sphere import c4_workload
+    w = c4_workload(base_level=2, m=16, steps=12, uniform=uniform) if uniform else c4_workload(base_level=2, m=16, steps=12)
+    qa, ca, pa = run(w, monkeypatch, True)
+    qb, cb, pb = run(w, monkeypatch, False)
+    assert pa == 2 and pb == 0
+    np.testing.assert_array_equal(qa, qb)
+    np.testing.assert_array_equal(ca, cb)
