@@ -1604,6 +1604,9 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
 //                    staged window is uniform, every wave of its update is exactly 0 and q_new = q
 //                    (already copied); its CFL comes from the state.  Others go to the active list;
 //   k_step           over the active list only.
+#ifndef COPY_V256
+#define COPY_V256 1
+#endif
 template <int MEQN, int T>
 __global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict__ qold, double* __restrict__ qnew,
                                                        int npatch, uint8_t* __restrict__ uflag,
@@ -1622,6 +1625,35 @@ __global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict_
 #pragma unroll
     for (int k = 0; k < MEQN; ++k) v0[k] = __ldg(src + k * n2);
     bool diff = false;
+#if COPY_V256
+    // 32-byte accesses (LDG/STG.E.ENL2.256 on sm_100a): 4 doubles per lane and access
+    constexpr int Q4 = T * T / 4, E4 = MEQN * Q4, NE4 = (E4 + 31) / 32, NC4 = NE4 < 8 ? NE4 : 8;
+#pragma unroll 1
+    for (int base = 0; base < E4; base += 32 * NC4) {
+      double x[NC4][4];
+#pragma unroll
+      for (int u = 0; u < NC4; ++u) {
+        const int e = base + lane + 32 * u;
+        const int k = e / Q4, c4 = e - k * Q4;
+        if (e < E4)
+          asm volatile("ld.global.cs.v4.f64 {%0, %1, %2, %3}, [%4];"
+                       : "=d"(x[u][0]), "=d"(x[u][1]), "=d"(x[u][2]), "=d"(x[u][3])
+                       : "l"(src + k * n2 + 4 * c4));
+      }
+#pragma unroll
+      for (int u = 0; u < NC4; ++u) {
+        const int e = base + lane + 32 * u;
+        if (e < E4) {
+          const int k = e / Q4, c4 = e - k * Q4;
+          asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst + k * n2 + 4 * c4), "d"(x[u][0]),
+                       "d"(x[u][1]), "d"(x[u][2]), "d"(x[u][3])
+                       : "memory");
+          diff |= (x[u][0] != v0[k]) | (x[u][1] != v0[k]) | (x[u][2] != v0[k]) | (x[u][3] != v0[k]);
+        }
+      }
+    }
+    (void)NC;
+#else
 #pragma unroll 1
     for (int base = 0; base < E; base += 32 * NC) {
       double2 x[NC];
@@ -1641,6 +1673,7 @@ __global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict_
         }
       }
     }
+#endif
     const bool uni = !__any_sync(0xffffffffu, diff);
     if (lane == 0) uflag[p] = uni ? 1 : 0;
     if (lane < MEQN) uval[(int64_t)p * MEQN + lane] = v0[lane < MEQN ? lane : 0];
