@@ -1944,7 +1944,7 @@ static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   const int mb = env_mb ? env_mb : dmb;
   if (a.m % 16 == 0) {
     // 384 threads (12 warps; 2 CTAs keep the 80-register budget): measured on C5 full update
-    // 8.58 -> 8.12 ms vs 352 (`tools/nt_variants.sh`; 400 does not launch)
+    // 8.58 -> 8.12 ms vs 352; 416 / 448 (72 registers, spills): 8.78 ms (`tools/nt_variants.sh`)
 #ifndef STEP_NT16
 #define STEP_NT16 384
 #endif
