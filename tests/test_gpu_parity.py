@@ -262,3 +262,23 @@ def test_systems_ragged_tilings_against_oracle(w):
     for skip in (1, 0):
         qg, cg, _ = fc.run(w, dt_list=do, skip_quiescent=skip)
         assert_parity(w, qg, qo, cg, co)
+
+
+@pytest.mark.parametrize("bc", ["outflow", "wall"])
+@pytest.mark.parametrize("m", [8, 16])
+def test_constant_velocity_physical_boundaries_against_oracle(bc, m):
+    """The register-sweep kernel's physical-boundary ghosts on the fused path (ring BC codes applied
+    in shared memory, uniform forests) and on the AMR fused path: outflow and (scalar) wall
+    boundaries, a uniform and a refined forest, both modes, against the oracle."""
+    conn = F.brick(2, 1, bc=F.OUTFLOW) if bc == "outflow" else F.walled_unit_square(F.WALL)
+    for fr in (F.forest_uniform(conn, 2),
+               F.forest_refined(conn, 2, lambda t, x, y, h: (x + t - 0.6) ** 2 + (y - 0.5) ** 2 < 0.1)):
+        X, Y = F.cell_centres(fr, m)
+        X = X + fr.tree_ids[:, None, None]
+        q0 = np.exp(-20.0 * ((X - 0.45) ** 2 + (Y - 0.4) ** 2))[:, None]
+        dt = 0.8 * (0.5 ** int(fr.levels.max()) / m) / 1.0
+        w = Workload(f"bc_{bc}_m{m}", fr, m, 1, 0, ADV_CONST, (0.9, -0.6), q0, None, 12, dt, "fixed")
+        qo, co, do = oracle.run(w)
+        for skip in (1, 0):
+            qg, cg, _ = fc.run(w, dt_list=do, skip_quiescent=skip)
+            assert_parity(w, qg, qo, cg, co, mass_rtol=1.0)   # (outflow: mass leaves the domain)
