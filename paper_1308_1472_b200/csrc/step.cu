@@ -1607,8 +1607,16 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
 #ifndef COPY_V256
 #define COPY_V256 1
 #endif
+// (tuning knobs; measured on C5: 8 x 32-byte loads in flight per lane at 2 CTAs/SM is best --
+// 3 CTAs/SM 0.747 ms, 4 loads per lane 0.755 ms, vs 0.714 ms; tools/copy_variants.sh)
+#ifndef COPY_MINB
+#define COPY_MINB 1
+#endif
+#ifndef COPY_NC4
+#define COPY_NC4 8
+#endif
 template <int MEQN, int T>
-__global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict__ qold, double* __restrict__ qnew,
+__global__ void __launch_bounds__(256, COPY_MINB) k_copy_classify(const double* __restrict__ qold, double* __restrict__ qnew,
                                                        int npatch, uint8_t* __restrict__ uflag,
                                                        double* __restrict__ uval) {
   // One warp per patch (T = m here).  The storage keeps each (patch, component) interior as one
@@ -1627,7 +1635,7 @@ __global__ void __launch_bounds__(256) k_copy_classify(const double* __restrict_
     bool diff = false;
 #if COPY_V256
     // 32-byte accesses (LDG/STG.E.ENL2.256 on sm_100a): 4 doubles per lane and access
-    constexpr int Q4 = T * T / 4, E4 = MEQN * Q4, NE4 = (E4 + 31) / 32, NC4 = NE4 < 8 ? NE4 : 8;
+    constexpr int Q4 = T * T / 4, E4 = MEQN * Q4, NE4 = (E4 + 31) / 32, NC4 = NE4 < COPY_NC4 ? NE4 : COPY_NC4;
 #pragma unroll 1
     for (int base = 0; base < E4; base += 32 * NC4) {
       double x[NC4][4];
