@@ -7,6 +7,7 @@ shares no code with it.  Every function cites the passage it follows in the C so
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 import os
 import subprocess
 
@@ -27,15 +28,21 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc -O2 -ffp-contract=off (plain C, optional OpenMP)."""
     srcs = [os.path.join(HERE, s) for s in SOURCES]
     hdrs = [os.path.join(HERE, h) for h in ("oracle.h", "oracle_internal.h")]
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
-        if all(os.path.getmtime(s) <= t for s in srcs + hdrs):
-            return LIB
+    flags = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-fopenmp", "-Wall"]
+    h = hashlib.sha256("\0".join(flags).encode())
+    for s in srcs + hdrs:   # content-hash stamp (not mtimes): a shipped .so is rebuilt if stale
+        with open(s, "rb") as f:
+            h.update(f.read())
+    stamp, stamp_file = h.hexdigest(), LIB + ".stamp"
+    if not force and os.path.exists(LIB) and os.path.exists(stamp_file):
+        with open(stamp_file) as f:
+            if f.read().strip() == stamp:
+                return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-fopenmp",
-           "-Wall", "-o", tmp] + srcs + ["-lm"]
-    subprocess.run(cmd, check=True)
+    subprocess.run(flags + ["-o", tmp] + srcs + ["-lm"], check=True)
     os.replace(tmp, LIB)
+    with open(stamp_file, "w") as f:
+        f.write(stamp + "\n")
     return LIB
 
 

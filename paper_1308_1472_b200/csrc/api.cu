@@ -948,6 +948,10 @@ int fc_set_problem(fc_forest* f, const fc_problem* pr) {
   }
   f->prob = *pr;
   f->has_problem = true;
+  // fc_run's captured graphs bake the problem's kernel arguments (kind, limiter, methods, p0/p1,
+  // skip_quiescent, reflux): a new problem invalidates them
+  for (auto& g : f->run_exec)
+    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
   return FC_OK;
 }
 

@@ -41,3 +41,22 @@ def test_run_rejected_is_undone():
     rc, c = f.run(w.dt0, 10)
     qa, ca, _ = fc.run(w)
     np.testing.assert_array_equal(f.get_q(), qa)
+
+
+def test_run_after_set_problem_uses_the_new_problem():
+    """fc_set_problem between two fc_run calls with the same dt: the second run must replay the
+    new problem's kernels (limiter, transverse variant, skip mode), not the first run's graphs."""
+    w = c2(steps=10)
+    f = fc.forest_for(w, 0)
+    f.set_q(np.ascontiguousarray(w.q0))
+    f.run(w.dt0, 5)                                    # graphs captured for MC, method3 = 2
+    q_mid = f.get_q()
+    f.set_problem(w.kind, *w.params, limiter=fc.FC_LIM_MINMOD, method3=1, skip_quiescent=0)
+    f.run(w.dt0, 5)
+    q_run = f.get_q()
+    g = fc.forest_for(w, 0)                            # reference: fc_step loop from the same state
+    g.set_problem(w.kind, *w.params, limiter=fc.FC_LIM_MINMOD, method3=1, skip_quiescent=0)
+    g.set_q(q_mid)
+    for _ in range(5):
+        g.step(w.dt0)
+    np.testing.assert_array_equal(q_run, g.get_q())
