@@ -8,12 +8,17 @@ update + CFL reduction) on 1..8 B200s, plus roofline, end-to-end and oracle base
 
 One "step" = one fc_step: ghost fill (for N > 1 the remote ring cells are read inside the update
 kernel from the owner GPU's memory over NVLink -- the peer-memory halo, `--halo nccl` for the NCCL
-send/recv exchange instead), the update of every
-local patch, the global CFL max-allreduce and the CFL read-back that drives the next dt (the
-Clawpack variable-dt rule of the workload).  The workload is BASELINE.json configs[4] (C5: Euler
-shock-bubble on a 4-tree brick, level 8, m = 16, 262,144 patches, 67.1M cells) -- the config
-BASELINE's metric is quoted on at 1/2/4/8 GPUs -- Morton-sharded across ranks (strong scaling).
-Its state (2 x 3.36 GB) is far larger than L2, so no flush is needed between steps.
+send/recv exchange instead), the full wave-propagation update of every local patch (skip_quiescent
+= 0: every tile's Riemann solves, limiters and corrections), the global CFL max-allreduce and the
+CFL read-back that drives the next dt (the Clawpack variable-dt rule of the workload).  The
+workload is BASELINE.json configs[4] (C5: Euler shock-bubble on a 4-tree brick, level 8, m = 16,
+262,144 patches, 67.1M cells) -- the config BASELINE's metric is quoted on at 1/2/4/8 GPUs --
+Morton-sharded across ranks (strong scaling).  Its state (2 x 3.36 GB) is far larger than L2, so no
+flush is needed between steps.
+
+Extra keys: `value_quiescent_skip` (the library's exact, data-dependent shortcut for patches whose
+window is one state), `variants_full_update` (SURVEY §8(d)'s T1-T4 on this GPU with their HBM
+roofline fractions), `roofline_hbm` (the headline step against HBM).
 """
 from __future__ import annotations
 
@@ -239,6 +244,64 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------------------------
+def run_variants(args, fc, hbm_peak):
+    """SURVEY §8(d)'s throughput variants on this GPU, full update (skip_quiescent = 0): T1 (C1
+    physics, uniform L10, m = 8), T2 (C2 physics, L8/L9, m = 16), T3 (C3 physics, L8, m = 32),
+    T4 (C4 physics, L7/L8 band, m = 16).  W warm-ups then K steps of each config's dt policy from
+    its IC, CUDA events around the step loop (each step includes its CFL read-back); states >> L2.
+    HBM fraction = compulsory bytes (16 meqn + 8 maux per cell-update) / measured copy peak."""
+    import numpy as np
+    import torch
+    from workloads.configs import c1, c2, c3
+    from workloads.cubed_sphere import c4_workload
+    makers = {"T1": lambda: c1(level=10, m=8), "T2": lambda: c2(base_level=8, m=16),
+              "T3": lambda: c3(level=8, m=32), "T4": lambda: c4_workload(base_level=7, m=16, steps=20)}
+    stream = torch.cuda.current_stream()
+    out = {}
+    for name, mk in makers.items():
+        t0 = time.perf_counter()
+        w = mk()
+        gen_s = time.perf_counter() - t0
+        qd = torch.from_numpy(np.ascontiguousarray(w.q0)).cuda()
+        f = fc.forest_for(w, torch.cuda.current_device(), skip_quiescent=0)
+        f.set_stream(stream.cuda_stream)
+
+        def run(n, dt):
+            for _ in range(n):
+                rc, cfl = f.step(dt, raise_on_reject=False)
+                if rc == fc.FC_ECFL:
+                    dt = dt * w.cfl_target / cfl
+                    rc, cfl = f.step(dt)
+                dt = w.next_dt(dt, cfl)
+            return dt
+        f.set_q(qd)
+        dt = run(max(3, args.warmup), w.dt0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run(args.variant_steps, dt)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.variant_steps
+        f.reset_stats()
+        f.set_timing(True)
+        run(3, dt)
+        st = f.stats()
+        f.set_timing(False)
+        f.close()
+        del qd
+        rate = w.cells / (ms / 1e3)
+        bpc = 16 * w.meqn + 8 * w.maux
+        out[name] = {"workload": w.name, "patches": w.num_patches, "cells": w.cells,
+                     "ms_per_step": ms, "value": rate, "unit": UNIT,
+                     "bytes_per_cell_update": bpc, "hbm_roofline_frac": rate * bpc / (hbm_peak * 1e9),
+                     "update_kernel_ms": st["ms_step"] / max(1, st["step_kernel_launches"]),
+                     "ghost_ms": st["ms_ghost"] / max(1, st["steps"]),
+                     "fused_path": st.get("uniform_fast_path"), "generate_s": gen_s,
+                     "steps": args.variant_steps, "mode": "full update (skip_quiescent = 0)"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -249,6 +312,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-patches", type=int, default=256)
+    ap.add_argument("--no-variants", dest="variants", action="store_false",
+                    help="skip the T1-T4 throughput variants (extra keys)")
+    ap.add_argument("--variant-steps", type=int, default=20)
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: peer-memory halo in the fused gather (default) or NCCL send/recv")
     args = ap.parse_args()
@@ -377,61 +443,65 @@ def main():
         f.set_timing(False)
         return ms, st, clk, cfls
 
-    # ---- device-resident timed runs: default (exact quiescent-tile shortcut on), full update ----
-    ms, _, clk, cfls = timed(1, True, False)
+    # ---- device-resident timed runs.  Headline: the method's full update (every tile's Riemann
+    # solves, limiters and corrections; skip_quiescent = 0).  Beside it, the exact quiescent
+    # shortcut (data-dependent: it skips the arithmetic of patches whose window is one state).
+    ms, _, clk, cfls = timed(0, True, False)
     value = cells_total * args.steps / (ms / 1000.0)
-    ms_i, st, _, _ = timed(1, False, True)          # instrumented twin: kernel / phase durations
-    ms_full, _, _, _ = timed(0, False, False)
-    value_full = cells_total * args.steps / (ms_full / 1000.0)
-    _, st_full, _, _ = timed(0, False, True)
-    set_mode(1)
+    ms_i, st, _, _ = timed(0, False, True)          # instrumented twin: kernel / phase durations
+    ms_q, _, _, _ = timed(1, False, False)
+    value_q = cells_total * args.steps / (ms_q / 1000.0)
+    _, st_q, _, _ = timed(1, False, True)
+    set_mode(0)
 
     pk, pk_src = peaks()
     bpc = bytes_per_cell_update(w)
     hbm_peak = float(pk["hbm_gbs"])
     flops = algorithmic_flops(args.workload)
     fp64_peak = fp64_peak_tflops(pk)
-    prof = profile_summary(args.workload)
-    kernel = {"C5": "k_step<EulerRoe,16,384,2>", "C3": "k_step<SweRoe,16,384,2>"}[args.workload]
-    # dominant kernel of the timed step: k_copy_classify (~70 % of the step; streams every cell's
-    # q_old -> q_new, 64 algorithmic bytes per cell-update, and classifies the patches), timed with
-    # CUDA events around its launches on the library's stream.  The whole update phase (copy +
-    # activity + k_step on the active patches) is reported beside it.
+    prof = profile_summary(args.workload) or {}
+    kernel = {"C5": "k_step<EulerRoe>", "C3": "k_step<SweRoe>"}[args.workload]
+    # dominant kernel of the full step: the update kernel (ghost kernels fill the rings first),
+    # its launch time from CUDA events around its launches on the library's stream
     step_ms = st["ms_step"] / max(1, st["step_kernel_launches"])
     ghost_ms = st["ms_ghost"] / max(1, st["steps"])
-    copy_ms = st["ms_copy"] / max(1, st["copy_launches"]) if st.get("copy_launches") else None
-    ach_phase = local_cells * bpc / (step_ms / 1000.0) / 1e9
-    roofline_phase = {"bound": "hbm", "achieved": ach_phase, "peak": hbm_peak, "unit": "GB/s",
-                      "frac": ach_phase / hbm_peak, "frac_vs_nominal_8000": ach_phase / 8000.0,
-                      "traffic": prof.get("dram_bytes_per_launch") if prof else None,
-                      "kernel": "update phase of fc_step: k_copy_classify + k_activity + " + kernel +
-                                " on the active patches", "launch_ms": step_ms,
-                      "algorithmic_bytes_per_cell_update": bpc}
-    if copy_ms:
-        ach_gbs = local_cells * bpc / (copy_ms / 1000.0) / 1e9
-        roofline = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm_peak, "unit": "GB/s",
+    step_share = step_ms / (ms_i / args.steps)
+    ach_tf = local_cells * flops / (step_ms / 1000.0) / 1e12 if flops else None
+    roofline = {"bound": "alu", "achieved": ach_tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": (ach_tf / fp64_peak) if ach_tf else None,
+                "traffic": prof.get("step_dram_bytes_per_launch"),
+                "traffic_full_step": prof.get("full_step_dram_bytes"),
+                "algorithmic_bytes_per_launch": local_cells * bpc,
+                "kernel": kernel + " (full update; dominant kernel of the step)", "launch_ms": step_ms,
+                "share_of_step": step_share,
+                "algorithmic_flops_per_cell_update": flops,
+                "peak_source": "derived (DESIGN.md §6): 148 SMs x 64 fp64 FMA lanes x 2 flops x sm_max_mhz "
+                               f"({pk.get('sm_max_mhz', 1965.0)} MHz, {pk_src} MEASURED_PEAKS.json); the DFMA "
+                               "microbenchmark measures 34.1 TF (profiles/r01/dfma_peak.json)",
+                "flops_source": "profiles/algorithmic_flops.json (fp64 ops of the oracle's own code per "
+                                "cell-update, tools/count_flops.py)",
+                "traffic_source": prof.get("source"),
+                "timing": "kernel duration from CUDA events on the library stream in an instrumented twin "
+                          "of the timed region (same steps from the same state); the headline pass runs "
+                          "without the library's events"}
+    # the same full step against HBM: compulsory bytes per cell-update at the measured copy peak
+    ach_gbs = local_cells * bpc / (ms / args.steps / 1000.0) / 1e9
+    roofline_hbm = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": ach_gbs / hbm_peak, "frac_vs_nominal_8000": ach_gbs / 8000.0,
-                    "traffic": prof.get("copy_dram_bytes_per_launch") if prof else None,
-                    "kernel": "k_copy_classify<4,16> (dominant: streams q_old -> q_new, classifies patches)",
-                    "launch_ms": copy_ms, "share_of_step": copy_ms / (ms_i / args.steps),
-                    "timing": "kernel durations from CUDA events on the library stream in an instrumented "
-                              "twin of the timed region (same steps from the same state); the headline "
-                              "pass runs without the library's events",
+                    "what": "whole full step, compulsory bytes (q read + written once, 16 meqn B per "
+                            "cell-update): fp64-bound for the Euler/SWE solvers (BASELINE.md §2)",
                     "algorithmic_bytes_per_cell_update": bpc,
                     "peak_source": f"{pk_src} MEASURED_PEAKS.json hbm_gbs (copy)"}
-    else:
-        roofline = dict(roofline_phase, peak_source=f"{pk_src} MEASURED_PEAKS.json hbm_gbs (copy)")
-    # the full update (no shortcut) is bound by the fp64 pipe: algorithmic flops per cell-update
-    # counted on the oracle's own code
-    step_ms_full = st_full["ms_step"] / max(1, st_full["step_kernel_launches"])
-    ach_tf = local_cells * flops / (step_ms_full / 1000.0) / 1e12 if flops else None
-    roofline_alu = {"bound": "alu", "achieved": ach_tf, "peak": fp64_peak, "unit": "TFLOP/s",
-                    "frac": (ach_tf / fp64_peak) if ach_tf else None, "kernel": kernel + " (full update)",
-                    "launch_ms": step_ms_full, "algorithmic_flops_per_cell_update": flops,
-                    "peak_source": "derived: 148 SMs x 64 fp64 FMA lanes x 2 flops x sm_max_mhz "
-                                   f"({pk.get('sm_max_mhz', 1965.0)} MHz, {pk_src} MEASURED_PEAKS.json)",
-                    "flops_source": "profiles/algorithmic_flops.json (oracle's own ops, tools/count_flops.py)"}
-
+    # the data-dependent quiescent shortcut (exact, library default): per-kernel durations
+    copy_ms = st_q["ms_copy"] / max(1, st_q["copy_launches"]) if st_q.get("copy_launches") else None
+    quiescent = {"value": value_q, "unit": UNIT, "ms_per_step": ms_q / args.steps,
+                 "what": "skip_quiescent = 1 (library default): patches whose staged window holds one "
+                         "state skip the update arithmetic (bitwise exact: every jump is 0); their cells "
+                         "are still read and written (k_copy_classify). DATA-DEPENDENT: it measures the "
+                         "flow (C5: ~96 % of patches quiescent), not the method's arithmetic",
+                 "copy_kernel_ms": copy_ms,
+                 "copy_kernel_hbm_frac": (local_cells * bpc / (copy_ms / 1000.0) / 1e9 / hbm_peak) if copy_ms else None,
+                 "update_phase_ms": st_q["ms_step"] / max(1, st_q["step_kernel_launches"])}
     # ---- end-to-end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -463,21 +533,24 @@ def main():
         if args.workload == "C5":         # the oracle with OpenMP on all host cores too
             cpu["openmp"] = oracle_rate_openmp(max(1.0, args.cpu_seconds / 3))
 
+    variants = run_variants(args, fc, hbm_peak) if (args.variants and world == 1) else None
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": WORKLOADS[args.workload], "patches": P, "cells": cells_total,
+                           "mode": "full update of every patch (skip_quiescent = 0)",
                            "parallelism": f"morton-shard x{world}" + (f" (halo: {halo})" if world > 1 else ""),
                            "l2": "state 2 x %.2f GB >> 126 MB L2 (no flush needed)" % (P * w.meqn * (w.m + 4) ** 2 * 8 / 1e9),
                            "dt_policy": "Clawpack variable dt (0.9 / CFL)", "final_cfl": cfls[-1]},
-                "roofline": roofline, "roofline_update_phase": roofline_phase,
-                "roofline_alu_full_update": roofline_alu,
-                "value_full_update": value_full, "ms_per_step_full_update": ms_full / args.steps,
+                "roofline": roofline, "roofline_hbm": roofline_hbm,
+                "value_quiescent_skip": quiescent,
+                "variants_full_update": variants,
                 "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": st["kernel_launches"],
-                "phase_ms_per_step": {"ghost": ghost_ms, "update": step_ms, "cfl_allreduce": st["ms_comm"] / max(1, st["steps"]),
-                                      "update_full": step_ms_full},
+                "phase_ms_per_step": {"ghost": ghost_ms, "update": step_ms,
+                                      "cfl_allreduce": st["ms_comm"] / max(1, st["steps"])},
                 "clocks": clk}
         print(json.dumps(line), flush=True)
     f.close()
