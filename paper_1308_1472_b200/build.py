@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfc.so")
-SOURCES = ["api.cu", "kernels.cu", "step.cu", "plan.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "step.cu", "step_ws.cu", "plan.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

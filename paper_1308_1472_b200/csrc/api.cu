@@ -386,11 +386,19 @@ static bool has_round2(const fc_forest* f) { return f->npack[1] || f->nunpack[1]
 // velocity advection (measured: T1 full 1.00 -> 0.67 ms, T2 0.27 -> 0.22 ms; for Euler the gather
 // of every patch's ring in the 352-thread k_step costs more than the ghost kernels: C5 full 9.5 ->
 // 10.3 ms).  FC_FUSED_RING=0 at creation keeps the ghost kernels; the capacity form always does.
+// systems whose update the warp-sweep kernel takes (step_ws.cu): it gathers its windows itself,
+// so their full-update mode runs on the fused path too (FC_WS=0: the phased k_step + ghost kernels)
+static bool ws_applies(const fc_forest* f) {
+  static const bool off = getenv("FC_WS") && atoi(getenv("FC_WS")) == 0;
+  return !off && (f->prob.kind == FC_SWE_ROE || f->prob.kind == FC_EULER_ROE) && f->pl.m % 16 == 0 &&
+         !f->prob.reflux;
+}
+
 static bool use_fused(const fc_forest* f) {
   if (!f->fused) return false;
   if (f->prob.kind == FC_ADV_EDGEVEL_CAPA)   // (aux staging of the fused multi-tile windows: not built)
     return (f->pl.m == 16 || f->pl.m == 8) && (std::getenv("FC_FUSED_CAPA") == nullptr || std::atoi(std::getenv("FC_FUSED_CAPA")) != 0);
-  return f->prob.skip_quiescent || f->prob.kind == FC_ADV_CONST;
+  return f->prob.skip_quiescent || f->prob.kind == FC_ADV_CONST || ws_applies(f);
 }
 
 static void run_ghost(fc_forest* f, int op, const DevList& l) {

@@ -26,95 +26,9 @@
 #include "../../include/fc.h"
 #include "fc_internal.h"
 #include "solvers.cuh"
+#include "step_common.cuh"
 
 namespace fc {
-
-// wave limiters as one branch-free form phi = max(lo, min(c1 + c2 theta, c3, c4 theta)):
-//   MC     (lo, c1, c2, c3, c4) = (0, 1/2, 1/2, 2, 2)   -> max(0, min((1+t)/2, 2, 2t))
-//   minmod                        (0, 1,   0,   1, 1)   -> max(0, min(1, t))
-//   none                          (1, 1,   0,   1, 1)   -> 1
-struct LimiterCoef {
-  double lo, c1, c2, c3, c4;
-};
-__host__ __device__ inline LimiterCoef limiter_coef(int lim) {
-  if (lim == 2) return {0.0, 0.5, 0.5, 2.0, 2.0};
-  if (lim == 1) return {0.0, 1.0, 0.0, 1.0, 1.0};
-  return {1.0, 1.0, 0.0, 1.0, 1.0};
-}
-__device__ __forceinline__ double limiter_phi(const LimiterCoef& L, double th) {
-  return fmax(L.lo, fmin(fmin(fma(L.c2, th, L.c1), L.c3), L.c4 * th));
-}
-
-struct StepArgs {
-  const double* __restrict__ qold;
-  double* __restrict__ qnew;
-  const double* __restrict__ aux;     // [Pl][3][n][n] or null
-  const int8_t* __restrict__ level;   // [Pl]
-  double dt, dx0;
-  SolverParams sp;
-  int limiter, method2, method3;
-  int skip_quiescent;                 // exact shortcut for tiles whose staged window is uniform
-  const int32_t* __restrict__ ring;   // fused ring gather (RingSources.src) or null: ring in q_old
-  const uint8_t* __restrict__ bcflag; // per patch: bit 0 BCX, bit 1 BCY entries present
-  const int32_t* __restrict__ active; // active-patch list (quiescent patches filtered out) or null
-  const int32_t* __restrict__ nactive;
-  LimiterCoef lim;
-  int m, tiles;                       // tiles per side
-  unsigned long long* cfl_bits;
-  double* fbuf;                       // method3 = 1 only: per-CTA F~ of each correction edge [MEQN][E2]
-  const int32_t* __restrict__ rslot;  // reflux: per patch flux-register slot (-1: none) or null
-  double* freg;                       // reflux: [slot][4 faces][m edges][MEQN] applied fluxes, outward
-  const uint8_t* __restrict__ rpeer;  // peer-memory halo: owner of each ring source (0 = this rank)
-  const double* peerq[16];            // peer-memory halo: rank r's current q_old (peer pointer)
-  const double* cg;                   // fused AMR ring gather: computed ghosts (ring peer code 255)
-};
-// base of a ring source: this rank's q_old, a peer's (code k = rank k - 1), the computed ghosts (255)
-__device__ __forceinline__ const double* ring_base(const StepArgs& A, int ow) {
-  return ow == 0 ? A.qold : (ow == 255 ? A.cg : A.peerq[ow - 1]);
-}
-
-// ---- TMA bulk copies + mbarrier (sm_90+ / sm_100a) -------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// global -> shared bulk copy (UBLKCP); bytes and both addresses multiples of 16
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-// an opaque copy: keeps per-thread index arithmetic inside the tile loop instead of letting the
-// compiler hoist (and keep live in registers) every phase's thread->edge mapping
-__device__ __forceinline__ int opaque(int x) {
-  int y;
-  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
-  return y;
-}
-// 8-byte async global -> shared copy (LDGSTS), completion tracked with cp.async groups
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 template <class S, int T>
 struct StepShape {
@@ -324,22 +238,6 @@ __device__ __forceinline__ void stage_tile(const StepArgs& A, int tile, double* 
       }
     }
   }
-}
-
-// window index (padded index, W = n) of ring cell r in ring storage order (j = -1..m+2 outer,
-// i = -1..m+2 inner, interior skipped)
-template <int T>
-__device__ __forceinline__ int ring_window_index(int r) {
-  constexpr int n = T + 4;
-  if (r < 2 * n) return r;                                   // rows j = -1, 0
-  r -= 2 * n;
-  if (r < 4 * T) {                                           // rows 1..m: i = -1, 0, m+1, m+2
-    const int j = r / 4 + 1, c = r % 4;
-    const int i = c < 2 ? c - 1 : T + c - 1;
-    return (j + 1) * n + (i + 1);
-  }
-  r -= 4 * T;
-  return (T + 2) * n + r;                                    // rows j = m+1, m+2
 }
 
 template <class S, int T, int NT>
@@ -1917,55 +1815,43 @@ static int launch_step_r(const StepArgs& a, int64_t npatch, cudaStream_t st) {
 
 template <class S>
 static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
-  // CTAs per SM requested from ptxas for the 16 x 16 tile (register budget 65536 / (352 MB));
-  // FC_STEP_MINB overrides it for tuning experiments (without reflux records)
-  static const int env_mb = getenv("FC_STEP_MINB") ? atoi(getenv("FC_STEP_MINB")) : 0;
-  // scalar solvers: the two-phase kernel (FC_SCALAR_PHASED=1 keeps the generic phased k_step)
-  static const bool phased = getenv("FC_SCALAR_PHASED") && atoi(getenv("FC_SCALAR_PHASED"));
   // constant-velocity advection on whole 8 x 8 / 16 x 16 patches: the register-sweep kernel
   // (FC_SCALAR_CV=0 keeps k_step_sc; reflux records need method3 = 2 here)
   static const bool cv = !(getenv("FC_SCALAR_CV") && atoi(getenv("FC_SCALAR_CV")) == 0);
   // (the choice may not depend on the local patch count: results must not depend on the sharding)
   if constexpr (std::is_same<S, AdvConst>::value) {
-    if (cv && !phased && (!a.rslot || a.method3 == 2) && a.tiles == 1 && a.limiter != 0) {
+    if (cv && (!a.rslot || a.method3 == 2) && a.tiles == 1 && a.limiter != 0) {
       if (a.m == 16) return launch_cv<16>(a, npatch, st);
       if (a.m == 8) return launch_cv<8>(a, npatch, st);
     }
   }
   if constexpr (std::is_same<S, AdvEdgeCapa>::value) {   // capacity form: the same sweep, aux from global
-    if (cv && !phased && !a.rslot && a.tiles == 1 && a.limiter != 0) {
+    if (cv && !a.rslot && a.tiles == 1 && a.limiter != 0) {
       const bool mt2 = a.method3 == 2;
       if (a.m == 16) return mt2 ? launch_cvc_t<16, true>(a, npatch, st) : launch_cvc_t<16, false>(a, npatch, st);
       if (a.m == 8) return mt2 ? launch_cvc_t<8, true>(a, npatch, st) : launch_cvc_t<8, false>(a, npatch, st);
     }
   }
-  if constexpr (S::MEQN == 1) {
-    if (!phased) {
-      if (a.m % 16 == 0) return launch_sc<S, 16>(a, npatch, st);
-      if (a.m % 8 == 0) return launch_sc<S, 8>(a, npatch, st);
-      if (a.m % 4 == 0) return launch_sc<S, 4>(a, npatch, st);
-      if (a.m % 2 == 0) return launch_sc<S, 2>(a, npatch, st);
+  if constexpr (S::MEQN == 1) {   // scalars: the two-phase kernel
+    if (a.m % 16 == 0) return launch_sc<S, 16>(a, npatch, st);
+    if (a.m % 8 == 0) return launch_sc<S, 8>(a, npatch, st);
+    if (a.m % 4 == 0) return launch_sc<S, 4>(a, npatch, st);
+    if (a.m % 2 == 0) return launch_sc<S, 2>(a, npatch, st);
+    return -1;
+  } else {
+    // systems: the phased kernel; CTAs per SM requested from ptxas for the 16 x 16 tile
+    // (HLLE's 15-slot edge scratch leaves shared memory for one 16 x 16 CTA per SM)
+    constexpr int dmb = std::is_same<S, EulerHlle>::value ? 1 : 2;
+    if (a.m % 16 == 0) {
+      // 384 threads (12 warps; 2 CTAs keep the 80-register budget): measured on C5 full update
+      // 8.58 -> 8.12 ms vs 352; 416 / 448 (72 registers, spills): 8.78 ms (`tools/nt_variants.sh`)
+      return launch_step_r<S, 16, 384, dmb>(a, npatch, st);
     }
+    if (a.m % 8 == 0) return launch_step_r<S, 8, 128, 4>(a, npatch, st);
+    if (a.m % 4 == 0) return launch_step_r<S, 4, 64, 8>(a, npatch, st);
+    if (a.m % 2 == 0) return launch_step_r<S, 2, 32, 8>(a, npatch, st);
+    return -1;
   }
-  // (HLLE's 15-slot edge scratch leaves shared memory for one 16 x 16 CTA per SM)
-  constexpr int dmb = std::is_same<S, EulerHlle>::value ? 1 : ((S::MEQN >= 3) ? 2 : 3);
-  const int mb = env_mb ? env_mb : dmb;
-  if (a.m % 16 == 0) {
-    // 384 threads (12 warps; 2 CTAs keep the 80-register budget): measured on C5 full update
-    // 8.58 -> 8.12 ms vs 352; 416 / 448 (72 registers, spills): 8.78 ms (`tools/nt_variants.sh`)
-#ifndef STEP_NT16
-#define STEP_NT16 384
-#endif
-    if (a.rslot || mb == dmb) return launch_step_r<S, 16, STEP_NT16, dmb>(a, npatch, st);
-    if (mb == 1) return launch_step_t<S, 16, 352, 1, false>(a, npatch, st);
-    if (mb == 2) return launch_step_t<S, 16, 352, 2, false>(a, npatch, st);
-    if (mb == 3) return launch_step_t<S, 16, 352, 3, false>(a, npatch, st);
-    return launch_step_t<S, 16, 352, 4, false>(a, npatch, st);
-  }
-  if (a.m % 8 == 0) return launch_step_r<S, 8, 128, 4>(a, npatch, st);
-  if (a.m % 4 == 0) return launch_step_r<S, 4, 64, 8>(a, npatch, st);
-  if (a.m % 2 == 0) return launch_step_r<S, 2, 32, 8>(a, npatch, st);
-  return -1;
 }
 
 int launch_step(int kind, const double* qold, double* qnew, const double* aux, const int8_t* level,
@@ -1994,6 +1880,10 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
   const int T = (m % 16 == 0) ? 16 : ((m % 8 == 0) ? 8 : ((m % 4 == 0) ? 4 : 2));
   a.tiles = m / T;
   a.cfl_bits = cfl_bits;
+  {   // systems on the fused ring gather: the warp-sweep kernel (step_ws.cu) where it applies
+    const int r = launch_step_ws(kind, a, npatch, st);
+    if (r != 0) return r;
+  }
   switch (kind) {
     case FC_ADV_CONST: return launch_step_s<AdvConst>(a, npatch, st);
     case FC_ADV_EDGEVEL_CAPA: return launch_step_s<AdvEdgeCapa>(a, npatch, st);

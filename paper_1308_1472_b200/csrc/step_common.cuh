@@ -1,0 +1,119 @@
+// step_common.cuh -- declarations shared by the step kernels (step.cu: phased / scalar / sweep
+// kernels; step_ws.cu: the warp-sweep kernel for systems).  libfc only, nothing shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fc_internal.h"
+#include "solvers.cuh"
+
+namespace fc {
+
+// wave limiters as one branch-free form phi = max(lo, min(c1 + c2 theta, c3, c4 theta)):
+//   MC     (lo, c1, c2, c3, c4) = (0, 1/2, 1/2, 2, 2)   -> max(0, min((1+t)/2, 2, 2t))
+//   minmod                        (0, 1,   0,   1, 1)   -> max(0, min(1, t))
+//   none                          (1, 1,   0,   1, 1)   -> 1
+struct LimiterCoef {
+  double lo, c1, c2, c3, c4;
+};
+__host__ __device__ inline LimiterCoef limiter_coef(int lim) {
+  if (lim == 2) return {0.0, 0.5, 0.5, 2.0, 2.0};
+  if (lim == 1) return {0.0, 1.0, 0.0, 1.0, 1.0};
+  return {1.0, 1.0, 0.0, 1.0, 1.0};
+}
+__device__ __forceinline__ double limiter_phi(const LimiterCoef& L, double th) {
+  return fmax(L.lo, fmin(fmin(fma(L.c2, th, L.c1), L.c3), L.c4 * th));
+}
+
+struct StepArgs {
+  const double* __restrict__ qold;
+  double* __restrict__ qnew;
+  const double* __restrict__ aux;     // [Pl][3][n][n] or null
+  const int8_t* __restrict__ level;   // [Pl]
+  double dt, dx0;
+  SolverParams sp;
+  int limiter, method2, method3;
+  int skip_quiescent;                 // exact shortcut for tiles whose staged window is uniform
+  const int32_t* __restrict__ ring;   // fused ring gather (RingSources.src) or null: ring in q_old
+  const uint8_t* __restrict__ bcflag; // per patch: bit 0 BCX, bit 1 BCY entries present
+  const int32_t* __restrict__ active; // active-patch list (quiescent patches filtered out) or null
+  const int32_t* __restrict__ nactive;
+  LimiterCoef lim;
+  int m, tiles;                       // tiles per side
+  unsigned long long* cfl_bits;
+  double* fbuf;                       // method3 = 1 only: per-CTA F~ of each correction edge [MEQN][E2]
+  const int32_t* __restrict__ rslot;  // reflux: per patch flux-register slot (-1: none) or null
+  double* freg;                       // reflux: [slot][4 faces][m edges][MEQN] applied fluxes, outward
+  const uint8_t* __restrict__ rpeer;  // peer-memory halo: owner of each ring source (0 = this rank)
+  const double* peerq[16];            // peer-memory halo: rank r's current q_old (peer pointer)
+  const double* cg;                   // fused AMR ring gather: computed ghosts (ring peer code 255)
+};
+// base of a ring source: this rank's q_old, a peer's (code k = rank k - 1), the computed ghosts (255)
+__device__ __forceinline__ const double* ring_base(const StepArgs& A, int ow) {
+  return ow == 0 ? A.qold : (ow == 255 ? A.cg : A.peerq[ow - 1]);
+}
+
+// ---- TMA bulk copies + mbarrier (sm_90+ / sm_100a) -------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy (UBLKCP); bytes and both addresses multiples of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// an opaque copy: keeps per-thread index arithmetic inside the tile loop instead of letting the
+// compiler hoist (and keep live in registers) every phase's thread->edge mapping
+__device__ __forceinline__ int opaque(int x) {
+  int y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+// 8-byte async global -> shared copy (LDGSTS), completion tracked with cp.async groups
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// window index (padded index, W = n) of ring cell r in ring storage order (j = -1..m+2 outer,
+// i = -1..m+2 inner, interior skipped)
+template <int T>
+__device__ __forceinline__ int ring_window_index(int r) {
+  constexpr int n = T + 4;
+  if (r < 2 * n) return r;                                   // rows j = -1, 0
+  r -= 2 * n;
+  if (r < 4 * T) {                                           // rows 1..m: i = -1, 0, m+1, m+2
+    const int j = r / 4 + 1, c = r % 4;
+    const int i = c < 2 ? c - 1 : T + c - 1;
+    return (j + 1) * n + (i + 1);
+  }
+  r -= 4 * T;
+  return (T + 2) * n + r;                                    // rows j = m+1, m+2
+}
+
+// the warp-sweep kernel for systems (step_ws.cu): 1 = launched, 0 = not applicable (the caller
+// falls back to k_step), < 0 = error
+int launch_step_ws(int kind, const StepArgs& a, int64_t npatch, cudaStream_t st);
+
+}  // namespace fc

@@ -1,0 +1,620 @@
+// step_ws.cu -- the warp-sweep step kernel for systems (libfc, sm_100a, fp64): Roe shallow water
+// (C3) and Roe Euler with the Harten-Hyman entropy fix (C5).
+//
+// PAPER.md:168-182 [§3]: Clawpack's unsplit wave propagation on one patch -- Riemann problems at
+// every edge, left/right-going waves, a wave limiter on the upwind neighbour's wave, second-order
+// corrections, transverse (rpt2) corrections (readings in DESIGN.md §3).  Same arithmetic as the
+// phased k_step (step.cu) and the oracle (oracle/claw.c), different schedule:
+//
+// One CTA (NW warps) per 16 x 16 tile at a time (persistent over tiles), its 20 x 20 window (tile +
+// 2-cell halo, natural layout, pitch 21: conflict-free column access) gathered by cp.async straight
+// from the neighbours' interiors (the fused ring gather: no ring is ever written to HBM), the next
+// tile's gather in flight while the current one computes.  Per tile three phases, one barrier each:
+//   X  the 18 x 19 x-edges of rows 0..17 as 12 warp-iterations of 32 consecutive edges (row-major,
+//      advancing 29: lanes 0 and 31 are halo edges for the limiter).  Per lane: both cells' derived
+//      fields, the Roe solve (+ Harten-Hyman A-dq), then per wave family the upwind neighbour's wave
+//      by one warp shuffle -> limiter, F~, CFL; the L part (A-dq + F~) of the next edge and its
+//      Roe state by shuffle; both transverse splits entering the lane's right cell -> up / dn (G~
+//      halves) and the x increment of the cell, to shared memory.
+//   Y  the same along y (column-major flat edges); the lane owning a cell also folds the x-sweep's
+//      G~ differences into its increment; transverse parts -> rt / lf (F~ halves).
+//   F  per cell q_new = q + dq - r (F~(i+1/2) - F~(i-1/2)), stored coalesced; non-finite check.
+// No per-edge scratch round trip through shared memory (the phased kernel's 7 barrier-separated
+// phases and 13-slot edge scratch), no index tables, every edge solved once per sweep except the two
+// halo lanes of each iteration.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "../../include/fc.h"
+#include "fc_internal.h"
+#include "solvers.cuh"
+#include "step_common.cuh"
+
+namespace fc {
+
+// ------------------------------------------------------------------------------------------------
+// register-resident views of the solvers (the same formulas as solvers.cuh / SURVEY §8(c.5))
+struct WsEuler {
+  static constexpr int MEQN = 4, MW = 4;
+  struct Cell {
+    double q[4];
+    double sr, u, v, H, c2;   // sqrt(rho), velocity, enthalpy, sound speed squared
+  };
+  struct Edge {
+    double a[4];              // wave strengths
+    double u, v, H, c, ic;    // Roe state
+    double am[4];             // A-dq (Harten-Hyman fixed)
+  };
+  __device__ static void cell(Cell& C, const SolverParams& P) {
+    const double gam = P.p0, gm1 = gam - 1.0;
+    const double rho = C.q[0];
+    const double rs = fast_rsqrt(rho);
+    const double ir = rs * rs;
+    C.sr = rho * rs;
+    C.u = C.q[1] * ir;
+    C.v = C.q[2] * ir;
+    const double p = gm1 * (C.q[3] - 0.5 * rho * (C.u * C.u + C.v * C.v));
+    C.H = (C.q[3] + p) * ir;
+    C.c2 = gam * p * ir;
+  }
+  // lambda = m/rho -+ c of a conserved state is beyond 0 (division-free: m^2 > gam (gam-1) (E rho - |m|^2/2))
+  __device__ static bool supersonic(double rho, double mn, double mt, double E, double gam) {
+    return mn * mn > gam * (gam - 1.0) * (E * rho - 0.5 * (mn * mn + mt * mt));
+  }
+  template <int D>
+  __device__ static void riemann(const Cell& L, const Cell& R, const SolverParams& P, Edge& E) {
+    constexpr int nd = D, td = 3 - D;
+    const double gam = P.p0, gm1 = gam - 1.0;
+    const double inv = fast_rcp(L.sr + R.sr);
+    const double al = L.sr * inv, ar = R.sr * inv;
+    const double u = al * L.u + ar * R.u;
+    const double v = al * L.v + ar * R.v;
+    const double H = al * L.H + ar * R.H;
+    const double c2 = gm1 * (H - 0.5 * (u * u + v * v));
+    const double ic = fast_rsqrt(c2);
+    const double c = c2 * ic;
+    const double un = nd == 1 ? u : v, vt = nd == 1 ? v : u;
+    double d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d[k] = R.q[k] - L.q[k];
+    const double a3 = d[td] - vt * d[0];
+    const double a2 = gm1 * (ic * ic) * ((H - un * un - vt * vt) * d[0] + un * d[nd] + vt * d[td] - d[3]);
+    const double a4 = (d[nd] + (c - un) * d[0] - c * a2) * (0.5 * ic);
+    const double a1 = d[0] - a2 - a4;
+    E.a[0] = a1; E.a[1] = a2; E.a[2] = a3; E.a[3] = a4;
+    E.u = u; E.v = v; E.H = H; E.c = c; E.ic = ic;
+    double W1[4], W4[4], W23[4];
+    W1[0] = a1; W1[nd] = a1 * (un - c); W1[td] = a1 * vt; W1[3] = a1 * (H - un * c);
+    W4[0] = a4; W4[nd] = a4 * (un + c); W4[td] = a4 * vt; W4[3] = a4 * (H + un * c);
+    W23[0] = a2; W23[nd] = a2 * un; W23[td] = a2 * vt + a3;
+    W23[3] = a2 * 0.5 * (un * un + vt * vt) + a3 * vt;
+    const double s1 = un - c, s2 = un, s4 = un + c;
+    if (P.p1 == 0.0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) E.am[k] = dmin0(s1) * W1[k] + dmin0(s2) * W23[k] + dmin0(s4) * W4[k];
+      return;
+    }
+    // Harten-Hyman; the signs of lambda_1(Q_l) and lambda_4(Q_r) by
+    // division-free tests, their values only in the (rare) transonic case
+    const double unl = nd == 1 ? L.u : L.v, unr = nd == 1 ? R.u : R.v;
+    const bool s0_nonneg = unl >= 0.0 && unl * unl >= L.c2;          // lambda_1(Q_l) >= 0
+#pragma unroll
+    for (int k = 0; k < 4; ++k) E.am[k] = 0.0;
+    if (s0_nonneg && s1 > 0.0) return;                                // (i) supersonic to the right
+    double beta = s1 < 0.0 ? s1 : 0.0;                                // (ii)
+    if (!s0_nonneg) {
+      double q1[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q1[k] = L.q[k] + W1[k];
+      if (q1[nd] > 0.0 && supersonic(q1[0], q1[nd], q1[td], q1[3], gam)) {   // lambda_1(Q_l + W1) > 0
+        const double s0 = unl - L.c2 * fast_rsqrt(L.c2);
+        const double ir = fast_rcp(q1[0]);
+        const double un1 = q1[nd] * ir, ut1 = q1[td] * ir;
+        const double p1 = gm1 * (q1[3] - 0.5 * q1[0] * (un1 * un1 + ut1 * ut1));
+        const double cc = gam * p1 * ir;
+        const double lr = un1 - cc * fast_rsqrt(cc);
+        beta = s0 * (lr - s1) * fast_rcp(lr - s0);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) E.am[k] = beta * W1[k];
+    if (s2 < 0.0) {                                                   // (iii)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) E.am[k] += s2 * W23[k];
+      double b4 = s4 < 0.0 ? s4 : 0.0;                                // (iv)
+      const bool s4r_pos = !(unr < 0.0 && unr * unr >= R.c2);         // lambda_4(Q_r) > 0
+      if (s4r_pos) {
+        double q3[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q3[k] = R.q[k] - W4[k];
+        if (q3[nd] < 0.0 && supersonic(q3[0], q3[nd], q3[td], q3[3], gam)) {   // lambda_4(Q_r - W4) < 0
+          const double s4r = unr + R.c2 * fast_rsqrt(R.c2);
+          const double ir = fast_rcp(q3[0]);
+          const double un3 = q3[nd] * ir, ut3 = q3[td] * ir;
+          const double p3 = gm1 * (q3[3] - 0.5 * q3[0] * (un3 * un3 + ut3 * ut3));
+          const double cc = gam * p3 * ir;
+          const double ll = un3 + cc * fast_rsqrt(cc);
+          b4 = ll * (s4r - s4) * fast_rcp(s4r - ll);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) E.am[k] += b4 * W4[k];
+    }
+  }
+  template <int D>
+  __device__ static double speed(const Edge& E, int p) {
+    const double un = D == 1 ? E.u : E.v;
+    return p == 0 ? un - E.c : (p == 3 ? un + E.c : un);
+  }
+  template <int D>
+  __device__ static void wave(const Edge& E, int p, double* W) {
+    constexpr int nd = D, td = 3 - D;
+    const double un = nd == 1 ? E.u : E.v, vt = nd == 1 ? E.v : E.u;
+    const double a = E.a[p];
+    if (p == 2) { W[0] = 0.0; W[nd] = 0.0; W[td] = a; W[3] = a * vt; return; }
+    if (p == 1) { W[0] = a; W[nd] = a * un; W[td] = a * vt; W[3] = a * 0.5 * (un * un + vt * vt); return; }
+    const double sg = p == 0 ? -1.0 : 1.0;
+    W[0] = a; W[nd] = a * (un + sg * E.c); W[td] = a * vt; W[3] = a * (E.H + sg * un * E.c);
+  }
+  // the Roe state an edge's transverse split needs (shuffled from the neighbouring lane)
+  struct Roe {
+    double u, v, H, c, ic;
+  };
+  __device__ static Roe roe(const Edge& E) { return {E.u, E.v, E.H, E.c, E.ic}; }
+  __device__ static Roe shfl_down(const Roe& r, int d) {
+    return {__shfl_down_sync(0xffffffffu, r.u, d), __shfl_down_sync(0xffffffffu, r.v, d),
+            __shfl_down_sync(0xffffffffu, r.H, d), __shfl_down_sync(0xffffffffu, r.c, d),
+            __shfl_down_sync(0xffffffffu, r.ic, d)};
+  }
+  template <int D>
+  __device__ static void transverse(const Roe& r, const SolverParams& P, const double* X, double* bm, double* bp) {
+    EulerRoe::roe_transverse<D>(r.u, r.v, r.H, r.c, r.ic, P.p0 - 1.0, X, bm, bp);
+  }
+  __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, double dtdx) {
+    return EulerRoe::quiescent_cfl(q, qs, P, nullptr, dtdx, 0, 0, 0, 0);
+  }
+};
+
+struct WsSwe {
+  static constexpr int MEQN = 3, MW = 3;
+  struct Cell {
+    double q[3];
+    double sr, u, v;
+  };
+  struct Edge {
+    double a[3];
+    double u, v, c, ic;
+    double am[3];
+  };
+  __device__ static void cell(Cell& C, const SolverParams&) {
+    const double h = C.q[0];
+    const double rs = fast_rsqrt(h);
+    const double ih = rs * rs;
+    C.sr = h * rs;
+    C.u = C.q[1] * ih;
+    C.v = C.q[2] * ih;
+  }
+  template <int D>
+  __device__ static void riemann(const Cell& L, const Cell& R, const SolverParams& P, Edge& E) {
+    constexpr int nd = D, td = 3 - D;
+    const double inv = fast_rcp(L.sr + R.sr);
+    const double al = L.sr * inv, ar = R.sr * inv;
+    const double u = al * L.u + ar * R.u;
+    const double v = al * L.v + ar * R.v;
+    const double c2 = 0.5 * P.p0 * (L.q[0] + R.q[0]);
+    const double ic = fast_rsqrt(c2);
+    const double c = c2 * ic;
+    const double un = nd == 1 ? u : v, ut = nd == 1 ? v : u;
+    const double dh = R.q[0] - L.q[0], dn = R.q[nd] - L.q[nd], dtg = R.q[td] - L.q[td];
+    const double i2c = 0.5 * ic;
+    E.a[0] = ((un + c) * dh - dn) * i2c;
+    E.a[1] = dtg - ut * dh;
+    E.a[2] = ((c - un) * dh + dn) * i2c;
+    E.u = u; E.v = v; E.c = c; E.ic = ic;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) E.am[k] = 0.0;
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      double W[3];
+      wave<D>(E, p, W);
+      const double s = speed<D>(E, p);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) E.am[k] += dmin0(s) * W[k];
+    }
+  }
+  template <int D>
+  __device__ static double speed(const Edge& E, int p) {
+    const double un = D == 1 ? E.u : E.v;
+    return p == 0 ? un - E.c : (p == 1 ? un : un + E.c);
+  }
+  template <int D>
+  __device__ static void wave(const Edge& E, int p, double* W) {
+    constexpr int nd = D, td = 3 - D;
+    const double un = nd == 1 ? E.u : E.v, ut = nd == 1 ? E.v : E.u;
+    const double a = E.a[p];
+    if (p == 1) { W[0] = 0.0; W[nd] = 0.0; W[td] = a; return; }
+    W[0] = a;
+    W[nd] = a * (p == 0 ? un - E.c : un + E.c);
+    W[td] = a * ut;
+  }
+  struct Roe {
+    double u, v, c, ic;
+  };
+  __device__ static Roe roe(const Edge& E) { return {E.u, E.v, E.c, E.ic}; }
+  __device__ static Roe shfl_down(const Roe& r, int d) {
+    return {__shfl_down_sync(0xffffffffu, r.u, d), __shfl_down_sync(0xffffffffu, r.v, d),
+            __shfl_down_sync(0xffffffffu, r.c, d), __shfl_down_sync(0xffffffffu, r.ic, d)};
+  }
+  template <int D>
+  __device__ static void transverse(const Roe& r, const SolverParams&, const double* X, double* bm, double* bp) {
+    constexpr int nd = 3 - D, td = D;   // eigen-decomposition along the transverse direction
+    const double vn = nd == 1 ? r.u : r.v, vt = nd == 1 ? r.v : r.u, c = r.c;
+    const double i2c = 0.5 * r.ic;
+    const double b1 = ((vn + c) * X[0] - X[nd]) * i2c;
+    const double b2 = X[td] - vt * X[0];
+    const double b3 = ((c - vn) * X[0] + X[nd]) * i2c;
+    double l1m, l1p, l2m, l2p, l3m, l3p;
+    split0(vn - c, l1m, l1p);
+    split0(vn, l2m, l2p);
+    split0(vn + c, l3m, l3p);
+    const double m1 = l1m * b1, m2 = l2m * b2, m3 = l3m * b3;
+    const double p1 = l1p * b1, p2 = l2p * b2, p3 = l3p * b3;
+    bm[0] = m1 + m3;
+    bm[nd] = m1 * (vn - c) + m3 * (vn + c);
+    bm[td] = (m1 + m3) * vt + m2;
+    bp[0] = p1 + p3;
+    bp[nd] = p1 * (vn - c) + p3 * (vn + c);
+    bp[td] = (p1 + p3) * vt + p2;
+  }
+  __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, double dtdx) {
+    return SweRoe::quiescent_cfl(q, qs, P, nullptr, dtdx, 0, 0, 0, 0);
+  }
+};
+
+// ------------------------------------------------------------------------------------------------
+template <class S>
+struct WsShape {
+  static constexpr int T = 16, W = T + 4, PW = W + 1;          // window 20 x 20, row pitch 21
+  static constexpr int WPW = W * PW;                           // component stride of the window
+  static constexpr int NE = T + 3, NR = T + 2, E = NR * NE;    // 19 edges x 18 rows per sweep
+  static constexpr int STEP = 29, NIT = (E + STEP - 1) / STEP; // 12 warp-iterations per sweep
+  static constexpr int QB = S::MEQN * WPW;
+  static constexpr int UPP = T + 1;                            // up / dn rows [k][j = 0..T+1][i = 1..T]
+  static constexpr int RTP = T + 3;                            // rt / lf rows [k][j = 1..T][i = 0..T+1]
+  static constexpr int DQP = T + 1;                            // dq rows [k][j = 1..T][i = 1..T]
+  static constexpr int N_UP = S::MEQN * NR * UPP;
+  static constexpr int N_RT = S::MEQN * T * RTP;
+  static constexpr int N_DQ = S::MEQN * T * DQP;
+  static constexpr size_t smem_doubles = 2 * (size_t)QB + 2 * (size_t)N_UP + 2 * (size_t)N_RT + N_DQ;
+  static constexpr size_t smem_bytes = smem_doubles * sizeof(double);
+};
+
+// tile -> (patch, tile column, tile row)
+__device__ __forceinline__ void ws_tile(const StepArgs& A, int tile, int& patch, int& tx, int& ty) {
+  patch = tile;
+  tx = ty = 0;
+  if (A.tiles > 1) {
+    const int t2 = A.tiles * A.tiles;
+    patch = tile / t2;
+    const int t = tile - patch * t2;
+    ty = t / A.tiles;
+    tx = t - ty * A.tiles;
+  }
+}
+
+// cp.async gather of tile `tile`'s 20 x 20 window (natural layout, pitch 21): cells inside the patch
+// interior from its own storage block, the others from the ring-source table (a neighbour's
+// interior, a peer rank's buffer, or a computed ghost); physical-boundary cells after the wait
+template <class S>
+__device__ __forceinline__ void ws_gather(const StepArgs& A, int tile, double* sq, int tid, int nt) {
+  using Sh = WsShape<S>;
+  constexpr int T = Sh::T, W = Sh::W, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN;
+  int patch, tx, ty;
+  ws_tile(A, tile, patch, tx, ty);
+  const int m = A.m, n = m + 4, n2 = n * n, G = n2 - m * m;
+  const double* qb = A.qold + (int64_t)patch * MEQN * n2;
+  const int32_t* rs = A.ring + (int64_t)patch * G;
+  const uint8_t* rp = A.rpeer ? A.rpeer + (int64_t)patch * G : nullptr;
+  for (int c = tid; c < W * W; c += nt) {
+    const int wj = c / W, wi = c - wj * W;
+    const int i = tx * T + wi - 1, j = ty * T + wj - 1;   // patch cell (1-based interior)
+    double* d = sq + wj * PW + wi;
+    const double* src;
+    if ((unsigned)(i - 1) < (unsigned)m && (unsigned)(j - 1) < (unsigned)m) {
+      src = qb + (j - 1) * m + (i - 1);
+    } else {
+      const int r = ring_index(i, j, m);
+      const int32_t v = __ldg(rs + r);
+      if (v < 0) continue;                                 // physical boundary: ws_bc
+      src = ring_base(A, rp ? __ldg(rp + r) : 0) + v;
+    }
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) cp_async8(d + k * WPW, src + (int64_t)k * n2);
+  }
+}
+
+// physical-boundary window cells, x faces (is_y = 0) then y faces: copy (wall: negate the normal
+// momentum) of the patch cell the ring-source code names (within 2 cells: inside this window)
+template <class S>
+__device__ __forceinline__ void ws_bc(const StepArgs& A, int tile, double* sq, int is_y, int tid, int nt) {
+  using Sh = WsShape<S>;
+  constexpr int T = Sh::T, W = Sh::W, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN;
+  int patch, tx, ty;
+  ws_tile(A, tile, patch, tx, ty);
+  const int m = A.m, n = m + 4, G = n * n - m * m;
+  const int32_t* rs = A.ring + (int64_t)patch * G;
+  for (int c = tid; c < W * W; c += nt) {
+    const int wj = c / W, wi = c - wj * W;
+    const int i = tx * T + wi - 1, j = ty * T + wj - 1;
+    if ((unsigned)(i - 1) < (unsigned)m && (unsigned)(j - 1) < (unsigned)m) continue;
+    const int32_t v = __ldg(rs + ring_index(i, j, m));
+    if (v >= 0) continue;
+    const int code = -1 - v;
+    if ((code & 1) != is_y) continue;
+    const int src = code >> 3, neg = (code >> 1) & 3;
+    const int si = src % n - 1, sj = src / n - 1;
+    const int ws = (sj - ty * T + 1) * PW + (si - tx * T + 1);
+    const int wd = wj * PW + wi;
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) {
+      const double x = sq[k * WPW + ws];
+      sq[k * WPW + wd] = (neg != 0 && k == neg) ? -x : x;
+    }
+  }
+}
+
+// One sweep (D = 1: x-edges of rows 0..T+1; D = 2: y-edges of columns 0..T+1) as NIT warp-iterations.
+template <class S, int D, int NW>
+__device__ __forceinline__ void ws_sweep(const StepArgs& A, const double* __restrict__ sq, double* __restrict__ up,
+                                         double* __restrict__ dn, double* __restrict__ dq, double r, double& cfl,
+                                         int warp, int lane) {
+  using Sh = WsShape<S>;
+  constexpr int T = Sh::T, PW = Sh::PW, WPW = Sh::WPW, NE = Sh::NE, E = Sh::E, MEQN = S::MEQN;
+  const double hr = -0.5 * r;
+  for (int it = warp; it < Sh::NIT; it += NW) {
+    const int e = it * Sh::STEP - 1 + lane;                 // flat edge index of this lane
+    const bool ev = (unsigned)e < (unsigned)E;
+    const int ee = ev ? e : 0;
+    const int line = ee / NE, pos = ee - line * NE;       // D=1: row j, edge i; D=2: column i, edge j
+    // the edge between window cells (pos-1, line) and (pos, line) along the sweep (1-based cells)
+    const int wr = D == 1 ? (line + 1) * PW + pos : pos * PW + (line + 1);   // window index of the right cell
+    const int wl = D == 1 ? wr - 1 : wr - PW;
+    typename S::Cell L, R;
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) {
+      L.q[k] = sq[k * WPW + wl];
+      R.q[k] = sq[k * WPW + wr];
+    }
+    S::cell(L, A.sp);
+    S::cell(R, A.sp);
+    typename S::Edge Ed;
+    S::template riemann<D>(L, R, A.sp, Ed);
+    // corrections: limiter on the upwind neighbour edge's wave of the same family (warp shuffle)
+    const bool corr = ev && lane >= 1 && lane <= 30 && pos >= 1 && pos <= T + 1;
+    double sw[MEQN], F[MEQN];
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) { sw[k] = 0.0; F[k] = 0.0; }
+#pragma unroll
+    for (int p = 0; p < S::MW; ++p) {
+      double Wp[MEQN], WI[MEQN];
+      S::template wave<D>(Ed, p, Wp);
+      const double s = S::template speed<D>(Ed, p);
+      if (corr) cfl = fmax(cfl, fmax(r * s, -r * s));
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) sw[k] = fma(s, Wp[k], sw[k]);
+      if (A.method2 == 2) {
+        const int src = s > 0.0 ? lane - 1 : lane + 1;    // (s = 0: the right neighbour, reading 1)
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) WI[k] = __shfl_sync(0xffffffffu, Wp[k], src & 31);
+        double wn2 = Wp[0] * Wp[0], dot = WI[0] * Wp[0];
+#pragma unroll
+        for (int k = 1; k < MEQN; ++k) { wn2 = fma(Wp[k], Wp[k], wn2); dot = fma(WI[k], Wp[k], dot); }
+        if (wn2 != 0.0) {                                 // a zero wave adds nothing
+          const double phi = limiter_phi(A.lim, dot * fast_rcp(wn2));
+          const double as = fabs(s);
+          const double c = 0.5 * as * (1.0 - as * r) * phi;
+#pragma unroll
+          for (int k = 0; k < MEQN; ++k) F[k] = fma(c, Wp[k], F[k]);
+        }
+      }
+    }
+    // L part P = A-dq + F~ (enters the left cell), R part Q = A+dq - F~ (the right cell)
+    double P[MEQN], Q[MEQN];
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) {
+      P[k] = Ed.am[k] + F[k];
+      Q[k] = (sw[k] - Ed.am[k]) - F[k];
+    }
+    // the next edge's L part (and, for the transverse split, its transverse input and Roe state)
+    double Pn[MEQN], XLn[MEQN];
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) {
+      Pn[k] = __shfl_down_sync(0xffffffffu, P[k], 1);
+      XLn[k] = A.method3 == 1 ? __shfl_down_sync(0xffffffffu, Ed.am[k], 1) : Pn[k];
+    }
+    const typename S::Roe rn = S::shfl_down(S::roe(Ed), 1);
+    // this lane's output cell: the right cell of its edge, (pos, line)
+    const bool out = ev && lane >= 1 && lane <= 29 && pos >= 1 && pos <= T;
+    if (!out) continue;
+    double XR[MEQN];
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) XR[k] = A.method3 == 1 ? sw[k] - Ed.am[k] : Q[k];
+    double bmQ[MEQN], bpQ[MEQN], bmP[MEQN], bpP[MEQN];
+    if (A.method3 >= 1) {
+      S::template transverse<D>(S::roe(Ed), A.sp, XR, bmQ, bpQ);
+      S::template transverse<D>(rn, A.sp, XLn, bmP, bpP);
+    } else {
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) bmQ[k] = bpQ[k] = bmP[k] = bpP[k] = 0.0;
+    }
+    if (D == 1) {   // cell (i = pos, j = line): G~ halves for rows 0..T+1, the x increment for rows 1..T
+      const int i = pos, j = line;
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) {
+        up[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = hr * bpP[k] + hr * bpQ[k];
+        dn[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = hr * bmP[k] + hr * bmQ[k];
+      }
+      if (j >= 1 && j <= T) {
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
+      }
+    } else {        // cell (i = line, j = pos): F~ halves for columns 0..T+1; interior columns fold
+      const int i = line, j = pos;
+      double* rt = up;   // (D = 2: the up / dn arguments are the rt / lf arrays)
+      double* lf = dn;
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) {
+        rt[(k * T + (j - 1)) * Sh::RTP + i] = hr * bpP[k] + hr * bpQ[k];
+        lf[(k * T + (j - 1)) * Sh::RTP + i] = hr * bmP[k] + hr * bmQ[k];
+      }
+      if (i >= 1 && i <= T) {   // the y increment on top of the x-sweep's (single writer per cell)
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) {
+          double* d = dq + (k * T + (j - 1)) * Sh::DQP + (i - 1);
+          *d = (*d - r * Pn[k]) - r * Q[k];
+        }
+      }
+    }
+  }
+}
+
+template <class S, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntiles) {
+  using Sh = WsShape<S>;
+  constexpr int T = Sh::T, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN, NT = NW * 32;
+  const int tiles2 = A.tiles * A.tiles;
+  if (A.active) ntiles = *A.nactive * tiles2;
+  auto tile_of = [&](int k) {
+    if (!A.active) return k;
+    const int a = k / tiles2;
+    return A.active[a] * tiles2 + (k - a * tiles2);
+  };
+  extern __shared__ __align__(128) double sm[];
+  double* sbuf = sm;                           // 2 x [MEQN][W][PW] windows
+  double* up = sbuf + 2 * Sh::QB;              // x-sweep G~ halves (up / dn)
+  double* dn = up + Sh::N_UP;
+  double* rt = dn + Sh::N_UP;                  // y-sweep F~ halves (right / left)
+  double* lf = rt + Sh::N_RT;
+  double* dq = lf + Sh::N_RT;
+  __shared__ double wmax[NW];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double cfl = 0.0;
+  bool bad = false;
+
+  if ((int)blockIdx.x < ntiles) ws_gather<S>(A, tile_of(blockIdx.x), sbuf, tid, NT);
+  cp_async_commit();
+  int it = 0;
+  for (int kt = blockIdx.x; kt < ntiles; kt += gridDim.x, ++it) {
+    double* sq = sbuf + (it & 1) * Sh::QB;
+    const int tile = tile_of(kt);
+    int patch, tx, ty;
+    ws_tile(A, tile, patch, tx, ty);
+    cp_async_wait<0>();
+    __syncthreads();                            // this tile's window is in; the previous tile is done
+    const int knext = kt + gridDim.x;           // the next tile's gather, into the other buffer
+    if (knext < ntiles) ws_gather<S>(A, tile_of(knext), sbuf + ((it + 1) & 1) * Sh::QB, tid, NT);
+    cp_async_commit();
+    const uint8_t bc = A.bcflag[patch];
+    if (bc & 1) { ws_bc<S>(A, tile, sq, 0, tid, NT); __syncthreads(); }
+    if (bc & 2) { ws_bc<S>(A, tile, sq, 1, tid, NT); __syncthreads(); }
+    const double dx = ldexp(A.dx0, -(int)A.level[patch]);
+    const double r = A.dt / dx;                 // square cells, no capacity: dt/dx = dt/dy
+    double* o = A.qnew + (int64_t)patch * MEQN * (A.m + 4) * (A.m + 4) + (int64_t)(ty * T) * A.m + tx * T;
+    const int64_t n2 = (int64_t)(A.m + 4) * (A.m + 4);
+    if (A.skip_quiescent) {   // one state in the whole window: every jump is 0, q_new = q bitwise
+      const double* q11 = sq + 2 * PW + 2;
+      bool diff = false;
+      for (int t = tid; t < Sh::W * Sh::W; t += NT) {
+        const int wj = t / Sh::W, wi = t - wj * Sh::W;
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k) diff |= sq[k * WPW + wj * PW + wi] != q11[k * WPW];
+      }
+      if (!__syncthreads_or(diff)) {
+        cfl = fmax(cfl, S::quiescent_cfl(q11, WPW, A.sp, r));
+        for (int t = tid; t < T * T; t += NT) {
+          const int j = t / T, i = t - j * T;
+#pragma unroll
+          for (int k = 0; k < MEQN; ++k) o[k * n2 + j * A.m + i] = q11[k * WPW];
+        }
+        continue;
+      }
+    }
+    ws_sweep<S, 1, NW>(A, sq, up, dn, dq, r, cfl, warp, lane);
+    __syncthreads();
+    ws_sweep<S, 2, NW>(A, sq, rt, lf, dq, r, cfl, warp, lane);
+    __syncthreads();
+    // fold the x-sweep's G~ and the y increments into dq: one thread per interior cell.  (Done here
+    // rather than in the y-sweep's output lanes: their column-major cells would read up / dn with
+    // a stride of a whole row.)
+    for (int t = tid; t < T * T; t += NT) {
+      const int jj = t / T, ii = t - jj * T;     // cell (ii + 1, jj + 1)
+      const int i = ii + 1, j = jj + 1;
+      const double* qs = sq + (j + 1) * PW + (i + 1);
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) {
+        const double* u_ = up + k * Sh::NR * Sh::UPP + ii;
+        const double* d_ = dn + k * Sh::NR * Sh::UPP + ii;
+        const double gt = u_[j * Sh::UPP] + d_[(j + 1) * Sh::UPP];
+        const double gb = u_[(j - 1) * Sh::UPP] + d_[j * Sh::UPP];
+        const double* rr = rt + (k * T + jj) * Sh::RTP;
+        const double* ll = lf + (k * T + jj) * Sh::RTP;
+        const double fr = rr[i] + ll[i + 1];
+        const double fl = rr[i - 1] + ll[i];
+        const double dxy = dq[(k * T + jj) * Sh::DQP + ii];
+        const double val = qs[k * WPW] + ((dxy - r * (gt - gb)) - r * (fr - fl));
+        bad |= !isfinite(val);
+        o[k * n2 + jj * A.m + ii] = val;
+      }
+    }
+  }
+  cp_async_wait<0>();
+  // a non-finite updated state makes the step's CFL +inf (fc_step -> FC_ENONFINITE)
+  if (__syncthreads_or(bad)) cfl = __longlong_as_double(0x7ff0000000000000ll);
+  if (cfl != cfl) cfl = __longlong_as_double(0x7ff0000000000000ll);
+  for (int o = 16; o > 0; o >>= 1) cfl = fmax(cfl, __shfl_xor_sync(0xffffffffu, cfl, o));
+  if (lane == 0) wmax[warp] = cfl;
+  __syncthreads();
+  if (tid == 0) {
+    double c = wmax[0];
+    for (int w = 1; w < NW; ++w) c = fmax(c, wmax[w]);
+    atomicMax(A.cfl_bits, (unsigned long long)__double_as_longlong(c));
+  }
+}
+
+template <class S, int NW, int MINB>
+static int launch_ws_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  const size_t smem = WsShape<S>::smem_bytes;
+  static int resident[64] = {};    // per device: CTAs resident at once (persistent grid)
+  static bool attr[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return -1;
+  if (!attr[dev]) {
+    cudaFuncSetAttribute(k_step_ws<S, NW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_step_ws<S, NW, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_ws<S, NW, MINB>, NW * 32, smem);
+    resident[dev] = sms * (per_sm > 0 ? per_sm : 1);
+    attr[dev] = true;
+  }
+  const int64_t ntiles = npatch * a.tiles * a.tiles;
+  if (ntiles >= (1ll << 31)) return -1;
+  const int64_t grid = ntiles < resident[dev] ? ntiles : resident[dev];
+  k_step_ws<S, NW, MINB><<<(unsigned)grid, NW * 32, smem, st>>>(a, (int)ntiles);
+  return 1;
+}
+
+int launch_step_ws(int kind, const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  static const bool off = getenv("FC_WS") && atoi(getenv("FC_WS")) == 0;
+  if (off || !a.ring || a.rslot || a.m % 16 != 0) return 0;
+#ifndef WS_MINB
+#define WS_MINB 2
+#endif
+  if (kind == FC_EULER_ROE) return launch_ws_t<WsEuler, 6, WS_MINB>(a, npatch, st);
+  if (kind == FC_SWE_ROE) return launch_ws_t<WsSwe, 6, WS_MINB>(a, npatch, st);
+  return 0;
+}
+
+}  // namespace fc
