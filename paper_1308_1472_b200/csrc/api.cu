@@ -389,8 +389,8 @@ static bool has_round2(const fc_forest* f) { return f->npack[1] || f->nunpack[1]
 // systems whose update the warp-sweep kernel takes (step_ws.cu): it gathers its windows itself,
 // so their full-update mode runs on the fused path too (FC_WS=0: the phased k_step + ghost kernels)
 static bool ws_applies(const fc_forest* f) {
-  static const bool off = getenv("FC_WS") && atoi(getenv("FC_WS")) == 0;
-  return !off && (f->prob.kind == FC_SWE_ROE || f->prob.kind == FC_EULER_ROE) && f->pl.m % 16 == 0 &&
+  const char* env = getenv("FC_WS");
+  return !(env && atoi(env) == 0) && (f->prob.kind == FC_SWE_ROE || f->prob.kind == FC_EULER_ROE) && f->pl.m % 16 == 0 &&
          !f->prob.reflux;
 }
 

@@ -37,6 +37,9 @@ namespace fc {
 // register-resident views of the solvers (the same formulas as solvers.cuh / SURVEY §8(c.5))
 struct WsEuler {
   static constexpr int MEQN = 4, MW = 4;
+  // components of wave p along sweep D that can be nonzero (the shear wave moves only the
+  // tangential momentum and the energy): the others are skipped at compile time
+  __host__ __device__ static constexpr bool wave_nz(int D, int p, int k) { return p != 2 || k == 3 - D || k == 3; }
   struct Cell {
     double q[4];
     double sr, u, v, H, c2;   // sqrt(rho), velocity, enthalpy, sound speed squared
@@ -147,6 +150,9 @@ struct WsEuler {
     const double un = D == 1 ? E.u : E.v;
     return p == 0 ? un - E.c : (p == 3 ? un + E.c : un);
   }
+  // max_p |s_p| = |un| + c (bitwise the larger of |un - c|, |un + c|)
+  template <int D>
+  __device__ static double max_speed(const Edge& E) { return fabs(D == 1 ? E.u : E.v) + E.c; }
   template <int D>
   __device__ static void wave(const Edge& E, int p, double* W) {
     constexpr int nd = D, td = 3 - D;
@@ -167,9 +173,32 @@ struct WsEuler {
             __shfl_down_sync(0xffffffffu, r.H, d), __shfl_down_sync(0xffffffffu, r.c, d),
             __shfl_down_sync(0xffffffffu, r.ic, d)};
   }
+  // B-X, B+X of the Roe matrix along the transverse direction of sweep D (EulerRoe::roe_transverse's
+  // formulas; the eigenvalue split as (lambda -+ |lambda|)/2, exact, on the fp64 pipe)
   template <int D>
   __device__ static void transverse(const Roe& r, const SolverParams& P, const double* X, double* bm, double* bp) {
-    EulerRoe::roe_transverse<D>(r.u, r.v, r.H, r.c, r.ic, P.p0 - 1.0, X, bm, bp);
+    constexpr int nd = 3 - D, td = D;
+    const double gm1 = P.p0 - 1.0, c = r.c, ic = r.ic, H = r.H;
+    const double vn = nd == 1 ? r.u : r.v, vt = nd == 1 ? r.v : r.u;
+    const double b3 = X[td] - vt * X[0];
+    const double b2 = gm1 * (ic * ic) * ((H - vn * vn - vt * vt) * X[0] + vn * X[nd] + vt * X[td] - X[3]);
+    const double b4 = (X[nd] + (c - vn) * X[0] - c * b2) * (0.5 * ic);
+    const double b1 = X[0] - b2 - b4;
+    const double ek = 0.5 * (vn * vn + vt * vt);
+    const double l1 = vn - c, l4 = vn + c;
+    const double l1m = 0.5 * (l1 - fabs(l1)), l1p = 0.5 * (l1 + fabs(l1));
+    const double l2m = 0.5 * (vn - fabs(vn)), l2p = 0.5 * (vn + fabs(vn));
+    const double l4m = 0.5 * (l4 - fabs(l4)), l4p = 0.5 * (l4 + fabs(l4));
+    const double m1 = l1m * b1, m2 = l2m * b2, m3 = l2m * b3, m4 = l4m * b4;
+    const double p1 = l1p * b1, p2 = l2p * b2, p3 = l2p * b3, p4 = l4p * b4;
+    bm[0] = m1 + m2 + m4;
+    bm[nd] = m1 * (vn - c) + m2 * vn + m4 * (vn + c);
+    bm[td] = (m1 + m2 + m4) * vt + m3;
+    bm[3] = m1 * (H - vn * c) + m2 * ek + m3 * vt + m4 * (H + vn * c);
+    bp[0] = p1 + p2 + p4;
+    bp[nd] = p1 * (vn - c) + p2 * vn + p4 * (vn + c);
+    bp[td] = (p1 + p2 + p4) * vt + p3;
+    bp[3] = p1 * (H - vn * c) + p2 * ek + p3 * vt + p4 * (H + vn * c);
   }
   __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, double dtdx) {
     return EulerRoe::quiescent_cfl(q, qs, P, nullptr, dtdx, 0, 0, 0, 0);
@@ -178,6 +207,7 @@ struct WsEuler {
 
 struct WsSwe {
   static constexpr int MEQN = 3, MW = 3;
+  __host__ __device__ static constexpr bool wave_nz(int D, int p, int k) { return p != 1 || k == 3 - D; }
   struct Cell {
     double q[3];
     double sr, u, v;
@@ -229,6 +259,8 @@ struct WsSwe {
     return p == 0 ? un - E.c : (p == 1 ? un : un + E.c);
   }
   template <int D>
+  __device__ static double max_speed(const Edge& E) { return fabs(D == 1 ? E.u : E.v) + E.c; }
+  template <int D>
   __device__ static void wave(const Edge& E, int p, double* W) {
     constexpr int nd = D, td = 3 - D;
     const double un = nd == 1 ? E.u : E.v, ut = nd == 1 ? E.v : E.u;
@@ -254,10 +286,10 @@ struct WsSwe {
     const double b1 = ((vn + c) * X[0] - X[nd]) * i2c;
     const double b2 = X[td] - vt * X[0];
     const double b3 = ((c - vn) * X[0] + X[nd]) * i2c;
-    double l1m, l1p, l2m, l2p, l3m, l3p;
-    split0(vn - c, l1m, l1p);
-    split0(vn, l2m, l2p);
-    split0(vn + c, l3m, l3p);
+    const double l1 = vn - c, l3 = vn + c;
+    const double l1m = 0.5 * (l1 - fabs(l1)), l1p = 0.5 * (l1 + fabs(l1));
+    const double l2m = 0.5 * (vn - fabs(vn)), l2p = 0.5 * (vn + fabs(vn));
+    const double l3m = 0.5 * (l3 - fabs(l3)), l3p = 0.5 * (l3 + fabs(l3));
     const double m1 = l1m * b1, m2 = l2m * b2, m3 = l3m * b3;
     const double p1 = l1p * b1, p2 = l2p * b2, p3 = l3p * b3;
     bm[0] = m1 + m3;
@@ -303,32 +335,64 @@ __device__ __forceinline__ void ws_tile(const StepArgs& A, int tile, int& patch,
   }
 }
 
-// cp.async gather of tile `tile`'s 20 x 20 window (natural layout, pitch 21): cells inside the patch
+// cp.async gather of a tile's 20 x 20 window (natural layout, pitch 21): cells inside the patch
 // interior from its own storage block, the others from the ring-source table (a neighbour's
-// interior, a peer rank's buffer, or a computed ghost); physical-boundary cells after the wait
+// interior, a peer rank's buffer, or a computed ghost); physical-boundary cells after the wait.
+// Two stages so that the ring-table loads never stall the issuing thread: ws_prep loads this
+// thread's (<= 3) table entries a whole tile ahead, ws_issue turns them into cp.async copies.
+constexpr int WS_GU = 3;   // window cells per thread (ceil(400 / 192))
+struct WsGather {
+  int tile;
+  int32_t v[WS_GU];        // ring source offset, or -1 - BC code, or INT32_MIN: own interior
+  uint8_t ow[WS_GU];       // owner code of a ring source (0 local, k peer rank k-1, 255 computed)
+};
 template <class S>
-__device__ __forceinline__ void ws_gather(const StepArgs& A, int tile, double* sq, int tid, int nt) {
+__device__ __forceinline__ void ws_prep(const StepArgs& A, int tile, WsGather& g, int tid, int nt) {
   using Sh = WsShape<S>;
-  constexpr int T = Sh::T, W = Sh::W, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN;
+  constexpr int T = Sh::T, W = Sh::W;
+  g.tile = tile;
+  if (tile < 0) return;
   int patch, tx, ty;
   ws_tile(A, tile, patch, tx, ty);
-  const int m = A.m, n = m + 4, n2 = n * n, G = n2 - m * m;
-  const double* qb = A.qold + (int64_t)patch * MEQN * n2;
+  const int m = A.m, n = m + 4, G = n * n - m * m;
   const int32_t* rs = A.ring + (int64_t)patch * G;
   const uint8_t* rp = A.rpeer ? A.rpeer + (int64_t)patch * G : nullptr;
-  for (int c = tid; c < W * W; c += nt) {
+#pragma unroll
+  for (int u = 0; u < WS_GU; ++u) {
+    const int c = tid + u * nt;
+    g.v[u] = INT32_MIN;
+    g.ow[u] = 0;
+    if (c >= W * W) continue;
     const int wj = c / W, wi = c - wj * W;
     const int i = tx * T + wi - 1, j = ty * T + wj - 1;   // patch cell (1-based interior)
-    double* d = sq + wj * PW + wi;
+    if ((unsigned)(i - 1) < (unsigned)m && (unsigned)(j - 1) < (unsigned)m) continue;
+    const int r = ring_index(i, j, m);
+    g.v[u] = __ldg(rs + r);
+    if (rp) g.ow[u] = __ldg(rp + r);
+  }
+}
+template <class S>
+__device__ __forceinline__ void ws_issue(const StepArgs& A, const WsGather& g, double* sq, int tid, int nt) {
+  using Sh = WsShape<S>;
+  constexpr int T = Sh::T, W = Sh::W, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN;
+  if (g.tile < 0) return;
+  int patch, tx, ty;
+  ws_tile(A, g.tile, patch, tx, ty);
+  const int m = A.m, n = m + 4, n2 = n * n;
+  const double* qb = A.qold + (int64_t)patch * MEQN * n2;
+#pragma unroll
+  for (int u = 0; u < WS_GU; ++u) {
+    const int c = tid + u * nt;
+    if (c >= W * W) continue;
+    const int wj = c / W, wi = c - wj * W;
     const double* src;
-    if ((unsigned)(i - 1) < (unsigned)m && (unsigned)(j - 1) < (unsigned)m) {
-      src = qb + (j - 1) * m + (i - 1);
+    if (g.v[u] == INT32_MIN) {
+      src = qb + (ty * T + wj - 2) * m + (tx * T + wi - 2);
     } else {
-      const int r = ring_index(i, j, m);
-      const int32_t v = __ldg(rs + r);
-      if (v < 0) continue;                                 // physical boundary: ws_bc
-      src = ring_base(A, rp ? __ldg(rp + r) : 0) + v;
+      if (g.v[u] < 0) continue;                          // physical boundary: ws_bc
+      src = ring_base(A, g.ow[u]) + g.v[u];
     }
+    double* d = sq + wj * PW + wi;
 #pragma unroll
     for (int k = 0; k < MEQN; ++k) cp_async8(d + k * WPW, src + (int64_t)k * n2);
   }
@@ -364,21 +428,85 @@ __device__ __forceinline__ void ws_bc(const StepArgs& A, int tile, double* sq, i
   }
 }
 
+// the output cell of a sweep lane (the right cell of its edge): both transverse splits, the
+// G~ / F~ halves and the normal increment (called with the whole warp converged after the shuffles)
+template <class S, int D>
+__device__ __forceinline__ void ws_output(const StepArgs& A, int m3, const typename S::Edge& Ed, const double* P,
+                                          const double* Q, const double* sw, const double* Pn,
+                                          const double* XLn, const typename S::Roe& rn, double* __restrict__ up,
+                                          double* __restrict__ dn, double* __restrict__ dq, double r, double hr,
+                                          int pos, int line) {
+  using Sh = WsShape<S>;
+  constexpr int T = Sh::T, MEQN = S::MEQN;
+  double XR[MEQN];
+#pragma unroll
+  for (int k = 0; k < MEQN; ++k) XR[k] = m3 == 1 ? sw[k] - Ed.am[k] : Q[k];
+  double bmQ[MEQN], bpQ[MEQN], bmP[MEQN], bpP[MEQN];
+  if (m3 >= 1) {
+    S::template transverse<D>(S::roe(Ed), A.sp, XR, bmQ, bpQ);
+    S::template transverse<D>(rn, A.sp, XLn, bmP, bpP);
+  } else {
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) bmQ[k] = bpQ[k] = bmP[k] = bpP[k] = 0.0;
+  }
+  if (D == 1) {   // cell (i = pos, j = line): G~ halves for rows 0..T+1, the x increment for rows 1..T
+    const int i = pos, j = line;
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) {
+      up[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = hr * bpP[k] + hr * bpQ[k];
+      dn[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = hr * bmP[k] + hr * bmQ[k];
+    }
+    if (j >= 1 && j <= T) {
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
+    }
+  } else {        // cell (i = line, j = pos): F~ halves for columns 0..T+1; interior columns fold
+    const int i = line, j = pos;
+    double* rt = up;   // (D = 2: the up / dn arguments are the rt / lf arrays)
+    double* lf = dn;
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) {
+      rt[(k * T + (j - 1)) * Sh::RTP + i] = hr * bpP[k] + hr * bpQ[k];
+      lf[(k * T + (j - 1)) * Sh::RTP + i] = hr * bmP[k] + hr * bmQ[k];
+    }
+    if (i >= 1 && i <= T) {   // the y increment on top of the x-sweep's (single writer per cell)
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) {
+        double* d = dq + (k * T + (j - 1)) * Sh::DQP + (i - 1);
+        *d = (*d - r * Pn[k]) - r * Q[k];
+      }
+    }
+  }
+}
+
+// wave limiter phi(theta) = max(lo, min(c1 + c2 theta, c3, c4 theta)) with compare-selects (the
+// operands are never NaN here: theta of a zero wave is replaced by 0 first)
+__device__ __forceinline__ double ws_phi(const LimiterCoef& L, double th) {
+  double t = fma(L.c2, th, L.c1);
+  t = t < L.c3 ? t : L.c3;
+  const double t4 = L.c4 * th;
+  t = t < t4 ? t : t4;
+  return t > L.lo ? t : L.lo;
+}
+
 // One sweep (D = 1: x-edges of rows 0..T+1; D = 2: y-edges of columns 0..T+1) as NIT warp-iterations.
-template <class S, int D, int NW>
+// FAST: method2 = 2 and method3 = 2 (the configs) known at compile time; otherwise read from A.
+template <class S, int D, int NW, bool FAST>
 __device__ __forceinline__ void ws_sweep(const StepArgs& A, const double* __restrict__ sq, double* __restrict__ up,
-                                         double* __restrict__ dn, double* __restrict__ dq, double r, double& cfl,
+                                         double* __restrict__ dn, double* __restrict__ dq, double r, double& smax,
                                          int warp, int lane) {
   using Sh = WsShape<S>;
   constexpr int T = Sh::T, PW = Sh::PW, WPW = Sh::WPW, NE = Sh::NE, E = Sh::E, MEQN = S::MEQN;
   const double hr = -0.5 * r;
+  const bool m2 = FAST || A.method2 == 2;
+  const int m3 = FAST ? 2 : A.method3;
   for (int it = warp; it < Sh::NIT; it += NW) {
     const int e = it * Sh::STEP - 1 + lane;                 // flat edge index of this lane
     const bool ev = (unsigned)e < (unsigned)E;
     const int ee = ev ? e : 0;
     const int line = ee / NE, pos = ee - line * NE;       // D=1: row j, edge i; D=2: column i, edge j
     // the edge between window cells (pos-1, line) and (pos, line) along the sweep (1-based cells)
-    const int wr = D == 1 ? (line + 1) * PW + pos : pos * PW + (line + 1);   // window index of the right cell
+    const int wr = D == 1 ? (line + 1) * PW + (pos + 1) : (pos + 1) * PW + (line + 1);   // the right cell
     const int wl = D == 1 ? wr - 1 : wr - PW;
     typename S::Cell L, R;
 #pragma unroll
@@ -390,8 +518,11 @@ __device__ __forceinline__ void ws_sweep(const StepArgs& A, const double* __rest
     S::cell(R, A.sp);
     typename S::Edge Ed;
     S::template riemann<D>(L, R, A.sp, Ed);
-    // corrections: limiter on the upwind neighbour edge's wave of the same family (warp shuffle)
+    // CFL of the corrected edges: max over waves of r |s| = r (|un| + c) (the max taken per tile)
     const bool corr = ev && lane >= 1 && lane <= 30 && pos >= 1 && pos <= T + 1;
+    const double ms = S::template max_speed<D>(Ed);
+    smax = corr && ms > smax ? ms : smax;
+    // corrections: limiter on the upwind neighbour edge's wave of the same family (warp shuffle)
     double sw[MEQN], F[MEQN];
 #pragma unroll
     for (int k = 0; k < MEQN; ++k) { sw[k] = 0.0; F[k] = 0.0; }
@@ -400,23 +531,26 @@ __device__ __forceinline__ void ws_sweep(const StepArgs& A, const double* __rest
       double Wp[MEQN], WI[MEQN];
       S::template wave<D>(Ed, p, Wp);
       const double s = S::template speed<D>(Ed, p);
-      if (corr) cfl = fmax(cfl, fmax(r * s, -r * s));
 #pragma unroll
-      for (int k = 0; k < MEQN; ++k) sw[k] = fma(s, Wp[k], sw[k]);
-      if (A.method2 == 2) {
+      for (int k = 0; k < MEQN; ++k)
+        if (S::wave_nz(D, p, k)) sw[k] = fma(s, Wp[k], sw[k]);
+      if (m2) {
         const int src = s > 0.0 ? lane - 1 : lane + 1;    // (s = 0: the right neighbour, reading 1)
+        double wn2 = 0.0, dot = 0.0;
 #pragma unroll
-        for (int k = 0; k < MEQN; ++k) WI[k] = __shfl_sync(0xffffffffu, Wp[k], src & 31);
-        double wn2 = Wp[0] * Wp[0], dot = WI[0] * Wp[0];
-#pragma unroll
-        for (int k = 1; k < MEQN; ++k) { wn2 = fma(Wp[k], Wp[k], wn2); dot = fma(WI[k], Wp[k], dot); }
-        if (wn2 != 0.0) {                                 // a zero wave adds nothing
-          const double phi = limiter_phi(A.lim, dot * fast_rcp(wn2));
-          const double as = fabs(s);
-          const double c = 0.5 * as * (1.0 - as * r) * phi;
-#pragma unroll
-          for (int k = 0; k < MEQN; ++k) F[k] = fma(c, Wp[k], F[k]);
+        for (int k = 0; k < MEQN; ++k) {
+          if (!S::wave_nz(D, p, k)) continue;
+          WI[k] = __shfl_sync(0xffffffffu, Wp[k], src & 31);
+          wn2 = fma(Wp[k], Wp[k], wn2);
+          dot = fma(WI[k], Wp[k], dot);
         }
+        // a zero wave adds nothing: theta = 0 there keeps the limiter's selects NaN-free
+        const double th = wn2 != 0.0 ? dot * fast_rcp(wn2) : 0.0;
+        const double as = fabs(s);
+        const double c = 0.5 * as * (1.0 - as * r) * ws_phi(A.lim, th);
+#pragma unroll
+        for (int k = 0; k < MEQN; ++k)
+          if (S::wave_nz(D, p, k)) F[k] = fma(c, Wp[k], F[k]);
       }
     }
     // L part P = A-dq + F~ (enters the left cell), R part Q = A+dq - F~ (the right cell)
@@ -429,63 +563,30 @@ __device__ __forceinline__ void ws_sweep(const StepArgs& A, const double* __rest
     // the next edge's L part (and, for the transverse split, its transverse input and Roe state)
     double Pn[MEQN], XLn[MEQN];
 #pragma unroll
-    for (int k = 0; k < MEQN; ++k) {
-      Pn[k] = __shfl_down_sync(0xffffffffu, P[k], 1);
-      XLn[k] = A.method3 == 1 ? __shfl_down_sync(0xffffffffu, Ed.am[k], 1) : Pn[k];
+    for (int k = 0; k < MEQN; ++k) Pn[k] = __shfl_down_sync(0xffffffffu, P[k], 1);
+    if (m3 == 1) {
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) XLn[k] = __shfl_down_sync(0xffffffffu, Ed.am[k], 1);
+    } else {
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) XLn[k] = Pn[k];
     }
     const typename S::Roe rn = S::shfl_down(S::roe(Ed), 1);
     // this lane's output cell: the right cell of its edge, (pos, line)
     const bool out = ev && lane >= 1 && lane <= 29 && pos >= 1 && pos <= T;
-    if (!out) continue;
-    double XR[MEQN];
-#pragma unroll
-    for (int k = 0; k < MEQN; ++k) XR[k] = A.method3 == 1 ? sw[k] - Ed.am[k] : Q[k];
-    double bmQ[MEQN], bpQ[MEQN], bmP[MEQN], bpP[MEQN];
-    if (A.method3 >= 1) {
-      S::template transverse<D>(S::roe(Ed), A.sp, XR, bmQ, bpQ);
-      S::template transverse<D>(rn, A.sp, XLn, bmP, bpP);
-    } else {
-#pragma unroll
-      for (int k = 0; k < MEQN; ++k) bmQ[k] = bpQ[k] = bmP[k] = bpP[k] = 0.0;
-    }
-    if (D == 1) {   // cell (i = pos, j = line): G~ halves for rows 0..T+1, the x increment for rows 1..T
-      const int i = pos, j = line;
-#pragma unroll
-      for (int k = 0; k < MEQN; ++k) {
-        up[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = hr * bpP[k] + hr * bpQ[k];
-        dn[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = hr * bmP[k] + hr * bmQ[k];
-      }
-      if (j >= 1 && j <= T) {
-#pragma unroll
-        for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
-      }
-    } else {        // cell (i = line, j = pos): F~ halves for columns 0..T+1; interior columns fold
-      const int i = line, j = pos;
-      double* rt = up;   // (D = 2: the up / dn arguments are the rt / lf arrays)
-      double* lf = dn;
-#pragma unroll
-      for (int k = 0; k < MEQN; ++k) {
-        rt[(k * T + (j - 1)) * Sh::RTP + i] = hr * bpP[k] + hr * bpQ[k];
-        lf[(k * T + (j - 1)) * Sh::RTP + i] = hr * bmP[k] + hr * bmQ[k];
-      }
-      if (i >= 1 && i <= T) {   // the y increment on top of the x-sweep's (single writer per cell)
-#pragma unroll
-        for (int k = 0; k < MEQN; ++k) {
-          double* d = dq + (k * T + (j - 1)) * Sh::DQP + (i - 1);
-          *d = (*d - r * Pn[k]) - r * Q[k];
-        }
-      }
-    }
+    if (out) ws_output<S, D>(A, m3, Ed, P, Q, sw, Pn, XLn, rn, up, dn, dq, r, hr, pos, line);
   }
 }
 
-template <class S, int NW, int MINB>
+template <class S, int NW, int MINB, bool FAST>
 __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntiles) {
   using Sh = WsShape<S>;
   constexpr int T = Sh::T, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN, NT = NW * 32;
+  static_assert(NT * WS_GU >= Sh::W * Sh::W, "window cells per thread");
   const int tiles2 = A.tiles * A.tiles;
   if (A.active) ntiles = *A.nactive * tiles2;
   auto tile_of = [&](int k) {
+    if (k >= ntiles) return -1;
     if (!A.active) return k;
     const int a = k / tiles2;
     return A.active[a] * tiles2 + (k - a * tiles2);
@@ -502,8 +603,22 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
   double cfl = 0.0;
   bool bad = false;
 
-  if ((int)blockIdx.x < ntiles) ws_gather<S>(A, tile_of(blockIdx.x), sbuf, tid, NT);
+  // pipeline: the window of tile k+1 is gathered while tile k computes, with the ring-table
+  // entries of tile k+2 and the patch metadata of tile k+1 loaded at the same time
+  WsGather g;
+  ws_prep<S>(A, tile_of(blockIdx.x), g, tid, NT);
+  ws_issue<S>(A, g, sbuf, tid, NT);
   cp_async_commit();
+  ws_prep<S>(A, tile_of(blockIdx.x + gridDim.x), g, tid, NT);
+  int meta = -1;                               // bcflag | level << 8 of the current tile
+  {
+    const int t0 = tile_of(blockIdx.x);
+    if (t0 >= 0) {
+      int p0, x0, y0;
+      ws_tile(A, t0, p0, x0, y0);
+      meta = A.bcflag[p0] | ((int)A.level[p0] << 8);
+    }
+  }
   int it = 0;
   for (int kt = blockIdx.x; kt < ntiles; kt += gridDim.x, ++it) {
     double* sq = sbuf + (it & 1) * Sh::QB;
@@ -512,13 +627,21 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
     ws_tile(A, tile, patch, tx, ty);
     cp_async_wait<0>();
     __syncthreads();                            // this tile's window is in; the previous tile is done
-    const int knext = kt + gridDim.x;           // the next tile's gather, into the other buffer
-    if (knext < ntiles) ws_gather<S>(A, tile_of(knext), sbuf + ((it + 1) & 1) * Sh::QB, tid, NT);
+    ws_issue<S>(A, g, sbuf + ((it + 1) & 1) * Sh::QB, tid, NT);   // tile k+1 (entries loaded last tile)
     cp_async_commit();
-    const uint8_t bc = A.bcflag[patch];
-    if (bc & 1) { ws_bc<S>(A, tile, sq, 0, tid, NT); __syncthreads(); }
-    if (bc & 2) { ws_bc<S>(A, tile, sq, 1, tid, NT); __syncthreads(); }
-    const double dx = ldexp(A.dx0, -(int)A.level[patch]);
+    ws_prep<S>(A, tile_of(kt + 2 * gridDim.x), g, tid, NT);        // tile k+2's entries
+    const int cur = meta;
+    {
+      const int tn = tile_of(kt + gridDim.x);
+      if (tn >= 0) {
+        int pn, xn, yn;
+        ws_tile(A, tn, pn, xn, yn);
+        meta = A.bcflag[pn] | ((int)A.level[pn] << 8);
+      }
+    }
+    if (cur & 1) { ws_bc<S>(A, tile, sq, 0, tid, NT); __syncthreads(); }
+    if (cur & 2) { ws_bc<S>(A, tile, sq, 1, tid, NT); __syncthreads(); }
+    const double dx = ldexp(A.dx0, -(cur >> 8));
     const double r = A.dt / dx;                 // square cells, no capacity: dt/dx = dt/dy
     double* o = A.qnew + (int64_t)patch * MEQN * (A.m + 4) * (A.m + 4) + (int64_t)(ty * T) * A.m + tx * T;
     const int64_t n2 = (int64_t)(A.m + 4) * (A.m + 4);
@@ -540,13 +663,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
         continue;
       }
     }
-    ws_sweep<S, 1, NW>(A, sq, up, dn, dq, r, cfl, warp, lane);
+    double smax = 0.0;
+    ws_sweep<S, 1, NW, FAST>(A, sq, up, dn, dq, r, smax, warp, lane);
     __syncthreads();
-    ws_sweep<S, 2, NW>(A, sq, rt, lf, dq, r, cfl, warp, lane);
+    ws_sweep<S, 2, NW, FAST>(A, sq, rt, lf, dq, r, smax, warp, lane);
+    cfl = fmax(cfl, r * smax);
     __syncthreads();
-    // fold the x-sweep's G~ and the y increments into dq: one thread per interior cell.  (Done here
-    // rather than in the y-sweep's output lanes: their column-major cells would read up / dn with
-    // a stride of a whole row.)
+    // fold: q_new = q + (x and y increments) - r (G~ and F~ differences), one thread per cell
     for (int t = tid; t < T * T; t += NT) {
       const int jj = t / T, ii = t - jj * T;     // cell (ii + 1, jj + 1)
       const int i = ii + 1, j = jj + 1;
@@ -582,38 +705,42 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
   }
 }
 
-template <class S, int NW, int MINB>
+template <class S, int NW, int MINB, bool FAST>
 static int launch_ws_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   const size_t smem = WsShape<S>::smem_bytes;
   static int resident[64] = {};    // per device: CTAs resident at once (persistent grid)
-  static bool attr[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return -1;
-  if (!attr[dev]) {
-    cudaFuncSetAttribute(k_step_ws<S, NW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_step_ws<S, NW, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (!resident[dev]) {            // (function attributes are per device)
+    cudaFuncSetAttribute(k_step_ws<S, NW, MINB, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_step_ws<S, NW, MINB, FAST>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_ws<S, NW, MINB>, NW * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_ws<S, NW, MINB, FAST>, NW * 32, smem);
     resident[dev] = sms * (per_sm > 0 ? per_sm : 1);
-    attr[dev] = true;
   }
   const int64_t ntiles = npatch * a.tiles * a.tiles;
   if (ntiles >= (1ll << 31)) return -1;
   const int64_t grid = ntiles < resident[dev] ? ntiles : resident[dev];
-  k_step_ws<S, NW, MINB><<<(unsigned)grid, NW * 32, smem, st>>>(a, (int)ntiles);
+  k_step_ws<S, NW, MINB, FAST><<<(unsigned)grid, NW * 32, smem, st>>>(a, (int)ntiles);
   return 1;
 }
 
-int launch_step_ws(int kind, const StepArgs& a, int64_t npatch, cudaStream_t st) {
-  static const bool off = getenv("FC_WS") && atoi(getenv("FC_WS")) == 0;
-  if (off || !a.ring || a.rslot || a.m % 16 != 0) return 0;
 #ifndef WS_MINB
 #define WS_MINB 2
 #endif
-  if (kind == FC_EULER_ROE) return launch_ws_t<WsEuler, 6, WS_MINB>(a, npatch, st);
-  if (kind == FC_SWE_ROE) return launch_ws_t<WsSwe, 6, WS_MINB>(a, npatch, st);
+template <class S>
+static int launch_ws_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  if (a.method2 == 2 && a.method3 == 2) return launch_ws_t<S, 6, WS_MINB, true>(a, npatch, st);
+  return launch_ws_t<S, 6, WS_MINB, false>(a, npatch, st);
+}
+
+int launch_step_ws(int kind, const StepArgs& a, int64_t npatch, cudaStream_t st) {
+  const char* env = getenv("FC_WS");   // (read per launch: tests switch kernels within a process)
+  if ((env && atoi(env) == 0) || !a.ring || a.rslot || a.m % 16 != 0) return 0;
+  if (kind == FC_EULER_ROE) return launch_ws_s<WsEuler>(a, npatch, st);
+  if (kind == FC_SWE_ROE) return launch_ws_s<WsSwe>(a, npatch, st);
   return 0;
 }
 

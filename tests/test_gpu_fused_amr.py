@@ -86,7 +86,9 @@ def test_fused_amr_gather_in_subcycled_steps(w, monkeypatch):
 def test_fused_gather_on_multi_tile_patches(w, monkeypatch):
     """Uniform forests with m = tiles x T (m = 32: 2 x 2 tiles of 16; m = 20: 5 x 5 of 4), walls:
     each tile's window takes its interior part by row copies and its ring part from the sources
-    (gather_ring_tiles, wall ghosts in shared memory) -- bitwise the ghost-kernel run."""
+    (gather_ring_tiles, wall ghosts in shared memory) -- bitwise the ghost-kernel run of the same
+    (phased) kernel.  (FC_WS=0: the warp-sweep kernel's own gather is checked below.)"""
+    monkeypatch.setenv("FC_WS", "0")
     qa, ca, pa = run(w, monkeypatch, True)
     qb, cb, pb = run(w, monkeypatch, False)
     assert pa == 1 and pb == 0
@@ -106,3 +108,20 @@ def test_fused_gather_capacity_form_on_the_cubed_sphere(uniform, monkeypatch):
     assert pa == 2 and pb == 0
     np.testing.assert_array_equal(qa, qb)
     np.testing.assert_array_equal(ca, cb)
+
+
+@pytest.mark.parametrize("w", [c3(level=2, m=32, steps=10), c3(level=3, m=16, steps=10)], ids=lambda w: w.name)
+def test_warp_sweep_gather_matches_ghost_kernel_run(w, monkeypatch):
+    """The warp-sweep systems kernel (step_ws.cu) gathers its windows itself (cp.async from the
+    neighbours' interiors, wall ghosts in shared memory; m = 32: 2 x 2 tiles).  Against the phased
+    kernel on ghost-kernel rings: the same method in another operation order, so agreement to
+    rounding (1e-13 relative), and both within the oracle's tolerance (tests/test_gpu_parity.py)."""
+    monkeypatch.delenv("FC_WS", raising=False)
+    qa, ca, pa = run(w, monkeypatch, True)
+    monkeypatch.setenv("FC_WS", "0")
+    qb, cb, pb = run(w, monkeypatch, False)
+    assert pa == 1 and pb == 0
+    for k in range(w.meqn):
+        scale = np.abs(qb[:, k]).max()
+        assert np.abs(qa[:, k] - qb[:, k]).max() <= 1e-13 * scale, k
+    np.testing.assert_allclose(ca, cb, rtol=1e-13, atol=0)
