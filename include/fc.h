@@ -63,6 +63,7 @@ extern "C" {
 #define FC_BC_WALL 1
 
 #define FC_TABLE_EXPANDED 1   /* per ghost cell records, see fc_get_ghost_table */
+#define FC_TABLE_COMPACT 2    /* per patch direction: kind, neighbours, orientation, see fc_get_ghost_table */
 
 /* ---- descriptors --------------------------------------------------------------------------- */
 typedef struct fc_forest fc_forest;
@@ -133,7 +134,12 @@ typedef struct {
 
 /* ---- calls --------------------------------------------------------------------------------- */
 
-/* Copy and validate the forest, decode Morton order, build the neighbour / ghost tables and the
+/* PAPER.md:105-113 [§2] (a forest of quadtrees, one m x m patch per leaf), PAPER.md:132-144 [§2]
+ * (multiblock: each tree a reference square with its own orientation; the connectivity; ghost
+ * cells from the neighbour relations), PAPER.md:150-155 [§2] (2:1 balance)
+ * [Fig. 1, §4] (leaves ordered along a space-filling curve and partitioned among processes, one
+ * layer of ghost leaves).
+ * Copy and validate the forest, decode Morton order, build the neighbour / ghost tables and the
  * shard + halo plan, allocate device state (q_old, q_new double buffer, aux) and, when
  * nranks > 1, create the NCCL communicator.  Validation: tree ids non-decreasing and every tree
  * tiled exactly (FC_ETILING); connectivity symmetric (FC_ECONN); m even >= 4, mbc == 2
@@ -143,15 +149,19 @@ int fc_forest_create(const fc_forest_desc* desc, fc_forest** out);
 /* Free everything the handle owns (device memory, streams, events, communicator). */
 int fc_forest_destroy(fc_forest* f);
 
-/* Select the solver.  FC_EINVAL if kind/meqn/maux disagree or parameters are out of range. */
+/* Select the solver (PAPER.md:168-182 [§3]: Clawpack's wave propagation with a problem-specific
+ * Riemann solver, wave limiters, second-order and transverse corrections; kinds and readings in
+ * DESIGN.md §3).  FC_EINVAL if kind/meqn/maux disagree or parameters are out of range. */
 int fc_set_problem(fc_forest* f, const fc_problem* pr);
 
 /* aux[P_local][maux][n][n] including the ghost ring (FC_ADV_EDGEVEL_CAPA only): kappa, u~ at
  * each cell's left edge, v~ at its bottom edge.  Copied into device memory. */
 int fc_set_aux(fc_forest* f, const double* aux, int where);
 
-/* q[P_local][meqn][m][m] -> interior of q_old.  The ghost ring becomes stale until the next
- * fill.  FC_ESTATE before fc_set_problem. */
+/* PAPER.md:113-125 [§2] (each leaf houses one patch of m^d cells: the numerical data).
+ * q[P_local][meqn][m][m] (x fastest; patches in global Morton order; host or device by
+ * `where`; caller keeps ownership) -> interior of q_old.  The ghost ring becomes stale until the
+ * next fill.  FC_ESTATE before fc_set_problem. */
 int fc_set_q(fc_forest* f, const double* q, int where);
 
 /* Fill the ghost rings of q_old (halo exchange included) -- inspection / tests; fc_step does its
@@ -224,13 +234,30 @@ int fc_regrid_finish(fc_forest* g);
  * = size query); *num_patches = P.  FC_EINVAL if cap < P. */
 int fc_get_leaves(fc_forest* f, int8_t* levels, int32_t* tree_ids, int64_t cap, int64_t* num_patches);
 
-/* Interior q_old -> q[P_local][meqn][m][m].  Synchronous. */
+/* PAPER.md:113-125 [§2] (the per-leaf patch data).  Interior q_old -> q[P_local][meqn][m][m]
+ * (layout as fc_set_q; host or device by `where`; caller-owned buffer).  Synchronous on the
+ * handle's stream.  FC_ESTATE on a host-only handle. */
 int fc_get_q(fc_forest* f, double* q, int where);
 
 /* Padded q_old (ring as left by the last fill) -> q[P_local][meqn][n][n].  Synchronous. */
 int fc_get_q_padded(fc_forest* f, double* q, int where);
 
-/* Canonical ghost table of the LOCAL patches (global patch ids, independent of sharding):
+/* Canonical ghost table of the LOCAL patches (global patch ids, independent of sharding).
+ * PAPER.md:141-144 [§2] (constant-time neighbour lookup, with the relative orientation across
+ * tree boundaries), PAPER.md:193-201 [§3] (the copy / average / interpolate ghost operations).
+ * which = FC_TABLE_COMPACT: for each local patch, 8 directions d (faces -x, +x, -y, +y, then
+ * corners (-x,-y), (+x,-y), (-x,+y), (+x,+y)), 5 int32 {kind, nbr0, nbr1, xform, half}:
+ *   kind  0 SAME level, 1 COARSER (one level), 2 FINER (one level), 3 PHYS (physical boundary),
+ *         4 CORNER3 (three-tree cube corner);
+ *   nbr0, nbr1  global ids: SAME / COARSER the neighbour leaf (nbr1 = -1); FINER face the two
+ *         finer leaves along the face, lower tangential coordinate of this patch's frame first;
+ *         FINER corner the one finer leaf at the corner (nbr1 = -1); PHYS / CORNER3 -1, -1;
+ *   xform orientation of this patch's frame in the neighbour's tree, 4 swap + 2 flip_x + flip_y:
+ *         e_x -> (-1)^flip_x e_x', e_y -> (-1)^flip_y e_y' (swap = 0) or e_x -> (-1)^flip_x e_y',
+ *         e_y -> (-1)^flip_y e_x' (swap = 1); -1 for PHYS / CORNER3;
+ *   half  COARSER faces: which half (0 lower, 1 upper, along this patch's tangential coordinate)
+ *         of the coarse leaf's face this patch touches; -1 otherwise.
+ *   *len = P_local * 40.
  * which = FC_TABLE_EXPANDED: for each local patch, for each ring cell in storage order
  * (j = -1..m+2 outer, i = -1..m+2 inner, interior skipped; G = n^2 - m^2 cells), 8 int32
  * {op, src_patch, src_i, src_j, a, b, c, d} with op 1 COPY (src cell), 2 AVG4 (lower-left cell of

@@ -1028,6 +1028,16 @@ int fc_halo_requests(fc_forest* f, int peer, int round, int64_t* buf, int64_t ca
 
 int fc_get_ghost_table(fc_forest* f, int which, int32_t* buf, int64_t cap, int64_t* len) {
   if (!f || !len) return fail(FC_EINVAL, "null argument");
+  if (which == FC_TABLE_COMPACT) {
+    *len = f->Pl * 40;
+    if (!buf || cap < *len) return fail(FC_EINVAL, "buffer too small");
+    std::string err;
+    for (int64_t lp = 0; lp < f->Pl; ++lp) {
+      const int rc = plan_compact_patch(f->pl, f->pl.p0 + lp, buf + 40 * lp, err);
+      if (rc) return fail(rc, err);
+    }
+    return FC_OK;
+  }
   if (which != FC_TABLE_EXPANDED) return fail(FC_EINVAL, "unknown table kind");
   *len = (int64_t)f->pl.table.size();
   if (!buf || cap < *len) return fail(FC_EINVAL, "buffer too small");

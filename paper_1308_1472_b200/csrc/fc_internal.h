@@ -135,6 +135,8 @@ int plan_build(const fc_forest_desc* d, Plan& pl, std::string& err);
 int plan_lists(const Plan& pl, int meqn, GhostLists& gl, std::string& err,
                const std::vector<uint8_t>* dst_mask = nullptr);
 int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& err, bool p2p = false);
+// COMPACT ghost-table rows of patch p (global id): 8 directions x {kind, nbr0, nbr1, xform, half}
+int plan_compact_patch(const Plan& pl, int64_t p, int32_t* out40, std::string& err);
 // fused two-hop ring gather on AMR forests: computed-ghost (AVG4 / INTERP) lists and slot count
 struct RingAmr {
   std::vector<int32_t> avg;                  // {dst slot offset, 4 q_old offsets}

@@ -227,6 +227,55 @@ static int patch_records(const Plan& pl, int64_t p, int32_t* rec, std::string& e
   return FC_OK;
 }
 
+// COMPACT ghost table of patch p (include/fc.h, FC_TABLE_COMPACT): per direction d (faces -x, +x,
+// -y, +y, then corners (-x,-y), (+x,-y), (-x,+y), (+x,+y)) {kind, nbr0, nbr1, xform, half}, from
+// the same per-direction lookup the ghost records use (PAPER.md:141-144 [§2]: constant-time
+// neighbour lookup with the relative orientation of the trees)
+int plan_compact_patch(const Plan& pl, int64_t p, int32_t* o, std::string& err) {
+  static const int DIR[8][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}, {-1, -1}, {1, -1}, {-1, 1}, {1, 1}};
+  const Leaf& L = pl.leaves[p];
+  const int64_t m2 = 2 * (int64_t)pl.m;
+  const int64_t sz = 1ll << (pl.lmax - L.level);
+  const int64_t S = m2 * sz;
+  const int64_t X0 = L.x * m2, Y0 = L.y * m2;
+  for (int d = 0; d < 8; ++d) {
+    const int di = DIR[d][0], dj = DIR[d][1];
+    DirInfo D;
+    int rc = dir_info(pl, p, di, dj, D, err);
+    if (rc) return rc;
+    int32_t* e = o + 5 * d;
+    e[0] = (int32_t)D.kind;
+    e[1] = e[2] = e[3] = e[4] = -1;
+    if (D.kind == D_PHYS || D.kind == D_CORNER3) continue;
+    // orientation of the linear part p-frame -> neighbour frame: 4 swap + 2 [e_x reversed] + [e_y reversed]
+    const Affine& T = D.T;
+    if (T.r00 != 0) e[3] = 2 * (T.r00 < 0) + (T.r11 < 0);
+    else e[3] = 4 + 2 * (T.r10 < 0) + (T.r01 < 0);
+    if (D.kind == D_SAME || D.kind == D_COARSER) {
+      e[1] = (int32_t)D.leaf;
+      if (D.kind == D_COARSER && d < 4)   // which half of the coarse face, along p's tangential axis
+        e[4] = (int32_t)(((d < 2 ? L.y : L.x) / sz) & 1);
+      continue;
+    }
+    // FINER: the finer leaves touching p's face (two, lower tangential coordinate first) or corner
+    const int64_t csz = sz / 2, cw = m2 * csz;
+    const int64_t px = di < 0 ? X0 - 1 : (di > 0 ? X0 + S + 1 : 0);
+    const int64_t py = dj < 0 ? Y0 - 1 : (dj > 0 ? Y0 + S + 1 : 0);
+    const int nq = d < 4 ? 2 : 1;
+    for (int q = 0; q < nq; ++q) {
+      int64_t X = px, Y = py;
+      if (d < 2) Y = Y0 + (2 * q + 1) * S / 4;
+      else if (d < 4) X = X0 + (2 * q + 1) * S / 4;
+      int64_t cx, cy;
+      apply(T, X, Y, cx, cy);
+      const int64_t id = find_leaf(pl, T.tree, L.level + 1, (cx / cw) * csz, (cy / cw) * csz);
+      if (id < 0) { err = "2:1 balance violated (finer-by-two neighbour)"; return FC_EBALANCE; }
+      e[1 + q] = (int32_t)id;
+    }
+  }
+  return FC_OK;
+}
+
 static int64_t owner_of(const Plan& pl, int64_t q) {   // the rank whose [part[r], part[r+1]) holds q
   return (int64_t)(std::upper_bound(pl.part.begin(), pl.part.end(), q) - pl.part.begin()) - 1;
 }

@@ -22,6 +22,7 @@ FC_HOST, FC_DEVICE = 0, 1
 FC_ADV_CONST, FC_ADV_EDGEVEL_CAPA, FC_SWE_ROE, FC_EULER_ROE, FC_EULER_HLLE = 0, 1, 2, 3, 4
 FC_LIM_NONE, FC_LIM_MINMOD, FC_LIM_MC = 0, 1, 2
 FC_TABLE_EXPANDED = 1
+FC_TABLE_COMPACT = 2
 
 ERRNAMES = {0: "FC_OK", -1: "FC_EINVAL", -2: "FC_ETILING", -3: "FC_ECONN", -4: "FC_EBALANCE",
             -5: "FC_ECUDA", -6: "FC_ENCCL", -7: "FC_ENOMEM", -8: "FC_ESTATE", -9: "FC_ECFL",
@@ -277,12 +278,15 @@ class Forest:
         _check(lib().fc_get_q_padded(self.h, p, where), "fc_get_q_padded")
         return out
 
-    def ghost_table(self) -> np.ndarray:
+    def ghost_table(self, which: int = FC_TABLE_EXPANDED) -> np.ndarray:
+        """EXPANDED: [P_local][G][8] per ring cell; COMPACT: [P_local][8 directions][5]."""
         n = C.c_int64()
-        lib().fc_get_ghost_table(self.h, FC_TABLE_EXPANDED, None, 0, C.byref(n))
+        lib().fc_get_ghost_table(self.h, which, None, 0, C.byref(n))
         buf = np.empty(n.value, np.int32)
-        _check(lib().fc_get_ghost_table(self.h, FC_TABLE_EXPANDED, buf.ctypes.data_as(C.c_void_p),
+        _check(lib().fc_get_ghost_table(self.h, which, buf.ctypes.data_as(C.c_void_p),
                                         n.value, C.byref(n)), "fc_get_ghost_table")
+        if which == FC_TABLE_COMPACT:
+            return buf.reshape(self.count, 8, 5)
         G = self.n * self.n - self.m * self.m
         return buf.reshape(self.count, G, 8)
 

@@ -204,3 +204,51 @@ def test_custom_partition_ranges_and_validation():
             fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, 1, device=-1, rank=0, nranks=4,
                       partition=bad)
         assert e.value.code == fc.FC_EINVAL
+
+
+# ---- COMPACT table (FC_TABLE_COMPACT): the planner's per-direction lookup vs the oracle's read-back
+# from its brute-force per-cell records (oracle/compact.py) -----------------------------------------
+def compact_pair(levels, tree_ids, conn, m):
+    from oracle.compact import compact_table
+    f = fc.Forest(levels, tree_ids, conn, m, 1, device=-1)
+    return f.ghost_table(fc.FC_TABLE_COMPACT), compact_table(oracle.OracleForest(levels, tree_ids, conn, m))
+
+
+@pytest.mark.parametrize("w", [c1(), c2(), c3(level=2, m=8), c5(level=2, m=8), c4_workload(base_level=2, m=8),
+                               c4_workload(base_level=2, m=8, uniform=True)], ids=lambda w: w.name)
+def test_compact_table_bit_exact_configs(w):
+    t, o = compact_pair(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m)
+    np.testing.assert_array_equal(t, o)
+    kinds = set(np.unique(t[:, :, 0]).tolist())
+    if w.name.startswith("C2") or "C4_L2_m8" == w.name:
+        assert {1, 2} <= kinds                       # coarser and finer neighbours occur
+    if w.name.startswith("C4"):
+        assert 4 in kinds and len(set(t[:, :, 3].ravel().tolist()) - {-1}) > 1   # corners, rotations
+
+
+@pytest.mark.parametrize("name", sorted(CONNS))
+def test_compact_table_bit_exact_random_two_level_forests(rng, name):
+    conn = CONNS[name]
+    for trial in range(3):
+        m = [4, 8, 6][trial]
+        fr = _random_forest(rng, conn, 2, m)
+        t, o = compact_pair(fr.levels, fr.tree_ids, conn, m)
+        np.testing.assert_array_equal(t, o)
+
+
+def test_compact_table_worked_example():
+    """Hand-checked rows: C2's mesh (reading 11) -- a level-3 patch left of the refined plus shape
+    sees two finer leaves on its +x face; a level-4 patch on the rim sees a coarser leaf, half given
+    by its own position; everything is axis-aligned (xform 0) on the single periodic tree."""
+    w = c2()
+    t, _ = compact_pair(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m)
+    assert (t[:, :, 3][t[:, :, 0] <= 2] == 0).all()
+    lv = w.forest.levels
+    fine_face = np.nonzero((t[:, :4, 0] == 2).any(axis=1))[0]
+    assert len(fine_face) and (lv[fine_face] == 3).all()
+    p = int(fine_face[0])
+    d = int(np.nonzero(t[p, :4, 0] == 2)[0][0])
+    a, b = t[p, d, 1], t[p, d, 2]
+    assert lv[a] == lv[b] == 4 and a != b
+    coarse = np.nonzero((t[:, :4, 0] == 1).any(axis=1))[0]
+    assert (lv[coarse] == 4).all() and set(t[coarse][:, :4, 4][t[coarse][:, :4, 0] == 1].tolist()) == {0, 1}
