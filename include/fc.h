@@ -299,8 +299,14 @@ int fc_halo_requests(fc_forest* f, int peer, int round, int64_t* buf, int64_t ca
  *           fc_halo_unpack; fc_step_local(phase 1) (ghost phases A, C); round 2 likewise (ring cells
  *           read by interpolation); fc_step_local(phase 2) (ghost phase B, update, this rank's CFL);
  *           fc_commit with the max of the ranks' CFLs.
+ *   (split)  uniform forests on the fused path without quiescent filter / reflux (e.g. the full
+ *           update): fc_halo_pack, fc_step_local(phase 4) (update of the interior patches -- those
+ *           whose ring reads no remote cell -- and the CFL reset), the transport, fc_halo_unpack,
+ *           fc_step_local(phase 5) (the boundary patches, this rank's CFL); FC_EUNSUP elsewhere.
  * fc_step on an NCCL handle is exactly this sequence with ncclSend/Recv as the transport and
- * ncclAllReduce(max) for the CFL (PAPER.md:264-272 [§4]: exchange, then local neighbour work).
+ * ncclAllReduce(max) for the CFL (PAPER.md:264-272 [§4]: exchange, then local neighbour work);
+ * where the split applies it overlaps the exchange (pack, NCCL, unpack on a high-priority
+ * stream) with the interior update, the boundary patches waiting on the exchange's event.
  * Used to test the sharded data path with several rank handles in one process. */
 int fc_halo_set_requests(fc_forest* f, int round, int peer, const int64_t* keys, int64_t n);
 int fc_halo_finalize(fc_forest* f);

@@ -103,6 +103,14 @@ struct fc_forest {
   unsigned long long* d_cfl = nullptr;
   double* h_cfl = nullptr;
   DevList copy, avg, bcx, bcy, corner3;
+  // halo overlap (NCCL halo on the fused path, several ranks): interior patches (no remote ring
+  // source) are updated while the exchange runs on a high-priority comm stream; the boundary
+  // patches after its event (SURVEY §8(e) "Overlap")
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_halo = nullptr;
+  int32_t *d_ilist = nullptr, *d_blist = nullptr, *d_icnt = nullptr, *d_bcnt = nullptr;
+  int64_t n_int = 0, n_bnd = 0;
+  bool split = false;
   // fused ring gather (uniform same-level forests, one tile per patch): ring never written
   bool fused = false;
   int32_t* d_ring = nullptr;
@@ -344,26 +352,26 @@ static int setup_p2p_ipc(fc_forest* f) {
 }
 
 // ---- halo transfer pieces (round: 0 = interior cells, 1 = ring cells read by interpolation) ----
-static int halo_pack(fc_forest* f, int round) {
+static int halo_pack(fc_forest* f, int round, cudaStream_t st) {
   f->st.kernel_launches += launch_pack(f->qold, f->d_pack[round], f->npack[round], f->pl.meqn,
-                                       f->pl.n * f->pl.n, f->d_sendbuf, f->stream);
+                                       f->pl.n * f->pl.n, f->d_sendbuf, st);
   CK(cudaGetLastError());
   return FC_OK;
 }
-static int halo_unpack(fc_forest* f, int round) {
+static int halo_unpack(fc_forest* f, int round, cudaStream_t st) {
   f->st.kernel_launches += launch_unpack(f->qold, f->d_unpack[round], f->nunpack[round], f->pl.meqn,
-                                         f->pl.n * f->pl.n, f->d_recvbuf, f->stream);
+                                         f->pl.n * f->pl.n, f->d_recvbuf, st);
   CK(cudaGetLastError());
   return FC_OK;
 }
-static int halo_nccl(fc_forest* f, int round) {
+static int halo_nccl(fc_forest* f, int round, cudaStream_t st) {
   const int R = f->pl.nranks, me = f->pl.rank, meqn = f->pl.meqn;
   NK(ncclGroupStart());
   int64_t so = 0, ro = 0;
   for (int s = 0; s < R; ++s) {
     const int64_t sc = f->send_cnt[round][s], rc = f->recv_cnt[round][s];
-    if (s != me && sc) NK(ncclSend(f->d_sendbuf + so * meqn, sc * meqn, ncclDouble, s, f->comm, f->stream));
-    if (s != me && rc) NK(ncclRecv(f->d_recvbuf + ro * meqn, rc * meqn, ncclDouble, s, f->comm, f->stream));
+    if (s != me && sc) NK(ncclSend(f->d_sendbuf + so * meqn, sc * meqn, ncclDouble, s, f->comm, st));
+    if (s != me && rc) NK(ncclRecv(f->d_recvbuf + ro * meqn, rc * meqn, ncclDouble, s, f->comm, st));
     so += sc;
     ro += rc;
   }
@@ -372,11 +380,12 @@ static int halo_nccl(fc_forest* f, int round) {
 }
 
 // one NCCL halo round (pack -> grouped send/recv -> unpack); no-op on one rank
-static int halo_round(fc_forest* f, int round) {
+static int halo_round(fc_forest* f, int round, cudaStream_t st = nullptr) {
   if (f->pl.nranks <= 1) return FC_OK;
   if (f->manual) return fail(FC_ESTATE, "manual halo transport: use the staged step calls");
+  if (!st) st = f->stream;
   int rc;
-  if ((rc = halo_pack(f, round)) || (rc = halo_nccl(f, round)) || (rc = halo_unpack(f, round))) return rc;
+  if ((rc = halo_pack(f, round, st)) || (rc = halo_nccl(f, round, st)) || (rc = halo_unpack(f, round, st))) return rc;
   return FC_OK;
 }
 
@@ -473,10 +482,34 @@ static int reflux_exchange(fc_forest* f) {
 
 // the update after the ghost data are in place: quiescent filter (fused path) + step kernel,
 // leaving this rank's CFL max in d_cfl
-static int update_local(fc_forest* f, double dt) {
-  CK(cudaMemsetAsync(f->d_cfl, 0, sizeof(unsigned long long), f->stream));
+// the split update applies on the fused NCCL-halo path when no quiescent filter and no reflux
+// records are involved (the filter's active list and the records span both patch classes)
+static bool overlap_ok(const fc_forest* f) {
+  if (!f->split || !use_fused(f) || f->prob.reflux || has_round2(f)) return false;
+  const bool want_filter = f->prob.skip_quiescent && f->prob.kind != FC_ADV_EDGEVEL_CAPA && f->Pl >= 512;
+  return !want_filter;
+}
+
+// part: 0 every local patch; 1 the interior patches only (no remote ring source: may run before
+// the halo arrives; resets the CFL); 2 the boundary patches (after the halo; keeps the CFL)
+static int update_local(fc_forest* f, double dt, int part = 0) {
+  if (part != 2) CK(cudaMemsetAsync(f->d_cfl, 0, sizeof(unsigned long long), f->stream));
   const fc_problem& p = f->prob;
   const bool fused = use_fused(f);
+  if (part != 0) {   // split update (halo overlap): fused path, no filter, no reflux records
+    const int32_t* lst = part == 1 ? f->d_ilist : f->d_blist;
+    const int32_t* cnt = part == 1 ? f->d_icnt : f->d_bcnt;
+    if ((part == 1 ? f->n_int : f->n_bnd) == 0) return FC_OK;
+    std::array<const double*, 16> pq{};
+    int lr = launch_step(p.kind, f->qold, f->qnew, f->aux, f->d_level, f->Pl, f->pl.m, dt, f->pl.dx0, p.p0, p.p1,
+                         p.limiter, p.method2, p.method3, p.skip_quiescent, f->d_ring, f->d_bcflag, lst, cnt,
+                         f->d_cfl, nullptr, nullptr, nullptr, pq.data(), f->d_cg, f->stream);
+    if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
+    f->st.kernel_launches += lr;
+    f->st.step_kernel_launches += lr;
+    CK(cudaGetLastError());
+    return FC_OK;
+  }
   const bool reflux = p.reflux && f->nrcells > 0;          // this rank applies corrections
   const bool records = p.reflux && (f->nrcells > 0 || f->rf_npack > 0);   // and / or serves records
   if (p.reflux && !f->rf_ready) return fail(FC_ESTATE, "reflux requests not finalized (fc_reflux_finalize)");
@@ -604,6 +637,10 @@ static void destroy(fc_forest* f) {
     cudaFree(f->d_sendbuf); cudaFree(f->d_recvbuf);
     for (auto& e : f->t_all) cudaEventDestroy(e);
     if (f->comm) ncclCommDestroy(f->comm);
+    cudaFree(f->d_ilist); cudaFree(f->d_blist); cudaFree(f->d_icnt); cudaFree(f->d_bcnt);
+    if (f->ev_fork) cudaEventDestroy(f->ev_fork);
+    if (f->ev_halo) cudaEventDestroy(f->ev_halo);
+    if (f->comm_stream) cudaStreamDestroy(f->comm_stream);
     if (f->own_stream) cudaStreamDestroy(f->own_stream);
   }
   delete f;
@@ -829,6 +866,33 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
       cudaMemcpy(f->d_negmask, rs.negmask.data(), rs.negmask.size(), cudaMemcpyHostToDevice);
       f->fused = true;
       f->st.uniform_fast_path = 1;
+      if (pl.nranks > 1 && !f->p2p) {   // halo overlap: interior / boundary patch lists
+        std::vector<int32_t> il, bl;
+        for (int64_t lp = 0; lp < f->Pl; ++lp) {
+          bool remote = false;
+          for (int k = 0; k < 8; ++k) remote |= rs.nbr[lp * 8 + k] == -2;
+          (remote ? bl : il).push_back((int32_t)lp);
+        }
+        f->n_int = (int64_t)il.size();
+        f->n_bnd = (int64_t)bl.size();
+        const int32_t ni = (int32_t)il.size(), nb = (int32_t)bl.size();
+        if ((e = cudaMalloc(&f->d_ilist, std::max<size_t>(1, il.size()) * sizeof(int32_t))) != cudaSuccess ||
+            (e = cudaMalloc(&f->d_blist, std::max<size_t>(1, bl.size()) * sizeof(int32_t))) != cudaSuccess ||
+            (e = cudaMalloc(&f->d_icnt, sizeof(int32_t))) != cudaSuccess ||
+            (e = cudaMalloc(&f->d_bcnt, sizeof(int32_t))) != cudaSuccess)
+          return cuda_fail(e, "cudaMalloc overlap lists");
+        if (ni) cudaMemcpy(f->d_ilist, il.data(), il.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+        if (nb) cudaMemcpy(f->d_blist, bl.data(), bl.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(f->d_icnt, &ni, sizeof(int32_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(f->d_bcnt, &nb, sizeof(int32_t), cudaMemcpyHostToDevice);
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if ((e = cudaStreamCreateWithPriority(&f->comm_stream, cudaStreamNonBlocking, hi)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&f->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&f->ev_halo, cudaEventDisableTiming)) != cudaSuccess)
+          return cuda_fail(e, "overlap stream / events");
+        f->split = true;
+      }
     } else if (allow && !pl.uniform_same && T == pl.m && pl.nranks == 1) {
       // AMR forest: fused two-hop gather (plan_ring_amr); unsupported forests keep the ghost kernels
       RingSources rs;
@@ -1139,10 +1203,24 @@ int fc_step(fc_forest* f, double dt, double* max_cfl) {
   // fused ring gather + quiescent filter when skipping is on (rings never written); otherwise the
   // ghost kernels fill the rings and every tile is bulk-copied whole (faster for the full update)
   // (peer-memory halo: the fused gather reads other ranks' cells itself; no exchange pass)
-  rc = use_fused(f) ? (f->p2p ? FC_OK : halo_round(f, 0)) : ghost_fill_internal(f);
-  if (rc) return rc;
-  if (f->timing) CK(cudaEventRecord(f->ev[1], f->stream));
-  if ((rc = update_local(f, dt))) return rc;
+  if (overlap_ok(f)) {
+    // halo exchange on the high-priority comm stream (pack -> NCCL send / recv -> unpack into the
+    // halo slots) while the interior patches update; the boundary patches after its event.  The
+    // halo slots are only read by boundary patches, and q_old is not written during the step.
+    CK(cudaEventRecord(f->ev_fork, f->stream));
+    CK(cudaStreamWaitEvent(f->comm_stream, f->ev_fork, 0));
+    if ((rc = halo_round(f, 0, f->comm_stream))) return rc;
+    CK(cudaEventRecord(f->ev_halo, f->comm_stream));
+    if (f->timing) CK(cudaEventRecord(f->ev[1], f->stream));
+    if ((rc = update_local(f, dt, 1))) return rc;
+    CK(cudaStreamWaitEvent(f->stream, f->ev_halo, 0));
+    if ((rc = update_local(f, dt, 2))) return rc;
+  } else {
+    rc = use_fused(f) ? (f->p2p ? FC_OK : halo_round(f, 0)) : ghost_fill_internal(f);
+    if (rc) return rc;
+    if (f->timing) CK(cudaEventRecord(f->ev[1], f->stream));
+    if ((rc = update_local(f, dt))) return rc;
+  }
   if (f->timing) CK(cudaEventRecord(f->ev[2], f->stream));
   if (f->pl.nranks > 1)
     NK(ncclAllReduce(f->d_cfl, f->d_cfl, 1, ncclDouble, ncclMax, f->comm, f->stream));
@@ -1850,7 +1928,7 @@ int fc_halo_pack(fc_forest* f, int round) {
   if (!f || (round != 1 && round != 2)) return fail(FC_EINVAL, "bad argument");
   if (f->host_only || !f->has_q) return fail(FC_ESTATE, "no state");
   CK(cudaSetDevice(f->device));
-  int rc = halo_pack(f, round - 1);
+  int rc = halo_pack(f, round - 1, f->stream);
   if (rc) return rc;
   CK(cudaStreamSynchronize(f->stream));
   return FC_OK;
@@ -1860,7 +1938,7 @@ int fc_halo_unpack(fc_forest* f, int round) {
   if (!f || (round != 1 && round != 2)) return fail(FC_EINVAL, "bad argument");
   if (f->host_only || !f->has_q) return fail(FC_ESTATE, "no state");
   CK(cudaSetDevice(f->device));
-  int rc = halo_unpack(f, round - 1);
+  int rc = halo_unpack(f, round - 1, f->stream);
   if (rc) return rc;
   CK(cudaStreamSynchronize(f->stream));
   return FC_OK;
@@ -1874,6 +1952,16 @@ int fc_step_local(fc_forest* f, double dt, int phase, double* local_cfl) {
     if (!use_fused(f) && (rc = ghost_phase_ac(f))) return rc;
   } else if (phase == 3) {   // after the caller moved the reflux records: apply the reflux
     if (f->prob.reflux && (rc = apply_reflux(f, dt))) return rc;
+  } else if (phase == 4 || phase == 5) {   // split update (the halo overlap's two halves)
+    if (!overlap_ok(f)) return fail(FC_EUNSUP, "split update: fused NCCL-halo path without filter / reflux only");
+    if ((rc = update_local(f, dt, phase == 4 ? 1 : 2))) return rc;
+    if (phase == 5) {
+      CK(cudaMemcpyAsync(f->h_cfl, f->d_cfl, sizeof(double), cudaMemcpyDeviceToHost, f->stream));
+      if (local_cfl) {
+        CK(cudaStreamSynchronize(f->stream));
+        *local_cfl = *f->h_cfl;
+      }
+    }
   } else if (phase == 2) {
     if (!use_fused(f) && (rc = ghost_phase_b(f))) return rc;
     if ((rc = update_local(f, dt))) return rc;
@@ -1883,7 +1971,7 @@ int fc_step_local(fc_forest* f, double dt, int phase, double* local_cfl) {
       *local_cfl = *f->h_cfl;
     }
   } else {
-    return fail(FC_EINVAL, "phase must be 1, 2 or 3");
+    return fail(FC_EINVAL, "phase must be 1 .. 5");
   }
   CK(cudaStreamSynchronize(f->stream));
   note_activity(f);

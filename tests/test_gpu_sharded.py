@@ -221,3 +221,58 @@ def test_sharded_custom_partition_bitwise(w):
     qr, cr = run_sharded(w, 4, do, 1, partition=part)
     np.testing.assert_array_equal(qr, q1)
     np.testing.assert_array_equal(cr, c1_)
+
+
+def run_sharded_split(w, R, dts, skip):
+    """The halo overlap's order (fc_step on NCCL handles): pack, interior update (phase 4) while
+    the halo slots still hold the previous step's values, then the transport, unpack and the
+    boundary update (phase 5).  An interior patch reading a halo slot would see stale data."""
+    hs = []
+    for r in range(R):
+        f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0, 0, r, R, None)
+        f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject, skip, 0)
+        hs.append(f)
+    for rnd in (1, 2):
+        for r in range(R):
+            for s in range(R):
+                if s != r:
+                    hs[s].halo_set_requests(rnd, r, hs[r].halo_requests(s, rnd))
+    for f in hs:
+        f.halo_finalize()
+        f.set_q(np.ascontiguousarray(w.q0[f.first:f.first + f.count]))
+    cfls = []
+    for dt in dts:
+        for f in hs:
+            f.halo_pack(1)
+        for f in hs:
+            f.step_local(dt, 4)
+        bufs = [f.halo_buffers(1) for f in hs]
+        for r in range(R):
+            _, recv, _, roff = bufs[r]
+            for s in range(R):
+                if s != r:
+                    send, _, soff, _ = bufs[s]
+                    d2d(recv + 8 * roff[s], send + 8 * soff[r], 8 * (roff[s + 1] - roff[s]))
+        for f in hs:
+            f.halo_unpack(1)
+        c = max(f.step_local(dt, 5) for f in hs)
+        for f in hs:
+            assert f.commit(c) == fc.FC_OK
+        cfls.append(c)
+    q = np.concatenate([f.get_q() for f in hs if f.count], axis=0)
+    for f in hs:
+        f.close()
+    return q, np.array(cfls)
+
+
+@pytest.mark.parametrize("R", [2, 3, 4])
+@pytest.mark.parametrize("w", [c5(level=2, m=16, steps=20), c3(level=2, m=32, steps=20), c1(steps=20)],
+                         ids=lambda w: w.name)
+def test_split_update_halo_overlap_bitwise(w, R):
+    """SURVEY §8(e) overlap: interior patches updated before the halo arrives, boundary patches
+    after -- bitwise the one-rank run (full update: no filter)."""
+    qo, co, do = oracle.run(w)
+    q1, c1_, _ = fc.run(w, dt_list=do, skip_quiescent=0)
+    qr, cr = run_sharded_split(w, R, do, 0)
+    np.testing.assert_array_equal(qr, q1)
+    np.testing.assert_array_equal(cr, c1_)
