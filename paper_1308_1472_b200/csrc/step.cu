@@ -985,9 +985,6 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
 #ifndef CV_UNROLL
 #define CV_UNROLL 0
 #endif
-#ifndef CV_ILIM
-#define CV_ILIM 0
-#endif
 template <int T>
 struct CvShape {
   static constexpr int W = T + 4, WW = W * W, LP = T / 2 + 1, PW = 32 / LP;
@@ -1006,7 +1003,8 @@ __device__ CV_STAGE_INLINE void cv_stage(const StepArgs& A, double* buf, uint64_
   constexpr int W = C::W, WW = C::WW, PW = C::PW, G = WW - T * T;
   const bool ring = A.ring != nullptr;
   auto patch_of = [&](int idx) { return A.active ? A.active[idx] : idx; };
-  if (lane == 0) mbar_expect_tx(bar, (uint32_t)cnt * (ring ? T * T : T * T + 4 * W) * (uint32_t)sizeof(double));
+  // (the ring path stages by cp.async only: the barrier just completes its phase)
+  if (lane == 0) mbar_expect_tx(bar, ring ? 0u : (uint32_t)cnt * (T * T + 4 * W) * (uint32_t)sizeof(double));
   __syncwarp();
   if (!ring) {
     const int mp = lane < cnt ? patch_of(i0 + lane) : 0;
@@ -1031,6 +1029,7 @@ __device__ CV_STAGE_INLINE void cv_stage(const StepArgs& A, double* buf, uint64_
   int pt[PW];
   int32_t src[PW][NR];
   uint8_t own[PW][NR];
+  const bool peers = A.rpeer != nullptr;   // (uniform: only peer-memory / AMR forests carry owners)
 #pragma unroll
   for (int q = 0; q < PW; ++q) pt[q] = q < cnt ? patch_of(i0 + q) : -1;
 #pragma unroll
@@ -1040,17 +1039,26 @@ __device__ CV_STAGE_INLINE void cv_stage(const StepArgs& A, double* buf, uint64_
       const int r = lane + 32 * t;
       const bool ok = pt[q] >= 0 && r < G;
       src[q][t] = ok ? __ldg(A.ring + (int64_t)pt[q] * G + r) : -1;
-      own[q][t] = (ok && A.rpeer) ? __ldg(A.rpeer + (int64_t)pt[q] * G + r) : 0;
+      own[q][t] = (ok && peers) ? __ldg(A.rpeer + (int64_t)pt[q] * G + r) : 0;
     }
+  // the interior as 16-byte cp.async chunks (two cells) into the natural window: every lane issues
+  // its own (a per-row bulk copy from per-lane addresses is serialised over the lanes)
+  constexpr int CH = T * T / 2;
 #pragma unroll
   for (int q = 0; q < PW; ++q) {
     if (pt[q] < 0) continue;
     double* b = buf + q * WW;
-    if (lane < T) bulk_g2s(b + (lane + 2) * W + 2, A.qold + (int64_t)pt[q] * WW + lane * T, T * sizeof(double), bar);
+    const double* qi = A.qold + (int64_t)pt[q] * WW;
+#pragma unroll
+    for (int c = lane; c < CH; c += 32) {
+      const int row = c / (T / 2), cp = c - row * (T / 2);
+      cp_async16(b + (row + 2) * W + 2 + 2 * cp, qi + row * T + 2 * cp);
+    }
 #pragma unroll
     for (int t = 0; t < NR; ++t) {
       const int r = lane + 32 * t;
-      if (src[q][t] >= 0) cp_async8(b + ring_window_index<T>(r), ring_base(A, own[q][t]) + src[q][t]);
+      if (src[q][t] >= 0)
+        cp_async8(b + ring_window_index<T>(r), (peers ? ring_base(A, own[q][t]) : A.qold) + src[q][t]);
     }
   }
   cp_async_commit();
@@ -1081,7 +1089,10 @@ __device__ __forceinline__ void cv_bcs(const StepArgs& A, double* gbuf, int mypa
 }
 
 template <int T, int SX, int SY, bool MT2, int NB, bool RF>
-__global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
+#ifndef CV_MINB
+#define CV_MINB 20
+#endif
+__global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch) {
   using C = CvShape<T>;
   constexpr int W = C::W, WW = C::WW, LP = C::LP, PW = C::PW, G = WW - T * T;
   extern __shared__ __align__(128) double sm[];     // [NB][PW][WW]
@@ -1110,31 +1121,17 @@ __global__ void __launch_bounds__(32) k_step_cv(StepArgs A, int npatch) {
   const double lc1 = A.lim.c1, lc2 = A.lim.c2, lc3 = A.lim.c3, lc4 = A.lim.c4;
   // phi(wi / w) w of the MC / minmod limiter (launched for those only), division- and branch-free:
   // with s the sign of w, s max(0, min(s (c1 w + c2 wi), c3 |w|, s c4 wi)) (s x: a sign-bit flip)
-#if CV_ILIM
-  // the min / max on the bit patterns as signed 64-bit integers: the order of non-negative doubles,
-  // and every negative double (sign bit set) is a negative integer, clamped to +0
+  // phi(wi / w) w of the MC / minmod limiter (launched for those only), division- and select-free:
+  // sign(w) min(c1 |w| + c2 |wi|, c3 |w|, c4 |wi|) when w and wi share a sign, else 0, with
+  // min(x, y) = (x + y - |x - y|) / 2 on the fp64 pipe (the sweeps are issue-bound; the rounding
+  // differs from the oracle's phi(theta) w by ulps, within the step tolerance, reading 24)
   auto limited = [&](double w, double wi) {
-    const long long sw = __double_as_longlong(w) & (long long)0x8000000000000000ull;
-    const long long a = __double_as_longlong(fma(lc1, w, lc2 * wi)) ^ sw;
-    const long long c = __double_as_longlong(lc4 * wi) ^ sw;
-    const long long b = __double_as_longlong(lc3 * fabs(w));
-    long long mm = a < b ? a : b;
-    mm = mm < c ? mm : c;
-    mm = mm > 0 ? mm : 0;
-    return __longlong_as_double(mm ^ sw);
+    const double a = fabs(w), b = fabs(wi);
+    const double x = fma(lc1, a, lc2 * b), y = lc3 * a, z = lc4 * b;
+    const double yz = 0.5 * ((y + z) - fabs(y - z));
+    const double mag = 0.5 * ((x + yz) - fabs(x - yz));
+    return w * wi > 0.0 ? copysign(mag, w) : 0.0;
   };
-#else
-  auto limited = [&](double w, double wi) {
-    const long long sw = __double_as_longlong(w) & (long long)0x8000000000000000ull;
-    const double a = __longlong_as_double(__double_as_longlong(fma(lc1, w, lc2 * wi)) ^ sw);
-    const double c = __longlong_as_double(__double_as_longlong(lc4 * wi) ^ sw);
-    const double b = lc3 * fabs(w);
-    double mm = a < b ? a : b;
-    mm = mm < c ? mm : c;
-    mm = mm > 0.0 ? mm : 0.0;
-    return __longlong_as_double(__double_as_longlong(mm) ^ sw);
-  };
-#endif
   double cfl = 0.0;
   double chk = 0.0;                     // sum of 0 * q_new: NaN iff some q_new is not finite
   int it = 0;
@@ -1340,14 +1337,11 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
   const double m3 = A.method3 == 2 ? 1.0 : 0.0, h = trans ? -0.5 : 0.0;
   const double lc1 = A.lim.c1, lc2 = A.lim.c2, lc3 = A.lim.c3, lc4 = A.lim.c4;
   auto limited = [&](double w, double wi) {   // as k_step_cv (MC / minmod)
-    const long long sw = __double_as_longlong(w) & (long long)0x8000000000000000ull;
-    const double a = __longlong_as_double(__double_as_longlong(fma(lc1, w, lc2 * wi)) ^ sw);
-    const double c = __longlong_as_double(__double_as_longlong(lc4 * wi) ^ sw);
-    const double b = lc3 * fabs(w);
-    double mm = a < b ? a : b;
-    mm = mm < c ? mm : c;
-    mm = mm > 0.0 ? mm : 0.0;
-    return __longlong_as_double(__double_as_longlong(mm) ^ sw);
+    const double a = fabs(w), b = fabs(wi);
+    const double x = fma(lc1, a, lc2 * b), y = lc3 * a, z = lc4 * b;
+    const double yz = 0.5 * ((y + z) - fabs(y - z));
+    const double mag = 0.5 * ((x + yz) - fabs(x - yz));
+    return w * wi > 0.0 ? copysign(mag, w) : 0.0;
   };
   double cfl = 0.0, chk = 0.0;
   int it = 0;

@@ -50,7 +50,9 @@ struct StepArgs {
 };
 // base of a ring source: this rank's q_old, a peer's (code k = rank k - 1), the computed ghosts (255)
 __device__ __forceinline__ const double* ring_base(const StepArgs& A, int ow) {
-  return ow == 0 ? A.qold : (ow == 255 ? A.cg : A.peerq[ow - 1]);
+  if (ow == 0) return A.qold;
+  if (ow == 255) return A.cg;
+  return A.peerq[ow - 1];
 }
 
 // ---- TMA bulk copies + mbarrier (sm_90+ / sm_100a) -------------------------------------------
