@@ -14,7 +14,7 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["forest.c", "ghost.c", "claw.c", "subcycle.c", "regrid.c"]
+SOURCES = ["forest.c", "ghost.c", "claw.c", "subcycle.c", "regrid.c", "forest3.c"]
 LIB = os.path.join(HERE, "liboracle.so")
 
 OK, EINVAL, ETILING, ECONN, EBALANCE, ENOMEM, EUNSUP, EPHYS = 0, -1, -2, -3, -4, -5, -6, -7

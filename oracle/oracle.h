@@ -140,6 +140,24 @@ int orc_rpt2(const orc_problem* pr, int ixy, const double* ql, const double* qr,
              const double* aux_recv, const double* aux_recv_next, const double* asdq,
              double* bmasdq, double* bpasdq);
 
+
+/* ---- forests of octrees (forest3.c): aligned bricks, meqn = 1 constant-velocity advection with
+ * Godunov dimensional splitting (reading 26) ---------------------------------------- */
+typedef struct orc3_forest orc3_forest;
+int orc3_forest_create(int64_t P, const int8_t* levels, const int32_t* tree_ids, int32_t T,
+                       const int32_t* t2t /* [6T] */, const int8_t* fbc /* [6T] 1 = outflow */, int m,
+                       orc3_forest** out);
+void orc3_forest_destroy(orc3_forest* f);
+int orc3_forest_coords(const orc3_forest* f, int64_t* x, int64_t* y, int64_t* z, int* lmax);
+int orc3_ring_count(int m);
+int orc3_ghost_records(const orc3_forest* f, int64_t p, int32_t* rec);
+int orc3_ghost_table(const orc3_forest* f, int32_t* rec);
+int orc3_ghost_fill(const orc3_forest* f, double* qpad);
+double orc3_step_patch(const orc3_forest* f, const double* qp, double u, double v, double w, int limiter,
+                       int method2, double dt, double dx, double* qnew);
+int orc3_step(const orc3_forest* f, double* qpad, double u, double v, double w, int limiter, int method2,
+              double dt, double dx0, double* qout, double* cfl);
+
 #ifdef __cplusplus
 }
 #endif
