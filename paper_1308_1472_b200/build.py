@@ -17,7 +17,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfc.so")
-SOURCES = ["api.cu", "kernels.cu", "step.cu", "step_ws.cu", "plan.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "step.cu", "step_ws.cu", "step3.cu", "plan.cpp"]
+# per-source extra flags: the octree path is bitwise the oracle (no fused multiply-add contraction)
+EXTRA = {"step3.cu": ["-fmad=false"]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -36,7 +38,8 @@ def nccl_dirs():
 
 def _deps():
     return [os.path.join(CSRC, s) for s in SOURCES] + glob.glob(os.path.join(CSRC, "*.h")) + \
-        glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "fc.h"), __file__]
+        glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(CSRC, "plan3.cpp")] + \
+        glob.glob(os.path.join(ROOT, "include", "*.h")) + [__file__]
 
 
 def _stamp(cmd) -> str:
@@ -77,7 +80,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     for s in SOURCES:
         o = os.path.join(odir, s + ".o")
         objs.append(o)
-        procs.append((s, subprocess.Popen(pre + ["-c", "-o", o, os.path.join(CSRC, s)],
+        procs.append((s, subprocess.Popen(pre + EXTRA.get(s, []) + ["-c", "-o", o, os.path.join(CSRC, s)],
                                           stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
     failed = False
     for s, p in procs:

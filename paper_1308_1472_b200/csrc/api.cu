@@ -58,6 +58,9 @@ int launch_filter(int kind, const double* qold, double* qnew, int npatch, int m,
 using namespace fc;
 
 static thread_local std::string g_err = "no error";
+namespace fc {
+void set_last_error(const std::string& m) { g_err = m; }   // (the octree ABI, step3.cu)
+}
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;

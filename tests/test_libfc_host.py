@@ -252,3 +252,30 @@ def test_compact_table_worked_example():
     assert lv[a] == lv[b] == 4 and a != b
     coarse = np.nonzero((t[:, :4, 0] == 1).any(axis=1))[0]
     assert (lv[coarse] == 4).all() and set(t[coarse][:, :4, 4][t[coarse][:, :4, 0] == 1].tolist()) == {0, 1}
+
+
+def test_library_exports_every_declared_octree_symbol():
+    from paper_1308_1472_b200 import fc3
+    hdr = open(os.path.join(ROOT, "include", "fc3.h")).read()
+    declared = sorted(set(re.findall(r"^\s*int\s+(fc3_\w+)\s*\(", hdr, re.M)))
+    assert declared == sorted(fc3.EXPORTS3)
+    L = fc.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def test_octree_tables_bit_exact_with_the_oracle():
+    """The planner's hash lookups (plan3.cpp) vs the oracle's Morton binary searches (forest3.c):
+    identical canonical records on uniform / AMR, periodic / outflow / mixed bricks."""
+    from oracle.octree import OracleForest3
+    from paper_1308_1472_b200 import fc3
+    from workloads.octree import forest3
+    cases = [forest3((2, 1, 1), 1), forest3((1, 2, 2), 1, periodic=(False, False, False)),
+             forest3((2, 2, 1), 1, refine=lambda t, x, y, z, h: t == 0 and x < 0.5 and (y + z) < 0.9),
+             forest3((2, 1, 2), 1, refine=lambda t, x, y, z, h: (t + x + y + z) < 1.2, periodic=(True, False, True)),
+             forest3((1, 1, 1), 2, refine=lambda t, x, y, z, h: x + y < 0.6, periodic=(False, True, False))]
+    for f in cases:
+        for m in (4, 6):
+            g = fc3.Forest3(f, m, device=-1)
+            np.testing.assert_array_equal(g.ghost_table(), OracleForest3(f, m).ghost_table())
+            g.close()
