@@ -27,6 +27,7 @@
 #include "fc_internal.h"
 #include "solvers.cuh"
 #include "step_common.cuh"
+#include "step_ws.cuh"
 
 namespace fc {
 
@@ -1610,7 +1611,11 @@ __global__ void __launch_bounds__(256) k_activity(int npatch, const uint8_t* __r
     }
     if (q) {
       const double dtdx = dt / ldexp(dx0, -(int)level[p]);
-      cfl = S::quiescent_cfl(v, 1, sp, nullptr, dtdx, 0, 0, 0, 1);
+      // Roe systems: the warp-sweep kernel's own CFL arithmetic for a uniform window (bitwise the
+      // full update's value, so both modes follow the same dt sequence); others: the state's speeds
+      if constexpr (std::is_same<S, EulerRoe>::value) cfl = ws_quiescent_cfl<WsEuler>(v, 1, sp, dtdx);
+      else if constexpr (std::is_same<S, SweRoe>::value) cfl = ws_quiescent_cfl<WsSwe>(v, 1, sp, dtdx);
+      else cfl = S::quiescent_cfl(v, 1, sp, nullptr, dtdx, 0, 0, 0, 1);
     } else {
       act = true;
     }

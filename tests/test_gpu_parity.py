@@ -115,6 +115,21 @@ def test_quiescent_shortcut_is_exact(w):
     np.testing.assert_allclose(c1_, c0_, rtol=1e-14, atol=0)
 
 
+@pytest.mark.parametrize("w", [c5(level=3, m=16, steps=40), c5(level=4, m=16, steps=30), c3(level=2, m=32, steps=40)],
+                         ids=lambda w: w.name)
+def test_quiescent_shortcut_follows_the_same_dt_sequence(w):
+    """under the workload's own variable-dt policy (no replayed dt list) the shortcut
+    and the full update must take the same dt decisions -- a quiescent window's CFL is computed
+    with the full update's own Roe arithmetic (step_ws.cuh, ws_quiescent_cfl), so the CFLs, hence
+    the dt sequence and the states, are bitwise equal.  (C5 L4: 1024 patches, the copy / activity
+    filter path; the others: the in-kernel uniform-window check.)"""
+    q1, c1_, d1 = fc.run(w, skip_quiescent=1)
+    q0, c0_, d0 = fc.run(w, skip_quiescent=0)
+    np.testing.assert_array_equal(c1_, c0_)
+    np.testing.assert_array_equal(d1, d0)
+    np.testing.assert_array_equal(q1, q0)
+
+
 def test_parity_c2_levels_and_dt_policy_on_gpu():
     """C2 with the GPU driving its own dt policy (fixed dt) equals the oracle's run."""
     w = c2()
