@@ -299,7 +299,50 @@ def run_variants(args, fc, hbm_peak):
                      "ghost_ms": st["ms_ghost"] / max(1, st["steps"]),
                      "fused_path": st.get("uniform_fast_path"), "generate_s": gen_s,
                      "steps": args.variant_steps, "mode": "full update (skip_quiescent = 0)"}
+    out["O3"] = run_octree(args, hbm_peak)
     return out
+
+
+def run_octree(args, hbm_peak):
+    """The octree path (include/fc3.h; reading 26) on this GPU: a 2 x 1 x 1 periodic
+    brick of octrees at uniform level 4, m = 16 (8192 patches, 33.6 M cells), a Gaussian bump,
+    velocity (0.8, -0.45, 0.3), MC, fixed dt at Courant 0.9; K steps after W warm-ups, CUDA events
+    around the step loop (each step reads its CFL back).  Bitwise the oracle (tests/test_gpu_octree.py)."""
+    import numpy as np
+    import torch
+    from paper_1308_1472_b200 import fc3
+    from workloads.octree import cell_centres, forest3
+    t0 = time.perf_counter()
+    f = forest3((2, 1, 1), 4)
+    m = 16
+    c = cell_centres(f, m)
+    q0 = np.exp(-8.0 * ((c[:, 0] - 0.6) ** 2 + (c[:, 1] - 0.5) ** 2 + (c[:, 2] - 0.45) ** 2))
+    gen_s = time.perf_counter() - t0
+    g = fc3.Forest3(f, m, torch.cuda.current_device())
+    vel = (0.8, -0.45, 0.3)
+    dt = 0.9 / (m * 2 ** 4) / 0.8
+    g.set_problem(vel)
+    stream = torch.cuda.current_stream()
+    g.set_stream(stream.cuda_stream)
+    g.set_q(np.ascontiguousarray(q0))
+    for _ in range(max(3, args.warmup)):
+        g.step(dt)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.variant_steps):
+        g.step(dt)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.variant_steps
+    g.close()
+    cells = f.num_patches * m ** 3
+    rate = cells / (ms / 1e3)
+    return {"workload": "octree brick 2x1x1, uniform level 4, m = 16, scalar advection (Godunov split)",
+            "patches": int(f.num_patches), "cells": int(cells), "ms_per_step": ms, "value": rate, "unit": UNIT,
+            "bytes_per_cell_update": 16, "hbm_roofline_frac": rate * 16 / (hbm_peak * 1e9),
+            "timing": "CUDA events on the library's stream around K fc3_step calls (each reads its CFL back)",
+            "generate_s": gen_s, "steps": args.variant_steps}
 
 
 def main():

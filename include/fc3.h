@@ -60,6 +60,9 @@ int fc3_ghost_fill(fc3_forest* f);
  * Commits iff max_cfl <= cfl_reject, else FC_ECFL with q unchanged; FC_EINVAL for dt <= 0. */
 int fc3_step(fc3_forest* f, double dt, double* max_cfl);
 
+/* Use the caller's cudaStream_t for all subsequent work (NULL = the handle's own stream). */
+int fc3_set_stream(fc3_forest* f, void* stream);
+
 /* interiors of q_old -> q[P][m][m][m]; padded blocks -> q[P][n][n][n] (n = m + 4).  Synchronous. */
 int fc3_get_q(fc3_forest* f, double* q, int where);
 int fc3_get_q_padded(fc3_forest* f, double* q, int where);

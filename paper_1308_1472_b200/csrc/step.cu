@@ -21,7 +21,10 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <map>
+#include <mutex>
 #include <type_traits>
+#include <utility>
 
 #include "../../include/fc.h"
 #include "fc_internal.h"
@@ -1688,8 +1691,12 @@ int launch_filter(int kind, const double* qold, double* qnew, int npatch, int m,
 template <class S, int T, int NT, int MINB, bool RF>
 static int launch_step_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   const size_t smem = StepShape<S, T>::smem_bytes;
-  static int resident = 0;   // CTAs that fit on the device at once (persistent grid)
-  if (!resident) {
+  static int resident_dev[64] = {};   // per device: CTAs that fit at once (persistent grid)
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (dev_ < 0 || dev_ >= 64) return -1;
+  int& resident = resident_dev[dev_];
+  if (!resident) {   // (function attributes are per device)
     cudaFuncSetAttribute(k_step<S, T, NT, MINB, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_step<S, T, NT, MINB, RF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int dev = 0, sms = 0, per_sm = 0;
@@ -1703,15 +1710,18 @@ static int launch_step_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   const int64_t grid = ntiles < resident ? ntiles : resident;   // (active list: at most ntiles)
   StepArgs b = a;
   b.fbuf = nullptr;
-  if (a.method3 == 1) {      // F~ scratch for the (rare) method3 = 1 transverse variant, kept for the
-    static double* fbuf[64] = {};    // process lifetime, one per device (resident CTAs x E2)
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) return -1;
-    if (!fbuf[dev] &&
-        cudaMalloc(&fbuf[dev], (size_t)resident * S::MEQN * StepShape<S, T>::E2 * sizeof(double)) != cudaSuccess)
+  if (a.method3 == 1) {      // F~ scratch for the (rare) method3 = 1 transverse variant: one per
+    // (device, stream) for the process lifetime (resident CTAs x E2), so handles stepping on
+    // different streams never share it; launches on one stream are ordered
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, double*> bufs;
+    std::lock_guard<std::mutex> lock(mu);
+    double*& fb = bufs[std::make_pair(dev_, st)];
+    if (!fb && cudaMalloc(&fb, (size_t)resident * S::MEQN * StepShape<S, T>::E2 * sizeof(double)) != cudaSuccess) {
+      fb = nullptr;
       return -1;
-    b.fbuf = fbuf[dev];
+    }
+    b.fbuf = fb;
   }
   k_step<S, T, NT, MINB, RF><<<(unsigned)grid, NT, smem, st>>>(b, (int)ntiles);
   return 1;
@@ -1723,7 +1733,11 @@ static int launch_sc_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   constexpr int NXE = (T + 1) * (T + 2);
   const size_t smem = ((size_t)sc_nbuf<S>() * StepShape<S, T>::BUF + 2 * (size_t)StepShape<S, T>::WW +
                        12 * (size_t)NXE) * sizeof(double);
-  static int resident = 0;
+  static int resident_dev[64] = {};
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (dev_ < 0 || dev_ >= 64) return -1;
+  int& resident = resident_dev[dev_];
   if (!resident) {
     cudaFuncSetAttribute(k_step_sc<S, T, NT, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_step_sc<S, T, NT, RF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1748,7 +1762,11 @@ static int launch_cv_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   constexpr int NB = CV_NB;
   using C = CvShape<T>;
   const size_t smem = (size_t)NB * C::PW * C::WW * sizeof(double);
-  static int resident = 0;
+  static int resident_dev[64] = {};
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (dev_ < 0 || dev_ >= 64) return -1;
+  int& resident = resident_dev[dev_];
   if (!resident) {
     cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB, RF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1770,7 +1788,11 @@ static int launch_cvc_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   constexpr int NB = CV_NB;
   using C = CvShape<T>;
   const size_t smem = (size_t)NB * C::PW * C::WW * sizeof(double);
-  static int resident = 0;
+  static int resident_dev[64] = {};
+  int dev_ = 0;
+  cudaGetDevice(&dev_);
+  if (dev_ < 0 || dev_ >= 64) return -1;
+  int& resident = resident_dev[dev_];
   if (!resident) {
     cudaFuncSetAttribute(k_step_cvc<T, MT2, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_step_cvc<T, MT2, NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);

@@ -10,7 +10,7 @@ import numpy as np
 from .fc import FC_LIM_MC, FC_OK, _check, _ptr, lib as _lib
 
 EXPORTS3 = ["fc3_forest_create", "fc3_forest_destroy", "fc3_set_problem", "fc3_set_q", "fc3_ghost_fill",
-            "fc3_step", "fc3_get_q", "fc3_get_q_padded", "fc3_get_ghost_table"]
+            "fc3_step", "fc3_get_q", "fc3_get_q_padded", "fc3_get_ghost_table", "fc3_set_stream"]
 
 
 class Forest3Desc(C.Structure):
@@ -36,6 +36,7 @@ def lib():
         L.fc3_get_q.argtypes = [P, P, C.c_int]
         L.fc3_get_q_padded.argtypes = [P, P, C.c_int]
         L.fc3_get_ghost_table.argtypes = [P, P, C.c_int64, C.POINTER(C.c_int64)]
+        L.fc3_set_stream.argtypes = [P, P]
         _init = True
     return L
 
@@ -69,6 +70,9 @@ class Forest3:
     def set_q(self, q):
         p, where = _ptr(q)
         _check(lib().fc3_set_q(self.h, p, where), "fc3_set_q")
+
+    def set_stream(self, stream_ptr):
+        _check(lib().fc3_set_stream(self.h, C.c_void_p(stream_ptr) if stream_ptr else None), "fc3_set_stream")
 
     def ghost_fill(self):
         _check(lib().fc3_ghost_fill(self.h), "fc3_ghost_fill")
