@@ -136,13 +136,13 @@ def test_sharded_eight_ranks_bitwise(w, R):
 
 
 # ---- peer-memory halo (halo_p2p): the fused gather reads other ranks' buffers directly -----------
-def run_sharded_p2p(w, R, dts):
+def run_sharded_p2p(w, R, dts, skip=1):
     """R rank handles with halo_p2p = 1 wired to each other's state buffers (same device: the peer
     pointers are plain device pointers here, CUDA IPC mappings with NCCL); no halo pass at all."""
     hs = [fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0, 0, r, R, None,
                     halo_p2p=1) for r in range(R)]
     for f in hs:
-        f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject, 1)
+        f.set_problem(w.kind, w.params[0], w.params[1], w.limiter, w.method2, w.method3, w.cfl_reject, skip)
     bufs = [f.p2p_buffers() for f in hs]
     for r, f in enumerate(hs):
         for s in range(R):
@@ -173,6 +173,18 @@ def test_peer_memory_halo_equals_single_rank_bitwise(w, R):
     _, _, do = oracle.run(w)
     q1, c1_, _ = fc.run(w, dt_list=do)
     qr, cr = run_sharded_p2p(w, R, do)
+    np.testing.assert_array_equal(qr, q1)
+    np.testing.assert_array_equal(cr, c1_)
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
+@pytest.mark.parametrize("w", [c5(level=3, m=16, steps=10), c3(level=2, m=32, steps=10)], ids=lambda w: w.name)
+def test_peer_memory_halo_full_update_bitwise(w, R):
+    """bench.py's multi-GPU mode: the full update (skip_quiescent = 0) with the peer-memory halo --
+    the warp-sweep kernel gathers remote ring cells straight from the owners' buffers."""
+    _, _, do = oracle.run(w)
+    q1, c1_, _ = fc.run(w, dt_list=do, skip_quiescent=0)
+    qr, cr = run_sharded_p2p(w, R, do, skip=0)
     np.testing.assert_array_equal(qr, q1)
     np.testing.assert_array_equal(cr, c1_)
 
