@@ -297,3 +297,37 @@ def test_constant_velocity_physical_boundaries_against_oracle(bc, m):
         for skip in (1, 0):
             qg, cg, _ = fc.run(w, dt_list=do, skip_quiescent=skip)
             assert_parity(w, qg, qo, cg, co, mass_rtol=1.0)   # (outflow: mass leaves the domain)
+
+
+def _amr_euler_m16(steps=10):
+    import dataclasses as _dc
+    import sys as _sys
+    import os as _os
+    _sys.path.insert(0, _os.path.dirname(__file__))
+    from test_gpu_subcycle import amr_euler
+    from workloads import forests as _F
+    from workloads.configs import EULER_ROE
+    r = np.random.default_rng(1308147 + 77)
+    fr = _F.forest_refined(_F.brick(2, 1, periodic_x=True, periodic_y=True), 1, lambda t, x, y, h: r.random(len(x)) < 0.5)
+    m = 16
+    X, Y = _F.cell_centres(fr, m)
+    X = X + fr.tree_ids[:, None, None]
+    rho = 1.0 + 0.5 * np.exp(-20 * ((X - 1.0) ** 2 + (Y - 0.5) ** 2))
+    u, v, p = 0.3 + 0 * X, -0.2 + 0 * X, 1.0 + 0.3 * np.sin(2 * np.pi * X)
+    g = 1.4
+    q0 = np.stack([rho, rho * u, rho * v, p / (g - 1) + 0.5 * rho * (u * u + v * v)], 1)
+    return Workload("amr_euler_m16", fr, m, 4, 0, EULER_ROE, (g, 1.0), q0, None, steps, 1e-3, "cfl")
+
+
+@pytest.mark.parametrize("skip", [1, 0], ids=["quiescent_skip", "full_update"])
+@pytest.mark.parametrize("w", [_amr_euler_m16(), c3(level=1, m=48, steps=20)], ids=lambda w: w.name)
+def test_warp_sweep_kernel_on_amr_and_3x3_tiles(w, skip):
+    """The warp-sweep kernel with the fused two-hop AMR gather (computed ghosts: ring owner code
+    255) on an m = 16 AMR Euler brick, and on m = 48 patches (3 x 3 tiles of 16), against the
+    oracle."""
+    qo, co, do = oracle.run(w)
+    f = gpu_forest(w)
+    if w.name.startswith("amr"):
+        assert f.stats()["uniform_fast_path"] == 2
+    qg, cg, _ = fc.run(w, dt_list=do, skip_quiescent=skip)
+    assert_parity(w, qg, qo, cg, co)

@@ -18,17 +18,17 @@ pytestmark = pytest.mark.gpu
 GAM = 1.4
 
 
-def amr_euler(steps=8):
+def amr_euler(steps=8, m=8):
     r = np.random.default_rng(1308147 + 31)
     fr = F.forest_refined(F.brick(2, 1, periodic_x=True, periodic_y=True), 1,
                           lambda t, x, y, h: r.random(len(x)) < 0.5)
-    m = 8
     X, Y = F.cell_centres(fr, m)
     X = X + fr.tree_ids[:, None, None]
     rho = 1.0 + 0.5 * np.exp(-20 * ((X - 1.0) ** 2 + (Y - 0.5) ** 2))
     u, v, p = 0.3 + 0 * X, -0.2 + 0 * X, 1.0 + 0.3 * np.sin(2 * np.pi * X)
     q0 = np.stack([rho, rho * u, rho * v, p / (GAM - 1) + 0.5 * rho * (u * u + v * v)], 1)
-    return Workload("amr_euler", fr, m, 4, 0, EULER_ROE, (GAM, 1.0), q0, None, steps, 1e-3, "cfl")
+    return Workload("amr_euler" + ("" if m == 8 else f"_m{m}"), fr, m, 4, 0, EULER_ROE, (GAM, 1.0), q0, None, steps,
+                    1e-3, "cfl")
 
 
 def three_levels(steps=6):
@@ -59,7 +59,8 @@ def sphere(steps=6):
     return CS.c4_workload(base_level=2, m=8, steps=steps)
 
 
-CASES = [c2(steps=15), c2(base_level=2, m=32, steps=8), amr_euler(), sphere(), three_levels()]
+CASES = [c2(steps=15), c2(base_level=2, m=32, steps=8), amr_euler(), sphere(), three_levels(),
+         amr_euler(steps=6, m=16)]   # (m = 16: the warp-sweep kernel with computed ghosts per level)
 
 
 def mass(w, q):
