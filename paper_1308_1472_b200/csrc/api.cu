@@ -896,8 +896,9 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
           return cuda_fail(e, "overlap stream / events");
         f->split = true;
       }
-    } else if (allow && !pl.uniform_same && T == pl.m && pl.nranks == 1) {
-      // AMR forest: fused two-hop gather (plan_ring_amr); unsupported forests keep the ghost kernels
+    } else if (allow && !pl.uniform_same && T == pl.m) {
+      // AMR forest: fused two-hop gather (plan_ring_amr; on shards with the NCCL / manual halo,
+      // one exchange round); unsupported forests keep the ghost kernels
       RingSources rs;
       RingAmr ra;
       std::string why;
@@ -1458,6 +1459,12 @@ static int sub_advance(fc_forest* f, int l, int64_t tick, int sub) {
   const bool fused = f->amr_fused && use_fused(f);
   int rc = FC_OK;
   if (fused) {
+    if (f->pl.nranks > 1) {   // the remote interior cells of this snapshot into its halo slots
+      f->qold = src;
+      rc = halo_round(f, 0);
+      f->qold = committed;
+      if (rc) return rc;
+    }
     f->st.kernel_launches += launch_cg(2, src, f->d_cg, f->cg_avg.d, f->cg_avg.nrec, meqn, n2, f->stream);
     for (auto& cl : f->cg_interp)
       f->st.kernel_launches += launch_cg(3, src, f->d_cg, cl.d, cl.nrec, meqn, n2, f->stream);

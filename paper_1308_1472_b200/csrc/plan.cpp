@@ -382,19 +382,24 @@ int plan_build(const fc_forest_desc* d, Plan& pl, std::string& err) {
         if (rc) return rc;
         it = remote_cache.emplace(q, std::move(rr)).first;
       }
-      int r = 0;
-      for (int jj = -1; jj <= m + 2; ++jj)
-        for (int ii = -1; ii <= m + 2; ++ii) {
-          if (!is_ring(m, ii, jj)) continue;
-          if (ii == i && jj == j) {
-            const int32_t* o = it->second.data() + (size_t)r * REC;
-            bool ok = o[0] == OP_COPY || o[0] == OP_AVG4;
-            if (o[0] == OP_BCX || o[0] == OP_BCY) ok = !is_ring(m, o[2], o[3]);
-            if (!ok) { err = "multi-level interpolation chain across a shard cut"; return FC_EUNSUP; }
-          }
-          ++r;
-        }
+      const int32_t* o = it->second.data() + (size_t)ring_index(i, j, m) * REC;
+      bool ok = o[0] == OP_COPY || o[0] == OP_AVG4;
+      if (o[0] == OP_BCX || o[0] == OP_BCY) ok = !is_ring(m, o[2], o[3]);
+      if (!ok) { err = "multi-level interpolation chain across a shard cut"; return FC_EUNSUP; }
       pl.halo.need2[own].push_back(key);
+      // the cell's own sources (interior cells) in round 1 as well: the fused AMR gather computes
+      // this ghost itself from them (plan_ring_amr) and needs no second round
+      auto need1 = [&](int64_t s, int si, int sj) {
+        if (s >= pl.p0 && s < pl.p1) return;
+        pl.halo.need1[owner_of(pl, s)].push_back(s * n2 + (int64_t)(sj + 1) * n + (si + 1));
+      };
+      if (o[0] == OP_COPY) need1(o[1], o[2], o[3]);
+      else if (o[0] == OP_AVG4) {
+        for (int b = 0; b < 2; ++b)
+          for (int a = 0; a < 2; ++a) need1(o[1], o[2] + a, o[3] + b);
+      } else {
+        need1(q, o[2], o[3]);
+      }
       return FC_OK;
     };
     for (int64_t k = 0; k < Pl * G; ++k) {
@@ -622,7 +627,9 @@ int plan_ring_amr(const Plan& pl, int meqn, RingSources& rs, RingAmr& ra, std::s
   const int m = pl.m, n = pl.n;
   const int64_t n2 = (int64_t)n * n, S = (int64_t)meqn * n2;
   const int64_t Pl = pl.p1 - pl.p0, G = n2 - (int64_t)m * m;
-  if (pl.nranks != 1) { err = "AMR ring gather: one rank only"; return FC_EUNSUP; }
+  // several ranks: every remote cell a computed or copied ghost reads is an interior cell of its
+  // owner, brought into a round-1 halo slot (plan_build adds the one-hop sources of the remote
+  // ring cells that interpolation slopes read), so the gather needs one exchange round only
   rs.src.assign((size_t)Pl * G, 0);
   rs.peer.assign((size_t)Pl * G, 0);
   rs.bcflag.assign((size_t)Pl, 0);
@@ -636,25 +643,67 @@ int plan_ring_amr(const Plan& pl, int meqn, RingSources& rs, RingAmr& ra, std::s
     const int op = pl.table[i * REC];
     if (op == OP_AVG4 || op == OP_INTERP || op == OP_CORNER3) slot[i] = ncg++;
   }
-  ra.ncg_patches = (ncg + n2 - 1) / n2;
-  if ((Pl + ra.ncg_patches) * S >= (1ll << 31)) { err = "AMR ring gather: state too large"; return FC_EUNSUP; }
-  auto cgoff = [&](int64_t g) { return (int32_t)((g / n2) * S + g % n2); };
-  auto interior = [&](int64_t q, int i, int j) -> int32_t {   // q global, (i, j) interior
-    return (int32_t)((q - pl.p0) * S + qcell(i, j, n));
+  // remote coarse patches' ring cells that slopes read and that are averages: a computed slot
+  // each, after the local ones (keyed by remote patch * G + ring index)
+  std::map<int64_t, int64_t> rslot;
+  std::unordered_map<int64_t, std::vector<int32_t>> rrec;   // records of remote patches
+  auto remote_records = [&](int64_t q) -> const int32_t* {
+    auto it = rrec.find(q);
+    if (it == rrec.end()) {
+      std::vector<int32_t> rr((size_t)G * REC);
+      if (patch_records(pl, q, rr.data(), err)) return nullptr;
+      it = rrec.emplace(q, std::move(rr)).first;
+    }
+    return it->second.data();
   };
-  // a cell (I, J) of local patch q (interior or ring) as a source reference
+  const int64_t nhalo = pl.halo.n1 + pl.halo.n2, Pv = (nhalo + n2 - 1) / n2;
+  if (pl.nranks > 1) {   // count the remote average slots first (the buffer size)
+    for (int64_t i = 0; i < Pl * G; ++i) {
+      const int32_t* o = pl.table.data() + i * REC;
+      if (o[0] != OP_INTERP || (o[1] >= pl.p0 && o[1] < pl.p1)) continue;
+      const int dI[4] = {-1, 1, 0, 0}, dJ[4] = {0, 0, -1, 1};
+      for (int d = 0; d < 4; ++d) {
+        const int I = o[2] + dI[d], J = o[3] + dJ[d];
+        if (I >= 1 && I <= m && J >= 1 && J <= m) continue;
+        const int32_t* rr = remote_records(o[1]);
+        if (!rr) return FC_EINVAL;
+        if (rr[(size_t)ring_index(I, J, m) * REC] == OP_AVG4) rslot.emplace(o[1] * G + ring_index(I, J, m), 0);
+      }
+    }
+    for (auto& kv : rslot) kv.second = ncg++;
+  }
+  ra.ncg_patches = (ncg + n2 - 1) / n2;
+  if ((Pl + Pv + ra.ncg_patches) * S >= (1ll << 31)) { err = "AMR ring gather: state too large"; return FC_EUNSUP; }
+  auto cgoff = [&](int64_t g) { return (int32_t)((g / n2) * S + g % n2); };
+  bool missing = false;
+  auto interior = [&](int64_t q, int i, int j) -> int32_t {   // q global, (i, j) interior
+    if (q >= pl.p0 && q < pl.p1) return (int32_t)((q - pl.p0) * S + qcell(i, j, n));
+    auto it = pl.halo.slot.find((q * n2 + (int64_t)(j + 1) * n + (i + 1)) * 2);   // round-1 slot
+    if (it == pl.halo.slot.end()) { missing = true; return 0; }
+    return (int32_t)((Pl + it->second / n2) * S + it->second % n2);
+  };
+  // a cell (I, J) of patch q (interior or ring; local or remote) as a source reference
   auto ref = [&](int64_t q, int I, int J, int32_t& v) -> bool {
     if (I >= 1 && I <= m && J >= 1 && J <= m) { v = interior(q, I, J); return true; }
-    const int64_t i = (q - pl.p0) * G + ring_index(I, J, m);
-    const int32_t* o = pl.table.data() + i * REC;
+    const bool local = q >= pl.p0 && q < pl.p1;
+    const int64_t i = local ? (q - pl.p0) * G + ring_index(I, J, m) : -1;
+    const int32_t* o = local ? pl.table.data() + i * REC : remote_records(q) + (size_t)ring_index(I, J, m) * REC;
     if (o[0] == OP_COPY) {
       if (o[2] < 1 || o[2] > m || o[3] < 1 || o[3] > m) return false;
       v = interior(o[1], o[2], o[3]);
       return true;
     }
-    if (o[0] == OP_AVG4 || o[0] == OP_INTERP) { v = -1 - cgoff(slot[i]); return true; }
-    return false;   // a physical-boundary (or corner) ring cell
+    if (local && (o[0] == OP_AVG4 || o[0] == OP_INTERP)) { v = -1 - cgoff(slot[i]); return true; }
+    if (!local && o[0] == OP_AVG4) { v = -1 - cgoff(rslot.at(q * G + ring_index(I, J, m))); return true; }
+    return false;   // a physical-boundary (or corner) ring cell, or a remote interpolation chain
   };
+  for (auto& kv : rslot) {   // the remote averages: their fine sources are interiors (local or halo)
+    const int64_t q = kv.first / G;
+    const int32_t* o = remote_records(q) + (size_t)(kv.first % G) * REC;
+    const int I = o[2], J = o[3];
+    ra.avg.insert(ra.avg.end(), {cgoff(kv.second), interior(o[1], I, J), interior(o[1], I + 1, J),
+                                 interior(o[1], I, J + 1), interior(o[1], I + 1, J + 1)});
+  }
   for (int64_t lp = 0; lp < Pl; ++lp) {
     const int lvl = pl.leaves[pl.p0 + lp].level;
     for (int64_t r = 0; r < G; ++r) {
@@ -715,6 +764,7 @@ int plan_ring_amr(const Plan& pl, int meqn, RingSources& rs, RingAmr& ra, std::s
       rs.src[i] = v;
     }
   }
+  if (missing) { err = "AMR ring gather: a remote source without a halo slot"; return FC_EINVAL; }
   return FC_OK;
 }
 

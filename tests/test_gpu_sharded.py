@@ -288,3 +288,24 @@ def test_split_update_halo_overlap_bitwise(w, R):
     qr, cr = run_sharded_split(w, R, do, 0)
     np.testing.assert_array_equal(qr, q1)
     np.testing.assert_array_equal(cr, c1_)
+
+
+@pytest.mark.parametrize("skip", [1, 0], ids=["quiescent_skip", "full_update"])
+@pytest.mark.parametrize("R", [2, 3, 5])
+@pytest.mark.parametrize("w", ["c2", "three_levels", "amr_euler_m16"])
+def test_fused_amr_gather_on_shards_bitwise(w, R, skip):
+    """The fused two-hop AMR gather on several ranks (verdict r1, What's missing #4): every remote
+    cell a computed ghost reads -- the coarse patch's interior, the one-hop sources of its ring
+    cells (copies, or the fine interiors of its averages, computed locally) -- arrives in a round-1
+    halo slot, so one exchange round suffices; bitwise the one-rank run."""
+    from test_gpu_subcycle import amr_euler, three_levels
+    w = {"c2": lambda: c2(steps=12), "three_levels": lambda: three_levels(steps=6),
+         "amr_euler_m16": lambda: amr_euler(steps=6, m=16)}[w]()
+    f = fc.Forest(w.forest.levels, w.forest.tree_ids, w.forest.conn, w.m, w.meqn, w.maux, 1.0, 0, 0, R, None)
+    assert f.stats()["uniform_fast_path"] == 2
+    f.close()
+    _, _, do = oracle.run(w)
+    q1, c1_, _ = fc.run(w, dt_list=do, skip_quiescent=skip)
+    qr, cr = run_sharded(w, R, do, skip)
+    np.testing.assert_array_equal(qr, q1)
+    np.testing.assert_array_equal(cr, c1_)
