@@ -26,6 +26,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "../../include/fc.h"
 #include "fc_internal.h"
 #include "solvers.cuh"
@@ -48,7 +50,7 @@ struct WsShape {
   static constexpr int N_UP = S::MEQN * NR * UPP;
   static constexpr int N_RT = S::MEQN * T * RTP;
   static constexpr int N_DQ = S::MEQN * T * DQP;
-  static constexpr size_t smem_doubles = 2 * (size_t)QB + 2 * (size_t)N_UP + 2 * (size_t)N_RT + N_DQ;
+  static constexpr size_t smem_doubles = 2 * (size_t)QB + 2 * (size_t)N_UP + 2 * (size_t)N_RT + 2 * (size_t)N_DQ;
   static constexpr size_t smem_bytes = smem_doubles * sizeof(double);
 };
 
@@ -199,12 +201,9 @@ __device__ __forceinline__ void ws_output(const StepArgs& A, int m3, const typen
       rt[(k * T + (j - 1)) * Sh::RTP + i] = hr * bpP[k] + hr * bpQ[k];
       lf[(k * T + (j - 1)) * Sh::RTP + i] = hr * bmP[k] + hr * bmQ[k];
     }
-    if (i >= 1 && i <= T) {   // the y increment on top of the x-sweep's (single writer per cell)
+    if (i >= 1 && i <= T) {   // the y increment (its own array: the sweeps run concurrently)
 #pragma unroll
-      for (int k = 0; k < MEQN; ++k) {
-        double* d = dq + (k * T + (j - 1)) * Sh::DQP + (i - 1);
-        *d = (*d - r * Pn[k]) - r * Q[k];
-      }
+      for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
     }
   }
 }
@@ -219,18 +218,19 @@ __device__ __forceinline__ double ws_phi(const LimiterCoef& L, double th) {
   return t > L.lo ? t : L.lo;
 }
 
-// One sweep (D = 1: x-edges of rows 0..T+1; D = 2: y-edges of columns 0..T+1) as NIT warp-iterations.
-// FAST: method2 = 2 and method3 = 2 (the configs) known at compile time; otherwise read from A.
-template <class S, int D, int NW, bool FAST>
-__device__ __forceinline__ void ws_sweep(const StepArgs& A, const double* __restrict__ sq, double* __restrict__ up,
-                                         double* __restrict__ dn, double* __restrict__ dq, double r, double& smax,
-                                         int warp, int lane) {
+// One warp-iteration `it` of a sweep (D = 1: x-edges of rows 0..T+1; D = 2: y-edges of columns
+// 0..T+1; NIT iterations per sweep).  FAST: method2 = 2 and method3 = 2 (the configs) known at
+// compile time; otherwise read from A.
+template <class S, int D, bool FAST>
+__device__ __forceinline__ void ws_iter(const StepArgs& A, const double* __restrict__ sq, double* __restrict__ up,
+                                        double* __restrict__ dn, double* __restrict__ dq, double r, double& smax,
+                                        int it, int lane) {
   using Sh = WsShape<S>;
   constexpr int T = Sh::T, PW = Sh::PW, WPW = Sh::WPW, NE = Sh::NE, E = Sh::E, MEQN = S::MEQN;
   const double hr = -0.5 * r;
   const bool m2 = FAST || A.method2 == 2;
   const int m3 = FAST ? 2 : A.method3;
-  for (int it = warp; it < Sh::NIT; it += NW) {
+  {
     const int e = it * Sh::STEP - 1 + lane;                 // flat edge index of this lane
     const bool ev = (unsigned)e < (unsigned)E;
     const int ee = ev ? e : 0;
@@ -327,7 +327,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
   double* dn = up + Sh::N_UP;
   double* rt = dn + Sh::N_UP;                  // y-sweep F~ halves (right / left)
   double* lf = rt + Sh::N_RT;
-  double* dq = lf + Sh::N_RT;
+  double* dq = lf + Sh::N_RT;                  // x increments
+  double* dqy = dq + Sh::N_DQ;                 // y increments
   __shared__ double wmax[NW];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double cfl = 0.0;
@@ -393,10 +394,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
         continue;
       }
     }
+    // both sweeps read Q^n only (unsplit): their 2 NIT warp-iterations are one phase
     double smax = 0.0;
-    ws_sweep<S, 1, NW, FAST>(A, sq, up, dn, dq, r, smax, warp, lane);
-    __syncthreads();
-    ws_sweep<S, 2, NW, FAST>(A, sq, rt, lf, dq, r, smax, warp, lane);
+    for (int v = warp; v < 2 * Sh::NIT; v += NW) {
+      if (v < Sh::NIT) ws_iter<S, 1, FAST>(A, sq, up, dn, dq, r, smax, v, lane);
+      else ws_iter<S, 2, FAST>(A, sq, rt, lf, dqy, r, smax, v - Sh::NIT, lane);
+    }
     cfl = fmax(cfl, r * smax);
     __syncthreads();
     // fold: q_new = q + (x and y increments) - r (G~ and F~ differences), one thread per cell
@@ -414,7 +417,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
         const double* ll = lf + (k * T + jj) * Sh::RTP;
         const double fr = rr[i] + ll[i + 1];
         const double fl = rr[i - 1] + ll[i];
-        const double dxy = dq[(k * T + jj) * Sh::DQP + ii];
+        const double dxy = dq[(k * T + jj) * Sh::DQP + ii] + dqy[(k * T + jj) * Sh::DQP + ii];
         const double val = qs[k * WPW] + ((dxy - r * (gt - gb)) - r * (fr - fl));
         bad |= !isfinite(val);
         o[k * n2 + jj * A.m + ii] = val;
@@ -460,10 +463,14 @@ static int launch_ws_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
 #ifndef WS_MINB
 #define WS_MINB 2
 #endif
+// warps per CTA: 24 warp-iterations per tile (both sweeps) over 6 or 8 warps; 2 CTAs per SM.
+// Measured (C5 / T3 full update): Euler 6 warps (166 registers) 8.45 ms, 8 warps (128: spills)
+// 9.53 ms; SWE 8 warps 5.51 ms vs 5.75 ms with 6
 template <class S>
 static int launch_ws_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
-  if (a.method2 == 2 && a.method3 == 2) return launch_ws_t<S, 6, WS_MINB, true>(a, npatch, st);
-  return launch_ws_t<S, 6, WS_MINB, false>(a, npatch, st);
+  constexpr int NW = std::is_same<S, WsSwe>::value ? 8 : 6;
+  if (a.method2 == 2 && a.method3 == 2) return launch_ws_t<S, NW, WS_MINB, true>(a, npatch, st);
+  return launch_ws_t<S, NW, WS_MINB, false>(a, npatch, st);
 }
 
 int launch_step_ws(int kind, const StepArgs& a, int64_t npatch, cudaStream_t st) {
