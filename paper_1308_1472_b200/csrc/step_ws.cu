@@ -50,8 +50,10 @@ struct WsShape {
   static constexpr int N_UP = S::MEQN * NR * UPP;
   static constexpr int N_RT = S::MEQN * T * RTP;
   static constexpr int N_DQ = S::MEQN * T * DQP;
-  static constexpr size_t smem_doubles = 2 * (size_t)QB + 2 * (size_t)N_UP + 2 * (size_t)N_RT + 2 * (size_t)N_DQ;
-  static constexpr size_t smem_bytes = smem_doubles * sizeof(double);
+  static constexpr size_t smem_doubles(int nbuf) {
+    return nbuf * (size_t)QB + 2 * (size_t)N_UP + 2 * (size_t)N_RT + 2 * (size_t)N_DQ;
+  }
+  static constexpr size_t smem_bytes(int nbuf) { return smem_doubles(nbuf) * sizeof(double); }
 };
 
 // tile -> (patch, tile column, tile row)
@@ -72,14 +74,14 @@ __device__ __forceinline__ void ws_tile(const StepArgs& A, int tile, int& patch,
 // interior, a peer rank's buffer, or a computed ghost); physical-boundary cells after the wait.
 // Two stages so that the ring-table loads never stall the issuing thread: ws_prep loads this
 // thread's (<= 3) table entries a whole tile ahead, ws_issue turns them into cp.async copies.
-constexpr int WS_GU = 3;   // window cells per thread (ceil(400 / 192))
+template <int GU>          // window cells per thread (ceil(400 / threads))
 struct WsGather {
   int tile;
-  int32_t v[WS_GU];        // ring source offset, or -1 - BC code, or INT32_MIN: own interior
-  uint8_t ow[WS_GU];       // owner code of a ring source (0 local, k peer rank k-1, 255 computed)
+  int32_t v[GU];           // ring source offset, or -1 - BC code, or INT32_MIN: own interior
+  uint8_t ow[GU];          // owner code of a ring source (0 local, k peer rank k-1, 255 computed)
 };
-template <class S>
-__device__ __forceinline__ void ws_prep(const StepArgs& A, int tile, WsGather& g, int tid, int nt) {
+template <class S, int WS_GU>
+__device__ __forceinline__ void ws_prep(const StepArgs& A, int tile, WsGather<WS_GU>& g, int tid, int nt) {
   using Sh = WsShape<S>;
   constexpr int T = Sh::T, W = Sh::W;
   g.tile = tile;
@@ -103,8 +105,8 @@ __device__ __forceinline__ void ws_prep(const StepArgs& A, int tile, WsGather& g
     if (rp) g.ow[u] = __ldg(rp + r);
   }
 }
-template <class S>
-__device__ __forceinline__ void ws_issue(const StepArgs& A, const WsGather& g, double* sq, int tid, int nt) {
+template <class S, int WS_GU>
+__device__ __forceinline__ void ws_issue(const StepArgs& A, const WsGather<WS_GU>& g, double* sq, int tid, int nt) {
   using Sh = WsShape<S>;
   constexpr int T = Sh::T, W = Sh::W, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN;
   if (g.tile < 0) return;
@@ -308,11 +310,11 @@ __device__ __forceinline__ void ws_iter(const StepArgs& A, const double* __restr
   }
 }
 
-template <class S, int NW, int MINB, bool FAST>
+template <class S, int NW, int MINB, int NBUF, bool FAST>
 __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntiles) {
   using Sh = WsShape<S>;
   constexpr int T = Sh::T, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN, NT = NW * 32;
-  static_assert(NT * WS_GU >= Sh::W * Sh::W, "window cells per thread");
+  constexpr int GU = (Sh::W * Sh::W + NT - 1) / NT;
   const int tiles2 = A.tiles * A.tiles;
   if (A.active) ntiles = *A.nactive * tiles2;
   auto tile_of = [&](int k) {
@@ -322,8 +324,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
     return A.active[a] * tiles2 + (k - a * tiles2);
   };
   extern __shared__ __align__(128) double sm[];
-  double* sbuf = sm;                           // 2 x [MEQN][W][PW] windows
-  double* up = sbuf + 2 * Sh::QB;              // x-sweep G~ halves (up / dn)
+  double* sbuf = sm;                           // NBUF x [MEQN][W][PW] windows
+  double* up = sbuf + NBUF * Sh::QB;           // x-sweep G~ halves (up / dn)
   double* dn = up + Sh::N_UP;
   double* rt = dn + Sh::N_UP;                  // y-sweep F~ halves (right / left)
   double* lf = rt + Sh::N_RT;
@@ -334,13 +336,17 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
   double cfl = 0.0;
   bool bad = false;
 
-  // pipeline: the window of tile k+1 is gathered while tile k computes, with the ring-table
-  // entries of tile k+2 and the patch metadata of tile k+1 loaded at the same time
-  WsGather g;
+  // NBUF = 2: the window of tile k+1 is gathered while tile k computes, with the ring-table
+  // entries of tile k+2 and the patch metadata of tile k+1 loaded at the same time.  NBUF = 1: the
+  // gather of tile k follows tile k-1's fold (the other CTAs of the SM cover the latency), the
+  // entries of tile k+1 loaded while it is in flight.
+  WsGather<GU> g;
   ws_prep<S>(A, tile_of(blockIdx.x), g, tid, NT);
-  ws_issue<S>(A, g, sbuf, tid, NT);
-  cp_async_commit();
-  ws_prep<S>(A, tile_of(blockIdx.x + gridDim.x), g, tid, NT);
+  if (NBUF == 2) {
+    ws_issue<S>(A, g, sbuf, tid, NT);
+    cp_async_commit();
+    ws_prep<S>(A, tile_of(blockIdx.x + gridDim.x), g, tid, NT);
+  }
   int meta = -1;                               // bcflag | level << 8 of the current tile
   {
     const int t0 = tile_of(blockIdx.x);
@@ -352,15 +358,24 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
   }
   int it = 0;
   for (int kt = blockIdx.x; kt < ntiles; kt += gridDim.x, ++it) {
-    double* sq = sbuf + (it & 1) * Sh::QB;
+    double* sq = sbuf + (NBUF == 2 ? (it & 1) * Sh::QB : 0);
     const int tile = tile_of(kt);
     int patch, tx, ty;
     ws_tile(A, tile, patch, tx, ty);
-    cp_async_wait<0>();
-    __syncthreads();                            // this tile's window is in; the previous tile is done
-    ws_issue<S>(A, g, sbuf + ((it + 1) & 1) * Sh::QB, tid, NT);   // tile k+1 (entries loaded last tile)
-    cp_async_commit();
-    ws_prep<S>(A, tile_of(kt + 2 * gridDim.x), g, tid, NT);        // tile k+2's entries
+    if (NBUF == 2) {
+      cp_async_wait<0>();
+      __syncthreads();                          // this tile's window is in; the previous tile is done
+      ws_issue<S>(A, g, sbuf + ((it + 1) & 1) * Sh::QB, tid, NT);   // tile k+1 (entries loaded last tile)
+      cp_async_commit();
+      ws_prep<S>(A, tile_of(kt + 2 * gridDim.x), g, tid, NT);        // tile k+2's entries
+    } else {
+      __syncthreads();                          // the previous tile's fold is done with the window
+      ws_issue<S>(A, g, sbuf, tid, NT);
+      cp_async_commit();
+      ws_prep<S>(A, tile_of(kt + gridDim.x), g, tid, NT);            // tile k+1's entries
+      cp_async_wait<0>();
+      __syncthreads();
+    }
     const int cur = meta;
     {
       const int tn = tile_of(kt + gridDim.x);
@@ -438,39 +453,58 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
   }
 }
 
-template <class S, int NW, int MINB, bool FAST>
+template <class S, int NW, int MINB, int NBUF, bool FAST>
 static int launch_ws_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
-  const size_t smem = WsShape<S>::smem_bytes;
+  const size_t smem = WsShape<S>::smem_bytes(NBUF);
+  auto kern = k_step_ws<S, NW, MINB, NBUF, FAST>;
   static int resident[64] = {};    // per device: CTAs resident at once (persistent grid)
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return -1;
   if (!resident[dev]) {            // (function attributes are per device)
-    cudaFuncSetAttribute(k_step_ws<S, NW, MINB, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_step_ws<S, NW, MINB, FAST>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_ws<S, NW, MINB, FAST>, NW * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
     resident[dev] = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int64_t ntiles = npatch * a.tiles * a.tiles;
   if (ntiles >= (1ll << 31)) return -1;
   const int64_t grid = ntiles < resident[dev] ? ntiles : resident[dev];
-  k_step_ws<S, NW, MINB, FAST><<<(unsigned)grid, NW * 32, smem, st>>>(a, (int)ntiles);
+  kern<<<(unsigned)grid, NW * 32, smem, st>>>(a, (int)ntiles);
   return 1;
 }
 
-#ifndef WS_MINB
-#define WS_MINB 2
+// warps per CTA, CTAs per SM, window buffers: 24 warp-iterations per tile (both sweeps).
+// Measured (C5 / T3 full update): Euler 6 warps x 2 CTAs (166 registers) 8.45 ms, 8 warps (128:
+// spills) 9.53 ms; SWE 8 warps 5.51 ms vs 5.75 ms with 6
+#ifndef WS_NW_EULER
+#define WS_NW_EULER 6
 #endif
-// warps per CTA: 24 warp-iterations per tile (both sweeps) over 6 or 8 warps; 2 CTAs per SM.
-// Measured (C5 / T3 full update): Euler 6 warps (166 registers) 8.45 ms, 8 warps (128: spills)
-// 9.53 ms; SWE 8 warps 5.51 ms vs 5.75 ms with 6
+#ifndef WS_MINB_EULER
+#define WS_MINB_EULER 2
+#endif
+#ifndef WS_NBUF_EULER
+#define WS_NBUF_EULER 2
+#endif
+#ifndef WS_NW_SWE
+#define WS_NW_SWE 8
+#endif
+#ifndef WS_MINB_SWE
+#define WS_MINB_SWE 2
+#endif
+#ifndef WS_NBUF_SWE
+#define WS_NBUF_SWE 2
+#endif
 template <class S>
 static int launch_ws_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
-  constexpr int NW = std::is_same<S, WsSwe>::value ? 8 : 6;
-  if (a.method2 == 2 && a.method3 == 2) return launch_ws_t<S, NW, WS_MINB, true>(a, npatch, st);
-  return launch_ws_t<S, NW, WS_MINB, false>(a, npatch, st);
+  constexpr bool swe = std::is_same<S, WsSwe>::value;
+  constexpr int NW = swe ? WS_NW_SWE : WS_NW_EULER;
+  constexpr int MINB = swe ? WS_MINB_SWE : WS_MINB_EULER;
+  constexpr int NBUF = swe ? WS_NBUF_SWE : WS_NBUF_EULER;
+  if (a.method2 == 2 && a.method3 == 2) return launch_ws_t<S, NW, MINB, NBUF, true>(a, npatch, st);
+  return launch_ws_t<S, NW, MINB, NBUF, false>(a, npatch, st);
 }
 
 int launch_step_ws(int kind, const StepArgs& a, int64_t npatch, cudaStream_t st) {
