@@ -477,25 +477,28 @@ static int launch_ws_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
 }
 
 // warps per CTA, CTAs per SM, window buffers: 24 warp-iterations per tile (both sweeps).
-// Measured (C5 / T3 full update): Euler 6 warps x 2 CTAs (166 registers) 8.45 ms, 8 warps (128:
-// spills) 9.53 ms; SWE 8 warps 5.51 ms vs 5.75 ms with 6
+// Measured (C5 / T3 full update, ms): Euler 6 warps x 2 CTAs double-buffered (166 registers) 8.45,
+// single-buffered 8.61, 8 warps x 1 CTA (181 registers) 10.0, 4 warps x 3 CTAs single-buffered
+// (168 registers, 70 KB) 7.75; SWE 8 x 2 double-buffered 5.51, single 5.66, 4 x 4 single
+// (128 registers, 52 KB) 4.97.  More, smaller CTAs per SM: a CTA at its barrier or waiting for its
+// window leaves the SM to the others.
 #ifndef WS_NW_EULER
-#define WS_NW_EULER 6
+#define WS_NW_EULER 4
 #endif
 #ifndef WS_MINB_EULER
-#define WS_MINB_EULER 2
+#define WS_MINB_EULER 3
 #endif
 #ifndef WS_NBUF_EULER
-#define WS_NBUF_EULER 2
+#define WS_NBUF_EULER 1
 #endif
 #ifndef WS_NW_SWE
-#define WS_NW_SWE 8
+#define WS_NW_SWE 4
 #endif
 #ifndef WS_MINB_SWE
-#define WS_MINB_SWE 2
+#define WS_MINB_SWE 4
 #endif
 #ifndef WS_NBUF_SWE
-#define WS_NBUF_SWE 2
+#define WS_NBUF_SWE 1
 #endif
 template <class S>
 static int launch_ws_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
