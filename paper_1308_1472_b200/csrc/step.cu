@@ -1897,6 +1897,7 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
   a.active = active;
   a.nactive = nactive;
   a.lim = limiter_coef(limiter);
+  a.limh = {0.5 * a.lim.lo, 0.5 * a.lim.c1, 0.5 * a.lim.c2, 0.5 * a.lim.c3, 0.5 * a.lim.c4};
   a.m = m;
   const int T = (m % 16 == 0) ? 16 : ((m % 8 == 0) ? 8 : ((m % 4 == 0) ? 4 : 2));
   a.tiles = m / T;

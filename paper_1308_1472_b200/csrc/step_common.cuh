@@ -39,6 +39,7 @@ struct StepArgs {
   const int32_t* __restrict__ active; // active-patch list (quiescent patches filtered out) or null
   const int32_t* __restrict__ nactive;
   LimiterCoef lim;
+  LimiterCoef limh;                   // lim with every coefficient halved: phi / 2, exactly
   int m, tiles;                       // tiles per side
   unsigned long long* cfl_bits;
   double* fbuf;                       // method3 = 1 only: per-CTA F~ of each correction edge [MEQN][E2]

@@ -176,6 +176,7 @@ __device__ __forceinline__ void ws_output(const StepArgs& A, int m3, const typen
 #pragma unroll
   for (int k = 0; k < MEQN; ++k) XR[k] = m3 == 1 ? sw[k] - Ed.am[k] : Q[k];
   double bmQ[MEQN], bpQ[MEQN], bmP[MEQN], bpP[MEQN];
+  hr *= 0.5;   // (transverse returns 2 B-X, 2 B+X)
   if (m3 >= 1) {
     S::template transverse<D>(S::roe(Ed), A.sp, XR, bmQ, bpQ);
     S::template transverse<D>(rn, A.sp, XLn, bmP, bpP);
@@ -276,10 +277,12 @@ __device__ __forceinline__ void ws_iter(const StepArgs& A, const double* __restr
           wn2 = fma(Wp[k], Wp[k], wn2);
           dot = fma(WI[k], Wp[k], dot);
         }
-        // a zero wave adds nothing: theta = 0 there keeps the limiter's selects NaN-free
-        const double th = wn2 != 0.0 ? dot * fast_rcp(wn2) : 0.0;
+        // a zero wave adds nothing: theta = 0 there (dot = 0; the 1e-300 changes wn2 only below
+        // 1e-284, i.e. for waves of norm < 1e-142) keeps the limiter's selects NaN-free
+        const double th = dot * fast_rcp(wn2 + 1e-300);
         const double as = fabs(s);
-        const double c = 0.5 * as * (1.0 - as * r) * ws_phi(A.lim, th);
+        // 0.5 |s| (1 - |s| r) phi(theta), the 1/2 carried by the halved limiter coefficients (exact)
+        const double c = as * (1.0 - as * r) * ws_phi(A.limh, th);
 #pragma unroll
         for (int k = 0; k < MEQN; ++k)
           if (S::wave_nz(D, p, k)) F[k] = fma(c, Wp[k], F[k]);

@@ -148,8 +148,12 @@ struct WsEuler {
             __shfl_down_sync(0xffffffffu, r.H, d), __shfl_down_sync(0xffffffffu, r.c, d),
             __shfl_down_sync(0xffffffffu, r.ic, d)};
   }
-  // B-X, B+X of the Roe matrix along the transverse direction of sweep D (EulerRoe::roe_transverse's
-  // formulas; the eigenvalue split as (lambda -+ |lambda|)/2, exact, on the fp64 pipe)
+  // 2 B-X, 2 B+X of the Roe matrix along the transverse direction of sweep D (EulerRoe::
+  // roe_transverse's formulas; the eigenvalue split as lambda -+ |lambda|, i.e. twice its halves,
+  // the caller scaling by 1/2: exact).  With the eigenvectors r1 = (1, vn - c, vt, H - vn c),
+  // r2 = (1, vn, vt, ek), r3 = (0, 0, 1, vt), r4 = (1, vn + c, vt, H + vn c) and weights m_p,
+  // sum_p m_p r_p = (S + m2, vn (S + m2) + D, vt (S + m2) + m3, H S + vn D + ek m2 + vt m3) with
+  // S = m1 + m4, D = c (m4 - m1): the same sum, regrouped.
   template <int D>
   __device__ static void transverse(const Roe& r, const SolverParams& P, const double* X, double* bm, double* bp) {
     constexpr int nd = 3 - D, td = D;
@@ -161,19 +165,16 @@ struct WsEuler {
     const double b1 = X[0] - b2 - b4;
     const double ek = 0.5 * (vn * vn + vt * vt);
     const double l1 = vn - c, l4 = vn + c;
-    const double l1m = 0.5 * (l1 - fabs(l1)), l1p = 0.5 * (l1 + fabs(l1));
-    const double l2m = 0.5 * (vn - fabs(vn)), l2p = 0.5 * (vn + fabs(vn));
-    const double l4m = 0.5 * (l4 - fabs(l4)), l4p = 0.5 * (l4 + fabs(l4));
-    const double m1 = l1m * b1, m2 = l2m * b2, m3 = l2m * b3, m4 = l4m * b4;
-    const double p1 = l1p * b1, p2 = l2p * b2, p3 = l2p * b3, p4 = l4p * b4;
-    bm[0] = m1 + m2 + m4;
-    bm[nd] = m1 * (vn - c) + m2 * vn + m4 * (vn + c);
-    bm[td] = (m1 + m2 + m4) * vt + m3;
-    bm[3] = m1 * (H - vn * c) + m2 * ek + m3 * vt + m4 * (H + vn * c);
-    bp[0] = p1 + p2 + p4;
-    bp[nd] = p1 * (vn - c) + p2 * vn + p4 * (vn + c);
-    bp[td] = (p1 + p2 + p4) * vt + p3;
-    bp[3] = p1 * (H - vn * c) + p2 * ek + p3 * vt + p4 * (H + vn * c);
+    auto set = [&](double w1, double w2, double w4, double* o) {
+      const double m1 = w1 * b1, m2 = w2 * b2, m3 = w2 * b3, m4 = w4 * b4;
+      const double S = m1 + m4, Dd = c * (m4 - m1), o0 = S + m2;
+      o[0] = o0;
+      o[nd] = fma(vn, o0, Dd);
+      o[td] = fma(vt, o0, m3);
+      o[3] = fma(H, S, fma(vn, Dd, fma(ek, m2, vt * m3)));
+    };
+    set(l1 - fabs(l1), vn - fabs(vn), l4 - fabs(l4), bm);
+    set(l1 + fabs(l1), vn + fabs(vn), l4 + fabs(l4), bp);
   }
   __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, double dtdx) {
     return EulerRoe::quiescent_cfl(q, qs, P, nullptr, dtdx, 0, 0, 0, 0);
@@ -253,6 +254,8 @@ struct WsSwe {
     return {__shfl_down_sync(0xffffffffu, r.u, d), __shfl_down_sync(0xffffffffu, r.v, d),
             __shfl_down_sync(0xffffffffu, r.c, d), __shfl_down_sync(0xffffffffu, r.ic, d)};
   }
+  // 2 B-X, 2 B+X (as WsEuler::transverse): sum_p m_p r_p with r1 = (1, vn - c, vt), r2 = (0, 0, 1),
+  // r3 = (1, vn + c, vt) is (S, vn S + c (m3 - m1), vt S + m2), S = m1 + m3
   template <int D>
   __device__ static void transverse(const Roe& r, const SolverParams&, const double* X, double* bm, double* bp) {
     constexpr int nd = 3 - D, td = D;   // eigen-decomposition along the transverse direction
@@ -262,17 +265,15 @@ struct WsSwe {
     const double b2 = X[td] - vt * X[0];
     const double b3 = ((c - vn) * X[0] + X[nd]) * i2c;
     const double l1 = vn - c, l3 = vn + c;
-    const double l1m = 0.5 * (l1 - fabs(l1)), l1p = 0.5 * (l1 + fabs(l1));
-    const double l2m = 0.5 * (vn - fabs(vn)), l2p = 0.5 * (vn + fabs(vn));
-    const double l3m = 0.5 * (l3 - fabs(l3)), l3p = 0.5 * (l3 + fabs(l3));
-    const double m1 = l1m * b1, m2 = l2m * b2, m3 = l3m * b3;
-    const double p1 = l1p * b1, p2 = l2p * b2, p3 = l3p * b3;
-    bm[0] = m1 + m3;
-    bm[nd] = m1 * (vn - c) + m3 * (vn + c);
-    bm[td] = (m1 + m3) * vt + m2;
-    bp[0] = p1 + p3;
-    bp[nd] = p1 * (vn - c) + p3 * (vn + c);
-    bp[td] = (p1 + p3) * vt + p2;
+    auto set = [&](double w1, double w2, double w3, double* o) {
+      const double m1 = w1 * b1, m2 = w2 * b2, m3 = w3 * b3;
+      const double S = m1 + m3;
+      o[0] = S;
+      o[nd] = fma(vn, S, c * (m3 - m1));
+      o[td] = fma(vt, S, m2);
+    };
+    set(l1 - fabs(l1), vn - fabs(vn), l3 - fabs(l3), bm);
+    set(l1 + fabs(l1), vn + fabs(vn), l3 + fabs(l3), bp);
   }
   __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, double dtdx) {
     return SweRoe::quiescent_cfl(q, qs, P, nullptr, dtdx, 0, 0, 0, 0);
