@@ -50,8 +50,9 @@ struct WsShape {
   static constexpr int N_UP = S::MEQN * NR * UPP;
   static constexpr int N_RT = S::MEQN * T * RTP;
   static constexpr int N_DQ = S::MEQN * T * DQP;
+  static constexpr int NDESC = 2 * NIT * 32;                  // lane descriptors of both sweeps (int32)
   static constexpr size_t smem_doubles(int nbuf) {
-    return nbuf * (size_t)QB + 2 * (size_t)N_UP + 2 * (size_t)N_RT + 2 * (size_t)N_DQ;
+    return nbuf * (size_t)QB + 2 * (size_t)N_UP + 2 * (size_t)N_RT + 2 * (size_t)N_DQ + NDESC / 2;
   }
   static constexpr size_t smem_bytes(int nbuf) { return smem_doubles(nbuf) * sizeof(double); }
 };
@@ -224,22 +225,40 @@ __device__ __forceinline__ double ws_phi(const LimiterCoef& L, double th) {
 // One warp-iteration `it` of a sweep (D = 1: x-edges of rows 0..T+1; D = 2: y-edges of columns
 // 0..T+1; NIT iterations per sweep).  FAST: method2 = 2 and method3 = 2 (the configs) known at
 // compile time; otherwise read from A.
+// Lane descriptor of warp-iteration `it` of sweep D (the same for every tile: built once per CTA
+// into shared memory): the right cell's window offset (9 bits), the edge position and line (5 + 5),
+// and the valid / corrected / output flags.
+template <class S, int D>
+__device__ __forceinline__ uint32_t ws_desc(int it, int lane) {
+  using Sh = WsShape<S>;
+  constexpr int T = Sh::T, PW = Sh::PW, NE = Sh::NE, E = Sh::E;
+  const int e = it * Sh::STEP - 1 + lane;                   // flat edge index of this lane
+  const bool ev = (unsigned)e < (unsigned)E;
+  const int ee = ev ? e : 0;
+  const int line = ee / NE, pos = ee - line * NE;         // D=1: row j, edge i; D=2: column i, edge j
+  // the edge between window cells (pos-1, line) and (pos, line) along the sweep (1-based cells)
+  const int wr = D == 1 ? (line + 1) * PW + (pos + 1) : (pos + 1) * PW + (line + 1);   // the right cell
+  const bool corr = ev && lane >= 1 && lane <= 30 && pos >= 1 && pos <= T + 1;
+  const bool out = ev && lane >= 1 && lane <= 29 && pos >= 1 && pos <= T;
+  static_assert((T + 3) * PW < 512 && T + 3 < 32, "descriptor fields");
+  return (uint32_t)wr | (uint32_t)pos << 9 | (uint32_t)line << 14 | (uint32_t)corr << 20 | (uint32_t)out << 21;
+}
+
+// One warp-iteration of a sweep (D = 1: x-edges of rows 0..T+1; D = 2: y-edges of columns
+// 0..T+1; NIT iterations per sweep), its lane's descriptor `dsc`.  FAST: method2 = 2 and
+// method3 = 2 (the configs) known at compile time; otherwise read from A.
 template <class S, int D, bool FAST>
 __device__ __forceinline__ void ws_iter(const StepArgs& A, const double* __restrict__ sq, double* __restrict__ up,
                                         double* __restrict__ dn, double* __restrict__ dq, double r, double& smax,
-                                        int it, int lane) {
+                                        uint32_t dsc, int lane) {
   using Sh = WsShape<S>;
-  constexpr int T = Sh::T, PW = Sh::PW, WPW = Sh::WPW, NE = Sh::NE, E = Sh::E, MEQN = S::MEQN;
+  constexpr int T = Sh::T, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN;
   const double hr = -0.5 * r;
   const bool m2 = FAST || A.method2 == 2;
   const int m3 = FAST ? 2 : A.method3;
   {
-    const int e = it * Sh::STEP - 1 + lane;                 // flat edge index of this lane
-    const bool ev = (unsigned)e < (unsigned)E;
-    const int ee = ev ? e : 0;
-    const int line = ee / NE, pos = ee - line * NE;       // D=1: row j, edge i; D=2: column i, edge j
-    // the edge between window cells (pos-1, line) and (pos, line) along the sweep (1-based cells)
-    const int wr = D == 1 ? (line + 1) * PW + (pos + 1) : (pos + 1) * PW + (line + 1);   // the right cell
+    const int wr = dsc & 511, pos = (dsc >> 9) & 31, line = (dsc >> 14) & 31;
+    const bool corr = (dsc >> 20) & 1, out = (dsc >> 21) & 1;
     const int wl = D == 1 ? wr - 1 : wr - PW;
     typename S::Cell L, R;
 #pragma unroll
@@ -252,7 +271,6 @@ __device__ __forceinline__ void ws_iter(const StepArgs& A, const double* __restr
     typename S::Edge Ed;
     S::template riemann<D>(L, R, A.sp, Ed);
     // CFL of the corrected edges: max over waves of r |s| = r (|un| + c) (the max taken per tile)
-    const bool corr = ev && lane >= 1 && lane <= 30 && pos >= 1 && pos <= T + 1;
     const double ms = S::template max_speed<D>(Ed);
     smax = corr && ms > smax ? ms : smax;
     // corrections: limiter on the upwind neighbour edge's wave of the same family (warp shuffle)
@@ -273,7 +291,7 @@ __device__ __forceinline__ void ws_iter(const StepArgs& A, const double* __restr
 #pragma unroll
         for (int k = 0; k < MEQN; ++k) {
           if (!S::wave_nz(D, p, k)) continue;
-          WI[k] = __shfl_sync(0xffffffffu, Wp[k], src & 31);
+          WI[k] = ws_shfl_idx(Wp[k], src & 31);
           wn2 = fma(Wp[k], Wp[k], wn2);
           dot = fma(WI[k], Wp[k], dot);
         }
@@ -298,17 +316,16 @@ __device__ __forceinline__ void ws_iter(const StepArgs& A, const double* __restr
     // the next edge's L part (and, for the transverse split, its transverse input and Roe state)
     double Pn[MEQN], XLn[MEQN];
 #pragma unroll
-    for (int k = 0; k < MEQN; ++k) Pn[k] = __shfl_down_sync(0xffffffffu, P[k], 1);
+    for (int k = 0; k < MEQN; ++k) Pn[k] = ws_shfl_down(P[k], 1);
     if (m3 == 1) {
 #pragma unroll
-      for (int k = 0; k < MEQN; ++k) XLn[k] = __shfl_down_sync(0xffffffffu, Ed.am[k], 1);
+      for (int k = 0; k < MEQN; ++k) XLn[k] = ws_shfl_down(Ed.am[k], 1);
     } else {
 #pragma unroll
       for (int k = 0; k < MEQN; ++k) XLn[k] = Pn[k];
     }
     const typename S::Roe rn = S::shfl_down(S::roe(Ed), 1);
     // this lane's output cell: the right cell of its edge, (pos, line)
-    const bool out = ev && lane >= 1 && lane <= 29 && pos >= 1 && pos <= T;
     if (out) ws_output<S, D>(A, m3, Ed, P, Q, sw, Pn, XLn, rn, up, dn, dq, r, hr, pos, line);
   }
 }
@@ -334,8 +351,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
   double* lf = rt + Sh::N_RT;
   double* dq = lf + Sh::N_RT;                  // x increments
   double* dqy = dq + Sh::N_DQ;                 // y increments
+  uint32_t* desc = reinterpret_cast<uint32_t*>(dqy + Sh::N_DQ);   // [2 NIT][32] lane descriptors
   __shared__ double wmax[NW];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int t = tid; t < Sh::NDESC; t += NT) {   // (read after the first tile's barrier)
+    const int v = t >> 5, l = t & 31;
+    desc[t] = v < Sh::NIT ? ws_desc<S, 1>(v, l) : ws_desc<S, 2>(v - Sh::NIT, l);
+  }
   double cfl = 0.0;
   bool bad = false;
 
@@ -415,8 +437,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
     // both sweeps read Q^n only (unsplit): their 2 NIT warp-iterations are one phase
     double smax = 0.0;
     for (int v = warp; v < 2 * Sh::NIT; v += NW) {
-      if (v < Sh::NIT) ws_iter<S, 1, FAST>(A, sq, up, dn, dq, r, smax, v, lane);
-      else ws_iter<S, 2, FAST>(A, sq, rt, lf, dqy, r, smax, v - Sh::NIT, lane);
+      const uint32_t d = desc[v * 32 + lane];
+      if (v < Sh::NIT) ws_iter<S, 1, FAST>(A, sq, up, dn, dq, r, smax, d, lane);
+      else ws_iter<S, 2, FAST>(A, sq, rt, lf, dqy, r, smax, d, lane);
     }
     cfl = fmax(cfl, r * smax);
     __syncthreads();

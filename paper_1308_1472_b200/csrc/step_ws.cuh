@@ -8,6 +8,28 @@
 
 namespace fc {
 
+// full-warp shuffles of a double as one non-volatile PTX block (the two 32-bit halves of the
+// register pair; the header's versions split and rejoin through volatile movs, which cost real
+// moves in the sweep loop).  Every caller runs with the whole warp converged.
+__device__ __forceinline__ double ws_shfl_idx(double x, int src) {
+  double y;
+  asm("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\t"
+      "shfl.sync.idx.b32 lo, lo, %2, 0x1f, 0xffffffff;\n\t"
+      "shfl.sync.idx.b32 hi, hi, %2, 0x1f, 0xffffffff;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "=d"(y) : "d"(x), "r"(src));
+  return y;
+}
+__device__ __forceinline__ double ws_shfl_down(double x, int d) {
+  double y;
+  asm("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\t"
+      "shfl.sync.down.b32 lo, lo, %2, 0x1f, 0xffffffff;\n\t"
+      "shfl.sync.down.b32 hi, hi, %2, 0x1f, 0xffffffff;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "=d"(y) : "d"(x), "r"(d));
+  return y;
+}
+
 // ------------------------------------------------------------------------------------------------
 // register-resident views of the solvers (the same formulas as solvers.cuh / SURVEY §8(c.5))
 struct WsEuler {
@@ -144,9 +166,8 @@ struct WsEuler {
   };
   __device__ static Roe roe(const Edge& E) { return {E.u, E.v, E.H, E.c, E.ic}; }
   __device__ static Roe shfl_down(const Roe& r, int d) {
-    return {__shfl_down_sync(0xffffffffu, r.u, d), __shfl_down_sync(0xffffffffu, r.v, d),
-            __shfl_down_sync(0xffffffffu, r.H, d), __shfl_down_sync(0xffffffffu, r.c, d),
-            __shfl_down_sync(0xffffffffu, r.ic, d)};
+    return {ws_shfl_down(r.u, d), ws_shfl_down(r.v, d), ws_shfl_down(r.H, d), ws_shfl_down(r.c, d),
+            ws_shfl_down(r.ic, d)};
   }
   // 2 B-X, 2 B+X of the Roe matrix along the transverse direction of sweep D (EulerRoe::
   // roe_transverse's formulas; the eigenvalue split as lambda -+ |lambda|, i.e. twice its halves,
@@ -251,8 +272,7 @@ struct WsSwe {
   };
   __device__ static Roe roe(const Edge& E) { return {E.u, E.v, E.c, E.ic}; }
   __device__ static Roe shfl_down(const Roe& r, int d) {
-    return {__shfl_down_sync(0xffffffffu, r.u, d), __shfl_down_sync(0xffffffffu, r.v, d),
-            __shfl_down_sync(0xffffffffu, r.c, d), __shfl_down_sync(0xffffffffu, r.ic, d)};
+    return {ws_shfl_down(r.u, d), ws_shfl_down(r.v, d), ws_shfl_down(r.c, d), ws_shfl_down(r.ic, d)};
   }
   // 2 B-X, 2 B+X (as WsEuler::transverse): sum_p m_p r_p with r1 = (1, vn - c, vt), r2 = (0, 0, 1),
   // r3 = (1, vn + c, vt) is (S, vn S + c (m3 - m1), vt S + m2), S = m1 + m3
