@@ -30,7 +30,8 @@ int launch_gather(const double* q, double* dst, int64_t P, int meqn, int m, cuda
 int launch_unpack_padded(const double* q, double* dst, int64_t nblocks, int n, cudaStream_t st);
 int launch_step(int kind, const double* qold, double* qnew, const double* aux, const int8_t* level,
                 int64_t npatch, int m, double dt, double dx0, double p0, double p1, int limiter,
-                int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
+                int method2, int method3, int skip_quiescent, const int32_t* ring, const int32_t* nb9,
+                const uint8_t* bcflag,
                 const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits,
                 const int32_t* rslot, double* freg, const uint8_t* rpeer, const double* const* peerq,
                 const double* cg, cudaStream_t st);
@@ -117,6 +118,7 @@ struct fc_forest {
   // fused ring gather (uniform same-level forests, one tile per patch): ring never written
   bool fused = false;
   int32_t* d_ring = nullptr;
+  int32_t* d_nb9 = nullptr;   // regular rings: per local patch the 9 neighbour block offsets (plan_ring_regular)
   uint8_t* d_bcflag = nullptr;
   // quiescent-patch filter (fused path): neighbour table, wall mask, flags, states, active list
   int32_t *d_nbr = nullptr, *d_active = nullptr, *d_nactive = nullptr;
@@ -505,7 +507,7 @@ static int update_local(fc_forest* f, double dt, int part = 0) {
     if ((part == 1 ? f->n_int : f->n_bnd) == 0) return FC_OK;
     std::array<const double*, 16> pq{};
     int lr = launch_step(p.kind, f->qold, f->qnew, f->aux, f->d_level, f->Pl, f->pl.m, dt, f->pl.dx0, p.p0, p.p1,
-                         p.limiter, p.method2, p.method3, p.skip_quiescent, f->d_ring, f->d_bcflag, lst, cnt,
+                         p.limiter, p.method2, p.method3, p.skip_quiescent, f->d_ring, f->d_nb9, f->d_bcflag, lst, cnt,
                          f->d_cfl, nullptr, nullptr, nullptr, pq.data(), f->d_cg, f->stream);
     if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
     f->st.kernel_launches += lr;
@@ -553,7 +555,7 @@ static int update_local(fc_forest* f, double dt, int part = 0) {
   }
   int lr = launch_step(p.kind, f->qold, f->qnew, f->aux, f->d_level, f->Pl, f->pl.m, dt, f->pl.dx0,
                        p.p0, p.p1, p.limiter, p.method2, p.method3, filtered ? 0 : p.skip_quiescent,
-                       fused ? f->d_ring : nullptr, f->d_bcflag, filtered ? f->d_active : nullptr,
+                       fused ? f->d_ring : nullptr, f->d_nb9, f->d_bcflag, filtered ? f->d_active : nullptr,
                        filtered ? f->d_nactive : nullptr, f->d_cfl, records ? f->d_rslot : nullptr,
                        records ? f->d_freg : nullptr, (fused && (f->p2p || f->amr_fused)) ? f->d_rpeer : nullptr,
                        peerq.data(), f->d_cg, f->stream);
@@ -605,7 +607,7 @@ static void destroy(fc_forest* f) {
     cudaSetDevice(f->device);
     if (f->stream) cudaStreamSynchronize(f->stream);
     cudaFree(f->qold); cudaFree(f->qnew); cudaFree(f->aux); cudaFree(f->d_level); cudaFree(f->d_cfl);
-    cudaFree(f->d_ring); cudaFree(f->d_bcflag);
+    cudaFree(f->d_ring); cudaFree(f->d_nb9); cudaFree(f->d_bcflag);
     cudaFree(f->d_nbr); cudaFree(f->d_active); cudaFree(f->d_nactive); cudaFree(f->d_negmask);
     cudaFree(f->d_uflag); cudaFree(f->d_uval);
     cudaFree(f->d_rslot); cudaFree(f->d_rcells); cudaFree(f->d_freg);
@@ -647,6 +649,24 @@ static void destroy(fc_forest* f) {
     if (f->own_stream) cudaStreamDestroy(f->own_stream);
   }
   delete f;
+}
+
+// regular-ring neighbour offsets of the fused gather (plan_ring_regular; FC_REGULAR_RING=0: off)
+static int upload_regular(fc_forest* f, const RingSources& rs) {
+  const char* env = getenv("FC_REGULAR_RING");
+  if (env && atoi(env) == 0) return FC_OK;
+  std::vector<int32_t> nb9;
+  const int64_t nreg = plan_ring_regular(f->pl, f->pl.meqn, rs, nb9);
+  f->st.regular_patches = nreg;
+  if (nreg == 0) return FC_OK;
+  cudaError_t e = cudaMalloc(&f->d_nb9, nb9.size() * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemcpy(f->d_nb9, nb9.data(), nb9.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    std::string m = std::string("regular ring table: ") + cudaGetErrorString(e);
+    destroy(f);
+    return fail(FC_ECUDA, m);
+  }
+  return FC_OK;
 }
 
 // accumulate the pending fc_step timing events into the stats and recycle them
@@ -867,6 +887,7 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
         return cuda_fail(e, "cudaMalloc filter");
       cudaMemcpy(f->d_nbr, rs.nbr.data(), rs.nbr.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
       cudaMemcpy(f->d_negmask, rs.negmask.data(), rs.negmask.size(), cudaMemcpyHostToDevice);
+      if ((rc = upload_regular(f, rs))) return rc;
       f->fused = true;
       f->st.uniform_fast_path = 1;
       if (pl.nranks > 1 && !f->p2p) {   // halo overlap: interior / boundary patch lists
@@ -919,6 +940,7 @@ int fc_forest_create(const fc_forest_desc* d, fc_forest** out) {
         f->cg_interp.resize(ra.interp.size());
         for (size_t l = 0; l < ra.interp.size(); ++l)
           if ((rc = to_dev(f, ra.interp[l], 8, f->cg_interp[l]))) { destroy(f); return fail(rc, g_err); }
+        if ((rc = upload_regular(f, rs))) return rc;
         f->fused = true;
         f->amr_fused = true;
         f->st.uniform_fast_path = 2;
@@ -1481,7 +1503,7 @@ static int sub_advance(fc_forest* f, int l, int64_t tick, int sub) {
   if (f->n_lvl[li] > 0) {
     int lr = launch_step(p.kind, src, f->qnew, f->aux, f->d_level, f->n_lvl[li], m, dt, f->pl.dx0, p.p0,
                          p.p1, p.limiter, p.method2, p.method3, p.skip_quiescent, fused ? f->d_ring : nullptr,
-                         f->d_bcflag, f->d_lvl[li], f->d_lvl_cnt + li, f->d_cfl, reflux ? f->d_rslot : nullptr,
+                         f->d_nb9, f->d_bcflag, f->d_lvl[li], f->d_lvl_cnt + li, f->d_cfl, reflux ? f->d_rslot : nullptr,
                          reflux ? f->d_freg : nullptr, fused ? f->d_rpeer : nullptr, nullptr,
                          fused ? f->d_cg : nullptr, f->stream);
     if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");

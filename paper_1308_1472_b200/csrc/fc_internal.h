@@ -145,6 +145,13 @@ struct RingAmr {
   int64_t ncg_patches = 0;                   // computed-ghost buffer size in n^2-cell virtual patches
 };
 int plan_ring_amr(const Plan& pl, int meqn, RingSources& rs, RingAmr& ra, std::string& err);
+// Regular rings: a local patch whose every ring cell is a COPY of the aligned cell of one of its 8
+// same-level neighbours (local, no wall / outflow cell) gets nb9[lp][3 (dy + 1) + dx + 1] = the
+// block offset (patch * meqn n^2) of the neighbour in direction (dx, dy) (its own at the centre):
+// the step kernels then compute every source address instead of loading it from rs.src.  Checked
+// entry by entry against rs.src (the same source cells, bitwise the same gather); -1 at [lp][0]:
+// use the table.  Returns the number of regular patches.
+int64_t plan_ring_regular(const Plan& pl, int meqn, const RingSources& rs, std::vector<int32_t>& nb9);
 // activity tables for the quiescent filter on any forest: nbr [Pl][8] / negmask [Pl] as in
 // RingSources; a patch with an AVG4 / INTERP / CORNER3 ghost record is always active (nbr[0] = -2)
 int plan_activity(const Plan& pl, int meqn, std::vector<int32_t>& nbr, std::vector<uint8_t>& negmask,

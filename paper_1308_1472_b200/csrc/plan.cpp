@@ -612,6 +612,41 @@ int plan_ring_sources(const Plan& pl, int meqn, RingSources& rs, std::string& er
   return FC_OK;
 }
 
+int64_t plan_ring_regular(const Plan& pl, int meqn, const RingSources& rs, std::vector<int32_t>& nb9) {
+  const int m = pl.m, n = pl.n;
+  const int64_t S = (int64_t)meqn * n * n, Pl = pl.p1 - pl.p0, G = (int64_t)n * n - (int64_t)m * m;
+  nb9.assign((size_t)std::max<int64_t>(1, Pl) * 9, -1);
+  int64_t count = 0;
+  for (int64_t lp = 0; lp < Pl; ++lp) {
+    const int32_t* src = rs.src.data() + lp * G;
+    const uint8_t* peer = rs.peer.empty() ? nullptr : rs.peer.data() + lp * G;
+    if (!rs.bcflag.empty() && rs.bcflag[lp]) continue;
+    int64_t off[9];
+    bool ok = true;
+    for (int d = 0; d < 9 && ok; ++d) {   // the neighbour from one representative ring cell
+      const int dx = d % 3 - 1, dy = d / 3 - 1;
+      if (d == 4) { off[d] = lp * S; continue; }
+      const int i = dx < 0 ? 0 : (dx > 0 ? m + 1 : 1), j = dy < 0 ? 0 : (dy > 0 ? m + 1 : 1);
+      const int32_t v = src[ring_index(i, j, m)];
+      if (v < 0) { ok = false; break; }
+      off[d] = v - (v % S);
+      if (off[d] / S >= Pl) ok = false;   // (a halo slot, not a local patch)
+    }
+    for (int j = -1; j <= m + 2 && ok; ++j)
+      for (int i = -1; i <= m + 2 && ok; ++i) {
+        if (i >= 1 && i <= m && j >= 1 && j <= m) continue;
+        const int dx = i < 1 ? -1 : (i > m ? 1 : 0), dy = j < 1 ? -1 : (j > m ? 1 : 0);
+        const int r = ring_index(i, j, m);
+        const int64_t want = off[3 * (dy + 1) + dx + 1] + (int64_t)(j - dy * m - 1) * m + (i - dx * m - 1);
+        if (src[r] != want || (peer && peer[r] != 0)) ok = false;
+      }
+    if (!ok) continue;
+    for (int d = 0; d < 9; ++d) nb9[lp * 9 + d] = (int32_t)off[d];
+    ++count;
+  }
+  return count;
+}
+
 // Fused two-hop ring gather for AMR forests (one rank, one tile per patch).  The
 // rings are never written: COPY ring cells are gathered by the step kernel straight from their
 // source cells; AVG4 and INTERP ring cells get a slot in a "computed ghost" buffer (virtual patches

@@ -1031,17 +1031,21 @@ __device__ CV_STAGE_INLINE void cv_stage(const StepArgs& A, double* buf, uint64_
   }
   constexpr int NR = (G + 31) / 32;
   int pt[PW];
+  bool rg[PW];                             // regular ring (plan_ring_regular): computed sources
   int32_t src[PW][NR];
   uint8_t own[PW][NR];
   const bool peers = A.rpeer != nullptr;   // (uniform: only peer-memory / AMR forests carry owners)
 #pragma unroll
-  for (int q = 0; q < PW; ++q) pt[q] = q < cnt ? patch_of(i0 + q) : -1;
+  for (int q = 0; q < PW; ++q) {
+    pt[q] = q < cnt ? patch_of(i0 + q) : -1;
+    rg[q] = pt[q] >= 0 && A.nb9 && __ldg(A.nb9 + (int64_t)pt[q] * 9) >= 0;
+  }
 #pragma unroll
   for (int q = 0; q < PW; ++q)
 #pragma unroll
     for (int t = 0; t < NR; ++t) {
       const int r = lane + 32 * t;
-      const bool ok = pt[q] >= 0 && r < G;
+      const bool ok = pt[q] >= 0 && !rg[q] && r < G;
       src[q][t] = ok ? __ldg(A.ring + (int64_t)pt[q] * G + r) : -1;
       own[q][t] = (ok && peers) ? __ldg(A.rpeer + (int64_t)pt[q] * G + r) : 0;
     }
@@ -1057,6 +1061,28 @@ __device__ CV_STAGE_INLINE void cv_stage(const StepArgs& A, double* buf, uint64_
     for (int c = lane; c < CH; c += 32) {
       const int row = c / (T / 2), cp = c - row * (T / 2);
       cp_async16(b + (row + 2) * W + 2 + 2 * cp, qi + row * T + 2 * cp);
+    }
+    if (rg[q]) {
+      // the ring as 16-byte pairs: rows -1, 0, T+1, T+2 whole (W / 2 pairs each), then the two side
+      // pairs of rows 1..T; every pair lies in one neighbour's interior row (m even: aligned)
+      const int32_t* nb = A.nb9 + (int64_t)pt[q] * 9;
+      constexpr int RCH = 2 * W + 2 * T;
+#pragma unroll
+      for (int c = lane; c < RCH; c += 32) {
+        int wi, wj;
+        if (c < 2 * W) {
+          const int rr = c / (W / 2);
+          wj = rr < 2 ? rr : T + rr;
+          wi = 2 * (c - rr * (W / 2));
+        } else {
+          wj = 2 + ((c - 2 * W) >> 1);
+          wi = (c & 1) ? T + 2 : 0;
+        }
+        const int i = wi - 1, j = wj - 1;   // patch cell (1-based interior)
+        const int dx = i < 1 ? -1 : (i > T ? 1 : 0), dy = j < 1 ? -1 : (j > T ? 1 : 0);
+        cp_async16(b + wj * W + wi, A.qold + __ldg(nb + 3 * dy + dx + 4) + (j - dy * T - 1) * T + (i - dx * T - 1));
+      }
+      continue;
     }
 #pragma unroll
     for (int t = 0; t < NR; ++t) {
@@ -1877,7 +1903,8 @@ static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
 
 int launch_step(int kind, const double* qold, double* qnew, const double* aux, const int8_t* level,
                 int64_t npatch, int m, double dt, double dx0, double p0, double p1, int limiter,
-                int method2, int method3, int skip_quiescent, const int32_t* ring, const uint8_t* bcflag,
+                int method2, int method3, int skip_quiescent, const int32_t* ring, const int32_t* nb9,
+                const uint8_t* bcflag,
                 const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits,
                 const int32_t* rslot, double* freg, const uint8_t* rpeer, const double* const* peerq,
                 const double* cg, cudaStream_t st) {
@@ -1893,6 +1920,7 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
   a.limiter = limiter; a.method2 = method2; a.method3 = method3;
   a.skip_quiescent = skip_quiescent;
   a.ring = ring;
+  a.nb9 = ring ? nb9 : nullptr;
   a.bcflag = bcflag;
   a.active = active;
   a.nactive = nactive;

@@ -35,6 +35,7 @@ struct StepArgs {
   int limiter, method2, method3;
   int skip_quiescent;                 // exact shortcut for tiles whose staged window is uniform
   const int32_t* __restrict__ ring;   // fused ring gather (RingSources.src) or null: ring in q_old
+  const int32_t* __restrict__ nb9;    // regular rings (plan_ring_regular): [P][9] neighbour block offsets, [p][0] < 0: table
   const uint8_t* __restrict__ bcflag; // per patch: bit 0 BCX, bit 1 BCY entries present
   const int32_t* __restrict__ active; // active-patch list (quiescent patches filtered out) or null
   const int32_t* __restrict__ nactive;

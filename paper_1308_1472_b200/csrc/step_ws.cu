@@ -92,6 +92,9 @@ __device__ __forceinline__ void ws_prep(const StepArgs& A, int tile, WsGather<WS
   const int m = A.m, n = m + 4, G = n * n - m * m;
   const int32_t* rs = A.ring + (int64_t)patch * G;
   const uint8_t* rp = A.rpeer ? A.rpeer + (int64_t)patch * G : nullptr;
+  // regular ring: every source address from the 9 neighbour block offsets (L1-resident), no table
+  const int32_t* nb = A.nb9 ? A.nb9 + (int64_t)patch * 9 : nullptr;
+  const bool reg = nb && __ldg(nb) >= 0;
 #pragma unroll
   for (int u = 0; u < WS_GU; ++u) {
     const int c = tid + u * nt;
@@ -101,6 +104,11 @@ __device__ __forceinline__ void ws_prep(const StepArgs& A, int tile, WsGather<WS
     const int wj = c / W, wi = c - wj * W;
     const int i = tx * T + wi - 1, j = ty * T + wj - 1;   // patch cell (1-based interior)
     if ((unsigned)(i - 1) < (unsigned)m && (unsigned)(j - 1) < (unsigned)m) continue;
+    if (reg) {
+      const int dx = i < 1 ? -1 : (i > m ? 1 : 0), dy = j < 1 ? -1 : (j > m ? 1 : 0);
+      g.v[u] = __ldg(nb + 3 * dy + dx + 4) + (j - dy * m - 1) * m + (i - dx * m - 1);
+      continue;
+    }
     const int r = ring_index(i, j, m);
     g.v[u] = __ldg(rs + r);
     if (rp) g.ow[u] = __ldg(rp + r);
