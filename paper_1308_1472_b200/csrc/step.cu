@@ -1001,8 +1001,31 @@ struct CvShape {
 #ifndef CV_STAGE_INLINE
 #define CV_STAGE_INLINE __forceinline__
 #endif
+// regular-ring neighbour offsets of a group of PW patches (plan_ring_regular): entry q 9 + d in
+// lane (q 9 + d) mod 32 of lo (< 32) or hi; -1 for a patch that reads the ring table.  Loaded a
+// group ahead of its staging (the loads complete under the current group's sweep).
+struct CvNb {
+  int32_t lo, hi;
+};
 template <int T>
-__device__ CV_STAGE_INLINE void cv_stage(const StepArgs& A, double* buf, uint64_t* bar, int lane, int i0, int cnt) {
+__device__ __forceinline__ CvNb cv_nb_load(const StepArgs& A, int i0, int cnt, int lane) {
+  constexpr int PW = CvShape<T>::PW;
+  CvNb r{-1, -1};
+  if (!A.nb9 || cnt <= 0) return r;
+  auto entry = [&](int e) {
+    const int q = e / 9;
+    if (q >= cnt || q >= PW) return -1;
+    const int patch = A.active ? A.active[i0 + q] : i0 + q;
+    return __ldg(A.nb9 + (int64_t)patch * 9 + (e - 9 * q));
+  };
+  r.lo = entry(lane);
+  if (PW * 9 > 32) r.hi = entry(lane + 32);
+  return r;
+}
+
+template <int T>
+__device__ CV_STAGE_INLINE void cv_stage(const StepArgs& A, double* buf, uint64_t* bar, int lane, int i0, int cnt,
+                                         const CvNb& nbv) {
   using C = CvShape<T>;
   constexpr int W = C::W, WW = C::WW, PW = C::PW, G = WW - T * T;
   const bool ring = A.ring != nullptr;
@@ -1029,17 +1052,49 @@ __device__ CV_STAGE_INLINE void cv_stage(const StepArgs& A, double* buf, uint64_
     cp_async_commit();
     return;
   }
+  // the neighbour offset of entry e = q 9 + d from the prefetched registers
+  auto nb_of = [&](int e) {
+    const int lo = __shfl_sync(0xffffffffu, nbv.lo, e & 31);
+    if (PW * 9 <= 32) return lo;
+    const int hi = __shfl_sync(0xffffffffu, nbv.hi, e & 31);
+    return e < 32 ? lo : hi;
+  };
+  // the ring as 16-byte pairs (regular patches): rows -1, 0, T+1, T+2 whole (W / 2 pairs each),
+  // then the two side pairs of rows 1..T; every pair lies in one neighbour's interior row (m even:
+  // aligned).  Per lane: the window offset, the direction and the offset within the neighbour of
+  // its pairs, the same for every patch.
+  constexpr int RCH = 2 * W + 2 * T, RU = (RCH + 31) / 32;
+  int rdst[RU], rdir[RU], rsrc[RU];
+#pragma unroll
+  for (int u = 0; u < RU; ++u) {
+    const int c = lane + 32 * u;
+    int wi, wj;
+    if (c < 2 * W) {
+      const int rr = c / (W / 2);
+      wj = rr < 2 ? rr : T + rr;
+      wi = 2 * (c - rr * (W / 2));
+    } else {
+      wj = 2 + ((c - 2 * W) >> 1);
+      wi = (c & 1) ? T + 2 : 0;
+    }
+    const int i = wi - 1, j = wj - 1;   // patch cell (1-based interior)
+    const int dx = i < 1 ? -1 : (i > T ? 1 : 0), dy = j < 1 ? -1 : (j > T ? 1 : 0);
+    rdst[u] = c < RCH ? wj * W + wi : -1;
+    rdir[u] = 3 * dy + dx + 4;
+    rsrc[u] = (j - dy * T - 1) * T + (i - dx * T - 1);
+  }
   constexpr int NR = (G + 31) / 32;
   int pt[PW];
-  bool rg[PW];                             // regular ring (plan_ring_regular): computed sources
+  bool rg[PW];                             // (warp-uniform)
   int32_t src[PW][NR];
   uint8_t own[PW][NR];
   const bool peers = A.rpeer != nullptr;   // (uniform: only peer-memory / AMR forests carry owners)
 #pragma unroll
   for (int q = 0; q < PW; ++q) {
     pt[q] = q < cnt ? patch_of(i0 + q) : -1;
-    rg[q] = pt[q] >= 0 && A.nb9 && __ldg(A.nb9 + (int64_t)pt[q] * 9) >= 0;
+    rg[q] = pt[q] >= 0 && nb_of(9 * q) >= 0;
   }
+  // the other patches' ring-table entries, all loaded first: one latency, not one per patch
 #pragma unroll
   for (int q = 0; q < PW; ++q)
 #pragma unroll
@@ -1063,24 +1118,10 @@ __device__ CV_STAGE_INLINE void cv_stage(const StepArgs& A, double* buf, uint64_
       cp_async16(b + (row + 2) * W + 2 + 2 * cp, qi + row * T + 2 * cp);
     }
     if (rg[q]) {
-      // the ring as 16-byte pairs: rows -1, 0, T+1, T+2 whole (W / 2 pairs each), then the two side
-      // pairs of rows 1..T; every pair lies in one neighbour's interior row (m even: aligned)
-      const int32_t* nb = A.nb9 + (int64_t)pt[q] * 9;
-      constexpr int RCH = 2 * W + 2 * T;
 #pragma unroll
-      for (int c = lane; c < RCH; c += 32) {
-        int wi, wj;
-        if (c < 2 * W) {
-          const int rr = c / (W / 2);
-          wj = rr < 2 ? rr : T + rr;
-          wi = 2 * (c - rr * (W / 2));
-        } else {
-          wj = 2 + ((c - 2 * W) >> 1);
-          wi = (c & 1) ? T + 2 : 0;
-        }
-        const int i = wi - 1, j = wj - 1;   // patch cell (1-based interior)
-        const int dx = i < 1 ? -1 : (i > T ? 1 : 0), dy = j < 1 ? -1 : (j > T ? 1 : 0);
-        cp_async16(b + wj * W + wi, A.qold + __ldg(nb + 3 * dy + dx + 4) + (j - dy * T - 1) * T + (i - dx * T - 1));
+      for (int u = 0; u < RU; ++u) {
+        const int off = nb_of(9 * q + rdir[u]);
+        if (rdst[u] >= 0) cp_async16(b + rdst[u], A.qold + off + rsrc[u]);
       }
       continue;
     }
@@ -1132,7 +1173,10 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
   const int ngroups = (npatch + PW - 1) / PW;
   const bool ring = A.ring != nullptr;
   auto patch_of = [&](int idx) { return A.active ? A.active[idx] : idx; };
-  auto stage = [&](int g, int s) { cv_stage<T>(A, sm + (size_t)s * PW * WW, &bars[s], lane, g * PW, min(PW, npatch - g * PW)); };
+  auto nbload = [&](int g) { return g < ngroups ? cv_nb_load<T>(A, g * PW, min(PW, npatch - g * PW), lane) : CvNb{-1, -1}; };
+  auto stage = [&](int g, int s, const CvNb& nb) {
+    cv_stage<T>(A, sm + (size_t)s * PW * WW, &bars[s], lane, g * PW, min(PW, npatch - g * PW), nb);
+  };
   if (lane == 0) {
     for (int q = 0; q < NB; ++q) mbar_init(&bars[q], 1);
     fence_proxy_async();
@@ -1140,7 +1184,7 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
   __syncwarp();
   for (int q = 0; q < (NB > 1 ? NB - 1 : 1); ++q) {
     const int g = blockIdx.x + q * gridDim.x;
-    if (g < ngroups) stage(g, q);
+    if (g < ngroups) stage(g, q, nbload(g));
     else cp_async_commit();
   }
   // lane -> (patch slot, columns c0 = 2k, c0 + 1); the 5 columns it reads: c0 - 1 .. c0 + 3 (the
@@ -1173,6 +1217,8 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
     const int mylevel = A.level[mypatch];
     const int myslot = RF ? A.rslot[mypatch] : -1;
     const int mybc = (ring && lane < cnt) ? A.bcflag[mypatch] : 0;
+    // the next staged group's regular-ring offsets (in flight during this group's sweep)
+    const CvNb nbn = ring ? nbload(g + (NB > 1 ? NB - 1 : 1) * gridDim.x) : CvNb{-1, -1};
     mbar_wait(&bars[b], (uint32_t)((it / NB) & 1));
     cp_async_wait<(NB > 1 ? NB - 2 : 0)>();
     __syncwarp();
@@ -1181,7 +1227,7 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
       const int gn = g + (NB > 1 ? NB - 1 : 1) * gridDim.x, bn = (it + NB - 1) % NB;
       if (gn < ngroups) {
         fence_proxy_async();
-        stage(gn, bn);
+        stage(gn, bn, nbn);
       } else {
         cp_async_commit();
       }
@@ -1351,7 +1397,10 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
   if (A.active) npatch = *A.nactive;
   const int ngroups = (npatch + PW - 1) / PW;
   auto patch_of = [&](int idx) { return A.active ? A.active[idx] : idx; };
-  auto stage = [&](int g, int s) { cv_stage<T>(A, sm + (size_t)s * PW * WW, &bars[s], lane, g * PW, min(PW, npatch - g * PW)); };
+  auto nbload = [&](int g) { return g < ngroups ? cv_nb_load<T>(A, g * PW, min(PW, npatch - g * PW), lane) : CvNb{-1, -1}; };
+  auto stage = [&](int g, int s, const CvNb& nb) {
+    cv_stage<T>(A, sm + (size_t)s * PW * WW, &bars[s], lane, g * PW, min(PW, npatch - g * PW), nb);
+  };
   if (lane == 0) {
     for (int q = 0; q < NB; ++q) mbar_init(&bars[q], 1);
     fence_proxy_async();
@@ -1359,7 +1408,7 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
   __syncwarp();
   for (int q = 0; q < (NB > 1 ? NB - 1 : 1); ++q) {
     const int g = blockIdx.x + q * gridDim.x;
-    if (g < ngroups) stage(g, q);
+    if (g < ngroups) stage(g, q, nbload(g));
     else cp_async_commit();
   }
   const int p = lane / LP, k = lane - p * LP, c0 = 2 * k;
@@ -1381,6 +1430,7 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
     const int mypatch = lane < cnt ? patch_of(g * PW + lane) : 0;
     const int mylevel = A.level[mypatch];
     const int mybc = (A.ring && lane < cnt) ? A.bcflag[mypatch] : 0;
+    const CvNb nbn = A.ring ? nbload(g + (NB > 1 ? NB - 1 : 1) * gridDim.x) : CvNb{-1, -1};
     mbar_wait(&bars[b], (uint32_t)((it / NB) & 1));
     cp_async_wait<(NB > 1 ? NB - 2 : 0)>();
     __syncwarp();
@@ -1388,7 +1438,7 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
       const int gn = g + (NB > 1 ? NB - 1 : 1) * gridDim.x, bn = (it + NB - 1) % NB;
       if (gn < ngroups) {
         fence_proxy_async();
-        stage(gn, bn);
+        stage(gn, bn, nbn);
       } else {
         cp_async_commit();
       }

@@ -92,8 +92,13 @@ __device__ __forceinline__ void ws_prep(const StepArgs& A, int tile, WsGather<WS
   const int m = A.m, n = m + 4, G = n * n - m * m;
   const int32_t* rs = A.ring + (int64_t)patch * G;
   const uint8_t* rp = A.rpeer ? A.rpeer + (int64_t)patch * G : nullptr;
-  // regular ring: every source address from the 9 neighbour block offsets (L1-resident), no table
-  const int32_t* nb = A.nb9 ? A.nb9 + (int64_t)patch * 9 : nullptr;
+  // regular ring: every source address from the 9 neighbour block offsets (L1-resident), no table.
+  // Off by default here (WS_REGULAR): the systems kernel is compute-bound and the extra address
+  // arithmetic measured +1.5 % on C5 (7.63 vs 7.52 ms); the scalar sweeps use it (cv_stage).
+#ifndef WS_REGULAR
+#define WS_REGULAR 0
+#endif
+  const int32_t* nb = (WS_REGULAR && A.nb9) ? A.nb9 + (int64_t)patch * 9 : nullptr;
   const bool reg = nb && __ldg(nb) >= 0;
 #pragma unroll
   for (int u = 0; u < WS_GU; ++u) {
