@@ -130,9 +130,11 @@ typedef struct {
   int32_t pad_;
   double ms_copy;               /* accumulated device time in the quiescent copy/classify kernel (part of ms_step) */
   int64_t copy_launches;        /* launches counted in ms_copy */
-  int64_t regular_patches;      /* local patches whose fused ring gather computes its source
-                                   addresses (every ring cell a copy of the aligned cell of a
-                                   same-level local neighbour); the others read the ring table */
+  int64_t regular_patches;      /* local patches with a regular ring (every ring cell a copy of
+                                   the aligned cell of a same-level local neighbour): the scalar
+                                   sweeps compute their gather addresses and move the ring in
+                                   16-byte pairs; other patches (and the systems kernel) read the
+                                   ring table.  Bitwise the same gather either way */
 } fc_stats;
 
 /* ---- calls --------------------------------------------------------------------------------- */
