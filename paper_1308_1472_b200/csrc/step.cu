@@ -1016,7 +1016,10 @@ __device__ __forceinline__ CvNb cv_nb_load(const StepArgs& A, int i0, int cnt, i
     const int q = e / 9;
     if (q >= cnt || q >= PW) return -1;
     const int patch = A.active ? A.active[i0 + q] : i0 + q;
-    return __ldg(A.nb9 + (int64_t)patch * 9 + (e - 9 * q));
+    // (a volatile load: issued here, not sunk to its use after the sweep)
+    int32_t v;
+    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(A.nb9 + (int64_t)patch * 9 + (e - 9 * q)));
+    return v;
   };
   r.lo = entry(lane);
   if (PW * 9 > 32) r.hi = entry(lane + 32);
@@ -1095,15 +1098,25 @@ __device__ CV_STAGE_INLINE void cv_stage(const StepArgs& A, double* buf, uint64_
     rg[q] = pt[q] >= 0 && nb_of(9 * q) >= 0;
   }
   // the other patches' ring-table entries, all loaded first: one latency, not one per patch
+  // (skipped as a whole -- a warp-uniform branch -- when every patch of the group is regular)
+  bool table = false;
+#pragma unroll
+  for (int q = 0; q < PW; ++q) table |= pt[q] >= 0 && !rg[q];
 #pragma unroll
   for (int q = 0; q < PW; ++q)
 #pragma unroll
-    for (int t = 0; t < NR; ++t) {
-      const int r = lane + 32 * t;
-      const bool ok = pt[q] >= 0 && !rg[q] && r < G;
-      src[q][t] = ok ? __ldg(A.ring + (int64_t)pt[q] * G + r) : -1;
-      own[q][t] = (ok && peers) ? __ldg(A.rpeer + (int64_t)pt[q] * G + r) : 0;
-    }
+    for (int t = 0; t < NR; ++t) { src[q][t] = -1; own[q][t] = 0; }
+  if (table) {
+#pragma unroll
+    for (int q = 0; q < PW; ++q)
+#pragma unroll
+      for (int t = 0; t < NR; ++t) {
+        const int r = lane + 32 * t;
+        const bool ok = pt[q] >= 0 && !rg[q] && r < G;
+        if (ok) src[q][t] = __ldg(A.ring + (int64_t)pt[q] * G + r);
+        if (ok && peers) own[q][t] = __ldg(A.rpeer + (int64_t)pt[q] * G + r);
+      }
+  }
   // the interior as 16-byte cp.async chunks (two cells) into the natural window: every lane issues
   // its own (a per-row bulk copy from per-lane addresses is serialised over the lanes)
   constexpr int CH = T * T / 2;
