@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(NT) k_step_sc(StepArgs A, int ntiles) {
       ty = tt / A.tiles;
       tx = tt - ty * A.tiles;
     }
-    const double dtdx = A.dt / ldexp(A.dx0, -(int)A.level[patch]);
+    const double dtdx = dtdx_level(A, (int)A.level[patch]);
     const int slot = RF ? A.rslot[patch] : -1;
     auto reg = [&](int face, int e) { return A.freg + (((int64_t)slot * 4 + face) * A.m + e); };
     mbar_wait(&bars[b], (uint32_t)((it / NB) & 1));
@@ -1259,7 +1259,7 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
 #pragma unroll
     for (int e = 0; e < 5; ++e) col[e] = sq + min(c0 - 1 + e, T + 2) + 1;
     auto ld = [&](int e, int j) { return col[e][(j + 1) * W]; };
-    const double r = A.dt / ldexp(A.dx0, -level);
+    const double r = dtdx_level(A, level);
     if (live) cfl = fmax(cfl, fmax(fmax(r * u0, -r * u0), fmax(r * v0, -r * v0)));
     const double cfx = second ? 0.5 * fabs(u0) * (1.0 - fabs(u0) * r) : 0.0;
     const double cfy = second ? 0.5 * fabs(v0) * (1.0 - fabs(v0) * r) : 0.0;
@@ -1472,7 +1472,7 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
     auto kap = [&](int cc, int j) { return __ldg(ax + (j + 1) * W + cc); };
     auto uu = [&](int cc, int j) { return __ldg(ax + WW + (j + 1) * W + cc); };
     auto vv = [&](int cc, int j) { return __ldg(ax + 2 * WW + (j + 1) * W + cc); };
-    const double dtdx = A.dt / ldexp(A.dx0, -level);
+    const double dtdx = A.dt / ldexp(A.dx0, -level);   // (the table lookup costs this kernel 5 spills, T4 +10 %)
     double* out = A.qnew + (int64_t)patch * WW;
     // edge parts from (w, upwind candidates, speed, r of the low / high cell); CFL when counted
     auto edge = [&](double w, double wup_lo, double wup_hi, double s, double rl, double rh, bool count,
@@ -1980,6 +1980,7 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
   for (int r = 0; r < 16; ++r) a.peerq[r] = peerq ? peerq[r] : nullptr;
   a.qold = qold; a.qnew = qnew; a.aux = aux; a.level = level;
   a.dt = dt; a.dx0 = dx0; a.sp.p0 = p0; a.sp.p1 = p1;
+  for (int L = 0; L < 29; ++L) a.dtdx[L] = dt / ldexp(dx0, -L);
   a.limiter = limiter; a.method2 = method2; a.method3 = method3;
   a.skip_quiescent = skip_quiescent;
   a.ring = ring;

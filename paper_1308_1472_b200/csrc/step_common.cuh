@@ -41,6 +41,7 @@ struct StepArgs {
   const int32_t* __restrict__ nactive;
   LimiterCoef lim;
   LimiterCoef limh;                   // lim with every coefficient halved: phi / 2, exactly
+  double dtdx[29];                    // dt / dx of a level-L patch (levels 0..28), dt / ldexp(dx0, -L) on the host
   int m, tiles;                       // tiles per side
   unsigned long long* cfl_bits;
   double* fbuf;                       // method3 = 1 only: per-CTA F~ of each correction edge [MEQN][E2]
@@ -50,6 +51,9 @@ struct StepArgs {
   const double* peerq[16];            // peer-memory halo: rank r's current q_old (peer pointer)
   const double* cg;                   // fused AMR ring gather: computed ghosts (ring peer code 255)
 };
+
+// dt / dx of a level-L patch (the host's table: no division in the kernels)
+__device__ __forceinline__ double dtdx_level(const StepArgs& A, int L) { return A.dtdx[L]; }
 // base of a ring source: this rank's q_old, a peer's (code k = rank k - 1), the computed ghosts (255)
 __device__ __forceinline__ const double* ring_base(const StepArgs& A, int ow) {
   if (ow == 0) return A.qold;

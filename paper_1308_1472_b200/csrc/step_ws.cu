@@ -425,8 +425,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
     }
     if (cur & 1) { ws_bc<S>(A, tile, sq, 0, tid, NT); __syncthreads(); }
     if (cur & 2) { ws_bc<S>(A, tile, sq, 1, tid, NT); __syncthreads(); }
-    const double dx = ldexp(A.dx0, -(cur >> 8));
-    const double r = A.dt / dx;                 // square cells, no capacity: dt/dx = dt/dy
+    const double r = dtdx_level(A, cur >> 8);   // square cells, no capacity: dt/dx = dt/dy
     double* o = A.qnew + (int64_t)patch * MEQN * (A.m + 4) * (A.m + 4) + (int64_t)(ty * T) * A.m + tx * T;
     const int64_t n2 = (int64_t)(A.m + 4) * (A.m + 4);
     if (A.skip_quiescent) {   // one state in the whole window: every jump is 0, q_new = q bitwise
