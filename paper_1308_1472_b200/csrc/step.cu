@@ -1205,20 +1205,9 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
   const int p = lane / LP, k = lane - p * LP, c0 = 2 * k;
   const double u0 = A.sp.p0, v0 = A.sp.p1;
   const bool trans = A.method3 >= 1, second = A.method2 == 2;
-  const double lc1 = A.lim.c1, lc2 = A.lim.c2, lc3 = A.lim.c3, lc4 = A.lim.c4;
-  // phi(wi / w) w of the MC / minmod limiter (launched for those only), division- and branch-free:
-  // with s the sign of w, s max(0, min(s (c1 w + c2 wi), c3 |w|, s c4 wi)) (s x: a sign-bit flip)
-  // phi(wi / w) w of the MC / minmod limiter (launched for those only), division- and select-free:
-  // sign(w) min(c1 |w| + c2 |wi|, c3 |w|, c4 |wi|) when w and wi share a sign, else 0, with
-  // min(x, y) = (x + y - |x - y|) / 2 on the fp64 pipe (the sweeps are issue-bound; the rounding
-  // differs from the oracle's phi(theta) w by ulps, within the step tolerance, reading 24)
-  auto limited = [&](double w, double wi) {
-    const double a = fabs(w), b = fabs(wi);
-    const double x = fma(lc1, a, lc2 * b), y = lc3 * a, z = lc4 * b;
-    const double yz = 0.5 * ((y + z) - fabs(y - z));
-    const double mag = 0.5 * ((x + yz) - fabs(x - yz));
-    return w * wi > 0.0 ? copysign(mag, w) : 0.0;
-  };
+  // phi(wi / w) w of the MC / minmod limiter (launched for those only): cv_limited
+  const double lp1 = A.lp1, lp2 = A.lp2, lk3 = A.lk3;
+  auto limited = [&](double w, double wi) { return cv_limited(w, wi, lp1, lp2, lk3); };
   double cfl = 0.0;
   double chk = 0.0;                     // sum of 0 * q_new: NaN iff some q_new is not finite
   int it = 0;
@@ -1427,14 +1416,8 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
   const int p = lane / LP, k = lane - p * LP, c0 = 2 * k;
   const bool trans = A.method3 >= 1, second = A.method2 == 2;
   const double m3 = A.method3 == 2 ? 1.0 : 0.0, h = trans ? -0.5 : 0.0;
-  const double lc1 = A.lim.c1, lc2 = A.lim.c2, lc3 = A.lim.c3, lc4 = A.lim.c4;
-  auto limited = [&](double w, double wi) {   // as k_step_cv (MC / minmod)
-    const double a = fabs(w), b = fabs(wi);
-    const double x = fma(lc1, a, lc2 * b), y = lc3 * a, z = lc4 * b;
-    const double yz = 0.5 * ((y + z) - fabs(y - z));
-    const double mag = 0.5 * ((x + yz) - fabs(x - yz));
-    return w * wi > 0.0 ? copysign(mag, w) : 0.0;
-  };
+  const double lp1 = A.lp1, lp2 = A.lp2, lk3 = A.lk3;
+  auto limited = [&](double w, double wi) { return cv_limited(w, wi, lp1, lp2, lk3); };   // as k_step_cv
   double cfl = 0.0, chk = 0.0;
   int it = 0;
   for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
@@ -1990,6 +1973,9 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
   a.nactive = nactive;
   a.lim = limiter_coef(limiter);
   a.limh = {0.5 * a.lim.lo, 0.5 * a.lim.c1, 0.5 * a.lim.c2, 0.5 * a.lim.c3, 0.5 * a.lim.c4};
+  a.lp1 = limiter == FC_LIM_MC ? 0.5 : 0.0;     // (cv_limited; the register sweeps run MC / minmod only)
+  a.lp2 = limiter == FC_LIM_MC ? 0.0 : 1.0;
+  a.lk3 = limiter == FC_LIM_MC ? 1.0 : 0.5;
   a.m = m;
   const int T = (m % 16 == 0) ? 16 : ((m % 8 == 0) ? 8 : ((m % 4 == 0) ? 4 : 2));
   a.tiles = m / T;

@@ -41,6 +41,7 @@ struct StepArgs {
   const int32_t* __restrict__ nactive;
   LimiterCoef lim;
   LimiterCoef limh;                   // lim with every coefficient halved: phi / 2, exactly
+  double lp1, lp2, lk3;               // MC / minmod as min(lp1 (a + b) + lp2 a, lk3 (a + b - |a - b|)), cv_limited
   double dtdx[29];                    // dt / dx of a level-L patch (levels 0..28), dt / ldexp(dx0, -L) on the host
   int m, tiles;                       // tiles per side
   unsigned long long* cfl_bits;
@@ -51,6 +52,21 @@ struct StepArgs {
   const double* peerq[16];            // peer-memory halo: rank r's current q_old (peer pointer)
   const double* cg;                   // fused AMR ring gather: computed ghosts (ring peer code 255)
 };
+
+// phi(wi / w) w of the MC / minmod limiter for the scalar register sweeps, division- and
+// select-free: with a = |w|, b = |wi|, s = a + b, MC is min(s / 2, 2 min(a, b)) and minmod
+// min(a, min(a, b)), i.e. min(lp1 s + lp2 a, lk3 (s - |a - b|)) with (lp1, lp2, lk3) = (1/2, 0, 1) /
+// (0, 1, 1/2); min(x, y) = (x + y - |x - y|) / 2 on the fp64 pipe; the sign of w when w and wi
+// share a sign (an integer test of the sign bits: a zero w or wi gives mag = 0 anyway), else 0.
+// The rounding differs from the oracle's phi(theta) w by ulps, within the step tolerance (reading 24).
+__device__ __forceinline__ double cv_limited(double w, double wi, double lp1, double lp2, double lk3) {
+  const double a = fabs(w), b = fabs(wi), s = a + b;
+  const double x = fma(lp1, s, lp2 * a), y = lk3 * (s - fabs(a - b));
+  const double mag = 0.5 * ((x + y) - fabs(x - y));
+  const int hw = __double2hiint(w);
+  const bool opp = (hw ^ __double2hiint(wi)) < 0;
+  return opp ? 0.0 : __hiloint2double((hw & 0x80000000) | __double2hiint(mag), __double2loint(mag));
+}
 
 // dt / dx of a level-L patch (the host's table: no division in the kernels)
 __device__ __forceinline__ double dtdx_level(const StepArgs& A, int L) { return A.dtdx[L]; }
