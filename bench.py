@@ -283,6 +283,16 @@ def run_variants(args, fc, hbm_peak):
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.variant_steps
+        # the same steps replayed as CUDA graphs (fc_run, fixed dt = the adaptive dt reached): no
+        # host turnaround between steps; each step still reduces its CFL (read back per call)
+        f.run(dt, 1)                                  # (graph capture outside the timed region)
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        rc_g, _ = f.run(dt, args.variant_steps, raise_on_reject=False)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        ms_g = g0.elapsed_time(g1) / args.variant_steps if rc_g == fc.FC_OK else None
         f.reset_stats()
         f.set_timing(True)
         run(3, dt)
@@ -292,13 +302,20 @@ def run_variants(args, fc, hbm_peak):
         del qd
         rate = w.cells / (ms / 1e3)
         bpc = 16 * w.meqn + 8 * w.maux
+        graph = None
+        if ms_g:
+            rg = w.cells / (ms_g / 1e3)
+            graph = {"ms_per_step": ms_g, "value": rg, "hbm_roofline_frac": rg * bpc / (hbm_peak * 1e9),
+                     "timing": "fc_run (CUDA graphs, fixed dt), CUDA events around one call of K steps, "
+                               "including its state backup copy and the CFL read-back"}
         out[name] = {"workload": w.name, "patches": w.num_patches, "cells": w.cells,
                      "ms_per_step": ms, "value": rate, "unit": UNIT,
                      "bytes_per_cell_update": bpc, "hbm_roofline_frac": rate * bpc / (hbm_peak * 1e9),
                      "update_kernel_ms": st["ms_step"] / max(1, st["step_kernel_launches"]),
                      "ghost_ms": st["ms_ghost"] / max(1, st["steps"]),
                      "fused_path": st.get("uniform_fast_path"), "generate_s": gen_s,
-                     "steps": args.variant_steps, "mode": "full update (skip_quiescent = 0)"}
+                     "steps": args.variant_steps, "mode": "full update (skip_quiescent = 0)",
+                     "graph": graph}
     out["O3"] = run_octree(args, hbm_peak)
     return out
 

@@ -13,4 +13,6 @@ out = bench.run_variants(a, fc, 6547.8)
 for k, v in out.items():
     print(json.dumps({"v": k, "ms": round(v["ms_per_step"], 4), "G_per_s": round(v["value"] / 1e9, 2),
                       "hbm_frac": round(v["hbm_roofline_frac"], 3),
+                      "graph_ms": round(v["graph"]["ms_per_step"], 4) if v.get("graph") else None,
+                      "graph_frac": round(v["graph"]["hbm_roofline_frac"], 3) if v.get("graph") else None,
                       "regular": os.environ.get("FC_REGULAR_RING", "1")}))
