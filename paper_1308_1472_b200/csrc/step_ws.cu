@@ -39,7 +39,14 @@ namespace fc {
 // ------------------------------------------------------------------------------------------------
 template <class S>
 struct WsShape {
-  static constexpr int T = 16, W = T + 4, PW = W + 1;          // window 20 x 20, row pitch 21
+#ifndef WS_CHUNK
+#define WS_CHUNK 1
+#endif
+  // window 20 x 20, row pitch 22 (WS_CHUNK: even, so that the tile interior's rows arrive as
+  // 16-byte copies) or 21 (odd: conflict-free column access, 8-byte copies only)
+  static constexpr bool CHUNK = WS_CHUNK != 0;
+  static constexpr int T = 16, W = T + 4, PW = CHUNK ? W + 2 : W + 1;
+  static constexpr int NH = W * W - T * T;                     // halo cells of the window (144)
   static constexpr int WPW = W * PW;                           // component stride of the window
   static constexpr int NE = T + 3, NR = T + 2, E = NR * NE;    // 19 edges x 18 rows per sweep
   static constexpr int STEP = 29, NIT = (E + STEP - 1) / STEP; // 12 warp-iterations per sweep
@@ -81,10 +88,33 @@ struct WsGather {
   int32_t v[GU];           // ring source offset, or -1 - BC code, or INT32_MIN: own interior
   uint8_t ow[GU];          // owner code of a ring source (0 local, k peer rank k-1, 255 computed)
 };
+// window cell c of a thread's gather share: with CHUNK the halo cells only (rows 0, 1, W-2, W-1
+// whole, then columns 0, 1, W-2, W-1 of rows 2..W-3), else every window cell; false past the end
+template <class S>
+__device__ __forceinline__ bool ws_cell(int c, int& wi, int& wj) {
+  using Sh = WsShape<S>;
+  constexpr int T = Sh::T, W = Sh::W;
+  if (!Sh::CHUNK) {
+    wj = c / W;
+    wi = c - wj * W;
+    return c < W * W;
+  }
+  if (c < 4 * W) {
+    const int r = c / W;
+    wj = r < 2 ? r : r + T;
+    wi = c - r * W;
+  } else {
+    const int h = c - 4 * W;
+    wj = 2 + (h >> 2);
+    wi = (h & 3) < 2 ? (h & 3) : (h & 3) + T;
+  }
+  return c < Sh::NH;
+}
+
 template <class S, int WS_GU>
 __device__ __forceinline__ void ws_prep(const StepArgs& A, int tile, WsGather<WS_GU>& g, int tid, int nt) {
   using Sh = WsShape<S>;
-  constexpr int T = Sh::T, W = Sh::W;
+  constexpr int T = Sh::T;
   g.tile = tile;
   if (tile < 0) return;
   int patch, tx, ty;
@@ -105,8 +135,8 @@ __device__ __forceinline__ void ws_prep(const StepArgs& A, int tile, WsGather<WS
     const int c = tid + u * nt;
     g.v[u] = INT32_MIN;
     g.ow[u] = 0;
-    if (c >= W * W) continue;
-    const int wj = c / W, wi = c - wj * W;
+    int wi, wj;
+    if (!ws_cell<S>(c, wi, wj)) continue;
     const int i = tx * T + wi - 1, j = ty * T + wj - 1;   // patch cell (1-based interior)
     if ((unsigned)(i - 1) < (unsigned)m && (unsigned)(j - 1) < (unsigned)m) continue;
     if (reg) {
@@ -122,17 +152,24 @@ __device__ __forceinline__ void ws_prep(const StepArgs& A, int tile, WsGather<WS
 template <class S, int WS_GU>
 __device__ __forceinline__ void ws_issue(const StepArgs& A, const WsGather<WS_GU>& g, double* sq, int tid, int nt) {
   using Sh = WsShape<S>;
-  constexpr int T = Sh::T, W = Sh::W, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN;
+  constexpr int T = Sh::T, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN;
   if (g.tile < 0) return;
   int patch, tx, ty;
   ws_tile(A, g.tile, patch, tx, ty);
   const int m = A.m, n = m + 4, n2 = n * n;
   const double* qb = A.qold + (int64_t)patch * MEQN * n2;
+  if (Sh::CHUNK) {   // the tile interior: rows of T cells as T / 2 16-byte copies per component
+    constexpr int HC = T / 2, PER = T * HC;
+    for (int t = tid; t < MEQN * PER; t += nt) {
+      const int k = t / PER, rem = t - k * PER, rr = rem / HC, cc = rem - rr * HC;
+      cp_async16(sq + k * WPW + (rr + 2) * PW + 2 + 2 * cc, qb + (int64_t)k * n2 + (ty * T + rr) * m + tx * T + 2 * cc);
+    }
+  }
 #pragma unroll
   for (int u = 0; u < WS_GU; ++u) {
     const int c = tid + u * nt;
-    if (c >= W * W) continue;
-    const int wj = c / W, wi = c - wj * W;
+    int wi, wj;
+    if (!ws_cell<S>(c, wi, wj)) continue;
     const double* src;
     if (g.v[u] == INT32_MIN) {
       src = qb + (ty * T + wj - 2) * m + (tx * T + wi - 2);
@@ -347,7 +384,7 @@ template <class S, int NW, int MINB, int NBUF, bool FAST>
 __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntiles) {
   using Sh = WsShape<S>;
   constexpr int T = Sh::T, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN, NT = NW * 32;
-  constexpr int GU = (Sh::W * Sh::W + NT - 1) / NT;
+  constexpr int GU = ((Sh::CHUNK ? Sh::NH : Sh::W * Sh::W) + NT - 1) / NT;
   const int tiles2 = A.tiles * A.tiles;
   if (A.active) ntiles = *A.nactive * tiles2;
   auto tile_of = [&](int k) {
