@@ -7,15 +7,16 @@
 // phased k_step (step.cu) and the oracle (oracle/claw.c), different schedule:
 //
 // One CTA (NW warps) per 16 x 16 tile at a time (persistent over tiles), its 20 x 20 window (tile +
-// 2-cell halo, natural layout, pitch 21: conflict-free column access) gathered by cp.async straight
+// 2-cell halo, natural layout, row pitch 22: 16-byte interior copies) gathered by cp.async straight
 // from the neighbours' interiors (the fused ring gather: no ring is ever written to HBM), the next
 // tile's gather in flight while the current one computes.  Per tile three phases, one barrier each:
 //   X  the 18 x 19 x-edges of rows 0..17 as 12 warp-iterations of 32 consecutive edges (row-major,
 //      advancing 29: lanes 0 and 31 are halo edges for the limiter).  Per lane: both cells' derived
 //      fields, the Roe solve (+ Harten-Hyman A-dq), then per wave family the upwind neighbour's wave
-//      by one warp shuffle -> limiter, F~, CFL; the L part (A-dq + F~) of the next edge and its
-//      Roe state by shuffle; both transverse splits entering the lane's right cell -> up / dn (G~
-//      halves) and the x increment of the cell, to shared memory.
+//      by one warp shuffle -> limiter, F~, CFL; both transverse splits of the edge with its own
+//      Roe state, of its L part P = A-dq + F~ (into the left cell: handed to the previous edge's
+//      lane with P by shuffle) and of its R part Q (the right cell, the lane's output cell) -> up /
+//      dn (G~ halves) and the x increment of the cell, to shared memory.
 //   Y  the same along y (column-major flat edges); the lane owning a cell also folds the x-sweep's
 //      G~ differences into its increment; transverse parts -> rt / lf (F~ halves).
 //   F  per cell q_new = q + dq - r (F~(i+1/2) - F~(i-1/2)), stored coalesced; non-finite check.
@@ -77,7 +78,7 @@ __device__ __forceinline__ void ws_tile(const StepArgs& A, int tile, int& patch,
   }
 }
 
-// cp.async gather of a tile's 20 x 20 window (natural layout, pitch 21): cells inside the patch
+// cp.async gather of a tile's 20 x 20 window (natural layout, pitch 22): cells inside the patch
 // interior from its own storage block, the others from the ring-source table (a neighbour's
 // interior, a peer rank's buffer, or a computed ghost); physical-boundary cells after the wait.
 // Two stages so that the ring-table loads never stall the issuing thread: ws_prep loads this
@@ -213,55 +214,6 @@ __device__ __forceinline__ void ws_bc(const StepArgs& A, int tile, double* sq, i
   }
 }
 
-// the output cell of a sweep lane (the right cell of its edge): both transverse splits, the
-// G~ / F~ halves and the normal increment (called with the whole warp converged after the shuffles)
-template <class S, int D>
-__device__ __forceinline__ void ws_output(const StepArgs& A, int m3, const typename S::Edge& Ed, const double* P,
-                                          const double* Q, const double* sw, const double* Pn,
-                                          const double* XLn, const typename S::Roe& rn, double* __restrict__ up,
-                                          double* __restrict__ dn, double* __restrict__ dq, double r, double hr,
-                                          int pos, int line) {
-  using Sh = WsShape<S>;
-  constexpr int T = Sh::T, MEQN = S::MEQN;
-  double XR[MEQN];
-#pragma unroll
-  for (int k = 0; k < MEQN; ++k) XR[k] = m3 == 1 ? sw[k] - Ed.am[k] : Q[k];
-  double bmQ[MEQN], bpQ[MEQN], bmP[MEQN], bpP[MEQN];
-  hr *= 0.5;   // (transverse returns 2 B-X, 2 B+X)
-  if (m3 >= 1) {
-    S::template transverse<D>(S::roe(Ed), A.sp, XR, bmQ, bpQ);
-    S::template transverse<D>(rn, A.sp, XLn, bmP, bpP);
-  } else {
-#pragma unroll
-    for (int k = 0; k < MEQN; ++k) bmQ[k] = bpQ[k] = bmP[k] = bpP[k] = 0.0;
-  }
-  if (D == 1) {   // cell (i = pos, j = line): G~ halves for rows 0..T+1, the x increment for rows 1..T
-    const int i = pos, j = line;
-#pragma unroll
-    for (int k = 0; k < MEQN; ++k) {
-      up[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = hr * bpP[k] + hr * bpQ[k];
-      dn[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = hr * bmP[k] + hr * bmQ[k];
-    }
-    if (j >= 1 && j <= T) {
-#pragma unroll
-      for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
-    }
-  } else {        // cell (i = line, j = pos): F~ halves for columns 0..T+1; interior columns fold
-    const int i = line, j = pos;
-    double* rt = up;   // (D = 2: the up / dn arguments are the rt / lf arrays)
-    double* lf = dn;
-#pragma unroll
-    for (int k = 0; k < MEQN; ++k) {
-      rt[(k * T + (j - 1)) * Sh::RTP + i] = hr * bpP[k] + hr * bpQ[k];
-      lf[(k * T + (j - 1)) * Sh::RTP + i] = hr * bmP[k] + hr * bmQ[k];
-    }
-    if (i >= 1 && i <= T) {   // the y increment (its own array: the sweeps run concurrently)
-#pragma unroll
-      for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
-    }
-  }
-}
-
 // wave limiter phi(theta) = max(lo, min(c1 + c2 theta, c3, c4 theta)) with compare-selects (the
 // operands are never NaN here: theta of a zero wave is replaced by 0 first)
 __device__ __forceinline__ double ws_phi(const LimiterCoef& L, double th) {
@@ -363,20 +315,56 @@ __device__ __forceinline__ void ws_iter(const StepArgs& A, const double* __restr
       P[k] = Ed.am[k] + F[k];
       Q[k] = (sw[k] - Ed.am[k]) - F[k];
     }
-    // the next edge's L part (and, for the transverse split, its transverse input and Roe state)
-    double Pn[MEQN], XLn[MEQN];
+    // both transverse splits with this edge's own Roe state (its Roe-only terms once): of Q (into
+    // the right cell, this lane's output) and of P (into the left cell: the previous edge's lane's
+    // output, handed down scaled together with P)
+    {
+      double XP[MEQN], XQ[MEQN], bmP[MEQN], bpP[MEQN], bmQ[MEQN], bpQ[MEQN];
 #pragma unroll
-    for (int k = 0; k < MEQN; ++k) Pn[k] = ws_shfl_down(P[k], 1);
-    if (m3 == 1) {
+      for (int k = 0; k < MEQN; ++k) {
+        XP[k] = m3 == 1 ? Ed.am[k] : P[k];
+        XQ[k] = m3 == 1 ? sw[k] - Ed.am[k] : Q[k];
+      }
+      if (m3 >= 1) {
+        S::template transverse2<D>(S::roe(Ed), A.sp, XP, XQ, bmP, bpP, bmQ, bpQ);
+      } else {
 #pragma unroll
-      for (int k = 0; k < MEQN; ++k) XLn[k] = ws_shfl_down(Ed.am[k], 1);
-    } else {
+        for (int k = 0; k < MEQN; ++k) bmQ[k] = bpQ[k] = bmP[k] = bpP[k] = 0.0;
+      }
+      const double hh = 0.5 * hr;   // (transverse returns 2 B-X, 2 B+X)
+      double Un[MEQN], Dn[MEQN], Pn[MEQN];
 #pragma unroll
-      for (int k = 0; k < MEQN; ++k) XLn[k] = Pn[k];
+      for (int k = 0; k < MEQN; ++k) {
+        Un[k] = ws_shfl_down(hh * bpP[k], 1);
+        Dn[k] = ws_shfl_down(hh * bmP[k], 1);
+        Pn[k] = ws_shfl_down(P[k], 1);
+      }
+      if (out) {
+        if (D == 1) {   // cell (i = pos, j = line): G~ halves for rows 0..T+1, the x increment for rows 1..T
+          const int i = pos, j = line;
+#pragma unroll
+          for (int k = 0; k < MEQN; ++k) {
+            up[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = fma(hh, bpQ[k], Un[k]);
+            dn[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = fma(hh, bmQ[k], Dn[k]);
+          }
+          if (j >= 1 && j <= T) {
+#pragma unroll
+            for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
+          }
+        } else {        // cell (i = line, j = pos): F~ halves (up / dn are the rt / lf arrays)
+          const int i = line, j = pos;
+#pragma unroll
+          for (int k = 0; k < MEQN; ++k) {
+            up[(k * T + (j - 1)) * Sh::RTP + i] = fma(hh, bpQ[k], Un[k]);
+            dn[(k * T + (j - 1)) * Sh::RTP + i] = fma(hh, bmQ[k], Dn[k]);
+          }
+          if (i >= 1 && i <= T) {
+#pragma unroll
+            for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
+          }
+        }
+      }
     }
-    const typename S::Roe rn = S::shfl_down(S::roe(Ed), 1);
-    // this lane's output cell: the right cell of its edge, (pos, line)
-    if (out) ws_output<S, D>(A, m3, Ed, P, Q, sw, Pn, XLn, rn, up, dn, dq, r, hr, pos, line);
   }
 }
 

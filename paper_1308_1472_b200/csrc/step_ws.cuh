@@ -160,42 +160,47 @@ struct WsEuler {
     const double sg = p == 0 ? -1.0 : 1.0;
     W[0] = a; W[nd] = a * (un + sg * E.c); W[td] = a * vt; W[3] = a * (E.H + sg * un * E.c);
   }
-  // the Roe state an edge's transverse split needs (shuffled from the neighbouring lane)
+  // the Roe state an edge's transverse splits need
   struct Roe {
     double u, v, H, c, ic;
   };
   __device__ static Roe roe(const Edge& E) { return {E.u, E.v, E.H, E.c, E.ic}; }
-  __device__ static Roe shfl_down(const Roe& r, int d) {
-    return {ws_shfl_down(r.u, d), ws_shfl_down(r.v, d), ws_shfl_down(r.H, d), ws_shfl_down(r.c, d),
-            ws_shfl_down(r.ic, d)};
-  }
-  // 2 B-X, 2 B+X of the Roe matrix along the transverse direction of sweep D (EulerRoe::
-  // roe_transverse's formulas; the eigenvalue split as lambda -+ |lambda|, i.e. twice its halves,
-  // the caller scaling by 1/2: exact).  With the eigenvectors r1 = (1, vn - c, vt, H - vn c),
-  // r2 = (1, vn, vt, ek), r3 = (0, 0, 1, vt), r4 = (1, vn + c, vt, H + vn c) and weights m_p,
-  // sum_p m_p r_p = (S + m2, vn (S + m2) + D, vt (S + m2) + m3, H S + vn D + ek m2 + vt m3) with
-  // S = m1 + m4, D = c (m4 - m1): the same sum, regrouped.
+  // 2 B-X, 2 B+X of the Roe matrix along the transverse direction of sweep D for two inputs X = XA,
+  // XB (EulerRoe::roe_transverse's formulas; the eigenvalue split as lambda -+ |lambda|, i.e. twice
+  // its halves, the caller scaling by 1/2: exact; the terms of the Roe state alone -- gm1/c^2,
+  // H - |v|^2, the eigenvalue halves -- once for both).  With the eigenvectors r1 = (1, vn - c, vt,
+  // H - vn c), r2 = (1, vn, vt, ek), r3 = (0, 0, 1, vt), r4 = (1, vn + c, vt, H + vn c) and weights
+  // m_p, sum_p m_p r_p = (S + m2, vn (S + m2) + D, vt (S + m2) + m3, H S + vn D + ek m2 + vt m3)
+  // with S = m1 + m4, D = c (m4 - m1): the same sum, regrouped.
   template <int D>
-  __device__ static void transverse(const Roe& r, const SolverParams& P, const double* X, double* bm, double* bp) {
+  __device__ static void transverse2(const Roe& r, const SolverParams& P, const double* XA, const double* XB,
+                                     double* bmA, double* bpA, double* bmB, double* bpB) {
     constexpr int nd = 3 - D, td = D;
     const double gm1 = P.p0 - 1.0, c = r.c, ic = r.ic, H = r.H;
     const double vn = nd == 1 ? r.u : r.v, vt = nd == 1 ? r.v : r.u;
-    const double b3 = X[td] - vt * X[0];
-    const double b2 = gm1 * (ic * ic) * ((H - vn * vn - vt * vt) * X[0] + vn * X[nd] + vt * X[td] - X[3]);
-    const double b4 = (X[nd] + (c - vn) * X[0] - c * b2) * (0.5 * ic);
-    const double b1 = X[0] - b2 - b4;
+    const double K = gm1 * (ic * ic), E = H - vn * vn - vt * vt, cv = c - vn, hic = 0.5 * ic;
     const double ek = 0.5 * (vn * vn + vt * vt);
     const double l1 = vn - c, l4 = vn + c;
-    auto set = [&](double w1, double w2, double w4, double* o) {
-      const double m1 = w1 * b1, m2 = w2 * b2, m3 = w2 * b3, m4 = w4 * b4;
-      const double S = m1 + m4, Dd = c * (m4 - m1), o0 = S + m2;
-      o[0] = o0;
-      o[nd] = fma(vn, o0, Dd);
-      o[td] = fma(vt, o0, m3);
-      o[3] = fma(H, S, fma(vn, Dd, fma(ek, m2, vt * m3)));
+    const double w1m = l1 - fabs(l1), w2m = vn - fabs(vn), w4m = l4 - fabs(l4);
+    const double w1p = l1 + fabs(l1), w2p = vn + fabs(vn), w4p = l4 + fabs(l4);
+    auto one = [&](const double* X, double* bm, double* bp) {
+      const double b3 = X[td] - vt * X[0];
+      const double b2 = K * (E * X[0] + vn * X[nd] + vt * X[td] - X[3]);
+      const double b4 = (X[nd] + cv * X[0] - c * b2) * hic;
+      const double b1 = X[0] - b2 - b4;
+      auto set = [&](double w1, double w2, double w4, double* o) {
+        const double m1 = w1 * b1, m2 = w2 * b2, m3 = w2 * b3, m4 = w4 * b4;
+        const double S = m1 + m4, Dd = c * (m4 - m1), o0 = S + m2;
+        o[0] = o0;
+        o[nd] = fma(vn, o0, Dd);
+        o[td] = fma(vt, o0, m3);
+        o[3] = fma(H, S, fma(vn, Dd, fma(ek, m2, vt * m3)));
+      };
+      set(w1m, w2m, w4m, bm);
+      set(w1p, w2p, w4p, bp);
     };
-    set(l1 - fabs(l1), vn - fabs(vn), l4 - fabs(l4), bm);
-    set(l1 + fabs(l1), vn + fabs(vn), l4 + fabs(l4), bp);
+    one(XA, bmA, bpA);
+    one(XB, bmB, bpB);
   }
   __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, double dtdx) {
     return EulerRoe::quiescent_cfl(q, qs, P, nullptr, dtdx, 0, 0, 0, 0);
@@ -271,29 +276,33 @@ struct WsSwe {
     double u, v, c, ic;
   };
   __device__ static Roe roe(const Edge& E) { return {E.u, E.v, E.c, E.ic}; }
-  __device__ static Roe shfl_down(const Roe& r, int d) {
-    return {ws_shfl_down(r.u, d), ws_shfl_down(r.v, d), ws_shfl_down(r.c, d), ws_shfl_down(r.ic, d)};
-  }
-  // 2 B-X, 2 B+X (as WsEuler::transverse): sum_p m_p r_p with r1 = (1, vn - c, vt), r2 = (0, 0, 1),
-  // r3 = (1, vn + c, vt) is (S, vn S + c (m3 - m1), vt S + m2), S = m1 + m3
+  // 2 B-X, 2 B+X for two inputs (as WsEuler::transverse2): sum_p m_p r_p with r1 = (1, vn - c, vt),
+  // r2 = (0, 0, 1), r3 = (1, vn + c, vt) is (S, vn S + c (m3 - m1), vt S + m2), S = m1 + m3
   template <int D>
-  __device__ static void transverse(const Roe& r, const SolverParams&, const double* X, double* bm, double* bp) {
-    constexpr int nd = 3 - D, td = D;   // eigen-decomposition along the transverse direction
+  __device__ static void transverse2(const Roe& r, const SolverParams&, const double* XA, const double* XB,
+                                     double* bmA, double* bpA, double* bmB, double* bpB) {
+    constexpr int nd = 3 - D, td = D;
     const double vn = nd == 1 ? r.u : r.v, vt = nd == 1 ? r.v : r.u, c = r.c;
-    const double i2c = 0.5 * r.ic;
-    const double b1 = ((vn + c) * X[0] - X[nd]) * i2c;
-    const double b2 = X[td] - vt * X[0];
-    const double b3 = ((c - vn) * X[0] + X[nd]) * i2c;
+    const double i2c = 0.5 * r.ic, pc = vn + c, mc = c - vn;
     const double l1 = vn - c, l3 = vn + c;
-    auto set = [&](double w1, double w2, double w3, double* o) {
-      const double m1 = w1 * b1, m2 = w2 * b2, m3 = w3 * b3;
-      const double S = m1 + m3;
-      o[0] = S;
-      o[nd] = fma(vn, S, c * (m3 - m1));
-      o[td] = fma(vt, S, m2);
+    const double w1m = l1 - fabs(l1), w2m = vn - fabs(vn), w3m = l3 - fabs(l3);
+    const double w1p = l1 + fabs(l1), w2p = vn + fabs(vn), w3p = l3 + fabs(l3);
+    auto one = [&](const double* X, double* bm, double* bp) {
+      const double b1 = (pc * X[0] - X[nd]) * i2c;
+      const double b2 = X[td] - vt * X[0];
+      const double b3 = (mc * X[0] + X[nd]) * i2c;
+      auto set = [&](double w1, double w2, double w3, double* o) {
+        const double m1 = w1 * b1, m2 = w2 * b2, m3 = w3 * b3;
+        const double S = m1 + m3;
+        o[0] = S;
+        o[nd] = fma(vn, S, c * (m3 - m1));
+        o[td] = fma(vt, S, m2);
+      };
+      set(w1m, w2m, w3m, bm);
+      set(w1p, w2p, w3p, bp);
     };
-    set(l1 - fabs(l1), vn - fabs(vn), l3 - fabs(l3), bm);
-    set(l1 + fabs(l1), vn + fabs(vn), l3 + fabs(l3), bp);
+    one(XA, bmA, bpA);
+    one(XB, bmB, bpB);
   }
   __device__ static double quiescent_cfl(const double* q, int qs, const SolverParams& P, double dtdx) {
     return SweRoe::quiescent_cfl(q, qs, P, nullptr, dtdx, 0, 0, 0, 0);
