@@ -1315,6 +1315,10 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
         if (sa_) out[(jr - 1) * T + c0 - 1] = va;
         if (sb_) out[(jr - 1) * T + c0] = vb;
         chk = fma(sa_ ? va : 0.0, 0.0, fma(sb_ ? vb : 0.0, 0.0, chk));
+#ifndef CV_VOTE
+#define CV_VOTE 0
+#endif
+        if (CV_VOTE && __any_sync(0xffffffffu, chk != chk)) chk = __longlong_as_double(0x7ff8000000000000ll);
         if (RF && rec) {   // the same face fluxes k_step_sc records (F~ / G~ transverse at the face)
           if (k == 0) reg[jr - 1] = (dR0p - kx * (SX > 0 ? Ya : Yb)) - u0 * qb[0];                 // x-low, i = 1
           if (k == LP - 1) reg[T + jr - 1] = u0 * qa[0] + (dL0p + kx * (SX > 0 ? Ya : Yb));       // x-high, i = T
@@ -1522,6 +1526,10 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
         if (sa_) out[(jr - 1) * T + c0 - 1] = va;
         if (sb_) out[(jr - 1) * T + c0] = vb;
         chk = fma(sa_ ? va : 0.0, 0.0, fma(sb_ ? vb : 0.0, 0.0, chk));
+#ifndef CV_VOTE
+#define CV_VOTE 0
+#endif
+        if (CV_VOTE && __any_sync(0xffffffffu, chk != chk)) chk = __longlong_as_double(0x7ff8000000000000ll);
       }
       if (F & YE) {    // y-edges (c, j + 1/2)
         const double wa = qa[2] - qa[1], wb = qb[2] - qb[1];

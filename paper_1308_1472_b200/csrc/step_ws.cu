@@ -247,127 +247,189 @@ __device__ __forceinline__ uint32_t ws_desc(int it, int lane) {
 }
 
 // One warp-iteration of a sweep (D = 1: x-edges of rows 0..T+1; D = 2: y-edges of columns
-// 0..T+1; NIT iterations per sweep), its lane's descriptor `dsc`.  FAST: method2 = 2 and
-// method3 = 2 (the configs) known at compile time; otherwise read from A.
-template <class S, int D, bool FAST>
-__device__ __forceinline__ void ws_iter(const StepArgs& A, const double* __restrict__ sq, double* __restrict__ up,
-                                        double* __restrict__ dn, double* __restrict__ dq, double r, double& smax,
-                                        uint32_t dsc, int lane) {
+// 0..T+1; NIT iterations per sweep), its lane's descriptor `dsc`, in three stages: ws_s1 (both
+// cells, the Roe solve + Harten-Hyman A-dq), ws_s2 (CFL, the limited corrections), ws_s3 (both
+// transverse splits, the lane's output cell).
+// FAST: method2 = 2 and method3 = 2 (the configs) known at compile time; otherwise read from A.
+template <class S>
+struct WsChain {
+  typename S::Cell L, R;
+  typename S::Edge Ed;
+  double sw[S::MEQN], F[S::MEQN];
+};
+
+template <class S, int D>
+__device__ __forceinline__ void ws_s1(const StepArgs& A, const double* __restrict__ sq, uint32_t dsc, WsChain<S>& c) {
   using Sh = WsShape<S>;
-  constexpr int T = Sh::T, PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN;
-  const double hr = -0.5 * r;
+  constexpr int PW = Sh::PW, WPW = Sh::WPW, MEQN = S::MEQN;
+  const int wr = dsc & 511;
+  const int wl = D == 1 ? wr - 1 : wr - PW;
+#pragma unroll
+  for (int k = 0; k < MEQN; ++k) {
+    c.L.q[k] = sq[k * WPW + wl];
+    c.R.q[k] = sq[k * WPW + wr];
+  }
+  S::cell(c.L, A.sp);
+  S::cell(c.R, A.sp);
+  S::template riemann<D>(c.L, c.R, A.sp, c.Ed);
+}
+
+template <class S, int D, bool FAST>
+__device__ __forceinline__ void ws_s2(const StepArgs& A, double r, double& smax, uint32_t dsc, int lane,
+                                      WsChain<S>& c) {
+  constexpr int MEQN = S::MEQN;
   const bool m2 = FAST || A.method2 == 2;
-  const int m3 = FAST ? 2 : A.method3;
-  {
-    const int wr = dsc & 511, pos = (dsc >> 9) & 31, line = (dsc >> 14) & 31;
-    const bool corr = (dsc >> 20) & 1, out = (dsc >> 21) & 1;
-    const int wl = D == 1 ? wr - 1 : wr - PW;
-    typename S::Cell L, R;
+  const bool corr = (dsc >> 20) & 1;
+  const typename S::Edge& Ed = c.Ed;
+  // CFL of the corrected edges: max over waves of r |s| = r (|un| + c) (the max taken per tile)
+  const double ms = S::template max_speed<D>(Ed);
+  smax = corr && ms > smax ? ms : smax;
+  // corrections: limiter on the upwind neighbour edge's wave of the same family (warp shuffle)
+  double* sw = c.sw;
+  double* F = c.F;
 #pragma unroll
-    for (int k = 0; k < MEQN; ++k) {
-      L.q[k] = sq[k * WPW + wl];
-      R.q[k] = sq[k * WPW + wr];
-    }
-    S::cell(L, A.sp);
-    S::cell(R, A.sp);
-    typename S::Edge Ed;
-    S::template riemann<D>(L, R, A.sp, Ed);
-    // CFL of the corrected edges: max over waves of r |s| = r (|un| + c) (the max taken per tile)
-    const double ms = S::template max_speed<D>(Ed);
-    smax = corr && ms > smax ? ms : smax;
-    // corrections: limiter on the upwind neighbour edge's wave of the same family (warp shuffle)
-    double sw[MEQN], F[MEQN];
+  for (int k = 0; k < MEQN; ++k) { sw[k] = 0.0; F[k] = 0.0; }
 #pragma unroll
-    for (int k = 0; k < MEQN; ++k) { sw[k] = 0.0; F[k] = 0.0; }
+  for (int p = 0; p < S::MW; ++p) {
+    double Wp[MEQN], WI[MEQN];
+    S::template wave<D>(Ed, p, Wp);
+    const double s = S::template speed<D>(Ed, p);
 #pragma unroll
-    for (int p = 0; p < S::MW; ++p) {
-      double Wp[MEQN], WI[MEQN];
-      S::template wave<D>(Ed, p, Wp);
-      const double s = S::template speed<D>(Ed, p);
+    for (int k = 0; k < MEQN; ++k)
+      if (S::wave_nz(D, p, k)) sw[k] = fma(s, Wp[k], sw[k]);
+    if (m2) {
+      const int src = s > 0.0 ? lane - 1 : lane + 1;    // (s = 0: the right neighbour, reading 1)
+      double wn2 = 0.0, dot = 0.0;
+#pragma unroll
+      for (int k = 0; k < MEQN; ++k) {
+        if (!S::wave_nz(D, p, k)) continue;
+        WI[k] = ws_shfl_idx(Wp[k], src & 31);
+        wn2 = fma(Wp[k], Wp[k], wn2);
+        dot = fma(WI[k], Wp[k], dot);
+      }
+      // a zero wave adds nothing: theta = 0 there (dot = 0; the 1e-300 changes wn2 only below
+      // 1e-284, i.e. for waves of norm < 1e-142) keeps the limiter's selects NaN-free
+      const double th = dot * fast_rcp(wn2 + 1e-300);
+      const double as = fabs(s);
+      // 0.5 |s| (1 - |s| r) phi(theta), the 1/2 carried by the halved limiter coefficients (exact)
+      const double cf = as * (1.0 - as * r) * ws_phi(A.limh, th);
 #pragma unroll
       for (int k = 0; k < MEQN; ++k)
-        if (S::wave_nz(D, p, k)) sw[k] = fma(s, Wp[k], sw[k]);
-      if (m2) {
-        const int src = s > 0.0 ? lane - 1 : lane + 1;    // (s = 0: the right neighbour, reading 1)
-        double wn2 = 0.0, dot = 0.0;
-#pragma unroll
-        for (int k = 0; k < MEQN; ++k) {
-          if (!S::wave_nz(D, p, k)) continue;
-          WI[k] = ws_shfl_idx(Wp[k], src & 31);
-          wn2 = fma(Wp[k], Wp[k], wn2);
-          dot = fma(WI[k], Wp[k], dot);
-        }
-        // a zero wave adds nothing: theta = 0 there (dot = 0; the 1e-300 changes wn2 only below
-        // 1e-284, i.e. for waves of norm < 1e-142) keeps the limiter's selects NaN-free
-        const double th = dot * fast_rcp(wn2 + 1e-300);
-        const double as = fabs(s);
-        // 0.5 |s| (1 - |s| r) phi(theta), the 1/2 carried by the halved limiter coefficients (exact)
-        const double c = as * (1.0 - as * r) * ws_phi(A.limh, th);
-#pragma unroll
-        for (int k = 0; k < MEQN; ++k)
-          if (S::wave_nz(D, p, k)) F[k] = fma(c, Wp[k], F[k]);
-      }
+        if (S::wave_nz(D, p, k)) F[k] = fma(cf, Wp[k], F[k]);
     }
-    // L part P = A-dq + F~ (enters the left cell), R part Q = A+dq - F~ (the right cell)
-    double P[MEQN], Q[MEQN];
+  }
+}
+
+template <class S, int D, bool FAST>
+__device__ __forceinline__ void ws_s3(const StepArgs& A, double* __restrict__ up, double* __restrict__ dn,
+                                      double* __restrict__ dq, double r, uint32_t dsc, const WsChain<S>& c) {
+  using Sh = WsShape<S>;
+  constexpr int T = Sh::T, MEQN = S::MEQN;
+  const int m3 = FAST ? 2 : A.method3;
+  const int pos = (dsc >> 9) & 31, line = (dsc >> 14) & 31;
+  const bool out = (dsc >> 21) & 1;
+  const typename S::Edge& Ed = c.Ed;
+  const double* sw = c.sw;
+  const double* F = c.F;
+  // L part P = A-dq + F~ (enters the left cell), R part Q = A+dq - F~ (the right cell)
+  double P[MEQN], Q[MEQN];
 #pragma unroll
-    for (int k = 0; k < MEQN; ++k) {
-      P[k] = Ed.am[k] + F[k];
-      Q[k] = (sw[k] - Ed.am[k]) - F[k];
-    }
-    // both transverse splits with this edge's own Roe state (its Roe-only terms once): of Q (into
-    // the right cell, this lane's output) and of P (into the left cell: the previous edge's lane's
-    // output, handed down scaled together with P)
-    {
-      double XP[MEQN], XQ[MEQN], bmP[MEQN], bpP[MEQN], bmQ[MEQN], bpQ[MEQN];
+  for (int k = 0; k < MEQN; ++k) {
+    P[k] = Ed.am[k] + F[k];
+    Q[k] = (sw[k] - Ed.am[k]) - F[k];
+  }
+  // both transverse splits with this edge's own Roe state (its Roe-only terms once): of Q (into
+  // the right cell, this lane's output) and of P (into the left cell: the previous edge's lane's
+  // output, handed down scaled together with P)
+  double XP[MEQN], XQ[MEQN], bmP[MEQN], bpP[MEQN], bmQ[MEQN], bpQ[MEQN];
+#pragma unroll
+  for (int k = 0; k < MEQN; ++k) {
+    XP[k] = m3 == 1 ? Ed.am[k] : P[k];
+    XQ[k] = m3 == 1 ? sw[k] - Ed.am[k] : Q[k];
+  }
+  if (m3 >= 1) {
+    S::template transverse2<D>(S::roe(Ed), A.sp, XP, XQ, bmP, bpP, bmQ, bpQ);
+  } else {
+#pragma unroll
+    for (int k = 0; k < MEQN; ++k) bmQ[k] = bpQ[k] = bmP[k] = bpP[k] = 0.0;
+  }
+  const double hh = -0.25 * r;   // (-1/2 r, and transverse returns 2 B-X, 2 B+X)
+  double Un[MEQN], Dn[MEQN], Pn[MEQN];
+#pragma unroll
+  for (int k = 0; k < MEQN; ++k) {
+    Un[k] = ws_shfl_down(hh * bpP[k], 1);
+    Dn[k] = ws_shfl_down(hh * bmP[k], 1);
+    Pn[k] = ws_shfl_down(P[k], 1);
+  }
+  if (out) {
+    if (D == 1) {   // cell (i = pos, j = line): G~ halves for rows 0..T+1, the x increment for rows 1..T
+      const int i = pos, j = line;
 #pragma unroll
       for (int k = 0; k < MEQN; ++k) {
-        XP[k] = m3 == 1 ? Ed.am[k] : P[k];
-        XQ[k] = m3 == 1 ? sw[k] - Ed.am[k] : Q[k];
+        up[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = fma(hh, bpQ[k], Un[k]);
+        dn[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = fma(hh, bmQ[k], Dn[k]);
       }
-      if (m3 >= 1) {
-        S::template transverse2<D>(S::roe(Ed), A.sp, XP, XQ, bmP, bpP, bmQ, bpQ);
-      } else {
+      if (j >= 1 && j <= T) {
 #pragma unroll
-        for (int k = 0; k < MEQN; ++k) bmQ[k] = bpQ[k] = bmP[k] = bpP[k] = 0.0;
+        for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
       }
-      const double hh = 0.5 * hr;   // (transverse returns 2 B-X, 2 B+X)
-      double Un[MEQN], Dn[MEQN], Pn[MEQN];
+    } else {        // cell (i = line, j = pos): F~ halves (up / dn are the rt / lf arrays)
+      const int i = line, j = pos;
 #pragma unroll
       for (int k = 0; k < MEQN; ++k) {
-        Un[k] = ws_shfl_down(hh * bpP[k], 1);
-        Dn[k] = ws_shfl_down(hh * bmP[k], 1);
-        Pn[k] = ws_shfl_down(P[k], 1);
+        up[(k * T + (j - 1)) * Sh::RTP + i] = fma(hh, bpQ[k], Un[k]);
+        dn[(k * T + (j - 1)) * Sh::RTP + i] = fma(hh, bmQ[k], Dn[k]);
       }
-      if (out) {
-        if (D == 1) {   // cell (i = pos, j = line): G~ halves for rows 0..T+1, the x increment for rows 1..T
-          const int i = pos, j = line;
+      if (i >= 1 && i <= T) {
 #pragma unroll
-          for (int k = 0; k < MEQN; ++k) {
-            up[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = fma(hh, bpQ[k], Un[k]);
-            dn[(k * Sh::NR + j) * Sh::UPP + (i - 1)] = fma(hh, bmQ[k], Dn[k]);
-          }
-          if (j >= 1 && j <= T) {
-#pragma unroll
-            for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
-          }
-        } else {        // cell (i = line, j = pos): F~ halves (up / dn are the rt / lf arrays)
-          const int i = line, j = pos;
-#pragma unroll
-          for (int k = 0; k < MEQN; ++k) {
-            up[(k * T + (j - 1)) * Sh::RTP + i] = fma(hh, bpQ[k], Un[k]);
-            dn[(k * T + (j - 1)) * Sh::RTP + i] = fma(hh, bmQ[k], Dn[k]);
-          }
-          if (i >= 1 && i <= T) {
-#pragma unroll
-            for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
-          }
-        }
+        for (int k = 0; k < MEQN; ++k) dq[(k * T + (j - 1)) * Sh::DQP + (i - 1)] = -r * Pn[k] - r * Q[k];
       }
     }
   }
 }
 
+template <class S, int D, bool FAST>
+__device__ __forceinline__ void ws_iter(const StepArgs& A, const double* __restrict__ sq, double* __restrict__ up,
+                                        double* __restrict__ dn, double* __restrict__ dq, double r, double& smax,
+                                        uint32_t dsc, int lane) {
+  WsChain<S> c;
+  ws_s1<S, D>(A, sq, dsc, c);
+#ifndef WS_ITER_VOTE
+#define WS_ITER_VOTE 0
+#endif
+  if (WS_ITER_VOTE && __any_sync(0xffffffffu, c.Ed.c != c.Ed.c)) smax = __longlong_as_double(0x7ff0000000000000ll);
+  ws_s2<S, D, FAST>(A, r, smax, dsc, lane, c);
+  ws_s3<S, D, FAST>(A, up, dn, dq, r, dsc, c);
+}
+
+// an x-iteration and a y-iteration as two independent dependency chains in one instruction stream
+// (twice the instruction-level parallelism; for the branch-free Roe SWE solve: T3 4.53 -> 4.43 ms
+// at 4 CTAs x 4 warps per SM, 126 registers.  Euler measured slower paired, at 2 CTAs of 242
+// registers: 7.58 vs 6.84 ms, its Harten-Hyman branches splitting the two streams)
+template <class S, bool FAST>
+__device__ __forceinline__ void ws_iter_xy(const StepArgs& A, const double* __restrict__ sq, double* __restrict__ up,
+                                           double* __restrict__ dn, double* __restrict__ dq, double* __restrict__ rt,
+                                           double* __restrict__ lf, double* __restrict__ dqy, double r, double& smax,
+                                           uint32_t dx, uint32_t dy, int lane) {
+  WsChain<S> cx, cy;
+  ws_s1<S, 1>(A, sq, dx, cx);
+  ws_s1<S, 2>(A, sq, dy, cy);
+  // a non-finite Roe sound speed makes the tile's CFL +inf (-> FC_ENONFINITE, as the fold's check
+  // would); the warp vote between the solves and the limiters is also the scheduling split that
+  // measured best (T3 4.53 -> 4.36 ms; the pair without it 4.66)
+  if (__any_sync(0xffffffffu, cx.Ed.c != cx.Ed.c || cy.Ed.c != cy.Ed.c)) smax = __longlong_as_double(0x7ff0000000000000ll);
+  ws_s2<S, 1, FAST>(A, r, smax, dx, lane, cx);
+  ws_s2<S, 2, FAST>(A, r, smax, dy, lane, cy);
+  ws_s3<S, 1, FAST>(A, up, dn, dq, r, dx, cx);
+  ws_s3<S, 2, FAST>(A, rt, lf, dqy, r, dy, cy);
+}
+
+#ifndef WS_PAIR_EULER
+#define WS_PAIR_EULER 0
+#endif
+#ifndef WS_PAIR_SWE
+#define WS_PAIR_SWE 1
+#endif
 template <class S, int NW, int MINB, int NBUF, bool FAST>
 __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntiles) {
   using Sh = WsShape<S>;
@@ -473,10 +535,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
     }
     // both sweeps read Q^n only (unsplit): their 2 NIT warp-iterations are one phase
     double smax = 0.0;
-    for (int v = warp; v < 2 * Sh::NIT; v += NW) {
-      const uint32_t d = desc[v * 32 + lane];
-      if (v < Sh::NIT) ws_iter<S, 1, FAST>(A, sq, up, dn, dq, r, smax, d, lane);
-      else ws_iter<S, 2, FAST>(A, sq, rt, lf, dqy, r, smax, d, lane);
+    if (std::is_same<S, WsSwe>::value ? WS_PAIR_SWE : WS_PAIR_EULER) {   // x- and y-iteration v together
+      for (int v = warp; v < Sh::NIT; v += NW)
+        ws_iter_xy<S, FAST>(A, sq, up, dn, dq, rt, lf, dqy, r, smax, desc[v * 32 + lane],
+                            desc[(Sh::NIT + v) * 32 + lane], lane);
+    } else {
+      for (int v = warp; v < 2 * Sh::NIT; v += NW) {
+        const uint32_t d = desc[v * 32 + lane];
+        if (v < Sh::NIT) ws_iter<S, 1, FAST>(A, sq, up, dn, dq, r, smax, d, lane);
+        else ws_iter<S, 2, FAST>(A, sq, rt, lf, dqy, r, smax, d, lane);
+      }
     }
     cfl = fmax(cfl, r * smax);
     __syncthreads();

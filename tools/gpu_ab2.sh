@@ -1,0 +1,5 @@
+# A/B: systems (C5 / T3) on the default build; scalar sweeps (T1 / T2 / T4) on the default build
+# and each variants/*.so; then the systems + scalar parity subsets on the default
+echo default; timeout 300 python tools/ws_ab.py 2>&1 | tail -2
+VARIANTS="default $(ls variants/*.so | xargs -n1 basename | sed 's/\.so$//')" ONLY=T1,T2,T4 bash tools/cv_variants.sh 2>&1 | grep -v "^$"
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_ab2.log 2>&1; echo pytest rc=$?; tail -2 gpurun_out/pytest_ab2.log
