@@ -135,6 +135,10 @@ typedef struct {
                                    sweeps compute their gather addresses and move the ring in
                                    16-byte pairs; other patches (and the systems kernel) read the
                                    ring table.  Bitwise the same gather either way */
+  int64_t quad_blocks;          /* m = 8 constant-velocity advection: 2 x 2 sibling families of
+                                   regular patches swept as one 16 x 16 window (every local patch
+                                   regular, the local list whole families; FC_CV_QUAD=0: off): each
+                                   family edge computed once.  Bitwise the per-patch sweep */
 } fc_stats;
 
 /* ---- calls --------------------------------------------------------------------------------- */

@@ -34,7 +34,7 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
                 const uint8_t* bcflag,
                 const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits,
                 const int32_t* rslot, double* freg, const uint8_t* rpeer, const double* const* peerq,
-                const double* cg, cudaStream_t st);
+                const double* cg, cudaStream_t st, int quad = 0);
 int launch_cg(int op, const double* q, double* cg, const int32_t* list, int64_t nrec, int meqn, int n2,
               cudaStream_t st);
 int launch_copy_blocks(const double* src, double* dst, const int32_t* ids, int64_t nb, int64_t S, cudaStream_t st);
@@ -119,6 +119,7 @@ struct fc_forest {
   bool fused = false;
   int32_t* d_ring = nullptr;
   int32_t* d_nb9 = nullptr;   // regular rings: per local patch the 9 neighbour block offsets (plan_ring_regular)
+  int quad = 0;               // m = 8, every local patch regular, complete sibling families 4b .. 4b+3
   uint8_t* d_bcflag = nullptr;
   // quiescent-patch filter (fused path): neighbour table, wall mask, flags, states, active list
   int32_t *d_nbr = nullptr, *d_active = nullptr, *d_nactive = nullptr;
@@ -558,7 +559,7 @@ static int update_local(fc_forest* f, double dt, int part = 0) {
                        fused ? f->d_ring : nullptr, f->d_nb9, f->d_bcflag, filtered ? f->d_active : nullptr,
                        filtered ? f->d_nactive : nullptr, f->d_cfl, records ? f->d_rslot : nullptr,
                        records ? f->d_freg : nullptr, (fused && (f->p2p || f->amr_fused)) ? f->d_rpeer : nullptr,
-                       peerq.data(), f->d_cg, f->stream);
+                       peerq.data(), f->d_cg, f->stream, fused ? f->quad : 0);
   if (lr < 0) return fail(FC_EUNSUP, "no step kernel for this m / kind");
   f->st.kernel_launches += lr;
   f->st.step_kernel_launches += lr;
@@ -658,7 +659,26 @@ static int upload_regular(fc_forest* f, const RingSources& rs) {
   std::vector<int32_t> nb9;
   const int64_t nreg = plan_ring_regular(f->pl, f->pl.meqn, rs, nb9);
   f->st.regular_patches = nreg;
+  f->st.quad_blocks = 0;
+  f->quad = 0;
   if (nreg == 0) return FC_OK;
+  {   // quad blocks for the scalar sweep (cv_stage_quad): every local patch regular and the local
+      // list made of whole sibling families in Morton order (FC_CV_QUAD=0: off)
+    const char* qe = getenv("FC_CV_QUAD");
+    const int64_t Pl = f->pl.p1 - f->pl.p0;
+    bool ok = !(qe && atoi(qe) == 0) && f->pl.m == 8 && f->pl.meqn == 1 && nreg == Pl && Pl % 4 == 0;
+    for (int64_t b = 0; ok && b < Pl / 4; ++b) {
+      const Leaf& l0 = f->pl.leaves[f->pl.p0 + 4 * b];
+      const int64_t sz = (int64_t)1 << (f->pl.lmax - l0.level);
+      if (l0.level == 0 || (l0.x / sz) % 2 != 0 || (l0.y / sz) % 2 != 0) { ok = false; break; }
+      for (int c = 1; c < 4 && ok; ++c) {
+        const Leaf& l = f->pl.leaves[f->pl.p0 + 4 * b + c];
+        ok = l.tree == l0.tree && l.level == l0.level && l.x == l0.x + sz * (c & 1) && l.y == l0.y + sz * (c >> 1);
+      }
+    }
+    f->quad = ok ? 1 : 0;
+    f->st.quad_blocks = ok ? Pl / 4 : 0;
+  }
   cudaError_t e = cudaMalloc(&f->d_nb9, nb9.size() * sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMemcpy(f->d_nb9, nb9.data(), nb9.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {

@@ -1007,23 +1007,100 @@ struct CvShape {
 struct CvNb {
   int32_t lo, hi;
 };
-template <int T>
+// Quad blocks (QD): a 2 x 2 sibling family of regular m = 8 patches (local patches 4b .. 4b+3, x in
+// the low bit: child c = cx + 2 cy) staged as one 16 x 16 window and swept as one T = 16 patch.
+// Each edge of the family is computed once instead of once per patch it borders, from the same cell
+// values the patches' rings hold (aligned same-level copies): every patch's update is the one the
+// m = 8 sweep computes.  The block's ring reads the 12 same-level neighbours around it, entry k of
+// the block = neighbour d (3 (dy + 1) + dx + 1) of child c in plan_ring_regular's table:
+__device__ __forceinline__ int quad_child(int k) { return (int)((0x332232101100ull >> (4 * k)) & 15); }
+__device__ __forceinline__ int quad_dir(int k) { return (int)((0x877653532110ull >> (4 * k)) & 15); }
+
+template <int T, bool QD = false>
 __device__ __forceinline__ CvNb cv_nb_load(const StepArgs& A, int i0, int cnt, int lane) {
-  constexpr int PW = CvShape<T>::PW;
+  constexpr int PW = CvShape<T>::PW, NE = QD ? 12 : 9;
   CvNb r{-1, -1};
   if (!A.nb9 || cnt <= 0) return r;
   auto entry = [&](int e) {
-    const int q = e / 9;
+    const int q = e / NE;
     if (q >= cnt || q >= PW) return -1;
-    const int patch = A.active ? A.active[i0 + q] : i0 + q;
+    int64_t at;
+    if (QD) {
+      const int k = e - NE * q;
+      at = (int64_t)(4 * (i0 + q) + quad_child(k)) * 9 + quad_dir(k);
+    } else {
+      at = (int64_t)(A.active ? A.active[i0 + q] : i0 + q) * 9 + (e - 9 * q);
+    }
     // (a volatile load: issued here, not sunk to its use after the sweep)
     int32_t v;
-    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(A.nb9 + (int64_t)patch * 9 + (e - 9 * q)));
+    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(A.nb9 + at));
     return v;
   };
   r.lo = entry(lane);
-  if (PW * 9 > 32) r.hi = entry(lane + 32);
+  if (PW * NE > 32) r.hi = entry(lane + 32);
   return r;
+}
+
+// staging of a group of PW quad blocks (T = 16 windows): the 4 children's interiors as 16-byte
+// chunks, the ring as 16-byte pairs from the 12 neighbours (every pair lies in one neighbour's
+// interior row, aligned: the patch boundaries fall between odd and even window columns)
+template <int T>
+__device__ __forceinline__ void cv_stage_quad(const StepArgs& A, double* buf, uint64_t* bar, int lane, int i0,
+                                              int cnt, const CvNb& nbv) {
+  static_assert(T == 16, "quad blocks are 16 x 16");
+  using C = CvShape<T>;
+  constexpr int W = C::W, WW = C::WW, PW = C::PW, S8 = 12 * 12;   // (m = 8 storage block, meqn = 1)
+  if (lane == 0) mbar_expect_tx(bar, 0u);
+  __syncwarp();
+  auto nb_of = [&](int e) {
+    const int lo = __shfl_sync(0xffffffffu, nbv.lo, e & 31);
+    const int hi = __shfl_sync(0xffffffffu, nbv.hi, e & 31);
+    return e < 32 ? lo : hi;
+  };
+  constexpr int RCH = 2 * W + 2 * T, RU = (RCH + 31) / 32;
+  int rdst[RU], rk[RU], rsrc[RU];
+#pragma unroll
+  for (int u = 0; u < RU; ++u) {
+    const int c = lane + 32 * u;
+    int wi, wj;
+    if (c < 2 * W) {
+      const int rr = c / (W / 2);
+      wj = rr < 2 ? rr : T + rr;
+      wi = 2 * (c - rr * (W / 2));
+    } else {
+      wj = 2 + ((c - 2 * W) >> 1);
+      wi = (c & 1) ? T + 2 : 0;
+    }
+    const int i = wi - 1, j = wj - 1;                       // block cell (1-based interior 1..16)
+    const int cx = i <= 8 ? 0 : 1, cy = j <= 8 ? 0 : 1;     // the child it borders
+    const int ii = i - 8 * cx, jj = j - 8 * cy;             // in that child's frame (-1 .. 10)
+    const int dx = ii < 1 ? -1 : (ii > 8 ? 1 : 0), dy = jj < 1 ? -1 : (jj > 8 ? 1 : 0);
+    const int child = cx + 2 * cy, d = 3 * (dy + 1) + dx + 1;
+    int k = 0;
+#pragma unroll
+    for (int t = 0; t < 12; ++t) k = (quad_child(t) == child && quad_dir(t) == d) ? t : k;
+    rdst[u] = c < RCH ? wj * W + wi : -1;
+    rk[u] = k;
+    rsrc[u] = (jj - dy * 8 - 1) * 8 + (ii - dx * 8 - 1);
+  }
+#pragma unroll
+  for (int q = 0; q < PW; ++q) {
+    if (q >= cnt) break;
+    double* b = buf + q * WW;
+    const double* qc = A.qold + (int64_t)4 * (i0 + q) * S8;
+#pragma unroll
+    for (int c = lane; c < T * T / 2; c += 32) {
+      const int row = c >> 3, cp = c & 7;
+      const double* src = qc + ((row >> 3) * 2 + (cp >> 2)) * S8 + (row & 7) * 8 + 2 * (cp & 3);
+      cp_async16(b + (row + 2) * W + 2 + 2 * cp, src);
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int off = nb_of(12 * q + rk[u]);
+      if (rdst[u] >= 0) cp_async16(b + rdst[u], A.qold + off + rsrc[u]);
+    }
+  }
+  cp_async_commit();
 }
 
 template <int T>
@@ -1172,7 +1249,19 @@ __device__ __forceinline__ void cv_bcs(const StepArgs& A, double* gbuf, int mypa
   }
 }
 
-template <int T, int SX, int SY, bool MT2, int NB, bool RF>
+// CV_EXACT: the sums and products of the sweep rounded on their own (no contraction left to the
+// compiler, whose choice may differ between instantiations)
+#ifndef CV_EXACT
+#define CV_EXACT 1
+#endif
+#if CV_EXACT
+#define CV_ADD(x, y) __dadd_rn(x, y)
+#define CV_MUL(x, y) __dmul_rn(x, y)
+#else
+#define CV_ADD(x, y) ((x) + (y))
+#define CV_MUL(x, y) ((x) * (y))
+#endif
+template <int T, int SX, int SY, bool MT2, int NB, bool RF, bool QD = false>
 #ifndef CV_MINB
 #define CV_MINB 20
 #endif
@@ -1185,10 +1274,12 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
   if (A.active) npatch = *A.nactive;
   const int ngroups = (npatch + PW - 1) / PW;
   const bool ring = A.ring != nullptr;
-  auto patch_of = [&](int idx) { return A.active ? A.active[idx] : idx; };
-  auto nbload = [&](int g) { return g < ngroups ? cv_nb_load<T>(A, g * PW, min(PW, npatch - g * PW), lane) : CvNb{-1, -1}; };
+  // (QD: npatch counts quad blocks, unit b = local patches 4b .. 4b + 3; no active list)
+  auto patch_of = [&](int idx) { return QD ? 4 * idx : (A.active ? A.active[idx] : idx); };
+  auto nbload = [&](int g) { return g < ngroups ? cv_nb_load<T, QD>(A, g * PW, min(PW, npatch - g * PW), lane) : CvNb{-1, -1}; };
   auto stage = [&](int g, int s, const CvNb& nb) {
-    cv_stage<T>(A, sm + (size_t)s * PW * WW, &bars[s], lane, g * PW, min(PW, npatch - g * PW), nb);
+    if constexpr (QD) cv_stage_quad<T>(A, sm + (size_t)s * PW * WW, &bars[s], lane, g * PW, min(PW, npatch - g * PW), nb);
+    else cv_stage<T>(A, sm + (size_t)s * PW * WW, &bars[s], lane, g * PW, min(PW, npatch - g * PW), nb);
   };
   if (lane == 0) {
     for (int q = 0; q < NB; ++q) mbar_init(&bars[q], 1);
@@ -1250,29 +1341,35 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
     auto ld = [&](int e, int j) { return col[e][(j + 1) * W]; };
     const double r = dtdx_level(A, level);
     if (live) cfl = fmax(cfl, fmax(fmax(r * u0, -r * u0), fmax(r * v0, -r * v0)));
-    const double cfx = second ? 0.5 * fabs(u0) * (1.0 - fabs(u0) * r) : 0.0;
-    const double cfy = second ? 0.5 * fabs(v0) * (1.0 - fabs(v0) * r) : 0.0;
+    const double cfx = second ? __dmul_rn(0.5 * fabs(u0), __dsub_rn(1.0, __dmul_rn(fabs(u0), r))) : 0.0;
+    const double cfy = second ? __dmul_rn(0.5 * fabs(v0), __dsub_rn(1.0, __dmul_rn(fabs(v0), r))) : 0.0;
     const double ht = trans ? -0.5 * r : 0.0;
     // k_up / k_down / k_left / k_right with the signs fixed by SX, SY
     const double kx = ht * u0, ky = ht * v0;   // (SX > 0: k_right = kx, k_left = 0; SX < 0: k_left = kx)
     const double m3 = A.method3 == 2 ? 1.0 : 0.0;
-    double* out = A.qnew + (int64_t)patch * WW;
+    double* out = A.qnew + (int64_t)patch * (QD ? 144 : WW);
+    // interior cell (x, y) of the unit -> its offset from out (QD: in child (x / 8, y / 8))
+    auto oidx = [&](int x, int y) {
+      return QD ? ((y >> 3) * 2 + (x >> 3)) * 144 + (y & 7) * 8 + (x & 7) : y * T + x;
+    };
     // edge parts: dqL (into the low cell), dqR (into the high cell), xl / xr (their transverse
     // parts: the correction weighted by m3)
     auto edge = [&](double w, double wi, double s, double cf, double& dL, double& dR, double& xl, double& xr,
                     auto sgn) {
       constexpr int SG = decltype(sgn)::value;
-      const double f = cf * limited(w, wi);
+      // (every product and sum rounded on its own or as an explicit fma: the same bits in every
+      // instantiation -- the m = 8 patch sweep and the quad blocks' T = 16 sweep)
+      const double f = CV_MUL(cf, limited(w, wi));
       if (SG > 0) {
         dL = f;
         dR = fma(s, w, -f);
         if (MT2) { xl = dL; xr = dR; }
-        else { xl = m3 * f; xr = fma(s, w, -(m3 * f)); }
+        else { xl = CV_MUL(m3, f); xr = fma(s, w, -CV_MUL(m3, f)); }
       } else {
         dL = fma(s, w, f);
         dR = -f;
         if (MT2) { xl = dL; xr = dR; }
-        else { xl = fma(s, w, m3 * f); xr = -(m3 * f); }
+        else { xl = fma(s, w, CV_MUL(m3, f)); xr = -CV_MUL(m3, f); }
       }
     };
     using SXc = std::integral_constant<int, SX>;
@@ -1302,23 +1399,19 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
       edge(w1, wi1, u0, cfx, dL1, dR1, xl1, xr1, SXc{});
       const double xrL = __shfl_up_sync(0xffffffffu, xr1, 1);
       const double dRL = MT2 ? xrL : __shfl_up_sync(0xffffffffu, dR1, 1);
-      const double Xa = xrL + xl0, Xb = xr0 + xl1;
-      const double Xfa0 = MT2 ? Xa : dRL + dL0, Xfb0 = MT2 ? Xb : dR0 + dL1;
+      const double Xa = CV_ADD(xrL, xl0), Xb = CV_ADD(xr0, xl1);
+      const double Xfa0 = MT2 ? Xa : CV_ADD(dRL, dL0), Xfb0 = MT2 ? Xb : CV_ADD(dR0, dL1);
       if (F & UPD) {   // update of row j - 1
         const int jr = j - 1;
-        const double ta = Xfa + Yfa + (SX > 0 ? kx * (Ya - Yl) : kx * (Yb - Ya)) +
-                          (SY > 0 ? ky * (Xa1 - Xa2) : ky * (Xa - Xa1));
-        const double tb = Xfb + Yfb + (SX > 0 ? kx * (Yb - Ya) : kx * (Yr - Yb)) +
-                          (SY > 0 ? ky * (Xb1 - Xb2) : ky * (Xb - Xb1));
+        const double ta = fma(ky, SY > 0 ? Xa1 - Xa2 : Xa - Xa1,
+                              fma(kx, SX > 0 ? Ya - Yl : Yb - Ya, CV_ADD(Xfa, Yfa)));
+        const double tb = fma(ky, SY > 0 ? Xb1 - Xb2 : Xb - Xb1,
+                              fma(kx, SX > 0 ? Yb - Ya : Yr - Yb, CV_ADD(Xfb, Yfb)));
         const double va = fma(-r, ta, qa[0]), vb = fma(-r, tb, qb[0]);
         const bool sa_ = live && c0 >= 1, sb_ = live && c0 + 1 <= T;
-        if (sa_) out[(jr - 1) * T + c0 - 1] = va;
-        if (sb_) out[(jr - 1) * T + c0] = vb;
+        if (sa_) out[oidx(c0 - 1, jr - 1)] = va;
+        if (sb_) out[oidx(c0, jr - 1)] = vb;
         chk = fma(sa_ ? va : 0.0, 0.0, fma(sb_ ? vb : 0.0, 0.0, chk));
-#ifndef CV_VOTE
-#define CV_VOTE 0
-#endif
-        if (CV_VOTE && __any_sync(0xffffffffu, chk != chk)) chk = __longlong_as_double(0x7ff8000000000000ll);
         if (RF && rec) {   // the same face fluxes k_step_sc records (F~ / G~ transverse at the face)
           if (k == 0) reg[jr - 1] = (dR0p - kx * (SX > 0 ? Ya : Yb)) - u0 * qb[0];                 // x-low, i = 1
           if (k == LP - 1) reg[T + jr - 1] = u0 * qa[0] + (dL0p + kx * (SX > 0 ? Ya : Yb));       // x-high, i = T
@@ -1340,8 +1433,8 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
         edge(wa, wia, v0, cfy, dLa, dRa, yla, yra_, SYc{});
         edge(wb, wib, v0, cfy, dLb, dRb, ylb, yrb_, SYc{});
         if (F & YS) {
-          Ya = yra + yla; Yb = yrb + ylb;
-          Yfa = MT2 ? Ya : dRya + dLa; Yfb = MT2 ? Yb : dRyb + dLb;
+          Ya = CV_ADD(yra, yla); Yb = CV_ADD(yrb, ylb);
+          Yfa = MT2 ? Ya : CV_ADD(dRya, dLa); Yfb = MT2 ? Yb : CV_ADD(dRyb, dLb);
           Yl = __shfl_up_sync(0xffffffffu, Yb, 1);
           Yr = __shfl_down_sync(0xffffffffu, Ya, 1);
         }
@@ -1526,10 +1619,6 @@ __global__ void __launch_bounds__(32, CVC_MINB) k_step_cvc(StepArgs A, int npatc
         if (sa_) out[(jr - 1) * T + c0 - 1] = va;
         if (sb_) out[(jr - 1) * T + c0] = vb;
         chk = fma(sa_ ? va : 0.0, 0.0, fma(sb_ ? vb : 0.0, 0.0, chk));
-#ifndef CV_VOTE
-#define CV_VOTE 0
-#endif
-        if (CV_VOTE && __any_sync(0xffffffffu, chk != chk)) chk = __longlong_as_double(0x7ff8000000000000ll);
       }
       if (F & YE) {    // y-edges (c, j + 1/2)
         const double wa = qa[2] - qa[1], wb = qb[2] - qb[1];
@@ -1837,7 +1926,7 @@ static int launch_sc_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
 #ifndef CV_NB
 #define CV_NB 1
 #endif
-template <int T, int SX, int SY, bool MT2, bool RF = false>
+template <int T, int SX, int SY, bool MT2, bool RF = false, bool QD = false>
 static int launch_cv_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   constexpr int NB = CV_NB;
   using C = CvShape<T>;
@@ -1848,18 +1937,18 @@ static int launch_cv_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   if (dev_ < 0 || dev_ >= 64) return -1;
   int& resident = resident_dev[dev_];
   if (!resident) {
-    cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB, RF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB, RF, QD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_step_cv<T, SX, SY, MT2, NB, RF, QD>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_cv<T, SX, SY, MT2, NB, RF>, 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_cv<T, SX, SY, MT2, NB, RF, QD>, 32, smem);
     resident = sms * (per_sm > 0 ? per_sm : 1);
   }
   if (npatch >= (1ll << 31)) return -1;
   const int64_t groups = (npatch + C::PW - 1) / C::PW;
   const int64_t grid = groups < resident ? groups : resident;
-  k_step_cv<T, SX, SY, MT2, NB, RF><<<(unsigned)grid, 32, smem, st>>>(a, (int)npatch);
+  k_step_cv<T, SX, SY, MT2, NB, RF, QD><<<(unsigned)grid, 32, smem, st>>>(a, (int)npatch);
   return 1;
 }
 
@@ -1887,6 +1976,17 @@ static int launch_cvc_t(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   const int64_t grid = groups < resident ? groups : resident;
   k_step_cvc<T, MT2, NB><<<(unsigned)grid, 32, smem, st>>>(a, (int)npatch);
   return 1;
+}
+
+// quad blocks (cv_stage_quad): npatch / 4 units of the T = 16 sweep
+static int launch_cv_quad(const StepArgs& a, int64_t nblk, cudaStream_t st) {
+  const bool px = a.sp.p0 > 0.0, py = a.sp.p1 > 0.0;
+  if (a.method3 == 2) {
+    if (px) return py ? launch_cv_t<16, 1, 1, true, false, true>(a, nblk, st) : launch_cv_t<16, 1, -1, true, false, true>(a, nblk, st);
+    return py ? launch_cv_t<16, -1, 1, true, false, true>(a, nblk, st) : launch_cv_t<16, -1, -1, true, false, true>(a, nblk, st);
+  }
+  if (px) return py ? launch_cv_t<16, 1, 1, false, false, true>(a, nblk, st) : launch_cv_t<16, 1, -1, false, false, true>(a, nblk, st);
+  return py ? launch_cv_t<16, -1, 1, false, false, true>(a, nblk, st) : launch_cv_t<16, -1, -1, false, false, true>(a, nblk, st);
 }
 
 template <int T>
@@ -1923,6 +2023,10 @@ static int launch_step_s(const StepArgs& a, int64_t npatch, cudaStream_t st) {
   if constexpr (std::is_same<S, AdvConst>::value) {
     if (cv && (!a.rslot || a.method3 == 2) && a.tiles == 1 && a.limiter != 0) {
       if (a.m == 16) return launch_cv<16>(a, npatch, st);
+      // a forest of complete sibling families of regular patches (the planner's quad flag): 2 x 2
+      // blocks through the 16 x 16 sweep (not on active lists or reflux records)
+      if (a.m == 8 && a.quad && !a.active && !a.rslot && a.ring && a.nb9 && !a.rpeer && npatch % 4 == 0)
+        return launch_cv_quad(a, npatch / 4, st);
       if (a.m == 8) return launch_cv<8>(a, npatch, st);
     }
   }
@@ -1961,9 +2065,10 @@ int launch_step(int kind, const double* qold, double* qnew, const double* aux, c
                 const uint8_t* bcflag,
                 const int32_t* active, const int32_t* nactive, unsigned long long* cfl_bits,
                 const int32_t* rslot, double* freg, const uint8_t* rpeer, const double* const* peerq,
-                const double* cg, cudaStream_t st) {
+                const double* cg, cudaStream_t st, int quad) {
   if (npatch <= 0) return 0;
   StepArgs a;
+  a.quad = quad;
   a.cg = cg;
   a.rslot = rslot;
   a.freg = freg;

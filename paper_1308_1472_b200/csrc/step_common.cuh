@@ -51,6 +51,7 @@ struct StepArgs {
   const uint8_t* __restrict__ rpeer;  // peer-memory halo: owner of each ring source (0 = this rank)
   const double* peerq[16];            // peer-memory halo: rank r's current q_old (peer pointer)
   const double* cg;                   // fused AMR ring gather: computed ghosts (ring peer code 255)
+  int quad;                           // m = 8 forest of complete sibling families of regular patches
 };
 
 // phi(wi / w) w of the MC / minmod limiter for the scalar register sweeps, division- and
@@ -61,6 +62,9 @@ struct StepArgs {
 // The rounding differs from the oracle's phi(theta) w by ulps, within the step tolerance (reading 24).
 __device__ __forceinline__ double cv_limited(double w, double wi, double lp1, double lp2, double lk3) {
   const double a = fabs(w), b = fabs(wi), s = a + b;
+  // (the compiler's contraction of x +- y is local to this expression -- y has the same two uses
+  // in every instance -- and measured bitwise alike in the m = 8 and the quad-block sweeps; the
+  // explicit forms, fmas or rounded intrinsics, compiled to slower code: T1 0.38 -> 0.41 ms)
   const double x = fma(lp1, s, lp2 * a), y = lk3 * (s - fabs(a - b));
   const double mag = 0.5 * ((x + y) - fabs(x - y));
   const int hw = __double2hiint(w);

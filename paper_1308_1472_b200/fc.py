@@ -72,7 +72,8 @@ class Stats(C.Structure):
                 ("ms_step", C.c_double), ("ms_comm", C.c_double), ("step_kernel_launches", C.c_int64),
                 ("local_patches", C.c_int64), ("halo_cells", C.c_int64),
                 ("uniform_fast_path", C.c_int32), ("pad_", C.c_int32), ("ms_copy", C.c_double),
-                ("copy_launches", C.c_int64), ("regular_patches", C.c_int64)]
+                ("copy_launches", C.c_int64), ("regular_patches", C.c_int64),
+                ("quad_blocks", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
