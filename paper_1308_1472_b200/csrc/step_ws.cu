@@ -472,15 +472,18 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
     cp_async_commit();
     ws_prep<S>(A, tile_of(blockIdx.x + gridDim.x), g, tid, NT);
   }
-  int meta = -1;                               // bcflag | level << 8 of the current tile
-  {
-    const int t0 = tile_of(blockIdx.x);
-    if (t0 >= 0) {
-      int p0, x0, y0;
-      ws_tile(A, t0, p0, x0, y0);
-      meta = A.bcflag[p0] | ((int)A.level[p0] << 8);
-    }
-  }
+  // boundary flags and level of the next tile, loaded a tile ahead into their own registers (volatile
+  // loads: the combination happens at their use, one tile later -- combined at the load, the
+  // compiler waited on the two loads every tile: 5.7 % of the stall samples)
+  int nbc = 0, nlv = 0;
+  auto load_meta = [&](int t) {
+    if (t < 0) return;
+    int pm, xm, ym;
+    ws_tile(A, t, pm, xm, ym);
+    asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(nbc) : "l"(A.bcflag + pm));
+    asm volatile("ld.global.nc.s8 %0, [%1];" : "=r"(nlv) : "l"(A.level + pm));
+  };
+  load_meta(tile_of(blockIdx.x));
   int it = 0;
   for (int kt = blockIdx.x; kt < ntiles; kt += gridDim.x, ++it) {
     double* sq = sbuf + (NBUF == 2 ? (it & 1) * Sh::QB : 0);
@@ -501,15 +504,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_step_ws(StepArgs A, int ntile
       cp_async_wait<0>();
       __syncthreads();
     }
-    const int cur = meta;
-    {
-      const int tn = tile_of(kt + gridDim.x);
-      if (tn >= 0) {
-        int pn, xn, yn;
-        ws_tile(A, tn, pn, xn, yn);
-        meta = A.bcflag[pn] | ((int)A.level[pn] << 8);
-      }
-    }
+    const int cur = nbc | (nlv << 8);             // bcflag | level << 8 of this tile
+    load_meta(tile_of(kt + gridDim.x));
     if (cur & 1) { ws_bc<S>(A, tile, sq, 0, tid, NT); __syncthreads(); }
     if (cur & 2) { ws_bc<S>(A, tile, sq, 1, tid, NT); __syncthreads(); }
     const double r = dtdx_level(A, cur >> 8);   // square cells, no capacity: dt/dx = dt/dy
