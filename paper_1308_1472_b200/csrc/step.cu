@@ -1301,15 +1301,28 @@ __global__ void __launch_bounds__(32, CV_MINB) k_step_cv(StepArgs A, int npatch)
   auto limited = [&](double w, double wi) { return cv_limited(w, wi, lp1, lp2, lk3); };
   double cfl = 0.0;
   double chk = 0.0;                     // sum of 0 * q_new: NaN iff some q_new is not finite
+  // a group's levels and boundary flags, loaded a group ahead into their own registers (volatile:
+  // issued here, consumed one group later -- loaded at the group's start, the boundary ballot after
+  // the staging wait stalled on them)
+  int nlev = 0, nbc = 0;
+  auto meta_load = [&](int gg) {
+    if (gg >= ngroups) return;
+    const int c = min(PW, npatch - gg * PW);
+    const int pt = lane < c ? patch_of(gg * PW + lane) : 0;
+    asm volatile("ld.global.nc.s8 %0, [%1];" : "=r"(nlev) : "l"(A.level + pt));
+    if (ring) asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(nbc) : "l"(A.bcflag + pt));
+  };
+  meta_load(blockIdx.x);
   int it = 0;
   for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
     const int b = it % NB;
     const int cnt = min(PW, npatch - g * PW);
-    // this group's patch ids, levels and boundary flags (loads in flight during the wait)
+    // this group's patch ids (the reflux slots load during the wait)
     const int mypatch = lane < cnt ? patch_of(g * PW + lane) : 0;
-    const int mylevel = A.level[mypatch];
+    const int mylevel = nlev;
     const int myslot = RF ? A.rslot[mypatch] : -1;
-    const int mybc = (ring && lane < cnt) ? A.bcflag[mypatch] : 0;
+    const int mybc = (ring && lane < cnt) ? nbc : 0;
+    meta_load(g + gridDim.x);
     // the next staged group's regular-ring offsets (in flight during this group's sweep)
     const CvNb nbn = ring ? nbload(g + (NB > 1 ? NB - 1 : 1) * gridDim.x) : CvNb{-1, -1};
     mbar_wait(&bars[b], (uint32_t)((it / NB) & 1));
