@@ -18,6 +18,10 @@ CASES = [
     ("amr_mixed", forest3((2, 1, 2), 1, refine=lambda t, x, y, z, h: (t + x + y + z) < 1.2,
                           periodic=(True, False, True)), 8),
     ("amr_deep", forest3((1, 1, 1), 2, refine=lambda t, x, y, z, h: x + y < 0.6, periodic=(False, True, False)), 4),
+    # m = 16 / 8 (the compiled-m kernels): regular patches (computed gather) and, in the second,
+    # outflow patches (table gather) in one forest
+    ("uniform_periodic_m16", forest3((1, 1, 1), 1), 16),
+    ("uniform_mixed_m8", forest3((2, 1, 1), 2, periodic=(False, True, True)), 8),
 ]
 
 
@@ -69,3 +73,25 @@ def test_courant_one_shift_and_reject():
     assert rc == fc.FC_ECFL and c == 1.5
     np.testing.assert_array_equal(g.get_q(), q0)
     g.close()
+
+
+@pytest.mark.parametrize("lim", [fc.FC_LIM_MC, fc.FC_LIM_MINMOD], ids=["mc", "minmod"])
+@pytest.mark.parametrize("name,f,m", [c for c in CASES if c[2] in (8, 16)], ids=[c[0] for c in CASES if c[2] in (8, 16)])
+def test_steps_bitwise_wide_range(name, f, m, lim):
+    """Limiter ratios across the whole double range (quotients that overflow, underflow to
+    subnormals, zero numerators and zero waves, exactly equal neighbours): the compiled-m pencils'
+    grouped division (nvcc's fast path, the operator where its range check fails) gives the
+    oracle's IEEE quotient bit for bit."""
+    rng = np.random.default_rng(1308147 + 91)
+    n = f.num_patches * m ** 3
+    q0 = rng.choice([-1.0, 1.0], n) * 10.0 ** rng.uniform(-160, 160, n)
+    q0[rng.random(n) < 0.15] = 0.0
+    rep = rng.random(n) < 0.15
+    q0[1:][rep[1:]] = q0[:-1][rep[1:]]
+    q0 = q0.reshape(f.num_patches, m, m, m)
+    vel = (0.8, -0.45, 0.3)
+    dt = 0.9 / (m * 2 ** int(f.levels.max())) / 0.8
+    qg, cg = fc3.run3(f, m, q0, vel, dt, 3, limiter=lim, method2=2)
+    qo, co = O.run3(f, m, q0, vel, dt, 3, limiter=lim, method2=2)
+    np.testing.assert_array_equal(qg.view(np.int64), qo.view(np.int64))
+    np.testing.assert_array_equal(cg, co)
