@@ -112,8 +112,10 @@ typedef struct {
                                    through that face replaced by the mean of the two fine fluxes, so
                                    sum kappa q is conserved across coarse/fine faces.  No-op on
                                    conforming meshes.  FC_EUNSUP (at fc_set_problem) for systems
-                                   (meqn > 1) across rotated tree links and for coarse/fine pairs
-                                   split between ranks.  0: off (the paper's global-dt step) */
+                                   (meqn > 1) across rotated tree links.  Coarse/fine pairs split
+                                   between ranks exchange the fine-face records every step
+                                   (fc_reflux_* below for the manual transport); only the sub-cycled
+                                   step refuses them.  0: off (the paper's global-dt step) */
 } fc_problem;
 
 typedef struct {
