@@ -95,3 +95,18 @@ def test_steps_bitwise_wide_range(name, f, m, lim):
     qo, co = O.run3(f, m, q0, vel, dt, 3, limiter=lim, method2=2)
     np.testing.assert_array_equal(qg.view(np.int64), qo.view(np.int64))
     np.testing.assert_array_equal(cg, co)
+
+
+def test_regular_rings_equal_the_table_gather(monkeypatch):
+    """Patches whose ring is all aligned same-level copies compute their sources from their 27
+    neighbours (csrc/step3.cu, `nb27` / `ring_reg`); FC3_REGULAR=0 (read when the forest is
+    created) keeps the per-patch table for every patch: the same copies, so the same bits."""
+    name, f, m = CASES[-1]
+    q0 = bump(f, m)
+    vel = (0.8, -0.45, 0.3)
+    dt = 0.9 / (m * 2 ** int(f.levels.max())) / 0.8
+    qa, ca = fc3.run3(f, m, q0, vel, dt, 6)
+    monkeypatch.setenv("FC3_REGULAR", "0")
+    qb, cb = fc3.run3(f, m, q0, vel, dt, 6)
+    np.testing.assert_array_equal(qa, qb)
+    np.testing.assert_array_equal(ca, cb)
